@@ -1,0 +1,309 @@
+// compress.cu — tol-bounded greedy piecewise-linear compression on sm_100a.
+//
+// Reference: detail::compress_range (compression.hpp:31-66), compress
+// (:70-83), partitional_compress (:167-193). The greedy parse is a
+// deterministic orbit p -> f(p) (f = piece end from start p), so the work is
+// split into fixed-size chunks of start positions and every chunk is parsed
+// SPECULATIVELY from its own first position by one thread. Orbits merge once
+// they share a point, so the true parse is recovered by (1) propagating true
+// chunk exits left to right with a parallel fixed-point iteration that
+// re-parses only the prefix of a chunk before the true orbit meets the
+// speculative one (usually zero pieces), then (2) rewriting only those
+// prefixes. All arithmetic in f is the reference's, in the reference's order,
+// compiled with -fmad=false, so boundaries and increments are bit-exact.
+#include <cub/cub.cuh>
+
+#include "jb_device.hpp"
+
+namespace jb {
+
+// Greedy piece end from `start` (compression.hpp:38-61), bit-exact.
+__device__ __forceinline__ int64_t piece_end(const double* __restrict__ v, int64_t start,
+                                             int64_t last, double tol2, int64_t max_len) {
+    const double base = v[start];
+    double s2 = 0.0, s3 = 0.0;
+    int64_t end = start;
+    for (;;) {
+        const int64_t cand = end + 1;
+        if (cand > last) break;
+        const double y = v[cand] - base;
+        const double d = (double)(cand - start);
+        const double ns2 = s2 + y * y;
+        const double ns3 = s3 + d * y;
+        const double sum_d2 = d * (d + 1.0) * (2.0 * d + 1.0) / 6.0;
+        const double sq_dev = y * y / (d * d) * sum_d2 - 2.0 * y / d * ns3 + ns2;
+        if (sq_dev > (d - 1.0) * tol2 && cand > start + 1) break;
+        end = cand;
+        s2 = ns2;
+        s3 = ns3;
+        if (max_len > 0 && end - start >= max_len) break;
+    }
+    return end;
+}
+
+struct ChunkGeom {
+    const int64_t* seg_first;
+    const int64_t* seg_steps;
+    const int64_t* chunk_off;  // n_seg + 1
+    int64_t n_seg;
+    int64_t C;
+};
+
+__device__ __forceinline__ void chunk_bounds(const ChunkGeom& g, int64_t ch, int64_t& s,
+                                             int64_t& c, int64_t& lo, int64_t& hi,
+                                             int64_t& last) {
+    int64_t a = 0, b = g.n_seg;  // find s: chunk_off[s] <= ch < chunk_off[s+1]
+    while (b - a > 1) {
+        const int64_t m = (a + b) >> 1;
+        if (g.chunk_off[m] <= ch) a = m;
+        else b = m;
+    }
+    s = a;
+    c = ch - g.chunk_off[s];
+    const int64_t first = g.seg_first[s];
+    last = first + g.seg_steps[s];
+    lo = first + c * g.C;
+    hi = lo + g.C < last ? lo + g.C : last;
+}
+
+// Phase 1: speculative parse of every chunk from its first start position.
+__global__ void k_spec(const double* __restrict__ v, ChunkGeom g, int64_t n_chunks, double tol2,
+                       int64_t max_len, uint8_t* __restrict__ flags,
+                       int64_t* __restrict__ exit_spec, int* __restrict__ bad) {
+    const int64_t ch = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (ch >= n_chunks) return;
+    int64_t s, c, lo, hi, last;
+    chunk_bounds(g, ch, s, c, lo, hi, last);
+    // compress() rejects non-finite samples (compression.hpp:73-74)
+    bool ok = true;
+    for (int64_t i = lo; i <= hi; ++i) ok &= isfinite(v[i]);
+    if (!ok) atomicExch(bad, 1);
+    int64_t p = lo;
+    while (p < hi) {
+        flags[p] = 1;
+        p = piece_end(v, p, last, tol2, max_len);
+    }
+    exit_spec[ch] = p;
+}
+
+// Phase 2: E_out[c] = F_c(E_in[c-1]), F_c = exit of chunk c when the true
+// orbit enters it at t.
+__global__ void k_fix(const double* __restrict__ v, ChunkGeom g, int64_t n_chunks, double tol2,
+                      int64_t max_len, const uint8_t* __restrict__ flags,
+                      const int64_t* __restrict__ exit_spec, const int64_t* __restrict__ E_in,
+                      int64_t* __restrict__ E_out, int* __restrict__ changed) {
+    const int64_t ch = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (ch >= n_chunks) return;
+    int64_t s, c, lo, hi, last;
+    chunk_bounds(g, ch, s, c, lo, hi, last);
+    int64_t r;
+    if (c == 0) {
+        r = exit_spec[ch];
+    } else {
+        const int64_t t = E_in[ch - 1];
+        if (t >= hi) {
+            r = t;
+        } else if (flags[t]) {
+            r = exit_spec[ch];
+        } else {
+            int64_t q = t;
+            do {
+                q = piece_end(v, q, last, tol2, max_len);
+            } while (q < hi && !flags[q]);
+            r = q < hi ? exit_spec[ch] : q;
+        }
+    }
+    E_out[ch] = r;
+    if (r != E_in[ch]) atomicExch(changed, 1);
+}
+
+// Phase 3: rewrite each chunk's flags to the true orbit and count its pieces.
+__global__ void k_apply(const double* __restrict__ v, ChunkGeom g, int64_t n_chunks, double tol2,
+                        int64_t max_len, uint8_t* __restrict__ flags,
+                        const int64_t* __restrict__ E, int64_t* __restrict__ count) {
+    const int64_t ch = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (ch >= n_chunks) return;
+    int64_t s, c, lo, hi, last;
+    chunk_bounds(g, ch, s, c, lo, hi, last);
+    const int64_t T = c == 0 ? lo : E[ch - 1];
+    if (T >= hi) {
+        for (int64_t i = lo; i < hi; ++i) flags[i] = 0;
+    } else {
+        for (int64_t i = lo; i < T; ++i) flags[i] = 0;
+        if (!flags[T]) {
+            int64_t p = T;
+            flags[p] = 1;
+            for (;;) {
+                const int64_t q = piece_end(v, p, last, tol2, max_len);
+                const int64_t z = q < hi ? q : hi;
+                for (int64_t i = p + 1; i < z; ++i) flags[i] = 0;
+                if (q >= hi || flags[q]) break;
+                flags[q] = 1;
+                p = q;
+            }
+        }
+    }
+    int64_t n = 0;
+    for (int64_t i = lo; i < hi; ++i) n += flags[i];
+    count[ch] = n;
+}
+
+// Phase 4: emit (len, inc) pieces in input order; per-block max|inc| and
+// max len for the fixed-point exponents downstream.
+__global__ void k_emit(const double* __restrict__ v, ChunkGeom g, int64_t n_chunks,
+                       const uint8_t* __restrict__ flags, const int64_t* __restrict__ E,
+                       const int64_t* __restrict__ base, int32_t* __restrict__ out_len,
+                       double* __restrict__ out_inc, unsigned long long* __restrict__ max_inc_bits,
+                       int* __restrict__ max_len) {
+    const int64_t ch = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    double mi = 0.0;
+    int ml = 0;
+    if (ch < n_chunks) {
+        int64_t s, c, lo, hi, last;
+        chunk_bounds(g, ch, s, c, lo, hi, last);
+        int64_t j = base[ch];
+        int64_t p = -1;
+        for (int64_t i = lo; i < hi; ++i) {
+            if (!flags[i]) continue;
+            if (p >= 0) {
+                const double inc = v[i] - v[p];
+                out_len[j] = (int32_t)(i - p);
+                out_inc[j] = inc;
+                mi = fmax(mi, fabs(inc));
+                ml = max(ml, (int)(i - p));
+                ++j;
+            }
+            p = i;
+        }
+        if (p >= 0) {
+            const int64_t e = E[ch];  // true exit: next start or segment end
+            const double inc = v[e] - v[p];
+            out_len[j] = (int32_t)(e - p);
+            out_inc[j] = inc;
+            mi = fmax(mi, fabs(inc));
+            ml = max(ml, (int)(e - p));
+        }
+    }
+    // block max
+    for (int o = 16; o > 0; o >>= 1) {
+        mi = fmax(mi, __shfl_down_sync(0xffffffffu, mi, o));
+        ml = max(ml, __shfl_down_sync(0xffffffffu, ml, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(max_inc_bits, dbits(mi));
+        atomicMax(max_len, ml);
+    }
+}
+
+__global__ void k_seg_offsets(const int64_t* __restrict__ chunk_off,
+                              const int64_t* __restrict__ base, int64_t n_seg, int64_t total,
+                              int64_t* __restrict__ seg_off) {
+    const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (s < n_seg) seg_off[s] = base[chunk_off[s]];
+    if (s == n_seg) seg_off[s] = total;
+}
+
+void compress_segments(const double* d_values, const SegTable& seg, double tol,
+                       int64_t max_piece_len, Pieces& out, cudaStream_t st, int* n_fix_iters) {
+    const int64_t n_seg = seg.n_seg;
+    // chunk size: enough chunks to fill 148 SMs, clamped to [32, 256] steps
+    int64_t C = 256;
+    while (C > 32 && seg.total_steps / C < (int64_t)kSMs * 1024) C >>= 1;
+    std::vector<int64_t> h_chunk_off(n_seg + 1);
+    int64_t max_last = 0;
+    h_chunk_off[0] = 0;
+    for (int64_t s = 0; s < n_seg; ++s) {
+        h_chunk_off[s + 1] = h_chunk_off[s] + (seg.h_steps[s] + C - 1) / C;
+        max_last = std::max(max_last, seg.h_first[s] + seg.h_steps[s]);
+    }
+    const int64_t n_chunks = h_chunk_off[n_seg];
+    DArr<int64_t> chunk_off(n_seg + 1, st);
+    chunk_off.upload(h_chunk_off.data(), n_seg + 1);
+    ChunkGeom g{seg.first.p, seg.steps.p, chunk_off.p, n_seg, C};
+
+    const double tol2 = tol * tol;
+    DArr<uint8_t> flags(max_last + 1, st);
+    flags.zero();
+    DArr<int64_t> exit_spec(n_chunks, st), Ea(n_chunks, st), Eb(n_chunks, st), cnt(n_chunks, st);
+    DArr<int> dflag(2, st);
+    dflag.zero();
+    const int TB = 128;
+    const int nb = ceil_div(n_chunks, TB);
+    {
+        JB_PROF("compress_spec", st);
+        k_spec<<<nb, TB, 0, st>>>(d_values, g, n_chunks, tol2, max_piece_len, flags.p, exit_spec.p,
+                              dflag.p);
+    }
+    JB_LAUNCH_CHECK();
+    int hflag[2];
+    dflag.download(hflag, 1);
+    JB_CUDA(cudaStreamSynchronize(st));
+    if (hflag[0]) throw Error(INVALID_INPUT, "compression input has non-finite values");
+
+    JB_CUDA(cudaMemcpyAsync(Ea.p, exit_spec.p, sizeof(int64_t) * n_chunks,
+                            cudaMemcpyDeviceToDevice, st));
+    int iters = 0;
+    for (;;) {
+        JB_CUDA(cudaMemsetAsync(dflag.p + 1, 0, sizeof(int), st));
+        {
+            JB_PROF("compress_fix", st);
+            k_fix<<<nb, TB, 0, st>>>(d_values, g, n_chunks, tol2, max_piece_len, flags.p,
+                                 exit_spec.p, Ea.p, Eb.p, dflag.p + 1);
+        }
+        JB_LAUNCH_CHECK();
+        ++iters;
+        int ch;
+        JB_CUDA(cudaMemcpyAsync(&ch, dflag.p + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+        JB_CUDA(cudaStreamSynchronize(st));
+        std::swap(Ea, Eb);
+        if (!ch) break;
+    }
+    if (n_fix_iters) *n_fix_iters = iters;
+    {
+        JB_PROF("compress_apply", st);
+        k_apply<<<nb, TB, 0, st>>>(d_values, g, n_chunks, tol2, max_piece_len, flags.p, Ea.p, cnt.p);
+    }
+    JB_LAUNCH_CHECK();
+
+    DArr<int64_t> base(n_chunks + 1, st);
+    size_t tmp_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt.p, base.p, n_chunks + 1, st);
+    // the scan input needs a trailing zero so base[n_chunks] is the total
+    DArr<int64_t> cnt1(n_chunks + 1, st);
+    JB_CUDA(cudaMemcpyAsync(cnt1.p, cnt.p, sizeof(int64_t) * n_chunks, cudaMemcpyDeviceToDevice,
+                            st));
+    JB_CUDA(cudaMemsetAsync(cnt1.p + n_chunks, 0, sizeof(int64_t), st));
+    DArr<uint8_t> tmp(tmp_bytes, st);
+    cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, cnt1.p, base.p, n_chunks + 1, st);
+    JB_LAUNCH_CHECK();
+    int64_t N = 0;
+    JB_CUDA(cudaMemcpyAsync(&N, base.p + n_chunks, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    JB_CUDA(cudaStreamSynchronize(st));
+
+    out.N = N;
+    out.len.alloc(N, st);
+    out.inc.alloc(N, st);
+    out.seg_offsets.alloc(n_seg + 1, st);
+    DArr<unsigned long long> mx(1, st);
+    mx.zero();
+    DArr<int> ml(1, st);
+    ml.zero();
+    {
+        JB_PROF("compress_emit", st);
+        k_emit<<<nb, TB, 0, st>>>(d_values, g, n_chunks, flags.p, Ea.p, base.p, out.len.p, out.inc.p,
+                              mx.p, ml.p);
+    }
+    JB_LAUNCH_CHECK();
+    k_seg_offsets<<<ceil_div(n_seg + 1, 256), 256, 0, st>>>(chunk_off.p, base.p, n_seg, N,
+                                                            out.seg_offsets.p);
+    JB_LAUNCH_CHECK();
+    unsigned long long hmx = 0;
+    int hml = 0;
+    mx.download(&hmx, 1);
+    ml.download(&hml, 1);
+    JB_CUDA(cudaStreamSynchronize(st));
+    memcpy(&out.max_abs_inc, &hmx, 8);
+    out.max_len = hml;
+}
+
+}  // namespace jb

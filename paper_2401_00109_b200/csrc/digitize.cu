@@ -1,0 +1,384 @@
+// digitize.cu — scaling (digitization.hpp:25-59), nearest-center assignment
+// with group statistics (clustering.hpp:146-163, digitization.hpp:217-253),
+// relabeling by cardinality rank (:255-291).
+//
+// Sums that the reference accumulates sequentially in fp64 are accumulated
+// here as 128-bit fixed-point integers (jb_common.cuh): deterministic for any
+// grid or GPU count, and within an ulp-scale of the sequential result.
+#include <cub/cub.cuh>
+
+#include <cmath>
+
+#include "jb_device.hpp"
+
+namespace jb {
+
+namespace {
+
+__device__ __forceinline__ unsigned long long ord_bits(double x) {
+    // order-preserving map of any double to u64
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+inline double ord_to_double(unsigned long long u) {
+    const unsigned long long b = (u >> 63) ? (u & 0x7FFFFFFFFFFFFFFFULL) : ~u;
+    double d;
+    memcpy(&d, &b, 8);
+    return d;
+}
+
+template <int TB>
+__device__ __forceinline__ i128 block_sum_i128(i128 v) {
+    __shared__ unsigned long long lo[TB / 32], hi[TB / 32];
+    v = fx_warp_sum(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        lo[w] = (unsigned long long)(u128)v;
+        hi[w] = (unsigned long long)((u128)v >> 64);
+    }
+    __syncthreads();
+    i128 r = 0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < TB / 32; ++i) r += (i128)(((u128)hi[i] << 64) | (u128)lo[i]);
+    __syncthreads();
+    return r;
+}
+
+constexpr int kTB = 256;
+
+__global__ void k_sum_inc(const double* __restrict__ inc, int64_t n, int E,
+                          unsigned long long* __restrict__ acc) {
+    i128 s = 0;
+    for (int64_t i = blockIdx.x * (int64_t)kTB + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * kTB)
+        s += fx_from_double(inc[i], E);
+    s = block_sum_i128<kTB>(s);
+    if (threadIdx.x == 0) fx_atomic_add(acc, s);
+}
+
+// var_len / var_inc accumulations of scale_pieces (digitization.hpp:39-45)
+__global__ void k_sum_var(const int32_t* __restrict__ len, const double* __restrict__ inc,
+                          int64_t n, double mean_len, double mean_inc, int El, int Ei,
+                          unsigned long long* __restrict__ acc) {
+    i128 sl = 0, si = 0;
+    for (int64_t i = blockIdx.x * (int64_t)kTB + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * kTB) {
+        const double dl = (double)len[i] - mean_len;
+        const double di = inc[i] - mean_inc;
+        sl += fx_from_double(dl * dl, El);
+        si += fx_from_double(di * di, Ei);
+    }
+    sl = block_sum_i128<kTB>(sl);
+    si = block_sum_i128<kTB>(si);
+    if (threadIdx.x == 0) {
+        fx_atomic_add(acc, sl);
+        fx_atomic_add(acc + 2, si);
+    }
+}
+
+// ScalingParams::apply (core.hpp:130-132) + bounding box
+__global__ void k_scale(const int32_t* __restrict__ len, const double* __restrict__ inc,
+                        int64_t n, double scl, double sl, double si, double* __restrict__ pts,
+                        unsigned long long* __restrict__ bb) {
+    unsigned long long xmn = ~0ULL, xmx = 0, ymn = ~0ULL, ymx = 0;
+    for (int64_t i = blockIdx.x * (int64_t)kTB + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * kTB) {
+        const double x = scl * (double)len[i] / sl;
+        const double y = inc[i] / si;
+        reinterpret_cast<double2*>(pts)[i] = make_double2(x, y);
+        const unsigned long long ox = ord_bits(x), oy = ord_bits(y);
+        xmn = min(xmn, ox);
+        xmx = max(xmx, ox);
+        ymn = min(ymn, oy);
+        ymx = max(ymx, oy);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        xmn = min(xmn, __shfl_down_sync(0xffffffffu, xmn, o));
+        xmx = max(xmx, __shfl_down_sync(0xffffffffu, xmx, o));
+        ymn = min(ymn, __shfl_down_sync(0xffffffffu, ymn, o));
+        ymx = max(ymx, __shfl_down_sync(0xffffffffu, ymx, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(bb + 0, xmn);
+        atomicMax(bb + 1, xmx);
+        atomicMin(bb + 2, ymn);
+        atomicMax(bb + 3, ymx);
+    }
+}
+
+int grid_for(int64_t n) {
+    const int64_t b = (n + kTB - 1) / kTB;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)kSMs * 8));
+}
+
+}  // namespace
+
+void scale_pieces(const Pieces& pc, int64_t total_steps, double scl, Scaled& out,
+                  cudaStream_t st) {
+    const int64_t N = pc.N;
+    if (N == 0) throw Error(INVALID_INPUT, "digitize: no pieces");
+    if (scl < 0.0) throw Error(INVALID_INPUT, "scale_pieces: scl must be >= 0");
+    const double n = (double)N;
+    // sum of (double)len over all pieces is exactly the total step count
+    // sum of lens over all pieces == total steps of all segments (exact)
+    DArr<unsigned long long> acc(6, st);
+    acc.zero();
+    const int Einc = fx_exponent_for(pc.max_abs_inc * n * 1.0000001 + 1e-300);
+    {
+        JB_PROF("scale_sum_inc", st);
+        k_sum_inc<<<grid_for(N), kTB, 0, st>>>(pc.inc.p, N, Einc, acc.p);
+    }
+    JB_LAUNCH_CHECK();
+    unsigned long long h[6];
+    acc.download(h, 2);
+    JB_CUDA(cudaStreamSynchronize(st));
+    // mean_len: sequential double sum of integer lens is exact (< 2^53)
+    const double mean_len = (double)total_steps / n;
+    const double mean_inc = fx_to_double(fx_load(h), Einc) / n;
+
+    const double dlmax = std::max((double)pc.max_len - mean_len, mean_len - 1.0) + 1.0;
+    const double dimax = pc.max_abs_inc + std::fabs(mean_inc) + 1e-300;
+    const int El = fx_exponent_for(dlmax * dlmax * n * 1.001 + 1e-300);
+    const int Ei = fx_exponent_for(dimax * dimax * n * 1.001 + 1e-300);
+    acc.zero();
+    {
+        JB_PROF("scale_sum_var", st);
+        k_sum_var<<<grid_for(N), kTB, 0, st>>>(pc.len.p, pc.inc.p, N, mean_len, mean_inc, El, Ei,
+                                          acc.p);
+    }
+    JB_LAUNCH_CHECK();
+    acc.download(h, 4);
+    JB_CUDA(cudaStreamSynchronize(st));
+    const double var_len = fx_to_double(fx_load(h), El);
+    const double var_inc = fx_to_double(fx_load(h + 2), Ei);
+    double sl = N > 1 ? std::sqrt(var_len / (n - 1.0)) : 0.0;
+    double si = N > 1 ? std::sqrt(var_inc / (n - 1.0)) : 0.0;
+    if (sl <= 0.0) sl = 1.0;
+    if (si <= 0.0) si = 1.0;
+    out.scl = scl;
+    out.sigma_len = sl;
+    out.sigma_inc = si;
+
+    out.pts.alloc(2 * N, st);
+    DArr<unsigned long long> bb(4, st);
+    unsigned long long init[4] = {~0ULL, 0ULL, ~0ULL, 0ULL};
+    bb.upload(init, 4);
+    {
+        JB_PROF("scale_points", st);
+        k_scale<<<grid_for(N), kTB, 0, st>>>(pc.len.p, pc.inc.p, N, scl, sl, si, out.pts.p, bb.p);
+    }
+    JB_LAUNCH_CHECK();
+    unsigned long long hb[4];
+    bb.download(hb, 4);
+    JB_CUDA(cudaStreamSynchronize(st));
+    out.xmin = ord_to_double(hb[0]);
+    out.xmax = ord_to_double(hb[1]);
+    out.ymin = ord_to_double(hb[2]);
+    out.ymax = ord_to_double(hb[3]);
+}
+
+// ---------------------------------------------------------------------------
+// Nearest-center assignment + group statistics.
+
+namespace {
+
+struct StatsAcc {
+    unsigned long long* counts;  // k
+    unsigned long long* first;   // k (min index)
+    unsigned long long* lens;    // k
+    unsigned long long* sx;      // 2k (lo, hi)
+    unsigned long long* sy;      // 2k
+};
+
+// nearest_center (clustering.hpp:146-157): strict <, lowest index on ties
+__device__ __forceinline__ uint32_t nearest(double px, double py, const double* cx,
+                                            const double* cy, int k) {
+    uint32_t best = 0;
+    double bd = __longlong_as_double(0x7FF0000000000000LL);  // +inf
+    for (int c = 0; c < k; ++c) {
+        const double d = dist2(px, py, cx[c], cy[c]);
+        if (d < bd) {
+            bd = d;
+            best = (uint32_t)c;
+        }
+    }
+    return best;
+}
+
+// block-privatized statistics in shared memory, flushed with global atomics
+__global__ void k_assign_stats(const double2* __restrict__ pts, const int32_t* __restrict__ len,
+                               int64_t n, const double* __restrict__ centers, int k,
+                               int do_assign, uint32_t* __restrict__ labels, int Ex, int Ey,
+                               StatsAcc g, int privatize) {
+    extern __shared__ unsigned char smem[];
+    double* cx = reinterpret_cast<double*>(smem);
+    double* cy = cx + k;
+    unsigned long long* s_cnt = reinterpret_cast<unsigned long long*>(cy + k);
+    unsigned long long* s_first = s_cnt + k;
+    unsigned long long* s_len = s_first + k;
+    unsigned long long* s_sx = s_len + k;
+    unsigned long long* s_sy = s_sx + 2 * k;
+    for (int c = threadIdx.x; c < k; c += blockDim.x) {
+        cx[c] = centers[2 * c];
+        cy[c] = centers[2 * c + 1];
+        if (privatize) {
+            s_cnt[c] = 0;
+            s_first[c] = ~0ULL;
+            s_len[c] = 0;
+            s_sx[2 * c] = s_sx[2 * c + 1] = 0;
+            s_sy[2 * c] = s_sy[2 * c + 1] = 0;
+        }
+    }
+    __syncthreads();
+    unsigned long long* t_cnt = privatize ? s_cnt : g.counts;
+    unsigned long long* t_first = privatize ? s_first : g.first;
+    unsigned long long* t_len = privatize ? s_len : g.lens;
+    unsigned long long* t_sx = privatize ? s_sx : g.sx;
+    unsigned long long* t_sy = privatize ? s_sy : g.sy;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double2 p = pts[i];
+        uint32_t lab;
+        if (do_assign) {
+            lab = nearest(p.x, p.y, cx, cy, k);
+            labels[i] = lab;
+        } else {
+            lab = labels[i];
+        }
+        atomicAdd(t_cnt + lab, 1ULL);
+        atomicMin(t_first + lab, (unsigned long long)i);
+        atomicAdd(t_len + lab, (unsigned long long)len[i]);
+        fx_atomic_add(t_sx + 2 * lab, fx_from_double(p.x, Ex));
+        fx_atomic_add(t_sy + 2 * lab, fx_from_double(p.y, Ey));
+    }
+    if (!privatize) return;
+    __syncthreads();
+    for (int c = threadIdx.x; c < k; c += blockDim.x) {
+        if (s_cnt[c] == 0) continue;
+        atomicAdd(g.counts + c, s_cnt[c]);
+        atomicMin(g.first + c, s_first[c]);
+        atomicAdd(g.lens + c, s_len[c]);
+        fx_atomic_add(g.sx + 2 * c, fx_load(s_sx + 2 * c));
+        fx_atomic_add(g.sy + 2 * c, fx_load(s_sy + 2 * c));
+    }
+}
+
+__global__ void k_relabel(uint32_t* __restrict__ labels, int64_t n,
+                          const uint32_t* __restrict__ rank_of, int k) {
+    extern __shared__ uint32_t rk[];
+    for (int c = threadIdx.x; c < k; c += blockDim.x) rk[c] = rank_of[c];
+    __syncthreads();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        labels[i] = rk[labels[i]];
+}
+
+__global__ void k_relabel_global(uint32_t* __restrict__ labels, int64_t n,
+                                 const uint32_t* __restrict__ rank_of) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        labels[i] = rank_of[labels[i]];
+}
+
+__global__ void k_sample_len(const uint64_t* __restrict__ sample,
+                             const uint32_t* __restrict__ slab, int64_t S,
+                             const int32_t* __restrict__ len, unsigned long long* __restrict__ ls,
+                             unsigned long long* __restrict__ lc) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < S;
+         s += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t g = slab[s];
+        atomicAdd(ls + g, (unsigned long long)len[sample[s]]);
+        atomicAdd(lc + g, 1ULL);
+    }
+}
+
+__global__ void k_gather(const double2* __restrict__ pts, const uint64_t* __restrict__ idx,
+                         int64_t S, double2* __restrict__ out) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < S;
+         s += (int64_t)gridDim.x * blockDim.x)
+        out[s] = pts[idx[s]];
+}
+
+}  // namespace
+
+void assign_and_stats(const double* d_pts, const int32_t* d_len, int64_t n,
+                      const std::vector<double>& centers, uint64_t k, const BBox& bb,
+                      bool do_assign, uint32_t* d_labels, GroupStats& gs, cudaStream_t st) {
+    DArr<double> dc(2 * k, st);
+    dc.upload(centers.data(), 2 * k);
+    DArr<unsigned long long> acc(7 * k, st);
+    acc.zero();
+    JB_CUDA(cudaMemsetAsync(acc.p + k, 0xFF, sizeof(unsigned long long) * k, st));
+    StatsAcc g{acc.p, acc.p + k, acc.p + 2 * k, acc.p + 3 * k, acc.p + 5 * k};
+    const double mx = std::max(std::fabs(bb.xmin), std::fabs(bb.xmax));
+    const double my = std::max(std::fabs(bb.ymin), std::fabs(bb.ymax));
+    const int Ex = fx_exponent_for(mx * (double)n * 1.001 + 1e-300);
+    const int Ey = fx_exponent_for(my * (double)n * 1.001 + 1e-300);
+    const size_t base_smem = sizeof(double) * 2 * k;
+    const size_t priv_smem = sizeof(unsigned long long) * 7 * k;
+    int privatize = base_smem + priv_smem <= 160 * 1024;
+    const size_t smem = base_smem + (privatize ? priv_smem : 0);
+    if (smem > 200 * 1024) throw Error(INVALID_INPUT, "k too large for the assignment kernel");
+    JB_CUDA(cudaFuncSetAttribute(k_assign_stats, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    const int TB = 256;
+    const int grid = (int)std::max<int64_t>(
+        1, std::min<int64_t>((n + TB - 1) / TB, (int64_t)kSMs * (privatize ? 2 : 8)));
+    {
+        JB_PROF("assign_stats", st);
+        k_assign_stats<<<grid, TB, smem, st>>>(reinterpret_cast<const double2*>(d_pts), d_len, n,
+                                           dc.p, (int)k, do_assign ? 1 : 0, d_labels, Ex, Ey, g,
+                                           privatize);
+    }
+    JB_LAUNCH_CHECK();
+    std::vector<unsigned long long> h = acc.to_host(7 * k);
+    gs.counts.assign(h.begin(), h.begin() + k);
+    gs.first_seen.assign(h.begin() + k, h.begin() + 2 * k);
+    gs.len_sums.assign(h.begin() + 2 * k, h.begin() + 3 * k);
+    gs.sum_x.resize(k);
+    gs.sum_y.resize(k);
+    for (uint64_t c = 0; c < k; ++c) {
+        gs.sum_x[c] = fx_to_double(fx_load(&h[3 * k + 2 * c]), Ex);
+        gs.sum_y[c] = fx_to_double(fx_load(&h[5 * k + 2 * c]), Ey);
+    }
+}
+
+void relabel(uint32_t* d_labels, int64_t n, const std::vector<uint32_t>& rank_of,
+             cudaStream_t st) {
+    const int k = (int)rank_of.size();
+    DArr<uint32_t> rk(k, st);
+    rk.upload(rank_of.data(), k);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, kSMs * 8));
+    if ((size_t)k * 4 <= 48 * 1024)
+        k_relabel<<<grid, 256, k * 4, st>>>(d_labels, n, rk.p, k);
+    else
+        k_relabel_global<<<grid, 256, 0, st>>>(d_labels, n, rk.p);
+    JB_LAUNCH_CHECK();
+    JB_CUDA(cudaStreamSynchronize(st));
+}
+
+void sample_len_stats(const uint64_t* d_sample, const uint32_t* d_sample_labels, int64_t S,
+                      const int32_t* d_len, uint64_t k, std::vector<uint64_t>& len_sum,
+                      std::vector<uint64_t>& count, cudaStream_t st) {
+    DArr<unsigned long long> acc(2 * k, st);
+    acc.zero();
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((S + 255) / 256, kSMs * 8));
+    k_sample_len<<<grid, 256, 0, st>>>(d_sample, d_sample_labels, S, d_len, acc.p, acc.p + k);
+    JB_LAUNCH_CHECK();
+    auto h = acc.to_host(2 * k);
+    len_sum.assign(h.begin(), h.begin() + k);
+    count.assign(h.begin() + k, h.end());
+}
+
+void gather_points(const double* d_pts, const uint64_t* d_idx, int64_t S, double* d_out,
+                   cudaStream_t st) {
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((S + 255) / 256, kSMs * 8));
+    {
+        JB_PROF("sample_gather", st);
+        k_gather<<<grid, 256, 0, st>>>(reinterpret_cast<const double2*>(d_pts), d_idx, S,
+                                   reinterpret_cast<double2*>(d_out));
+    }
+    JB_LAUNCH_CHECK();
+}
+
+}  // namespace jb

@@ -1,0 +1,198 @@
+// jb_common.cuh — shared device utilities for the B200 JABBA path.
+//
+// Built with -fmad=false: every fp64 expression that mirrors a reference
+// expression must round exactly as the reference's SSE2 build does
+// (proj/CMakeLists.txt:5-10 has no -march, hence no FMA contraction).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace jb {
+
+// Status codes mirror the reference's error hierarchy (core.hpp:20-30).
+enum Status : int {
+    OK = 0,
+    INVALID_INPUT = 1,
+    INVALID_PIECE = 2,
+    INVALID_PARTITION = 3,
+    UNKNOWN_SYMBOL = 4,
+    PARSE_ERROR = 5,
+    LAYOUT_ERROR = 6,
+    VERSION_ERROR = 7,
+    CUDA_ERROR = 100,
+    NCCL_ERROR = 101,
+    NO_DEVICE = 102,
+    INTERNAL = 103,
+};
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define JB_CUDA(call)                                                                   \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            throw ::jb::Error(::jb::CUDA_ERROR, std::string(#call) + ": " +             \
+                                                    cudaGetErrorString(e_));            \
+    } while (0)
+
+#define JB_LAUNCH_CHECK() JB_CUDA(cudaGetLastError())
+
+typedef unsigned __int128 u128;
+typedef __int128 i128;
+
+// ---------------------------------------------------------------------------
+// Deterministic fp64 summation: every addend is converted to a signed 128-bit
+// fixed-point integer with a per-quantity binary exponent E (value * 2^E,
+// magnitude truncated), and accumulated with integer adds. Integer addition is
+// associative, so the result is bitwise identical for any launch geometry,
+// atomic order or GPU count (the determinism contract of parallel.hpp:3-5,
+// extended to 1/2/4/8 GPUs). E is chosen so the largest possible |sum| stays
+// below 2^126; addends >= 2^(53-E) are represented exactly.
+
+__host__ __device__ inline int fx_exponent_for(double max_abs_sum) {
+    // smallest e with max_abs_sum < 2^e, then E = 125 - e
+    if (!(max_abs_sum > 0.0)) return 0;
+    int e = 0;
+    double m = max_abs_sum;
+    // frexp-free exponent extraction (works on host and device)
+    uint64_t bits;
+    memcpy(&bits, &m, 8);
+    e = (int)((bits >> 52) & 0x7FF) - 1022;  // m < 2^e
+    int E = 125 - e;
+    if (E > 1000) E = 1000;
+    return E;
+}
+
+// |x| * 2^E truncated to an integer, with x's sign.
+__device__ __forceinline__ i128 fx_from_double(double x, int E) {
+    uint64_t bits = (uint64_t)__double_as_longlong(x);
+    const int bexp = (int)((bits >> 52) & 0x7FF);
+    if (bexp == 0) return 0;  // zero / subnormal: below any resolution we use
+    const uint64_t mant = (bits & 0x000FFFFFFFFFFFFFULL) | 0x0010000000000000ULL;
+    // x = mant * 2^(bexp - 1075)
+    const int sh = bexp - 1075 + E;
+    u128 mag;
+    if (sh >= 0) {
+        if (sh > 74) mag = ((u128)1) << 126;  // saturate (caller's E makes this unreachable)
+        else mag = ((u128)mant) << sh;
+    } else {
+        mag = (sh <= -64) ? 0 : (u128)(mant >> (-sh));
+    }
+    const i128 v = (i128)mag;
+    return (bits >> 63) ? -v : v;
+}
+
+// Correctly rounded (nearest-even) conversion of a fixed-point integer back to
+// double, then exact scaling by 2^-E.
+__host__ __device__ inline double fx_to_double(i128 v, int E) {
+    if (v == 0) return 0.0;
+    const bool neg = v < 0;
+    u128 m = neg ? (u128)(-v) : (u128)v;
+    int lz = 0;
+    {
+        uint64_t hi = (uint64_t)(m >> 64);
+        uint64_t lo = (uint64_t)m;
+        if (hi) {
+#ifdef __CUDA_ARCH__
+            lz = __clzll((long long)hi);
+#else
+            lz = __builtin_clzll(hi);
+#endif
+        } else {
+#ifdef __CUDA_ARCH__
+            lz = 64 + __clzll((long long)lo);
+#else
+            lz = 64 + __builtin_clzll(lo);
+#endif
+        }
+    }
+    const int msb = 127 - lz;  // index of the leading one
+    uint64_t mant;
+    int exp2;  // value = mant * 2^exp2
+    if (msb <= 52) {
+        mant = (uint64_t)m;
+        exp2 = 0;
+    } else {
+        const int drop = msb - 52;
+        const u128 keep = m >> drop;
+        const u128 rem = m - (keep << drop);
+        const u128 half = ((u128)1) << (drop - 1);
+        mant = (uint64_t)keep;
+        exp2 = drop;
+        if (rem > half || (rem == half && (mant & 1))) {
+            ++mant;
+            if (mant == (1ULL << 53)) {
+                mant >>= 1;
+                ++exp2;
+            }
+        }
+    }
+    // mant < 2^53 exactly representable; scale by 2^(exp2 - E)
+    double d = (double)mant;
+    int s = exp2 - E;
+    // scale in steps to avoid overflow/underflow of the factor itself
+    while (s > 600) { d *= 0x1p600; s -= 600; }
+    while (s < -600) { d *= 0x1p-600; s += 600; }
+    double f;
+    {
+        uint64_t fb = (uint64_t)(s + 1023) << 52;
+        memcpy(&f, &fb, 8);
+    }
+    d *= f;
+    return neg ? -d : d;
+}
+
+// Global int128 accumulator stored as two u64 words (lo, hi).
+__device__ __forceinline__ void fx_atomic_add(unsigned long long* lohi, i128 v) {
+    if (v == 0) return;
+    const u128 u = (u128)v;
+    const unsigned long long lo = (unsigned long long)u;
+    const unsigned long long hi = (unsigned long long)(u >> 64);
+    const unsigned long long old = atomicAdd(lohi, lo);
+    const unsigned long long carry = (old + lo) < old ? 1ULL : 0ULL;
+    const unsigned long long h = hi + carry;
+    if (h) atomicAdd(lohi + 1, h);
+}
+
+__host__ __device__ inline i128 fx_load(const unsigned long long* lohi) {
+    return (i128)(((u128)lohi[1] << 64) | (u128)lohi[0]);
+}
+
+// warp-level int128 sum (deterministic: integer adds)
+__device__ __forceinline__ i128 fx_warp_sum(i128 v) {
+    unsigned long long lo = (unsigned long long)(u128)v;
+    unsigned long long hi = (unsigned long long)((u128)v >> 64);
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long olo = __shfl_down_sync(0xffffffffu, lo, o);
+        const unsigned long long ohi = __shfl_down_sync(0xffffffffu, hi, o);
+        const unsigned long long nlo = lo + olo;
+        hi = hi + ohi + (nlo < lo ? 1ULL : 0ULL);
+        lo = nlo;
+    }
+    return (i128)(((u128)hi << 64) | (u128)lo);
+}
+
+// exact reference distance: dx*dx + dy*dy with no contraction (clustering.hpp:52-56)
+__device__ __forceinline__ double dist2(double ax, double ay, double bx, double by) {
+    const double dx = __dsub_rn(ax, bx);
+    const double dy = __dsub_rn(ay, by);
+    return __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+}
+
+// non-negative double <-> order-preserving u64 (for atomicMax on >= 0 values)
+__device__ __forceinline__ unsigned long long dbits(double x) {
+    return (unsigned long long)__double_as_longlong(x);
+}
+
+inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+constexpr int kSMs = 148;
+
+}  // namespace jb

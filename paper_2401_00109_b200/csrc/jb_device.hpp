@@ -1,0 +1,203 @@
+// jb_device.hpp — stream-ordered device arrays and the kernel entry points
+// shared between the translation units of libjabba_b200.so.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <utility>
+#include <vector>
+
+#include "jb_common.cuh"
+
+namespace jb {
+
+// Move-only device array allocated from the stream-ordered pool
+// (cudaMallocAsync): buffers are recycled across fits without device syncs.
+template <class T>
+struct DArr {
+    T* p = nullptr;
+    size_t n = 0;
+    cudaStream_t s = 0;
+    DArr() = default;
+    DArr(size_t count, cudaStream_t st) { alloc(count, st); }
+    DArr(const DArr&) = delete;
+    DArr& operator=(const DArr&) = delete;
+    DArr(DArr&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+    DArr& operator=(DArr&& o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p;
+            n = o.n;
+            s = o.s;
+            o.p = nullptr;
+            o.n = 0;
+        }
+        return *this;
+    }
+    ~DArr() { release(); }
+    void alloc(size_t count, cudaStream_t st) {
+        release();
+        s = st;
+        n = count;
+        if (count) JB_CUDA(cudaMallocAsync((void**)&p, sizeof(T) * count, st));
+    }
+    void release() {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        n = 0;
+    }
+    void zero() {
+        if (n) JB_CUDA(cudaMemsetAsync(p, 0, sizeof(T) * n, s));
+    }
+    void upload(const T* h, size_t count) {
+        if (count) JB_CUDA(cudaMemcpyAsync(p, h, sizeof(T) * count, cudaMemcpyHostToDevice, s));
+    }
+    void download(T* h, size_t count) const {
+        if (count) JB_CUDA(cudaMemcpyAsync(h, p, sizeof(T) * count, cudaMemcpyDeviceToHost, s));
+    }
+    std::vector<T> to_host(size_t count) const {
+        std::vector<T> h(count);
+        download(h.data(), count);
+        JB_CUDA(cudaStreamSynchronize(s));
+        return h;
+    }
+};
+
+// ---------------------------------------------------------------------------
+// Kernel-level CUDA-event profiler (api.cu). When enabled, every instrumented
+// launch site records an event pair on the launching stream; totals are
+// collected per kernel name by jb_profile_read().
+
+void prof_begin(const char* name, cudaStream_t st);
+void prof_end(cudaStream_t st);
+
+struct ProfScope {
+    cudaStream_t st;
+    ProfScope(const char* name, cudaStream_t s) : st(s) { prof_begin(name, s); }
+    ~ProfScope() { prof_end(st); }
+};
+#define JB_CAT2(a, b) a##b
+#define JB_CAT(a, b) JB_CAT2(a, b)
+#define JB_PROF(name, st) ::jb::ProfScope JB_CAT(jb_prof_scope_, __LINE__)(name, st)
+
+// ---------------------------------------------------------------------------
+// Compression (compress.cu)
+
+struct SegTable {
+    int64_t n_seg = 0;
+    DArr<int64_t> first, steps;  // per segment: first sample index, steps
+    std::vector<int64_t> h_first, h_steps;
+    int64_t total_steps = 0;
+};
+
+struct Pieces {
+    int64_t N = 0;
+    DArr<int32_t> len;
+    DArr<double> inc;
+    DArr<int64_t> seg_offsets;  // n_seg + 1
+    double max_abs_inc = 0.0;
+    int32_t max_len = 0;
+};
+
+// Compresses every segment (compression.hpp:31-83, 167-193) with the
+// speculative-chunk scheme; validates finiteness. Throws jb::Error.
+void compress_segments(const double* d_values, const SegTable& seg, double tol,
+                       int64_t max_piece_len, Pieces& out, cudaStream_t st,
+                       int* n_fix_iters = nullptr);
+
+// ---------------------------------------------------------------------------
+// Scaling (digitize.cu): scale_pieces digitization.hpp:25-59
+
+struct Scaled {
+    DArr<double> pts;  // 2N interleaved (x, y)
+    double scl = 1.0, sigma_len = 1.0, sigma_inc = 1.0;
+    double xmin = 0, xmax = 0, ymin = 0, ymax = 0;  // bounding box of pts
+};
+
+void scale_pieces(const Pieces& pc, int64_t total_steps, double scl, Scaled& out,
+                  cudaStream_t st);
+
+struct BBox {
+    double xmin, xmax, ymin, ymax;
+};
+
+// ---------------------------------------------------------------------------
+// k-means family (kmeans.cu)
+
+struct KMeansOut {
+    uint64_t k = 0;
+    std::vector<double> centers;  // 2k, backend cluster order
+    DArr<uint32_t> labels;        // per input point (lloyd labels)
+    uint64_t iterations = 0;
+    double sse = 0.0;
+};
+
+// sample_indices (clustering.hpp:74-85) on device; idx is S entries.
+// Returns the number of engine draws consumed (>= S).
+uint64_t sample_indices_device(uint64_t n, uint64_t S, const uint64_t* d_raw, uint64_t raw_count,
+                               DArr<uint64_t>& idx, cudaStream_t st);
+
+// Raw std::mt19937_64 stream on device.
+void mt19937_64_generate(uint64_t seed, uint64_t count, DArr<uint64_t>& out, cudaStream_t st);
+
+// Best-of-n_init lloyd_once (clustering.hpp:200-236) on points (2n interleaved,
+// device). Draws are consumed from d_raw starting at *cursor (updated).
+void lloyd_best_device(const double* d_pts, int64_t n, uint64_t k, uint64_t max_iters,
+                       uint64_t n_init, const uint64_t* d_raw, uint64_t raw_count,
+                       uint64_t* cursor, const BBox& bb, KMeansOut& out, cudaStream_t st);
+
+// Per-point nearest center (clustering.hpp:146-163) with exact tie rule, plus
+// group statistics for digitize (digitization.hpp:217-231).
+struct GroupStats {
+    std::vector<uint64_t> counts, first_seen, len_sums;
+    std::vector<double> sum_x, sum_y;  // rounded exact sums
+};
+void assign_and_stats(const double* d_pts, const int32_t* d_len, int64_t n,
+                      const std::vector<double>& centers, uint64_t k, const BBox& bb,
+                      bool do_assign, uint32_t* d_labels, GroupStats& gs, cudaStream_t st);
+
+void relabel(uint32_t* d_labels, int64_t n, const std::vector<uint32_t>& rank_of,
+             cudaStream_t st);
+
+// Sum of len and count over sample labels (svq empty-cluster fallback,
+// digitization.hpp:240-252).
+void sample_len_stats(const uint64_t* d_sample, const uint32_t* d_sample_labels, int64_t S,
+                      const int32_t* d_len, uint64_t k, std::vector<uint64_t>& len_sum,
+                      std::vector<uint64_t>& count, cudaStream_t st);
+
+void gather_points(const double* d_pts, const uint64_t* d_idx, int64_t S, double* d_out,
+                   cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+// Greedy aggregation (ga.cu): greedy_aggregate clustering.hpp:328-375
+
+struct GAOut {
+    uint64_t groups = 0;
+    DArr<uint32_t> labels;
+    int rounds = 0;  // decision rounds of the parallel sweep
+};
+void greedy_aggregate_device(const double* d_pts, int64_t n, double alpha, int sort_key,
+                             bool early_stop, const BBox& bb, GAOut& out, cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+// Inverse (inverse.cu): inverse.hpp:32-132
+
+struct InverseIn {
+    const uint32_t* labels;       // N ranked labels (device)
+    const int64_t* seg_offsets;   // n_seg+1 (device)
+    const double* anchors;        // n_seg (device)
+    const int64_t* source_lengths;// n_seg (device)
+    const int64_t* out_offsets;   // n_seg (device): first output index of each segment
+    int64_t n_seg, N;
+    int32_t layout;
+    uint64_t k;
+    const double* centers;        // 2k (device)
+    const double* mean_lengths;   // k (device)
+    double scl, sigma_len, sigma_inc;
+};
+// Writes reconstructed samples into d_out. Throws on unknown_symbol /
+// invalid_piece exactly where the reference throws.
+void inverse_transform_device(const InverseIn& in, double* d_out, cudaStream_t st);
+
+}  // namespace jb
