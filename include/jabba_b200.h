@@ -171,6 +171,10 @@ void jb_profile_enable(int32_t on);
 void jb_profile_reset(void);
 int32_t jb_profile_read(char* names, double* total_ms, int64_t* launches, int32_t cap);
 
+/* Measured fp64 DFMA throughput of `device` in TFLOP/s (2 flops per DFMA):
+ * the roofline denominator for fp64-bound kernels. */
+jb_status jb_probe_fp64_tflops(int device, double* tflops);
+
 /* symbol token of cluster rank r in an alphabet of size k (core.hpp:186-193);
  * writes a NUL-terminated string into buf (>= 24 bytes); returns its length */
 int32_t jb_symbol_token(uint64_t rank, uint64_t alphabet_size, char* buf);

@@ -304,8 +304,9 @@ __global__ void k_gather(const double2* __restrict__ pts, const uint64_t* __rest
 void assign_and_stats(const double* d_pts, const int32_t* d_len, int64_t n,
                       const std::vector<double>& centers, uint64_t k, const BBox& bb,
                       bool do_assign, uint32_t* d_labels, GroupStats& gs, cudaStream_t st) {
-    DArr<double> dc(2 * k, st);
-    dc.upload(centers.data(), 2 * k);
+    DArr<double> dc(std::max<uint64_t>(2 * k, 1), st);
+    if (centers.size() >= 2 * k) dc.upload(centers.data(), 2 * k);  // GA: no centers needed
+    else if (do_assign) throw Error(INTERNAL, "assignment without centers");
     DArr<unsigned long long> acc(7 * k, st);
     acc.zero();
     JB_CUDA(cudaMemsetAsync(acc.p + k, 0xFF, sizeof(unsigned long long) * k, st));
