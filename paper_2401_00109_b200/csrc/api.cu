@@ -339,8 +339,8 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
             mt19937_64_generate(c.seed, raw_count, raw, st);
             uint64_t cursor = 0;
             KMeansOut km;
-            lloyd_best_device(sc.pts.p, N, c.k, c.max_iters, c.n_init, raw.p, raw_count, &cursor,
-                              bb, km, st);
+            lloyd_best_device(sc.pts.p, nullptr, N, c.k, c.max_iters, c.n_init, raw.p, raw_count,
+                              &cursor, bb, km, st);
             k = c.k;
             backend_centers = km.centers;
             labels = std::move(km.labels);
@@ -359,11 +359,9 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
             const uint64_t raw_count = S + (c.k + 1) * c.n_init + 4096;
             mt19937_64_generate(c.seed, raw_count, raw, st);
             uint64_t cursor = sample_indices_device((uint64_t)N, S, raw.p, raw_count, sample, st);
-            DArr<double> sp(2 * S, st);
-            gather_points(sc.pts.p, sample.p, (int64_t)S, sp.p, st);
             KMeansOut km;
-            lloyd_best_device(sp.p, (int64_t)S, c.k, c.max_iters, c.n_init, raw.p, raw_count,
-                              &cursor, bb, km, st);
+            lloyd_best_device(sc.pts.p, sample.p, (int64_t)S, c.k, c.max_iters, c.n_init, raw.p,
+                              raw_count, &cursor, bb, km, st);
             k = c.k;
             backend_centers = km.centers;
             sample_labels = std::move(km.labels);

@@ -141,11 +141,14 @@ uint64_t sample_indices_device(uint64_t n, uint64_t S, const uint64_t* d_raw, ui
 // Raw std::mt19937_64 stream on device.
 void mt19937_64_generate(uint64_t seed, uint64_t count, DArr<uint64_t>& out, cudaStream_t st);
 
-// Best-of-n_init lloyd_once (clustering.hpp:200-236) on points (2n interleaved,
-// device). Draws are consumed from d_raw starting at *cursor (updated).
-void lloyd_best_device(const double* d_pts, int64_t n, uint64_t k, uint64_t max_iters,
-                       uint64_t n_init, const uint64_t* d_raw, uint64_t raw_count,
-                       uint64_t* cursor, const BBox& bb, KMeansOut& out, cudaStream_t st);
+// Best-of-n_init lloyd_once (clustering.hpp:200-236) on the points
+// d_pts[d_idx[i]] (or d_pts[i] when d_idx is null), i < n; 2-interleaved
+// device doubles. Draws are consumed from d_raw starting at *cursor (updated).
+// out.labels are in the original point order.
+void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, uint64_t k,
+                       uint64_t max_iters, uint64_t n_init, const uint64_t* d_raw,
+                       uint64_t raw_count, uint64_t* cursor, const BBox& bb, KMeansOut& out,
+                       cudaStream_t st);
 
 // Per-point nearest center (clustering.hpp:146-163) with exact tie rule, plus
 // group statistics for digitize (digitization.hpp:217-231).

@@ -7,14 +7,18 @@
 //    idx[i] = value at position j_i just before swap i, recovered from the
 //    "last earlier swap that touched this position" chains after one stable
 //    radix sort of (j_i, i).
-//  * d2_seed (:92-131): per round one fused pass (D^2 min-update + block
-//    partial sums) and one single-block pick; the sums are exact 128-bit
-//    fixed point, so the weighted pick is deterministic. The engine draw
-//    cursor lives on device, so the k rounds run without host round trips.
-//  * lloyd_once (:200-220): assignment with the exact tie rule, cluster sums
-//    maintained incrementally as exact fixed-point integers (only points
-//    whose label changed contribute), empty-cluster repair exactly as
-//    update_means (:181-197).
+//  * the points are put in Morton order once; warp tiles of 128 consecutive
+//    points then cover small boxes.
+//  * d2_seed (:92-131): per round one tile pass (D^2 min-update, skipping
+//    every tile whose box cannot beat its current max D^2; exact deltas of
+//    per-original-block 128-bit fixed-point partial sums) and one
+//    single-block pick in ORIGINAL sample order. The engine draw cursor lives
+//    on device, so the k rounds run without host round trips.
+//  * lloyd_once (:200-220): per tile, the exact candidate centers of the
+//    tile's box, then nearest_center over them with the exact tie rule;
+//    cluster sums maintained incrementally as exact fixed-point integers
+//    (only points whose label changed contribute), empty-cluster repair
+//    exactly as update_means (:181-197).
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -232,69 +236,155 @@ uint64_t sample_indices_device(uint64_t n, uint64_t S, const uint64_t* d_raw, ui
 }
 
 // ---------------------------------------------------------------------------
-// D^2 seeding
+// Spatial order of the k-means points.
+//
+// The points are visited in Morton (Z) order so that every warp tile of
+// TILE consecutive points covers a small box. This is a pure re-ordering:
+// labels, sums (exact integers) and the convergence test are order
+// independent, the D^2 pick keeps the ORIGINAL sample order through exact
+// per-original-block partial sums, and every tie-break that depends on an
+// index (lowest index on equal distance) uses the original index.
 
 namespace {
 
-constexpr int D2_TB = 256;
-constexpr int D2_ITEMS = 8;
-constexpr int D2_R = D2_TB * D2_ITEMS;  // elements per partial-sum block
+constexpr int TILE = 128;  // points per warp tile
+constexpr int D2_R = 2048; // original-order elements per partial-sum block
+
+__device__ __forceinline__ uint32_t spread16(uint32_t v) {
+    v &= 0xFFFFu;
+    v = (v | (v << 8)) & 0x00FF00FFu;
+    v = (v | (v << 4)) & 0x0F0F0F0Fu;
+    v = (v | (v << 2)) & 0x33333333u;
+    v = (v | (v << 1)) & 0x55555555u;
+    return v;
+}
+
+__device__ __forceinline__ double2 load_pt(const double2* __restrict__ pts,
+                                           const uint64_t* __restrict__ idx, int64_t i) {
+    return idx ? pts[idx[i]] : pts[i];
+}
+
+__global__ void k_morton(const double2* __restrict__ pts, const uint64_t* __restrict__ idx,
+                         int64_t n, double x0, double sx, double y0, double sy,
+                         uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double2 p = load_pt(pts, idx, i);
+        const uint32_t qx = (uint32_t)fmin(fmax((p.x - x0) * sx, 0.0), 65535.0);
+        const uint32_t qy = (uint32_t)fmin(fmax((p.y - y0) * sy, 0.0), 65535.0);
+        keys[i] = spread16(qx) | (spread16(qy) << 1);
+        vals[i] = (uint32_t)i;
+    }
+}
+
+__global__ void k_sorted_gather(const double2* __restrict__ pts, const uint64_t* __restrict__ idx,
+                                const uint32_t* __restrict__ orig, int64_t n,
+                                double2* __restrict__ spts, uint32_t* __restrict__ pos) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t o = orig[r];
+        spts[r] = load_pt(pts, idx, o);
+        pos[o] = (uint32_t)r;
+    }
+}
+
+// box = (x0, x1, y0, y1)
+__global__ void k_tile_boxes(const double2* __restrict__ spts, int64_t n,
+                             double4* __restrict__ tbox) {
+    const int lane = threadIdx.x & 31;
+    const int64_t ntiles = (n + TILE - 1) / TILE;
+    for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < ntiles;
+         t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        double x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY;
+        for (int i = 0; i < TILE / 32; ++i) {
+            const int64_t r = t * TILE + i * 32 + lane;
+            if (r < n) {
+                const double2 p = spts[r];
+                x0 = fmin(x0, p.x);
+                x1 = fmax(x1, p.x);
+                y0 = fmin(y0, p.y);
+                y1 = fmax(y1, p.y);
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            x0 = fmin(x0, __shfl_xor_sync(0xffffffffu, x0, o));
+            x1 = fmax(x1, __shfl_xor_sync(0xffffffffu, x1, o));
+            y0 = fmin(y0, __shfl_xor_sync(0xffffffffu, y0, o));
+            y1 = fmax(y1, __shfl_xor_sync(0xffffffffu, y1, o));
+        }
+        if (lane == 0) tbox[t] = make_double4(x0, x1, y0, y1);
+    }
+}
+
+// Squared distance bounds between center c and box b. Each carries at most
+// ~4 ulps of relative rounding error, which the 1e-12 margins below absorb:
+// a center is dropped only when for EVERY point of the box its rounded
+// reference distance (dx*dx+dy*dy, no FMA) is strictly larger than that of
+// the center realising the min-max bound -- so it can be neither the
+// argmin nor a lower-index tie.
+__device__ __forceinline__ void box_d2(double cx, double cy, const double4& b, double& dmin2,
+                                       double& dmax2) {
+    const double ex = fmax(fmax(b.x - cx, cx - b.y), 0.0);
+    const double ey = fmax(fmax(b.z - cy, cy - b.w), 0.0);
+    dmin2 = ex * ex + ey * ey;
+    const double fx = fmax(fabs(b.x - cx), fabs(b.y - cx));
+    const double fy = fmax(fabs(b.z - cy), fabs(b.w - cy));
+    dmax2 = fx * fx + fy * fy;
+}
+
+constexpr double kKeepMargin = 1e-12;
+
+// block-wide exclusive scan of int128 values (blockDim.x == 1024)
+__device__ __forceinline__ i128 block_exscan_i128(i128 v, i128* total,
+                                                  unsigned long long* s_lo,
+                                                  unsigned long long* s_hi) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    unsigned long long lo = (unsigned long long)(u128)v, hi = (unsigned long long)((u128)v >> 64);
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long plo = __shfl_up_sync(0xffffffffu, lo, o);
+        const unsigned long long phi = __shfl_up_sync(0xffffffffu, hi, o);
+        if (lane >= o) {
+            const unsigned long long nlo = lo + plo;
+            hi = hi + phi + (nlo < lo ? 1ULL : 0ULL);
+            lo = nlo;
+        }
+    }
+    if (lane == 31) {
+        s_lo[w] = lo;
+        s_hi[w] = hi;
+    }
+    __syncthreads();
+    if (w == 0) {
+        unsigned long long a = s_lo[lane], b = s_hi[lane];
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long plo = __shfl_up_sync(0xffffffffu, a, o);
+            const unsigned long long phi = __shfl_up_sync(0xffffffffu, b, o);
+            if (lane >= o) {
+                const unsigned long long nlo = a + plo;
+                b = b + phi + (nlo < a ? 1ULL : 0ULL);
+                a = nlo;
+            }
+        }
+        s_lo[lane] = a;  // inclusive warp prefix
+        s_hi[lane] = b;
+    }
+    __syncthreads();
+    const i128 incl = (i128)(((u128)hi << 64) | (u128)lo);
+    const i128 wpre = w > 0 ? (i128)(((u128)s_hi[w - 1] << 64) | (u128)s_lo[w - 1]) : (i128)0;
+    *total = (i128)(((u128)s_hi[31] << 64) | (u128)s_lo[31]);
+    __syncthreads();
+    return wpre + incl - v;
+}
+
+// ---------------------------------------------------------------------------
+// D^2 seeding (d2_seed clustering.hpp:92-131)
 
 struct SeedState {
     uint64_t cursor;    // next engine draw
-    int64_t last;       // index of the latest center in the sample
-    int32_t degenerate; // total == 0 round happened
+    int64_t last;       // ORIGINAL index of the latest center
+    int32_t degenerate; // a total == 0 round happened
     int32_t pad;
 };
-
-// d2[i] = min(d2[i], dist2(p_i, c_last)) (or init when `init`), plus the
-// block's exact fixed-point partial sum of d2.
-__global__ void __launch_bounds__(D2_TB) k_d2_update(const double2* __restrict__ pts, int64_t n,
-                                                    double* __restrict__ d2,
-                                                    const SeedState* __restrict__ ss, int init,
-                                                    int E, unsigned long long* __restrict__ part) {
-    const int64_t c = ss->last;
-    const double2 cc = pts[c];
-    const int64_t b0 = (int64_t)blockIdx.x * D2_R;
-    i128 s = 0;
-#pragma unroll
-    for (int it = 0; it < D2_ITEMS; ++it) {
-        const int64_t i = b0 + it * D2_TB + threadIdx.x;
-        if (i < n) {
-            const double2 p = pts[i];
-            const double dd = dist2(p.x, p.y, cc.x, cc.y);
-            double v;
-            if (init) {
-                v = dd;
-            } else {
-                v = d2[i];
-                if (dd < v) v = dd;  // std::min(a, b) == (b < a) ? b : a
-            }
-            d2[i] = v;
-            s += fx_from_double(v, E);
-        }
-    }
-    __shared__ unsigned long long lo[D2_TB / 32], hi[D2_TB / 32];
-    s = fx_warp_sum(s);
-    if ((threadIdx.x & 31) == 0) {
-        lo[threadIdx.x >> 5] = (unsigned long long)(u128)s;
-        hi[threadIdx.x >> 5] = (unsigned long long)((u128)s >> 64);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        i128 t = 0;
-        for (int w = 0; w < D2_TB / 32; ++w) t += (i128)(((u128)hi[w] << 64) | (u128)lo[w]);
-        part[2 * blockIdx.x] = (unsigned long long)(u128)t;
-        part[2 * blockIdx.x + 1] = (unsigned long long)((u128)t >> 64);
-    }
-}
-
-// floor(u * 2^E) for u >= 0 as an integer (u * 2^E < 2^126)
-__device__ __forceinline__ i128 fx_floor(double u, int E) {
-    return fx_from_double(u, E);  // magnitude truncation == floor for u >= 0
-}
-
-constexpr int PICK_TB = 1024;
 
 // First center: uniform_int(0, n-1) (clustering.hpp:103-104).
 __global__ void k_pick_first(const uint64_t* __restrict__ raw, uint64_t n, SeedState* ss,
@@ -306,42 +396,80 @@ __global__ void k_pick_first(const uint64_t* __restrict__ raw, uint64_t n, SeedS
     chosen[0] = (int64_t)r;
 }
 
+// One warp per tile: d2 = min(d2, dist2(p, c_last)) (init: d2 = dist2), the
+// tile's max d2, and exact deltas of the per-original-block partial sums.
+// A tile is skipped when no point in its box can come closer to the new
+// center than the tile's current max d2.
+__global__ void __launch_bounds__(256) k_d2_tiles(
+    const double2* __restrict__ spts, const uint32_t* __restrict__ orig,
+    const uint32_t* __restrict__ pos, int64_t n, const double4* __restrict__ tbox,
+    double* __restrict__ tmax, double* __restrict__ d2s, const SeedState* __restrict__ ss,
+    int init, int E, unsigned long long* __restrict__ part) {
+    const int lane = threadIdx.x & 31;
+    const int64_t ntiles = (n + TILE - 1) / TILE;
+    const double2 c = spts[pos[ss->last]];
+    for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < ntiles;
+         t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        if (!init) {
+            double dmin2, dmax2;
+            box_d2(c.x, c.y, tbox[t], dmin2, dmax2);
+            if (dmin2 * (1.0 - kKeepMargin) > tmax[t]) continue;  // warp-uniform
+        }
+        double mx = 0.0;
+        for (int i = 0; i < TILE / 32; ++i) {
+            const int64_t r = t * TILE + i * 32 + lane;
+            if (r >= n) break;
+            const double2 p = spts[r];
+            const double dd = dist2(p.x, p.y, c.x, c.y);
+            double v;
+            if (init) {
+                v = dd;
+                d2s[r] = v;
+                fx_atomic_add(part + 2 * (orig[r] / D2_R), fx_from_double(v, E));
+            } else {
+                v = d2s[r];
+                if (dd < v) {  // std::min(d2, dd)
+                    fx_atomic_add(part + 2 * (orig[r] / D2_R),
+                                  fx_from_double(dd, E) - fx_from_double(v, E));
+                    v = dd;
+                    d2s[r] = v;
+                }
+            }
+            mx = fmax(mx, v);
+        }
+        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane == 0) tmax[t] = mx;
+    }
+}
+
+constexpr int PICK_TB = 1024;
+
 // One D^2 round pick: total > 0 ? weighted_index (:59-71) : first unchosen.
-// Single block: find the partial-sum block holding the crossing, then the
-// element; all prefix arithmetic is exact 128-bit integer.
+// Finds the original-order partial-sum block holding the crossing, then the
+// element (d2 gathered through pos[]); all prefix arithmetic is exact.
 __global__ void __launch_bounds__(PICK_TB) k_pick(const uint64_t* __restrict__ raw,
-                                                  const double* __restrict__ d2, int64_t n,
+                                                  const double* __restrict__ d2s,
+                                                  const uint32_t* __restrict__ pos, int64_t n,
                                                   int nblocks,
                                                   const unsigned long long* __restrict__ part,
                                                   int E, SeedState* ss,
                                                   int64_t* __restrict__ chosen, int c) {
-    __shared__ unsigned long long s_lo[PICK_TB], s_hi[PICK_TB];
-    __shared__ unsigned long long s_total[2], s_before[2];
+    __shared__ unsigned long long s_lo[32], s_hi[32];
     __shared__ int s_found_block;
     __shared__ unsigned long long s_found_elem;
+    __shared__ unsigned long long s_before[2];
     const int t = threadIdx.x;
     const int per = (nblocks + PICK_TB - 1) / PICK_TB;
     const int b_lo = min(nblocks, t * per), b_hi = min(nblocks, b_lo + per);
     i128 local = 0;
     for (int b = b_lo; b < b_hi; ++b) local += fx_load(part + 2 * b);
-    s_lo[t] = (unsigned long long)(u128)local;
-    s_hi[t] = (unsigned long long)((u128)local >> 64);
-    __syncthreads();
-    if (t == 0) {  // exclusive scan of the per-thread totals (deterministic)
-        i128 run = 0;
-        for (int i = 0; i < PICK_TB; ++i) {
-            const i128 v = (i128)(((u128)s_hi[i] << 64) | (u128)s_lo[i]);
-            s_lo[i] = (unsigned long long)(u128)run;
-            s_hi[i] = (unsigned long long)((u128)run >> 64);
-            run += v;
-        }
-        s_total[0] = (unsigned long long)(u128)run;
-        s_total[1] = (unsigned long long)((u128)run >> 64);
+    if (t == 0) {
         s_found_block = 0x7FFFFFFF;
         s_found_elem = ~0ULL;
     }
-    __syncthreads();
-    const double total = fx_to_double(fx_load(s_total), E);
+    i128 total_fx;
+    const i128 excl = block_exscan_i128(local, &total_fx, s_lo, s_hi);
+    const double total = fx_to_double(total_fx, E);
     if (!(total > 0.0)) {
         // every remaining point duplicates a center: first free slot (:120-124)
         if (t == 0) {
@@ -362,12 +490,11 @@ __global__ void __launch_bounds__(PICK_TB) k_pick(const uint64_t* __restrict__ r
     double canon = __ull2double_rn(x) * 0x1p-64;  // generate_canonical<double,53>
     if (canon >= 1.0) canon = 0x1.fffffffffffffp-1;  // nextafter(1, 0)
     const double u = canon * total + 0.0;             // uniform_real(0, total)
-    const i128 U = fx_floor(u, E);
-    // first partial-sum block whose inclusive prefix exceeds U
+    const i128 U = fx_from_double(u, E);               // floor(u * 2^E), u >= 0
     int my_block = 0x7FFFFFFF;
     i128 my_before = 0;
     {
-        i128 run = (i128)(((u128)s_hi[t] << 64) | (u128)s_lo[t]);
+        i128 run = excl;
         for (int b = b_lo; b < b_hi; ++b) {
             const i128 v = fx_load(part + 2 * b);
             if (U < run + v) {
@@ -386,7 +513,7 @@ __global__ void __launch_bounds__(PICK_TB) k_pick(const uint64_t* __restrict__ r
         if (t == 0) {
             int64_t next = n - 1;
             for (int64_t i = n - 1; i >= 0; --i)
-                if (d2[i] > 0.0) {
+                if (d2s[pos[i]] > 0.0) {
                     next = i;
                     break;
                 }
@@ -401,27 +528,16 @@ __global__ void __launch_bounds__(PICK_TB) k_pick(const uint64_t* __restrict__ r
         s_before[1] = (unsigned long long)((u128)my_before >> 64);
     }
     __syncthreads();
-    // within block fb: 1024 threads x 2 elements, exclusive scan of pairs
+    const i128 before_block = fx_load(s_before);
+    // within block fb: 1024 threads x 2 elements (original order)
     const int64_t e0 = (int64_t)fb * D2_R + 2 * t;
     i128 a = 0, bsum = 0;
-    if (e0 < n) a = fx_from_double(d2[e0], E);
-    if (e0 + 1 < n) bsum = fx_from_double(d2[e0 + 1], E);
-    const i128 pair = a + bsum;
-    s_lo[t] = (unsigned long long)(u128)pair;
-    s_hi[t] = (unsigned long long)((u128)pair >> 64);
-    __syncthreads();
-    if (t == 0) {
-        i128 run = fx_load(s_before);
-        for (int i = 0; i < PICK_TB; ++i) {
-            const i128 v = (i128)(((u128)s_hi[i] << 64) | (u128)s_lo[i]);
-            s_lo[i] = (unsigned long long)(u128)run;
-            s_hi[i] = (unsigned long long)((u128)run >> 64);
-            run += v;
-        }
-    }
-    __syncthreads();
+    if (e0 < n) a = fx_from_double(d2s[pos[e0]], E);
+    if (e0 + 1 < n) bsum = fx_from_double(d2s[pos[e0 + 1]], E);
+    i128 dummy;
+    const i128 ex2 = block_exscan_i128(a + bsum, &dummy, s_lo, s_hi);
     {
-        const i128 before = (i128)(((u128)s_hi[t] << 64) | (u128)s_lo[t]);
+        const i128 before = before_block + ex2;
         unsigned long long hit = ~0ULL;
         if (e0 < n && U < before + a) hit = (unsigned long long)e0;
         else if (e0 + 1 < n && U < before + a + bsum) hit = (unsigned long long)(e0 + 1);
@@ -436,10 +552,11 @@ __global__ void __launch_bounds__(PICK_TB) k_pick(const uint64_t* __restrict__ r
     }
 }
 
-__global__ void k_copy_center(const double2* __restrict__ pts, const int64_t* __restrict__ chosen,
-                              int k, double* __restrict__ centers) {
+__global__ void k_copy_center(const double2* __restrict__ spts, const uint32_t* __restrict__ pos,
+                              const int64_t* __restrict__ chosen, int k,
+                              double* __restrict__ centers) {
     for (int c = threadIdx.x; c < k; c += blockDim.x) {
-        const double2 p = pts[chosen[c]];
+        const double2 p = spts[pos[chosen[c]]];
         centers[2 * c] = p.x;
         centers[2 * c + 1] = p.y;
     }
@@ -454,18 +571,26 @@ struct ClusterAcc {
     unsigned long long* cnt;  // k (two's complement deltas)
 };
 
-// labels := nearest(centers); cluster sums updated by the delta of every
-// label change (full accumulation when `full`). Also counts changes.
-__global__ void k_lloyd_assign(const double2* __restrict__ pts, int64_t n,
-                               const double* __restrict__ centers, int k,
-                               uint32_t* __restrict__ labels, int full, int Ex, int Ey,
-                               ClusterAcc acc, unsigned long long* __restrict__ changed) {
+constexpr int LL_TB = 256;
+constexpr int LL_WARPS = LL_TB / 32;
+
+// One warp per tile of TILE Morton-ordered points: exact candidate set of the
+// tile's box (every center that can be the reference argmin for some point
+// in it, in index order), then nearest_center over the candidates only
+// (clustering.hpp:146-157: strict <, lowest index). Cluster sums follow the
+// label changes as exact integer deltas (full accumulation when `full`).
+__global__ void __launch_bounds__(LL_TB) k_lloyd_tiles(
+    const double2* __restrict__ spts, int64_t n, const double* __restrict__ centers, int k,
+    uint32_t* __restrict__ labs, int full, int Ex, int Ey, ClusterAcc acc,
+    unsigned long long* __restrict__ changed, const int* __restrict__ skip_flag) {
     extern __shared__ unsigned char smem[];
+    if (skip_flag && *skip_flag) return;  // empty clusters pending: host repairs first
     double* cx = reinterpret_cast<double*>(smem);
     double* cy = cx + k;
     unsigned long long* s_sx = reinterpret_cast<unsigned long long*>(cy + k);
     unsigned long long* s_sy = s_sx + 2 * k;
     unsigned long long* s_cnt = s_sy + 2 * k;
+    uint16_t* s_cand = reinterpret_cast<uint16_t*>(s_cnt + k);
     __shared__ unsigned long long s_changed;
     for (int c = threadIdx.x; c < k; c += blockDim.x) {
         cx[c] = centers[2 * c];
@@ -476,41 +601,93 @@ __global__ void k_lloyd_assign(const double2* __restrict__ pts, int64_t n,
     }
     if (threadIdx.x == 0) s_changed = 0;
     __syncthreads();
+    const int lane = threadIdx.x & 31;
+    uint16_t* cand = s_cand + (threadIdx.x >> 5) * k;
+    const unsigned lt = (1u << lane) - 1u;
     unsigned long long my_changed = 0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const double2 p = pts[i];
-        uint32_t best = 0;
-        double bd = __longlong_as_double(0x7FF0000000000000LL);
-        for (int c = 0; c < k; ++c) {
-            const double d = dist2(p.x, p.y, cx[c], cy[c]);
-            if (d < bd) {
-                bd = d;
-                best = (uint32_t)c;
+    const int64_t ntiles = (n + TILE - 1) / TILE;
+    for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < ntiles;
+         t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        double2 p[TILE / 32];
+        double x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < TILE / 32; ++i) {
+            const int64_t r = t * TILE + i * 32 + lane;
+            if (r < n) {
+                p[i] = spts[r];
+                x0 = fmin(x0, p[i].x);
+                x1 = fmax(x1, p[i].x);
+                y0 = fmin(y0, p[i].y);
+                y1 = fmax(y1, p[i].y);
             }
         }
-        if (full) {
-            labels[i] = best;
-            fx_atomic_add(s_sx + 2 * best, fx_from_double(p.x, Ex));
-            fx_atomic_add(s_sy + 2 * best, fx_from_double(p.y, Ey));
-            atomicAdd(s_cnt + best, 1ULL);
-        } else {
-            const uint32_t old = labels[i];
-            if (old != best) {
-                labels[i] = best;
-                ++my_changed;
-                const i128 fx = fx_from_double(p.x, Ex), fy = fx_from_double(p.y, Ey);
-                fx_atomic_add(s_sx + 2 * best, fx);
-                fx_atomic_add(s_sy + 2 * best, fy);
+        for (int o = 16; o > 0; o >>= 1) {
+            x0 = fmin(x0, __shfl_xor_sync(0xffffffffu, x0, o));
+            x1 = fmax(x1, __shfl_xor_sync(0xffffffffu, x1, o));
+            y0 = fmin(y0, __shfl_xor_sync(0xffffffffu, y0, o));
+            y1 = fmax(y1, __shfl_xor_sync(0xffffffffu, y1, o));
+        }
+        const double4 box = make_double4(x0, x1, y0, y1);
+        double M = INFINITY;
+        for (int c = lane; c < k; c += 32) {
+            double dmn, dmx;
+            box_d2(cx[c], cy[c], box, dmn, dmx);
+            M = fmin(M, dmx);
+        }
+        for (int o = 16; o > 0; o >>= 1) M = fmin(M, __shfl_xor_sync(0xffffffffu, M, o));
+        const double thr = M * (1.0 + kKeepMargin) + 1e-300;
+        int nc = 0;
+        for (int c0 = 0; c0 < k; c0 += 32) {
+            const int c = c0 + lane;
+            bool keep = false;
+            if (c < k) {
+                double dmn, dmx;
+                box_d2(cx[c], cy[c], box, dmn, dmx);
+                keep = dmn <= thr;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            if (keep) cand[nc + __popc(m & lt)] = (uint16_t)c;
+            nc += __popc(m);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < TILE / 32; ++i) {
+            const int64_t r = t * TILE + i * 32 + lane;
+            if (r >= n) break;
+            uint32_t best = cand[0];
+            double bd = dist2(p[i].x, p[i].y, cx[best], cy[best]);
+            for (int j = 1; j < nc; ++j) {
+                const int c = cand[j];
+                const double d = dist2(p[i].x, p[i].y, cx[c], cy[c]);
+                if (d < bd) {
+                    bd = d;
+                    best = (uint32_t)c;
+                }
+            }
+            if (full) {
+                labs[r] = best;
+                fx_atomic_add(s_sx + 2 * best, fx_from_double(p[i].x, Ex));
+                fx_atomic_add(s_sy + 2 * best, fx_from_double(p[i].y, Ey));
                 atomicAdd(s_cnt + best, 1ULL);
-                fx_atomic_add(s_sx + 2 * old, -fx);
-                fx_atomic_add(s_sy + 2 * old, -fy);
-                atomicAdd(s_cnt + old, ~0ULL);
+            } else {
+                const uint32_t old = labs[r];
+                if (old != best) {
+                    labs[r] = best;
+                    ++my_changed;
+                    const i128 fx = fx_from_double(p[i].x, Ex), fy = fx_from_double(p[i].y, Ey);
+                    fx_atomic_add(s_sx + 2 * best, fx);
+                    fx_atomic_add(s_sy + 2 * best, fy);
+                    atomicAdd(s_cnt + best, 1ULL);
+                    fx_atomic_add(s_sx + 2 * old, -fx);
+                    fx_atomic_add(s_sy + 2 * old, -fy);
+                    atomicAdd(s_cnt + old, ~0ULL);
+                }
             }
         }
+        __syncwarp();
     }
     for (int o = 16; o > 0; o >>= 1) my_changed += __shfl_down_sync(0xffffffffu, my_changed, o);
-    if ((threadIdx.x & 31) == 0 && my_changed) atomicAdd(&s_changed, my_changed);
+    if (lane == 0 && my_changed) atomicAdd(&s_changed, my_changed);
     __syncthreads();
     for (int c = threadIdx.x; c < k; c += blockDim.x) {
         const i128 vx = fx_load(s_sx + 2 * c), vy = fx_load(s_sy + 2 * c);
@@ -542,38 +719,44 @@ __global__ void k_means(ClusterAcc acc, int k, int Ex, int Ey, double* __restric
 }
 
 // farthest point among clusters with count > 1 (update_means :183-192):
-// max distance, lowest index on ties. Per-block candidates.
-__global__ void k_far_block(const double2* __restrict__ pts, int64_t n,
-                            const uint32_t* __restrict__ labels,
+// max distance, lowest ORIGINAL index on ties. Per-block candidates
+// (distance bits, original index, sorted position).
+__global__ void k_far_block(const double2* __restrict__ spts, const uint32_t* __restrict__ orig,
+                            int64_t n, const uint32_t* __restrict__ labs,
                             const double* __restrict__ centers,
                             const unsigned long long* __restrict__ cnt,
                             unsigned long long* __restrict__ out) {
     double bd = -1.0;
-    int64_t bi = INT64_MAX;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t l = labels[i];
+    int64_t bi = INT64_MAX, br = -1;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t l = labs[r];
         if ((long long)cnt[l] <= 1) continue;
-        const double2 p = pts[i];
+        const double2 p = spts[r];
         const double d = dist2(p.x, p.y, centers[2 * l], centers[2 * l + 1]);
-        if (d > bd || (d == bd && i < bi)) {
+        const int64_t o = orig[r];
+        if (d > bd || (d == bd && o < bi)) {
             bd = d;
-            bi = i;
+            bi = o;
+            br = r;
         }
     }
-    for (int o = 16; o > 0; o >>= 1) {
-        const double od = __shfl_down_sync(0xffffffffu, bd, o);
-        const int64_t oi = __shfl_down_sync(0xffffffffu, bi, o);
+    for (int off = 16; off > 0; off >>= 1) {
+        const double od = __shfl_down_sync(0xffffffffu, bd, off);
+        const int64_t oi = __shfl_down_sync(0xffffffffu, bi, off);
+        const int64_t orr = __shfl_down_sync(0xffffffffu, br, off);
         if (od > bd || (od == bd && oi < bi)) {
             bd = od;
             bi = oi;
+            br = orr;
         }
     }
     __shared__ double sd[32];
-    __shared__ int64_t si[32];
+    __shared__ int64_t si[32], sr[32];
     if ((threadIdx.x & 31) == 0) {
         sd[threadIdx.x >> 5] = bd;
         si[threadIdx.x >> 5] = bi;
+        sr[threadIdx.x >> 5] = br;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -581,40 +764,40 @@ __global__ void k_far_block(const double2* __restrict__ pts, int64_t n,
             if (sd[w] > bd || (sd[w] == bd && si[w] < bi)) {
                 bd = sd[w];
                 bi = si[w];
+                br = sr[w];
             }
-        out[2 * blockIdx.x] = (unsigned long long)__double_as_longlong(bd);
-        out[2 * blockIdx.x + 1] = (unsigned long long)bi;
+        out[3 * blockIdx.x] = (unsigned long long)__double_as_longlong(bd);
+        out[3 * blockIdx.x + 1] = (unsigned long long)bi;
+        out[3 * blockIdx.x + 2] = (unsigned long long)br;
     }
 }
 
 // re-seed empty cluster c at the farthest point (update_means :193-196)
-__global__ void k_repair(const double2* __restrict__ pts, uint32_t* __restrict__ labels,
-                         double* __restrict__ centers, ClusterAcc acc, int Ex, int Ey,
-                         const unsigned long long* __restrict__ blk, int nblk, int c) {
+__global__ void k_repair(const double2* __restrict__ spts, const uint32_t* __restrict__ pos,
+                         uint32_t* __restrict__ labs, double* __restrict__ centers, ClusterAcc acc,
+                         int Ex, int Ey, const unsigned long long* __restrict__ blk, int nblk,
+                         int c) {
     double bd = -1.0;
-    int64_t bi = INT64_MAX;
+    int64_t bi = INT64_MAX, br = -1;
     for (int b = 0; b < nblk; ++b) {
-        const double d = __longlong_as_double((long long)blk[2 * b]);
-        const int64_t i = (int64_t)blk[2 * b + 1];
+        const double d = __longlong_as_double((long long)blk[3 * b]);
+        const int64_t i = (int64_t)blk[3 * b + 1];
         if (d > bd || (d == bd && i < bi)) {
             bd = d;
             bi = i;
+            br = (int64_t)blk[3 * b + 2];
         }
     }
-    const int64_t far_i = (bi == INT64_MAX) ? 0 : bi;  // no candidate: far_i stays 0
-    const uint32_t donor = labels[far_i];
-    const double2 p = pts[far_i];
+    if (br < 0) br = pos[0];  // no candidate: far_i stays 0 (original index)
+    const uint32_t donor = labs[br];
+    const double2 p = spts[br];
     const i128 fx = fx_from_double(p.x, Ex), fy = fx_from_double(p.y, Ey);
     fx_atomic_add(acc.sx + 2 * donor, -fx);
     fx_atomic_add(acc.sy + 2 * donor, -fy);
     acc.cnt[donor] -= 1;
-    labels[far_i] = (uint32_t)c;
-    // counts[c] = 1 and sums[c] = p (the cluster was empty: its sums are 0
-    // up to exactness of the integer bookkeeping)
-    acc.sx[2 * c] = 0;
-    acc.sx[2 * c + 1] = 0;
-    acc.sy[2 * c] = 0;
-    acc.sy[2 * c + 1] = 0;
+    labs[br] = (uint32_t)c;
+    acc.sx[2 * c] = acc.sx[2 * c + 1] = 0;
+    acc.sy[2 * c] = acc.sy[2 * c + 1] = 0;
     fx_atomic_add(acc.sx + 2 * c, fx);
     fx_atomic_add(acc.sy + 2 * c, fy);
     acc.cnt[c] = 1;
@@ -622,111 +805,161 @@ __global__ void k_repair(const double2* __restrict__ pts, uint32_t* __restrict__
     centers[2 * c + 1] = p.y;
 }
 
-__global__ void k_sse(const double2* __restrict__ pts, int64_t n,
-                      const uint32_t* __restrict__ labels, const double* __restrict__ centers,
+__global__ void k_sse(const double2* __restrict__ spts, int64_t n,
+                      const uint32_t* __restrict__ labs, const double* __restrict__ centers,
                       int E, unsigned long long* __restrict__ acc) {
     i128 s = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t l = labels[i];
-        const double2 p = pts[i];
+        const uint32_t l = labs[i];
+        const double2 p = spts[i];
         s += fx_from_double(dist2(p.x, p.y, centers[2 * l], centers[2 * l + 1]), E);
     }
     s = fx_warp_sum(s);
     if ((threadIdx.x & 31) == 0) fx_atomic_add(acc, s);
 }
 
-}  // namespace
-
-namespace {
+__global__ void k_unsort_labels(const uint32_t* __restrict__ labs,
+                                const uint32_t* __restrict__ orig, int64_t n,
+                                uint32_t* __restrict__ out) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x)
+        out[orig[r]] = labs[r];
+}
 
 struct LloydCtx {
-    const double* pts;
+    const double2* spts;
+    const uint32_t* orig;
+    const uint32_t* pos;
     int64_t n;
     int k;
     int Ex, Ey;
-    BBox bb;
     cudaStream_t st;
     DArr<double> centers;
-    DArr<uint32_t> labels;
+    DArr<uint32_t> labs;           // sorted order
     DArr<unsigned long long> acc;  // 5k: sx(2k) sy(2k) cnt(k)
-    DArr<unsigned long long> changed;
-    DArr<int> empties;  // k + 1 (last = count)
+    DArr<unsigned long long> flags;  // [0] changed
+    DArr<int> empties;             // k + 1 (last = count)
     DArr<unsigned long long> far_blk;
     ClusterAcc cacc() { return ClusterAcc{acc.p, acc.p + 2 * k, acc.p + 4 * k}; }
-    size_t smem() const { return sizeof(double) * 2 * k + sizeof(unsigned long long) * 5 * k; }
-    int grid_assign() const {
-        return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)kSMs * 2));
+    size_t smem() const {
+        return sizeof(double) * 2 * k + sizeof(unsigned long long) * 5 * k +
+               sizeof(uint16_t) * LL_WARPS * k;
+    }
+    int grid() const {
+        const int64_t ntiles = (n + TILE - 1) / TILE;
+        return (int)std::max<int64_t>(
+            1, std::min<int64_t>((ntiles + LL_WARPS - 1) / LL_WARPS, (int64_t)kSMs * 4));
     }
 };
 
-void lloyd_assign(LloydCtx& L, bool full) {
-    JB_CUDA(cudaMemsetAsync(L.changed.p, 0, 8, L.st));
+void lloyd_assign(LloydCtx& L, bool full, bool gate_on_empties) {
+    JB_CUDA(cudaMemsetAsync(L.flags.p, 0, 8, L.st));
     JB_PROF("lloyd_assign", L.st);
-    k_lloyd_assign<<<L.grid_assign(), 256, L.smem(), L.st>>>(
-        reinterpret_cast<const double2*>(L.pts), L.n, L.centers.p, L.k, L.labels.p, full ? 1 : 0,
-        L.Ex, L.Ey, L.cacc(), L.changed.p);
+    k_lloyd_tiles<<<L.grid(), LL_TB, L.smem(), L.st>>>(
+        L.spts, L.n, L.centers.p, L.k, L.labs.p, full ? 1 : 0, L.Ex, L.Ey, L.cacc(), L.flags.p,
+        gate_on_empties ? L.empties.p + L.k : nullptr);
     JB_LAUNCH_CHECK();
 }
 
-// update_means (:167-198) with the exact repair sequence
-void lloyd_update_means(LloydCtx& L) {
-    {
-        JB_PROF("lloyd_means", L.st);
-        k_means<<<1, 1024, 0, L.st>>>(L.cacc(), L.k, L.Ex, L.Ey, L.centers.p, L.empties.p,
+void lloyd_means(LloydCtx& L) {
+    JB_PROF("lloyd_means", L.st);
+    k_means<<<1, 1024, 0, L.st>>>(L.cacc(), L.k, L.Ex, L.Ey, L.centers.p, L.empties.p,
                                   L.empties.p + L.k);
-    }
     JB_LAUNCH_CHECK();
+}
+
+// empty-cluster re-seeding (update_means :181-197), in cluster order
+void lloyd_repair(LloydCtx& L, int ne) {
+    std::vector<int> em(ne);
+    JB_CUDA(cudaMemcpyAsync(em.data(), L.empties.p, sizeof(int) * ne, cudaMemcpyDeviceToHost,
+                            L.st));
+    JB_CUDA(cudaStreamSynchronize(L.st));
+    const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>((L.n + 255) / 256, kSMs * 4));
+    if (L.far_blk.n < (size_t)(3 * nblk)) L.far_blk.alloc(3 * nblk, L.st);
+    for (int c : em) {
+        k_far_block<<<nblk, 256, 0, L.st>>>(L.spts, L.orig, L.n, L.labs.p, L.centers.p,
+                                            L.cacc().cnt, L.far_blk.p);
+        JB_LAUNCH_CHECK();
+        k_repair<<<1, 1, 0, L.st>>>(L.spts, L.pos, L.labs.p, L.centers.p, L.cacc(), L.Ex, L.Ey,
+                                    L.far_blk.p, nblk, c);
+        JB_LAUNCH_CHECK();
+    }
+    const int zero = 0;
+    JB_CUDA(cudaMemcpyAsync(L.empties.p + L.k, &zero, sizeof(int), cudaMemcpyHostToDevice, L.st));
+}
+
+// update_means for the final centers (after the loop): means + repairs
+void lloyd_update_means_sync(LloydCtx& L) {
+    lloyd_means(L);
     int ne = 0;
     JB_CUDA(cudaMemcpyAsync(&ne, L.empties.p + L.k, sizeof(int), cudaMemcpyDeviceToHost, L.st));
     JB_CUDA(cudaStreamSynchronize(L.st));
-    if (ne == 0) return;
-    std::vector<int> em(ne);
-    JB_CUDA(cudaMemcpy(em.data(), L.empties.p, sizeof(int) * ne, cudaMemcpyDeviceToHost));
-    const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>((L.n + 255) / 256, kSMs * 4));
-    if (L.far_blk.n < (size_t)(2 * nblk)) L.far_blk.alloc(2 * nblk, L.st);
-    for (int c : em) {
-        k_far_block<<<nblk, 256, 0, L.st>>>(reinterpret_cast<const double2*>(L.pts), L.n,
-                                            L.labels.p, L.centers.p, L.cacc().cnt, L.far_blk.p);
-        JB_LAUNCH_CHECK();
-        k_repair<<<1, 1, 0, L.st>>>(reinterpret_cast<const double2*>(L.pts), L.labels.p,
-                                    L.centers.p, L.cacc(), L.Ex, L.Ey, L.far_blk.p, nblk, c);
-        JB_LAUNCH_CHECK();
-    }
+    if (ne) lloyd_repair(L, ne);
 }
 
 }  // namespace
 
-void lloyd_best_device(const double* d_pts, int64_t n, uint64_t k, uint64_t max_iters,
-                       uint64_t n_init, const uint64_t* d_raw, uint64_t raw_count,
-                       uint64_t* cursor, const BBox& bb, KMeansOut& out, cudaStream_t st) {
+void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, uint64_t k,
+                       uint64_t max_iters, uint64_t n_init, const uint64_t* d_raw,
+                       uint64_t raw_count, uint64_t* cursor, const BBox& bb, KMeansOut& out,
+                       cudaStream_t st) {
     if (k < 1) throw Error(INVALID_INPUT, "d2_seed: k must be >= 1");
     if ((int64_t)k > n) throw Error(INVALID_INPUT, "d2_seed: k exceeds points");
-    if (k > 4096) throw Error(INVALID_INPUT, "k > 4096 is not supported by the Lloyd kernel");
+    if (k > 2048) throw Error(INVALID_INPUT, "k > 2048 is not supported by the Lloyd kernel");
+    if (n >= (1LL << 32)) throw Error(INVALID_INPUT, "k-means on more than 2^32 points");
+    const double2* pts = reinterpret_cast<const double2*>(d_pts);
     const double mx = std::max(std::fabs(bb.xmin), std::fabs(bb.xmax));
     const double my = std::max(std::fabs(bb.ymin), std::fabs(bb.ymax));
     const double wx = bb.xmax - bb.xmin, wy = bb.ymax - bb.ymin;
     const double d2max = (wx * wx + wy * wy) * (1.0 + 1e-9) + 1e-300;
     const int Ed2 = fx_exponent_for(d2max * (double)n * 1.001);
 
+    // ---- Morton order of the points ----
+    DArr<double2> spts(n, st);
+    DArr<uint32_t> orig(n, st), pos(n, st);
+    {
+        DArr<uint32_t> keys(n, st), skeys(n, st), vals(n, st);
+        const double sx = wx > 0 ? 65535.0 / wx : 0.0, sy = wy > 0 ? 65535.0 / wy : 0.0;
+        k_morton<<<grid_cap(n), 256, 0, st>>>(pts, d_idx, n, bb.xmin, sx, bb.ymin, sy, keys.p,
+                                              vals.p);
+        JB_LAUNCH_CHECK();
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.p, skeys.p, vals.p, orig.p, n, 0, 32,
+                                        st);
+        DArr<uint8_t> tmp(tb, st);
+        cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.p, skeys.p, vals.p, orig.p, n, 0, 32, st);
+        JB_LAUNCH_CHECK();
+        k_sorted_gather<<<grid_cap(n), 256, 0, st>>>(pts, d_idx, orig.p, n, spts.p, pos.p);
+        JB_LAUNCH_CHECK();
+    }
+    const int64_t ntiles = (n + TILE - 1) / TILE;
+    DArr<double4> tbox(ntiles, st);
+    DArr<double> tmax(ntiles, st);
+    const int tile_grid = (int)std::max<int64_t>(1, std::min<int64_t>((ntiles + 7) / 8, kSMs * 8));
+    k_tile_boxes<<<tile_grid, 256, 0, st>>>(spts.p, n, tbox.p);
+    JB_LAUNCH_CHECK();
+
     LloydCtx L;
-    L.pts = d_pts;
+    L.spts = spts.p;
+    L.orig = orig.p;
+    L.pos = pos.p;
     L.n = n;
     L.k = (int)k;
     L.Ex = fx_exponent_for(mx * (double)n * 1.001 + 1e-300);
     L.Ey = fx_exponent_for(my * (double)n * 1.001 + 1e-300);
-    L.bb = bb;
     L.st = st;
     L.centers.alloc(2 * k, st);
-    L.labels.alloc(n, st);
+    L.labs.alloc(n, st);
     L.acc.alloc(5 * k, st);
-    L.changed.alloc(1, st);
+    L.flags.alloc(1, st);
     L.empties.alloc(k + 1, st);
-    JB_CUDA(cudaFuncSetAttribute(k_lloyd_assign, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    L.empties.zero();
+    JB_CUDA(cudaFuncSetAttribute(k_lloyd_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)L.smem()));
 
     const int nblocks = (int)((n + D2_R - 1) / D2_R);
-    DArr<double> d2(n, st);
+    DArr<double> d2s(n, st);
     DArr<unsigned long long> part(2 * nblocks, st);
     DArr<SeedState> ss(1, st);
     DArr<int64_t> chosen(k, st);
@@ -736,59 +969,66 @@ void lloyd_best_device(const double* d_pts, int64_t n, uint64_t k, uint64_t max_
         // ---- d2_seed ----
         SeedState h{*cursor, 0, 0, 0};
         ss.upload(&h, 1);
+        part.zero();
         k_pick_first<<<1, 1, 0, st>>>(d_raw, (uint64_t)n, ss.p, chosen.p);
         JB_LAUNCH_CHECK();
         {
             JB_PROF("d2_update", st);
-            k_d2_update<<<nblocks, D2_TB, 0, st>>>(reinterpret_cast<const double2*>(d_pts), n,
-                                                   d2.p, ss.p, 1, Ed2, part.p);
+            k_d2_tiles<<<tile_grid, 256, 0, st>>>(spts.p, orig.p, pos.p, n, tbox.p, tmax.p,
+                                                  d2s.p, ss.p, 1, Ed2, part.p);
         }
         JB_LAUNCH_CHECK();
         for (uint64_t c = 1; c < k; ++c) {
             {
                 JB_PROF("d2_pick", st);
-                k_pick<<<1, PICK_TB, 0, st>>>(d_raw, d2.p, n, nblocks, part.p, Ed2, ss.p, chosen.p,
-                                          (int)c);
+                k_pick<<<1, PICK_TB, 0, st>>>(d_raw, d2s.p, pos.p, n, nblocks, part.p, Ed2, ss.p,
+                                              chosen.p, (int)c);
             }
             JB_LAUNCH_CHECK();
             if (c + 1 < k) {
                 JB_PROF("d2_update", st);
-                k_d2_update<<<nblocks, D2_TB, 0, st>>>(reinterpret_cast<const double2*>(d_pts),
-                                                       n, d2.p, ss.p, 0, Ed2, part.p);
+                k_d2_tiles<<<tile_grid, 256, 0, st>>>(spts.p, orig.p, pos.p, n, tbox.p, tmax.p,
+                                                      d2s.p, ss.p, 0, Ed2, part.p);
                 JB_LAUNCH_CHECK();
             }
         }
-        k_copy_center<<<1, 256, 0, st>>>(reinterpret_cast<const double2*>(d_pts), chosen.p,
-                                         (int)k, L.centers.p);
+        k_copy_center<<<1, 256, 0, st>>>(spts.p, pos.p, chosen.p, (int)k, L.centers.p);
         JB_LAUNCH_CHECK();
         ss.download(&h, 1);
         JB_CUDA(cudaStreamSynchronize(st));
         if (h.cursor > raw_count) throw Error(INTERNAL, "rng stream exhausted");
         *cursor = h.cursor;
 
-        // ---- Lloyd ----
+        // ---- Lloyd (lloyd_once :200-220) ----
         L.acc.zero();
-        lloyd_assign(L, true);
+        lloyd_assign(L, true, false);
         uint64_t it = 0;
         for (; it < max_iters; ++it) {
-            lloyd_update_means(L);
-            lloyd_assign(L, false);
+            lloyd_means(L);                // update_means ...
+            lloyd_assign(L, false, true);  // ... gated: skipped if repairs are pending
+            int ne = 0;
             unsigned long long ch = 0;
-            JB_CUDA(cudaMemcpyAsync(&ch, L.changed.p, 8, cudaMemcpyDeviceToHost, st));
+            JB_CUDA(cudaMemcpyAsync(&ne, L.empties.p + L.k, sizeof(int), cudaMemcpyDeviceToHost,
+                                    st));
+            JB_CUDA(cudaMemcpyAsync(&ch, L.flags.p, 8, cudaMemcpyDeviceToHost, st));
             JB_CUDA(cudaStreamSynchronize(st));
-            if (ch == 0) {
+            if (ne) {
+                lloyd_repair(L, ne);        // ... empty-cluster re-seeding
+                lloyd_assign(L, false, false);
+                JB_CUDA(cudaMemcpyAsync(&ch, L.flags.p, 8, cudaMemcpyDeviceToHost, st));
+                JB_CUDA(cudaStreamSynchronize(st));
+            }
+            if (ch == 0) {  // next_labels == labels
                 ++it;
                 break;
             }
         }
-        lloyd_update_means(L);
+        lloyd_update_means_sync(L);
         double sse = 0.0;
         if (n_init > 1) {
             DArr<unsigned long long> sacc(2, st);
             sacc.zero();
-            k_sse<<<(int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, kSMs * 8)), 256,
-                    0, st>>>(reinterpret_cast<const double2*>(d_pts), n, L.labels.p, L.centers.p,
-                             Ed2, sacc.p);
+            k_sse<<<grid_cap(n), 256, 0, st>>>(spts.p, n, L.labs.p, L.centers.p, Ed2, sacc.p);
             JB_LAUNCH_CHECK();
             auto hs = sacc.to_host(2);
             sse = fx_to_double(fx_load(hs.data()), Ed2);
@@ -798,8 +1038,8 @@ void lloyd_best_device(const double* d_pts, int64_t n, uint64_t k, uint64_t max_
             out.k = k;
             out.centers = L.centers.to_host(2 * k);
             out.labels.alloc(n, st);
-            JB_CUDA(cudaMemcpyAsync(out.labels.p, L.labels.p, sizeof(uint32_t) * n,
-                                    cudaMemcpyDeviceToDevice, st));
+            k_unsort_labels<<<grid_cap(n), 256, 0, st>>>(L.labs.p, orig.p, n, out.labels.p);
+            JB_LAUNCH_CHECK();
             out.iterations = it;
             out.sse = sse;
         }
