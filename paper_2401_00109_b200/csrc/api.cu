@@ -32,23 +32,32 @@ using jb_api::MaxOp;
 
 namespace jb {
 namespace prof_detail {
+// Events come from a pool created when profiling is enabled, so a profiled
+// launch costs two cudaEventRecord calls and nothing else.
 struct ProfRec {
-    std::string name;
-    cudaEvent_t a, b;
+    const char* name;
+    int a, b;  // pool slots
 };
 bool g_prof_on = false;
 std::mutex g_prof_mu;
+std::vector<cudaEvent_t> g_pool;
+size_t g_pool_next = 0;
 std::vector<ProfRec> g_prof_pending;
 std::map<std::string, std::pair<double, int64_t>> g_prof_totals;
-thread_local std::vector<std::pair<std::string, cudaEvent_t>> g_prof_stack;
+thread_local std::vector<std::pair<const char*, int>> g_prof_stack;
+
+int take_event() {
+    if (g_pool_next >= g_pool.size()) return -1;
+    return (int)g_pool_next++;
+}
 }  // namespace prof_detail
 using namespace prof_detail;
 
 void prof_begin(const char* name, cudaStream_t st) {
     if (!g_prof_on) return;
-    cudaEvent_t a;
-    if (cudaEventCreate(&a) != cudaSuccess) return;
-    cudaEventRecord(a, st);
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    const int a = take_event();
+    if (a >= 0) cudaEventRecord(g_pool[a], st);
     g_prof_stack.emplace_back(name, a);
 }
 
@@ -56,10 +65,11 @@ void prof_end(cudaStream_t st) {
     if (!g_prof_on || g_prof_stack.empty()) return;
     auto top = g_prof_stack.back();
     g_prof_stack.pop_back();
-    cudaEvent_t b;
-    if (cudaEventCreate(&b) != cudaSuccess) return;
-    cudaEventRecord(b, st);
     std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (top.second < 0) return;
+    const int b = take_event();
+    if (b < 0) return;
+    cudaEventRecord(g_pool[b], st);
     g_prof_pending.push_back(ProfRec{top.first, top.second, b});
 }
 }  // namespace jb
@@ -71,16 +81,15 @@ namespace {
 void prof_collect() {
     std::lock_guard<std::mutex> lk(g_prof_mu);
     for (auto& r : g_prof_pending) {
-        cudaEventSynchronize(r.b);
+        cudaEventSynchronize(g_pool[r.b]);
         float ms = 0.f;
-        cudaEventElapsedTime(&ms, r.a, r.b);
+        cudaEventElapsedTime(&ms, g_pool[r.a], g_pool[r.b]);
         auto& t = g_prof_totals[r.name];
         t.first += ms;
         t.second += 1;
-        cudaEventDestroy(r.a);
-        cudaEventDestroy(r.b);
     }
     g_prof_pending.clear();
+    g_pool_next = 0;
 }
 
 thread_local std::string g_last_error;
@@ -723,6 +732,10 @@ jb_status jb_inverse_transform(jb_context* ctx, const double* centers, const dou
 
 void jb_profile_enable(int32_t on) {
     prof_collect();
+    if (on && g_pool.empty()) {
+        g_pool.resize(1 << 15);
+        for (auto& e : g_pool) cudaEventCreate(&e);
+    }
     g_prof_on = on != 0;
 }
 

@@ -120,7 +120,7 @@ __global__ void k_fix(const double* __restrict__ v, ChunkGeom g, int64_t n_chunk
 // Phase 3: rewrite each chunk's flags to the true orbit and count its pieces.
 __global__ void k_apply(const double* __restrict__ v, ChunkGeom g, int64_t n_chunks, double tol2,
                         int64_t max_len, uint8_t* __restrict__ flags,
-                        const int64_t* __restrict__ E, int64_t* __restrict__ count) {
+                        const int64_t* __restrict__ E) {
     const int64_t ch = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (ch >= n_chunks) return;
     int64_t s, c, lo, hi, last;
@@ -143,53 +143,83 @@ __global__ void k_apply(const double* __restrict__ v, ChunkGeom g, int64_t n_chu
             }
         }
     }
-    int64_t n = 0;
-    for (int64_t i = lo; i < hi; ++i) n += flags[i];
-    count[ch] = n;
 }
 
-// Phase 4: emit (len, inc) pieces in input order; per-block max|inc| and
-// max len for the fixed-point exponents downstream.
+// Phase 4a: pieces per chunk (one warp per chunk; lane l owns a contiguous
+// slice of C/32 start positions).
+__global__ void k_count(ChunkGeom g, int64_t n_chunks, const uint8_t* __restrict__ flags,
+                        int64_t* __restrict__ count) {
+    const int lane = threadIdx.x & 31;
+    const int per = (int)(g.C / 32);
+    for (int64_t ch = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; ch < n_chunks;
+         ch += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        int64_t s, c, lo, hi, last;
+        chunk_bounds(g, ch, s, c, lo, hi, last);
+        int n = 0;
+        const int64_t p0 = lo + (int64_t)lane * per;
+        for (int i = 0; i < per; ++i)
+            if (p0 + i < hi) n += flags[p0 + i];
+        for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+        if (lane == 0) count[ch] = n;
+    }
+}
+
+// Phase 4b: emit (len, inc) pieces in input order, one warp per chunk. A
+// piece ends at the next start (same lane slice, a later lane's first start,
+// or the chunk's true exit E). Also max|inc| and max len for the fixed-point
+// exponents downstream.
 __global__ void k_emit(const double* __restrict__ v, ChunkGeom g, int64_t n_chunks,
                        const uint8_t* __restrict__ flags, const int64_t* __restrict__ E,
                        const int64_t* __restrict__ base, int32_t* __restrict__ out_len,
                        double* __restrict__ out_inc, unsigned long long* __restrict__ max_inc_bits,
                        int* __restrict__ max_len) {
-    const int64_t ch = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int per = (int)(g.C / 32);
     double mi = 0.0;
     int ml = 0;
-    if (ch < n_chunks) {
+    for (int64_t ch = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; ch < n_chunks;
+         ch += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         int64_t s, c, lo, hi, last;
         chunk_bounds(g, ch, s, c, lo, hi, last);
-        int64_t j = base[ch];
-        int64_t p = -1;
-        for (int64_t i = lo; i < hi; ++i) {
-            if (!flags[i]) continue;
-            if (p >= 0) {
-                const double inc = v[i] - v[p];
-                out_len[j] = (int32_t)(i - p);
-                out_inc[j] = inc;
-                mi = fmax(mi, fabs(inc));
-                ml = max(ml, (int)(i - p));
-                ++j;
-            }
-            p = i;
+        const int64_t p0 = lo + (int64_t)lane * per;
+        unsigned bits = 0;  // flagged positions of this lane's slice
+        for (int i = 0; i < per; ++i)
+            if (p0 + i < hi && flags[p0 + i]) bits |= 1u << i;
+        const int cnt = __popc(bits);
+        int excl = cnt;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, excl, o);
+            if (lane >= o) excl += y;
         }
-        if (p >= 0) {
-            const int64_t e = E[ch];  // true exit: next start or segment end
+        excl -= cnt;
+        // first start of any later lane (suffix min), else the chunk exit
+        int64_t first = bits ? p0 + (__ffs(bits) - 1) : INT64_MAX;
+        int64_t after = INT64_MAX;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t y = __shfl_down_sync(0xffffffffu, first, o);
+            if (lane + o < 32) after = min(after, y);
+            first = min(first, y);  // becomes suffix-min including self
+        }
+        if (after == INT64_MAX) after = E[ch];
+        int64_t j = base[ch] + excl;
+        while (bits) {
+            const int i = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const int64_t p = p0 + i;
+            const int64_t e = bits ? p0 + (__ffs(bits) - 1) : after;
             const double inc = v[e] - v[p];
             out_len[j] = (int32_t)(e - p);
             out_inc[j] = inc;
             mi = fmax(mi, fabs(inc));
             ml = max(ml, (int)(e - p));
+            ++j;
         }
     }
-    // block max
     for (int o = 16; o > 0; o >>= 1) {
         mi = fmax(mi, __shfl_down_sync(0xffffffffu, mi, o));
         ml = max(ml, __shfl_down_sync(0xffffffffu, ml, o));
     }
-    if ((threadIdx.x & 31) == 0) {
+    if (lane == 0) {
         atomicMax(max_inc_bits, dbits(mi));
         atomicMax(max_len, ml);
     }
@@ -261,7 +291,14 @@ void compress_segments(const double* d_values, const SegTable& seg, double tol,
     if (n_fix_iters) *n_fix_iters = iters;
     {
         JB_PROF("compress_apply", st);
-        k_apply<<<nb, TB, 0, st>>>(d_values, g, n_chunks, tol2, max_piece_len, flags.p, Ea.p, cnt.p);
+        k_apply<<<nb, TB, 0, st>>>(d_values, g, n_chunks, tol2, max_piece_len, flags.p, Ea.p);
+    }
+    JB_LAUNCH_CHECK();
+    const int wgrid = (int)std::max<int64_t>(
+        1, std::min<int64_t>((n_chunks * 32 + 255) / 256, (int64_t)kSMs * 16));
+    {
+        JB_PROF("compress_count", st);
+        k_count<<<wgrid, 256, 0, st>>>(g, n_chunks, flags.p, cnt.p);
     }
     JB_LAUNCH_CHECK();
 
@@ -290,8 +327,8 @@ void compress_segments(const double* d_values, const SegTable& seg, double tol,
     ml.zero();
     {
         JB_PROF("compress_emit", st);
-        k_emit<<<nb, TB, 0, st>>>(d_values, g, n_chunks, flags.p, Ea.p, base.p, out.len.p, out.inc.p,
-                              mx.p, ml.p);
+        k_emit<<<wgrid, 256, 0, st>>>(d_values, g, n_chunks, flags.p, Ea.p, base.p, out.len.p,
+                                      out.inc.p, mx.p, ml.p);
     }
     JB_LAUNCH_CHECK();
     k_seg_offsets<<<ceil_div(n_seg + 1, 256), 256, 0, st>>>(chunk_off.p, base.p, n_seg, N,

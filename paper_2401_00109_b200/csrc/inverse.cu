@@ -1,16 +1,19 @@
 // inverse.cu — inverse symbolization on sm_100a (inverse.hpp:32-132,
 // compression.hpp:87-103, 198-213).
 //
-// Two kernels:
-//  1. one thread per segment runs the three inherently sequential
-//     recurrences exactly as the reference does: inverse digitization
-//     (:32-51), error-carrying rounding with clamp (quantize_lengths :63-74),
-//     the backward length fix-up (match_total_length :81-93), and the running
-//     start value v += inc (inverse_compress :94-101). It records, per piece,
-//     the start value and the absolute output position.
-//  2. one thread per piece writes its interpolated samples
-//     v + inc * (i / len) straight into the (optionally stitched) output: the
-//     bandwidth-bound fill.
+// One warp per segment. The recurrences of the reference are sequential and
+// are kept sequential -- every lane replays the same chain on values
+// broadcast by shuffles, so the rounding is the reference's exactly -- while
+// all memory traffic is warp-coalesced:
+//   pass 1  labels -> real lengths (inverse_digitize_series :32-51, per-label
+//           table) -> error-carrying rounding with clamp (quantize_lengths
+//           :63-74) -> int32 lengths, then the backward fix-up
+//           (match_total_length :81-93);
+//   pass 2  running start value v += inc (inverse_compress :94-101) and an
+//           exact integer scan of the lengths give every piece its start
+//           value and output position; the warp then writes the group's
+//           samples v + inc * (i / len) contiguously, straight into the
+//           (optionally stitched, :198-213) output.
 #include <algorithm>
 
 #include "jb_device.hpp"
@@ -19,72 +22,125 @@ namespace jb {
 
 namespace {
 
-constexpr int64_t SKIP_LAST = 1LL << 62;  // flag: don't write this piece's last sample
-
-__global__ void k_inv_seq(InverseIn in, int64_t* __restrict__ qlen, double* __restrict__ vstart,
-                          int64_t* __restrict__ pstart, double* __restrict__ out,
-                          unsigned long long* __restrict__ err) {
-    const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (s >= in.n_seg) return;
-    const int64_t a = in.seg_offsets[s], b = in.seg_offsets[s + 1];
-    const double scl = in.scl, sl = in.sigma_len, si = in.sigma_inc;
-    // inverse_digitize_series + quantize_lengths
-    double carry = 0.0;
-    int64_t total = 0;
-    for (int64_t j = a; j < b; ++j) {
-        const uint32_t lab = in.labels[j];
-        if ((uint64_t)lab >= in.k) {
-            atomicMin(err, (unsigned long long)(s * 16 + UNKNOWN_SYMBOL));
-            return;
-        }
-        const double l = scl > 0.0 ? in.centers[2 * lab] * sl / scl : in.mean_lengths[lab];
-        int64_t r = llround(l + carry);
-        if (r < 1) r = 1;
-        carry = l + carry - (double)r;
-        qlen[j] = r;
-        total += r;
-    }
-    // match_total_length
-    int64_t residual = in.source_lengths[s] - total;
-    for (int64_t j = b; j-- > a && residual != 0;) {
-        int64_t adj = qlen[j] + residual;
-        if (adj < 1) adj = 1;
-        residual -= adj - qlen[j];
-        qlen[j] = adj;
-    }
-    if (residual != 0 || b == a) {
-        atomicMin(err, (unsigned long long)(s * 16 + INVALID_PIECE));
-        return;
-    }
-    // inverse_compress: running value and output positions
-    const int64_t base = in.out_offsets[s];
-    const double anchor = in.anchors[s];
-    out[base] = anchor;
-    double v = anchor;
-    int64_t pos = base;
-    const bool drop_last = in.layout == 0 && s + 1 < in.n_seg;  // stitch_partitions
-    for (int64_t j = a; j < b; ++j) {
-        vstart[j] = v;
-        pstart[j] = pos | ((drop_last && j == b - 1) ? SKIP_LAST : 0);
-        const uint32_t lab = in.labels[j];
-        v += in.centers[2 * lab + 1] * si;  // RealPiece::inc = c1 * sigma_inc
-        pos += qlen[j];
+__global__ void k_inv_tables(const double* __restrict__ centers,
+                             const double* __restrict__ mean_lengths, uint64_t k, double scl,
+                             double sl, double si, double* __restrict__ rlen,
+                             double* __restrict__ rinc) {
+    for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < k;
+         c += (uint64_t)gridDim.x * blockDim.x) {
+        rlen[c] = scl > 0.0 ? centers[2 * c] * sl / scl : mean_lengths[c];
+        rinc[c] = centers[2 * c + 1] * si;
     }
 }
 
-__global__ void k_inv_fill(InverseIn in, const int64_t* __restrict__ qlen,
-                           const double* __restrict__ vstart, const int64_t* __restrict__ pstart,
-                           double* __restrict__ out) {
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < in.N;
-         j += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t len = qlen[j];
-        const int64_t ps = pstart[j];
-        const int64_t p0 = ps & ~SKIP_LAST;
-        const int64_t n_write = (ps & SKIP_LAST) ? len - 1 : len;
-        const double v = vstart[j];
-        const double inc = in.centers[2 * in.labels[j] + 1] * in.sigma_inc;
-        const double l = (double)len;
-        for (int64_t i = 1; i <= n_write; ++i) out[p0 + i] = v + inc * ((double)i / l);
+constexpr int INV_TB = 256;
+
+__global__ void __launch_bounds__(INV_TB) k_inv_warp(InverseIn in, const double* __restrict__ rlen,
+                                                    const double* __restrict__ rinc,
+                                                    int32_t* __restrict__ qlen,
+                                                    double* __restrict__ out,
+                                                    unsigned long long* __restrict__ err) {
+    const int lane = threadIdx.x & 31;
+    const unsigned FULL = 0xffffffffu;
+    for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; s < in.n_seg;
+         s += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t a = in.seg_offsets[s], b = in.seg_offsets[s + 1];
+        // ---- pass 1: quantize ----
+        double carry = 0.0;
+        long long total = 0;
+        bool bad = false;
+        for (int64_t base = a; base < b; base += 32) {
+            const int64_t j = base + lane;
+            const bool valid = j < b;
+            const uint32_t lab = valid ? in.labels[j] : 0u;
+            if (__any_sync(FULL, valid && (uint64_t)lab >= in.k)) {
+                bad = true;
+                break;
+            }
+            const double l = valid ? __ldg(rlen + lab) : 0.0;
+            const int cnt = (int)((b - base) < 32 ? (b - base) : 32);
+            int myr = 0;
+            for (int i = 0; i < cnt; ++i) {
+                const double li = __shfl_sync(FULL, l, i);
+                const double x = li + carry;
+                long long r = llround(x);
+                if (r < 1) r = 1;
+                carry = x - (double)r;
+                if (lane == i) myr = (int)r;
+            }
+            if (valid) qlen[j] = myr;
+            long long t = myr;
+            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(FULL, t, o);
+            total += t;
+        }
+        if (bad) {
+            if (lane == 0) atomicMin(err, (unsigned long long)(s * 16 + UNKNOWN_SYMBOL));
+            continue;
+        }
+        // ---- match_total_length (backward cascade, almost always 1 piece) ----
+        __syncwarp();
+        int ok = 1;
+        if (lane == 0) {
+            long long residual = in.source_lengths[s] - total;
+            for (int64_t j = b; j-- > a && residual != 0;) {
+                long long adj = (long long)qlen[j] + residual;
+                if (adj < 1) adj = 1;
+                residual -= adj - qlen[j];
+                qlen[j] = (int32_t)adj;
+            }
+            ok = (residual == 0 && b > a) ? 1 : 0;
+            if (!ok) atomicMin(err, (unsigned long long)(s * 16 + INVALID_PIECE));
+        }
+        ok = __shfl_sync(FULL, ok, 0);
+        if (!ok) continue;
+        __syncwarp();
+        // ---- pass 2: start values, positions, interpolation fill ----
+        const bool drop_last = in.layout == 0 && s + 1 < in.n_seg;  // stitch_partitions
+        int64_t pos = in.out_offsets[s];
+        double v = in.anchors[s];
+        if (lane == 0) out[pos] = v;
+        for (int64_t base = a; base < b; base += 32) {
+            const int64_t j = base + lane;
+            const bool valid = j < b;
+            const uint32_t lab = valid ? in.labels[j] : 0u;
+            const int len = valid ? qlen[j] : 0;
+            const double inc = valid ? __ldg(rinc + lab) : 0.0;
+            const int cnt = (int)((b - base) < 32 ? (b - base) : 32);
+            double myv = 0.0;
+            for (int i = 0; i < cnt; ++i) {  // v += p.inc, sequential as the reference
+                if (lane == i) myv = v;
+                v += __shfl_sync(FULL, inc, i);
+            }
+            // inclusive scan of lengths (exact integers)
+            long long incl = len;
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long y = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const long long L = __shfl_sync(FULL, incl, 31);
+            const bool last_group = base + 32 >= b;
+            for (long long q0 = 1; q0 <= L; q0 += 32) {
+                const long long q = q0 + lane;  // 1-based sample within the group
+                // piece lo with excl_lo < q <= incl_lo
+                int lo = 0, hi = cnt - 1;
+                while (lo < hi) {  // warp-uniform trip count (cnt is uniform)
+                    const int mid = (lo + hi) >> 1;
+                    const long long cm = __shfl_sync(FULL, incl, mid);
+                    if (q <= cm) hi = mid;
+                    else lo = mid + 1;
+                }
+                const long long ci = __shfl_sync(FULL, incl, lo);
+                const int li = __shfl_sync(FULL, len, lo);
+                const double vi = __shfl_sync(FULL, myv, lo);
+                const double ii = __shfl_sync(FULL, inc, lo);
+                if (q <= L) {
+                    const long long i = q - (ci - li);  // 1..len within piece lo
+                    const bool skip = drop_last && last_group && q == L;
+                    if (!skip) out[pos + q] = vi + ii * ((double)i / (double)li);
+                }
+            }
+            pos += L;
+        }
     }
 }
 
@@ -93,15 +149,23 @@ __global__ void k_inv_fill(InverseIn in, const int64_t* __restrict__ qlen,
 void inverse_transform_device(const InverseIn& in, double* d_out, cudaStream_t st) {
     if (in.layout == 0 && in.n_seg == 0)
         throw Error(INVALID_INPUT, "stitch_partitions: no segments");
-    DArr<int64_t> qlen(std::max<int64_t>(in.N, 1), st), pstart(std::max<int64_t>(in.N, 1), st);
-    DArr<double> vstart(std::max<int64_t>(in.N, 1), st);
+    DArr<int32_t> qlen(std::max<int64_t>(in.N, 1), st);
+    const uint64_t kk = std::max<uint64_t>(in.k, 1);
+    DArr<double> tab(2 * kk, st);
     DArr<unsigned long long> err(1, st);
     const unsigned long long none = ~0ULL;
     err.upload(&none, 1);
+    if (in.k > 0) {
+        k_inv_tables<<<(int)std::min<uint64_t>((in.k + 255) / 256, 1024), 256, 0, st>>>(
+            in.centers, in.mean_lengths, in.k, in.scl, in.sigma_len, in.sigma_inc, tab.p,
+            tab.p + kk);
+        JB_LAUNCH_CHECK();
+    }
     {
-        JB_PROF("inverse_seq", st);
-        k_inv_seq<<<(int)((in.n_seg + 127) / 128), 128, 0, st>>>(in, qlen.p, vstart.p, pstart.p,
-                                                              d_out, err.p);
+        JB_PROF("inverse_warp", st);
+        const int grid = (int)std::max<int64_t>(
+            1, std::min<int64_t>((in.n_seg * 32 + INV_TB - 1) / INV_TB, (int64_t)kSMs * 16));
+        k_inv_warp<<<grid, INV_TB, 0, st>>>(in, tab.p, tab.p + kk, qlen.p, d_out, err.p);
     }
     JB_LAUNCH_CHECK();
     unsigned long long e;
@@ -116,15 +180,6 @@ void inverse_transform_device(const InverseIn& in, double* d_out, cudaStream_t s
                             " (segment " + std::to_string(seg) + ")");
         throw Error(INVALID_PIECE, "cannot fit pieces into the segment's steps (segment " +
                                        std::to_string(seg) + ")");
-    }
-    if (in.N > 0) {
-        const int grid =
-            (int)std::max<int64_t>(1, std::min<int64_t>((in.N + 255) / 256, (int64_t)kSMs * 16));
-        {
-            JB_PROF("inverse_fill", st);
-            k_inv_fill<<<grid, 256, 0, st>>>(in, qlen.p, vstart.p, pstart.p, d_out);
-        }
-        JB_LAUNCH_CHECK();
     }
 }
 
