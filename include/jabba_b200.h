@@ -175,6 +175,14 @@ int32_t jb_profile_read(char* names, double* total_ms, int64_t* launches, int32_
  * the roofline denominator for fp64-bound kernels. */
 jb_status jb_probe_fp64_tflops(int device, double* tflops);
 
+/* Building blocks, exposed for parity tests against the reference's RNG use:
+ * the first `count` draws of std::mt19937_64(seed) generated on the device
+ * (multi-CTA jump-ahead), and detail::sample_indices (clustering.hpp:74-85)
+ * resolved on the device. Host output buffers. */
+jb_status jb_mt19937_64_stream(jb_context* ctx, uint64_t seed, uint64_t count, uint64_t* out);
+jb_status jb_sample_indices(jb_context* ctx, uint64_t n, uint64_t sample_size, uint64_t seed,
+                            uint64_t* out);
+
 /* symbol token of cluster rank r in an alphabet of size k (core.hpp:186-193);
  * writes a NUL-terminated string into buf (>= 24 bytes); returns its length */
 int32_t jb_symbol_token(uint64_t rank, uint64_t alphabet_size, char* buf);

@@ -24,7 +24,7 @@ EXPORTS = [
     "jb_fit_reconstruct_size", "jb_fit_copy_pieces", "jb_fit_copy_symbolic", "jb_fit_stats",
     "jb_fit_inverse_transform", "jb_reconstruct_size", "jb_inverse_transform",
     "jb_symbol_token", "jb_profile_enable", "jb_profile_reset", "jb_profile_read",
-    "jb_probe_fp64_tflops",
+    "jb_probe_fp64_tflops", "jb_mt19937_64_stream", "jb_sample_indices",
 ]
 
 
@@ -86,6 +86,10 @@ def lib() -> C.CDLL:
     L.jb_profile_enable.argtypes = [C.c_int32]
     L.jb_profile_read.argtypes = [C.c_char_p, vp, vp, C.c_int32]
     L.jb_profile_read.restype = C.c_int32
+    L.jb_mt19937_64_stream.argtypes = [vp, C.c_uint64, C.c_uint64, vp]
+    L.jb_mt19937_64_stream.restype = C.c_int
+    L.jb_sample_indices.argtypes = [vp, C.c_uint64, C.c_uint64, C.c_uint64, vp]
+    L.jb_sample_indices.restype = C.c_int
     L.jb_probe_fp64_tflops.argtypes = [C.c_int, C.POINTER(C.c_double)]
     L.jb_probe_fp64_tflops.restype = C.c_int
     for name in ("jb_fit_transform", "jb_plan_segments", "jb_context_create",

@@ -13,8 +13,10 @@ HBM as a CUDA tensor).
 """
 from __future__ import annotations
 
+import atexit
 import ctypes as C
 import enum
+import weakref
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
@@ -328,22 +330,39 @@ def plan_segments(series_lengths, layout: int, parts: int):
     return first[: nseg.value].copy(), steps[: nseg.value].copy()
 
 
+_LIVE = weakref.WeakSet()
+
+
+@atexit.register
+def _release_all():
+    """Free device-resident handles while the CUDA runtime is still alive
+    (interpreter teardown order is otherwise unspecified)."""
+    fits = [o for o in list(_LIVE) if isinstance(o, NativeFit)]
+    engines = [o for o in list(_LIVE) if isinstance(o, Engine)]
+    for o in fits + engines:
+        o.close()
+
+
 class NativeFit:
     """Device-resident result of one fit_transform (owns a jb_fit handle)."""
 
     def __init__(self, engine: "Engine", handle: C.c_void_p):
         self.engine = engine
         self.h = handle
+        _LIVE.add(self)
         L = N.lib()
         self.n_seg = L.jb_fit_n_segments(handle)
         self.n_pieces = L.jb_fit_n_pieces(handle)
         self.k = L.jb_fit_k(handle)
         self.layout = L.jb_fit_layout(handle)
 
+    def close(self):
+        if getattr(self, "h", None) and N is not None and N._lib is not None:
+            N._lib.jb_fit_free(self.h)
+        self.h = None
+
     def __del__(self):
-        if getattr(self, "h", None):
-            N.lib().jb_fit_free(self.h)
-            self.h = None
+        self.close()
 
     def pieces(self):
         off = np.zeros(self.n_seg + 1, np.int64)
@@ -411,11 +430,15 @@ class Engine:
         _check(N.lib().jb_context_create(int(device), C.byref(h)))
         self.ctx = h
         self.device = device
+        _LIVE.add(self)
+
+    def close(self):
+        if getattr(self, "ctx", None) and N is not None and N._lib is not None:
+            N._lib.jb_context_destroy(self.ctx)
+        self.ctx = None
 
     def __del__(self):
-        if getattr(self, "ctx", None):
-            N.lib().jb_context_destroy(self.ctx)
-            self.ctx = None
+        self.close()
 
     def fit_arrays(self, values, seg_first, seg_steps, layout: int, cfg: JabbaConfig,
                    device_ptr: Optional[int] = None, n_values: Optional[int] = None) -> NativeFit:
@@ -433,6 +456,16 @@ class Engine:
             _check(N.lib().jb_fit_transform(self.ctx, v.ctypes.data, v.size, 0, sf, ss, len(sf),
                                             int(layout), C.byref(c), C.byref(h)))
         return NativeFit(self, h)
+
+    def mt19937_64_stream(self, seed: int, count: int) -> np.ndarray:
+        out = np.zeros(max(count, 1), np.uint64)
+        _check(N.lib().jb_mt19937_64_stream(self.ctx, seed, count, out.ctypes.data))
+        return out[:count]
+
+    def sample_indices(self, n: int, sample_size: int, seed: int) -> np.ndarray:
+        out = np.zeros(max(sample_size, 1), np.uint64)
+        _check(N.lib().jb_sample_indices(self.ctx, n, sample_size, seed, out.ctypes.data))
+        return out[:sample_size]
 
     def inverse_arrays(self, centers, mean_lengths, scaling, labels, piece_offsets, anchors,
                        source_lengths, layout: int) -> np.ndarray:

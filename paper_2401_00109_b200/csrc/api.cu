@@ -760,6 +760,30 @@ int32_t jb_profile_read(char* names, double* total_ms, int64_t* launches, int32_
     return (int32_t)g_prof_totals.size();
 }
 
+jb_status jb_mt19937_64_stream(jb_context* ctx, uint64_t seed, uint64_t count, uint64_t* out) {
+    return (jb_status)guarded([&] {
+        JB_CUDA(cudaSetDevice(ctx->device));
+        DArr<uint64_t> raw;
+        mt19937_64_generate(seed, count, raw, ctx->stream);
+        raw.download(out, count);
+        JB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+jb_status jb_sample_indices(jb_context* ctx, uint64_t n, uint64_t sample_size, uint64_t seed,
+                            uint64_t* out) {
+    return (jb_status)guarded([&] {
+        JB_CUDA(cudaSetDevice(ctx->device));
+        if (sample_size > n) throw Error(INVALID_INPUT, "sample larger than population");
+        DArr<uint64_t> raw, idx;
+        const uint64_t raw_count = sample_size + 4096;
+        mt19937_64_generate(seed, raw_count, raw, ctx->stream);
+        sample_indices_device(n, sample_size, raw.p, raw_count, idx, ctx->stream);
+        idx.download(out, sample_size);
+        JB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
 int32_t jb_symbol_token(uint64_t rank, uint64_t alphabet_size, char* buf) {
     // symbol_token (core.hpp:186-193)
     if (alphabet_size <= 94) {

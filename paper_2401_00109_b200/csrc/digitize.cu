@@ -10,6 +10,7 @@
 #include <cmath>
 
 #include "jb_device.hpp"
+#include "jb_grid.cuh"
 
 namespace jb {
 
@@ -190,99 +191,11 @@ struct StatsAcc {
     unsigned long long* sy;      // 2k
 };
 
-// Uniform grid over the points' bounding box. Every cell keeps the exact
-// candidate centers of its (slightly inflated) box, in index order: a center
-// is dropped only when, for every point of the box, its rounded reference
-// distance is strictly larger than that of the center realising the
-// min-over-centers of the box's max distance (the same 1e-12 margin argument
-// as the Lloyd tiles in kmeans.cu). nearest_center over the candidates with
-// strict < is therefore exactly nearest_center over all centers
-// (clustering.hpp:146-157).
-struct GridDesc {
-    double x0, y0, w, h, invw, invh, mw, mh;
-    int G;
-};
-
-__device__ __forceinline__ double4 cell_box(const GridDesc& g, int cell) {
-    const int ix = cell % g.G, iy = cell / g.G;
-    return make_double4(g.x0 + ix * g.w - g.mw, g.x0 + (ix + 1) * g.w + g.mw,
-                        g.y0 + iy * g.h - g.mh, g.y0 + (iy + 1) * g.h + g.mh);
-}
-
-__device__ __forceinline__ void box_bounds(double cx, double cy, const double4& b, double& dmin2,
-                                           double& dmax2) {
-    const double ex = fmax(fmax(b.x - cx, cx - b.y), 0.0);
-    const double ey = fmax(fmax(b.z - cy, cy - b.w), 0.0);
-    dmin2 = ex * ex + ey * ey;
-    const double fx = fmax(fabs(b.x - cx), fabs(b.y - cx));
-    const double fy = fmax(fabs(b.z - cy), fabs(b.w - cy));
-    dmax2 = fx * fx + fy * fy;
-}
-
-// warp per cell; pass 0 counts, pass 1 writes (offsets from a scan)
-__global__ void k_grid_cands(GridDesc g, const double* __restrict__ centers, int k, int pass,
-                             int* __restrict__ counts, const int* __restrict__ off,
-                             uint16_t* __restrict__ cand) {
-    const int lane = threadIdx.x & 31;
-    const int ncell = g.G * g.G;
-    for (int cell = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; cell < ncell;
-         cell += (gridDim.x * blockDim.x) >> 5) {
-        const double4 b = cell_box(g, cell);
-        double M = INFINITY;
-        for (int c = lane; c < k; c += 32) {
-            double dmn, dmx;
-            box_bounds(centers[2 * c], centers[2 * c + 1], b, dmn, dmx);
-            M = fmin(M, dmx);
-        }
-        for (int o = 16; o > 0; o >>= 1) M = fmin(M, __shfl_xor_sync(0xffffffffu, M, o));
-        const double thr = M * (1.0 + 1e-12) + 1e-300;
-        int nc = 0;
-        const int base = pass ? off[cell] : 0;
-        for (int c0 = 0; c0 < k; c0 += 32) {
-            const int c = c0 + lane;
-            bool keep = false;
-            if (c < k) {
-                double dmn, dmx;
-                box_bounds(centers[2 * c], centers[2 * c + 1], b, dmn, dmx);
-                keep = dmn <= thr;
-            }
-            const unsigned m = __ballot_sync(0xffffffffu, keep);
-            if (pass && keep) cand[base + nc + __popc(m & ((1u << lane) - 1u))] = (uint16_t)c;
-            nc += __popc(m);
-        }
-        if (!pass && lane == 0) counts[cell] = nc;
-    }
-}
-
-__device__ __forceinline__ uint32_t nearest_grid(double px, double py, const double* cx,
-                                                 const double* cy, const GridDesc& g,
-                                                 const int* __restrict__ off,
-                                                 const uint16_t* __restrict__ cand) {
-    int ix = (int)((px - g.x0) * g.invw);
-    int iy = (int)((py - g.y0) * g.invh);
-    ix = min(max(ix, 0), g.G - 1);
-    iy = min(max(iy, 0), g.G - 1);
-    const int cell = iy * g.G + ix;
-    const int a = __ldg(off + cell), b = __ldg(off + cell + 1);
-    uint32_t best = __ldg(cand + a);
-    double bd = dist2(px, py, cx[best], cy[best]);
-    for (int j = a + 1; j < b; ++j) {
-        const uint32_t c = __ldg(cand + j);
-        const double d = dist2(px, py, cx[c], cy[c]);
-        if (d < bd) {
-            bd = d;
-            best = c;
-        }
-    }
-    return best;
-}
-
 // block-privatized statistics in shared memory, flushed with global atomics
 __global__ void k_assign_stats(const double2* __restrict__ pts, const int32_t* __restrict__ len,
                                int64_t n, const double* __restrict__ centers, int k,
                                int do_assign, uint32_t* __restrict__ labels, int Ex, int Ey,
-                               StatsAcc g, int privatize, GridDesc gd,
-                               const int* __restrict__ goff, const uint16_t* __restrict__ gcand) {
+                               StatsAcc g, int privatize, CandGrid cg) {
     extern __shared__ unsigned char smem[];
     double* cx = reinterpret_cast<double*>(smem);
     double* cy = cx + k;
@@ -313,7 +226,7 @@ __global__ void k_assign_stats(const double2* __restrict__ pts, const int32_t* _
         const double2 p = pts[i];
         uint32_t lab;
         if (do_assign) {
-            lab = nearest_grid(p.x, p.y, cx, cy, gd, goff, gcand);
+            lab = grid_nearest(cg, p.x, p.y, cx, cy, k);
             labels[i] = lab;
         } else {
             lab = labels[i];
@@ -395,45 +308,18 @@ void assign_and_stats(const double* d_pts, const int32_t* d_len, int64_t n,
     if (smem > 200 * 1024) throw Error(INVALID_INPUT, "k too large for the assignment kernel");
     JB_CUDA(cudaFuncSetAttribute(k_assign_stats, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
-    // candidate grid over the points' bounding box
-    GridDesc gd{};
-    DArr<int> gcount, goff;
-    DArr<uint16_t> gcand;
+    // exact candidate grid over the points' bounding box (jb_grid.cuh)
+    CandGrid cg{};
+    DArr<uint16_t> cg_cnt, cg_cand;
     if (do_assign) {
-        int G = 16;
-        while (G < 256 && (double)G * G < 16.0 * (double)k) G <<= 1;
-        gd.G = G;
-        const double wx = bb.xmax - bb.xmin, wy = bb.ymax - bb.ymin;
-        gd.x0 = bb.xmin;
-        gd.y0 = bb.ymin;
-        gd.w = wx > 0 ? wx / G : 1.0;
-        gd.h = wy > 0 ? wy / G : 1.0;
-        gd.invw = 1.0 / gd.w;
-        gd.invh = 1.0 / gd.h;
-        gd.mw = gd.w * 1e-9 + 1e-15 * (std::fabs(bb.xmin) + std::fabs(bb.xmax));
-        gd.mh = gd.h * 1e-9 + 1e-15 * (std::fabs(bb.ymin) + std::fabs(bb.ymax));
-        const int ncell = G * G;
-        gcount.alloc(ncell + 1, st);
-        goff.alloc(ncell + 1, st);
-        JB_CUDA(cudaMemsetAsync(gcount.p + ncell, 0, sizeof(int), st));
-        const int gb = std::max(1, std::min(ncell / 8, kSMs * 8));
-        {
-            JB_PROF("assign_grid", st);
-            k_grid_cands<<<gb, 256, 0, st>>>(gd, dc.p, (int)k, 0, gcount.p, nullptr, nullptr);
-        }
-        JB_LAUNCH_CHECK();
-        size_t tb = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tb, gcount.p, goff.p, ncell + 1, st);
-        DArr<uint8_t> tmp(tb, st);
-        cub::DeviceScan::ExclusiveSum(tmp.p, tb, gcount.p, goff.p, ncell + 1, st);
-        int total = 0;
-        JB_CUDA(cudaMemcpyAsync(&total, goff.p + ncell, sizeof(int), cudaMemcpyDeviceToHost, st));
-        JB_CUDA(cudaStreamSynchronize(st));
-        gcand.alloc(std::max(total, 1), st);
-        {
-            JB_PROF("assign_grid", st);
-            k_grid_cands<<<gb, 256, 0, st>>>(gd, dc.p, (int)k, 1, nullptr, goff.p, gcand.p);
-        }
+        const int G = grid_side_for(k), cap = 32;
+        cg = make_grid_desc(bb.xmin, bb.xmax, bb.ymin, bb.ymax, G, cap);
+        cg_cnt.alloc((size_t)G * G, st);
+        cg_cand.alloc((size_t)G * G * cap, st);
+        cg.cnt = cg_cnt.p;
+        cg.cand = cg_cand.p;
+        JB_PROF("assign_grid", st);
+        k_grid_build<<<std::min(G * G / 8, kSMs * 16), 256, 0, st>>>(cg, dc.p, (int)k);
         JB_LAUNCH_CHECK();
     }
     const int TB = 256;
@@ -443,7 +329,7 @@ void assign_and_stats(const double* d_pts, const int32_t* d_len, int64_t n,
         JB_PROF("assign_stats", st);
         k_assign_stats<<<grid, TB, smem, st>>>(reinterpret_cast<const double2*>(d_pts), d_len, n,
                                            dc.p, (int)k, do_assign ? 1 : 0, d_labels, Ex, Ey, g,
-                                           privatize, gd, goff.p, gcand.p);
+                                           privatize, cg);
     }
     JB_LAUNCH_CHECK();
     std::vector<unsigned long long> h = acc.to_host(7 * k);

@@ -121,14 +121,15 @@ __global__ void __launch_bounds__(INV_TB) k_inv_warp(InverseIn in, const double*
             const bool last_group = base + 32 >= b;
             for (long long q0 = 1; q0 <= L; q0 += 32) {
                 const long long q = q0 + lane;  // 1-based sample within the group
-                // piece lo with excl_lo < q <= incl_lo
-                int lo = 0, hi = cnt - 1;
-                while (lo < hi) {  // warp-uniform trip count (cnt is uniform)
-                    const int mid = (lo + hi) >> 1;
-                    const long long cm = __shfl_sync(FULL, incl, mid);
-                    if (q <= cm) hi = mid;
-                    else lo = mid + 1;
+                // piece lo with excl_lo < q <= incl_lo: fixed 5-step search so
+                // every lane executes the same full-mask shuffles
+                int last_below = -1;  // last piece with incl < q
+                for (int step = 16; step > 0; step >>= 1) {
+                    const int t = last_below + step;
+                    const long long cm = __shfl_sync(FULL, incl, t < 31 ? t : 31);
+                    if (t < cnt && cm < q) last_below = t;
                 }
+                const int lo = last_below + 1 < 32 ? last_below + 1 : 31;
                 const long long ci = __shfl_sync(FULL, incl, lo);
                 const int li = __shfl_sync(FULL, len, lo);
                 const double vi = __shfl_sync(FULL, myv, lo);

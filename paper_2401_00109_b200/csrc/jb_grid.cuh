@@ -1,0 +1,134 @@
+// jb_grid.cuh — exact candidate grid for nearest-center queries.
+//
+// A uniform G x G grid over the points' bounding box. Every cell stores, in
+// index order, the centers that can be the reference's nearest center
+// (clustering.hpp:146-157: rounded dx*dx+dy*dy, strict <, lowest index) for
+// SOME point of the cell's slightly inflated box. A center c is dropped only if
+//     dmin2(c, box) > M * (1 + 1e-12),   M = min over centers of dmax2(., box);
+// then for every point p of the box, with D the exact squared distance,
+//     D(p,c) >= dmin2/(1+4u) > M(1+1e-12)/(1+4u) >= D(p,c*)(1+1e-12)/(1+4u)^2
+// and the rounded distances (relative error <= 4u, u = 2^-53) satisfy
+// d(p,c) > d(p,c*): c is neither the argmin nor a lower-index tie. Looping
+// over the candidates in index order with strict < is therefore exactly the
+// reference's loop over all centers. Cells with more than `cap` candidates
+// fall back to all centers.
+#pragma once
+
+#include <cmath>
+
+#include "jb_common.cuh"
+
+namespace jb {
+
+struct CandGrid {
+    double x0, y0, w, h, invw, invh, mw, mh;
+    int G, cap;
+    uint16_t* cnt;   // G*G; 0xFFFF = use all centers
+    uint16_t* cand;  // G*G*cap
+};
+
+__host__ inline CandGrid make_grid_desc(double xmin, double xmax, double ymin, double ymax,
+                                        int G, int cap) {
+    CandGrid g{};
+    g.G = G;
+    g.cap = cap;
+    const double wx = xmax - xmin, wy = ymax - ymin;
+    g.x0 = xmin;
+    g.y0 = ymin;
+    g.w = wx > 0 ? wx / G : 1.0;
+    g.h = wy > 0 ? wy / G : 1.0;
+    g.invw = 1.0 / g.w;
+    g.invh = 1.0 / g.h;
+    // inflation covers the rounding of the cell index and of the box corners
+    g.mw = g.w * 1e-9 + 1e-15 * (std::fabs(xmin) + std::fabs(xmax));
+    g.mh = g.h * 1e-9 + 1e-15 * (std::fabs(ymin) + std::fabs(ymax));
+    return g;
+}
+
+__device__ __forceinline__ void grid_box_d2(double cx, double cy, double bx0, double bx1,
+                                            double by0, double by1, double& dmin2,
+                                            double& dmax2) {
+    const double ex = fmax(fmax(bx0 - cx, cx - bx1), 0.0);
+    const double ey = fmax(fmax(by0 - cy, cy - by1), 0.0);
+    dmin2 = ex * ex + ey * ey;
+    const double fx = fmax(fabs(bx0 - cx), fabs(bx1 - cx));
+    const double fy = fmax(fabs(by0 - cy), fabs(by1 - cy));
+    dmax2 = fx * fx + fy * fy;
+}
+
+// one warp per cell
+static __global__ void k_grid_build(CandGrid g, const double* __restrict__ centers, int k) {
+    const int lane = threadIdx.x & 31;
+    const int ncell = g.G * g.G;
+    for (int cell = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; cell < ncell;
+         cell += (gridDim.x * blockDim.x) >> 5) {
+        const int ix = cell % g.G, iy = cell / g.G;
+        const double bx0 = g.x0 + ix * g.w - g.mw, bx1 = g.x0 + (ix + 1) * g.w + g.mw;
+        const double by0 = g.y0 + iy * g.h - g.mh, by1 = g.y0 + (iy + 1) * g.h + g.mh;
+        double M = INFINITY;
+        for (int c = lane; c < k; c += 32) {
+            double dmn, dmx;
+            grid_box_d2(centers[2 * c], centers[2 * c + 1], bx0, bx1, by0, by1, dmn, dmx);
+            M = fmin(M, dmx);
+        }
+        for (int o = 16; o > 0; o >>= 1) M = fmin(M, __shfl_xor_sync(0xffffffffu, M, o));
+        const double thr = M * (1.0 + 1e-12) + 1e-300;
+        int nc = 0;
+        uint16_t* out = g.cand + (size_t)cell * g.cap;
+        for (int c0 = 0; c0 < k; c0 += 32) {
+            const int c = c0 + lane;
+            bool keep = false;
+            if (c < k) {
+                double dmn, dmx;
+                grid_box_d2(centers[2 * c], centers[2 * c + 1], bx0, bx1, by0, by1, dmn, dmx);
+                keep = dmn <= thr;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            const int at = nc + __popc(m & ((1u << lane) - 1u));
+            if (keep && at < g.cap) out[at] = (uint16_t)c;
+            nc += __popc(m);
+        }
+        if (lane == 0) g.cnt[cell] = nc <= g.cap ? (uint16_t)nc : (uint16_t)0xFFFF;
+    }
+}
+
+// nearest_center (clustering.hpp:146-157) through the grid; cx/cy in smem
+__device__ __forceinline__ uint32_t grid_nearest(const CandGrid& g, double px, double py,
+                                                 const double* cx, const double* cy, int k) {
+    int ix = (int)((px - g.x0) * g.invw);
+    int iy = (int)((py - g.y0) * g.invh);
+    ix = min(max(ix, 0), g.G - 1);
+    iy = min(max(iy, 0), g.G - 1);
+    const int cell = iy * g.G + ix;
+    const int n = __ldg(g.cnt + cell);
+    uint32_t best = 0;
+    double bd = __longlong_as_double(0x7FF0000000000000LL);  // +inf
+    if (n == 0xFFFF) {
+        for (int c = 0; c < k; ++c) {
+            const double d = dist2(px, py, cx[c], cy[c]);
+            if (d < bd) {
+                bd = d;
+                best = (uint32_t)c;
+            }
+        }
+        return best;
+    }
+    const uint16_t* cl = g.cand + (size_t)cell * g.cap;
+    for (int j = 0; j < n; ++j) {
+        const uint32_t c = __ldg(cl + j);
+        const double d = dist2(px, py, cx[c], cy[c]);
+        if (d < bd) {
+            bd = d;
+            best = c;
+        }
+    }
+    return best;
+}
+
+inline int grid_side_for(uint64_t k) {
+    int G = 64;
+    while (G < 256 && (double)G * G < 256.0 * (double)k) G <<= 1;
+    return G;
+}
+
+}  // namespace jb

@@ -21,10 +21,17 @@
 //    exactly as update_means (:181-197).
 #include <cub/cub.cuh>
 
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <mutex>
+#include <string>
+#include <vector>
 
 #include "jb_device.hpp"
+#include "jb_grid.cuh"
 
 namespace jb {
 
@@ -75,6 +82,71 @@ __global__ void __launch_bounds__(320) k_mt_generate(uint64_t seed, uint64_t cou
         if (t >= 156 && t < 312) mt[t] = v;
         __syncthreads();
         if (t < 312 && base + t < count) out[base + t] = mt_temper(mt[t]);
+    }
+}
+
+// Multi-CTA engine: CTA c produces draws [c*B, (c+1)*B). Its starting window
+// (x_{cB} .. x_{cB+311}) is g_c(A) applied to the seeded window, g_c the
+// build-time jump polynomial (mt64_jump.c): XOR of the windows x_{i..i+311}
+// over the set coefficients i of g_c (64 batches of 312 windows). The 31 low
+// bits of the window's first word may differ from the sequential engine, but
+// the twist never reads them. buf[312+i] = twist(buf[i], buf[i+1], buf[i+156])
+// is x_{k+312} = f(x_k, x_{k+1}, x_{k+156}) on a 624-word sliding buffer.
+__global__ void __launch_bounds__(320) k_mt_jump_generate(uint64_t seed, uint64_t count,
+                                                          uint64_t B,
+                                                          const uint64_t* __restrict__ jump,
+                                                          uint64_t* __restrict__ out) {
+    __shared__ uint64_t buf[624];
+    __shared__ uint64_t acc[312];
+    __shared__ uint64_t gbits[312];
+    const int t = threadIdx.x;
+    const uint64_t start = (uint64_t)blockIdx.x * B;
+    if (start >= count) return;
+    const uint64_t nout = min(B, count - start);
+    if (t == 0) {
+        buf[0] = seed;
+        for (int i = 1; i < 312; ++i)
+            buf[i] = 6364136223846793005ULL * (buf[i - 1] ^ (buf[i - 1] >> 62)) + (uint64_t)i;
+    }
+    if (t < 312) {
+        gbits[t] = jump[(size_t)blockIdx.x * 312 + t];
+        acc[t] = 0;
+    }
+    __syncthreads();
+    auto advance = [&]() {  // buf[312..623] from buf[0..311]
+        if (t < 156) buf[312 + t] = mt_twist(buf[t], buf[t + 1], buf[t + 156]);
+        __syncthreads();
+        if (t >= 156 && t < 312) buf[312 + t] = mt_twist(buf[t], buf[t + 1], buf[t + 156]);
+        __syncthreads();
+    };
+    auto slide = [&]() {  // buf[0..311] = buf[312..623]
+        uint64_t v = 0;
+        if (t < 312) v = buf[312 + t];
+        __syncthreads();
+        if (t < 312) buf[t] = v;
+        __syncthreads();
+    };
+    if (blockIdx.x > 0) {
+        for (int b = 0; b < 64; ++b) {
+            advance();
+            if (t < 312) {
+                uint64_t a = acc[t];
+                for (int tt = 0; tt < 312; ++tt) {
+                    const int bit = 312 * b + tt;
+                    if (bit < 19937 && ((gbits[bit >> 6] >> (bit & 63)) & 1ULL)) a ^= buf[tt + t];
+                }
+                acc[t] = a;
+            }
+            __syncthreads();
+            slide();
+        }
+        if (t < 312) buf[t] = acc[t];
+        __syncthreads();
+    }
+    for (uint64_t base = 0; base < nout; base += 312) {
+        advance();
+        if (t < 312 && base + t < nout) out[start + base + t] = mt_temper(buf[312 + t]);
+        slide();
     }
 }
 
@@ -153,10 +225,59 @@ int grid_cap(uint64_t n, int tb = 256, int per_sm = 8) {
 
 }  // namespace
 
+namespace {
+// jump table produced by mt64_jump at build time, next to libjabba_b200.so
+struct JumpTable {
+    bool tried = false;
+    uint64_t B = 0, count = 0;
+    uint64_t* d = nullptr;  // device copy (process lifetime)
+    int device = -1;
+};
+JumpTable g_jump;
+std::mutex g_jump_mu;
+
+const JumpTable* jump_table() {
+    std::lock_guard<std::mutex> lk(g_jump_mu);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (g_jump.tried && g_jump.device == dev) return g_jump.d ? &g_jump : nullptr;
+    g_jump.tried = true;
+    g_jump.device = dev;
+    g_jump.d = nullptr;
+    Dl_info info;
+    if (!dladdr((void*)&jump_table, &info) || !info.dli_fname) return nullptr;
+    std::string path(info.dli_fname);
+    path = path.substr(0, path.rfind('/') + 1) + "mt64_jump.bin";
+    FILE* f = fopen(path.c_str(), "rb");
+    if (!f) return nullptr;
+    uint64_t hdr[4];
+    std::vector<uint64_t> tab;
+    bool ok = fread(hdr, 8, 4, f) == 4 && hdr[0] == 0x4A4D54364A4D5031ULL && hdr[3] == 312;
+    if (ok) {
+        tab.resize(hdr[2] * 312);
+        ok = fread(tab.data(), 8, tab.size(), f) == tab.size();
+    }
+    fclose(f);
+    if (!ok) return nullptr;
+    if (cudaMalloc((void**)&g_jump.d, tab.size() * 8) != cudaSuccess) {
+        g_jump.d = nullptr;
+        return nullptr;
+    }
+    cudaMemcpy(g_jump.d, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice);
+    g_jump.B = hdr[1];
+    g_jump.count = hdr[2];
+    return &g_jump;
+}
+}  // namespace
+
 void mt19937_64_generate(uint64_t seed, uint64_t count, DArr<uint64_t>& out, cudaStream_t st) {
     out.alloc(count, st);
-    {
-        JB_PROF("mt19937_64", st);
+    const JumpTable* jt = jump_table();
+    JB_PROF("mt19937_64", st);
+    if (jt && (count + jt->B - 1) / jt->B <= jt->count) {
+        const int ctas = (int)((count + jt->B - 1) / jt->B);
+        k_mt_jump_generate<<<ctas, 320, 0, st>>>(seed, count, jt->B, jt->d, out.p);
+    } else {  // no table (or beyond it): one CTA walks the engine
         k_mt_generate<<<1, 320, 0, st>>>(seed, count, out.p);
     }
     JB_LAUNCH_CHECK();
@@ -572,16 +693,14 @@ struct ClusterAcc {
 };
 
 constexpr int LL_TB = 256;
-constexpr int LL_WARPS = LL_TB / 32;
 
-// One warp per tile of TILE Morton-ordered points: exact candidate set of the
-// tile's box (every center that can be the reference argmin for some point
-// in it, in index order), then nearest_center over the candidates only
-// (clustering.hpp:146-157: strict <, lowest index). Cluster sums follow the
-// label changes as exact integer deltas (full accumulation when `full`).
-__global__ void __launch_bounds__(LL_TB) k_lloyd_tiles(
+// Point-parallel Lloyd assignment through the exact candidate grid
+// (jb_grid.cuh): labels := nearest_center with the reference tie rule;
+// cluster sums follow the label changes as exact integer deltas (full
+// accumulation when `full`).
+__global__ void __launch_bounds__(LL_TB) k_lloyd_grid(
     const double2* __restrict__ spts, int64_t n, const double* __restrict__ centers, int k,
-    uint32_t* __restrict__ labs, int full, int Ex, int Ey, ClusterAcc acc,
+    CandGrid g, uint32_t* __restrict__ labs, int full, int Ex, int Ey, ClusterAcc acc,
     unsigned long long* __restrict__ changed, const int* __restrict__ skip_flag) {
     extern __shared__ unsigned char smem[];
     if (skip_flag && *skip_flag) return;  // empty clusters pending: host repairs first
@@ -590,7 +709,6 @@ __global__ void __launch_bounds__(LL_TB) k_lloyd_tiles(
     unsigned long long* s_sx = reinterpret_cast<unsigned long long*>(cy + k);
     unsigned long long* s_sy = s_sx + 2 * k;
     unsigned long long* s_cnt = s_sy + 2 * k;
-    uint16_t* s_cand = reinterpret_cast<uint16_t*>(s_cnt + k);
     __shared__ unsigned long long s_changed;
     for (int c = threadIdx.x; c < k; c += blockDim.x) {
         cx[c] = centers[2 * c];
@@ -601,93 +719,33 @@ __global__ void __launch_bounds__(LL_TB) k_lloyd_tiles(
     }
     if (threadIdx.x == 0) s_changed = 0;
     __syncthreads();
-    const int lane = threadIdx.x & 31;
-    uint16_t* cand = s_cand + (threadIdx.x >> 5) * k;
-    const unsigned lt = (1u << lane) - 1u;
     unsigned long long my_changed = 0;
-    const int64_t ntiles = (n + TILE - 1) / TILE;
-    for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < ntiles;
-         t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        double2 p[TILE / 32];
-        double x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY;
-#pragma unroll
-        for (int i = 0; i < TILE / 32; ++i) {
-            const int64_t r = t * TILE + i * 32 + lane;
-            if (r < n) {
-                p[i] = spts[r];
-                x0 = fmin(x0, p[i].x);
-                x1 = fmax(x1, p[i].x);
-                y0 = fmin(y0, p[i].y);
-                y1 = fmax(y1, p[i].y);
-            }
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            x0 = fmin(x0, __shfl_xor_sync(0xffffffffu, x0, o));
-            x1 = fmax(x1, __shfl_xor_sync(0xffffffffu, x1, o));
-            y0 = fmin(y0, __shfl_xor_sync(0xffffffffu, y0, o));
-            y1 = fmax(y1, __shfl_xor_sync(0xffffffffu, y1, o));
-        }
-        const double4 box = make_double4(x0, x1, y0, y1);
-        double M = INFINITY;
-        for (int c = lane; c < k; c += 32) {
-            double dmn, dmx;
-            box_d2(cx[c], cy[c], box, dmn, dmx);
-            M = fmin(M, dmx);
-        }
-        for (int o = 16; o > 0; o >>= 1) M = fmin(M, __shfl_xor_sync(0xffffffffu, M, o));
-        const double thr = M * (1.0 + kKeepMargin) + 1e-300;
-        int nc = 0;
-        for (int c0 = 0; c0 < k; c0 += 32) {
-            const int c = c0 + lane;
-            bool keep = false;
-            if (c < k) {
-                double dmn, dmx;
-                box_d2(cx[c], cy[c], box, dmn, dmx);
-                keep = dmn <= thr;
-            }
-            const unsigned m = __ballot_sync(0xffffffffu, keep);
-            if (keep) cand[nc + __popc(m & lt)] = (uint16_t)c;
-            nc += __popc(m);
-        }
-        __syncwarp();
-#pragma unroll
-        for (int i = 0; i < TILE / 32; ++i) {
-            const int64_t r = t * TILE + i * 32 + lane;
-            if (r >= n) break;
-            uint32_t best = cand[0];
-            double bd = dist2(p[i].x, p[i].y, cx[best], cy[best]);
-            for (int j = 1; j < nc; ++j) {
-                const int c = cand[j];
-                const double d = dist2(p[i].x, p[i].y, cx[c], cy[c]);
-                if (d < bd) {
-                    bd = d;
-                    best = (uint32_t)c;
-                }
-            }
-            if (full) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const double2 p = spts[r];
+        const uint32_t best = grid_nearest(g, p.x, p.y, cx, cy, k);
+        if (full) {
+            labs[r] = best;
+            fx_atomic_add(s_sx + 2 * best, fx_from_double(p.x, Ex));
+            fx_atomic_add(s_sy + 2 * best, fx_from_double(p.y, Ey));
+            atomicAdd(s_cnt + best, 1ULL);
+        } else {
+            const uint32_t old = labs[r];
+            if (old != best) {
                 labs[r] = best;
-                fx_atomic_add(s_sx + 2 * best, fx_from_double(p[i].x, Ex));
-                fx_atomic_add(s_sy + 2 * best, fx_from_double(p[i].y, Ey));
+                ++my_changed;
+                const i128 fx = fx_from_double(p.x, Ex), fy = fx_from_double(p.y, Ey);
+                fx_atomic_add(s_sx + 2 * best, fx);
+                fx_atomic_add(s_sy + 2 * best, fy);
                 atomicAdd(s_cnt + best, 1ULL);
-            } else {
-                const uint32_t old = labs[r];
-                if (old != best) {
-                    labs[r] = best;
-                    ++my_changed;
-                    const i128 fx = fx_from_double(p[i].x, Ex), fy = fx_from_double(p[i].y, Ey);
-                    fx_atomic_add(s_sx + 2 * best, fx);
-                    fx_atomic_add(s_sy + 2 * best, fy);
-                    atomicAdd(s_cnt + best, 1ULL);
-                    fx_atomic_add(s_sx + 2 * old, -fx);
-                    fx_atomic_add(s_sy + 2 * old, -fy);
-                    atomicAdd(s_cnt + old, ~0ULL);
-                }
+                fx_atomic_add(s_sx + 2 * old, -fx);
+                fx_atomic_add(s_sy + 2 * old, -fy);
+                atomicAdd(s_cnt + old, ~0ULL);
             }
         }
-        __syncwarp();
     }
     for (int o = 16; o > 0; o >>= 1) my_changed += __shfl_down_sync(0xffffffffu, my_changed, o);
-    if (lane == 0 && my_changed) atomicAdd(&s_changed, my_changed);
+    if ((threadIdx.x & 31) == 0 && my_changed) atomicAdd(&s_changed, my_changed);
     __syncthreads();
     for (int c = threadIdx.x; c < k; c += blockDim.x) {
         const i128 vx = fx_load(s_sx + 2 * c), vy = fx_load(s_sy + 2 * c);
@@ -841,24 +899,28 @@ struct LloydCtx {
     DArr<unsigned long long> flags;  // [0] changed
     DArr<int> empties;             // k + 1 (last = count)
     DArr<unsigned long long> far_blk;
+    CandGrid cg;
+    DArr<uint16_t> cg_cnt, cg_cand;
     ClusterAcc cacc() { return ClusterAcc{acc.p, acc.p + 2 * k, acc.p + 4 * k}; }
-    size_t smem() const {
-        return sizeof(double) * 2 * k + sizeof(unsigned long long) * 5 * k +
-               sizeof(uint16_t) * LL_WARPS * k;
-    }
+    size_t smem() const { return sizeof(double) * 2 * k + sizeof(unsigned long long) * 5 * k; }
     int grid() const {
-        const int64_t ntiles = (n + TILE - 1) / TILE;
-        return (int)std::max<int64_t>(
-            1, std::min<int64_t>((ntiles + LL_WARPS - 1) / LL_WARPS, (int64_t)kSMs * 4));
+        return (int)std::max<int64_t>(1, std::min<int64_t>((n + LL_TB - 1) / LL_TB,
+                                                           (int64_t)kSMs * 6));
     }
 };
 
 void lloyd_assign(LloydCtx& L, bool full, bool gate_on_empties) {
     JB_CUDA(cudaMemsetAsync(L.flags.p, 0, 8, L.st));
+    {
+        JB_PROF("lloyd_grid", L.st);
+        const int ncell = L.cg.G * L.cg.G;
+        k_grid_build<<<std::min(ncell / 8, kSMs * 16), 256, 0, L.st>>>(L.cg, L.centers.p, L.k);
+    }
+    JB_LAUNCH_CHECK();
     JB_PROF("lloyd_assign", L.st);
-    k_lloyd_tiles<<<L.grid(), LL_TB, L.smem(), L.st>>>(
-        L.spts, L.n, L.centers.p, L.k, L.labs.p, full ? 1 : 0, L.Ex, L.Ey, L.cacc(), L.flags.p,
-        gate_on_empties ? L.empties.p + L.k : nullptr);
+    k_lloyd_grid<<<L.grid(), LL_TB, L.smem(), L.st>>>(
+        L.spts, L.n, L.centers.p, L.k, L.cg, L.labs.p, full ? 1 : 0, L.Ex, L.Ey, L.cacc(),
+        L.flags.p, gate_on_empties ? L.empties.p + L.k : nullptr);
     JB_LAUNCH_CHECK();
 }
 
@@ -955,7 +1017,15 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
     L.flags.alloc(1, st);
     L.empties.alloc(k + 1, st);
     L.empties.zero();
-    JB_CUDA(cudaFuncSetAttribute(k_lloyd_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    {
+        const int G = grid_side_for(k), cap = 32;
+        L.cg = make_grid_desc(bb.xmin, bb.xmax, bb.ymin, bb.ymax, G, cap);
+        L.cg_cnt.alloc((size_t)G * G, st);
+        L.cg_cand.alloc((size_t)G * G * cap, st);
+        L.cg.cnt = L.cg_cnt.p;
+        L.cg.cand = L.cg_cand.p;
+    }
+    JB_CUDA(cudaFuncSetAttribute(k_lloyd_grid, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)L.smem()));
 
     const int nblocks = (int)((n + D2_R - 1) / D2_R);

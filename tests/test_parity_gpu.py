@@ -183,3 +183,23 @@ def test_reference_api_round_trip(engine):
         assert abs(inc_rec - inc_orig) <= 1e-9 * max(1.0, abs(inc_orig))
         toks = fit.symbolic.tokens(0)
         assert all(cb.index_of(t) == l for t, l in zip(toks, fit.symbolic.series[0].labels))
+
+
+# ---------------------------------------------------------------------------
+# RNG building blocks against the reference's std::mt19937_64 use
+
+def test_device_engine_matches_libstdcxx(engine, oracle):
+    """Multi-CTA jump-ahead engine == sequential std::mt19937_64 (restated by
+    the oracle, pinned against libstdc++ in the CPU suite), across chunk
+    boundaries (B = 2^22 draws per CTA)."""
+    count = 3 * (1 << 22) + 1234
+    for seed in (0, 12345):
+        dev = engine.mt19937_64_stream(seed, count)
+        ref = oracle.mt_stream(seed, count)
+        assert np.array_equal(dev, ref)
+
+
+@pytest.mark.parametrize("n,s,seed", [(1000, 1000, 3), (50000, 7000, 0), (9_000_000, 2_000_000, 5)])
+def test_device_sample_indices(engine, oracle, n, s, seed):
+    """detail::sample_indices (clustering.hpp:74-85) resolved on device."""
+    assert np.array_equal(engine.sample_indices(n, s, seed), oracle.sample_indices(n, s, seed))
