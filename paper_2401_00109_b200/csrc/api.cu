@@ -76,6 +76,23 @@ void prof_end(cudaStream_t st) {
 
 using namespace jb::prof_detail;
 
+namespace jb {
+void trace_mark(const char* what, cudaStream_t st) {
+    static const bool on = [] {
+        const char* e = getenv("JB_TRACE");
+        return e && *e == '1';
+    }();
+    if (!on) return;
+    static thread_local std::chrono::steady_clock::time_point last =
+        std::chrono::steady_clock::now();
+    cudaStreamSynchronize(st);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[jb] %-28s %9.3f ms\n", what,
+            std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
+}
+}  // namespace jb
+
 namespace {
 
 void prof_collect() {
@@ -302,6 +319,7 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
     seg.steps.alloc(n_seg, st);
     seg.first.upload(seg_first, n_seg);
     seg.steps.upload(seg_steps, n_seg);
+    JB_TRACE("fit: start", st);
     DArr<double> dvals;
     const double* d_values = values;
     if (!on_device) {
@@ -311,7 +329,9 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
     }
 
     // ---- compression ----
+    JB_TRACE("fit: values on device", st);
     compress_segments(d_values, seg, c.tol, c.max_piece_len, fit->pieces, st, &fit->fix_rounds);
+    JB_TRACE("fit: compressed", st);
     fit->anchors.alloc(n_seg, st);
     k_gather_anchors<<<(int)((n_seg + 255) / 256), 256, 0, st>>>(d_values, seg.first.p, n_seg,
                                                                  fit->anchors.p);
@@ -325,6 +345,7 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
     const int64_t N = fit->pieces.N;
     Scaled sc;
     scale_pieces(fit->pieces, seg.total_steps, c.scl, sc, st);
+    JB_TRACE("fit: scaled", st);
     fit->scaling[0] = sc.scl;
     fit->scaling[1] = sc.sigma_len;
     fit->scaling[2] = sc.sigma_inc;
@@ -367,7 +388,9 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
             DArr<uint64_t> raw;
             const uint64_t raw_count = S + (c.k + 1) * c.n_init + 4096;
             mt19937_64_generate(c.seed, raw_count, raw, st);
+            JB_TRACE("svq: engine draws", st);
             uint64_t cursor = sample_indices_device((uint64_t)N, S, raw.p, raw_count, sample, st);
+            JB_TRACE("svq: sample indices", st);
             KMeansOut km;
             lloyd_best_device(sc.pts.p, sample.p, (int64_t)S, c.k, c.max_iters, c.n_init, raw.p,
                               raw_count, &cursor, bb, km, st);
@@ -407,6 +430,7 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
         default:
             throw Error(INVALID_INPUT, "unknown backend");
     }
+    JB_TRACE("fit: backend", st);
     fit->phase_ms[2] = ms_since(t2);
 
     // ---- group statistics, ranking, codebook (digitization.hpp:217-291) ----
@@ -458,6 +482,7 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
     fit->d_centers.upload(fit->centers.data(), 2 * k);
     fit->d_mean_lengths.upload(fit->mean_lengths.data(), k);
     JB_CUDA(cudaStreamSynchronize(st));
+    JB_TRACE("fit: stats+codebook", st);
     fit->phase_ms[3] = ms_since(t3);
     fit->phase_ms[4] = ms_since(t_start);
 }

@@ -130,6 +130,7 @@ void scale_pieces(const Pieces& pc, int64_t total_steps, double scl, Scaled& out
         k_sum_inc<<<grid_for(N), kTB, 0, st>>>(pc.inc.p, N, Einc, acc.p);
     }
     JB_LAUNCH_CHECK();
+    JB_TRACE("scale: sum inc", st);
     unsigned long long h[6];
     acc.download(h, 2);
     JB_CUDA(cudaStreamSynchronize(st));
@@ -160,7 +161,9 @@ void scale_pieces(const Pieces& pc, int64_t total_steps, double scl, Scaled& out
     out.sigma_len = sl;
     out.sigma_inc = si;
 
+    JB_TRACE("scale: variances", st);
     out.pts.alloc(2 * N, st);
+    JB_TRACE("scale: alloc points", st);
     DArr<unsigned long long> bb(4, st);
     unsigned long long init[4] = {~0ULL, 0ULL, ~0ULL, 0ULL};
     bb.upload(init, 4);

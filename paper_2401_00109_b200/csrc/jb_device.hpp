@@ -77,6 +77,10 @@ struct ProfScope {
     ProfScope(const char* name, cudaStream_t s) : st(s) { prof_begin(name, s); }
     ~ProfScope() { prof_end(st); }
 };
+// host-side phase trace (env JB_TRACE=1): prints ms since the previous mark
+void trace_mark(const char* what, cudaStream_t st);
+#define JB_TRACE(what, st) ::jb::trace_mark(what, st)
+
 #define JB_CAT2(a, b) a##b
 #define JB_CAT(a, b) JB_CAT2(a, b)
 #define JB_PROF(name, st) ::jb::ProfScope JB_CAT(jb_prof_scope_, __LINE__)(name, st)

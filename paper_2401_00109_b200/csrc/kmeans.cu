@@ -995,6 +995,7 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
         k_sorted_gather<<<grid_cap(n), 256, 0, st>>>(pts, d_idx, orig.p, n, spts.p, pos.p);
         JB_LAUNCH_CHECK();
     }
+    JB_TRACE("kmeans: morton order", st);
     const int64_t ntiles = (n + TILE - 1) / TILE;
     DArr<double4> tbox(ntiles, st);
     DArr<double> tmax(ntiles, st);
@@ -1068,6 +1069,7 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
         JB_CUDA(cudaStreamSynchronize(st));
         if (h.cursor > raw_count) throw Error(INTERNAL, "rng stream exhausted");
         *cursor = h.cursor;
+        JB_TRACE("kmeans: d2 seeding", st);
 
         // ---- Lloyd (lloyd_once :200-220) ----
         L.acc.zero();
@@ -1094,6 +1096,7 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
             }
         }
         lloyd_update_means_sync(L);
+        JB_TRACE("kmeans: lloyd", st);
         double sse = 0.0;
         if (n_init > 1) {
             DArr<unsigned long long> sacc(2, st);
