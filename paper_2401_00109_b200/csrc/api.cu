@@ -77,6 +77,65 @@ void prof_end(cudaStream_t st) {
 using namespace jb::prof_detail;
 
 namespace jb {
+namespace cache_detail {
+std::mutex g_mu;
+std::map<std::pair<cudaStream_t, size_t>, std::vector<void*>> g_free;
+
+size_t bucket(size_t bytes) {
+    if (bytes <= 256) return 256;
+    if (bytes < (1u << 20)) {
+        size_t b = 256;
+        while (b < bytes) b <<= 1;
+        return b;
+    }
+    return (bytes + (1u << 20) - 1) & ~(size_t)((1u << 20) - 1);
+}
+}  // namespace cache_detail
+
+void* dev_alloc(size_t bytes, cudaStream_t st) {
+    using namespace cache_detail;
+    const size_t b = bucket(bytes);
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        auto it = g_free.find({st, b});
+        if (it != g_free.end() && !it->second.empty()) {
+            void* p = it->second.back();
+            it->second.pop_back();
+            return p;
+        }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, b, st);
+    if (e == cudaErrorMemoryAllocation) {  // trim this stream's cache and retry once
+        cudaGetLastError();
+        dev_cache_drop(st);
+        e = cudaMallocAsync(&p, b, st);
+    }
+    if (e != cudaSuccess)
+        throw Error(CUDA_ERROR, std::string("device allocation of ") + std::to_string(b) +
+                                    " bytes: " + cudaGetErrorString(e));
+    return p;
+}
+
+void dev_free(void* p, size_t bytes, cudaStream_t st) {
+    using namespace cache_detail;
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_free[{st, bucket(bytes)}].push_back(p);
+}
+
+void dev_cache_drop(cudaStream_t st) {
+    using namespace cache_detail;
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (auto it = g_free.begin(); it != g_free.end();) {
+        if (it->first.first == st) {
+            for (void* p : it->second) cudaFreeAsync(p, st);
+            it = g_free.erase(it);
+        } else {
+            ++it;
+        }
+    }
+}
+
 void trace_mark(const char* what, cudaStream_t st) {
     static const bool on = [] {
         const char* e = getenv("JB_TRACE");
@@ -546,7 +605,10 @@ void jb_context_destroy(jb_context* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    cudaStreamDestroy(ctx->stream);
+    jb::dev_cache_drop(ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+    // buffers of fits that outlive the context stay valid (the stream handle
+    // is not destroyed: a jb_fit still references it)
     delete ctx;
 }
 

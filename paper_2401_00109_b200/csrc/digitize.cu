@@ -224,21 +224,38 @@ __global__ void k_assign_stats(const double2* __restrict__ pts, const int32_t* _
     unsigned long long* t_len = privatize ? s_len : g.lens;
     unsigned long long* t_sx = privatize ? s_sx : g.sx;
     unsigned long long* t_sy = privatize ? s_sy : g.sy;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const double2 p = pts[i];
-        uint32_t lab;
-        if (do_assign) {
-            lab = grid_nearest(cg, p.x, p.y, cx, cy, k);
-            labels[i] = lab;
-        } else {
-            lab = labels[i];
+    constexpr int U = 4;  // points in flight per thread
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * U;
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x * U + threadIdx.x; base < n;
+         base += stride) {
+        double2 pp[U];
+        int32_t ll[U];
+        uint32_t lb[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = base + (int64_t)u * blockDim.x;
+            if (i < n) {
+                pp[u] = pts[i];
+                ll[u] = len[i];
+                lb[u] = do_assign ? 0u : labels[i];
+            }
         }
-        atomicAdd(t_cnt + lab, 1ULL);
-        atomicMin(t_first + lab, (unsigned long long)i);
-        atomicAdd(t_len + lab, (unsigned long long)len[i]);
-        fx_atomic_add(t_sx + 2 * lab, fx_from_double(p.x, Ex));
-        fx_atomic_add(t_sy + 2 * lab, fx_from_double(p.y, Ey));
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = base + (int64_t)u * blockDim.x;
+            if (i >= n) break;
+            const double2 p = pp[u];
+            uint32_t lab = lb[u];
+            if (do_assign) {
+                lab = grid_nearest(cg, p.x, p.y, cx, cy, k);
+                labels[i] = lab;
+            }
+            atomicAdd(t_cnt + lab, 1ULL);
+            if ((unsigned long long)i < t_first[lab]) atomicMin(t_first + lab, (unsigned long long)i);
+            atomicAdd(t_len + lab, (unsigned long long)ll[u]);
+            fx_atomic_add(t_sx + 2 * lab, fx_from_double(p.x, Ex));
+            fx_atomic_add(t_sy + 2 * lab, fx_from_double(p.y, Ey));
+        }
     }
     if (!privatize) return;
     __syncthreads();

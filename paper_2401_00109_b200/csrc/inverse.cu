@@ -60,13 +60,18 @@ __global__ void __launch_bounds__(INV_TB) k_inv_warp(InverseIn in, const double*
             const double l = valid ? __ldg(rlen + lab) : 0.0;
             const int cnt = (int)((b - base) < 32 ? (b - base) : 32);
             int myr = 0;
-            for (int i = 0; i < cnt; ++i) {
+            // fully unrolled (cnt is warp-uniform): the 32 broadcasts are
+            // independent of the carry, so only the rounding chain is serial
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
                 const double li = __shfl_sync(FULL, l, i);
-                const double x = li + carry;
-                long long r = llround(x);
-                if (r < 1) r = 1;
-                carry = x - (double)r;
-                if (lane == i) myr = (int)r;
+                if (i < cnt) {
+                    const double x = li + carry;
+                    long long r = llround(x);
+                    if (r < 1) r = 1;
+                    carry = x - (double)r;
+                    if (lane == i) myr = (int)r;
+                }
             }
             if (valid) qlen[j] = myr;
             long long t = myr;
@@ -107,9 +112,13 @@ __global__ void __launch_bounds__(INV_TB) k_inv_warp(InverseIn in, const double*
             const double inc = valid ? __ldg(rinc + lab) : 0.0;
             const int cnt = (int)((b - base) < 32 ? (b - base) : 32);
             double myv = 0.0;
-            for (int i = 0; i < cnt; ++i) {  // v += p.inc, sequential as the reference
-                if (lane == i) myv = v;
-                v += __shfl_sync(FULL, inc, i);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {  // v += p.inc, sequential as the reference
+                const double ii = __shfl_sync(FULL, inc, i);
+                if (i < cnt) {
+                    if (lane == i) myv = v;
+                    v += ii;
+                }
             }
             // inclusive scan of lengths (exact integers)
             long long incl = len;

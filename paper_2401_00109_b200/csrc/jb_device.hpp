@@ -12,8 +12,15 @@
 
 namespace jb {
 
-// Move-only device array allocated from the stream-ordered pool
-// (cudaMallocAsync): buffers are recycled across fits without device syncs.
+// Per-stream, size-bucketed cache of device buffers (api.cu). Buffers freed
+// on a stream are reused only by later work on the same stream, so reuse is
+// stream-ordered and needs no sync; repeated fits of the same shape never
+// touch the allocator (a cudaMallocAsync pool growth of 14 GB costs ~1 s).
+void* dev_alloc(size_t bytes, cudaStream_t st);
+void dev_free(void* p, size_t bytes, cudaStream_t st);
+void dev_cache_drop(cudaStream_t st);  // release everything cached for st
+
+// Move-only device array over dev_alloc/dev_free.
 template <class T>
 struct DArr {
     T* p = nullptr;
@@ -40,10 +47,10 @@ struct DArr {
         release();
         s = st;
         n = count;
-        if (count) JB_CUDA(cudaMallocAsync((void**)&p, sizeof(T) * count, st));
+        if (count) p = static_cast<T*>(dev_alloc(sizeof(T) * count, st));
     }
     void release() {
-        if (p) cudaFreeAsync(p, s);
+        if (p) dev_free(p, sizeof(T) * n, s);
         p = nullptr;
         n = 0;
     }

@@ -720,27 +720,40 @@ __global__ void __launch_bounds__(LL_TB) k_lloyd_grid(
     if (threadIdx.x == 0) s_changed = 0;
     __syncthreads();
     unsigned long long my_changed = 0;
-    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
-         r += (int64_t)gridDim.x * blockDim.x) {
-        const double2 p = spts[r];
-        const uint32_t best = grid_nearest(g, p.x, p.y, cx, cy, k);
-        if (full) {
-            labs[r] = best;
-            fx_atomic_add(s_sx + 2 * best, fx_from_double(p.x, Ex));
-            fx_atomic_add(s_sy + 2 * best, fx_from_double(p.y, Ey));
-            atomicAdd(s_cnt + best, 1ULL);
-        } else {
-            const uint32_t old = labs[r];
-            if (old != best) {
+    constexpr int U = 4;  // points in flight per thread (memory-level parallelism)
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * U;
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x * U + threadIdx.x; base < n;
+         base += stride) {
+        double2 p[U];
+        uint32_t old[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t r = base + (int64_t)u * blockDim.x;
+            if (r < n) {
+                p[u] = spts[r];
+                old[u] = full ? 0u : labs[r];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t r = base + (int64_t)u * blockDim.x;
+            if (r >= n) break;
+            const uint32_t best = grid_nearest(g, p[u].x, p[u].y, cx, cy, k);
+            if (full) {
+                labs[r] = best;
+                fx_atomic_add(s_sx + 2 * best, fx_from_double(p[u].x, Ex));
+                fx_atomic_add(s_sy + 2 * best, fx_from_double(p[u].y, Ey));
+                atomicAdd(s_cnt + best, 1ULL);
+            } else if (old[u] != best) {
                 labs[r] = best;
                 ++my_changed;
-                const i128 fx = fx_from_double(p.x, Ex), fy = fx_from_double(p.y, Ey);
+                const i128 fx = fx_from_double(p[u].x, Ex), fy = fx_from_double(p[u].y, Ey);
                 fx_atomic_add(s_sx + 2 * best, fx);
                 fx_atomic_add(s_sy + 2 * best, fy);
                 atomicAdd(s_cnt + best, 1ULL);
-                fx_atomic_add(s_sx + 2 * old, -fx);
-                fx_atomic_add(s_sy + 2 * old, -fy);
-                atomicAdd(s_cnt + old, ~0ULL);
+                fx_atomic_add(s_sx + 2 * old[u], -fx);
+                fx_atomic_add(s_sy + 2 * old[u], -fy);
+                atomicAdd(s_cnt + old[u], ~0ULL);
             }
         }
     }

@@ -203,3 +203,17 @@ def test_device_engine_matches_libstdcxx(engine, oracle):
 def test_device_sample_indices(engine, oracle, n, s, seed):
     """detail::sample_indices (clustering.hpp:74-85) resolved on device."""
     assert np.array_equal(engine.sample_indices(n, s, seed), oracle.sample_indices(n, s, seed))
+
+
+def test_cpp_facade_against_reference_api():
+    """The reference's own C++ entry points (jabba::jabba_fit / reconstruct,
+    unmodified headers) and the drop-in C++ facade (include/jabba_b200.hpp)
+    run side by side on the reference suite's generators: oracle/facade_parity."""
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle",
+                       "_ref", "facade_parity")
+    if not os.path.exists(exe):
+        pytest.skip("facade_parity not built (needs the reference tree at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
