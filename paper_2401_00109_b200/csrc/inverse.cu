@@ -1,19 +1,11 @@
 // inverse.cu — inverse symbolization on sm_100a (inverse.hpp:32-132,
 // compression.hpp:87-103, 198-213).
 //
-// One warp per segment. The recurrences of the reference are sequential and
-// are kept sequential -- every lane replays the same chain on values
-// broadcast by shuffles, so the rounding is the reference's exactly -- while
-// all memory traffic is warp-coalesced:
-//   pass 1  labels -> real lengths (inverse_digitize_series :32-51, per-label
-//           table) -> error-carrying rounding with clamp (quantize_lengths
-//           :63-74) -> int32 lengths, then the backward fix-up
-//           (match_total_length :81-93);
-//   pass 2  running start value v += inc (inverse_compress :94-101) and an
-//           exact integer scan of the lengths give every piece its start
-//           value and output position; the warp then writes the group's
-//           samples v + inc * (i / len) contiguously, straight into the
-//           (optionally stitched, :198-213) output.
+// The reference's recurrences are sequential and stay sequential: one
+// thread per segment runs the carry / length-fix-up / start-value chains in
+// the reference's rounding (all segments are resident in one wave), then a
+// piece-parallel fill writes the interpolated samples v + inc * (i / len)
+// straight into the (optionally stitched, :198-213) output.
 #include <algorithm>
 
 #include "jb_device.hpp"
@@ -33,124 +25,122 @@ __global__ void k_inv_tables(const double* __restrict__ centers,
     }
 }
 
-constexpr int INV_TB = 256;
+// llround (round half away from zero) of x, as a double, using only exact
+// fp64 operations: trunc, the exact remainder x - trunc(x), one compare.
+__device__ __forceinline__ double llround_d(double x) {
+    double r = trunc(x);
+    const double f = x - r;  // exact
+    if (f >= 0.5) r += 1.0;
+    else if (f <= -0.5) r -= 1.0;
+    return r;
+}
 
-__global__ void __launch_bounds__(INV_TB) k_inv_warp(InverseIn in, const double* __restrict__ rlen,
-                                                    const double* __restrict__ rinc,
-                                                    int32_t* __restrict__ qlen,
-                                                    double* __restrict__ out,
-                                                    unsigned long long* __restrict__ err) {
-    const int lane = threadIdx.x & 31;
-    const unsigned FULL = 0xffffffffu;
-    for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; s < in.n_seg;
-         s += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        const int64_t a = in.seg_offsets[s], b = in.seg_offsets[s + 1];
-        // ---- pass 1: quantize ----
-        double carry = 0.0;
-        long long total = 0;
-        bool bad = false;
-        for (int64_t base = a; base < b; base += 32) {
-            const int64_t j = base + lane;
-            const bool valid = j < b;
-            const uint32_t lab = valid ? in.labels[j] : 0u;
-            if (__any_sync(FULL, valid && (uint64_t)lab >= in.k)) {
-                bad = true;
-                break;
-            }
-            const double l = valid ? __ldg(rlen + lab) : 0.0;
-            const int cnt = (int)((b - base) < 32 ? (b - base) : 32);
-            int myr = 0;
-            // fully unrolled (cnt is warp-uniform): the 32 broadcasts are
-            // independent of the carry, so only the rounding chain is serial
+constexpr int64_t SKIP_LAST = 1LL << 62;  // flag: don't write this piece's last sample
+
+// One thread per segment: the reference's sequential recurrences, exactly.
+//   quantize_lengths (:63-74): r = llround(l + carry), clamp >= 1,
+//     carry = (l + carry) - r  -- r kept as an exact double, so the carry
+//     chain has no int<->fp conversions;
+//   match_total_length (:81-93): backward cascade on the tail;
+//   inverse_compress (:94-101): v += inc (start value of every piece) and
+//     the running output position.
+// The three chains are independent and run interleaved in one loop.
+__global__ void __launch_bounds__(128) k_inv_chain(InverseIn in, const double* __restrict__ rlen,
+                                                   const double* __restrict__ rinc,
+                                                   int32_t* __restrict__ qlen,
+                                                   double* __restrict__ vstart,
+                                                   int64_t* __restrict__ pstart,
+                                                   double* __restrict__ out,
+                                                   unsigned long long* __restrict__ err) {
+    const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (s >= in.n_seg) return;
+    const int64_t a = in.seg_offsets[s], b = in.seg_offsets[s + 1];
+    for (int64_t j = a; j < b; ++j)  // inverse_digitize_series validates first (:41-44)
+        if ((uint64_t)in.labels[j] >= in.k) {
+            atomicMin(err, (unsigned long long)(s * 16 + UNKNOWN_SYMBOL));
+            return;
+        }
+    const bool drop_last = in.layout == 0 && s + 1 < in.n_seg;  // stitch_partitions
+    const int64_t base = in.out_offsets[s];
+    double carry = 0.0, v = in.anchors[s];
+    int64_t pos = base, total = 0;
+    out[base] = v;
+    int64_t j = a;
+    constexpr int U = 4;
+    for (; j + U <= b; j += U) {
+        uint32_t lab[U];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const double li = __shfl_sync(FULL, l, i);
-                if (i < cnt) {
-                    const double x = li + carry;
-                    long long r = llround(x);
-                    if (r < 1) r = 1;
-                    carry = x - (double)r;
-                    if (lane == i) myr = (int)r;
-                }
-            }
-            if (valid) qlen[j] = myr;
-            long long t = myr;
-            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(FULL, t, o);
-            total += t;
-        }
-        if (bad) {
-            if (lane == 0) atomicMin(err, (unsigned long long)(s * 16 + UNKNOWN_SYMBOL));
-            continue;
-        }
-        // ---- match_total_length (backward cascade, almost always 1 piece) ----
-        __syncwarp();
-        int ok = 1;
-        if (lane == 0) {
-            long long residual = in.source_lengths[s] - total;
-            for (int64_t j = b; j-- > a && residual != 0;) {
-                long long adj = (long long)qlen[j] + residual;
-                if (adj < 1) adj = 1;
-                residual -= adj - qlen[j];
-                qlen[j] = (int32_t)adj;
-            }
-            ok = (residual == 0 && b > a) ? 1 : 0;
-            if (!ok) atomicMin(err, (unsigned long long)(s * 16 + INVALID_PIECE));
-        }
-        ok = __shfl_sync(FULL, ok, 0);
-        if (!ok) continue;
-        __syncwarp();
-        // ---- pass 2: start values, positions, interpolation fill ----
-        const bool drop_last = in.layout == 0 && s + 1 < in.n_seg;  // stitch_partitions
-        int64_t pos = in.out_offsets[s];
-        double v = in.anchors[s];
-        if (lane == 0) out[pos] = v;
-        for (int64_t base = a; base < b; base += 32) {
-            const int64_t j = base + lane;
-            const bool valid = j < b;
-            const uint32_t lab = valid ? in.labels[j] : 0u;
-            const int len = valid ? qlen[j] : 0;
-            const double inc = valid ? __ldg(rinc + lab) : 0.0;
-            const int cnt = (int)((b - base) < 32 ? (b - base) : 32);
-            double myv = 0.0;
+        for (int u = 0; u < U; ++u) lab[u] = in.labels[j + u];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {  // v += p.inc, sequential as the reference
-                const double ii = __shfl_sync(FULL, inc, i);
-                if (i < cnt) {
-                    if (lane == i) myv = v;
-                    v += ii;
-                }
-            }
-            // inclusive scan of lengths (exact integers)
-            long long incl = len;
-            for (int o = 1; o < 32; o <<= 1) {
-                const long long y = __shfl_up_sync(FULL, incl, o);
-                if (lane >= o) incl += y;
-            }
-            const long long L = __shfl_sync(FULL, incl, 31);
-            const bool last_group = base + 32 >= b;
-            for (long long q0 = 1; q0 <= L; q0 += 32) {
-                const long long q = q0 + lane;  // 1-based sample within the group
-                // piece lo with excl_lo < q <= incl_lo: fixed 5-step search so
-                // every lane executes the same full-mask shuffles
-                int last_below = -1;  // last piece with incl < q
-                for (int step = 16; step > 0; step >>= 1) {
-                    const int t = last_below + step;
-                    const long long cm = __shfl_sync(FULL, incl, t < 31 ? t : 31);
-                    if (t < cnt && cm < q) last_below = t;
-                }
-                const int lo = last_below + 1 < 32 ? last_below + 1 : 31;
-                const long long ci = __shfl_sync(FULL, incl, lo);
-                const int li = __shfl_sync(FULL, len, lo);
-                const double vi = __shfl_sync(FULL, myv, lo);
-                const double ii = __shfl_sync(FULL, inc, lo);
-                if (q <= L) {
-                    const long long i = q - (ci - li);  // 1..len within piece lo
-                    const bool skip = drop_last && last_group && q == L;
-                    if (!skip) out[pos + q] = vi + ii * ((double)i / (double)li);
-                }
-            }
-            pos += L;
+        for (int u = 0; u < U; ++u) {
+            const double l = __ldg(rlen + lab[u]);
+            const double x = l + carry;
+            double r = llround_d(x);
+            if (r < 1.0) r = 1.0;
+            carry = x - r;
+            const int32_t q = (int32_t)r;
+            qlen[j + u] = q;
+            vstart[j + u] = v;
+            pstart[j + u] = pos;
+            v += __ldg(rinc + lab[u]);
+            pos += q;
+            total += q;
         }
+    }
+    for (; j < b; ++j) {
+        const uint32_t lab = in.labels[j];
+        const double l = __ldg(rlen + lab);
+        const double x = l + carry;
+        double r = llround_d(x);
+        if (r < 1.0) r = 1.0;
+        carry = x - r;
+        const int32_t q = (int32_t)r;
+        qlen[j] = q;
+        vstart[j] = v;
+        pstart[j] = pos;
+        v += __ldg(rinc + lab);
+        pos += q;
+        total += q;
+    }
+    // match_total_length: backward cascade; positions after the first
+    // modified piece are recomputed
+    long long residual = in.source_lengths[s] - total;
+    int64_t first_mod = b;
+    for (int64_t t = b; t-- > a && residual != 0;) {
+        long long adj = (long long)qlen[t] + residual;
+        if (adj < 1) adj = 1;
+        residual -= adj - qlen[t];
+        qlen[t] = (int32_t)adj;
+        first_mod = t;
+    }
+    if (residual != 0 || b == a) {
+        atomicMin(err, (unsigned long long)(s * 16 + INVALID_PIECE));
+        return;
+    }
+    if (first_mod < b) {
+        int64_t p = pstart[first_mod];
+        for (int64_t t = first_mod; t < b; ++t) {
+            pstart[t] = p;
+            p += qlen[t];
+        }
+    }
+    if (drop_last) pstart[b - 1] |= SKIP_LAST;
+}
+
+// interpolation fill (inverse_compress :97-99): v + inc * (i / len)
+__global__ void k_inv_fill(InverseIn in, const double* __restrict__ rinc,
+                           const int32_t* __restrict__ qlen, const double* __restrict__ vstart,
+                           const int64_t* __restrict__ pstart, double* __restrict__ out) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < in.N;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t len = qlen[j];
+        const int64_t ps = pstart[j];
+        const int64_t p0 = ps & ~SKIP_LAST;
+        const int64_t n_write = (ps & SKIP_LAST) ? len - 1 : len;
+        const double v = vstart[j];
+        const double inc = __ldg(rinc + in.labels[j]);
+        const double l = (double)len;
+        for (int64_t i = 1; i <= n_write; ++i) out[p0 + i] = v + inc * ((double)i / l);
     }
 }
 
@@ -171,11 +161,12 @@ void inverse_transform_device(const InverseIn& in, double* d_out, cudaStream_t s
             tab.p + kk);
         JB_LAUNCH_CHECK();
     }
+    DArr<double> vstart(std::max<int64_t>(in.N, 1), st);
+    DArr<int64_t> pstart(std::max<int64_t>(in.N, 1), st);
     {
-        JB_PROF("inverse_warp", st);
-        const int grid = (int)std::max<int64_t>(
-            1, std::min<int64_t>((in.n_seg * 32 + INV_TB - 1) / INV_TB, (int64_t)kSMs * 16));
-        k_inv_warp<<<grid, INV_TB, 0, st>>>(in, tab.p, tab.p + kk, qlen.p, d_out, err.p);
+        JB_PROF("inverse_chain", st);
+        k_inv_chain<<<(int)((in.n_seg + 127) / 128), 128, 0, st>>>(
+            in, tab.p, tab.p + kk, qlen.p, vstart.p, pstart.p, d_out, err.p);
     }
     JB_LAUNCH_CHECK();
     unsigned long long e;
@@ -190,6 +181,13 @@ void inverse_transform_device(const InverseIn& in, double* d_out, cudaStream_t s
                             " (segment " + std::to_string(seg) + ")");
         throw Error(INVALID_PIECE, "cannot fit pieces into the segment's steps (segment " +
                                        std::to_string(seg) + ")");
+    }
+    if (in.N > 0) {
+        JB_PROF("inverse_fill", st);
+        const int grid =
+            (int)std::max<int64_t>(1, std::min<int64_t>((in.N + 255) / 256, (int64_t)kSMs * 16));
+        k_inv_fill<<<grid, 256, 0, st>>>(in, tab.p + kk, qlen.p, vstart.p, pstart.p, d_out);
+        JB_LAUNCH_CHECK();
     }
 }
 

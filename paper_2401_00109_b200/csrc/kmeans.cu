@@ -694,16 +694,94 @@ struct ClusterAcc {
 
 constexpr int LL_TB = 256;
 
-// Point-parallel Lloyd assignment through the exact candidate grid
-// (jb_grid.cuh): labels := nearest_center with the reference tie rule;
-// cluster sums follow the label changes as exact integer deltas (full
-// accumulation when `full`).
-__global__ void __launch_bounds__(LL_TB) k_lloyd_grid(
+// ---- tile-level skipping --------------------------------------------------
+// A tile (TILE consecutive Morton-ordered points, box tbox[t]) is SINGLE with
+// center c when c is the only possible reference argmin for every point of
+// the box: the union of the candidate lists of the grid cells covering the
+// box is pruned again with the tile's own (much smaller) box by the same
+// min-max argument (jb_grid.cuh); the survivors are a superset of the
+// argmins, so one survivor decides every label. A tile that is SINGLE with
+// the same center as when it was last processed holds that label on every
+// point already: it is skipped without reading its points.
+constexpr uint32_t MIXED = 0xFFFFFFFFu;
+
+__global__ void k_tile_check(const double4* __restrict__ tbox, int64_t ntiles, CandGrid g,
+                             const double* __restrict__ centers,
+                             const uint32_t* __restrict__ tlab, uint32_t* __restrict__ tnew,
+                             uint32_t* __restrict__ work, unsigned long long* __restrict__ nwork,
+                             const int* __restrict__ skip_flag, int force_all) {
+    if (skip_flag && *skip_flag) return;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntiles;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const double4 b = tbox[t];  // (x0, x1, y0, y1)
+        int ix0 = (int)((b.x - g.x0) * g.invw), ix1 = (int)((b.y - g.x0) * g.invw);
+        int iy0 = (int)((b.z - g.y0) * g.invh), iy1 = (int)((b.w - g.y0) * g.invh);
+        ix0 = min(max(ix0, 0), g.G - 1);
+        ix1 = min(max(ix1, 0), g.G - 1);
+        iy0 = min(max(iy0, 0), g.G - 1);
+        iy1 = min(max(iy1, 0), g.G - 1);
+        uint32_t single = MIXED;
+        if ((ix1 - ix0 + 1) * (iy1 - iy0 + 1) <= 4) {
+            bool ok = true;
+            double M = INFINITY;
+            for (int iy = iy0; iy <= iy1 && ok; ++iy)
+                for (int ix = ix0; ix <= ix1 && ok; ++ix) {
+                    const int cell = iy * g.G + ix;
+                    const int n = __ldg(g.cnt + cell);
+                    if (n == 0xFFFF) {
+                        ok = false;
+                        break;
+                    }
+                    const uint16_t* cl = g.cand + (size_t)cell * g.cap;
+                    for (int j = 0; j < n; ++j) {
+                        const int c = __ldg(cl + j);
+                        double dmn, dmx;
+                        box_d2(__ldg(centers + 2 * c), __ldg(centers + 2 * c + 1), b, dmn, dmx);
+                        M = fmin(M, dmx);
+                    }
+                }
+            if (ok) {
+                const double thr = M * (1.0 + kKeepMargin) + 1e-300;
+                uint32_t first = MIXED;
+                bool multi = false;
+                for (int iy = iy0; iy <= iy1 && !multi; ++iy)
+                    for (int ix = ix0; ix <= ix1 && !multi; ++ix) {
+                        const int cell = iy * g.G + ix;
+                        const int n = __ldg(g.cnt + cell);
+                        const uint16_t* cl = g.cand + (size_t)cell * g.cap;
+                        for (int j = 0; j < n; ++j) {
+                            const uint32_t c = __ldg(cl + j);
+                            double dmn, dmx;
+                            box_d2(__ldg(centers + 2 * c), __ldg(centers + 2 * c + 1), b, dmn,
+                                   dmx);
+                            if (dmn <= thr) {
+                                if (first == MIXED) first = c;
+                                else if (c != first) {
+                                    multi = true;
+                                    break;
+                                }
+                            }
+                        }
+                    }
+                if (!multi) single = first;
+            }
+        }
+        tnew[t] = single;
+        if (force_all || single == MIXED || single != tlab[t])
+            work[atomicAdd(nwork, 1ULL)] = (uint32_t)t;
+    }
+}
+
+// One warp per listed tile: labels := the single center, or nearest_center
+// through the grid; exact integer deltas of the cluster sums.
+__global__ void __launch_bounds__(LL_TB) k_lloyd_work(
     const double2* __restrict__ spts, int64_t n, const double* __restrict__ centers, int k,
-    CandGrid g, uint32_t* __restrict__ labs, int full, int Ex, int Ey, ClusterAcc acc,
+    CandGrid g, uint32_t* __restrict__ labs, const uint32_t* __restrict__ work,
+    const unsigned long long* __restrict__ nwork, const uint32_t* __restrict__ tnew,
+    uint32_t* __restrict__ tlab, int full, int Ex, int Ey, ClusterAcc acc,
     unsigned long long* __restrict__ changed, const int* __restrict__ skip_flag) {
     extern __shared__ unsigned char smem[];
-    if (skip_flag && *skip_flag) return;  // empty clusters pending: host repairs first
+    if (skip_flag && *skip_flag) return;
     double* cx = reinterpret_cast<double*>(smem);
     double* cy = cx + k;
     unsigned long long* s_sx = reinterpret_cast<unsigned long long*>(cy + k);
@@ -719,46 +797,54 @@ __global__ void __launch_bounds__(LL_TB) k_lloyd_grid(
     }
     if (threadIdx.x == 0) s_changed = 0;
     __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)*nwork;
     unsigned long long my_changed = 0;
-    constexpr int U = 4;  // points in flight per thread (memory-level parallelism)
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x * U;
-    for (int64_t base = blockIdx.x * (int64_t)blockDim.x * U + threadIdx.x; base < n;
-         base += stride) {
-        double2 p[U];
-        uint32_t old[U];
+    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nw;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint32_t t = work[w];
+        const uint32_t single = tnew[t];
+        uint32_t old[TILE / 32];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t r = base + (int64_t)u * blockDim.x;
-            if (r < n) {
-                p[u] = spts[r];
-                old[u] = full ? 0u : labs[r];
-            }
+        for (int i = 0; i < TILE / 32; ++i) {
+            const int64_t r = (int64_t)t * TILE + i * 32 + lane;
+            old[i] = (r < n && !full) ? labs[r] : 0u;
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t r = base + (int64_t)u * blockDim.x;
+        for (int i = 0; i < TILE / 32; ++i) {
+            const int64_t r = (int64_t)t * TILE + i * 32 + lane;
             if (r >= n) break;
-            const uint32_t best = grid_nearest(g, p[u].x, p[u].y, cx, cy, k);
+            double2 p;
+            uint32_t best;
+            if (single != MIXED) {
+                best = single;
+                if (!full && old[i] == best) continue;  // unchanged: point not needed
+                p = spts[r];
+            } else {
+                p = spts[r];
+                best = grid_nearest(g, p.x, p.y, cx, cy, k);
+            }
             if (full) {
                 labs[r] = best;
-                fx_atomic_add(s_sx + 2 * best, fx_from_double(p[u].x, Ex));
-                fx_atomic_add(s_sy + 2 * best, fx_from_double(p[u].y, Ey));
+                fx_atomic_add(s_sx + 2 * best, fx_from_double(p.x, Ex));
+                fx_atomic_add(s_sy + 2 * best, fx_from_double(p.y, Ey));
                 atomicAdd(s_cnt + best, 1ULL);
-            } else if (old[u] != best) {
+            } else if (old[i] != best) {
                 labs[r] = best;
                 ++my_changed;
-                const i128 fx = fx_from_double(p[u].x, Ex), fy = fx_from_double(p[u].y, Ey);
+                const i128 fx = fx_from_double(p.x, Ex), fy = fx_from_double(p.y, Ey);
                 fx_atomic_add(s_sx + 2 * best, fx);
                 fx_atomic_add(s_sy + 2 * best, fy);
                 atomicAdd(s_cnt + best, 1ULL);
-                fx_atomic_add(s_sx + 2 * old[u], -fx);
-                fx_atomic_add(s_sy + 2 * old[u], -fy);
-                atomicAdd(s_cnt + old[u], ~0ULL);
+                fx_atomic_add(s_sx + 2 * old[i], -fx);
+                fx_atomic_add(s_sy + 2 * old[i], -fy);
+                atomicAdd(s_cnt + old[i], ~0ULL);
             }
         }
+        if (lane == 0) tlab[t] = single;
     }
     for (int o = 16; o > 0; o >>= 1) my_changed += __shfl_down_sync(0xffffffffu, my_changed, o);
-    if ((threadIdx.x & 31) == 0 && my_changed) atomicAdd(&s_changed, my_changed);
+    if (lane == 0 && my_changed) atomicAdd(&s_changed, my_changed);
     __syncthreads();
     for (int c = threadIdx.x; c < k; c += blockDim.x) {
         const i128 vx = fx_load(s_sx + 2 * c), vy = fx_load(s_sy + 2 * c);
@@ -847,7 +933,7 @@ __global__ void k_far_block(const double2* __restrict__ spts, const uint32_t* __
 __global__ void k_repair(const double2* __restrict__ spts, const uint32_t* __restrict__ pos,
                          uint32_t* __restrict__ labs, double* __restrict__ centers, ClusterAcc acc,
                          int Ex, int Ey, const unsigned long long* __restrict__ blk, int nblk,
-                         int c) {
+                         int c, uint32_t* __restrict__ tlab) {
     double bd = -1.0;
     int64_t bi = INT64_MAX, br = -1;
     for (int b = 0; b < nblk; ++b) {
@@ -867,6 +953,7 @@ __global__ void k_repair(const double2* __restrict__ spts, const uint32_t* __res
     fx_atomic_add(acc.sy + 2 * donor, -fy);
     acc.cnt[donor] -= 1;
     labs[br] = (uint32_t)c;
+    tlab[br / TILE] = MIXED;  // the tile no longer holds one label
     acc.sx[2 * c] = acc.sx[2 * c + 1] = 0;
     acc.sy[2 * c] = acc.sy[2 * c + 1] = 0;
     fx_atomic_add(acc.sx + 2 * c, fx);
@@ -914,6 +1001,10 @@ struct LloydCtx {
     DArr<unsigned long long> far_blk;
     CandGrid cg;
     DArr<uint16_t> cg_cnt, cg_cand;
+    const double4* tbox = nullptr;
+    int64_t ntiles = 0;
+    DArr<uint32_t> tlab, tnew, work;
+    DArr<unsigned long long> nwork;
     ClusterAcc cacc() { return ClusterAcc{acc.p, acc.p + 2 * k, acc.p + 4 * k}; }
     size_t smem() const { return sizeof(double) * 2 * k + sizeof(unsigned long long) * 5 * k; }
     int grid() const {
@@ -924,16 +1015,26 @@ struct LloydCtx {
 
 void lloyd_assign(LloydCtx& L, bool full, bool gate_on_empties) {
     JB_CUDA(cudaMemsetAsync(L.flags.p, 0, 8, L.st));
+    JB_CUDA(cudaMemsetAsync(L.nwork.p, 0, 8, L.st));
+    const int* gate = gate_on_empties ? L.empties.p + L.k : nullptr;
     {
         JB_PROF("lloyd_grid", L.st);
         const int ncell = L.cg.G * L.cg.G;
         k_grid_build<<<std::min(ncell / 8, kSMs * 16), 256, 0, L.st>>>(L.cg, L.centers.p, L.k);
     }
     JB_LAUNCH_CHECK();
+    {
+        JB_PROF("lloyd_tile_check", L.st);
+        k_tile_check<<<(int)std::max<int64_t>(1, std::min<int64_t>((L.ntiles + 255) / 256,
+                                                                  kSMs * 16)),
+                       256, 0, L.st>>>(L.tbox, L.ntiles, L.cg, L.centers.p, L.tlab.p, L.tnew.p,
+                                       L.work.p, L.nwork.p, gate, full ? 1 : 0);
+    }
+    JB_LAUNCH_CHECK();
     JB_PROF("lloyd_assign", L.st);
-    k_lloyd_grid<<<L.grid(), LL_TB, L.smem(), L.st>>>(
-        L.spts, L.n, L.centers.p, L.k, L.cg, L.labs.p, full ? 1 : 0, L.Ex, L.Ey, L.cacc(),
-        L.flags.p, gate_on_empties ? L.empties.p + L.k : nullptr);
+    k_lloyd_work<<<L.grid(), LL_TB, L.smem(), L.st>>>(
+        L.spts, L.n, L.centers.p, L.k, L.cg, L.labs.p, L.work.p, L.nwork.p, L.tnew.p, L.tlab.p,
+        full ? 1 : 0, L.Ex, L.Ey, L.cacc(), L.flags.p, gate);
     JB_LAUNCH_CHECK();
 }
 
@@ -957,7 +1058,7 @@ void lloyd_repair(LloydCtx& L, int ne) {
                                             L.cacc().cnt, L.far_blk.p);
         JB_LAUNCH_CHECK();
         k_repair<<<1, 1, 0, L.st>>>(L.spts, L.pos, L.labs.p, L.centers.p, L.cacc(), L.Ex, L.Ey,
-                                    L.far_blk.p, nblk, c);
+                                    L.far_blk.p, nblk, c, L.tlab.p);
         JB_LAUNCH_CHECK();
     }
     const int zero = 0;
@@ -1039,7 +1140,14 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
         L.cg.cnt = L.cg_cnt.p;
         L.cg.cand = L.cg_cand.p;
     }
-    JB_CUDA(cudaFuncSetAttribute(k_lloyd_grid, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    L.tbox = tbox.p;
+    L.ntiles = ntiles;
+    L.tlab.alloc(ntiles, st);
+    L.tnew.alloc(ntiles, st);
+    L.work.alloc(ntiles, st);
+    L.nwork.alloc(1, st);
+    JB_CUDA(cudaMemsetAsync(L.tlab.p, 0xFF, sizeof(uint32_t) * ntiles, st));
+    JB_CUDA(cudaFuncSetAttribute(k_lloyd_work, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)L.smem()));
 
     const int nblocks = (int)((n + D2_R - 1) / D2_R);
@@ -1086,6 +1194,7 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
 
         // ---- Lloyd (lloyd_once :200-220) ----
         L.acc.zero();
+        JB_CUDA(cudaMemsetAsync(L.tlab.p, 0xFF, sizeof(uint32_t) * ntiles, st));
         lloyd_assign(L, true, false);
         uint64_t it = 0;
         for (; it < max_iters; ++it) {
