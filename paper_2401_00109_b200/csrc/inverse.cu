@@ -35,23 +35,36 @@ __device__ __forceinline__ double llround_d(double x) {
     return r;
 }
 
-constexpr int64_t SKIP_LAST = 1LL << 62;  // flag: don't write this piece's last sample
-
-// One thread per segment: the reference's sequential recurrences, exactly.
+// Pass A -- one thread per segment runs the reference's sequential chains:
 //   quantize_lengths (:63-74): r = llround(l + carry), clamp >= 1,
-//     carry = (l + carry) - r  -- r kept as an exact double, so the carry
-//     chain has no int<->fp conversions;
-//   match_total_length (:81-93): backward cascade on the tail;
-//   inverse_compress (:94-101): v += inc (start value of every piece) and
-//     the running output position.
-// The three chains are independent and run interleaved in one loop.
-__global__ void __launch_bounds__(128) k_inv_chain(InverseIn in, const double* __restrict__ rlen,
-                                                   const double* __restrict__ rinc,
-                                                   int32_t* __restrict__ qlen,
-                                                   double* __restrict__ vstart,
-                                                   int64_t* __restrict__ pstart,
-                                                   double* __restrict__ out,
-                                                   unsigned long long* __restrict__ err) {
+//     carry = (l + carry) - r  (r kept as an exact double: no int<->fp
+//     conversions on the ~90-cycle critical path);
+//   inverse_compress (:94-101): v += inc, and the running output position.
+// Only the rounded lengths (int32, 16-byte vector stores on the aligned
+// body) and, every GROUP pieces, checkpoints (v, position) leave the
+// thread, so the per-thread streams cost ~5 B/piece. Then the backward
+// fix-up (match_total_length :81-93) and a re-checkpoint of the tail.
+constexpr int GROUP = 32;
+
+struct ChainOut {
+    int32_t* qlen;      // N
+    double* ck_v;       // one per group
+    int64_t* ck_pos;    // one per group
+    int64_t* grp_off;   // n_seg + 1: first group of each segment
+};
+
+__device__ __forceinline__ void chain_step(double l, double& carry, int32_t& q) {
+    const double x = l + carry;
+    double r = llround_d(x);
+    if (r < 1.0) r = 1.0;
+    carry = x - r;
+    q = (int32_t)r;
+}
+
+__global__ void __launch_bounds__(32) k_inv_chain(InverseIn in, const double* __restrict__ rlen,
+                                                  const double* __restrict__ rinc, ChainOut co,
+                                                  double* __restrict__ out,
+                                                  unsigned long long* __restrict__ err) {
     const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (s >= in.n_seg) return;
     const int64_t a = in.seg_offsets[s], b = in.seg_offsets[s + 1];
@@ -60,87 +73,122 @@ __global__ void __launch_bounds__(128) k_inv_chain(InverseIn in, const double* _
             atomicMin(err, (unsigned long long)(s * 16 + UNKNOWN_SYMBOL));
             return;
         }
-    const bool drop_last = in.layout == 0 && s + 1 < in.n_seg;  // stitch_partitions
-    const int64_t base = in.out_offsets[s];
+    const int64_t g0 = co.grp_off[s];
     double carry = 0.0, v = in.anchors[s];
-    int64_t pos = base, total = 0;
-    out[base] = v;
-    int64_t j = a;
-    constexpr int U = 4;
-    for (; j + U <= b; j += U) {
-        uint32_t lab[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) lab[u] = in.labels[j + u];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const double l = __ldg(rlen + lab[u]);
-            const double x = l + carry;
-            double r = llround_d(x);
-            if (r < 1.0) r = 1.0;
-            carry = x - r;
-            const int32_t q = (int32_t)r;
-            qlen[j + u] = q;
-            vstart[j + u] = v;
-            pstart[j + u] = pos;
-            v += __ldg(rinc + lab[u]);
-            pos += q;
-            total += q;
+    int64_t pos = in.out_offsets[s], total = 0;
+    out[pos] = v;
+    auto step = [&](int64_t j, uint32_t lab) -> int32_t {
+        if (((j - a) & (GROUP - 1)) == 0) {
+            const int64_t g = g0 + ((j - a) >> 5);
+            co.ck_v[g] = v;
+            co.ck_pos[g] = pos;
         }
-    }
-    for (; j < b; ++j) {
-        const uint32_t lab = in.labels[j];
-        const double l = __ldg(rlen + lab);
-        const double x = l + carry;
-        double r = llround_d(x);
-        if (r < 1.0) r = 1.0;
-        carry = x - r;
-        const int32_t q = (int32_t)r;
-        qlen[j] = q;
-        vstart[j] = v;
-        pstart[j] = pos;
+        int32_t q;
+        chain_step(__ldg(rlen + lab), carry, q);
         v += __ldg(rinc + lab);
         pos += q;
         total += q;
+        return q;
+    };
+    int64_t j = a;
+    for (; j < b && (j & 3); ++j) co.qlen[j] = step(j, in.labels[j]);
+    for (; j + 4 <= b; j += 4) {
+        const uint4 L = *reinterpret_cast<const uint4*>(in.labels + j);
+        int4 Q;
+        Q.x = step(j, L.x);
+        Q.y = step(j + 1, L.y);
+        Q.z = step(j + 2, L.z);
+        Q.w = step(j + 3, L.w);
+        *reinterpret_cast<int4*>(co.qlen + j) = Q;
     }
-    // match_total_length: backward cascade; positions after the first
-    // modified piece are recomputed
+    for (; j < b; ++j) co.qlen[j] = step(j, in.labels[j]);
+    // match_total_length: backward cascade
     long long residual = in.source_lengths[s] - total;
     int64_t first_mod = b;
     for (int64_t t = b; t-- > a && residual != 0;) {
-        long long adj = (long long)qlen[t] + residual;
+        long long adj = (long long)co.qlen[t] + residual;
         if (adj < 1) adj = 1;
-        residual -= adj - qlen[t];
-        qlen[t] = (int32_t)adj;
+        residual -= adj - co.qlen[t];
+        co.qlen[t] = (int32_t)adj;
         first_mod = t;
     }
     if (residual != 0 || b == a) {
         atomicMin(err, (unsigned long long)(s * 16 + INVALID_PIECE));
         return;
     }
-    if (first_mod < b) {
-        int64_t p = pstart[first_mod];
-        for (int64_t t = first_mod; t < b; ++t) {
-            pstart[t] = p;
-            p += qlen[t];
+    if (first_mod < b) {  // positions of the groups after the modified piece
+        const int64_t gm = (first_mod - a) >> 5;
+        int64_t p = co.ck_pos[g0 + gm];
+        for (int64_t t = a + gm * GROUP; t < b; ++t) {
+            if (((t - a) & (GROUP - 1)) == 0) co.ck_pos[g0 + ((t - a) >> 5)] = p;
+            p += co.qlen[t];
         }
     }
-    if (drop_last) pstart[b - 1] |= SKIP_LAST;
 }
 
-// interpolation fill (inverse_compress :97-99): v + inc * (i / len)
-__global__ void k_inv_fill(InverseIn in, const double* __restrict__ rinc,
-                           const int32_t* __restrict__ qlen, const double* __restrict__ vstart,
-                           const int64_t* __restrict__ pstart, double* __restrict__ out) {
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < in.N;
-         j += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t len = qlen[j];
-        const int64_t ps = pstart[j];
-        const int64_t p0 = ps & ~SKIP_LAST;
-        const int64_t n_write = (ps & SKIP_LAST) ? len - 1 : len;
-        const double v = vstart[j];
-        const double inc = __ldg(rinc + in.labels[j]);
-        const double l = (double)len;
-        for (int64_t i = 1; i <= n_write; ++i) out[p0 + i] = v + inc * ((double)i / l);
+// Pass B -- one warp per group of GROUP pieces: v within the group replayed
+// sequentially from the checkpoint (shuffled, same rounding), positions by
+// an exact integer scan, then the group's samples v + inc * (i / len)
+// (inverse_compress :97-99) written contiguously into the output; a
+// non-final part of a univariate-partitioned fit drops its last sample
+// (stitch_partitions :198-213).
+__global__ void __launch_bounds__(256) k_inv_fill(InverseIn in, const double* __restrict__ rinc,
+                                                  ChainOut co, int64_t n_groups,
+                                                  double* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const unsigned FULL = 0xffffffffu;
+    for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; g < n_groups;
+         g += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        // segment of group g: grp_off[s] <= g < grp_off[s+1]
+        int64_t lo = 0, hi = in.n_seg;
+        while (hi - lo > 1) {
+            const int64_t m = (lo + hi) >> 1;
+            if (co.grp_off[m] <= g) lo = m;
+            else hi = m;
+        }
+        const int64_t s = lo;
+        const int64_t a = in.seg_offsets[s], b = in.seg_offsets[s + 1];
+        const int64_t base = a + (g - co.grp_off[s]) * GROUP;
+        const int cnt = (int)((b - base) < GROUP ? (b - base) : GROUP);
+        const int64_t j = base + lane;
+        const bool valid = lane < cnt;
+        const int len = valid ? co.qlen[j] : 0;
+        const double inc = valid ? __ldg(rinc + in.labels[j]) : 0.0;
+        double v = co.ck_v[g], myv = 0.0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            const double ii = __shfl_sync(FULL, inc, i);
+            if (i < cnt) {
+                if (lane == i) myv = v;
+                v += ii;
+            }
+        }
+        long long incl = len;
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const long long L = __shfl_sync(FULL, incl, 31);
+        const int64_t pos = co.ck_pos[g];
+        const bool drop_last = in.layout == 0 && s + 1 < in.n_seg && base + GROUP >= b;
+        for (long long q0 = 1; q0 <= L; q0 += 32) {
+            const long long q = q0 + lane;  // 1-based sample within the group
+            int last_below = -1;  // last piece with incl < q (fixed 5 steps)
+            for (int st = 16; st > 0; st >>= 1) {
+                const int t = last_below + st;
+                const long long cm = __shfl_sync(FULL, incl, t < 31 ? t : 31);
+                if (t < cnt && cm < q) last_below = t;
+            }
+            const int pc = last_below + 1 < 32 ? last_below + 1 : 31;
+            const long long ci = __shfl_sync(FULL, incl, pc);
+            const int li = __shfl_sync(FULL, len, pc);
+            const double vi = __shfl_sync(FULL, myv, pc);
+            const double ii = __shfl_sync(FULL, inc, pc);
+            if (q <= L && !(drop_last && q == L)) {
+                const long long i = q - (ci - li);  // 1..len within the piece
+                out[pos + q] = vi + ii * ((double)i / (double)li);
+            }
+        }
     }
 }
 
@@ -149,7 +197,6 @@ __global__ void k_inv_fill(InverseIn in, const double* __restrict__ rinc,
 void inverse_transform_device(const InverseIn& in, double* d_out, cudaStream_t st) {
     if (in.layout == 0 && in.n_seg == 0)
         throw Error(INVALID_INPUT, "stitch_partitions: no segments");
-    DArr<int32_t> qlen(std::max<int64_t>(in.N, 1), st);
     const uint64_t kk = std::max<uint64_t>(in.k, 1);
     DArr<double> tab(2 * kk, st);
     DArr<unsigned long long> err(1, st);
@@ -161,12 +208,25 @@ void inverse_transform_device(const InverseIn& in, double* d_out, cudaStream_t s
             tab.p + kk);
         JB_LAUNCH_CHECK();
     }
-    DArr<double> vstart(std::max<int64_t>(in.N, 1), st);
-    DArr<int64_t> pstart(std::max<int64_t>(in.N, 1), st);
+    // group layout (host: segment piece counts are needed anyway for the offsets)
+    std::vector<int64_t> h_off(in.n_seg + 1), h_goff(in.n_seg + 1);
+    JB_CUDA(cudaMemcpyAsync(h_off.data(), in.seg_offsets, sizeof(int64_t) * (in.n_seg + 1),
+                            cudaMemcpyDeviceToHost, st));
+    JB_CUDA(cudaStreamSynchronize(st));
+    h_goff[0] = 0;
+    for (int64_t s = 0; s < in.n_seg; ++s)
+        h_goff[s + 1] = h_goff[s] + (h_off[s + 1] - h_off[s] + GROUP - 1) / GROUP;
+    const int64_t n_groups = h_goff[in.n_seg];
+    DArr<int64_t> goff(in.n_seg + 1, st);
+    goff.upload(h_goff.data(), in.n_seg + 1);
+    DArr<int32_t> qlen(std::max<int64_t>(in.N, 1) + 4, st);
+    DArr<double> ck_v(std::max<int64_t>(n_groups, 1), st);
+    DArr<int64_t> ck_pos(std::max<int64_t>(n_groups, 1), st);
+    ChainOut co{qlen.p, ck_v.p, ck_pos.p, goff.p};
     {
         JB_PROF("inverse_chain", st);
-        k_inv_chain<<<(int)((in.n_seg + 127) / 128), 128, 0, st>>>(
-            in, tab.p, tab.p + kk, qlen.p, vstart.p, pstart.p, d_out, err.p);
+        k_inv_chain<<<(int)((in.n_seg + 31) / 32), 32, 0, st>>>(in, tab.p, tab.p + kk, co, d_out,
+                                                                 err.p);
     }
     JB_LAUNCH_CHECK();
     unsigned long long e;
@@ -182,11 +242,11 @@ void inverse_transform_device(const InverseIn& in, double* d_out, cudaStream_t s
         throw Error(INVALID_PIECE, "cannot fit pieces into the segment's steps (segment " +
                                        std::to_string(seg) + ")");
     }
-    if (in.N > 0) {
+    if (n_groups > 0) {
         JB_PROF("inverse_fill", st);
-        const int grid =
-            (int)std::max<int64_t>(1, std::min<int64_t>((in.N + 255) / 256, (int64_t)kSMs * 16));
-        k_inv_fill<<<grid, 256, 0, st>>>(in, tab.p + kk, qlen.p, vstart.p, pstart.p, d_out);
+        const int grid = (int)std::max<int64_t>(
+            1, std::min<int64_t>((n_groups * 32 + 255) / 256, (int64_t)kSMs * 16));
+        k_inv_fill<<<grid, 256, 0, st>>>(in, tab.p + kk, co, n_groups, d_out);
         JB_LAUNCH_CHECK();
     }
 }
