@@ -51,7 +51,15 @@ struct ChainOut {
     double* ck_v;       // one per group
     int64_t* ck_pos;    // one per group
     int64_t* grp_off;   // n_seg + 1: first group of each segment
+    int32_t* grp_seg;   // segment of every group
 };
+
+__global__ void k_group_segments(const int64_t* __restrict__ grp_off, int64_t n_seg,
+                                 int32_t* __restrict__ grp_seg) {
+    const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (s >= n_seg) return;
+    for (int64_t g = grp_off[s]; g < grp_off[s + 1]; ++g) grp_seg[g] = (int32_t)s;
+}
 
 __device__ __forceinline__ void chain_step(double l, double& carry, int32_t& q) {
     const double x = l + carry;
@@ -139,14 +147,7 @@ __global__ void __launch_bounds__(256) k_inv_fill(InverseIn in, const double* __
     const unsigned FULL = 0xffffffffu;
     for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; g < n_groups;
          g += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        // segment of group g: grp_off[s] <= g < grp_off[s+1]
-        int64_t lo = 0, hi = in.n_seg;
-        while (hi - lo > 1) {
-            const int64_t m = (lo + hi) >> 1;
-            if (co.grp_off[m] <= g) lo = m;
-            else hi = m;
-        }
-        const int64_t s = lo;
+        const int64_t s = co.grp_seg[g];
         const int64_t a = in.seg_offsets[s], b = in.seg_offsets[s + 1];
         const int64_t base = a + (g - co.grp_off[s]) * GROUP;
         const int cnt = (int)((b - base) < GROUP ? (b - base) : GROUP);
@@ -222,7 +223,10 @@ void inverse_transform_device(const InverseIn& in, double* d_out, cudaStream_t s
     DArr<int32_t> qlen(std::max<int64_t>(in.N, 1) + 4, st);
     DArr<double> ck_v(std::max<int64_t>(n_groups, 1), st);
     DArr<int64_t> ck_pos(std::max<int64_t>(n_groups, 1), st);
-    ChainOut co{qlen.p, ck_v.p, ck_pos.p, goff.p};
+    DArr<int32_t> gseg(std::max<int64_t>(n_groups, 1), st);
+    ChainOut co{qlen.p, ck_v.p, ck_pos.p, goff.p, gseg.p};
+    k_group_segments<<<(int)((in.n_seg + 127) / 128), 128, 0, st>>>(goff.p, in.n_seg, gseg.p);
+    JB_LAUNCH_CHECK();
     {
         JB_PROF("inverse_chain", st);
         k_inv_chain<<<(int)((in.n_seg + 31) / 32), 32, 0, st>>>(in, tab.p, tab.p + kk, co, d_out,
