@@ -186,44 +186,42 @@ void scale_pieces(const Pieces& pc, int64_t total_steps, double scl, Scaled& out
 
 namespace {
 
-struct StatsAcc {
-    unsigned long long* counts;  // k
-    unsigned long long* first;   // k (min index)
-    unsigned long long* lens;    // k
-    unsigned long long* sx;      // 2k (lo, hi)
-    unsigned long long* sy;      // 2k
-};
-
-// block-privatized statistics in shared memory, flushed with global atomics
+// Group statistics of digitize (digitization.hpp:217-231) fused with the
+// final assignment: count, first index, sum of lengths, sums of x and y.
+// Sums use a per-element-biased fixed point (fx(v) + B >= 0, < 2^63) so a
+// point costs one shared-memory atomic per coordinate; count and length
+// share one packed 64-bit atomic (count << 40 | len) per point. The host
+// removes the bias exactly (count * B). Deterministic for any schedule.
 __global__ void k_assign_stats(const double2* __restrict__ pts, const int32_t* __restrict__ len,
                                int64_t n, const double* __restrict__ centers, int k,
                                int do_assign, uint32_t* __restrict__ labels, int Ex, int Ey,
-                               StatsAcc g, int privatize, CandGrid cg) {
+                               unsigned long long Bx, unsigned long long By,
+                               unsigned long long* __restrict__ gacc, int use_smem, int packed,
+                               CandGrid cg) {
+    // accumulator layout (smem or global): cl(k) len(k) first(k) sx(2k) sy(2k)
     extern __shared__ unsigned char smem[];
     double* cx = reinterpret_cast<double*>(smem);
     double* cy = cx + k;
-    unsigned long long* s_cnt = reinterpret_cast<unsigned long long*>(cy + k);
-    unsigned long long* s_first = s_cnt + k;
-    unsigned long long* s_len = s_first + k;
-    unsigned long long* s_sx = s_len + k;
+    unsigned long long* s_cl =
+        use_smem ? reinterpret_cast<unsigned long long*>(cy + k) : gacc;  // count(|len)
+    unsigned long long* s_len = s_cl + k;
+    unsigned long long* s_first = s_len + k;
+    unsigned long long* s_sx = s_first + k;
     unsigned long long* s_sy = s_sx + 2 * k;
     for (int c = threadIdx.x; c < k; c += blockDim.x) {
-        cx[c] = centers[2 * c];
-        cy[c] = centers[2 * c + 1];
-        if (privatize) {
-            s_cnt[c] = 0;
-            s_first[c] = ~0ULL;
+        if (do_assign) {
+            cx[c] = centers[2 * c];
+            cy[c] = centers[2 * c + 1];
+        }
+        if (use_smem) {
+            s_cl[c] = 0;
             s_len[c] = 0;
+            s_first[c] = ~0ULL;
             s_sx[2 * c] = s_sx[2 * c + 1] = 0;
             s_sy[2 * c] = s_sy[2 * c + 1] = 0;
         }
     }
     __syncthreads();
-    unsigned long long* t_cnt = privatize ? s_cnt : g.counts;
-    unsigned long long* t_first = privatize ? s_first : g.first;
-    unsigned long long* t_len = privatize ? s_len : g.lens;
-    unsigned long long* t_sx = privatize ? s_sx : g.sx;
-    unsigned long long* t_sy = privatize ? s_sy : g.sy;
     constexpr int U = 4;  // points in flight per thread
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * U;
     for (int64_t base = blockIdx.x * (int64_t)blockDim.x * U + threadIdx.x; base < n;
@@ -250,22 +248,28 @@ __global__ void k_assign_stats(const double2* __restrict__ pts, const int32_t* _
                 lab = grid_nearest(cg, p.x, p.y, cx, cy, k);
                 labels[i] = lab;
             }
-            atomicAdd(t_cnt + lab, 1ULL);
-            if ((unsigned long long)i < t_first[lab]) atomicMin(t_first + lab, (unsigned long long)i);
-            atomicAdd(t_len + lab, (unsigned long long)ll[u]);
-            fx_atomic_add(t_sx + 2 * lab, fx_from_double(p.x, Ex));
-            fx_atomic_add(t_sy + 2 * lab, fx_from_double(p.y, Ey));
+            if (packed) {
+                atomicAdd(s_cl + lab, (1ULL << 40) | (unsigned long long)ll[u]);
+            } else {
+                atomicAdd(s_cl + lab, 1ULL);
+                atomicAdd(s_len + lab, (unsigned long long)ll[u]);
+            }
+            if ((unsigned long long)i < s_first[lab]) atomicMin(s_first + lab, (unsigned long long)i);
+            fx_atomic_add_small(s_sx + 2 * lab, (u128)(fx_from_double(p.x, Ex) + (i128)Bx));
+            fx_atomic_add_small(s_sy + 2 * lab, (u128)(fx_from_double(p.y, Ey) + (i128)By));
         }
     }
-    if (!privatize) return;
+    if (!use_smem) return;
     __syncthreads();
     for (int c = threadIdx.x; c < k; c += blockDim.x) {
-        if (s_cnt[c] == 0) continue;
-        atomicAdd(g.counts + c, s_cnt[c]);
-        atomicMin(g.first + c, s_first[c]);
-        atomicAdd(g.lens + c, s_len[c]);
-        fx_atomic_add(g.sx + 2 * c, fx_load(s_sx + 2 * c));
-        fx_atomic_add(g.sy + 2 * c, fx_load(s_sy + 2 * c));
+        if (s_cl[c] == 0) continue;
+        const unsigned long long cnt = packed ? (s_cl[c] >> 40) : s_cl[c];
+        const unsigned long long ls = packed ? (s_cl[c] & ((1ULL << 40) - 1)) : s_len[c];
+        atomicAdd(gacc + c, cnt);
+        atomicAdd(gacc + k + c, ls);
+        atomicMin(gacc + 2 * k + c, s_first[c]);
+        fx_atomic_add(gacc + 3 * k + 2 * c, fx_load(s_sx + 2 * c));
+        fx_atomic_add(gacc + 5 * k + 2 * c, fx_load(s_sy + 2 * c));
     }
 }
 
@@ -309,25 +313,30 @@ __global__ void k_gather(const double2* __restrict__ pts, const uint64_t* __rest
 
 void assign_and_stats(const double* d_pts, const int32_t* d_len, int64_t n,
                       const std::vector<double>& centers, uint64_t k, const BBox& bb,
-                      bool do_assign, uint32_t* d_labels, GroupStats& gs, cudaStream_t st) {
+                      bool do_assign, uint32_t* d_labels, GroupStats& gs, cudaStream_t st,
+                      int32_t max_len) {
     DArr<double> dc(std::max<uint64_t>(2 * k, 1), st);
     if (centers.size() >= 2 * k) dc.upload(centers.data(), 2 * k);  // GA: no centers needed
     else if (do_assign) throw Error(INTERNAL, "assignment without centers");
-    DArr<unsigned long long> acc(7 * k, st);
+    DArr<unsigned long long> acc(7 * k, st);  // cl(k) len(k) first(k) sx(2k) sy(2k)
     acc.zero();
-    JB_CUDA(cudaMemsetAsync(acc.p + k, 0xFF, sizeof(unsigned long long) * k, st));
-    StatsAcc g{acc.p, acc.p + k, acc.p + 2 * k, acc.p + 3 * k, acc.p + 5 * k};
+    JB_CUDA(cudaMemsetAsync(acc.p + 2 * k, 0xFF, sizeof(unsigned long long) * k, st));
     const double mx = std::max(std::fabs(bb.xmin), std::fabs(bb.xmax));
     const double my = std::max(std::fabs(bb.ymin), std::fabs(bb.ymax));
-    const int Ex = fx_exponent_for(mx * (double)n * 1.001 + 1e-300);
-    const int Ey = fx_exponent_for(my * (double)n * 1.001 + 1e-300);
-    const size_t base_smem = sizeof(double) * 2 * k;
-    const size_t priv_smem = sizeof(unsigned long long) * 7 * k;
-    int privatize = base_smem + priv_smem <= 160 * 1024;
-    const size_t smem = base_smem + (privatize ? priv_smem : 0);
-    if (smem > 200 * 1024) throw Error(INVALID_INPUT, "k too large for the assignment kernel");
+    // biased per-element fixed point: fx(v) + B in [0, 2^62)
+    auto exp_for = [](double m) {
+        const int e = fx_exponent_for(m + 1e-300);  // 125 - e', m < 2^e'
+        return e - 125 + 61;                         // 61 - e'
+    };
+    const int Ex = exp_for(mx), Ey = exp_for(my);
+    const unsigned long long Bx = (unsigned long long)fx_from_double(mx, Ex);
+    const unsigned long long By = (unsigned long long)fx_from_double(my, Ey);
+    const size_t centers_smem = do_assign ? sizeof(double) * 2 * k : 0;
+    if (centers_smem > 160 * 1024) throw Error(INVALID_INPUT, "k too large for the assignment kernel");
+    const int use_smem = centers_smem + sizeof(unsigned long long) * 7 * k <= 160 * 1024;
+    const size_t smem = centers_smem + (use_smem ? sizeof(unsigned long long) * 7 * k : 0);
     JB_CUDA(cudaFuncSetAttribute(k_assign_stats, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
+                                 (int)std::max<size_t>(smem, 1)));
     // exact candidate grid over the points' bounding box (jb_grid.cuh)
     CandGrid cg{};
     DArr<uint16_t> cg_cnt, cg_cand;
@@ -344,23 +353,30 @@ void assign_and_stats(const double* d_pts, const int32_t* d_len, int64_t n,
     }
     const int TB = 256;
     const int grid = (int)std::max<int64_t>(
-        1, std::min<int64_t>((n + TB - 1) / TB, (int64_t)kSMs * (privatize ? 2 : 8)));
+        1, std::min<int64_t>((n + TB * 4 - 1) / (TB * 4), (int64_t)kSMs * 2));
+    // packed count|len is safe when a block's count < 2^24 and length sum < 2^40
+    const int64_t per_block = (n + grid - 1) / grid;
+    const int packed = use_smem && per_block < (1LL << 24) &&
+                       (double)per_block * max_len < 1099511627776.0;
     {
         JB_PROF("assign_stats", st);
-        k_assign_stats<<<grid, TB, smem, st>>>(reinterpret_cast<const double2*>(d_pts), d_len, n,
-                                           dc.p, (int)k, do_assign ? 1 : 0, d_labels, Ex, Ey, g,
-                                           privatize, cg);
+        k_assign_stats<<<use_smem ? grid : (int)std::max<int64_t>(
+                                              1, std::min<int64_t>((n + TB - 1) / TB, kSMs * 8)),
+                         TB, smem, st>>>(reinterpret_cast<const double2*>(d_pts), d_len, n, dc.p,
+                                         (int)k, do_assign ? 1 : 0, d_labels, Ex, Ey, Bx, By,
+                                         acc.p, use_smem, packed, cg);
     }
     JB_LAUNCH_CHECK();
     std::vector<unsigned long long> h = acc.to_host(7 * k);
     gs.counts.assign(h.begin(), h.begin() + k);
-    gs.first_seen.assign(h.begin() + k, h.begin() + 2 * k);
-    gs.len_sums.assign(h.begin() + 2 * k, h.begin() + 3 * k);
+    gs.len_sums.assign(h.begin() + k, h.begin() + 2 * k);
+    gs.first_seen.assign(h.begin() + 2 * k, h.begin() + 3 * k);
     gs.sum_x.resize(k);
     gs.sum_y.resize(k);
     for (uint64_t c = 0; c < k; ++c) {
-        gs.sum_x[c] = fx_to_double(fx_load(&h[3 * k + 2 * c]), Ex);
-        gs.sum_y[c] = fx_to_double(fx_load(&h[5 * k + 2 * c]), Ey);
+        const i128 cnt = (i128)gs.counts[c];
+        gs.sum_x[c] = fx_to_double(fx_load(&h[3 * k + 2 * c]) - cnt * (i128)Bx, Ex);
+        gs.sum_y[c] = fx_to_double(fx_load(&h[5 * k + 2 * c]) - cnt * (i128)By, Ey);
     }
 }
 

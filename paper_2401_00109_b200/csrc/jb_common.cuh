@@ -71,8 +71,9 @@ __host__ __device__ inline int fx_exponent_for(double max_abs_sum) {
 }
 
 // |x| * 2^E truncated to an integer, with x's sign.
-__device__ __forceinline__ i128 fx_from_double(double x, int E) {
-    uint64_t bits = (uint64_t)__double_as_longlong(x);
+__host__ __device__ __forceinline__ i128 fx_from_double(double x, int E) {
+    uint64_t bits;
+    memcpy(&bits, &x, 8);
     const int bexp = (int)((bits >> 52) & 0x7FF);
     if (bexp == 0) return 0;  // zero / subnormal: below any resolution we use
     const uint64_t mant = (bits & 0x000FFFFFFFFFFFFFULL) | 0x0010000000000000ULL;
@@ -158,6 +159,16 @@ __device__ __forceinline__ void fx_atomic_add(unsigned long long* lohi, i128 v) 
     const unsigned long long old = atomicAdd(lohi, lo);
     const unsigned long long carry = (old + lo) < old ? 1ULL : 0ULL;
     const unsigned long long h = hi + carry;
+    if (h) atomicAdd(lohi + 1, h);
+}
+
+// add a NON-NEGATIVE value (< 2^64 in the common case) to a (lo, hi)
+// accumulator: one atomic unless the low word carries
+__device__ __forceinline__ void fx_atomic_add_small(unsigned long long* lohi, u128 v) {
+    const unsigned long long lo = (unsigned long long)v;
+    const unsigned long long hi = (unsigned long long)(v >> 64);
+    const unsigned long long old = atomicAdd(lohi, lo);
+    const unsigned long long h = hi + ((old + lo) < old ? 1ULL : 0ULL);
     if (h) atomicAdd(lohi + 1, h);
 }
 

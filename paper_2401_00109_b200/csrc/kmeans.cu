@@ -517,40 +517,66 @@ __global__ void k_pick_first(const uint64_t* __restrict__ raw, uint64_t n, SeedS
     chosen[0] = (int64_t)r;
 }
 
-// One warp per tile: d2 = min(d2, dist2(p, c_last)) (init: d2 = dist2), the
-// tile's max d2, and exact deltas of the per-original-block partial sums.
-// A tile is skipped when no point in its box can come closer to the new
-// center than the tile's current max d2.
+// D^2 round, pass 1 (thread per tile): a tile needs work only if some point
+// of its box can come closer to the new center than the tile's current max
+// d2; every other tile keeps all its d2 (the rounded distances of its points
+// are all > max d2 >= d2, so std::min leaves them unchanged).
+__global__ void k_d2_cull(const double4* __restrict__ tbox, const double* __restrict__ tmax,
+                          int64_t ntiles, const double2* __restrict__ spts,
+                          const uint32_t* __restrict__ pos, const SeedState* __restrict__ ss,
+                          uint32_t* __restrict__ work, unsigned long long* __restrict__ nwork) {
+    const double2 c = spts[pos[ss->last]];
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntiles;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        double dmin2, dmax2;
+        box_d2(c.x, c.y, tbox[t], dmin2, dmax2);
+        if (!(dmin2 * (1.0 - kKeepMargin) > tmax[t])) work[atomicAdd(nwork, 1ULL)] = (uint32_t)t;
+    }
+}
+
+// D^2 round, pass 2 (warp per listed tile; init: every tile): d2 = min(d2,
+// dist2(p, c_last)), the tile's new max d2, and exact deltas of the
+// per-ORIGINAL-block partial sums (the pick scans in sample order).
 __global__ void __launch_bounds__(256) k_d2_tiles(
     const double2* __restrict__ spts, const uint32_t* __restrict__ orig,
-    const uint32_t* __restrict__ pos, int64_t n, const double4* __restrict__ tbox,
-    double* __restrict__ tmax, double* __restrict__ d2s, const SeedState* __restrict__ ss,
-    int init, int E, unsigned long long* __restrict__ part) {
+    const uint32_t* __restrict__ pos, int64_t n, const uint32_t* __restrict__ work,
+    const unsigned long long* __restrict__ nwork, double* __restrict__ tmax,
+    double* __restrict__ d2s, const SeedState* __restrict__ ss, int init, int E,
+    unsigned long long* __restrict__ part) {
     const int lane = threadIdx.x & 31;
     const int64_t ntiles = (n + TILE - 1) / TILE;
+    const int64_t nw = init ? ntiles : (int64_t)*nwork;
     const double2 c = spts[pos[ss->last]];
-    for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < ntiles;
-         t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        if (!init) {
-            double dmin2, dmax2;
-            box_d2(c.x, c.y, tbox[t], dmin2, dmax2);
-            if (dmin2 * (1.0 - kKeepMargin) > tmax[t]) continue;  // warp-uniform
+    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nw;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t t = init ? w : (int64_t)work[w];
+        double2 p[TILE / 32];
+        double old[TILE / 32];
+        uint32_t o[TILE / 32];
+#pragma unroll
+        for (int i = 0; i < TILE / 32; ++i) {
+            const int64_t r = t * TILE + i * 32 + lane;
+            if (r < n) {
+                p[i] = spts[r];
+                old[i] = init ? 0.0 : d2s[r];
+                o[i] = orig[r];
+            }
         }
         double mx = 0.0;
+#pragma unroll
         for (int i = 0; i < TILE / 32; ++i) {
             const int64_t r = t * TILE + i * 32 + lane;
             if (r >= n) break;
-            const double2 p = spts[r];
-            const double dd = dist2(p.x, p.y, c.x, c.y);
+            const double dd = dist2(p[i].x, p[i].y, c.x, c.y);
             double v;
             if (init) {
                 v = dd;
                 d2s[r] = v;
-                fx_atomic_add(part + 2 * (orig[r] / D2_R), fx_from_double(v, E));
+                fx_atomic_add(part + 2 * (o[i] / D2_R), fx_from_double(v, E));
             } else {
-                v = d2s[r];
+                v = old[i];
                 if (dd < v) {  // std::min(d2, dd)
-                    fx_atomic_add(part + 2 * (orig[r] / D2_R),
+                    fx_atomic_add(part + 2 * (o[i] / D2_R),
                                   fx_from_double(dd, E) - fx_from_double(v, E));
                     v = dd;
                     d2s[r] = v;
@@ -558,7 +584,7 @@ __global__ void __launch_bounds__(256) k_d2_tiles(
             }
             mx = fmax(mx, v);
         }
-        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
         if (lane == 0) tmax[t] = mx;
     }
 }
@@ -1151,6 +1177,10 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
                                  (int)L.smem()));
 
     const int nblocks = (int)((n + D2_R - 1) / D2_R);
+    DArr<uint32_t> d2_work(ntiles, st);
+    DArr<unsigned long long> d2_nwork(1, st);
+    const int cull_grid =
+        (int)std::max<int64_t>(1, std::min<int64_t>((ntiles + 255) / 256, kSMs * 16));
     DArr<double> d2s(n, st);
     DArr<unsigned long long> part(2 * nblocks, st);
     DArr<SeedState> ss(1, st);
@@ -1166,8 +1196,8 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
         JB_LAUNCH_CHECK();
         {
             JB_PROF("d2_update", st);
-            k_d2_tiles<<<tile_grid, 256, 0, st>>>(spts.p, orig.p, pos.p, n, tbox.p, tmax.p,
-                                                  d2s.p, ss.p, 1, Ed2, part.p);
+            k_d2_tiles<<<tile_grid, 256, 0, st>>>(spts.p, orig.p, pos.p, n, nullptr, nullptr,
+                                                  tmax.p, d2s.p, ss.p, 1, Ed2, part.p);
         }
         JB_LAUNCH_CHECK();
         for (uint64_t c = 1; c < k; ++c) {
@@ -1179,8 +1209,12 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
             JB_LAUNCH_CHECK();
             if (c + 1 < k) {
                 JB_PROF("d2_update", st);
-                k_d2_tiles<<<tile_grid, 256, 0, st>>>(spts.p, orig.p, pos.p, n, tbox.p, tmax.p,
-                                                      d2s.p, ss.p, 0, Ed2, part.p);
+                JB_CUDA(cudaMemsetAsync(d2_nwork.p, 0, 8, st));
+                k_d2_cull<<<cull_grid, 256, 0, st>>>(tbox.p, tmax.p, ntiles, spts.p, pos.p, ss.p,
+                                                     d2_work.p, d2_nwork.p);
+                k_d2_tiles<<<tile_grid, 256, 0, st>>>(spts.p, orig.p, pos.p, n, d2_work.p,
+                                                      d2_nwork.p, tmax.p, d2s.p, ss.p, 0, Ed2,
+                                                      part.p);
                 JB_LAUNCH_CHECK();
             }
         }
