@@ -201,9 +201,10 @@ __global__ void k_assign_stats(const double2* __restrict__ pts, const int32_t* _
     // accumulator layout (smem or global): cl(k) len(k) first(k) sx(2k) sy(2k)
     extern __shared__ unsigned char smem[];
     double* cx = reinterpret_cast<double*>(smem);
-    double* cy = cx + k;
+    double* cy = cx + k;  // centers only when assigning (smem sized accordingly)
     unsigned long long* s_cl =
-        use_smem ? reinterpret_cast<unsigned long long*>(cy + k) : gacc;  // count(|len)
+        use_smem ? reinterpret_cast<unsigned long long*>(cx + (do_assign ? 2 * k : 0))
+                 : gacc;  // count(|len)
     unsigned long long* s_len = s_cl + k;
     unsigned long long* s_first = s_len + k;
     unsigned long long* s_sx = s_first + k;

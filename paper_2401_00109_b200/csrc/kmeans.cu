@@ -736,7 +736,7 @@ __global__ void k_tile_check(const double4* __restrict__ tbox, int64_t ntiles, C
                              const uint32_t* __restrict__ tlab, uint32_t* __restrict__ tnew,
                              uint32_t* __restrict__ work, unsigned long long* __restrict__ nwork,
                              const int* __restrict__ skip_flag, int force_all) {
-    if (skip_flag && *skip_flag) return;
+    if (skip_flag && (skip_flag[0] | skip_flag[1])) return;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntiles;
          t += (int64_t)gridDim.x * blockDim.x) {
         const double4 b = tbox[t];  // (x0, x1, y0, y1)
@@ -807,7 +807,7 @@ __global__ void __launch_bounds__(LL_TB) k_lloyd_work(
     uint32_t* __restrict__ tlab, int full, int Ex, int Ey, ClusterAcc acc,
     unsigned long long* __restrict__ changed, const int* __restrict__ skip_flag) {
     extern __shared__ unsigned char smem[];
-    if (skip_flag && *skip_flag) return;
+    if (skip_flag && (skip_flag[0] | skip_flag[1])) return;
     double* cx = reinterpret_cast<double*>(smem);
     double* cy = cx + k;
     unsigned long long* s_sx = reinterpret_cast<unsigned long long*>(cy + k);
@@ -884,7 +884,9 @@ __global__ void __launch_bounds__(LL_TB) k_lloyd_work(
 // centers[c] = sums[c] / counts[c] for non-empty clusters (update_means
 // :177-180); reports the empty clusters in index order.
 __global__ void k_means(ClusterAcc acc, int k, int Ex, int Ey, double* __restrict__ centers,
-                        int* __restrict__ empties, int* __restrict__ n_empty) {
+                        int* __restrict__ empties, int* __restrict__ n_empty,
+                        const int* __restrict__ gate) {
+    if (gate && (gate[0] | gate[1])) return;
     for (int c = threadIdx.x; c < k; c += blockDim.x) {
         const long long cnt = (long long)acc.cnt[c];
         if (cnt > 0) {
@@ -1039,9 +1041,19 @@ struct LloydCtx {
     }
 };
 
+// end of one batched Lloyd iteration (lloyd_once :209-213): ++iterations,
+// stop when no label changed; resets the per-iteration counters. Gated like
+// the other kernels, so iterations launched past convergence are no-ops.
+__global__ void k_iter_end(int* __restrict__ state, unsigned long long* __restrict__ changed,
+                           unsigned long long* __restrict__ nwork) {
+    if (state[0] | state[1]) return;  // pending repair / converged
+    state[2] += 1;
+    if (*changed == 0) state[1] = 1;
+    *changed = 0;
+    *nwork = 0;
+}
+
 void lloyd_assign(LloydCtx& L, bool full, bool gate_on_empties) {
-    JB_CUDA(cudaMemsetAsync(L.flags.p, 0, 8, L.st));
-    JB_CUDA(cudaMemsetAsync(L.nwork.p, 0, 8, L.st));
     const int* gate = gate_on_empties ? L.empties.p + L.k : nullptr;
     {
         JB_PROF("lloyd_grid", L.st);
@@ -1064,11 +1076,22 @@ void lloyd_assign(LloydCtx& L, bool full, bool gate_on_empties) {
     JB_LAUNCH_CHECK();
 }
 
-void lloyd_means(LloydCtx& L) {
+void lloyd_means(LloydCtx& L, bool gated) {
     JB_PROF("lloyd_means", L.st);
     k_means<<<1, 1024, 0, L.st>>>(L.cacc(), L.k, L.Ex, L.Ey, L.centers.p, L.empties.p,
-                                  L.empties.p + L.k);
+                                  L.empties.p + L.k, gated ? L.empties.p + L.k : nullptr);
     JB_LAUNCH_CHECK();
+}
+
+struct LoopState {
+    int n_empty, converged, iters;
+};
+
+LoopState lloyd_state(LloydCtx& L) {
+    LoopState h;
+    JB_CUDA(cudaMemcpyAsync(&h, L.empties.p + L.k, sizeof h, cudaMemcpyDeviceToHost, L.st));
+    JB_CUDA(cudaStreamSynchronize(L.st));
+    return h;
 }
 
 // empty-cluster re-seeding (update_means :181-197), in cluster order
@@ -1093,7 +1116,7 @@ void lloyd_repair(LloydCtx& L, int ne) {
 
 // update_means for the final centers (after the loop): means + repairs
 void lloyd_update_means_sync(LloydCtx& L) {
-    lloyd_means(L);
+    lloyd_means(L, false);
     int ne = 0;
     JB_CUDA(cudaMemcpyAsync(&ne, L.empties.p + L.k, sizeof(int), cudaMemcpyDeviceToHost, L.st));
     JB_CUDA(cudaStreamSynchronize(L.st));
@@ -1156,7 +1179,7 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
     L.labs.alloc(n, st);
     L.acc.alloc(5 * k, st);
     L.flags.alloc(1, st);
-    L.empties.alloc(k + 1, st);
+    L.empties.alloc(k + 3, st);  // list | n_empty | converged | iterations
     L.empties.zero();
     {
         const int G = grid_side_for(k), cap = 32;
@@ -1227,30 +1250,42 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
         JB_TRACE("kmeans: d2 seeding", st);
 
         // ---- Lloyd (lloyd_once :200-220) ----
+        // Iterations are launched in batches; device-side state gates every
+        // kernel (pending empty-cluster repair, convergence) so the host
+        // syncs once per batch. Iterations launched after convergence are
+        // no-ops; the count is taken on the device.
         L.acc.zero();
         JB_CUDA(cudaMemsetAsync(L.tlab.p, 0xFF, sizeof(uint32_t) * ntiles, st));
-        lloyd_assign(L, true, false);
+        JB_CUDA(cudaMemsetAsync(L.empties.p + L.k, 0, 3 * sizeof(int), st));
+        JB_CUDA(cudaMemsetAsync(L.flags.p, 0, 8, st));
+        JB_CUDA(cudaMemsetAsync(L.nwork.p, 0, 8, st));
+        lloyd_assign(L, true, false);  // assign_all(points, seeds) (:204)
+        JB_CUDA(cudaMemsetAsync(L.flags.p, 0, 8, st));
+        JB_CUDA(cudaMemsetAsync(L.nwork.p, 0, 8, st));
         uint64_t it = 0;
-        for (; it < max_iters; ++it) {
-            lloyd_means(L);                // update_means ...
-            lloyd_assign(L, false, true);  // ... gated: skipped if repairs are pending
-            int ne = 0;
-            unsigned long long ch = 0;
-            JB_CUDA(cudaMemcpyAsync(&ne, L.empties.p + L.k, sizeof(int), cudaMemcpyDeviceToHost,
-                                    st));
-            JB_CUDA(cudaMemcpyAsync(&ch, L.flags.p, 8, cudaMemcpyDeviceToHost, st));
-            JB_CUDA(cudaStreamSynchronize(st));
-            if (ne) {
-                lloyd_repair(L, ne);        // ... empty-cluster re-seeding
-                lloyd_assign(L, false, false);
-                JB_CUDA(cudaMemcpyAsync(&ch, L.flags.p, 8, cudaMemcpyDeviceToHost, st));
-                JB_CUDA(cudaStreamSynchronize(st));
+        constexpr uint64_t kBatch = 16;
+        while (it < max_iters) {
+            const uint64_t B = std::min<uint64_t>(kBatch, max_iters - it);
+            for (uint64_t b = 0; b < B; ++b) {
+                lloyd_means(L, true);          // update_means ...
+                lloyd_assign(L, false, true);  // ... assign_all, label comparison
+                k_iter_end<<<1, 1, 0, st>>>(L.empties.p + L.k, L.flags.p, L.nwork.p);
+                JB_LAUNCH_CHECK();
             }
-            if (ch == 0) {  // next_labels == labels
-                ++it;
-                break;
+            LoopState h = lloyd_state(L);
+            it = (uint64_t)h.iters;
+            if (h.converged) break;
+            if (h.n_empty) {  // empty clusters: re-seed on the host path, finish the iteration
+                lloyd_repair(L, h.n_empty);
+                lloyd_assign(L, false, true);
+                k_iter_end<<<1, 1, 0, st>>>(L.empties.p + L.k, L.flags.p, L.nwork.p);
+                JB_LAUNCH_CHECK();
+                h = lloyd_state(L);
+                it = (uint64_t)h.iters;
+                if (h.converged) break;
             }
         }
+        JB_CUDA(cudaMemsetAsync(L.empties.p + L.k, 0, 2 * sizeof(int), st));  // ungate
         lloyd_update_means_sync(L);
         JB_TRACE("kmeans: lloyd", st);
         double sse = 0.0;
