@@ -192,7 +192,7 @@ namespace {
 // point costs one shared-memory atomic per coordinate; count and length
 // share one packed 64-bit atomic (count << 40 | len) per point. The host
 // removes the bias exactly (count * B). Deterministic for any schedule.
-__global__ void k_assign_stats(const double2* __restrict__ pts, const int32_t* __restrict__ len,
+__global__ void __launch_bounds__(256, 3) k_assign_stats(const double2* __restrict__ pts, const int32_t* __restrict__ len,
                                int64_t n, const double* __restrict__ centers, int k,
                                int do_assign, uint32_t* __restrict__ labels, int Ex, int Ey,
                                unsigned long long Bx, unsigned long long By,
@@ -354,7 +354,7 @@ void assign_and_stats(const double* d_pts, const int32_t* d_len, int64_t n,
     }
     const int TB = 256;
     const int grid = (int)std::max<int64_t>(
-        1, std::min<int64_t>((n + TB * 4 - 1) / (TB * 4), (int64_t)kSMs * 2));
+        1, std::min<int64_t>((n + TB * 4 - 1) / (TB * 4), (int64_t)kSMs * 4));
     // packed count|len is safe when a block's count < 2^24 and length sum < 2^40
     const int64_t per_block = (n + grid - 1) / grid;
     const int packed = use_smem && per_block < (1LL << 24) &&

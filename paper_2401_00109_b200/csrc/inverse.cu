@@ -48,11 +48,29 @@ constexpr int GROUP = 32;
 
 struct ChainOut {
     int32_t* qlen;      // N
-    double* ck_v;       // one per group
+    double* vstart;     // N: start value of every piece
+    double* ck_v;       // one per group (unused)
     int64_t* ck_pos;    // one per group
     int64_t* grp_off;   // n_seg + 1: first group of each segment
     int32_t* grp_seg;   // segment of every group
 };
+
+// inverse_digitize_series (:41-44): the first segment holding a label >= k
+__global__ void k_inv_validate(InverseIn in, const int32_t* __restrict__ grp_seg,
+                               unsigned long long* __restrict__ err) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < in.N;
+         j += (int64_t)gridDim.x * blockDim.x)
+        if ((uint64_t)in.labels[j] >= in.k) {
+            // segment of piece j: binary search of the piece offsets
+            int64_t lo = 0, hi = in.n_seg;
+            while (hi - lo > 1) {
+                const int64_t m = (lo + hi) >> 1;
+                if (in.seg_offsets[m] <= j) lo = m;
+                else hi = m;
+            }
+            atomicMin(err, (unsigned long long)(lo * 16 + UNKNOWN_SYMBOL));
+        }
+}
 
 __global__ void k_group_segments(const int64_t* __restrict__ grp_off, int64_t n_seg,
                                  int32_t* __restrict__ grp_seg) {
@@ -76,40 +94,42 @@ __global__ void __launch_bounds__(32) k_inv_chain(InverseIn in, const double* __
     const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (s >= in.n_seg) return;
     const int64_t a = in.seg_offsets[s], b = in.seg_offsets[s + 1];
-    for (int64_t j = a; j < b; ++j)  // inverse_digitize_series validates first (:41-44)
-        if ((uint64_t)in.labels[j] >= in.k) {
-            atomicMin(err, (unsigned long long)(s * 16 + UNKNOWN_SYMBOL));
-            return;
-        }
+    // (labels were validated by k_inv_validate)
     const int64_t g0 = co.grp_off[s];
     double carry = 0.0, v = in.anchors[s];
     int64_t pos = in.out_offsets[s], total = 0;
     out[pos] = v;
-    auto step = [&](int64_t j, uint32_t lab) -> int32_t {
-        if (((j - a) & (GROUP - 1)) == 0) {
-            const int64_t g = g0 + ((j - a) >> 5);
-            co.ck_v[g] = v;
-            co.ck_pos[g] = pos;
-        }
+    auto step = [&](int64_t j, uint32_t lab, double& vs) -> int32_t {
+        if (((j - a) & (GROUP - 1)) == 0) co.ck_pos[g0 + ((j - a) >> 5)] = pos;
         int32_t q;
         chain_step(__ldg(rlen + lab), carry, q);
+        vs = v;
         v += __ldg(rinc + lab);
         pos += q;
         total += q;
         return q;
     };
     int64_t j = a;
-    for (; j < b && (j & 3); ++j) co.qlen[j] = step(j, in.labels[j]);
+    double vs0, vs1, vs2, vs3;
+    for (; j < b && (j & 3); ++j) {
+        co.qlen[j] = step(j, in.labels[j], vs0);
+        co.vstart[j] = vs0;
+    }
     for (; j + 4 <= b; j += 4) {
         const uint4 L = *reinterpret_cast<const uint4*>(in.labels + j);
         int4 Q;
-        Q.x = step(j, L.x);
-        Q.y = step(j + 1, L.y);
-        Q.z = step(j + 2, L.z);
-        Q.w = step(j + 3, L.w);
+        Q.x = step(j, L.x, vs0);
+        Q.y = step(j + 1, L.y, vs1);
+        Q.z = step(j + 2, L.z, vs2);
+        Q.w = step(j + 3, L.w, vs3);
         *reinterpret_cast<int4*>(co.qlen + j) = Q;
+        *reinterpret_cast<double2*>(co.vstart + j) = make_double2(vs0, vs1);
+        *reinterpret_cast<double2*>(co.vstart + j + 2) = make_double2(vs2, vs3);
     }
-    for (; j < b; ++j) co.qlen[j] = step(j, in.labels[j]);
+    for (; j < b; ++j) {
+        co.qlen[j] = step(j, in.labels[j], vs0);
+        co.vstart[j] = vs0;
+    }
     // match_total_length: backward cascade
     long long residual = in.source_lengths[s] - total;
     int64_t first_mod = b;
@@ -140,9 +160,17 @@ __global__ void __launch_bounds__(32) k_inv_chain(InverseIn in, const double* __
 // (inverse_compress :97-99) written contiguously into the output; a
 // non-final part of a univariate-partitioned fit drops its last sample
 // (stitch_partitions :198-213).
+constexpr int DIV_MAX = 31;  // exact i/len table for len <= DIV_MAX (7.9 KB smem)
+
 __global__ void __launch_bounds__(256) k_inv_fill(InverseIn in, const double* __restrict__ rinc,
                                                   ChainOut co, int64_t n_groups,
                                                   double* __restrict__ out) {
+    __shared__ double div_tab[(DIV_MAX + 1) * (DIV_MAX + 1)];
+    for (int t = threadIdx.x; t < (DIV_MAX + 1) * (DIV_MAX + 1); t += blockDim.x) {
+        const int l = t / (DIV_MAX + 1), i = t % (DIV_MAX + 1);
+        div_tab[t] = l > 0 ? (double)i / (double)l : 0.0;  // the same IEEE division
+    }
+    __syncthreads();
     const int lane = threadIdx.x & 31;
     const unsigned FULL = 0xffffffffu;
     for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; g < n_groups;
@@ -155,15 +183,7 @@ __global__ void __launch_bounds__(256) k_inv_fill(InverseIn in, const double* __
         const bool valid = lane < cnt;
         const int len = valid ? co.qlen[j] : 0;
         const double inc = valid ? __ldg(rinc + in.labels[j]) : 0.0;
-        double v = co.ck_v[g], myv = 0.0;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-            const double ii = __shfl_sync(FULL, inc, i);
-            if (i < cnt) {
-                if (lane == i) myv = v;
-                v += ii;
-            }
-        }
+        const double myv = valid ? co.vstart[j] : 0.0;
         long long incl = len;
         for (int o = 1; o < 32; o <<= 1) {
             const long long y = __shfl_up_sync(FULL, incl, o);
@@ -187,7 +207,10 @@ __global__ void __launch_bounds__(256) k_inv_fill(InverseIn in, const double* __
             const double ii = __shfl_sync(FULL, inc, pc);
             if (q <= L && !(drop_last && q == L)) {
                 const long long i = q - (ci - li);  // 1..len within the piece
-                out[pos + q] = vi + ii * ((double)i / (double)li);
+                // (double)i / l, IEEE-rounded; exact table for short pieces
+                const double frac = li <= DIV_MAX ? div_tab[li * (DIV_MAX + 1) + (int)i]
+                                                  : (double)i / (double)li;
+                out[pos + q] = vi + ii * frac;
             }
         }
     }
@@ -221,12 +244,24 @@ void inverse_transform_device(const InverseIn& in, double* d_out, cudaStream_t s
     DArr<int64_t> goff(in.n_seg + 1, st);
     goff.upload(h_goff.data(), in.n_seg + 1);
     DArr<int32_t> qlen(std::max<int64_t>(in.N, 1) + 4, st);
-    DArr<double> ck_v(std::max<int64_t>(n_groups, 1), st);
+    DArr<double> ck_v(1, st);
     DArr<int64_t> ck_pos(std::max<int64_t>(n_groups, 1), st);
     DArr<int32_t> gseg(std::max<int64_t>(n_groups, 1), st);
-    ChainOut co{qlen.p, ck_v.p, ck_pos.p, goff.p, gseg.p};
+    DArr<double> vstart(std::max<int64_t>(in.N, 1) + 4, st);
+    ChainOut co{qlen.p, vstart.p, ck_v.p, ck_pos.p, goff.p, gseg.p};
     k_group_segments<<<(int)((in.n_seg + 127) / 128), 128, 0, st>>>(goff.p, in.n_seg, gseg.p);
     JB_LAUNCH_CHECK();
+    if (in.N > 0) {
+        k_inv_validate<<<(int)std::max<int64_t>(1, std::min<int64_t>((in.N + 255) / 256, kSMs * 8)),
+                         256, 0, st>>>(in, gseg.p, err.p);
+        JB_LAUNCH_CHECK();
+        unsigned long long e0;
+        err.download(&e0, 1);
+        JB_CUDA(cudaStreamSynchronize(st));
+        if (e0 != ~0ULL)
+            throw Error(UNKNOWN_SYMBOL, "label not in codebook of size " + std::to_string(in.k) +
+                                            " (segment " + std::to_string(e0 / 16) + ")");
+    }
     {
         JB_PROF("inverse_chain", st);
         k_inv_chain<<<(int)((in.n_seg + 31) / 32), 32, 0, st>>>(in, tab.p, tab.p + kk, co, d_out,
