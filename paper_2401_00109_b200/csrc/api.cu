@@ -213,7 +213,7 @@ struct jb_fit {
     DArr<double> d_centers, d_mean_lengths;
     double scaling[3] = {1.0, 1.0, 1.0};
     // diagnostics
-    uint64_t iterations = 0, sample_size = 0, draws = 0;
+    uint64_t iterations = 0, sample_size = 0, draws = 0, work_tiles = 0, changed_labels = 0;
     int32_t fix_rounds = 0, ga_rounds = 0;
     double phase_ms[5] = {0, 0, 0, 0, 0};
 };
@@ -456,6 +456,8 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
             k = c.k;
             backend_centers = km.centers;
             sample_labels = std::move(km.labels);
+            fit->work_tiles = km.work_tiles;
+            fit->changed_labels = km.changed_labels;
             labels.alloc(N, st);
             assign_needed = true;
             fit->iterations = km.iterations;
@@ -724,6 +726,10 @@ jb_status jb_fit_stats(const jb_fit* f, uint64_t* iterations, uint64_t* sample_s
     if (fix_rounds) *fix_rounds = f->fix_rounds;
     if (ga_rounds) *ga_rounds = f->ga_rounds;
     if (phase_ms) std::copy(f->phase_ms, f->phase_ms + 5, phase_ms);
+    if (phase_ms) {  // extended diagnostics after the 5 phase timings
+        phase_ms[5] = (double)f->work_tiles;
+        phase_ms[6] = (double)f->changed_labels;
+    }
     return JB_OK;
 }
 

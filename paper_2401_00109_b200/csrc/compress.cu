@@ -22,6 +22,10 @@ __device__ __forceinline__ int64_t piece_end(const double* __restrict__ v, int64
                                              int64_t last, double tol2, int64_t max_len) {
     const double base = v[start];
     double s2 = 0.0, s3 = 0.0;
+    // sum_{i<=d} i^2 kept as a running integer-valued double: identical to the
+    // reference's d*(d+1)*(2d+1)/6 while d*(d+1)*(2d+1) < 2^53 (every value
+    // involved is an exactly representable integer), the formula beyond that
+    double sq = 0.0;
     int64_t end = start;
     for (;;) {
         const int64_t cand = end + 1;
@@ -30,7 +34,9 @@ __device__ __forceinline__ int64_t piece_end(const double* __restrict__ v, int64
         const double d = (double)(cand - start);
         const double ns2 = s2 + y * y;
         const double ns3 = s3 + d * y;
-        const double sum_d2 = d * (d + 1.0) * (2.0 * d + 1.0) / 6.0;
+        sq += d * d;
+        const double sum_d2 =
+            cand - start <= 165000 ? sq : d * (d + 1.0) * (2.0 * d + 1.0) / 6.0;
         const double sq_dev = y * y / (d * d) * sum_d2 - 2.0 * y / d * ns3 + ns2;
         if (sq_dev > (d - 1.0) * tol2 && cand > start + 1) break;
         end = cand;

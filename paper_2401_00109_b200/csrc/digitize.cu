@@ -62,12 +62,25 @@ __global__ void k_sum_var(const int32_t* __restrict__ len, const double* __restr
                           int64_t n, double mean_len, double mean_inc, int El, int Ei,
                           unsigned long long* __restrict__ acc) {
     i128 sl = 0, si = 0;
-    for (int64_t i = blockIdx.x * (int64_t)kTB + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * kTB) {
-        const double dl = (double)len[i] - mean_len;
-        const double di = inc[i] - mean_inc;
-        sl += fx_from_double(dl * dl, El);
-        si += fx_from_double(di * di, Ei);
+    constexpr int U = 4;
+    for (int64_t b = blockIdx.x * (int64_t)kTB * U + threadIdx.x; b < n;
+         b += (int64_t)gridDim.x * kTB * U) {
+        int32_t L[U];
+        double I[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = b + (int64_t)u * kTB;
+            L[u] = i < n ? len[i] : 0;
+            I[u] = i < n ? inc[i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (b + (int64_t)u * kTB >= n) break;
+            const double dl = (double)L[u] - mean_len;  // digitization.hpp:41-44
+            const double di = I[u] - mean_inc;
+            sl += fx_from_double(dl * dl, El);
+            si += fx_from_double(di * di, Ei);
+        }
     }
     sl = block_sum_i128<kTB>(sl);
     si = block_sum_i128<kTB>(si);
@@ -82,16 +95,30 @@ __global__ void k_scale(const int32_t* __restrict__ len, const double* __restric
                         int64_t n, double scl, double sl, double si, double* __restrict__ pts,
                         unsigned long long* __restrict__ bb) {
     unsigned long long xmn = ~0ULL, xmx = 0, ymn = ~0ULL, ymx = 0;
-    for (int64_t i = blockIdx.x * (int64_t)kTB + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * kTB) {
-        const double x = scl * (double)len[i] / sl;
-        const double y = inc[i] / si;
-        reinterpret_cast<double2*>(pts)[i] = make_double2(x, y);
-        const unsigned long long ox = ord_bits(x), oy = ord_bits(y);
-        xmn = min(xmn, ox);
-        xmx = max(xmx, ox);
-        ymn = min(ymn, oy);
-        ymx = max(ymx, oy);
+    constexpr int U = 4;
+    for (int64_t b = blockIdx.x * (int64_t)kTB * U + threadIdx.x; b < n;
+         b += (int64_t)gridDim.x * kTB * U) {
+        int32_t L[U];
+        double I[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = b + (int64_t)u * kTB;
+            L[u] = i < n ? len[i] : 0;
+            I[u] = i < n ? inc[i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = b + (int64_t)u * kTB;
+            if (i >= n) break;
+            const double x = scl * (double)L[u] / sl;
+            const double y = I[u] / si;
+            reinterpret_cast<double2*>(pts)[i] = make_double2(x, y);
+            const unsigned long long ox = ord_bits(x), oy = ord_bits(y);
+            xmn = min(xmn, ox);
+            xmx = max(xmx, ox);
+            ymn = min(ymn, oy);
+            ymx = max(ymx, oy);
+        }
     }
     for (int o = 16; o > 0; o >>= 1) {
         xmn = min(xmn, __shfl_down_sync(0xffffffffu, xmn, o));

@@ -142,6 +142,7 @@ struct KMeansOut {
     DArr<uint32_t> labels;        // per input point (lloyd labels)
     uint64_t iterations = 0;
     double sse = 0.0;
+    uint64_t work_tiles = 0, changed_labels = 0;  // Lloyd diagnostics (all iterations)
 };
 
 // sample_indices (clustering.hpp:74-85) on device; idx is S entries.

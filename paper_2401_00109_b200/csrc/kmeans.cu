@@ -1032,7 +1032,7 @@ struct LloydCtx {
     const double4* tbox = nullptr;
     int64_t ntiles = 0;
     DArr<uint32_t> tlab, tnew, work;
-    DArr<unsigned long long> nwork;
+    DArr<unsigned long long> nwork, diag;
     ClusterAcc cacc() { return ClusterAcc{acc.p, acc.p + 2 * k, acc.p + 4 * k}; }
     size_t smem() const { return sizeof(double) * 2 * k + sizeof(unsigned long long) * 5 * k; }
     int grid() const {
@@ -1045,9 +1045,12 @@ struct LloydCtx {
 // stop when no label changed; resets the per-iteration counters. Gated like
 // the other kernels, so iterations launched past convergence are no-ops.
 __global__ void k_iter_end(int* __restrict__ state, unsigned long long* __restrict__ changed,
-                           unsigned long long* __restrict__ nwork) {
+                           unsigned long long* __restrict__ nwork,
+                           unsigned long long* __restrict__ diag) {
     if (state[0] | state[1]) return;  // pending repair / converged
     state[2] += 1;
+    diag[0] += *nwork;  // diagnostics: tiles processed / labels changed
+    diag[1] += *changed;
     if (*changed == 0) state[1] = 1;
     *changed = 0;
     *nwork = 0;
@@ -1180,6 +1183,7 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
     L.acc.alloc(5 * k, st);
     L.flags.alloc(1, st);
     L.empties.alloc(k + 3, st);  // list | n_empty | converged | iterations
+    L.diag.alloc(2, st);
     L.empties.zero();
     {
         const int G = grid_side_for(k), cap = 32;
@@ -1257,6 +1261,7 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
         L.acc.zero();
         JB_CUDA(cudaMemsetAsync(L.tlab.p, 0xFF, sizeof(uint32_t) * ntiles, st));
         JB_CUDA(cudaMemsetAsync(L.empties.p + L.k, 0, 3 * sizeof(int), st));
+        L.diag.zero();
         JB_CUDA(cudaMemsetAsync(L.flags.p, 0, 8, st));
         JB_CUDA(cudaMemsetAsync(L.nwork.p, 0, 8, st));
         lloyd_assign(L, true, false);  // assign_all(points, seeds) (:204)
@@ -1269,7 +1274,7 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
             for (uint64_t b = 0; b < B; ++b) {
                 lloyd_means(L, true);          // update_means ...
                 lloyd_assign(L, false, true);  // ... assign_all, label comparison
-                k_iter_end<<<1, 1, 0, st>>>(L.empties.p + L.k, L.flags.p, L.nwork.p);
+                k_iter_end<<<1, 1, 0, st>>>(L.empties.p + L.k, L.flags.p, L.nwork.p, L.diag.p);
                 JB_LAUNCH_CHECK();
             }
             LoopState h = lloyd_state(L);
@@ -1278,7 +1283,7 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
             if (h.n_empty) {  // empty clusters: re-seed on the host path, finish the iteration
                 lloyd_repair(L, h.n_empty);
                 lloyd_assign(L, false, true);
-                k_iter_end<<<1, 1, 0, st>>>(L.empties.p + L.k, L.flags.p, L.nwork.p);
+                k_iter_end<<<1, 1, 0, st>>>(L.empties.p + L.k, L.flags.p, L.nwork.p, L.diag.p);
                 JB_LAUNCH_CHECK();
                 h = lloyd_state(L);
                 it = (uint64_t)h.iters;
@@ -1286,6 +1291,13 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
             }
         }
         JB_CUDA(cudaMemsetAsync(L.empties.p + L.k, 0, 2 * sizeof(int), st));  // ungate
+        {
+            unsigned long long diag[2];
+            JB_CUDA(cudaMemcpyAsync(diag, L.diag.p, 16, cudaMemcpyDeviceToHost, st));
+            JB_CUDA(cudaStreamSynchronize(st));
+            out.work_tiles = diag[0];
+            out.changed_labels = diag[1];
+        }
         lloyd_update_means_sync(L);
         JB_TRACE("kmeans: lloyd", st);
         double sse = 0.0;
