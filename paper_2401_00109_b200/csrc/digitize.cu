@@ -250,13 +250,17 @@ __global__ void __launch_bounds__(256, 3) k_assign_stats(const double2* __restri
         }
     }
     __syncthreads();
+    __shared__ AggScratch agg_all[8];
+    AggScratch* agg = agg_all + (threadIdx.x >> 5);
     constexpr int U = 4;  // points in flight per thread
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * U;
-    for (int64_t base = blockIdx.x * (int64_t)blockDim.x * U + threadIdx.x; base < n;
-         base += stride) {
+    // every lane runs the same trip count (warp-uniform loop for the
+    // aggregation's full-mask shuffles)
+    for (int64_t base0 = blockIdx.x * (int64_t)blockDim.x * U; base0 < n; base0 += stride) {
+        const int64_t base = base0 + threadIdx.x;
         double2 pp[U];
         int32_t ll[U];
-        uint32_t lb[U];
+        uint32_t lb[U] = {0, 0, 0, 0};
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int64_t i = base + (int64_t)u * blockDim.x;
@@ -269,22 +273,28 @@ __global__ void __launch_bounds__(256, 3) k_assign_stats(const double2* __restri
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int64_t i = base + (int64_t)u * blockDim.x;
-            if (i >= n) break;
-            const double2 p = pp[u];
+            const bool valid = i < n;
+            const double2 p = valid ? pp[u] : make_double2(0.0, 0.0);
             uint32_t lab = lb[u];
-            if (do_assign) {
+            if (valid && do_assign) {
                 lab = grid_nearest(cg, p.x, p.y, cx, cy, k);
                 labels[i] = lab;
             }
-            if (packed) {
-                atomicAdd(s_cl + lab, (1ULL << 40) | (unsigned long long)ll[u]);
-            } else {
-                atomicAdd(s_cl + lab, 1ULL);
-                atomicAdd(s_len + lab, (unsigned long long)ll[u]);
-            }
-            if ((unsigned long long)i < s_first[lab]) atomicMin(s_first + lab, (unsigned long long)i);
-            fx_atomic_add_small(s_sx + 2 * lab, (u128)(fx_from_double(p.x, Ex) + (i128)Bx));
-            fx_atomic_add_small(s_sy + 2 * lab, (u128)(fx_from_double(p.y, Ey) + (i128)By));
+            if (valid && (unsigned long long)i < s_first[lab])
+                atomicMin(s_first + lab, (unsigned long long)i);
+            const u128 vx = valid ? (u128)(fx_from_double(p.x, Ex) + (i128)Bx) : 0;
+            const u128 vy = valid ? (u128)(fx_from_double(p.y, Ey) + (i128)By) : 0;
+            warp_aggregate(valid, lab, vx, vy, valid ? (unsigned long long)ll[u] : 0ULL, agg,
+                           [&](uint32_t L, u128 sa, u128 sb, unsigned long long lsum, int cnt) {
+                               if (packed) {
+                                   atomicAdd(s_cl + L, ((unsigned long long)cnt << 40) | lsum);
+                               } else {
+                                   atomicAdd(s_cl + L, (unsigned long long)cnt);
+                                   atomicAdd(s_len + L, lsum);
+                               }
+                               fx_atomic_add_small(s_sx + 2 * L, sa);
+                               fx_atomic_add_small(s_sy + 2 * L, sb);
+                           });
         }
     }
     if (!use_smem) return;

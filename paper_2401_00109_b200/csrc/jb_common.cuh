@@ -190,6 +190,44 @@ __device__ __forceinline__ i128 fx_warp_sum(i128 v) {
     return (i128)(((u128)hi << 64) | (u128)lo);
 }
 
+// Warp-aggregated accumulation. Lanes with the same key (active lanes only)
+// form a group (__match_any_sync); the group's leader sums the members' values
+// from a per-warp shared scratch and issues ONE set of atomics for the group.
+// Integer sums: the result is independent of grouping and order.
+struct AggScratch {  // per warp, in shared memory
+    unsigned long long a_lo[32], a_hi[32], b_lo[32], b_hi[32], c[32];
+};
+
+template <class Flush>
+__device__ __forceinline__ void warp_aggregate(bool active, uint32_t key, u128 a, u128 b,
+                                               unsigned long long c, AggScratch* sc,
+                                               Flush&& flush) {
+    const int lane = threadIdx.x & 31;
+    const unsigned act = __ballot_sync(0xffffffffu, active);
+    if (!act) return;
+    const unsigned grp = __match_any_sync(0xffffffffu, active ? key : 0xFFFFFFFFu);
+    sc->a_lo[lane] = (unsigned long long)a;
+    sc->a_hi[lane] = (unsigned long long)(a >> 64);
+    sc->b_lo[lane] = (unsigned long long)b;
+    sc->b_hi[lane] = (unsigned long long)(b >> 64);
+    sc->c[lane] = c;
+    __syncwarp();
+    if (active && (__ffs(grp) - 1) == lane) {  // group leader
+        u128 sa = 0, sb = 0;
+        unsigned long long sc_ = 0;
+        unsigned m = grp;
+        while (m) {
+            const int l = __ffs(m) - 1;
+            m &= m - 1;
+            sa += ((u128)sc->a_hi[l] << 64) | sc->a_lo[l];
+            sb += ((u128)sc->b_hi[l] << 64) | sc->b_lo[l];
+            sc_ += sc->c[l];
+        }
+        flush(key, sa, sb, sc_, __popc(grp));
+    }
+    __syncwarp();
+}
+
 // exact reference distance: dx*dx + dy*dy with no contraction (clustering.hpp:52-56)
 __device__ __forceinline__ double dist2(double ax, double ay, double bx, double by) {
     const double dx = __dsub_rn(ax, bx);

@@ -824,6 +824,8 @@ __global__ void __launch_bounds__(LL_TB) k_lloyd_work(
     if (threadIdx.x == 0) s_changed = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31;
+    __shared__ AggScratch agg_all[LL_TB / 32];
+    AggScratch* agg = agg_all + (threadIdx.x >> 5);
     const int64_t nw = (int64_t)*nwork;
     unsigned long long my_changed = 0;
     for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nw;
@@ -839,33 +841,36 @@ __global__ void __launch_bounds__(LL_TB) k_lloyd_work(
 #pragma unroll
         for (int i = 0; i < TILE / 32; ++i) {
             const int64_t r = (int64_t)t * TILE + i * 32 + lane;
-            if (r >= n) break;
-            double2 p;
-            uint32_t best;
-            if (single != MIXED) {
+            const bool valid = r < n;
+            double2 p = make_double2(0.0, 0.0);
+            uint32_t best = 0;
+            bool need_p = valid;
+            if (valid && single != MIXED) {
                 best = single;
-                if (!full && old[i] == best) continue;  // unchanged: point not needed
-                p = spts[r];
-            } else {
-                p = spts[r];
-                best = grid_nearest(g, p.x, p.y, cx, cy, k);
+                need_p = full || old[i] != best;  // unchanged: point not needed
             }
-            if (full) {
-                labs[r] = best;
-                fx_atomic_add(s_sx + 2 * best, fx_from_double(p.x, Ex));
-                fx_atomic_add(s_sy + 2 * best, fx_from_double(p.y, Ey));
-                atomicAdd(s_cnt + best, 1ULL);
-            } else if (old[i] != best) {
-                labs[r] = best;
-                ++my_changed;
-                const i128 fx = fx_from_double(p.x, Ex), fy = fx_from_double(p.y, Ey);
-                fx_atomic_add(s_sx + 2 * best, fx);
-                fx_atomic_add(s_sy + 2 * best, fy);
-                atomicAdd(s_cnt + best, 1ULL);
-                fx_atomic_add(s_sx + 2 * old[i], -fx);
-                fx_atomic_add(s_sy + 2 * old[i], -fy);
-                atomicAdd(s_cnt + old[i], ~0ULL);
-            }
+            if (need_p) p = spts[r];
+            if (valid && single == MIXED) best = grid_nearest(g, p.x, p.y, cx, cy, k);
+            const bool moved = valid && (full || old[i] != best);
+            if (moved) labs[r] = best;
+            if (!full && moved) ++my_changed;
+            // group lanes by (old, new) label pair; one set of atomics per group
+            const uint32_t key = full ? best : ((old[i] << 16) | best);
+            const i128 fx = moved ? fx_from_double(p.x, Ex) : (i128)0;
+            const i128 fy = moved ? fx_from_double(p.y, Ey) : (i128)0;
+            warp_aggregate(moved, key, (u128)fx, (u128)fy, 0ULL, agg,
+                           [&](uint32_t kk, u128 sa, u128 sb, unsigned long long, int cnt) {
+                               const uint32_t nb = full ? kk : (kk & 0xFFFFu);
+                               fx_atomic_add(s_sx + 2 * nb, (i128)sa);
+                               fx_atomic_add(s_sy + 2 * nb, (i128)sb);
+                               atomicAdd(s_cnt + nb, (unsigned long long)cnt);
+                               if (!full) {
+                                   const uint32_t ob = kk >> 16;
+                                   fx_atomic_add(s_sx + 2 * ob, -(i128)sa);
+                                   fx_atomic_add(s_sy + 2 * ob, -(i128)sb);
+                                   atomicAdd(s_cnt + ob, (unsigned long long)(-(long long)cnt));
+                               }
+                           });
         }
         if (lane == 0) tlab[t] = single;
     }
