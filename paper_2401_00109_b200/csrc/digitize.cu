@@ -250,8 +250,6 @@ __global__ void __launch_bounds__(256, 3) k_assign_stats(const double2* __restri
         }
     }
     __syncthreads();
-    __shared__ AggScratch agg_all[8];
-    AggScratch* agg = agg_all + (threadIdx.x >> 5);
     constexpr int U = 4;  // points in flight per thread
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * U;
     // every lane runs the same trip count (warp-uniform loop for the
@@ -282,19 +280,33 @@ __global__ void __launch_bounds__(256, 3) k_assign_stats(const double2* __restri
             }
             if (valid && (unsigned long long)i < s_first[lab])
                 atomicMin(s_first + lab, (unsigned long long)i);
-            const u128 vx = valid ? (u128)(fx_from_double(p.x, Ex) + (i128)Bx) : 0;
-            const u128 vy = valid ? (u128)(fx_from_double(p.y, Ey) + (i128)By) : 0;
-            warp_aggregate(valid, lab, vx, vy, valid ? (unsigned long long)ll[u] : 0ULL, agg,
-                           [&](uint32_t L, u128 sa, u128 sb, unsigned long long lsum, int cnt) {
-                               if (packed) {
-                                   atomicAdd(s_cl + L, ((unsigned long long)cnt << 40) | lsum);
-                               } else {
-                                   atomicAdd(s_cl + L, (unsigned long long)cnt);
-                                   atomicAdd(s_len + L, lsum);
-                               }
-                               fx_atomic_add_small(s_sx + 2 * L, sa);
-                               fx_atomic_add_small(s_sy + 2 * L, sb);
-                           });
+            // biased fixed point in [0, 2^62): group sums by hardware warp
+            // reductions over 16-bit chunks (exact: <= 32 * 65535 per chunk)
+            const unsigned long long vx =
+                valid ? (unsigned long long)(fx_from_double(p.x, Ex) + (i128)Bx) : 0ULL;
+            const unsigned long long vy =
+                valid ? (unsigned long long)(fx_from_double(p.y, Ey) + (i128)By) : 0ULL;
+            const unsigned grp = __match_any_sync(0xffffffffu, valid ? lab : 0xFFFFFFFFu);
+            u128 sx = 0, sy = 0;  // up to 32 * 2^62: wider than 64 bits
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) {
+                sx += (u128)__reduce_add_sync(grp, (unsigned)((vx >> (16 * ch)) & 0xFFFFu))
+                      << (16 * ch);
+                sy += (u128)__reduce_add_sync(grp, (unsigned)((vy >> (16 * ch)) & 0xFFFFu))
+                      << (16 * ch);
+            }
+            const unsigned lsum = __reduce_add_sync(grp, valid ? (unsigned)ll[u] : 0u);
+            if (valid && (__ffs(grp) - 1) == (int)(threadIdx.x & 31)) {
+                const unsigned cnt = __popc(grp);
+                if (packed) {
+                    atomicAdd(s_cl + lab, ((unsigned long long)cnt << 40) | lsum);
+                } else {
+                    atomicAdd(s_cl + lab, (unsigned long long)cnt);
+                    atomicAdd(s_len + lab, (unsigned long long)lsum);
+                }
+                fx_atomic_add_small(s_sx + 2 * lab, sx);
+                fx_atomic_add_small(s_sy + 2 * lab, sy);
+            }
         }
     }
     if (!use_smem) return;
