@@ -280,32 +280,16 @@ __global__ void __launch_bounds__(256, 3) k_assign_stats(const double2* __restri
             }
             if (valid && (unsigned long long)i < s_first[lab])
                 atomicMin(s_first + lab, (unsigned long long)i);
-            // biased fixed point in [0, 2^62): group sums by hardware warp
-            // reductions over 16-bit chunks (exact: <= 32 * 65535 per chunk)
-            const unsigned long long vx =
-                valid ? (unsigned long long)(fx_from_double(p.x, Ex) + (i128)Bx) : 0ULL;
-            const unsigned long long vy =
-                valid ? (unsigned long long)(fx_from_double(p.y, Ey) + (i128)By) : 0ULL;
-            const unsigned grp = __match_any_sync(0xffffffffu, valid ? lab : 0xFFFFFFFFu);
-            u128 sx = 0, sy = 0;  // up to 32 * 2^62: wider than 64 bits
-#pragma unroll
-            for (int ch = 0; ch < 4; ++ch) {
-                sx += (u128)__reduce_add_sync(grp, (unsigned)((vx >> (16 * ch)) & 0xFFFFu))
-                      << (16 * ch);
-                sy += (u128)__reduce_add_sync(grp, (unsigned)((vy >> (16 * ch)) & 0xFFFFu))
-                      << (16 * ch);
-            }
-            const unsigned lsum = __reduce_add_sync(grp, valid ? (unsigned)ll[u] : 0u);
-            if (valid && (__ffs(grp) - 1) == (int)(threadIdx.x & 31)) {
-                const unsigned cnt = __popc(grp);
+            if (valid) {
                 if (packed) {
-                    atomicAdd(s_cl + lab, ((unsigned long long)cnt << 40) | lsum);
+                    atomicAdd(s_cl + lab, (1ULL << 40) | (unsigned long long)ll[u]);
                 } else {
-                    atomicAdd(s_cl + lab, (unsigned long long)cnt);
-                    atomicAdd(s_len + lab, (unsigned long long)lsum);
+                    atomicAdd(s_cl + lab, 1ULL);
+                    atomicAdd(s_len + lab, (unsigned long long)ll[u]);
                 }
-                fx_atomic_add_small(s_sx + 2 * lab, sx);
-                fx_atomic_add_small(s_sy + 2 * lab, sy);
+                // biased fixed point in [0, 2^62): one atomic unless the low word carries
+                fx_atomic_add_small(s_sx + 2 * lab, (u128)(fx_from_double(p.x, Ex) + (i128)Bx));
+                fx_atomic_add_small(s_sy + 2 * lab, (u128)(fx_from_double(p.y, Ey) + (i128)By));
             }
         }
     }
