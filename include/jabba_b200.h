@@ -164,6 +164,31 @@ jb_status jb_inverse_transform(jb_context* ctx, const double* centers,
                                const double* anchors, const int64_t* source_lengths,
                                int64_t n_seg, int32_t layout, double* out_values);
 
+/* ---- Joint fit sharded over ranks (one process per GPU) -----------------
+ * Every rank passes ITS contiguous range of the global segment table (and a
+ * values buffer covering it). Compression, scaling, the final assignment and
+ * the inverse are local; the exchanges are tiny and exact (piece counts,
+ * 128-bit fixed-point partial sums, D^2 partial sums / picks, Lloyd cluster
+ * deltas, group statistics), so every rank ends with the same codebook and
+ * labels bit-identical to the single-GPU fit. The only collective needed is
+ * an allgather of host bytes, supplied by the caller (NCCL or gloo through
+ * torch.distributed in the Python mirror). Returns a fit holding this rank's
+ * segments; jb_fit_inverse_transform reconstructs them (a univariate-
+ * partitioned fit drops the last sample of every rank but the last). */
+typedef struct {
+    void* user;
+    int32_t rank, world;
+    /* gather `bytes` from every rank into recv (world * bytes, rank order);
+       return 0 on success */
+    int32_t (*allgather)(void* user, const void* send, uint64_t bytes, void* recv);
+} jb_comm;
+
+jb_status jb_fit_transform_dist(jb_context* ctx, const jb_comm* comm, const double* values,
+                                int64_t n_values, int32_t values_on_device,
+                                const int64_t* seg_first, const int64_t* seg_steps,
+                                int64_t n_seg_local, int64_t n_seg_global, int32_t layout,
+                                const jb_config* cfg, jb_fit** out);
+
 /* Kernel-level CUDA-event profiler: when enabled, every launch of the hot
  * kernels is bracketed by events on its stream. jb_profile_read fills up to
  * `cap` records (names: 64 bytes each) and returns the number of kernels. */

@@ -25,7 +25,16 @@ EXPORTS = [
     "jb_fit_inverse_transform", "jb_reconstruct_size", "jb_inverse_transform",
     "jb_symbol_token", "jb_profile_enable", "jb_profile_reset", "jb_profile_read",
     "jb_probe_fp64_tflops", "jb_mt19937_64_stream", "jb_sample_indices",
+    "jb_fit_transform_dist",
 ]
+
+# int32_t (*allgather)(void* user, const void* send, uint64_t bytes, void* recv)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p)
+
+
+class JbComm(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("rank", C.c_int32), ("world", C.c_int32),
+                ("allgather", ALLGATHER_FN)]
 
 
 class JbConfig(C.Structure):
@@ -90,6 +99,10 @@ def lib() -> C.CDLL:
     L.jb_mt19937_64_stream.restype = C.c_int
     L.jb_sample_indices.argtypes = [vp, C.c_uint64, C.c_uint64, C.c_uint64, vp]
     L.jb_sample_indices.restype = C.c_int
+    L.jb_fit_transform_dist.argtypes = [vp, C.POINTER(JbComm), vp, C.c_int64, C.c_int32, i64p,
+                                        i64p, C.c_int64, C.c_int64, C.c_int32,
+                                        C.POINTER(JbConfig), C.POINTER(vp)]
+    L.jb_fit_transform_dist.restype = C.c_int
     L.jb_probe_fp64_tflops.argtypes = [C.c_int, C.POINTER(C.c_double)]
     L.jb_probe_fp64_tflops.restype = C.c_int
     for name in ("jb_fit_transform", "jb_plan_segments", "jb_context_create",

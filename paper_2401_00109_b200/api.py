@@ -482,6 +482,91 @@ class Engine:
         return out[:n]
 
 
+# ---------------------------------------------------------------------------
+# multi-GPU: one joint fit sharded over ranks (jb_fit_transform_dist)
+
+def shard_segments(seg_steps, world: int, rank: int):
+    """Contiguous segment range [s0, s1) of `rank`, balanced by steps
+    (compression, scaling, final assignment and inverse work are all
+    proportional to samples)."""
+    steps = np.asarray(seg_steps, np.int64)
+    n = len(steps)
+    if world > n:
+        raise InvalidPartition(f"{n} segments cannot be sharded over {world} ranks")
+    cum = np.concatenate([[0], np.cumsum(steps)])
+    total = cum[-1]
+    cuts = [0]
+    for r in range(1, world):
+        c = int(np.searchsorted(cum, total * r / world, side="left"))
+        c = max(c, cuts[-1] + 1)              # every rank gets >= 1 segment
+        c = min(c, n - (world - r))
+        cuts.append(c)
+    cuts.append(n)
+    return cuts[rank], cuts[rank + 1]
+
+
+def local_view(seg_first, seg_steps, s0: int, s1: int):
+    """Sample range [lo, hi] this rank needs for segments [s0, s1) and the
+    segment table rebased onto it (split segments share boundary samples)."""
+    f = np.asarray(seg_first, np.int64)[s0:s1]
+    st = np.asarray(seg_steps, np.int64)[s0:s1]
+    lo = int(f[0])
+    hi = int((f + st).max())
+    return lo, hi, f - lo, st
+
+
+class TorchComm:
+    """jb_comm over torch.distributed: an exact allgather of host bytes
+    (gloo on host tensors; nccl staged through the rank's GPU)."""
+
+    def __init__(self, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        backend = dist.get_backend(group)
+        world = self.world
+
+        def _allgather(user, send, nbytes, recv):
+            try:
+                if nbytes == 0:
+                    return 0
+                src = np.ctypeslib.as_array((C.c_uint8 * nbytes).from_address(send))
+                t = torch.from_numpy(src.copy())
+                if backend == "nccl":
+                    t = t.to(device)
+                outs = [torch.empty_like(t) for _ in range(world)]
+                dist.all_gather(outs, t, group=group)
+                cat = torch.cat(outs).cpu().numpy()
+                C.memmove(recv, cat.ctypes.data, nbytes * world)
+                return 0
+            except Exception:  # noqa: BLE001 -- reported as JB_NCCL_ERROR by the library
+                return 1
+
+        self._fn = N.ALLGATHER_FN(_allgather)
+        self.c = N.JbComm(None, self.rank, self.world, self._fn)
+
+
+def fit_arrays_dist(engine: "Engine", comm: TorchComm, values_local, seg_first_local,
+                    seg_steps_local, n_seg_global: int, layout: int, cfg: JabbaConfig,
+                    device_ptr: Optional[int] = None, n_values: Optional[int] = None) -> "NativeFit":
+    """This rank's part of a joint fit_transform (see jb_fit_transform_dist)."""
+    sf = np.ascontiguousarray(seg_first_local, np.int64)
+    ss = np.ascontiguousarray(seg_steps_local, np.int64)
+    c = cfg.to_c()
+    h = C.c_void_p()
+    if device_ptr is not None:
+        _check(N.lib().jb_fit_transform_dist(engine.ctx, C.byref(comm.c), C.c_void_p(device_ptr),
+                                             int(n_values), 1, sf, ss, len(sf), n_seg_global,
+                                             int(layout), C.byref(c), C.byref(h)))
+    else:
+        v = np.ascontiguousarray(values_local, np.float64)
+        _check(N.lib().jb_fit_transform_dist(engine.ctx, C.byref(comm.c), v.ctypes.data, v.size,
+                                             0, sf, ss, len(sf), n_seg_global, int(layout),
+                                             C.byref(c), C.byref(h)))
+    return NativeFit(engine, h)
+
+
 _default_engine: Optional[Engine] = None
 
 

@@ -3,6 +3,7 @@
 // partitional_compress (compression.hpp:167-193) + digitize
 // (digitization.hpp:207-293), and reconstruct (inverse.hpp:127-132).
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
 #include <chrono>
@@ -18,6 +19,7 @@
 using namespace jb;
 
 namespace jb_api {
+struct MaxOp2 {};  // (placeholder to keep the named namespace non-empty)
 struct MaxOp {
     __device__ int64_t operator()(int64_t a, int64_t b) const { return a > b ? a : b; }
 };
@@ -203,6 +205,8 @@ struct jb_context {
 
 struct jb_fit {
     int32_t layout = JB_LAYOUT_COLLECTION;
+    bool drop_local_last = false;  // distributed univariate-partitioned: not the last rank
+    int64_t piece_base = 0;        // global index of this rank's first piece
     SegTable seg;
     Pieces pieces;
     DArr<double> anchors;  // per segment (device)
@@ -224,6 +228,32 @@ __global__ void k_gather_anchors(const double* __restrict__ v, const int64_t* __
                                  int64_t n_seg, double* __restrict__ out) {
     const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (s < n_seg) out[s] = v[first[s]];
+}
+
+// distributed svq: sample entries whose piece this rank owns
+__global__ void k_own_flags(const uint64_t* __restrict__ idx, uint64_t S, uint64_t base,
+                            uint64_t n_local, uint8_t* __restrict__ flags) {
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < S;
+         s += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t g = idx[s];
+        flags[s] = (g >= base && g < base + n_local) ? 1 : 0;
+    }
+}
+
+__global__ void k_local_idx(const uint64_t* __restrict__ idx, const uint32_t* __restrict__ gpos,
+                            int64_t n, uint64_t base, uint64_t* __restrict__ lidx) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        lidx[i] = idx[gpos[i]] - base;
+}
+
+__global__ void k_iota_pos(uint32_t* __restrict__ gpos, uint64_t* __restrict__ lidx, int64_t n,
+                           uint64_t base) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        gpos[i] = (uint32_t)(base + i);
+        lidx[i] = (uint64_t)i;
+    }
 }
 
 __global__ void k_embed_axis(const double2* __restrict__ pts, int64_t n, int axis,
@@ -349,7 +379,7 @@ double auto_alpha_host(int64_t n, int64_t N, double tol, double eta) {
 
 void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_device,
              const int64_t* seg_first, const int64_t* seg_steps, int64_t n_seg, int32_t layout,
-             const jb_config& c, jb_fit* fit) {
+             const jb_config& c, jb_fit* fit, const Comm& cm, int64_t n_seg_global) {
     cudaStream_t st = ctx->stream;
     JB_CUDA(cudaSetDevice(ctx->device));
     const auto t_start = Clock::now();
@@ -359,6 +389,7 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
     if (n_seg <= 0) throw Error(INVALID_INPUT, "empty dataset");
     if (layout < 0 || layout > 2) throw Error(LAYOUT_ERROR, "unknown layout");
     fit->layout = layout;
+    fit->drop_local_last = layout == 0 && cm.rank + 1 < cm.world;
     SegTable& seg = fit->seg;
     seg.n_seg = n_seg;
     seg.h_first.assign(seg_first, seg_first + n_seg);
@@ -374,6 +405,7 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
         seg.total_steps += seg_steps[s];
     }
     if (max_last >= n_values) throw Error(INVALID_INPUT, "segment table exceeds the value buffer");
+    (void)n_seg_global;
     seg.first.alloc(n_seg, st);
     seg.steps.alloc(n_seg, st);
     seg.first.upload(seg_first, n_seg);
@@ -387,7 +419,7 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
         d_values = dvals.p;
     }
 
-    // ---- compression ----
+    // ---- compression (local segments) ----
     JB_TRACE("fit: values on device", st);
     compress_segments(d_values, seg, c.tol, c.max_piece_len, fit->pieces, st, &fit->fix_rounds);
     JB_TRACE("fit: compressed", st);
@@ -399,11 +431,29 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
     dvals.release();
     fit->phase_ms[0] = ms_since(t_start);
 
+    // global piece layout: this rank's pieces are [base, base + N) of N_glob
+    const int64_t N = fit->pieces.N;
+    int64_t base = 0, N_glob = N, steps_glob = seg.total_steps;
+    std::vector<int64_t> N_all(1, N);
+    if (cm.dist()) {
+        const int64_t mine[2] = {N, seg.total_steps};
+        std::vector<int64_t> all(2 * cm.world);
+        cm.allgather(mine, sizeof mine, all.data());
+        N_all.assign(cm.world, 0);
+        N_glob = steps_glob = 0;
+        for (int r = 0; r < cm.world; ++r) {
+            N_all[r] = all[2 * r];
+            if (r < cm.rank) base += all[2 * r];
+            N_glob += all[2 * r];
+            steps_glob += all[2 * r + 1];
+        }
+    }
+    fit->piece_base = base;
+
     // ---- digitize: scale_pieces ----
     auto t1 = Clock::now();
-    const int64_t N = fit->pieces.N;
     Scaled sc;
-    scale_pieces(fit->pieces, seg.total_steps, c.scl, sc, st);
+    scale_pieces(fit->pieces, steps_glob, c.scl, sc, st, &cm);
     JB_TRACE("fit: scaled", st);
     fit->scaling[0] = sc.scl;
     fit->scaling[1] = sc.sigma_len;
@@ -416,20 +466,30 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
     uint64_t k = 0;
     std::vector<double> backend_centers;
     DArr<uint32_t> labels;
-    DArr<uint64_t> sample;
-    DArr<uint32_t> sample_labels;
+    DArr<uint64_t> sample;         // piece index (this rank's numbering) per sample entry
+    DArr<uint32_t> sample_labels;  // per sample entry
+    int64_t n_sample_local = 0;
     bool assign_needed = false;
     switch (c.backend) {
         case JB_BACKEND_VQ: {
             validate_vq(c, 1.0);
-            if ((int64_t)c.k > N) throw Error(INVALID_INPUT, "kmeans: k exceeds points");
+            if ((int64_t)c.k > N_glob) throw Error(INVALID_INPUT, "kmeans: k exceeds points");
             DArr<uint64_t> raw;
             const uint64_t raw_count = (c.k + 1) * c.n_init + 4096;
             mt19937_64_generate(c.seed, raw_count, raw, st);
             uint64_t cursor = 0;
             KMeansOut km;
-            lloyd_best_device(sc.pts.p, nullptr, N, c.k, c.max_iters, c.n_init, raw.p, raw_count,
-                              &cursor, bb, km, st);
+            if (cm.dist()) {
+                DArr<uint32_t> gpos(std::max<int64_t>(N, 1), st);
+                DArr<uint64_t> lidx(std::max<int64_t>(N, 1), st);
+                k_iota_pos<<<gsz(N), 256, 0, st>>>(gpos.p, lidx.p, N, (uint64_t)base);
+                JB_LAUNCH_CHECK();
+                lloyd_best_dist(cm, sc.pts.p, lidx.p, gpos.p, N, (uint64_t)N_glob, c.k, c.max_iters,
+                                c.n_init, raw.p, raw_count, &cursor, bb, km, st);
+            } else {
+                lloyd_best_device(sc.pts.p, nullptr, N, c.k, c.max_iters, c.n_init, raw.p,
+                                  raw_count, &cursor, bb, km, st);
+            }
             k = c.k;
             backend_centers = km.centers;
             labels = std::move(km.labels);
@@ -439,7 +499,7 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
         }
         case JB_BACKEND_SVQ: {
             validate_vq(c, c.r);
-            const uint64_t S = (uint64_t)std::llround(c.r * (double)N);
+            const uint64_t S = (uint64_t)std::llround(c.r * (double)N_glob);
             if (S < c.k)
                 throw Error(INVALID_INPUT, "sampling_kmeans: sample of " + std::to_string(S) +
                                                " points is smaller than k=" +
@@ -448,17 +508,43 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
             const uint64_t raw_count = S + (c.k + 1) * c.n_init + 4096;
             mt19937_64_generate(c.seed, raw_count, raw, st);
             JB_TRACE("svq: engine draws", st);
-            uint64_t cursor = sample_indices_device((uint64_t)N, S, raw.p, raw_count, sample, st);
+            uint64_t cursor =
+                sample_indices_device((uint64_t)N_glob, S, raw.p, raw_count, sample, st);
             JB_TRACE("svq: sample indices", st);
             KMeansOut km;
-            lloyd_best_device(sc.pts.p, sample.p, (int64_t)S, c.k, c.max_iters, c.n_init, raw.p,
-                              raw_count, &cursor, bb, km, st);
+            if (cm.dist()) {  // the entries this rank owns, in sample order
+                DArr<uint8_t> flags(S, st);
+                k_own_flags<<<gsz((int64_t)S), 256, 0, st>>>(sample.p, S, (uint64_t)base,
+                                                             (uint64_t)N, flags.p);
+                JB_LAUNCH_CHECK();
+                DArr<uint32_t> gpos(S, st);
+                DArr<int64_t> nsel(1, st);
+                size_t tb = 0;
+                thrust::counting_iterator<uint32_t> it0(0);
+                cub::DeviceSelect::Flagged(nullptr, tb, it0, flags.p, gpos.p, nsel.p, (int64_t)S, st);
+                DArr<uint8_t> tmp(tb, st);
+                cub::DeviceSelect::Flagged(tmp.p, tb, it0, flags.p, gpos.p, nsel.p, (int64_t)S, st);
+                JB_LAUNCH_CHECK();
+                nsel.download(&n_sample_local, 1);
+                JB_CUDA(cudaStreamSynchronize(st));
+                DArr<uint64_t> lidx(std::max<int64_t>(n_sample_local, 1), st);
+                k_local_idx<<<gsz(n_sample_local), 256, 0, st>>>(sample.p, gpos.p, n_sample_local,
+                                                                 (uint64_t)base, lidx.p);
+                JB_LAUNCH_CHECK();
+                lloyd_best_dist(cm, sc.pts.p, lidx.p, gpos.p, n_sample_local, S, c.k, c.max_iters,
+                                c.n_init, raw.p, raw_count, &cursor, bb, km, st);
+                sample = std::move(lidx);
+            } else {
+                lloyd_best_device(sc.pts.p, sample.p, (int64_t)S, c.k, c.max_iters, c.n_init,
+                                  raw.p, raw_count, &cursor, bb, km, st);
+                n_sample_local = (int64_t)S;
+            }
             k = c.k;
             backend_centers = km.centers;
             sample_labels = std::move(km.labels);
             fit->work_tiles = km.work_tiles;
             fit->changed_labels = km.changed_labels;
-            labels.alloc(N, st);
+            labels.alloc(std::max<int64_t>(N, 1), st);
             assign_needed = true;
             fit->iterations = km.iterations;
             fit->sample_size = S;
@@ -466,26 +552,54 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
             break;
         }
         case JB_BACKEND_GA:
-        case JB_BACKEND_GA_AUTO: {
+        case JB_BACKEND_GA_AUTO:
+        case JB_BACKEND_GA_HIER: {
             double alpha = c.alpha;
             if (c.backend == JB_BACKEND_GA_AUTO) {
                 if (!(c.eta > 0.0)) throw Error(INVALID_INPUT, "AutoDigitizeConfig: eta must be > 0");
-                alpha = auto_alpha_host(seg.total_steps, N, c.tol, c.eta);
+                alpha = auto_alpha_host(steps_glob, N_glob, c.tol, c.eta);
             }
             validate_ga(c, alpha);
-            GAOut ga;
-            greedy_aggregate_device(sc.pts.p, N, alpha, c.sort_key, c.early_stop != 0, bb, ga,
-                                    st);
-            k = ga.groups;
-            labels = std::move(ga.labels);
-            fit->ga_rounds = ga.rounds;
-            break;
-        }
-        case JB_BACKEND_GA_HIER: {
-            validate_ga(c, c.alpha);
-            int rounds = 0;
-            k = ga_hier_device(sc.pts.p, N, c, bb, labels, rounds, st);
-            fit->ga_rounds = rounds;
+            // GA is one sequential sweep over all points in key order (SURVEY
+            // §8e): every rank runs it on the gathered points (replicated)
+            DArr<double> all_pts;
+            const double* gpts = sc.pts.p;
+            if (cm.dist()) {
+                int64_t mx = 0;
+                for (auto v : N_all) mx = std::max(mx, v);
+                std::vector<double> mine(2 * mx, 0.0), all(2 * mx * cm.world);
+                if (N) JB_CUDA(cudaMemcpy(mine.data(), sc.pts.p, 16 * N, cudaMemcpyDeviceToHost));
+                cm.allgather(mine.data(), 16 * mx, all.data());
+                std::vector<double> cat;
+                cat.reserve(2 * N_glob);
+                for (int r = 0; r < cm.world; ++r)
+                    cat.insert(cat.end(), all.begin() + 2 * mx * r,
+                               all.begin() + 2 * mx * r + 2 * N_all[r]);
+                all_pts.alloc(2 * N_glob, st);
+                all_pts.upload(cat.data(), 2 * N_glob);
+                gpts = all_pts.p;
+            }
+            DArr<uint32_t> glabels;
+            if (c.backend == JB_BACKEND_GA_HIER) {
+                int rounds = 0;
+                k = ga_hier_device(gpts, N_glob, c, bb, glabels, rounds, st);
+                fit->ga_rounds = rounds;
+            } else {
+                GAOut ga;
+                greedy_aggregate_device(gpts, N_glob, alpha, c.sort_key, c.early_stop != 0, bb, ga,
+                                        st);
+                k = ga.groups;
+                glabels = std::move(ga.labels);
+                fit->ga_rounds = ga.rounds;
+            }
+            if (cm.dist()) {
+                labels.alloc(std::max<int64_t>(N, 1), st);
+                if (N)
+                    JB_CUDA(cudaMemcpyAsync(labels.p, glabels.p + base, 4 * N,
+                                            cudaMemcpyDeviceToDevice, st));
+            } else {
+                labels = std::move(glabels);
+            }
             break;
         }
         default:
@@ -498,14 +612,26 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
     auto t3 = Clock::now();
     GroupStats gs;
     assign_and_stats(sc.pts.p, fit->pieces.len.p, N, backend_centers, k, bb, assign_needed,
-                     labels.p, gs, st, fit->pieces.max_len);
+                     labels.p, gs, st, sc.max_len_global, &cm, base);
     std::vector<double> centers(2 * k), mean_lengths(k);
     bool need_sample_stats = false;
     for (uint64_t g = 0; g < k; ++g) need_sample_stats |= gs.counts[g] == 0;
-    std::vector<uint64_t> sls, slc;
-    if (need_sample_stats && sample.p)
-        sample_len_stats(sample.p, sample_labels.p, (int64_t)fit->sample_size,
-                         fit->pieces.len.p, k, sls, slc, st);
+    std::vector<uint64_t> sls(k, 0), slc(k, 0);
+    if (need_sample_stats && c.backend == JB_BACKEND_SVQ) {
+        if (n_sample_local > 0)
+            sample_len_stats(sample.p, sample_labels.p, n_sample_local, fit->pieces.len.p, k, sls,
+                             slc, st);
+        if (cm.dist()) {
+            auto a = cm.gather(sls), b = cm.gather(slc);
+            std::fill(sls.begin(), sls.end(), 0);
+            std::fill(slc.begin(), slc.end(), 0);
+            for (int r = 0; r < cm.world; ++r)
+                for (uint64_t g = 0; g < k; ++g) {
+                    sls[g] += a[(size_t)r * k + g];
+                    slc[g] += b[(size_t)r * k + g];
+                }
+        }
+    }
     for (uint64_t g = 0; g < k; ++g) {
         if (gs.counts[g] > 0) {
             centers[2 * g] = gs.sum_x[g] / (double)gs.counts[g];
@@ -514,7 +640,7 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
         } else {
             centers[2 * g] = backend_centers.at(2 * g);
             centers[2 * g + 1] = backend_centers.at(2 * g + 1);
-            const uint64_t lc = slc.empty() ? 0 : slc[g];
+            const uint64_t lc = slc[g];
             mean_lengths[g] = lc > 0 ? (double)sls[g] / (double)lc : 1.0;
         }
     }
@@ -536,7 +662,7 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
         if (!std::isfinite(fit->centers[2 * r]) || !std::isfinite(fit->centers[2 * r + 1]))
             throw Error(INVALID_INPUT, "codebook: non-finite center");  // core.hpp:173-175
     }
-    if (k > 0) relabel(labels.p, N, rank_of, st);
+    if (k > 0 && N > 0) relabel(labels.p, N, rank_of, st);
     fit->labels = std::move(labels);
     fit->d_centers.alloc(std::max<uint64_t>(2 * k, 1), st);
     fit->d_mean_lengths.alloc(std::max<uint64_t>(k, 1), st);
@@ -549,12 +675,13 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
 }
 
 std::vector<int64_t> out_offsets_for(const std::vector<int64_t>& steps, int32_t layout,
-                                     int64_t* total) {
+                                     int64_t* total, bool drop_local_last = false) {
     std::vector<int64_t> off(steps.size());
     int64_t pos = 0;
     for (size_t s = 0; s < steps.size(); ++s) {
         off[s] = pos;
-        pos += (layout == 0 && s + 1 < steps.size()) ? steps[s] : steps[s] + 1;
+        const bool drop = layout == 0 && (s + 1 < steps.size() || drop_local_last);
+        pos += drop ? steps[s] : steps[s] + 1;
     }
     *total = pos;
     return off;
@@ -663,7 +790,34 @@ jb_status jb_fit_transform(jb_context* ctx, const double* values, int64_t n_valu
     jb_fit* fit = new jb_fit;
     const int rc = guarded([&] {
         run_fit(ctx, values, n_values, values_on_device != 0, seg_first, seg_steps, n_seg, layout,
-                *cfg, fit);
+                *cfg, fit, Comm{}, n_seg);
+    });
+    if (rc != JB_OK) {
+        delete fit;
+        cudaGetLastError();
+        return (jb_status)rc;
+    }
+    *out = fit;
+    return JB_OK;
+}
+
+jb_status jb_fit_transform_dist(jb_context* ctx, const jb_comm* comm, const double* values,
+                                int64_t n_values, int32_t values_on_device,
+                                const int64_t* seg_first, const int64_t* seg_steps,
+                                int64_t n_seg_local, int64_t n_seg_global, int32_t layout,
+                                const jb_config* cfg, jb_fit** out) {
+    *out = nullptr;
+    jb_fit* fit = new jb_fit;
+    const int rc = guarded([&] {
+        if (!comm || comm->world < 1 || comm->rank < 0 || comm->rank >= comm->world ||
+            (comm->world > 1 && !comm->allgather))
+            throw Error(INVALID_INPUT, "invalid communicator");
+        Comm cm;
+        cm.c = comm;
+        cm.rank = comm->rank;
+        cm.world = comm->world;
+        run_fit(ctx, values, n_values, values_on_device != 0, seg_first, seg_steps, n_seg_local,
+                layout, *cfg, fit, cm, n_seg_global);
     });
     if (rc != JB_OK) {
         delete fit;
@@ -683,7 +837,7 @@ int32_t jb_fit_layout(const jb_fit* f) { return f->layout; }
 
 int64_t jb_fit_reconstruct_size(const jb_fit* f) {
     int64_t total = 0;
-    out_offsets_for(f->seg.h_steps, f->layout, &total);
+    out_offsets_for(f->seg.h_steps, f->layout, &total, f->drop_local_last);
     return total;
 }
 
@@ -739,7 +893,7 @@ jb_status jb_fit_inverse_transform(jb_context* ctx, const jb_fit* f, double* out
         cudaStream_t st = ctx->stream;
         JB_CUDA(cudaSetDevice(ctx->device));
         int64_t total = 0;
-        const auto off = out_offsets_for(f->seg.h_steps, f->layout, &total);
+        const auto off = out_offsets_for(f->seg.h_steps, f->layout, &total, f->drop_local_last);
         DArr<int64_t> d_off(f->seg.n_seg, st);
         d_off.upload(off.data(), f->seg.n_seg);
         DArr<double> d_out;
@@ -763,7 +917,8 @@ jb_status jb_fit_inverse_transform(jb_context* ctx, const jb_fit* f, double* out
                      f->d_mean_lengths.p,
                      f->scaling[0],
                      f->scaling[1],
-                     f->scaling[2]};
+                     f->scaling[2],
+                     f->drop_local_last};
         inverse_transform_device(in, dst, st);
         if (!out_on_device) d_out.download(out_values, total);
         JB_CUDA(cudaStreamSynchronize(st));
@@ -816,7 +971,7 @@ jb_status jb_inverse_transform(jb_context* ctx, const double* centers, const dou
         d_c.upload(centers, 2 * k);
         d_ml.upload(mean_lengths, k);
         InverseIn in{d_lab.p, d_po.p, d_anc.p, d_sl.p, d_off.p, n_seg, N, layout, k, d_c.p,
-                     d_ml.p, scaling[0], scaling[1], scaling[2]};
+                     d_ml.p, scaling[0], scaling[1], scaling[2], false};
         inverse_transform_device(in, d_out.p, st);
         d_out.download(out_values, total);
         JB_CUDA(cudaStreamSynchronize(st));

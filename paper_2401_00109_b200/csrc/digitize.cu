@@ -142,44 +142,63 @@ int grid_for(int64_t n) {
 }  // namespace
 
 void scale_pieces(const Pieces& pc, int64_t total_steps, double scl, Scaled& out,
-                  cudaStream_t st) {
-    const int64_t N = pc.N;
+                  cudaStream_t st, const Comm* cm) {
+    const Comm one;
+    const Comm& C = cm ? *cm : one;
+    // global N, max|inc|, max len (identical fixed-point exponents on every rank)
+    int64_t N = pc.N;
+    double max_abs_inc = pc.max_abs_inc;
+    int32_t max_len = pc.max_len;
+    if (C.dist()) {
+        struct Loc {
+            int64_t n;
+            double mi;
+            int64_t ml;
+        } loc{pc.N, pc.max_abs_inc, pc.max_len};
+        std::vector<Loc> all(C.world);
+        C.allgather(&loc, sizeof loc, all.data());
+        N = 0;
+        for (const auto& l : all) {
+            N += l.n;
+            max_abs_inc = std::max(max_abs_inc, l.mi);
+            max_len = std::max<int32_t>(max_len, (int32_t)l.ml);
+        }
+    }
     if (N == 0) throw Error(INVALID_INPUT, "digitize: no pieces");
     if (scl < 0.0) throw Error(INVALID_INPUT, "scale_pieces: scl must be >= 0");
     const double n = (double)N;
-    // sum of (double)len over all pieces is exactly the total step count
     // sum of lens over all pieces == total steps of all segments (exact)
     DArr<unsigned long long> acc(6, st);
     acc.zero();
-    const int Einc = fx_exponent_for(pc.max_abs_inc * n * 1.0000001 + 1e-300);
-    {
+    const int Einc = fx_exponent_for(max_abs_inc * n * 1.0000001 + 1e-300);
+    if (pc.N > 0) {
         JB_PROF("scale_sum_inc", st);
-        k_sum_inc<<<grid_for(N), kTB, 0, st>>>(pc.inc.p, N, Einc, acc.p);
+        k_sum_inc<<<grid_for(pc.N), kTB, 0, st>>>(pc.inc.p, pc.N, Einc, acc.p);
     }
     JB_LAUNCH_CHECK();
     JB_TRACE("scale: sum inc", st);
-    unsigned long long h[6];
-    acc.download(h, 2);
-    JB_CUDA(cudaStreamSynchronize(st));
+    std::vector<unsigned long long> h = acc.to_host(2);
+    h = C.sum_i128(h);
     // mean_len: sequential double sum of integer lens is exact (< 2^53)
     const double mean_len = (double)total_steps / n;
-    const double mean_inc = fx_to_double(fx_load(h), Einc) / n;
+    const double mean_inc = fx_to_double(fx_load(h.data()), Einc) / n;
 
-    const double dlmax = std::max((double)pc.max_len - mean_len, mean_len - 1.0) + 1.0;
-    const double dimax = pc.max_abs_inc + std::fabs(mean_inc) + 1e-300;
+    const double dlmax = std::max((double)max_len - mean_len, mean_len - 1.0) + 1.0;
+    const double dimax = max_abs_inc + std::fabs(mean_inc) + 1e-300;
     const int El = fx_exponent_for(dlmax * dlmax * n * 1.001 + 1e-300);
     const int Ei = fx_exponent_for(dimax * dimax * n * 1.001 + 1e-300);
     acc.zero();
-    {
+    if (pc.N > 0) {
         JB_PROF("scale_sum_var", st);
-        k_sum_var<<<grid_for(N), kTB, 0, st>>>(pc.len.p, pc.inc.p, N, mean_len, mean_inc, El, Ei,
-                                          acc.p);
+        k_sum_var<<<grid_for(pc.N), kTB, 0, st>>>(pc.len.p, pc.inc.p, pc.N, mean_len, mean_inc, El,
+                                                 Ei, acc.p);
     }
     JB_LAUNCH_CHECK();
-    acc.download(h, 4);
-    JB_CUDA(cudaStreamSynchronize(st));
-    const double var_len = fx_to_double(fx_load(h), El);
-    const double var_inc = fx_to_double(fx_load(h + 2), Ei);
+    h = acc.to_host(4);
+    h = C.sum_i128(h);
+    JB_TRACE("scale: variances", st);
+    const double var_len = fx_to_double(fx_load(h.data()), El);
+    const double var_inc = fx_to_double(fx_load(h.data() + 2), Ei);
     double sl = N > 1 ? std::sqrt(var_len / (n - 1.0)) : 0.0;
     double si = N > 1 ? std::sqrt(var_inc / (n - 1.0)) : 0.0;
     if (sl <= 0.0) sl = 1.0;
@@ -188,24 +207,33 @@ void scale_pieces(const Pieces& pc, int64_t total_steps, double scl, Scaled& out
     out.sigma_len = sl;
     out.sigma_inc = si;
 
-    JB_TRACE("scale: variances", st);
-    out.pts.alloc(2 * N, st);
+    out.pts.alloc(2 * pc.N, st);
     JB_TRACE("scale: alloc points", st);
     DArr<unsigned long long> bb(4, st);
     unsigned long long init[4] = {~0ULL, 0ULL, ~0ULL, 0ULL};
     bb.upload(init, 4);
-    {
+    if (pc.N > 0) {
         JB_PROF("scale_points", st);
-        k_scale<<<grid_for(N), kTB, 0, st>>>(pc.len.p, pc.inc.p, N, scl, sl, si, out.pts.p, bb.p);
+        k_scale<<<grid_for(pc.N), kTB, 0, st>>>(pc.len.p, pc.inc.p, pc.N, scl, sl, si, out.pts.p,
+                                               bb.p);
     }
     JB_LAUNCH_CHECK();
-    unsigned long long hb[4];
-    bb.download(hb, 4);
-    JB_CUDA(cudaStreamSynchronize(st));
+    std::vector<unsigned long long> hb = bb.to_host(4);
+    if (C.dist()) {
+        auto all = C.gather(hb);
+        for (int r = 1; r < C.world; ++r) {
+            hb[0] = std::min(hb[0], all[4 * r]);
+            hb[1] = std::max(hb[1], all[4 * r + 1]);
+            hb[2] = std::min(hb[2], all[4 * r + 2]);
+            hb[3] = std::max(hb[3], all[4 * r + 3]);
+        }
+    }
     out.xmin = ord_to_double(hb[0]);
     out.xmax = ord_to_double(hb[1]);
     out.ymin = ord_to_double(hb[2]);
     out.ymax = ord_to_double(hb[3]);
+    out.N_global = N;
+    out.max_len_global = max_len;
 }
 
 // ---------------------------------------------------------------------------
@@ -348,7 +376,7 @@ __global__ void k_gather(const double2* __restrict__ pts, const uint64_t* __rest
 void assign_and_stats(const double* d_pts, const int32_t* d_len, int64_t n,
                       const std::vector<double>& centers, uint64_t k, const BBox& bb,
                       bool do_assign, uint32_t* d_labels, GroupStats& gs, cudaStream_t st,
-                      int32_t max_len) {
+                      int32_t max_len, const Comm* cm, int64_t first_base) {
     DArr<double> dc(std::max<uint64_t>(2 * k, 1), st);
     if (centers.size() >= 2 * k) dc.upload(centers.data(), 2 * k);  // GA: no centers needed
     else if (do_assign) throw Error(INTERNAL, "assignment without centers");
@@ -357,6 +385,7 @@ void assign_and_stats(const double* d_pts, const int32_t* d_len, int64_t n,
     JB_CUDA(cudaMemsetAsync(acc.p + 2 * k, 0xFF, sizeof(unsigned long long) * k, st));
     const double mx = std::max(std::fabs(bb.xmin), std::fabs(bb.xmax));
     const double my = std::max(std::fabs(bb.ymin), std::fabs(bb.ymax));
+    (void)n;
     // biased per-element fixed point: fx(v) + B in [0, 2^62)
     auto exp_for = [](double m) {
         const int e = fx_exponent_for(m + 1e-300);  // 125 - e', m < 2^e'
@@ -402,15 +431,49 @@ void assign_and_stats(const double* d_pts, const int32_t* d_len, int64_t n,
     }
     JB_LAUNCH_CHECK();
     std::vector<unsigned long long> h = acc.to_host(7 * k);
-    gs.counts.assign(h.begin(), h.begin() + k);
-    gs.len_sums.assign(h.begin() + k, h.begin() + 2 * k);
-    gs.first_seen.assign(h.begin() + 2 * k, h.begin() + 3 * k);
+    // exact per-cluster records: count, len sum, first index (global), unbiased sums
+    std::vector<unsigned long long> rec(7 * k);
+    for (uint64_t c = 0; c < k; ++c) {
+        const i128 cnt = (i128)h[c];
+        const u128 ux = (u128)(fx_load(&h[3 * k + 2 * c]) - cnt * (i128)Bx);
+        const u128 uy = (u128)(fx_load(&h[5 * k + 2 * c]) - cnt * (i128)By);
+        rec[7 * c + 0] = h[c];
+        rec[7 * c + 1] = h[k + c];
+        rec[7 * c + 2] = h[2 * k + c] == ~0ULL ? ~0ULL : h[2 * k + c] + (unsigned long long)first_base;
+        rec[7 * c + 3] = (unsigned long long)ux;
+        rec[7 * c + 4] = (unsigned long long)(ux >> 64);
+        rec[7 * c + 5] = (unsigned long long)uy;
+        rec[7 * c + 6] = (unsigned long long)(uy >> 64);
+    }
+    if (cm && cm->dist()) {  // group statistics of all ranks (exact integers)
+        const auto all = cm->gather(rec);
+        for (int r = 1; r < cm->world; ++r)
+            for (uint64_t c = 0; c < k; ++c) {
+                const unsigned long long* o = &all[(size_t)r * 7 * k + 7 * c];
+                rec[7 * c + 0] += o[0];
+                rec[7 * c + 1] += o[1];
+                rec[7 * c + 2] = std::min(rec[7 * c + 2], o[2]);
+                u128 x = ((u128)rec[7 * c + 4] << 64) | rec[7 * c + 3];
+                u128 y = ((u128)rec[7 * c + 6] << 64) | rec[7 * c + 5];
+                x += ((u128)o[4] << 64) | o[3];
+                y += ((u128)o[6] << 64) | o[5];
+                rec[7 * c + 3] = (unsigned long long)x;
+                rec[7 * c + 4] = (unsigned long long)(x >> 64);
+                rec[7 * c + 5] = (unsigned long long)y;
+                rec[7 * c + 6] = (unsigned long long)(y >> 64);
+            }
+    }
+    gs.counts.resize(k);
+    gs.len_sums.resize(k);
+    gs.first_seen.resize(k);
     gs.sum_x.resize(k);
     gs.sum_y.resize(k);
     for (uint64_t c = 0; c < k; ++c) {
-        const i128 cnt = (i128)gs.counts[c];
-        gs.sum_x[c] = fx_to_double(fx_load(&h[3 * k + 2 * c]) - cnt * (i128)Bx, Ex);
-        gs.sum_y[c] = fx_to_double(fx_load(&h[5 * k + 2 * c]) - cnt * (i128)By, Ey);
+        gs.counts[c] = rec[7 * c];
+        gs.len_sums[c] = rec[7 * c + 1];
+        gs.first_seen[c] = rec[7 * c + 2];
+        gs.sum_x[c] = fx_to_double((i128)(((u128)rec[7 * c + 4] << 64) | rec[7 * c + 3]), Ex);
+        gs.sum_y[c] = fx_to_double((i128)(((u128)rec[7 * c + 6] << 64) | rec[7 * c + 5]), Ey);
     }
 }
 

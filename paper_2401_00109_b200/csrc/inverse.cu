@@ -191,7 +191,8 @@ __global__ void __launch_bounds__(256) k_inv_fill(InverseIn in, const double* __
         }
         const long long L = __shfl_sync(FULL, incl, 31);
         const int64_t pos = co.ck_pos[g];
-        const bool drop_last = in.layout == 0 && s + 1 < in.n_seg && base + GROUP >= b;
+        const bool drop_last = in.layout == 0 && (s + 1 < in.n_seg || in.drop_local_last) &&
+                               base + GROUP >= b;
         for (long long q0 = 1; q0 <= L; q0 += 32) {
             const long long q = q0 + lane;  // 1-based sample within the group
             int last_below = -1;  // last piece with incl < q (fixed 5 steps)

@@ -8,9 +8,47 @@
 #include <utility>
 #include <vector>
 
+#include "../../include/jabba_b200.h"
 #include "jb_common.cuh"
 
 namespace jb {
+
+// Host side of the distributed fit's collectives: an exact allgather of host
+// bytes (rank order). world == 1 means single-GPU.
+struct Comm {
+    const jb_comm* c = nullptr;
+    int rank = 0, world = 1;
+    bool dist() const { return world > 1; }
+    void allgather(const void* send, size_t bytes, void* recv) const {
+        if (!dist()) {
+            memcpy(recv, send, bytes);
+            return;
+        }
+        if (c->allgather(c->user, send, bytes, recv) != 0)
+            throw Error(NCCL_ERROR, "allgather callback failed");
+    }
+    template <class T>
+    std::vector<T> gather(const std::vector<T>& v) const {
+        std::vector<T> out(v.size() * world);
+        allgather(v.data(), sizeof(T) * v.size(), out.data());
+        return out;
+    }
+    // exact element-wise sum of int128 vectors held as (lo, hi) u64 pairs
+    std::vector<unsigned long long> sum_i128(const std::vector<unsigned long long>& v) const {
+        if (!dist()) return v;
+        auto all = gather(v);
+        std::vector<unsigned long long> out(v.size(), 0);
+        for (int r = 0; r < world; ++r)
+            for (size_t i = 0; i + 1 < v.size(); i += 2) {
+                const u128 a = ((u128)out[i + 1] << 64) | out[i];
+                const u128 b = ((u128)all[r * v.size() + i + 1] << 64) | all[r * v.size() + i];
+                const u128 c2 = a + b;
+                out[i] = (unsigned long long)c2;
+                out[i + 1] = (unsigned long long)(c2 >> 64);
+            }
+        return out;
+    }
+};
 
 // Per-stream, size-bucketed cache of device buffers (api.cu). Buffers freed
 // on a stream are reused only by later work on the same stream, so reuse is
@@ -121,13 +159,16 @@ void compress_segments(const double* d_values, const SegTable& seg, double tol,
 // Scaling (digitize.cu): scale_pieces digitization.hpp:25-59
 
 struct Scaled {
-    DArr<double> pts;  // 2N interleaved (x, y)
+    DArr<double> pts;  // 2N interleaved (x, y) (this rank's pieces)
     double scl = 1.0, sigma_len = 1.0, sigma_inc = 1.0;
-    double xmin = 0, xmax = 0, ymin = 0, ymax = 0;  // bounding box of pts
+    double xmin = 0, xmax = 0, ymin = 0, ymax = 0;  // bounding box of ALL points
+    int64_t N_global = 0;
+    int32_t max_len_global = 0;
 };
 
+// total_steps: of ALL ranks' segments; cm: null or world == 1 for one GPU
 void scale_pieces(const Pieces& pc, int64_t total_steps, double scl, Scaled& out,
-                  cudaStream_t st);
+                  cudaStream_t st, const Comm* cm = nullptr);
 
 struct BBox {
     double xmin, xmax, ymin, ymax;
@@ -162,6 +203,15 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
                        uint64_t raw_count, uint64_t* cursor, const BBox& bb, KMeansOut& out,
                        cudaStream_t st);
 
+// Distributed variant: this rank holds the sample entries it owns -- local
+// piece index d_lidx[i] and global sample position d_gpos[i] (ascending), n
+// entries -- of a global sample of S points. Same results on every rank,
+// equal to lloyd_best_device on the whole sample.
+void lloyd_best_dist(const Comm& cm, const double* d_pts, const uint64_t* d_lidx,
+                     const uint32_t* d_gpos, int64_t n, uint64_t S, uint64_t k, uint64_t max_iters,
+                     uint64_t n_init, const uint64_t* d_raw, uint64_t raw_count, uint64_t* cursor,
+                     const BBox& bb, KMeansOut& out, cudaStream_t st);
+
 // Per-point nearest center (clustering.hpp:146-163) with exact tie rule, plus
 // group statistics for digitize (digitization.hpp:217-231).
 struct GroupStats {
@@ -171,7 +221,7 @@ struct GroupStats {
 void assign_and_stats(const double* d_pts, const int32_t* d_len, int64_t n,
                       const std::vector<double>& centers, uint64_t k, const BBox& bb,
                       bool do_assign, uint32_t* d_labels, GroupStats& gs, cudaStream_t st,
-                      int32_t max_len);
+                      int32_t max_len, const Comm* cm = nullptr, int64_t first_base = 0);
 
 void relabel(uint32_t* d_labels, int64_t n, const std::vector<uint32_t>& rank_of,
              cudaStream_t st);
@@ -211,6 +261,7 @@ struct InverseIn {
     const double* centers;        // 2k (device)
     const double* mean_lengths;   // k (device)
     double scl, sigma_len, sigma_inc;
+    bool drop_local_last;         // distributed stitched fit: this rank is not the last
 };
 // Writes reconstructed samples into d_out. Throws on unknown_symbol /
 // invalid_piece exactly where the reference throws.

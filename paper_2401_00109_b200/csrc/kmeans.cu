@@ -150,6 +150,18 @@ __global__ void __launch_bounds__(320) k_mt_jump_generate(uint64_t seed, uint64_
     }
 }
 
+// libstdc++ _S_nd<unsigned __int128> on the host (distributed seeding)
+inline bool lemire_host(uint64_t x, uint64_t erange, uint64_t& r) {
+    const u128 prod = (u128)x * erange;
+    const uint64_t low = (uint64_t)prod;
+    r = (uint64_t)(prod >> 64);
+    if (low < erange) {
+        const uint64_t thresh = (0 - erange) % erange;
+        if (low < thresh) return false;
+    }
+    return true;
+}
+
 // libstdc++ _S_nd<unsigned __int128>: returns true if the draw is accepted
 __device__ __forceinline__ bool lemire(uint64_t x, uint64_t erange, uint64_t& r) {
     const u128 prod = (u128)x * erange;
@@ -524,8 +536,9 @@ __global__ void k_pick_first(const uint64_t* __restrict__ raw, uint64_t n, SeedS
 __global__ void k_d2_cull(const double4* __restrict__ tbox, const double* __restrict__ tmax,
                           int64_t ntiles, const double2* __restrict__ spts,
                           const uint32_t* __restrict__ pos, const SeedState* __restrict__ ss,
-                          uint32_t* __restrict__ work, unsigned long long* __restrict__ nwork) {
-    const double2 c = spts[pos[ss->last]];
+                          uint32_t* __restrict__ work, unsigned long long* __restrict__ nwork,
+                          const double2* __restrict__ cur) {
+    const double2 c = cur ? *cur : spts[pos[ss->last]];
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntiles;
          t += (int64_t)gridDim.x * blockDim.x) {
         double dmin2, dmax2;
@@ -542,11 +555,15 @@ __global__ void __launch_bounds__(256) k_d2_tiles(
     const uint32_t* __restrict__ pos, int64_t n, const uint32_t* __restrict__ work,
     const unsigned long long* __restrict__ nwork, double* __restrict__ tmax,
     double* __restrict__ d2s, const SeedState* __restrict__ ss, int init, int E,
-    unsigned long long* __restrict__ part) {
+    unsigned long long* __restrict__ part, const double2* __restrict__ cur,
+    const uint32_t* __restrict__ gkey) {
+    // cur: center given directly (distributed fit); gkey: partial-sum block
+    // key per sorted point (global sample position) instead of orig
     const int lane = threadIdx.x & 31;
     const int64_t ntiles = (n + TILE - 1) / TILE;
     const int64_t nw = init ? ntiles : (int64_t)*nwork;
-    const double2 c = spts[pos[ss->last]];
+    const double2 c = cur ? *cur : spts[pos[ss->last]];
+    const uint32_t* key = gkey ? gkey : orig;
     for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nw;
          w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int64_t t = init ? w : (int64_t)work[w];
@@ -559,7 +576,7 @@ __global__ void __launch_bounds__(256) k_d2_tiles(
             if (r < n) {
                 p[i] = spts[r];
                 old[i] = init ? 0.0 : d2s[r];
-                o[i] = orig[r];
+                o[i] = key[r];
             }
         }
         double mx = 0.0;
@@ -1038,7 +1055,12 @@ struct LloydCtx {
     int64_t ntiles = 0;
     DArr<uint32_t> tlab, tnew, work;
     DArr<unsigned long long> nwork, diag;
+    DArr<unsigned long long> dacc;  // distributed fit: this rank's deltas (5k)
+    bool use_dacc = false;
     ClusterAcc cacc() { return ClusterAcc{acc.p, acc.p + 2 * k, acc.p + 4 * k}; }
+    ClusterAcc tacc() {  // where the assignment writes
+        return use_dacc ? ClusterAcc{dacc.p, dacc.p + 2 * k, dacc.p + 4 * k} : cacc();
+    }
     size_t smem() const { return sizeof(double) * 2 * k + sizeof(unsigned long long) * 5 * k; }
     int grid() const {
         return (int)std::max<int64_t>(1, std::min<int64_t>((n + LL_TB - 1) / LL_TB,
@@ -1063,6 +1085,7 @@ __global__ void k_iter_end(int* __restrict__ state, unsigned long long* __restri
 
 void lloyd_assign(LloydCtx& L, bool full, bool gate_on_empties) {
     const int* gate = gate_on_empties ? L.empties.p + L.k : nullptr;
+    if (L.n == 0) return;  // a rank may hold no sample points
     {
         JB_PROF("lloyd_grid", L.st);
         const int ncell = L.cg.G * L.cg.G;
@@ -1080,7 +1103,7 @@ void lloyd_assign(LloydCtx& L, bool full, bool gate_on_empties) {
     JB_PROF("lloyd_assign", L.st);
     k_lloyd_work<<<L.grid(), LL_TB, L.smem(), L.st>>>(
         L.spts, L.n, L.centers.p, L.k, L.cg, L.labs.p, L.work.p, L.nwork.p, L.tnew.p, L.tlab.p,
-        full ? 1 : 0, L.Ex, L.Ey, L.cacc(), L.flags.p, gate);
+        full ? 1 : 0, L.Ex, L.Ey, L.tacc(), L.flags.p, gate);
     JB_LAUNCH_CHECK();
 }
 
@@ -1229,7 +1252,8 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
         {
             JB_PROF("d2_update", st);
             k_d2_tiles<<<tile_grid, 256, 0, st>>>(spts.p, orig.p, pos.p, n, nullptr, nullptr,
-                                                  tmax.p, d2s.p, ss.p, 1, Ed2, part.p);
+                                                  tmax.p, d2s.p, ss.p, 1, Ed2, part.p, nullptr,
+                                                  nullptr);
         }
         JB_LAUNCH_CHECK();
         for (uint64_t c = 1; c < k; ++c) {
@@ -1243,10 +1267,10 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
                 JB_PROF("d2_update", st);
                 JB_CUDA(cudaMemsetAsync(d2_nwork.p, 0, 8, st));
                 k_d2_cull<<<cull_grid, 256, 0, st>>>(tbox.p, tmax.p, ntiles, spts.p, pos.p, ss.p,
-                                                     d2_work.p, d2_nwork.p);
+                                                     d2_work.p, d2_nwork.p, nullptr);
                 k_d2_tiles<<<tile_grid, 256, 0, st>>>(spts.p, orig.p, pos.p, n, d2_work.p,
                                                       d2_nwork.p, tmax.p, d2s.p, ss.p, 0, Ed2,
-                                                      part.p);
+                                                      part.p, nullptr, nullptr);
                 JB_LAUNCH_CHECK();
             }
         }
@@ -1321,6 +1345,504 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
             out.labels.alloc(n, st);
             k_unsort_labels<<<grid_cap(n), 256, 0, st>>>(L.labs.p, orig.p, n, out.labels.p);
             JB_LAUNCH_CHECK();
+            out.iterations = it;
+            out.sse = sse;
+        }
+    }
+    JB_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace jb
+
+// ===========================================================================
+// Distributed k-means++ (one joint fit sharded over ranks).
+//
+// Every rank holds the sample entries whose pieces it owns (global sample
+// positions gpos, ascending). All exchanges are exact integers or the
+// owner's exact doubles, so every rank makes the same decisions as the
+// single-GPU path:
+//  * D^2 round: this rank's per-global-block partial sums -> allgather ->
+//    exact global prefix on the host -> block; the block's 2048 weights from
+//    their owners -> element; the chosen point's coordinates from its owner.
+//  * Lloyd iteration: this rank's exact cluster-sum deltas and change count
+//    -> allgather -> identical global accumulators on every rank.
+//  * Empty clusters: per-rank farthest candidates -> global (max d, lowest
+//    global sample position) -> applied by every rank (labels by the owner).
+
+namespace jb {
+namespace {
+
+__global__ void k_gkey(const uint32_t* __restrict__ gpos, const uint32_t* __restrict__ orig,
+                       int64_t n, uint32_t* __restrict__ gkey) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x)
+        gkey[r] = gpos[orig[r]];
+}
+
+// local entry holding global sample position q (gpos ascending), or -1
+__global__ void k_find_gpos(const uint32_t* __restrict__ gpos, int64_t n, uint64_t q,
+                            long long* __restrict__ out) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t m = (lo + hi) >> 1;
+        if (gpos[m] < q) lo = m + 1;
+        else hi = m;
+    }
+    *out = (lo < n && gpos[lo] == q) ? lo : -1;
+}
+
+// d2 of this rank's entries of global block b into w[0..R) (zeros elsewhere)
+__global__ void k_block_weights(const uint32_t* __restrict__ gpos, const uint32_t* __restrict__ pos,
+                                int64_t n, const double* __restrict__ d2s, uint64_t b,
+                                double* __restrict__ w) {
+    const uint64_t q0 = b * D2_R, q1 = q0 + D2_R;
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t m = (lo + hi) >> 1;
+        if (gpos[m] < q0) lo = m + 1;
+        else hi = m;
+    }
+    for (int64_t i = lo + threadIdx.x; i < n && gpos[i] < q1; i += blockDim.x)
+        w[gpos[i] - q0] = d2s[pos[i]];
+}
+
+// largest global position with d2 > 0 (roundoff spill of weighted_index)
+__global__ void k_last_positive(const uint32_t* __restrict__ gpos, const uint32_t* __restrict__ pos,
+                                int64_t n, const double* __restrict__ d2s,
+                                long long* __restrict__ out) {
+    long long best = -1;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+        if (d2s[pos[i]] > 0.0) best = max(best, (long long)gpos[i]);
+    for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, best);
+}
+
+// acc += delta (sx, sy as int128; counts as two's complement u64)
+__global__ void k_add_acc(unsigned long long* __restrict__ acc,
+                          const unsigned long long* __restrict__ delta, int k) {
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < 2 * k; c += gridDim.x * blockDim.x) {
+        fx_atomic_add(acc + 2 * c, fx_load(delta + 2 * c));  // sx[k], sy[k] interleaved pairs
+    }
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < k; c += gridDim.x * blockDim.x)
+        acc[4 * k + c] += delta[4 * k + c];
+}
+
+// re-seed empty cluster c at the globally chosen far point (update_means :193-196)
+__global__ void k_repair_dist(unsigned long long* __restrict__ acc, double* __restrict__ centers,
+                              uint32_t* __restrict__ labs, uint32_t* __restrict__ tlab, int k,
+                              int Ex, int Ey, int c, int donor, double px, double py,
+                              long long owner_r) {
+    const i128 fx = fx_from_double(px, Ex), fy = fx_from_double(py, Ey);
+    ClusterAcc a{acc, acc + 2 * k, acc + 4 * k};
+    fx_atomic_add(a.sx + 2 * donor, -fx);
+    fx_atomic_add(a.sy + 2 * donor, -fy);
+    a.cnt[donor] -= 1;
+    a.sx[2 * c] = a.sx[2 * c + 1] = 0;
+    a.sy[2 * c] = a.sy[2 * c + 1] = 0;
+    fx_atomic_add(a.sx + 2 * c, fx);
+    fx_atomic_add(a.sy + 2 * c, fy);
+    a.cnt[c] = 1;
+    centers[2 * c] = px;
+    centers[2 * c + 1] = py;
+    if (owner_r >= 0) {
+        labs[owner_r] = (uint32_t)c;
+        tlab[owner_r / TILE] = MIXED;
+    }
+}
+
+struct FarRec {
+    double d;
+    long long gp;  // global sample position (INT64_MAX: none)
+    long long r;   // this rank's sorted position
+    double x, y;
+    long long donor;
+};
+
+}  // namespace
+
+void lloyd_best_dist(const Comm& cm, const double* d_pts, const uint64_t* d_lidx,
+                     const uint32_t* d_gpos, int64_t n, uint64_t S, uint64_t k, uint64_t max_iters,
+                     uint64_t n_init, const uint64_t* d_raw, uint64_t raw_count, uint64_t* cursor,
+                     const BBox& bb, KMeansOut& out, cudaStream_t st) {
+    if (k < 1) throw Error(INVALID_INPUT, "d2_seed: k must be >= 1");
+    if (k > S) throw Error(INVALID_INPUT, "d2_seed: k exceeds points");
+    if (k > 2048) throw Error(INVALID_INPUT, "k > 2048 is not supported by the Lloyd kernel");
+    if (S >= (1ULL << 32)) throw Error(INVALID_INPUT, "k-means on more than 2^32 points");
+    const double2* pts = reinterpret_cast<const double2*>(d_pts);
+    const double mx = std::max(std::fabs(bb.xmin), std::fabs(bb.xmax));
+    const double my = std::max(std::fabs(bb.ymin), std::fabs(bb.ymax));
+    const double wx = bb.xmax - bb.xmin, wy = bb.ymax - bb.ymin;
+    const double d2max = (wx * wx + wy * wy) * (1.0 + 1e-9) + 1e-300;
+    const int Ed2 = fx_exponent_for(d2max * (double)S * 1.001);
+    const int64_t nn = std::max<int64_t>(n, 1);
+
+    // ---- Morton order of this rank's points ----
+    DArr<double2> spts(nn, st);
+    DArr<uint32_t> orig(nn, st), pos(nn, st), gkey(nn, st);
+    if (n > 0) {
+        DArr<uint32_t> keys(n, st), skeys(n, st), vals(n, st);
+        const double sx = wx > 0 ? 65535.0 / wx : 0.0, sy = wy > 0 ? 65535.0 / wy : 0.0;
+        k_morton<<<grid_cap(n), 256, 0, st>>>(pts, d_lidx, n, bb.xmin, sx, bb.ymin, sy, keys.p,
+                                              vals.p);
+        JB_LAUNCH_CHECK();
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.p, skeys.p, vals.p, orig.p, n, 0, 32,
+                                        st);
+        DArr<uint8_t> tmp(tb, st);
+        cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.p, skeys.p, vals.p, orig.p, n, 0, 32, st);
+        k_sorted_gather<<<grid_cap(n), 256, 0, st>>>(pts, d_lidx, orig.p, n, spts.p, pos.p);
+        k_gkey<<<grid_cap(n), 256, 0, st>>>(d_gpos, orig.p, n, gkey.p);
+        JB_LAUNCH_CHECK();
+    }
+    const int64_t ntiles = (n + TILE - 1) / TILE;
+    DArr<double4> tbox(std::max<int64_t>(ntiles, 1), st);
+    DArr<double> tmax(std::max<int64_t>(ntiles, 1), st);
+    const int tile_grid = (int)std::max<int64_t>(1, std::min<int64_t>((ntiles + 7) / 8, kSMs * 8));
+    if (n > 0) k_tile_boxes<<<tile_grid, 256, 0, st>>>(spts.p, n, tbox.p);
+    JB_LAUNCH_CHECK();
+
+    LloydCtx L;
+    L.spts = spts.p;
+    L.orig = gkey.p;  // tie-breaks by global sample position
+    L.pos = pos.p;
+    L.n = n;
+    L.k = (int)k;
+    L.Ex = fx_exponent_for(mx * (double)S * 1.001 + 1e-300);
+    L.Ey = fx_exponent_for(my * (double)S * 1.001 + 1e-300);
+    L.st = st;
+    L.centers.alloc(2 * k, st);
+    L.labs.alloc(nn, st);
+    L.acc.alloc(5 * k, st);
+    L.dacc.alloc(5 * k, st);
+    L.use_dacc = true;
+    L.flags.alloc(1, st);
+    L.empties.alloc(k + 3, st);
+    L.empties.zero();
+    L.diag.alloc(2, st);
+    {
+        const int G = grid_side_for(k), cap = 32;
+        L.cg = make_grid_desc(bb.xmin, bb.xmax, bb.ymin, bb.ymax, G, cap);
+        L.cg_cnt.alloc((size_t)G * G, st);
+        L.cg_cand.alloc((size_t)G * G * cap, st);
+        L.cg.cnt = L.cg_cnt.p;
+        L.cg.cand = L.cg_cand.p;
+    }
+    L.tbox = tbox.p;
+    L.ntiles = ntiles;
+    L.tlab.alloc(std::max<int64_t>(ntiles, 1), st);
+    L.tnew.alloc(std::max<int64_t>(ntiles, 1), st);
+    L.work.alloc(std::max<int64_t>(ntiles, 1), st);
+    L.nwork.alloc(1, st);
+    JB_CUDA(cudaFuncSetAttribute(k_lloyd_work, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)L.smem()));
+
+    const uint64_t nblocks = (S + D2_R - 1) / D2_R;
+    DArr<uint32_t> d2_work(std::max<int64_t>(ntiles, 1), st);
+    DArr<unsigned long long> d2_nwork(1, st);
+    const int cull_grid =
+        (int)std::max<int64_t>(1, std::min<int64_t>((ntiles + 255) / 256, kSMs * 16));
+    DArr<double> d2s(nn, st);
+    DArr<unsigned long long> part(2 * nblocks, st);
+    DArr<SeedState> ss(1, st);
+    DArr<double2> cur(1, st);
+    DArr<double> wblk(D2_R, st);
+    DArr<long long> dll(1, st);
+
+    // the engine draws the seeding consumes (identical on every rank)
+    const uint64_t tail_n = std::min<uint64_t>(raw_count - *cursor, (k + 1) * n_init + 4096);
+    std::vector<uint64_t> raw_h(tail_n);
+    JB_CUDA(cudaMemcpyAsync(raw_h.data(), d_raw + *cursor, 8 * tail_n, cudaMemcpyDeviceToHost, st));
+    JB_CUDA(cudaStreamSynchronize(st));
+    const uint64_t raw_base = *cursor;
+    auto draw = [&](uint64_t at) {
+        if (at - raw_base >= tail_n) throw Error(INTERNAL, "rng stream exhausted");
+        return raw_h[at - raw_base];
+    };
+
+    // coordinates of global sample position q, from its owner
+    auto center_of = [&](uint64_t q) -> std::pair<double, double> {
+        struct Rec {
+            long long has;
+            double x, y;
+        } rec{0, 0.0, 0.0};
+        if (n > 0) {
+            k_find_gpos<<<1, 1, 0, st>>>(d_gpos, n, q, dll.p);
+            long long i = -1;
+            dll.download(&i, 1);
+            JB_CUDA(cudaStreamSynchronize(st));
+            if (i >= 0) {
+                uint64_t li;
+                double2 p;
+                JB_CUDA(cudaMemcpyAsync(&li, d_lidx + i, 8, cudaMemcpyDeviceToHost, st));
+                JB_CUDA(cudaStreamSynchronize(st));
+                JB_CUDA(cudaMemcpyAsync(&p, pts + li, 16, cudaMemcpyDeviceToHost, st));
+                JB_CUDA(cudaStreamSynchronize(st));
+                rec = Rec{1, p.x, p.y};
+            }
+        }
+        std::vector<Rec> all(cm.world);
+        cm.allgather(&rec, sizeof rec, all.data());
+        for (const auto& r : all)
+            if (r.has) return {r.x, r.y};
+        throw Error(INTERNAL, "distributed seeding: no owner for a sample position");
+    };
+
+    auto exchange_deltas = [&]() -> unsigned long long {  // returns global changed count
+        std::vector<unsigned long long> h(5 * k + 1);
+        L.dacc.download(h.data(), 5 * k);
+        L.flags.download(h.data() + 5 * k, 1);
+        JB_CUDA(cudaStreamSynchronize(st));
+        const auto all = cm.gather(h);
+        std::vector<unsigned long long> sum(5 * k + 1, 0);
+        for (int r = 0; r < cm.world; ++r) {
+            const unsigned long long* o = &all[(size_t)r * (5 * k + 1)];
+            for (uint64_t i = 0; i < 4 * k; i += 2) {
+                const u128 a = ((u128)sum[i + 1] << 64) | sum[i];
+                const u128 b = ((u128)o[i + 1] << 64) | o[i];
+                const u128 c2 = a + b;
+                sum[i] = (unsigned long long)c2;
+                sum[i + 1] = (unsigned long long)(c2 >> 64);
+            }
+            for (uint64_t i = 4 * k; i < 5 * k + 1; ++i) sum[i] += o[i];
+        }
+        L.dacc.upload(sum.data(), 5 * k);
+        k_add_acc<<<1, 256, 0, st>>>(L.acc.p, L.dacc.p, (int)k);
+        JB_LAUNCH_CHECK();
+        L.dacc.zero();
+        JB_CUDA(cudaMemsetAsync(L.flags.p, 0, 8, st));
+        JB_CUDA(cudaMemsetAsync(L.nwork.p, 0, 8, st));
+        return sum[5 * k];
+    };
+
+    auto repair_dist = [&]() {  // update_means :181-197 across ranks
+        lloyd_means(L, false);
+        int ne = 0;
+        JB_CUDA(cudaMemcpyAsync(&ne, L.empties.p + L.k, sizeof(int), cudaMemcpyDeviceToHost, st));
+        JB_CUDA(cudaStreamSynchronize(st));
+        if (!ne) return;
+        std::vector<int> em(ne);
+        L.empties.download(em.data(), ne);
+        JB_CUDA(cudaStreamSynchronize(st));
+        const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, kSMs * 4));
+        if (L.far_blk.n < (size_t)(3 * nblk)) L.far_blk.alloc(3 * nblk, st);
+        for (int c : em) {
+            FarRec mine{-1.0, INT64_MAX, -1, 0.0, 0.0, -1};
+            if (n > 0) {
+                k_far_block<<<nblk, 256, 0, st>>>(spts.p, gkey.p, n, L.labs.p, L.centers.p,
+                                                  L.cacc().cnt, L.far_blk.p);
+                JB_LAUNCH_CHECK();
+                auto blk = L.far_blk.to_host(3 * nblk);
+                for (int b = 0; b < nblk; ++b) {
+                    double d;
+                    memcpy(&d, &blk[3 * b], 8);
+                    const long long gp = (long long)blk[3 * b + 1];
+                    if (d > mine.d || (d == mine.d && gp < mine.gp)) {
+                        mine.d = d;
+                        mine.gp = gp;
+                        mine.r = (long long)blk[3 * b + 2];
+                    }
+                }
+                if (mine.r >= 0) {
+                    double2 p;
+                    uint32_t lab;
+                    JB_CUDA(cudaMemcpyAsync(&p, spts.p + mine.r, 16, cudaMemcpyDeviceToHost, st));
+                    JB_CUDA(cudaMemcpyAsync(&lab, L.labs.p + mine.r, 4, cudaMemcpyDeviceToHost, st));
+                    JB_CUDA(cudaStreamSynchronize(st));
+                    mine.x = p.x;
+                    mine.y = p.y;
+                    mine.donor = lab;
+                }
+            }
+            std::vector<FarRec> all(cm.world);
+            cm.allgather(&mine, sizeof mine, all.data());
+            int owner = -1;
+            FarRec best{-1.0, INT64_MAX, -1, 0.0, 0.0, -1};
+            for (int r = 0; r < cm.world; ++r)
+                if (all[r].r >= 0 &&
+                    (all[r].d > best.d || (all[r].d == best.d && all[r].gp < best.gp))) {
+                    best = all[r];
+                    owner = r;
+                }
+            if (owner < 0) {  // no cluster with count > 1: far_i stays 0 (global position 0)
+                const auto xy = center_of(0);
+                // owner of position 0 supplies its label
+                struct L0 {
+                    long long has, lab, r;
+                } l0{0, 0, -1};
+                if (n > 0) {
+                    k_find_gpos<<<1, 1, 0, st>>>(d_gpos, n, 0, dll.p);
+                    long long i = -1;
+                    dll.download(&i, 1);
+                    JB_CUDA(cudaStreamSynchronize(st));
+                    if (i >= 0) {
+                        uint32_t pr, lab;
+                        JB_CUDA(cudaMemcpyAsync(&pr, pos.p + i, 4, cudaMemcpyDeviceToHost, st));
+                        JB_CUDA(cudaStreamSynchronize(st));
+                        JB_CUDA(cudaMemcpyAsync(&lab, L.labs.p + pr, 4, cudaMemcpyDeviceToHost, st));
+                        JB_CUDA(cudaStreamSynchronize(st));
+                        l0 = L0{1, lab, (long long)pr};
+                    }
+                }
+                std::vector<L0> a0(cm.world);
+                cm.allgather(&l0, sizeof l0, a0.data());
+                for (int r = 0; r < cm.world; ++r)
+                    if (a0[r].has) {
+                        best = FarRec{0.0, 0, a0[r].r, xy.first, xy.second, a0[r].lab};
+                        owner = r;
+                    }
+            }
+            k_repair_dist<<<1, 1, 0, st>>>(L.acc.p, L.centers.p, L.labs.p, L.tlab.p, (int)k, L.Ex,
+                                           L.Ey, c, (int)best.donor, best.x, best.y,
+                                           owner == cm.rank ? best.r : -1);
+            JB_LAUNCH_CHECK();
+        }
+        const int zero = 0;
+        JB_CUDA(cudaMemcpyAsync(L.empties.p + L.k, &zero, sizeof(int), cudaMemcpyHostToDevice, st));
+    };
+
+    double best_sse = 0.0;
+    for (uint64_t restart = 0; restart < n_init; ++restart) {
+        // ---- d2_seed (clustering.hpp:92-131) ----
+        std::vector<uint64_t> chosen;
+        std::vector<double> ch_xy;
+        uint64_t cur_draw = *cursor, r0;
+        while (!lemire_host(draw(cur_draw), S, r0)) ++cur_draw;
+        cur_draw += 1;
+        chosen.push_back(r0);
+        auto xy = center_of(r0);
+        ch_xy.push_back(xy.first);
+        ch_xy.push_back(xy.second);
+        double2 hc = make_double2(xy.first, xy.second);
+        cur.upload(&hc, 1);
+        part.zero();
+        if (n > 0) {
+            JB_PROF("d2_update", st);
+            k_d2_tiles<<<tile_grid, 256, 0, st>>>(spts.p, orig.p, pos.p, n, nullptr, nullptr,
+                                                  tmax.p, d2s.p, ss.p, 1, Ed2, part.p, cur.p,
+                                                  gkey.p);
+        }
+        JB_LAUNCH_CHECK();
+        for (uint64_t c = 1; c < k; ++c) {
+            std::vector<unsigned long long> hp = part.to_host(2 * nblocks);
+            hp = cm.sum_i128(hp);
+            i128 total = 0;
+            for (uint64_t b = 0; b < nblocks; ++b) total += fx_load(&hp[2 * b]);
+            const double total_d = fx_to_double(total, Ed2);
+            uint64_t next;
+            if (!(total_d > 0.0)) {  // every remaining point duplicates a center (:120-124)
+                next = 0;
+                while (std::find(chosen.begin(), chosen.end(), next) != chosen.end()) ++next;
+            } else {
+                const uint64_t x = draw(cur_draw);
+                double canon = (double)x * 0x1p-64;  // generate_canonical<double,53>
+                if (canon >= 1.0) canon = 0x1.fffffffffffffp-1;
+                const double u = canon * total_d + 0.0;
+                const i128 U = fx_from_double(u, Ed2);
+                i128 run = 0;
+                uint64_t fb = nblocks;
+                for (uint64_t b = 0; b < nblocks; ++b) {
+                    const i128 v = fx_load(&hp[2 * b]);
+                    if (U < run + v) {
+                        fb = b;
+                        break;
+                    }
+                    run += v;
+                }
+                if (fb == nblocks) {  // roundoff spill: last positive-weight index (:67-70)
+                    long long lp = -1;
+                    if (n > 0) {
+                        dll.upload(&lp, 1);
+                        k_last_positive<<<1, 256, 0, st>>>(d_gpos, pos.p, n, d2s.p, dll.p);
+                        dll.download(&lp, 1);
+                        JB_CUDA(cudaStreamSynchronize(st));
+                    }
+                    std::vector<long long> all(cm.world);
+                    cm.allgather(&lp, sizeof lp, all.data());
+                    long long m = (long long)S - 1, best = -1;
+                    for (auto v : all) best = std::max(best, v);
+                    next = best >= 0 ? (uint64_t)best : (uint64_t)m;
+                } else {
+                    wblk.zero();
+                    if (n > 0) k_block_weights<<<1, 256, 0, st>>>(d_gpos, pos.p, n, d2s.p, fb, wblk.p);
+                    JB_LAUNCH_CHECK();
+                    std::vector<double> w = wblk.to_host(D2_R);
+                    const auto all = cm.gather(w);  // every position owned by exactly one rank
+                    next = UINT64_MAX;
+                    i128 before = run;
+                    for (uint64_t e = 0; e < D2_R && fb * D2_R + e < S; ++e) {
+                        double we = 0.0;
+                        for (int r = 0; r < cm.world; ++r) we += all[(size_t)r * D2_R + e];
+                        const i128 a = fx_from_double(we, Ed2);
+                        if (U < before + a) {
+                            next = fb * D2_R + e;
+                            break;
+                        }
+                        before += a;
+                    }
+                    if (next == UINT64_MAX) throw Error(INTERNAL, "distributed D2 pick failed");
+                }
+                cur_draw += 1;
+            }
+            chosen.push_back(next);
+            xy = center_of(next);
+            ch_xy.push_back(xy.first);
+            ch_xy.push_back(xy.second);
+            if (c + 1 < k && n > 0) {
+                hc = make_double2(xy.first, xy.second);
+                cur.upload(&hc, 1);
+                JB_PROF("d2_update", st);
+                JB_CUDA(cudaMemsetAsync(d2_nwork.p, 0, 8, st));
+                k_d2_cull<<<cull_grid, 256, 0, st>>>(tbox.p, tmax.p, ntiles, spts.p, pos.p, ss.p,
+                                                     d2_work.p, d2_nwork.p, cur.p);
+                k_d2_tiles<<<tile_grid, 256, 0, st>>>(spts.p, orig.p, pos.p, n, d2_work.p,
+                                                      d2_nwork.p, tmax.p, d2s.p, ss.p, 0, Ed2,
+                                                      part.p, cur.p, gkey.p);
+                JB_LAUNCH_CHECK();
+            }
+        }
+        *cursor = cur_draw;
+        L.centers.upload(ch_xy.data(), 2 * k);
+
+        // ---- Lloyd (lloyd_once :200-220), one exchange per iteration ----
+        L.acc.zero();
+        L.dacc.zero();
+        L.diag.zero();
+        JB_CUDA(cudaMemsetAsync(L.tlab.p, 0xFF, sizeof(uint32_t) * std::max<int64_t>(ntiles, 1), st));
+        JB_CUDA(cudaMemsetAsync(L.empties.p + L.k, 0, 3 * sizeof(int), st));
+        JB_CUDA(cudaMemsetAsync(L.flags.p, 0, 8, st));
+        JB_CUDA(cudaMemsetAsync(L.nwork.p, 0, 8, st));
+        lloyd_assign(L, true, false);
+        exchange_deltas();
+        uint64_t it = 0;
+        for (; it < max_iters; ++it) {
+            repair_dist();                 // update_means (+ empty-cluster re-seeding)
+            lloyd_assign(L, false, false); // assign_all
+            const unsigned long long ch = exchange_deltas();
+            if (ch == 0) {
+                ++it;
+                break;
+            }
+        }
+        repair_dist();  // final update_means
+        double sse = 0.0;
+        if (n_init > 1) {
+            DArr<unsigned long long> sacc(2, st);
+            sacc.zero();
+            if (n > 0)
+                k_sse<<<grid_cap(n), 256, 0, st>>>(spts.p, n, L.labs.p, L.centers.p, Ed2, sacc.p);
+            JB_LAUNCH_CHECK();
+            auto hs = cm.sum_i128(sacc.to_host(2));
+            sse = fx_to_double(fx_load(hs.data()), Ed2);
+        }
+        if (restart == 0 || sse < best_sse) {
+            best_sse = sse;
+            out.k = k;
+            out.centers = L.centers.to_host(2 * k);
+            out.labels.alloc(nn, st);
+            if (n > 0) {
+                k_unsort_labels<<<grid_cap(n), 256, 0, st>>>(L.labs.p, orig.p, n, out.labels.p);
+                JB_LAUNCH_CHECK();
+            }
             out.iterations = it;
             out.sse = sse;
         }

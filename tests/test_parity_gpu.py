@@ -217,3 +217,16 @@ def test_cpp_facade_against_reference_api():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_joint_fit_two_ranks_bitwise():
+    """jb_fit_transform_dist over 2 ranks (gloo; both may share the GPU) equals
+    the single-GPU fit bit for bit (tools/dist_check.py)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--standalone",
+                        "--nproc-per-node", "2", os.path.join(root, "tools", "dist_check.py")],
+                       capture_output=True, text=True, timeout=900, cwd=root)
+    print(r.stdout[-4000:])
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
