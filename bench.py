@@ -17,8 +17,11 @@ GPU. One step = one fit_transform + inverse_transform of the whole series.
           headers compiled here) on a bounded sample of the same workload
 
 `--impl reference` runs the reference's CPU implementation alone (rank 0).
-Multi-GPU (torchrun): every rank fits its own config-4-sized series
-(replicas; weak scaling) and value = all ranks' points / max-over-ranks time.
+Multi-GPU (torchrun): ONE joint fit of the same 1e9-sample series, its
+10,000 partitions sharded over the ranks by samples (jb_fit_transform_dist:
+exact exchanges of tiny partials over torch.distributed/NCCL, results
+bitwise identical to one GPU); strong scaling, value = 1e9 / max-over-ranks
+step time.
 """
 from __future__ import annotations
 
@@ -41,12 +44,13 @@ METRIC = "input points/sec for JABBA fit_transform and inverse_transform"
 CFG4 = dict(tol=0.1, backend="svq", k=200, r=0.1, seed=0, scl=1.0)
 
 
-def workload_desc(n, m, scale):
+def workload_desc(n, m, scale, world=1):
     return {"workload": "cfg4: 1 random walk with N(0,5) level shifts, "
                         f"{n:.3g} fp64 samples, {m} partitions, tol 0.1, svq k=200 r=0.1",
             "n_points": int(n), "partitions": int(m), "scale": scale,
             "l2": "inputs (8 B/sample) exceed the 126 MB L2 every step; no flush needed",
-            "parallelism": "replicas"}
+            "parallelism": "single GPU" if world == 1 else
+            f"joint fit, partitions sharded over {world} ranks (NCCL allgather of exact partials)"}
 
 
 # ---------------------------------------------------------------------------
@@ -134,14 +138,16 @@ def algorithmic_work(name, launches, info):
     """Algorithmic bytes or flops of ALL launches of `name`."""
     S, k, N, n = info["S"], info["k"], info["N"], info["n"]
     it = info["iterations"]
-    if name == "lloyd_assign":      # (I+1) assigns: 6 flops per point-center + 2 per point
-        return "fp64", launches * (6.0 * S * k + 2.0 * S)
-    if name == "assign_stats":       # final assign over all N pieces
-        return "fp64", launches * (6.0 * N * k + 3.0 * N)
+    if name == "lloyd_assign":      # points of the tiles that need work: 16 B point + 4 B label r/w
+        return "hbm", 24.0 * 128 * info.get("lloyd_tiles", 0) + launches * 0.0
+    if name == "assign_stats":       # final assign + group stats: point 16 B + len 4 B in, label 4 B out
+        return "hbm", launches * 24.0 * N
     if name == "d2_update":          # 16 B point + 8 B d2 read, 8 B d2 write per sample
         return "hbm", launches * 32.0 * S
     if name == "compress_spec":      # 23 flops per candidate test, T ~ 1.89 n (cfg4)
         return "fp64", 23.0 * info.get("tests", 1.89 * n)
+    if name == "inverse_chain":      # label 4 B in; quantized length 4 B + start value 8 B out
+        return "hbm", 16.0 * N
     if name == "inverse_fill":
         return "hbm", 8.0 * n + 28.0 * N
     return None, None
@@ -230,22 +236,47 @@ def main():
     import torch.distributed as dist
     from paper_2401_00109_b200 import _native, api
 
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        # JB_BENCH_DIST_BACKEND=gloo: code-path check with several ranks on one
+        # GPU (host-side exchanges only; never a timing)
+        backend = os.environ.get("JB_BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     n = int(round(1e9 * args.scale))
     m = max(1, int(round(10000 * args.scale)))
-    x = make_series_gpu(n, rank, dev)
-    first, steps = api.plan_segments([n], 0, m)
+    x_full = make_series_gpu(n, 0, dev)  # the same series on every rank
+    first_g, steps_g = api.plan_segments([n], 0, m)
     cfg = api.JabbaConfig.of(**CFG4)
     eng = api.Engine(local)
-    out = torch.empty(n, dtype=torch.float64, device=dev)
+    if world > 1:
+        comm = api.TorchComm(device=dev)
+        s0, s1 = api.shard_segments(steps_g, world, rank)
+        lo, hi, first, steps = api.local_view(first_g, steps_g, s0, s1)
+        x = x_full[lo:hi + 1].clone()
+        del x_full
+    else:
+        comm = None
+        lo, hi, first, steps = 0, n - 1, first_g, steps_g
+        x = x_full
+    n_local = hi - lo + 1
+    out = torch.empty(n_local, dtype=torch.float64, device=dev)
+    torch.cuda.empty_cache()
     torch.cuda.synchronize()
 
+    def fit(values=None, ptr=None):
+        if comm is None:
+            return eng.fit_arrays(values, first, steps, 0, cfg, device_ptr=ptr, n_values=n_local)
+        return api.fit_arrays_dist(eng, comm, values, first, steps, len(first_g), 0, cfg,
+                                   device_ptr=ptr, n_values=n_local)
+
     def step():
-        nf = eng.fit_arrays(None, first, steps, 0, cfg, device_ptr=x.data_ptr(), n_values=n)
+        nf = fit(ptr=x.data_ptr())
         nf.inverse(out_ptr=out.data_ptr(), on_device=True)
         return nf
 
@@ -281,24 +312,26 @@ def main():
     ms_profiled = e4.elapsed_time(e5)
     st = nf.stats()
     N = nf.n_pieces
-    info = dict(S=st["sample_size"], k=nf.k, N=N, n=n, iterations=st["iterations"])
-    t_local = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    info = dict(S=st["sample_size"], k=nf.k, N=N, n=n, iterations=st["iterations"],
+                lloyd_tiles=st.get("lloyd_tiles_processed", 0))
+    red_dev = dev if world == 1 or dist.get_backend() == "nccl" else "cpu"
+    t_local = torch.tensor([ms_total], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
     ms_step = float(t_local.item()) / args.steps
-    value = world * n / (ms_step / 1e3)
+    value = n / (ms_step / 1e3)  # the whole series, all ranks together
 
     # ---- e2e through the C ABI with host buffers ----
-    host_in = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    host_in = torch.empty(n_local, dtype=torch.float64, pin_memory=True)
     host_in.copy_(x)
-    host_out = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    host_out = torch.empty(n_local, dtype=torch.float64, pin_memory=True)
     host_lab = torch.empty(N, dtype=torch.int32, pin_memory=True)
     hin, hout, hlab = host_in.numpy(), host_out.numpy(), host_lab.numpy().view(np.uint32)
     del x
     torch.cuda.empty_cache()
 
     def e2e_step():
-        nf2 = eng.fit_arrays(hin, first, steps, 0, cfg)
+        nf2 = fit(values=hin)
         nf2.labels_into(hlab)
         nf2.inverse(out=hout)
         return nf2
@@ -314,12 +347,13 @@ def main():
     e3.record()
     barrier()
     e2e_ms = e2.elapsed_time(e3) / args.e2e_steps
-    t_e = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    t_e = torch.tensor([e2e_ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
     e2e_ms = float(t_e.item())
-    e2e = {"value": world * n / (e2e_ms / 1e3), "unit": "points/s",
-           "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n + 4 * nf2.n_pieces}
+    e2e = {"value": n / (e2e_ms / 1e3), "unit": "points/s",
+           "h2d_bytes_per_step": 8 * n_local, "d2h_bytes_per_step": 8 * n_local + 4 * nf2.n_pieces,
+           "per": "rank" if world > 1 else "step"}
 
     # ---- roofline of the dominant kernel ----
     peaks, peak_kind = measured_peaks()
@@ -362,8 +396,9 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": workload_desc(n, m, args.scale),
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_desc(n, m, args.scale, world),
             "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
             "clocks": clk.summary(), "gpu_launches": gpu_launches,
             "phase_ms": st["ms"], "profiled_step_ms": ms_profiled, "fit_stats": {k: st[k] for k in ("iterations", "sample_size",

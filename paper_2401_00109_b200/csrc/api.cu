@@ -568,7 +568,10 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
                 int64_t mx = 0;
                 for (auto v : N_all) mx = std::max(mx, v);
                 std::vector<double> mine(2 * mx, 0.0), all(2 * mx * cm.world);
-                if (N) JB_CUDA(cudaMemcpy(mine.data(), sc.pts.p, 16 * N, cudaMemcpyDeviceToHost));
+                if (N) {
+                    JB_CUDA(cudaMemcpyAsync(mine.data(), sc.pts.p, 16 * N, cudaMemcpyDeviceToHost, st));
+                    JB_CUDA(cudaStreamSynchronize(st));
+                }
                 cm.allgather(mine.data(), 16 * mx, all.data());
                 std::vector<double> cat;
                 cat.reserve(2 * N_glob);

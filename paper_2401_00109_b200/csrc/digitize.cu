@@ -221,6 +221,7 @@ void scale_pieces(const Pieces& pc, int64_t total_steps, double scl, Scaled& out
     std::vector<unsigned long long> hb = bb.to_host(4);
     if (C.dist()) {
         auto all = C.gather(hb);
+        for (int j = 0; j < 4; ++j) hb[j] = all[j];  // rank 0's box, then the others
         for (int r = 1; r < C.world; ++r) {
             hb[0] = std::min(hb[0], all[4 * r]);
             hb[1] = std::max(hb[1], all[4 * r + 1]);
@@ -447,6 +448,7 @@ void assign_and_stats(const double* d_pts, const int32_t* d_len, int64_t n,
     }
     if (cm && cm->dist()) {  // group statistics of all ranks (exact integers)
         const auto all = cm->gather(rec);
+        std::copy(all.begin(), all.begin() + 7 * k, rec.begin());  // rank 0's, then the others
         for (int r = 1; r < cm->world; ++r)
             for (uint64_t c = 0; c < k; ++c) {
                 const unsigned long long* o = &all[(size_t)r * 7 * k + 7 * c];

@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <utility>
 #include <vector>
 
@@ -12,6 +14,18 @@
 #include "jb_common.cuh"
 
 namespace jb {
+
+// JB_DEBUG=1: host-side diagnostics on stderr (collective sequence, k-means
+// seeds and per-iteration label changes) for comparing ranks / paths.
+inline bool dbg_on() {
+    static const bool on = getenv("JB_DEBUG") != nullptr;
+    return on;
+}
+inline uint64_t dbg_hash(const void* p, size_t bytes) {  // FNV-1a
+    uint64_t h = 1469598103934665603ULL;
+    for (size_t i = 0; i < bytes; ++i) h = (h ^ static_cast<const unsigned char*>(p)[i]) * 1099511628211ULL;
+    return h;
+}
 
 // Host side of the distributed fit's collectives: an exact allgather of host
 // bytes (rank order). world == 1 means single-GPU.
@@ -23,6 +37,10 @@ struct Comm {
         if (!dist()) {
             memcpy(recv, send, bytes);
             return;
+        }
+        if (dbg_on()) {
+            static int seq = 0;
+            fprintf(stderr, "[jb r%d] allgather #%d: %zu bytes\n", rank, seq++, bytes);
         }
         if (c->allgather(c->user, send, bytes, recv) != 0)
             throw Error(NCCL_ERROR, "allgather callback failed");

@@ -1280,6 +1280,14 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
         JB_CUDA(cudaStreamSynchronize(st));
         if (h.cursor > raw_count) throw Error(INTERNAL, "rng stream exhausted");
         *cursor = h.cursor;
+        if (dbg_on()) {
+            auto ch = chosen.to_host(k);
+            auto cc = L.centers.to_host(2 * k);
+            fprintf(stderr, "[jb] seeds: S=%lld Ed2=%d Ex=%d Ey=%d chosen[0..3]=%lld %lld %lld %lld hash=%016llx cursor=%llu\n",
+                    (long long)n, Ed2, L.Ex, L.Ey, (long long)ch[0], (long long)ch[std::min<uint64_t>(1, k - 1)],
+                    (long long)ch[std::min<uint64_t>(2, k - 1)], (long long)ch[k - 1],
+                    (unsigned long long)dbg_hash(cc.data(), 16 * k), (unsigned long long)h.cursor);
+        }
         JB_TRACE("kmeans: d2 seeding", st);
 
         // ---- Lloyd (lloyd_once :200-220) ----
@@ -1297,7 +1305,7 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
         JB_CUDA(cudaMemsetAsync(L.flags.p, 0, 8, st));
         JB_CUDA(cudaMemsetAsync(L.nwork.p, 0, 8, st));
         uint64_t it = 0;
-        constexpr uint64_t kBatch = 16;
+        const uint64_t kBatch = dbg_on() ? 1 : 16;
         while (it < max_iters) {
             const uint64_t B = std::min<uint64_t>(kBatch, max_iters - it);
             for (uint64_t b = 0; b < B; ++b) {
@@ -1308,6 +1316,13 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
             }
             LoopState h = lloyd_state(L);
             it = (uint64_t)h.iters;
+            if (dbg_on()) {
+                auto cc = L.centers.to_host(2 * k);
+                auto dg = L.diag.to_host(2);
+                fprintf(stderr, "[jb] iter %d: empty=%d conv=%d cum_changed=%llu centers=%016llx\n",
+                        h.iters, h.n_empty, h.converged, dg[1],
+                        (unsigned long long)dbg_hash(cc.data(), 16 * k));
+            }
             if (h.converged) break;
             if (h.n_empty) {  // empty clusters: re-seed on the host path, finish the iteration
                 lloyd_repair(L, h.n_empty);
@@ -1802,6 +1817,12 @@ void lloyd_best_dist(const Comm& cm, const double* d_pts, const uint64_t* d_lidx
         }
         *cursor = cur_draw;
         L.centers.upload(ch_xy.data(), 2 * k);
+        if (dbg_on())
+            fprintf(stderr, "[jb r%d] dist seeds: S=%llu n=%lld Ed2=%d Ex=%d Ey=%d chosen[0..3]=%llu %llu %llu %llu hash=%016llx cursor=%llu\n",
+                    cm.rank, (unsigned long long)S, (long long)n, Ed2, L.Ex, L.Ey,
+                    (unsigned long long)chosen[0], (unsigned long long)chosen[std::min<uint64_t>(1, k - 1)],
+                    (unsigned long long)chosen[std::min<uint64_t>(2, k - 1)], (unsigned long long)chosen[k - 1],
+                    (unsigned long long)dbg_hash(ch_xy.data(), 16 * k), (unsigned long long)cur_draw);
 
         // ---- Lloyd (lloyd_once :200-220), one exchange per iteration ----
         L.acc.zero();
@@ -1818,6 +1839,11 @@ void lloyd_best_dist(const Comm& cm, const double* d_pts, const uint64_t* d_lidx
             repair_dist();                 // update_means (+ empty-cluster re-seeding)
             lloyd_assign(L, false, false); // assign_all
             const unsigned long long ch = exchange_deltas();
+            if (dbg_on()) {
+                auto cc = L.centers.to_host(2 * k);
+                fprintf(stderr, "[jb r%d] dist iter %llu: changed=%llu centers=%016llx\n", cm.rank,
+                        (unsigned long long)it, ch, (unsigned long long)dbg_hash(cc.data(), 16 * k));
+            }
             if (ch == 0) {
                 ++it;
                 break;

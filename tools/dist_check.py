@@ -27,14 +27,14 @@ def cases():
     zz = np.tile([0.0, 1.0], 3000)
     out = [
         ("cfg1 svq", datasets.config1(0.25)),
-        ("cfg4 partitioned svq", datasets.config4(2e-4)),
+        ("cfg4 partitioned svq", datasets.config4(2e-4, partitions=6)),
         ("cfg2 ga two-norm", datasets.config2(0.003)),
         ("cfg5 svq k500", datasets.config5(4e-4)),
         ("walk vq n_init 2", datasets.Workload("vq", walk, np.array([walk.size]), 0, 12,
                                                 dict(tol=0.3, backend="vq", k=9, n_init=2, seed=3))),
         ("walk ga-hier", datasets.Workload("gh", walk, np.array([walk.size]), 0, 6,
                                             dict(tol=0.2, backend="ga-hier", alpha=0.4))),
-        ("zigzag svq empty clusters", datasets.Workload("zz", zz, np.array([zz.size]), 2, 1,
+        ("zigzag svq empty clusters", datasets.Workload("zz", zz, np.array([zz.size]), 0, 4,
                                                          dict(tol=1e-3, backend="svq", k=3, r=0.5,
                                                               seed=2, max_iters=5))),
     ]
@@ -53,7 +53,10 @@ def main():
     eng = api.Engine(dev)
     comm = api.TorchComm()
     failures = 0
+    only = sys.argv[1:]  # optional case-name filters
     for name, w in cases():
+        if only and not any(o in name for o in only):
+            continue
         first, steps = api.plan_segments(w.series_lengths, w.layout, w.parts)
         if len(first) < world:
             continue
