@@ -615,7 +615,7 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
     auto t3 = Clock::now();
     GroupStats gs;
     assign_and_stats(sc.pts.p, fit->pieces.len.p, N, backend_centers, k, bb, assign_needed,
-                     labels.p, gs, st, sc.max_len_global, &cm, base);
+                     labels.p, gs, st, sc.max_len_global, sc.scl, sc.sigma_len, &cm, base);
     std::vector<double> centers(2 * k), mean_lengths(k);
     bool need_sample_stats = false;
     for (uint64_t g = 0; g < k; ++g) need_sample_stats |= gs.counts[g] == 0;

@@ -11,6 +11,7 @@
 
 #include "jb_device.hpp"
 #include "jb_grid.cuh"
+#include "jb_rowgrid.cuh"
 
 namespace jb {
 
@@ -244,95 +245,136 @@ namespace {
 
 // Group statistics of digitize (digitization.hpp:217-231) fused with the
 // final assignment: count, first index, sum of lengths, sums of x and y.
-// Sums use a per-element-biased fixed point (fx(v) + B >= 0, < 2^63) so a
-// point costs one shared-memory atomic per coordinate; count and length
-// share one packed 64-bit atomic (count << 40 | len) per point. The host
-// removes the bias exactly (count * B). Deterministic for any schedule.
-__global__ void __launch_bounds__(256, 3) k_assign_stats(const double2* __restrict__ pts, const int32_t* __restrict__ len,
-                               int64_t n, const double* __restrict__ centers, int k,
-                               int do_assign, uint32_t* __restrict__ labels, int Ex, int Ey,
-                               unsigned long long Bx, unsigned long long By,
-                               unsigned long long* __restrict__ gacc, int use_smem, int packed,
-                               CandGrid cg) {
-    // accumulator layout (smem or global): cl(k) len(k) first(k) sx(2k) sy(2k)
-    extern __shared__ unsigned char smem[];
-    double* cx = reinterpret_cast<double*>(smem);
-    double* cy = cx + k;  // centers only when assigning (smem sized accordingly)
-    unsigned long long* s_cl =
-        use_smem ? reinterpret_cast<unsigned long long*>(cx + (do_assign ? 2 * k : 0))
-                 : gacc;  // count(|len)
-    unsigned long long* s_len = s_cl + k;
-    unsigned long long* s_first = s_len + k;
-    unsigned long long* s_sx = s_first + k;
-    unsigned long long* s_sy = s_sx + 2 * k;
-    for (int c = threadIdx.x; c < k; c += blockDim.x) {
+// Only native 32-bit shared-memory atomics (64-bit ones are CAS loops):
+//  * count, length sum and x sum come from a per-block histogram over
+//    (piece length, cluster): x = scl*len/sigma_len is a function of len, so
+//    the exact fixed-point x sum is sum_l hist[l] * fx(x_l);
+//  * y (biased fixed point fx(y) + B in [0, 2^62)) is split into three
+//    21-bit limbs, each accumulated in a u32 counter; 2048 points cannot
+//    overflow a counter, so the counters are folded into 64-bit per-cluster
+//    totals every two 1024-point rounds;
+//  * first index: u32 atomicMin, taken only when it can lower the minimum.
+// Pieces longer than the histogram (rare) go straight to global 64-bit
+// atomics (native in L2). Everything is exact integer arithmetic, hence
+// independent of the schedule; the host removes the bias (count * B).
+constexpr int AS_TB = 256, AS_U = 4;
+
+__global__ void __launch_bounds__(AS_TB) k_assign_stats(
+    const double2* __restrict__ pts, const int32_t* __restrict__ len, int64_t n,
+    const double* __restrict__ centers, int k, int do_assign, uint32_t* __restrict__ labels,
+    int Ex, int Ey, unsigned long long Bx, unsigned long long By,
+    unsigned long long* __restrict__ gacc, CandGrid cg, RowGrid rg, int RH) {
+    // gacc layout: count(k) len(k) first(k) sx(2k) sy(2k), sums biased
+    extern __shared__ unsigned long long smem64[];
+    double* cx = reinterpret_cast<double*>(smem64);
+    double* cy = cx + k;
+    unsigned long long* yacc = smem64 + (do_assign ? 2 * k : 0);  // 3k limb totals
+    uint32_t* hist = reinterpret_cast<uint32_t*>(yacc + 3 * k);    // RH x k
+    uint32_t* ylimb = hist + (size_t)RH * k;                        // 3k
+    uint32_t* first = ylimb + 3 * k;                                // k
+    for (int c = threadIdx.x; c < k; c += AS_TB) {
         if (do_assign) {
             cx[c] = centers[2 * c];
             cy[c] = centers[2 * c + 1];
         }
-        if (use_smem) {
-            s_cl[c] = 0;
-            s_len[c] = 0;
-            s_first[c] = ~0ULL;
-            s_sx[2 * c] = s_sx[2 * c + 1] = 0;
-            s_sy[2 * c] = s_sy[2 * c + 1] = 0;
-        }
+        yacc[c] = yacc[k + c] = yacc[2 * k + c] = 0;
+        ylimb[c] = ylimb[k + c] = ylimb[2 * k + c] = 0;
+        first[c] = 0xFFFFFFFFu;
     }
+    for (int j = threadIdx.x; j < RH * k; j += AS_TB) hist[j] = 0;
     __syncthreads();
-    constexpr int U = 4;  // points in flight per thread
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x * U;
-    // every lane runs the same trip count (warp-uniform loop for the
-    // aggregation's full-mask shuffles)
-    for (int64_t base0 = blockIdx.x * (int64_t)blockDim.x * U; base0 < n; base0 += stride) {
+    auto fold = [&]() {
+        __syncthreads();
+        for (int c = threadIdx.x; c < 3 * k; c += AS_TB) {
+            yacc[c] += ylimb[c];
+            ylimb[c] = 0;
+        }
+        __syncthreads();
+    };
+    const int64_t stride = (int64_t)gridDim.x * AS_TB * AS_U;
+    int round = 0;
+    for (int64_t base0 = blockIdx.x * (int64_t)AS_TB * AS_U; base0 < n; base0 += stride) {
         const int64_t base = base0 + threadIdx.x;
-        double2 pp[U];
-        int32_t ll[U];
-        uint32_t lb[U] = {0, 0, 0, 0};
+        double2 pp[AS_U];
+        int32_t ll[AS_U];
+        uint32_t lb[AS_U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t i = base + (int64_t)u * blockDim.x;
+        for (int u = 0; u < AS_U; ++u) {
+            const int64_t i = base + (int64_t)u * AS_TB;
+            pp[u] = make_double2(0.0, 0.0);
+            ll[u] = 0;
+            lb[u] = 0;
             if (i < n) {
                 pp[u] = pts[i];
                 ll[u] = len[i];
-                lb[u] = do_assign ? 0u : labels[i];
+                if (!do_assign) lb[u] = labels[i];
             }
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t i = base + (int64_t)u * blockDim.x;
-            const bool valid = i < n;
-            const double2 p = valid ? pp[u] : make_double2(0.0, 0.0);
+        for (int u = 0; u < AS_U; ++u) {
+            const int64_t i = base + (int64_t)u * AS_TB;
+            if (i >= n) continue;
+            const double2 p = pp[u];
+            const int32_t l = ll[u];
             uint32_t lab = lb[u];
-            if (valid && do_assign) {
-                lab = grid_nearest(cg, p.x, p.y, cx, cy, k);
+            if (do_assign) {
+                lab = row_nearest(rg, cg, l, p.x, p.y, cx, cy, k);
                 labels[i] = lab;
             }
-            if (valid && (unsigned long long)i < s_first[lab])
-                atomicMin(s_first + lab, (unsigned long long)i);
-            if (valid) {
-                if (packed) {
-                    atomicAdd(s_cl + lab, (1ULL << 40) | (unsigned long long)ll[u]);
-                } else {
-                    atomicAdd(s_cl + lab, 1ULL);
-                    atomicAdd(s_len + lab, (unsigned long long)ll[u]);
-                }
-                // biased fixed point in [0, 2^62): one atomic unless the low word carries
-                fx_atomic_add_small(s_sx + 2 * lab, (u128)(fx_from_double(p.x, Ex) + (i128)Bx));
-                fx_atomic_add_small(s_sy + 2 * lab, (u128)(fx_from_double(p.y, Ey) + (i128)By));
+            if ((uint32_t)i < first[lab]) atomicMin(first + lab, (uint32_t)i);
+            if (l >= 1 && l <= RH) {
+                atomicAdd(hist + (size_t)(l - 1) * k + lab, 1u);
+            } else {  // rare: long piece
+                atomicAdd(gacc + lab, 1ULL);
+                atomicAdd(gacc + k + lab, (unsigned long long)l);
+                fx_atomic_add_small(gacc + 3 * k + 2 * lab, (u128)(fx_from_double(p.x, Ex) + (i128)Bx));
             }
+            const unsigned long long yb = (unsigned long long)(fx_from_double(p.y, Ey) + (i128)By);
+            atomicAdd(ylimb + lab, (uint32_t)(yb & 0x1FFFFFu));
+            atomicAdd(ylimb + k + lab, (uint32_t)((yb >> 21) & 0x1FFFFFu));
+            atomicAdd(ylimb + 2 * k + lab, (uint32_t)(yb >> 42));
         }
+        if (++round & 1) continue;
+        fold();
     }
-    if (!use_smem) return;
-    __syncthreads();
-    for (int c = threadIdx.x; c < k; c += blockDim.x) {
-        if (s_cl[c] == 0) continue;
-        const unsigned long long cnt = packed ? (s_cl[c] >> 40) : s_cl[c];
-        const unsigned long long ls = packed ? (s_cl[c] & ((1ULL << 40) - 1)) : s_len[c];
-        atomicAdd(gacc + c, cnt);
-        atomicAdd(gacc + k + c, ls);
-        atomicMin(gacc + 2 * k + c, s_first[c]);
-        fx_atomic_add(gacc + 3 * k + 2 * c, fx_load(s_sx + 2 * c));
-        fx_atomic_add(gacc + 5 * k + 2 * c, fx_load(s_sy + 2 * c));
+    fold();
+    for (int c = threadIdx.x; c < k; c += AS_TB) {
+        unsigned long long cnt = 0, ls = 0;
+        u128 sx = 0;
+        for (int l = 1; l <= RH; ++l) {
+            const uint32_t h = hist[(size_t)(l - 1) * k + c];
+            if (!h) continue;
+            cnt += h;
+            ls += (unsigned long long)h * (unsigned long long)l;
+            const u128 xb = (u128)(fx_from_double(row_x(rg, l), Ex) + (i128)Bx);
+            sx += xb * (u128)h;
+        }
+        if (cnt) {
+            atomicAdd(gacc + c, cnt);
+            atomicAdd(gacc + k + c, ls);
+            fx_atomic_add(gacc + 3 * k + 2 * c, (i128)sx);
+        }
+        const u128 sy = (u128)yacc[c] + ((u128)yacc[k + c] << 21) + ((u128)yacc[2 * k + c] << 42);
+        if (sy) fx_atomic_add(gacc + 5 * k + 2 * c, (i128)sy);
+        if (first[c] != 0xFFFFFFFFu) atomicMin(gacc + 2 * k + c, (unsigned long long)first[c]);
+    }
+}
+
+// Large alphabets (GA can form thousands of groups; labels are given): the
+// same exact statistics with global 64-bit atomics (native in L2).
+__global__ void k_stats_global(const double2* __restrict__ pts, const int32_t* __restrict__ len,
+                               int64_t n, const uint32_t* __restrict__ labels, int k, int Ex,
+                               int Ey, unsigned long long Bx, unsigned long long By,
+                               unsigned long long* __restrict__ gacc) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t lab = labels[i];
+        const double2 p = pts[i];
+        atomicAdd(gacc + lab, 1ULL);
+        atomicAdd(gacc + k + lab, (unsigned long long)len[i]);
+        if ((unsigned long long)i < gacc[2 * k + lab]) atomicMin(gacc + 2 * k + lab, (unsigned long long)i);
+        fx_atomic_add_small(gacc + 3 * k + 2 * lab, (u128)(fx_from_double(p.x, Ex) + (i128)Bx));
+        fx_atomic_add_small(gacc + 5 * k + 2 * lab, (u128)(fx_from_double(p.y, Ey) + (i128)By));
     }
 }
 
@@ -377,7 +419,8 @@ __global__ void k_gather(const double2* __restrict__ pts, const uint64_t* __rest
 void assign_and_stats(const double* d_pts, const int32_t* d_len, int64_t n,
                       const std::vector<double>& centers, uint64_t k, const BBox& bb,
                       bool do_assign, uint32_t* d_labels, GroupStats& gs, cudaStream_t st,
-                      int32_t max_len, const Comm* cm, int64_t first_base) {
+                      int32_t max_len, double scl, double sigma_len, const Comm* cm,
+                      int64_t first_base) {
     DArr<double> dc(std::max<uint64_t>(2 * k, 1), st);
     if (centers.size() >= 2 * k) dc.upload(centers.data(), 2 * k);  // GA: no centers needed
     else if (do_assign) throw Error(INTERNAL, "assignment without centers");
@@ -395,42 +438,63 @@ void assign_and_stats(const double* d_pts, const int32_t* d_len, int64_t n,
     const int Ex = exp_for(mx), Ey = exp_for(my);
     const unsigned long long Bx = (unsigned long long)fx_from_double(mx, Ex);
     const unsigned long long By = (unsigned long long)fx_from_double(my, Ey);
-    const size_t centers_smem = do_assign ? sizeof(double) * 2 * k : 0;
-    if (centers_smem > 160 * 1024) throw Error(INVALID_INPUT, "k too large for the assignment kernel");
-    const int use_smem = centers_smem + sizeof(unsigned long long) * 7 * k <= 160 * 1024;
-    const size_t smem = centers_smem + (use_smem ? sizeof(unsigned long long) * 7 * k : 0);
-    JB_CUDA(cudaFuncSetAttribute(k_assign_stats, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)std::max<size_t>(smem, 1)));
-    // exact candidate grid over the points' bounding box (jb_grid.cuh)
+    if (n >= (1LL << 32)) throw Error(INVALID_INPUT, "more than 2^32 pieces on one GPU");
+    if (k > 2048 && do_assign)
+        throw Error(INVALID_INPUT, "k > 2048 is not supported by the assignment kernel");
+    // histogram rows: piece lengths 1..RH (longer pieces take the global path)
+    int64_t rh = std::min<int64_t>(std::max<int32_t>(max_len, 1), 64);
+    rh = std::min<int64_t>(rh, std::max<int64_t>(1, 8192 / (int64_t)std::max<uint64_t>(k, 1)));
+    const int RH = (int)rh;
+    const size_t smem = (do_assign ? sizeof(double) * 2 * k : 0) + sizeof(unsigned long long) * 3 * k +
+                        sizeof(uint32_t) * ((size_t)RH * k + 4 * k);
+    if (k <= 2048)
+        JB_CUDA(cudaFuncSetAttribute(k_assign_stats, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)std::max<size_t>(smem, 1)));
+    RowGrid rg = make_row_grid_desc(bb.ymin, bb.ymax, scl, sigma_len, max_len, 1 << 20);
     CandGrid cg{};
     DArr<uint16_t> cg_cnt, cg_cand;
+    DArr<uint64_t> rg_cell;
     if (do_assign) {
+        // exact candidate grids over the points' bounding box (jb_grid.cuh,
+        // jb_rowgrid.cuh): rows for short pieces, 2-D for the rest
         const int G = grid_side_for(k), cap = 32;
         cg = make_grid_desc(bb.xmin, bb.xmax, bb.ymin, bb.ymax, G, cap);
         cg_cnt.alloc((size_t)G * G, st);
         cg_cand.alloc((size_t)G * G * cap, st);
         cg.cnt = cg_cnt.p;
         cg.cand = cg_cand.p;
+        rg_cell.alloc((size_t)rg.R * rg.Gy, st);
+        rg.cell = rg_cell.p;
         JB_PROF("assign_grid", st);
         k_grid_build<<<std::min(G * G / 8, kSMs * 16), 256, 0, st>>>(cg, dc.p, (int)k);
         JB_LAUNCH_CHECK();
+        const int64_t rcells = (int64_t)rg.R * rg.Gy;
+        k_row_grid_build<<<(int)std::min<int64_t>((rcells + 7) / 8, kSMs * 16), 256, 0, st>>>(
+            rg, dc.p, (int)k);
+        JB_LAUNCH_CHECK();
     }
-    const int TB = 256;
+    if (k > 2048) {
+        if (n > 0) {
+            JB_PROF("assign_stats", st);
+            k_stats_global<<<(int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, kSMs * 8)),
+                             256, 0, st>>>(reinterpret_cast<const double2*>(d_pts), d_len, n, d_labels,
+                                           (int)k, Ex, Ey, Bx, By, acc.p);
+        }
+        JB_LAUNCH_CHECK();
+    } else {
+    int per_sm = 1;
+    JB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_assign_stats, AS_TB, smem));
     const int grid = (int)std::max<int64_t>(
-        1, std::min<int64_t>((n + TB * 4 - 1) / (TB * 4), (int64_t)kSMs * 4));
-    // packed count|len is safe when a block's count < 2^24 and length sum < 2^40
-    const int64_t per_block = (n + grid - 1) / grid;
-    const int packed = use_smem && per_block < (1LL << 24) &&
-                       (double)per_block * max_len < 1099511627776.0;
-    {
+        1, std::min<int64_t>((n + AS_TB * AS_U - 1) / (AS_TB * AS_U),
+                             (int64_t)kSMs * std::max(per_sm, 1)));
+    if (n > 0) {
         JB_PROF("assign_stats", st);
-        k_assign_stats<<<use_smem ? grid : (int)std::max<int64_t>(
-                                              1, std::min<int64_t>((n + TB - 1) / TB, kSMs * 8)),
-                         TB, smem, st>>>(reinterpret_cast<const double2*>(d_pts), d_len, n, dc.p,
-                                         (int)k, do_assign ? 1 : 0, d_labels, Ex, Ey, Bx, By,
-                                         acc.p, use_smem, packed, cg);
+        k_assign_stats<<<grid, AS_TB, smem, st>>>(reinterpret_cast<const double2*>(d_pts), d_len, n,
+                                                  dc.p, (int)k, do_assign ? 1 : 0, d_labels, Ex, Ey,
+                                                  Bx, By, acc.p, cg, rg, RH);
     }
     JB_LAUNCH_CHECK();
+    }
     std::vector<unsigned long long> h = acc.to_host(7 * k);
     // exact per-cluster records: count, len sum, first index (global), unbiased sums
     std::vector<unsigned long long> rec(7 * k);

@@ -239,7 +239,8 @@ struct GroupStats {
 void assign_and_stats(const double* d_pts, const int32_t* d_len, int64_t n,
                       const std::vector<double>& centers, uint64_t k, const BBox& bb,
                       bool do_assign, uint32_t* d_labels, GroupStats& gs, cudaStream_t st,
-                      int32_t max_len, const Comm* cm = nullptr, int64_t first_base = 0);
+                      int32_t max_len, double scl, double sigma_len, const Comm* cm = nullptr,
+                      int64_t first_base = 0);
 
 void relabel(uint32_t* d_labels, int64_t n, const std::vector<uint32_t>& rank_of,
              cudaStream_t st);
