@@ -459,6 +459,11 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
     fit->scaling[1] = sc.sigma_len;
     fit->scaling[2] = sc.sigma_inc;
     const BBox bb{sc.xmin, sc.xmax, sc.ymin, sc.ymax};
+    PieceRows rows;  // x = scl * len / sigma_len: exact row grids in k-means
+    rows.len = fit->pieces.len.p;
+    rows.scl = sc.scl;
+    rows.sl = sc.sigma_len;
+    rows.max_len = sc.max_len_global;
     fit->phase_ms[1] = ms_since(t1);
 
     // ---- run_backend (digitization.hpp:131-198) ----
@@ -485,10 +490,10 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
                 k_iota_pos<<<gsz(N), 256, 0, st>>>(gpos.p, lidx.p, N, (uint64_t)base);
                 JB_LAUNCH_CHECK();
                 lloyd_best_dist(cm, sc.pts.p, lidx.p, gpos.p, N, (uint64_t)N_glob, c.k, c.max_iters,
-                                c.n_init, raw.p, raw_count, &cursor, bb, km, st);
+                                c.n_init, raw.p, raw_count, &cursor, bb, km, st, rows);
             } else {
                 lloyd_best_device(sc.pts.p, nullptr, N, c.k, c.max_iters, c.n_init, raw.p,
-                                  raw_count, &cursor, bb, km, st);
+                                  raw_count, &cursor, bb, km, st, rows);
             }
             k = c.k;
             backend_centers = km.centers;
@@ -532,11 +537,11 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
                                                                  (uint64_t)base, lidx.p);
                 JB_LAUNCH_CHECK();
                 lloyd_best_dist(cm, sc.pts.p, lidx.p, gpos.p, n_sample_local, S, c.k, c.max_iters,
-                                c.n_init, raw.p, raw_count, &cursor, bb, km, st);
+                                c.n_init, raw.p, raw_count, &cursor, bb, km, st, rows);
                 sample = std::move(lidx);
             } else {
                 lloyd_best_device(sc.pts.p, sample.p, (int64_t)S, c.k, c.max_iters, c.n_init,
-                                  raw.p, raw_count, &cursor, bb, km, st);
+                                  raw.p, raw_count, &cursor, bb, km, st, rows);
                 n_sample_local = (int64_t)S;
             }
             k = c.k;

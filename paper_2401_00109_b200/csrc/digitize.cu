@@ -466,11 +466,9 @@ void assign_and_stats(const double* d_pts, const int32_t* d_len, int64_t n,
         rg_cell.alloc((size_t)rg.R * rg.Gy, st);
         rg.cell = rg_cell.p;
         JB_PROF("assign_grid", st);
-        k_grid_build<<<std::min(G * G / 8, kSMs * 16), 256, 0, st>>>(cg, dc.p, (int)k);
+        launch_grid_build(cg, dc.p, (int)k, st);
         JB_LAUNCH_CHECK();
-        const int64_t rcells = (int64_t)rg.R * rg.Gy;
-        k_row_grid_build<<<(int)std::min<int64_t>((rcells + 7) / 8, kSMs * 16), 256, 0, st>>>(
-            rg, dc.p, (int)k);
+        launch_row_grid_build(rg, dc.p, (int)k, st);
         JB_LAUNCH_CHECK();
     }
     if (k > 2048) {

@@ -177,6 +177,30 @@ __host__ __device__ inline i128 fx_load(const unsigned long long* lohi) {
     return (i128)(((u128)lohi[1] << 64) | (u128)lohi[0]);
 }
 
+// int128 accumulator held as three u64 limb sums: bits 0-31 and 32-63 of each
+// addend (unsigned) and bits 64-127 (two's complement). No add needs the old
+// value, so every add is a fire-and-forget RED (an int128 add through a
+// (lo, hi) pair must wait for the low word to learn its carry). Exact while
+// fewer than 2^32 addends reach a limb between normalisations (l3_norm).
+__device__ __forceinline__ void l3_add(unsigned long long* p, i128 v) {
+    const u128 u = (u128)v;
+    const unsigned long long a = (unsigned long long)(u & 0xFFFFFFFFu);
+    const unsigned long long b = (unsigned long long)((u >> 32) & 0xFFFFFFFFu);
+    const unsigned long long c = (unsigned long long)(u >> 64);
+    if (a) atomicAdd(p, a);
+    if (b) atomicAdd(p + 1, b);
+    if (c) atomicAdd(p + 2, c);
+}
+__host__ __device__ __forceinline__ i128 l3_load(const unsigned long long* p) {
+    return (i128)((u128)p[0] + ((u128)p[1] << 32) + ((u128)p[2] << 64));
+}
+__host__ __device__ __forceinline__ void l3_store(unsigned long long* p, i128 v) {
+    const u128 u = (u128)v;
+    p[0] = (unsigned long long)(u & 0xFFFFFFFFu);
+    p[1] = (unsigned long long)((u >> 32) & 0xFFFFFFFFu);
+    p[2] = (unsigned long long)(u >> 64);
+}
+
 // warp-level int128 sum (deterministic: integer adds)
 __device__ __forceinline__ i128 fx_warp_sum(i128 v) {
     unsigned long long lo = (unsigned long long)(u128)v;

@@ -212,6 +212,15 @@ uint64_t sample_indices_device(uint64_t n, uint64_t S, const uint64_t* d_raw, ui
 // Raw std::mt19937_64 stream on device.
 void mt19937_64_generate(uint64_t seed, uint64_t count, DArr<uint64_t>& out, cudaStream_t st);
 
+// Integer piece lengths behind the scaled points (x = scl * len / sl): lets
+// the k-means kernels use the exact row grid (jb_rowgrid.cuh). len == null:
+// 2-D grid only.
+struct PieceRows {
+    const int32_t* len = nullptr;  // per piece, indexed like d_pts
+    double scl = 1.0, sl = 1.0;
+    int32_t max_len = 0;           // global maximum piece length
+};
+
 // Best-of-n_init lloyd_once (clustering.hpp:200-236) on the points
 // d_pts[d_idx[i]] (or d_pts[i] when d_idx is null), i < n; 2-interleaved
 // device doubles. Draws are consumed from d_raw starting at *cursor (updated).
@@ -219,7 +228,7 @@ void mt19937_64_generate(uint64_t seed, uint64_t count, DArr<uint64_t>& out, cud
 void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, uint64_t k,
                        uint64_t max_iters, uint64_t n_init, const uint64_t* d_raw,
                        uint64_t raw_count, uint64_t* cursor, const BBox& bb, KMeansOut& out,
-                       cudaStream_t st);
+                       cudaStream_t st, const PieceRows& rows = PieceRows{});
 
 // Distributed variant: this rank holds the sample entries it owns -- local
 // piece index d_lidx[i] and global sample position d_gpos[i] (ascending), n
@@ -228,7 +237,8 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
 void lloyd_best_dist(const Comm& cm, const double* d_pts, const uint64_t* d_lidx,
                      const uint32_t* d_gpos, int64_t n, uint64_t S, uint64_t k, uint64_t max_iters,
                      uint64_t n_init, const uint64_t* d_raw, uint64_t raw_count, uint64_t* cursor,
-                     const BBox& bb, KMeansOut& out, cudaStream_t st);
+                     const BBox& bb, KMeansOut& out, cudaStream_t st,
+                     const PieceRows& rows = PieceRows{});
 
 // Per-point nearest center (clustering.hpp:146-163) with exact tie rule, plus
 // group statistics for digitize (digitization.hpp:217-231).

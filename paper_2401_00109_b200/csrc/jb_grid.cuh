@@ -56,51 +56,135 @@ __device__ __forceinline__ void grid_box_d2(double cx, double cy, double bx0, do
     dmax2 = fx * fx + fy * fy;
 }
 
-// one warp per cell
-static __global__ void k_grid_build(CandGrid g, const double* __restrict__ centers, int k) {
-    const int lane = threadIdx.x & 31;
-    const int ncell = g.G * g.G;
-    for (int cell = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; cell < ncell;
-         cell += (gridDim.x * blockDim.x) >> 5) {
-        const int ix = cell % g.G, iy = cell / g.G;
-        const double bx0 = g.x0 + ix * g.w - g.mw, bx1 = g.x0 + (ix + 1) * g.w + g.mw;
-        const double by0 = g.y0 + iy * g.h - g.mh, by1 = g.y0 + (iy + 1) * g.h + g.mh;
-        double M = INFINITY;
-        for (int c = lane; c < k; c += 32) {
+// Candidate lists of a block of cells (one CTA): the centers kept for the
+// block's bounding box, then every cell filtered against that short list.
+// Exactly the flat per-cell result: for a cell box b inside the block box B
+// (B's edges are the SAME rounded expressions as the edge cells' edges, and
+// rounding is monotone), dmin2(c,b) >= dmin2(c,B) and M_b <= M_B, so a center
+// dropped for B is dropped for b; and the argmin of dmax2(., b) is never
+// dropped for B (dmax2(c*,b) = M_b <= M_B < dmin2(c*,B) <= dmax2(c*,b) would
+// follow), so M over the short list is M_b.
+constexpr int kBuildTB = 256;
+constexpr int kBuildList = 512;  // block candidates kept in smem (else: all centers)
+
+struct BlockCands {
+    uint16_t list[kBuildList];
+    int n;
+    int wc[kBuildTB / 32];
+    double wmin[kBuildTB / 32];
+};
+
+// block-wide: s.list/s.n := centers kept for box (bx0,bx1,by0,by1), index order
+__device__ inline void block_candidates(BlockCands& s, const double* __restrict__ centers, int k,
+                                        double bx0, double bx1, double by0, double by1) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double M = INFINITY;
+    for (int c = threadIdx.x; c < k; c += kBuildTB) {
+        double dmn, dmx;
+        grid_box_d2(centers[2 * c], centers[2 * c + 1], bx0, bx1, by0, by1, dmn, dmx);
+        M = fmin(M, dmx);
+    }
+    for (int o = 16; o > 0; o >>= 1) M = fmin(M, __shfl_xor_sync(0xffffffffu, M, o));
+    if (lane == 0) s.wmin[warp] = M;
+    if (threadIdx.x == 0) s.n = 0;
+    __syncthreads();
+    M = s.wmin[0];
+    for (int w = 1; w < kBuildTB / 32; ++w) M = fmin(M, s.wmin[w]);
+    const double thr = M * (1.0 + 1e-12) + 1e-300;
+    for (int c0 = 0; c0 < k; c0 += kBuildTB) {
+        const int c = c0 + threadIdx.x;
+        bool keep = false;
+        if (c < k) {
             double dmn, dmx;
             grid_box_d2(centers[2 * c], centers[2 * c + 1], bx0, bx1, by0, by1, dmn, dmx);
-            M = fmin(M, dmx);
+            keep = dmn <= thr;
         }
-        for (int o = 16; o > 0; o >>= 1) M = fmin(M, __shfl_xor_sync(0xffffffffu, M, o));
-        const double thr = M * (1.0 + 1e-12) + 1e-300;
-        int nc = 0;
-        uint16_t* out = g.cand + (size_t)cell * g.cap;
-        for (int c0 = 0; c0 < k; c0 += 32) {
-            const int c = c0 + lane;
-            bool keep = false;
-            if (c < k) {
-                double dmn, dmx;
-                grid_box_d2(centers[2 * c], centers[2 * c + 1], bx0, bx1, by0, by1, dmn, dmx);
-                keep = dmn <= thr;
-            }
-            const unsigned m = __ballot_sync(0xffffffffu, keep);
-            const int at = nc + __popc(m & ((1u << lane) - 1u));
-            if (keep && at < g.cap) out[at] = (uint16_t)c;
-            nc += __popc(m);
-        }
-        if (lane == 0) g.cnt[cell] = nc <= g.cap ? (uint16_t)nc : (uint16_t)0xFFFF;
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) s.wc[warp] = __popc(m);
+        __syncthreads();
+        int off = s.n;
+        for (int w = 0; w < warp; ++w) off += s.wc[w];
+        off += __popc(m & ((1u << lane) - 1u));
+        if (keep && off < kBuildList) s.list[off] = (uint16_t)c;
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int w = 0; w < kBuildTB / 32; ++w) s.n += s.wc[w];
+        __syncthreads();
     }
+}
+
+constexpr int kGridBlock = 16;  // cells per block side: one thread per cell
+
+// thread-wide candidate filter of one cell box over the block list (or all k
+// centers); writes up to cap indices in index order, returns the full count
+__device__ __forceinline__ int thread_cell_candidates(const double* __restrict__ centers, int k,
+                                                      const BlockCands& s, double bx0, double bx1,
+                                                      double by0, double by1, uint16_t* out,
+                                                      int cap) {
+    const bool all = s.n > kBuildList;
+    const int m = all ? k : s.n;
+    double M = INFINITY;
+    for (int j = 0; j < m; ++j) {
+        const int c = all ? j : s.list[j];
+        double dmn, dmx;
+        grid_box_d2(centers[2 * c], centers[2 * c + 1], bx0, bx1, by0, by1, dmn, dmx);
+        M = fmin(M, dmx);
+    }
+    const double thr = M * (1.0 + 1e-12) + 1e-300;
+    int nc = 0;
+    for (int j = 0; j < m; ++j) {
+        const int c = all ? j : s.list[j];
+        double dmn, dmx;
+        grid_box_d2(centers[2 * c], centers[2 * c + 1], bx0, bx1, by0, by1, dmn, dmx);
+        if (dmn <= thr) {
+            if (nc < cap) out[nc] = (uint16_t)c;
+            ++nc;
+        }
+    }
+    return nc;
+}
+
+// one CTA per kGridBlock x kGridBlock block of cells, one thread per cell
+static __global__ void __launch_bounds__(kBuildTB) k_grid_build(CandGrid g,
+                                                                const double* __restrict__ centers,
+                                                                int k) {
+    __shared__ BlockCands s;
+    const int Gb = (g.G + kGridBlock - 1) / kGridBlock;
+    for (int blk = blockIdx.x; blk < Gb * Gb; blk += gridDim.x) {
+        const int ix0 = (blk % Gb) * kGridBlock, iy0 = (blk / Gb) * kGridBlock;
+        const int ix1 = min(ix0 + kGridBlock, g.G) - 1, iy1 = min(iy0 + kGridBlock, g.G) - 1;
+        block_candidates(s, centers, k, g.x0 + ix0 * g.w - g.mw, g.x0 + (ix1 + 1) * g.w + g.mw,
+                         g.y0 + iy0 * g.h - g.mh, g.y0 + (iy1 + 1) * g.h + g.mh);
+        const int ix = ix0 + (int)threadIdx.x % kGridBlock, iy = iy0 + (int)threadIdx.x / kGridBlock;
+        if (ix <= ix1 && iy <= iy1) {
+            const int cell = iy * g.G + ix;
+            const int nc = thread_cell_candidates(
+                centers, k, s, g.x0 + ix * g.w - g.mw, g.x0 + (ix + 1) * g.w + g.mw,
+                g.y0 + iy * g.h - g.mh, g.y0 + (iy + 1) * g.h + g.mh,
+                g.cand + (size_t)cell * g.cap, g.cap);
+            g.cnt[cell] = nc <= g.cap ? (uint16_t)nc : (uint16_t)0xFFFF;
+        }
+        __syncthreads();
+    }
+}
+
+inline void launch_grid_build(const CandGrid& g, const double* centers, int k, cudaStream_t st) {
+    const int Gb = (g.G + kGridBlock - 1) / kGridBlock;
+    k_grid_build<<<Gb * Gb, kBuildTB, 0, st>>>(g, centers, k);
 }
 
 // nearest_center (clustering.hpp:146-157) through the grid; cx/cy in smem
 __device__ __forceinline__ uint32_t grid_nearest(const CandGrid& g, double px, double py,
                                                  const double* cx, const double* cy, int k) {
-    int ix = (int)((px - g.x0) * g.invw);
-    int iy = (int)((py - g.y0) * g.invh);
-    ix = min(max(ix, 0), g.G - 1);
-    iy = min(max(iy, 0), g.G - 1);
-    const int cell = iy * g.G + ix;
-    const int n = __ldg(g.cnt + cell);
+    int n = 0xFFFF, cell = 0;  // G == 0: no grid, every center
+    if (g.G > 0) {
+        int ix = (int)((px - g.x0) * g.invw);
+        int iy = (int)((py - g.y0) * g.invh);
+        ix = min(max(ix, 0), g.G - 1);
+        iy = min(max(iy, 0), g.G - 1);
+        cell = iy * g.G + ix;
+        n = __ldg(g.cnt + cell);
+    }
     uint32_t best = 0;
     double bd = __longlong_as_double(0x7FF0000000000000LL);  // +inf
     if (n == 0xFFFF) {

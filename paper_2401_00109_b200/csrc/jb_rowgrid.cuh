@@ -9,7 +9,8 @@
 // very expression k_scale uses, so a point of length l lies on x_l exactly.
 // A cell packs up to 4 candidate indices (ascending) in one 64-bit word; a
 // cell with ONE candidate decides the label without any arithmetic. Longer
-// pieces and overflowing cells fall back to the 2-D grid.
+// pieces, overflowing cells (low half-word 0xFFFE) and cells not built (all
+// ones: a built cell always holds >= 1 candidate) fall back to the 2-D grid.
 #pragma once
 
 #include "jb_grid.cuh"
@@ -48,46 +49,65 @@ __device__ __forceinline__ double row_x(const RowGrid& g, int l) {
     return __ddiv_rn(__dmul_rn(g.scl, (double)l), g.sl);  // == k_scale: scl * (double)L / sl
 }
 
-// one warp per cell
-static __global__ void k_row_grid_build(RowGrid g, const double* __restrict__ centers, int k) {
-    const int lane = threadIdx.x & 31;
-    const int64_t ncell = (int64_t)g.R * g.Gy;
-    for (int64_t cell = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; cell < ncell;
-         cell += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        const int row = (int)(cell / g.Gy), iy = (int)(cell % g.Gy);
+constexpr int kRowSeg = kBuildTB;  // y cells per CTA block, one thread per cell
+
+// one CTA per (length, kRowSeg y cells) segment; blocks: the segments to
+// build (null: all of them)
+static __global__ void __launch_bounds__(kBuildTB) k_row_grid_build(RowGrid g,
+                                                                    const double* __restrict__ centers,
+                                                                    int k, const int* __restrict__ blocks,
+                                                                    int nblocks) {
+    __shared__ BlockCands s;
+    const int nseg = (g.Gy + kRowSeg - 1) / kRowSeg;
+    for (int bi = blockIdx.x; bi < nblocks; bi += gridDim.x) {
+        const int blk = blocks ? blocks[bi] : bi;
+        const int row = blk / nseg, iy0 = (blk % nseg) * kRowSeg;
+        const int iy1 = min(iy0 + kRowSeg, g.Gy) - 1;
         const double x = row_x(g, row + 1);
-        const double by0 = g.y0 + iy * g.h - g.mh, by1 = g.y0 + (iy + 1) * g.h + g.mh;
-        double M = INFINITY;
-        for (int c = lane; c < k; c += 32) {
-            double dmn, dmx;
-            grid_box_d2(centers[2 * c], centers[2 * c + 1], x, x, by0, by1, dmn, dmx);
-            M = fmin(M, dmx);
-        }
-        for (int o = 16; o > 0; o >>= 1) M = fmin(M, __shfl_xor_sync(0xffffffffu, M, o));
-        const double thr = M * (1.0 + 1e-12) + 1e-300;
-        int nc = 0;
-        uint64_t word = ~0ull;  // all slots empty
-        for (int c0 = 0; c0 < k && nc <= 4; c0 += 32) {
-            const int c = c0 + lane;
-            bool keep = false;
-            if (c < k) {
-                double dmn, dmx;
-                grid_box_d2(centers[2 * c], centers[2 * c + 1], x, x, by0, by1, dmn, dmx);
-                keep = dmn <= thr;
-            }
-            unsigned m = __ballot_sync(0xffffffffu, keep);
-            while (m && nc < 5) {
-                const int l = __ffs(m) - 1;
-                m &= m - 1;
-                if (nc < 4) {
-                    word &= ~(0xFFFFull << (16 * nc));
-                    word |= (uint64_t)(c0 + l) << (16 * nc);
+        block_candidates(s, centers, k, x, x, g.y0 + iy0 * g.h - g.mh, g.y0 + (iy1 + 1) * g.h + g.mh);
+        const int iy = iy0 + (int)threadIdx.x;
+        if (iy <= iy1) {
+            uint16_t tmp[4];
+            const int nc = thread_cell_candidates(centers, k, s, x, x, g.y0 + iy * g.h - g.mh,
+                                                  g.y0 + (iy + 1) * g.h + g.mh, tmp, 4);
+            uint64_t word;
+            if (nc > 4) {
+                word = (~0ull << 16) | kRowOverflow;
+            } else {
+                word = ~0ull;
+                for (int j = 0; j < nc; ++j) {
+                    word &= ~(0xFFFFull << (16 * j));
+                    word |= (uint64_t)tmp[j] << (16 * j);
                 }
-                ++nc;
             }
+            g.cell[(size_t)row * g.Gy + iy] = word;
         }
-        if (nc > 4) word = (~0ull << 16) | kRowOverflow;
-        if (lane == 0) g.cell[cell] = word;
+        __syncthreads();
+    }
+}
+
+inline int row_grid_segments(const RowGrid& g) { return g.R * ((g.Gy + kRowSeg - 1) / kRowSeg); }
+
+inline void launch_row_grid_build(const RowGrid& g, const double* centers, int k, cudaStream_t st,
+                                  const int* blocks = nullptr, int nblocks = -1) {
+    if (nblocks < 0) nblocks = row_grid_segments(g);
+    if (nblocks > 0)
+        k_row_grid_build<<<nblocks, kBuildTB, 0, st>>>(g, centers, k, blocks, nblocks);
+}
+
+// segments holding at least one point (length l <= R, y) -> flags[segment] = 1
+static __global__ void k_row_occupancy(RowGrid g, const double2* __restrict__ pts,
+                                       const int32_t* __restrict__ len, int64_t n,
+                                       int* __restrict__ flags) {
+    const int nseg = (g.Gy + kRowSeg - 1) / kRowSeg;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int l = len[i];
+        if (l < 1 || l > g.R) continue;
+        int iy = (int)((pts[i].y - g.y0) * g.invh);
+        iy = min(max(iy, 0), g.Gy - 1);
+        const int f = (l - 1) * nseg + iy / kRowSeg;
+        if (!flags[f]) flags[f] = 1;
     }
 }
 
@@ -101,7 +121,7 @@ __device__ __forceinline__ uint32_t row_nearest(const RowGrid& rg, const CandGri
         const uint64_t w = __ldg(reinterpret_cast<const unsigned long long*>(rg.cell) +
                                  (size_t)(len - 1) * rg.Gy + iy);
         const uint32_t c0 = (uint32_t)(w & 0xFFFF);
-        if (c0 != kRowOverflow) {
+        if (c0 < kRowOverflow) {
             uint32_t best = c0;
             const uint32_t c1 = (uint32_t)((w >> 16) & 0xFFFF);
             if (c1 == kRowEmpty) return best;  // the only possible argmin

@@ -32,6 +32,7 @@
 
 #include "jb_device.hpp"
 #include "jb_grid.cuh"
+#include "jb_rowgrid.cuh"
 
 namespace jb {
 
@@ -412,23 +413,27 @@ __global__ void k_morton(const double2* __restrict__ pts, const uint64_t* __rest
 
 __global__ void k_sorted_gather(const double2* __restrict__ pts, const uint64_t* __restrict__ idx,
                                 const uint32_t* __restrict__ orig, int64_t n,
-                                double2* __restrict__ spts, uint32_t* __restrict__ pos) {
+                                double2* __restrict__ spts, uint32_t* __restrict__ pos,
+                                const int32_t* __restrict__ len, int32_t* __restrict__ slen) {
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
          r += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t o = orig[r];
         spts[r] = load_pt(pts, idx, o);
         pos[o] = (uint32_t)r;
+        if (len) slen[r] = len[idx ? idx[o] : o];
     }
 }
 
 // box = (x0, x1, y0, y1)
 __global__ void k_tile_boxes(const double2* __restrict__ spts, int64_t n,
-                             double4* __restrict__ tbox) {
+                             double4* __restrict__ tbox, const int32_t* __restrict__ slen,
+                             int32_t* __restrict__ tlen) {
     const int lane = threadIdx.x & 31;
     const int64_t ntiles = (n + TILE - 1) / TILE;
     for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < ntiles;
          t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         double x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY;
+        int lmin = 0x7FFFFFFF, lmax = -1;
         for (int i = 0; i < TILE / 32; ++i) {
             const int64_t r = t * TILE + i * 32 + lane;
             if (r < n) {
@@ -437,7 +442,16 @@ __global__ void k_tile_boxes(const double2* __restrict__ spts, int64_t n,
                 x1 = fmax(x1, p.x);
                 y0 = fmin(y0, p.y);
                 y1 = fmax(y1, p.y);
+                if (slen) {
+                    lmin = min(lmin, slen[r]);
+                    lmax = max(lmax, slen[r]);
+                }
             }
+        }
+        if (slen) {  // the tile's common piece length, or 0
+            lmin = __reduce_min_sync(0xffffffffu, lmin);
+            lmax = __reduce_max_sync(0xffffffffu, lmax);
+            if (lane == 0) tlen[t] = lmin == lmax ? lmin : 0;
         }
         for (int o = 16; o > 0; o >>= 1) {
             x0 = fmin(x0, __shfl_xor_sync(0xffffffffu, x0, o));
@@ -730,8 +744,8 @@ __global__ void k_copy_center(const double2* __restrict__ spts, const uint32_t* 
 // Lloyd
 
 struct ClusterAcc {
-    unsigned long long* sx;   // 2k
-    unsigned long long* sy;   // 2k
+    unsigned long long* sx;   // 3k: l3 limbs per cluster
+    unsigned long long* sy;   // 3k
     unsigned long long* cnt;  // k (two's complement deltas)
 };
 
@@ -748,95 +762,227 @@ constexpr int LL_TB = 256;
 // point already: it is skipped without reading its points.
 constexpr uint32_t MIXED = 0xFFFFFFFFu;
 
-__global__ void k_tile_check(const double4* __restrict__ tbox, int64_t ntiles, CandGrid g,
-                             const double* __restrict__ centers,
-                             const uint32_t* __restrict__ tlab, uint32_t* __restrict__ tnew,
-                             uint32_t* __restrict__ work, unsigned long long* __restrict__ nwork,
-                             const int* __restrict__ skip_flag, int force_all) {
-    if (skip_flag && (skip_flag[0] | skip_flag[1])) return;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntiles;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const double4 b = tbox[t];  // (x0, x1, y0, y1)
-        int ix0 = (int)((b.x - g.x0) * g.invw), ix1 = (int)((b.y - g.x0) * g.invw);
-        int iy0 = (int)((b.z - g.y0) * g.invh), iy1 = (int)((b.w - g.y0) * g.invh);
-        ix0 = min(max(ix0, 0), g.G - 1);
-        ix1 = min(max(ix1, 0), g.G - 1);
-        iy0 = min(max(iy0, 0), g.G - 1);
-        iy1 = min(max(iy1, 0), g.G - 1);
-        uint32_t single = MIXED;
-        if ((ix1 - ix0 + 1) * (iy1 - iy0 + 1) <= 4) {
-            bool ok = true;
-            double M = INFINITY;
-            for (int iy = iy0; iy <= iy1 && ok; ++iy)
-                for (int ix = ix0; ix <= ix1 && ok; ++ix) {
-                    const int cell = iy * g.G + ix;
-                    const int n = __ldg(g.cnt + cell);
-                    if (n == 0xFFFF) {
-                        ok = false;
-                        break;
-                    }
-                    const uint16_t* cl = g.cand + (size_t)cell * g.cap;
-                    for (int j = 0; j < n; ++j) {
-                        const int c = __ldg(cl + j);
-                        double dmn, dmx;
-                        box_d2(__ldg(centers + 2 * c), __ldg(centers + 2 * c + 1), b, dmn, dmx);
-                        M = fmin(M, dmx);
-                    }
+// Row tile (every point of one length l, so x0 == x1 == x_l): the union of
+// the candidate words of the row cells covering [y0, y1], pruned again with
+// the tile box. Returns false when a cell overflows or the span is long.
+__device__ __forceinline__ bool row_tile_single(const RowGrid& rg, int l, const double4& b,
+                                                const double* __restrict__ centers,
+                                                uint32_t& single) {
+    int iy0 = (int)((b.z - rg.y0) * rg.invh), iy1 = (int)((b.w - rg.y0) * rg.invh);
+    iy0 = min(max(iy0, 0), rg.Gy - 1);
+    iy1 = min(max(iy1, 0), rg.Gy - 1);
+    if (iy1 - iy0 >= 8) return false;
+    const unsigned long long* row =
+        reinterpret_cast<const unsigned long long*>(rg.cell) + (size_t)(l - 1) * rg.Gy;
+    double M = INFINITY;
+    for (int iy = iy0; iy <= iy1; ++iy) {
+        const uint64_t w = __ldg(row + iy);
+        if ((w & 0xFFFF) >= kRowOverflow) return false;  // overflow / not built
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t c = (uint32_t)((w >> (16 * j)) & 0xFFFF);
+            if (c == kRowEmpty) break;
+            double dmn, dmx;
+            box_d2(__ldg(centers + 2 * c), __ldg(centers + 2 * c + 1), b, dmn, dmx);
+            M = fmin(M, dmx);
+        }
+    }
+    const double thr = M * (1.0 + kKeepMargin) + 1e-300;
+    uint32_t first = MIXED;
+    for (int iy = iy0; iy <= iy1; ++iy) {
+        const uint64_t w = __ldg(row + iy);
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t c = (uint32_t)((w >> (16 * j)) & 0xFFFF);
+            if (c == kRowEmpty) break;
+            double dmn, dmx;
+            box_d2(__ldg(centers + 2 * c), __ldg(centers + 2 * c + 1), b, dmn, dmx);
+            if (dmn <= thr) {
+                if (first == MIXED) first = c;
+                else if (c != first) {
+                    single = MIXED;
+                    return true;
                 }
-            if (ok) {
-                const double thr = M * (1.0 + kKeepMargin) + 1e-300;
-                uint32_t first = MIXED;
-                bool multi = false;
-                for (int iy = iy0; iy <= iy1 && !multi; ++iy)
-                    for (int ix = ix0; ix <= ix1 && !multi; ++ix) {
-                        const int cell = iy * g.G + ix;
-                        const int n = __ldg(g.cnt + cell);
-                        const uint16_t* cl = g.cand + (size_t)cell * g.cap;
-                        for (int j = 0; j < n; ++j) {
-                            const uint32_t c = __ldg(cl + j);
-                            double dmn, dmx;
-                            box_d2(__ldg(centers + 2 * c), __ldg(centers + 2 * c + 1), b, dmn,
-                                   dmx);
-                            if (dmn <= thr) {
-                                if (first == MIXED) first = c;
-                                else if (c != first) {
-                                    multi = true;
-                                    break;
-                                }
-                            }
-                        }
-                    }
-                if (!multi) single = first;
             }
         }
-        tnew[t] = single;
-        if (force_all || single == MIXED || single != tlab[t])
-            work[atomicAdd(nwork, 1ULL)] = (uint32_t)t;
+    }
+    single = first;
+    return true;
+}
+
+// Single-center test of a box b (tile or super-tile) with common piece length
+// l (0: mixed): the row grid when it applies, else the 2-D grid cells.
+__device__ __forceinline__ uint32_t box_single(const double4& b, int l, const CandGrid& g,
+                                               const RowGrid& rg,
+                                               const double* __restrict__ centers) {
+    uint32_t single;
+    if (l >= 1 && l <= rg.R && row_tile_single(rg, l, b, centers, single)) return single;
+    if (g.G == 0) return MIXED;  // no 2-D grid (row grid in use)
+    int ix0 = (int)((b.x - g.x0) * g.invw), ix1 = (int)((b.y - g.x0) * g.invw);
+    int iy0 = (int)((b.z - g.y0) * g.invh), iy1 = (int)((b.w - g.y0) * g.invh);
+    ix0 = min(max(ix0, 0), g.G - 1);
+    ix1 = min(max(ix1, 0), g.G - 1);
+    iy0 = min(max(iy0, 0), g.G - 1);
+    iy1 = min(max(iy1, 0), g.G - 1);
+    if ((ix1 - ix0 + 1) * (iy1 - iy0 + 1) > 4) return MIXED;
+    double M = INFINITY;
+    for (int iy = iy0; iy <= iy1; ++iy)
+        for (int ix = ix0; ix <= ix1; ++ix) {
+            const int cell = iy * g.G + ix;
+            const int n = __ldg(g.cnt + cell);
+            if (n == 0xFFFF) return MIXED;
+            const uint16_t* cl = g.cand + (size_t)cell * g.cap;
+            for (int j = 0; j < n; ++j) {
+                const int c = __ldg(cl + j);
+                double dmn, dmx;
+                box_d2(__ldg(centers + 2 * c), __ldg(centers + 2 * c + 1), b, dmn, dmx);
+                M = fmin(M, dmx);
+            }
+        }
+    const double thr = M * (1.0 + kKeepMargin) + 1e-300;
+    uint32_t first = MIXED;
+    for (int iy = iy0; iy <= iy1; ++iy)
+        for (int ix = ix0; ix <= ix1; ++ix) {
+            const int cell = iy * g.G + ix;
+            const int n = __ldg(g.cnt + cell);
+            const uint16_t* cl = g.cand + (size_t)cell * g.cap;
+            for (int j = 0; j < n; ++j) {
+                const uint32_t c = __ldg(cl + j);
+                double dmn, dmx;
+                box_d2(__ldg(centers + 2 * c), __ldg(centers + 2 * c + 1), b, dmn, dmx);
+                if (dmn <= thr) {
+                    if (first == MIXED) first = c;
+                    else if (c != first) return MIXED;
+                }
+            }
+        }
+    return first;
+}
+
+// Super-tile check (32 consecutive tiles = 4096 points), one thread each. A
+// super-tile whose box is SINGLE with the center it was SINGLE with last
+// time holds that label on all its points (its state is reset to MIXED
+// whenever a point of it is relabeled outside this scheme, k_repair): it is
+// skipped. The others are listed for k_lloyd_work. State: tlab[ntiles + s].
+__global__ void k_super_check(const double4* __restrict__ sbox, const int32_t* __restrict__ slenc,
+                              int64_t ntiles, CandGrid g, const double* __restrict__ centers,
+                              uint32_t* __restrict__ tlab, uint32_t* __restrict__ swork,
+                              unsigned long long* __restrict__ nswork,
+                              const int* __restrict__ skip_flag, int force_all, RowGrid rg) {
+    if (skip_flag && (skip_flag[0] | skip_flag[1])) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t nsuper = (ntiles + 31) / 32;
+    uint32_t* stlab = tlab + ntiles;
+    const int64_t wstride = (((int64_t)gridDim.x * blockDim.x) >> 5) * 32;
+    for (int64_t s0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * 32; s0 < nsuper;
+         s0 += wstride) {
+        const int64_t sidx = s0 + lane;
+        bool need = false;
+        if (sidx < nsuper) {
+            const uint32_t ss = force_all ? MIXED
+                                          : box_single(sbox[sidx], slenc ? slenc[sidx] : 0, g, rg,
+                                                       centers);
+            need = force_all || ss == MIXED || ss != stlab[sidx];
+            if (need) stlab[sidx] = ss;  // all its points carry ss after this iteration
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, need);
+        unsigned long long base = 0;
+        if (lane == 0 && m) base = atomicAdd(nswork, (unsigned long long)__popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (need) swork[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)sidx;
+    }
+}
+
+// Tiles of the listed super-tiles (warp per super-tile, lane per tile): the
+// tiles whose single-center state changed or is MIXED are listed for
+// k_lloyd_work with their new state in tnew.
+__global__ void k_tile_expand(const uint32_t* __restrict__ swork,
+                              const unsigned long long* __restrict__ nswork,
+                              const double4* __restrict__ tbox, const int32_t* __restrict__ tlen,
+                              int64_t ntiles, CandGrid g, const double* __restrict__ centers,
+                              const uint32_t* __restrict__ tlab, uint32_t* __restrict__ tnew,
+                              uint32_t* __restrict__ work, unsigned long long* __restrict__ nwork,
+                              const int* __restrict__ skip_flag, int force_all, RowGrid rg) {
+    if (skip_flag && (skip_flag[0] | skip_flag[1])) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)*nswork;
+    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nw;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t t = (int64_t)swork[w] * 32 + lane;
+        bool add = false;
+        if (t < ntiles) {
+            const uint32_t single =
+                force_all ? MIXED : box_single(tbox[t], tlen ? tlen[t] : 0, g, rg, centers);
+            tnew[t] = single;
+            add = force_all || single == MIXED || single != tlab[t];
+        }
+        const unsigned am = __ballot_sync(0xffffffffu, add);
+        unsigned long long base = 0;
+        if (lane == 0 && am) base = atomicAdd(nwork, (unsigned long long)__popc(am));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (add) work[base + __popc(am & ((1u << lane) - 1u))] = (uint32_t)t;
+    }
+}
+
+// super-tile boxes and common lengths (32 tiles each)
+__global__ void k_super_boxes(const double4* __restrict__ tbox, const int32_t* __restrict__ tlen,
+                              int64_t ntiles, double4* __restrict__ sbox,
+                              int32_t* __restrict__ slenc) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nsuper = (ntiles + 31) / 32;
+    for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; s < nsuper;
+         s += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t t = s * 32 + lane;
+        double4 b = make_double4(INFINITY, -INFINITY, INFINITY, -INFINITY);
+        int lmin = 0x7FFFFFFF, lmax = -1;
+        if (t < ntiles) {
+            b = tbox[t];
+            const int l = tlen ? tlen[t] : 0;
+            lmin = l;
+            lmax = l;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            b.x = fmin(b.x, __shfl_xor_sync(0xffffffffu, b.x, o));
+            b.y = fmax(b.y, __shfl_xor_sync(0xffffffffu, b.y, o));
+            b.z = fmin(b.z, __shfl_xor_sync(0xffffffffu, b.z, o));
+            b.w = fmax(b.w, __shfl_xor_sync(0xffffffffu, b.w, o));
+        }
+        lmin = __reduce_min_sync(0xffffffffu, lmin);
+        lmax = __reduce_max_sync(0xffffffffu, lmax);
+        if (lane == 0) {
+            sbox[s] = b;
+            slenc[s] = (lmin == lmax && lmin > 0) ? lmin : 0;
+        }
     }
 }
 
 // One warp per listed tile: labels := the single center, or nearest_center
-// through the grid; exact integer deltas of the cluster sums.
+// through the grids; exact integer deltas of the cluster sums. The first
+// (full) assignment accumulates per block in shared memory; the incremental
+// ones move few points, so each (old, new) label group of a warp adds its
+// deltas straight to the global accumulators (native 64-bit atomics in L2).
+template <bool FULL>
 __global__ void __launch_bounds__(LL_TB) k_lloyd_work(
     const double2* __restrict__ spts, int64_t n, const double* __restrict__ centers, int k,
     CandGrid g, uint32_t* __restrict__ labs, const uint32_t* __restrict__ work,
     const unsigned long long* __restrict__ nwork, const uint32_t* __restrict__ tnew,
-    uint32_t* __restrict__ tlab, int full, int Ex, int Ey, ClusterAcc acc,
-    unsigned long long* __restrict__ changed, const int* __restrict__ skip_flag) {
+    uint32_t* __restrict__ tlab, int Ex, int Ey, ClusterAcc acc,
+    unsigned long long* __restrict__ changed, const int* __restrict__ skip_flag, RowGrid rg,
+    const int32_t* __restrict__ slen) {
     extern __shared__ unsigned char smem[];
     if (skip_flag && (skip_flag[0] | skip_flag[1])) return;
     double* cx = reinterpret_cast<double*>(smem);
     double* cy = cx + k;
-    unsigned long long* s_sx = reinterpret_cast<unsigned long long*>(cy + k);
+    unsigned long long* s_sx = reinterpret_cast<unsigned long long*>(cy + k);  // FULL only
     unsigned long long* s_sy = s_sx + 2 * k;
     unsigned long long* s_cnt = s_sy + 2 * k;
     __shared__ unsigned long long s_changed;
     for (int c = threadIdx.x; c < k; c += blockDim.x) {
         cx[c] = centers[2 * c];
         cy[c] = centers[2 * c + 1];
-        s_sx[2 * c] = s_sx[2 * c + 1] = 0;
-        s_sy[2 * c] = s_sy[2 * c + 1] = 0;
-        s_cnt[c] = 0;
+        if (FULL) {
+            s_sx[2 * c] = s_sx[2 * c + 1] = 0;
+            s_sy[2 * c] = s_sy[2 * c + 1] = 0;
+            s_cnt[c] = 0;
+        }
     }
     if (threadIdx.x == 0) s_changed = 0;
     __syncthreads();
@@ -847,13 +993,14 @@ __global__ void __launch_bounds__(LL_TB) k_lloyd_work(
     unsigned long long my_changed = 0;
     for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nw;
          w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+      {
         const uint32_t t = work[w];
         const uint32_t single = tnew[t];
         uint32_t old[TILE / 32];
 #pragma unroll
         for (int i = 0; i < TILE / 32; ++i) {
             const int64_t r = (int64_t)t * TILE + i * 32 + lane;
-            old[i] = (r < n && !full) ? labs[r] : 0u;
+            old[i] = (r < n && !FULL) ? labs[r] : 0u;
         }
 #pragma unroll
         for (int i = 0; i < TILE / 32; ++i) {
@@ -864,65 +1011,93 @@ __global__ void __launch_bounds__(LL_TB) k_lloyd_work(
             bool need_p = valid;
             if (valid && single != MIXED) {
                 best = single;
-                need_p = full || old[i] != best;  // unchanged: point not needed
+                need_p = FULL || old[i] != best;  // unchanged: point not needed
             }
             if (need_p) p = spts[r];
-            if (valid && single == MIXED) best = grid_nearest(g, p.x, p.y, cx, cy, k);
-            const bool moved = valid && (full || old[i] != best);
+            if (valid && single == MIXED)
+                best = slen ? row_nearest(rg, g, slen[r], p.x, p.y, cx, cy, k)
+                            : grid_nearest(g, p.x, p.y, cx, cy, k);
+            const bool moved = valid && (FULL || old[i] != best);
             if (moved) labs[r] = best;
-            if (!full && moved) ++my_changed;
+            if (!FULL && moved) ++my_changed;
             // group lanes by (old, new) label pair; one set of atomics per group
-            const uint32_t key = full ? best : ((old[i] << 16) | best);
+            const uint32_t key = FULL ? best : ((old[i] << 16) | best);
             const i128 fx = moved ? fx_from_double(p.x, Ex) : (i128)0;
             const i128 fy = moved ? fx_from_double(p.y, Ey) : (i128)0;
             warp_aggregate(moved, key, (u128)fx, (u128)fy, 0ULL, agg,
                            [&](uint32_t kk, u128 sa, u128 sb, unsigned long long, int cnt) {
-                               const uint32_t nb = full ? kk : (kk & 0xFFFFu);
-                               fx_atomic_add(s_sx + 2 * nb, (i128)sa);
-                               fx_atomic_add(s_sy + 2 * nb, (i128)sb);
-                               atomicAdd(s_cnt + nb, (unsigned long long)cnt);
-                               if (!full) {
-                                   const uint32_t ob = kk >> 16;
-                                   fx_atomic_add(s_sx + 2 * ob, -(i128)sa);
-                                   fx_atomic_add(s_sy + 2 * ob, -(i128)sb);
-                                   atomicAdd(s_cnt + ob, (unsigned long long)(-(long long)cnt));
+                               if (FULL) {
+                                   fx_atomic_add(s_sx + 2 * kk, (i128)sa);
+                                   fx_atomic_add(s_sy + 2 * kk, (i128)sb);
+                                   atomicAdd(s_cnt + kk, (unsigned long long)cnt);
+                               } else {
+                                   const uint32_t nb = kk & 0xFFFFu, ob = kk >> 16;
+                                   l3_add(acc.sx + 3 * nb, (i128)sa);
+                                   l3_add(acc.sy + 3 * nb, (i128)sb);
+                                   atomicAdd(acc.cnt + nb, (unsigned long long)cnt);
+                                   l3_add(acc.sx + 3 * ob, -(i128)sa);
+                                   l3_add(acc.sy + 3 * ob, -(i128)sb);
+                                   atomicAdd(acc.cnt + ob, (unsigned long long)(-(long long)cnt));
                                }
                            });
         }
         if (lane == 0) tlab[t] = single;
+      }
     }
     for (int o = 16; o > 0; o >>= 1) my_changed += __shfl_down_sync(0xffffffffu, my_changed, o);
     if (lane == 0 && my_changed) atomicAdd(&s_changed, my_changed);
     __syncthreads();
-    for (int c = threadIdx.x; c < k; c += blockDim.x) {
-        const i128 vx = fx_load(s_sx + 2 * c), vy = fx_load(s_sy + 2 * c);
-        if (vx) fx_atomic_add(acc.sx + 2 * c, vx);
-        if (vy) fx_atomic_add(acc.sy + 2 * c, vy);
-        if (s_cnt[c]) atomicAdd(acc.cnt + c, s_cnt[c]);
+    if (FULL) {
+        for (int c = threadIdx.x; c < k; c += blockDim.x) {
+            const i128 vx = fx_load(s_sx + 2 * c), vy = fx_load(s_sy + 2 * c);
+            if (vx) l3_add(acc.sx + 3 * c, vx);
+            if (vy) l3_add(acc.sy + 3 * c, vy);
+            if (s_cnt[c]) atomicAdd(acc.cnt + c, s_cnt[c]);
+        }
     }
     if (threadIdx.x == 0 && s_changed) atomicAdd(changed, s_changed);
 }
 
 // centers[c] = sums[c] / counts[c] for non-empty clusters (update_means
 // :177-180); reports the empty clusters in index order.
-__global__ void k_means(ClusterAcc acc, int k, int Ex, int Ey, double* __restrict__ centers,
-                        int* __restrict__ empties, int* __restrict__ n_empty,
-                        const int* __restrict__ gate) {
-    if (gate && (gate[0] | gate[1])) return;
-    for (int c = threadIdx.x; c < k; c += blockDim.x) {
-        const long long cnt = (long long)acc.cnt[c];
-        if (cnt > 0) {
-            centers[2 * c] = fx_to_double(fx_load(acc.sx + 2 * c), Ex) / (double)cnt;
-            centers[2 * c + 1] = fx_to_double(fx_load(acc.sy + 2 * c), Ey) / (double)cnt;
-        }
-    }
+__global__ void __launch_bounds__(256) k_means(ClusterAcc acc, int k, int Ex, int Ey,
+                                               double* __restrict__ centers,
+                                               int* __restrict__ empties, int* __restrict__ n_empty,
+                                               const int* __restrict__ gate) {
+    if (gate && (gate[0] | gate[1])) return;  // uniform over the block
+    __shared__ int wc[32];
+    __shared__ int base;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) base = 0;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        int ne = 0;
-        for (int c = 0; c < k; ++c)
-            if ((long long)acc.cnt[c] <= 0) empties[ne++] = c;
-        *n_empty = ne;
+    for (int c0 = 0; c0 < k; c0 += blockDim.x) {
+        const int c = c0 + threadIdx.x;
+        bool empty = false;
+        if (c < k) {
+            const long long cnt = (long long)acc.cnt[c];
+            const i128 sx = l3_load(acc.sx + 3 * c), sy = l3_load(acc.sy + 3 * c);
+            l3_store(acc.sx + 3 * c, sx);  // renormalise the limbs once per iteration
+            l3_store(acc.sy + 3 * c, sy);
+            if (cnt > 0) {
+                centers[2 * c] = fx_to_double(sx, Ex) / (double)cnt;
+                centers[2 * c + 1] = fx_to_double(sy, Ey) / (double)cnt;
+            } else {
+                empty = true;
+            }
+        }
+        // empty clusters listed in index order (block-wide ballot compaction)
+        const unsigned m = __ballot_sync(0xffffffffu, empty);
+        if (lane == 0) wc[warp] = __popc(m);
+        __syncthreads();
+        int off = base;
+        for (int w = 0; w < warp; ++w) off += wc[w];
+        if (empty) empties[off + __popc(m & ((1u << lane) - 1u))] = c;
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) base += wc[w];
+        __syncthreads();
     }
+    if (threadIdx.x == 0) *n_empty = base;
 }
 
 // farthest point among clusters with count > 1 (update_means :183-192):
@@ -983,7 +1158,7 @@ __global__ void k_far_block(const double2* __restrict__ spts, const uint32_t* __
 __global__ void k_repair(const double2* __restrict__ spts, const uint32_t* __restrict__ pos,
                          uint32_t* __restrict__ labs, double* __restrict__ centers, ClusterAcc acc,
                          int Ex, int Ey, const unsigned long long* __restrict__ blk, int nblk,
-                         int c, uint32_t* __restrict__ tlab) {
+                         int c, uint32_t* __restrict__ tlab, int64_t ntiles) {
     double bd = -1.0;
     int64_t bi = INT64_MAX, br = -1;
     for (int b = 0; b < nblk; ++b) {
@@ -999,15 +1174,14 @@ __global__ void k_repair(const double2* __restrict__ spts, const uint32_t* __res
     const uint32_t donor = labs[br];
     const double2 p = spts[br];
     const i128 fx = fx_from_double(p.x, Ex), fy = fx_from_double(p.y, Ey);
-    fx_atomic_add(acc.sx + 2 * donor, -fx);
-    fx_atomic_add(acc.sy + 2 * donor, -fy);
+    l3_store(acc.sx + 3 * donor, l3_load(acc.sx + 3 * donor) - fx);
+    l3_store(acc.sy + 3 * donor, l3_load(acc.sy + 3 * donor) - fy);
     acc.cnt[donor] -= 1;
     labs[br] = (uint32_t)c;
     tlab[br / TILE] = MIXED;  // the tile no longer holds one label
-    acc.sx[2 * c] = acc.sx[2 * c + 1] = 0;
-    acc.sy[2 * c] = acc.sy[2 * c + 1] = 0;
-    fx_atomic_add(acc.sx + 2 * c, fx);
-    fx_atomic_add(acc.sy + 2 * c, fy);
+    tlab[ntiles + br / (TILE * 32)] = MIXED;  // nor its super-tile
+    l3_store(acc.sx + 3 * c, fx);
+    l3_store(acc.sy + 3 * c, fy);
     acc.cnt[c] = 1;
     centers[2 * c] = p.x;
     centers[2 * c + 1] = p.y;
@@ -1053,15 +1227,29 @@ struct LloydCtx {
     DArr<uint16_t> cg_cnt, cg_cand;
     const double4* tbox = nullptr;
     int64_t ntiles = 0;
-    DArr<uint32_t> tlab, tnew, work;
+    DArr<uint32_t> tlab, tnew, work;  // tile | super-tile states, new tile states, listed tiles
+    DArr<uint32_t> swork;             // listed super-tiles
+    DArr<unsigned long long> nswork;
     DArr<unsigned long long> nwork, diag;
+    RowGrid rg{};                   // rg.R == 0: no row grid
+    DArr<uint64_t> rg_cell;
+    DArr<int> rg_blocks;            // row-grid segments holding points
+    int rg_nblocks = 0;
+    const int32_t* slen = nullptr;  // piece length per sorted point
+    const int32_t* tlen = nullptr;  // common piece length per tile (0: mixed)
+    DArr<double4> sbox;             // super-tile boxes (32 tiles)
+    DArr<int32_t> slenc;            // super-tile common piece length (0: mixed)
+    int64_t nsuper() const { return (ntiles + 31) / 32; }
+    int64_t nstate() const { return std::max<int64_t>(ntiles, 1) + nsuper(); }  // tlab | stlab
     DArr<unsigned long long> dacc;  // distributed fit: this rank's deltas (5k)
     bool use_dacc = false;
-    ClusterAcc cacc() { return ClusterAcc{acc.p, acc.p + 2 * k, acc.p + 4 * k}; }
+    ClusterAcc cacc() { return ClusterAcc{acc.p, acc.p + 3 * k, acc.p + 6 * k}; }
     ClusterAcc tacc() {  // where the assignment writes
-        return use_dacc ? ClusterAcc{dacc.p, dacc.p + 2 * k, dacc.p + 4 * k} : cacc();
+        return use_dacc ? ClusterAcc{dacc.p, dacc.p + 3 * k, dacc.p + 6 * k} : cacc();
     }
-    size_t smem() const { return sizeof(double) * 2 * k + sizeof(unsigned long long) * 5 * k; }
+    size_t smem(bool full) const {
+        return sizeof(double) * 2 * k + (full ? sizeof(unsigned long long) * 5 * k : 0);
+    }
     int grid() const {
         return (int)std::max<int64_t>(1, std::min<int64_t>((n + LL_TB - 1) / LL_TB,
                                                            (int64_t)kSMs * 6));
@@ -1073,14 +1261,17 @@ struct LloydCtx {
 // the other kernels, so iterations launched past convergence are no-ops.
 __global__ void k_iter_end(int* __restrict__ state, unsigned long long* __restrict__ changed,
                            unsigned long long* __restrict__ nwork,
+                           unsigned long long* __restrict__ nswork,
                            unsigned long long* __restrict__ diag) {
     if (state[0] | state[1]) return;  // pending repair / converged
     state[2] += 1;
-    diag[0] += *nwork;  // diagnostics: tiles processed / labels changed
+    diag[0] += *nwork;  // diagnostics: tiles / super-tiles listed, labels changed
+    diag[2] += *nswork;
     diag[1] += *changed;
     if (*changed == 0) state[1] = 1;
     *changed = 0;
     *nwork = 0;
+    *nswork = 0;
 }
 
 void lloyd_assign(LloydCtx& L, bool full, bool gate_on_empties) {
@@ -1088,28 +1279,38 @@ void lloyd_assign(LloydCtx& L, bool full, bool gate_on_empties) {
     if (L.n == 0) return;  // a rank may hold no sample points
     {
         JB_PROF("lloyd_grid", L.st);
-        const int ncell = L.cg.G * L.cg.G;
-        k_grid_build<<<std::min(ncell / 8, kSMs * 16), 256, 0, L.st>>>(L.cg, L.centers.p, L.k);
+        if (L.cg.G > 0) launch_grid_build(L.cg, L.centers.p, L.k, L.st);
+        if (L.rg.R > 0)
+            launch_row_grid_build(L.rg, L.centers.p, L.k, L.st, L.rg_blocks.p, L.rg_nblocks);
     }
     JB_LAUNCH_CHECK();
     {
         JB_PROF("lloyd_tile_check", L.st);
-        k_tile_check<<<(int)std::max<int64_t>(1, std::min<int64_t>((L.ntiles + 255) / 256,
-                                                                  kSMs * 16)),
-                       256, 0, L.st>>>(L.tbox, L.ntiles, L.cg, L.centers.p, L.tlab.p, L.tnew.p,
-                                       L.work.p, L.nwork.p, gate, full ? 1 : 0);
+        k_super_check<<<(int)std::max<int64_t>(1, std::min<int64_t>((L.nsuper() + 255) / 256,
+                                                                   kSMs * 16)),
+                        256, 0, L.st>>>(L.sbox.p, L.rg.R > 0 ? L.slenc.p : nullptr, L.ntiles, L.cg,
+                                        L.centers.p, L.tlab.p, L.swork.p, L.nswork.p, gate,
+                                        full ? 1 : 0, L.rg);
+        k_tile_expand<<<full ? (int)std::max<int64_t>(1, std::min<int64_t>((L.nsuper() + 7) / 8,
+                                                                            kSMs * 16))
+                             : kSMs * 4,
+                        256, 0, L.st>>>(L.swork.p, L.nswork.p, L.tbox,
+                                        L.rg.R > 0 ? L.tlen : nullptr, L.ntiles, L.cg, L.centers.p,
+                                        L.tlab.p, L.tnew.p, L.work.p, L.nwork.p, gate,
+                                        full ? 1 : 0, L.rg);
     }
     JB_LAUNCH_CHECK();
     JB_PROF("lloyd_assign", L.st);
-    k_lloyd_work<<<L.grid(), LL_TB, L.smem(), L.st>>>(
+    auto kern = full ? k_lloyd_work<true> : k_lloyd_work<false>;
+    kern<<<L.grid(), LL_TB, L.smem(full), L.st>>>(
         L.spts, L.n, L.centers.p, L.k, L.cg, L.labs.p, L.work.p, L.nwork.p, L.tnew.p, L.tlab.p,
-        full ? 1 : 0, L.Ex, L.Ey, L.tacc(), L.flags.p, gate);
+        L.Ex, L.Ey, L.tacc(), L.flags.p, gate, L.rg, L.rg.R > 0 ? L.slen : nullptr);
     JB_LAUNCH_CHECK();
 }
 
 void lloyd_means(LloydCtx& L, bool gated) {
     JB_PROF("lloyd_means", L.st);
-    k_means<<<1, 1024, 0, L.st>>>(L.cacc(), L.k, L.Ex, L.Ey, L.centers.p, L.empties.p,
+    k_means<<<1, 256, 0, L.st>>>(L.cacc(), L.k, L.Ex, L.Ey, L.centers.p, L.empties.p,
                                   L.empties.p + L.k, gated ? L.empties.p + L.k : nullptr);
     JB_LAUNCH_CHECK();
 }
@@ -1138,7 +1339,7 @@ void lloyd_repair(LloydCtx& L, int ne) {
                                             L.cacc().cnt, L.far_blk.p);
         JB_LAUNCH_CHECK();
         k_repair<<<1, 1, 0, L.st>>>(L.spts, L.pos, L.labs.p, L.centers.p, L.cacc(), L.Ex, L.Ey,
-                                    L.far_blk.p, nblk, c, L.tlab.p);
+                                    L.far_blk.p, nblk, c, L.tlab.p, L.ntiles);
         JB_LAUNCH_CHECK();
     }
     const int zero = 0;
@@ -1159,7 +1360,7 @@ void lloyd_update_means_sync(LloydCtx& L) {
 void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, uint64_t k,
                        uint64_t max_iters, uint64_t n_init, const uint64_t* d_raw,
                        uint64_t raw_count, uint64_t* cursor, const BBox& bb, KMeansOut& out,
-                       cudaStream_t st) {
+                       cudaStream_t st, const PieceRows& rows) {
     if (k < 1) throw Error(INVALID_INPUT, "d2_seed: k must be >= 1");
     if ((int64_t)k > n) throw Error(INVALID_INPUT, "d2_seed: k exceeds points");
     if (k > 2048) throw Error(INVALID_INPUT, "k > 2048 is not supported by the Lloyd kernel");
@@ -1174,6 +1375,7 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
     // ---- Morton order of the points ----
     DArr<double2> spts(n, st);
     DArr<uint32_t> orig(n, st), pos(n, st);
+    DArr<int32_t> slen(rows.len ? n : 0, st), tlen((n + TILE - 1) / TILE, st);
     {
         DArr<uint32_t> keys(n, st), skeys(n, st), vals(n, st);
         const double sx = wx > 0 ? 65535.0 / wx : 0.0, sy = wy > 0 ? 65535.0 / wy : 0.0;
@@ -1186,7 +1388,8 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
         DArr<uint8_t> tmp(tb, st);
         cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.p, skeys.p, vals.p, orig.p, n, 0, 32, st);
         JB_LAUNCH_CHECK();
-        k_sorted_gather<<<grid_cap(n), 256, 0, st>>>(pts, d_idx, orig.p, n, spts.p, pos.p);
+        k_sorted_gather<<<grid_cap(n), 256, 0, st>>>(pts, d_idx, orig.p, n, spts.p, pos.p,
+                                                     rows.len, slen.p);
         JB_LAUNCH_CHECK();
     }
     JB_TRACE("kmeans: morton order", st);
@@ -1194,7 +1397,8 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
     DArr<double4> tbox(ntiles, st);
     DArr<double> tmax(ntiles, st);
     const int tile_grid = (int)std::max<int64_t>(1, std::min<int64_t>((ntiles + 7) / 8, kSMs * 8));
-    k_tile_boxes<<<tile_grid, 256, 0, st>>>(spts.p, n, tbox.p);
+    k_tile_boxes<<<tile_grid, 256, 0, st>>>(spts.p, n, tbox.p, rows.len ? slen.p : nullptr,
+                                            tlen.p);
     JB_LAUNCH_CHECK();
 
     LloydCtx L;
@@ -1208,10 +1412,10 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
     L.st = st;
     L.centers.alloc(2 * k, st);
     L.labs.alloc(n, st);
-    L.acc.alloc(5 * k, st);
+    L.acc.alloc(7 * k, st);
     L.flags.alloc(1, st);
     L.empties.alloc(k + 3, st);  // list | n_empty | converged | iterations
-    L.diag.alloc(2, st);
+    L.diag.alloc(4, st);
     L.empties.zero();
     {
         const int G = grid_side_for(k), cap = 32;
@@ -1221,15 +1425,51 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
         L.cg.cnt = L.cg_cnt.p;
         L.cg.cand = L.cg_cand.p;
     }
+    if (rows.len) {  // exact row grid over the integer piece lengths (jb_rowgrid.cuh)
+        L.rg = make_row_grid_desc(bb.ymin, bb.ymax, rows.scl, rows.sl, rows.max_len, 1 << 16);
+        L.rg_cell.alloc((size_t)L.rg.R * L.rg.Gy, st);
+        L.rg.cell = L.rg_cell.p;
+        L.slen = slen.p;
+        L.tlen = tlen.p;
+        // only segments holding points are rebuilt each iteration; the others
+        // stay "not built" (all ones) and send their queries to the fallback
+        JB_CUDA(cudaMemsetAsync(L.rg_cell.p, 0xFF, sizeof(uint64_t) * L.rg.R * L.rg.Gy, st));
+        const int nseg_all = row_grid_segments(L.rg);
+        DArr<int> occ(nseg_all, st);
+        occ.zero();
+        if (n > 0)
+            k_row_occupancy<<<grid_cap(n), 256, 0, st>>>(L.rg, spts.p, slen.p, n, occ.p);
+        JB_LAUNCH_CHECK();
+        std::vector<int> h_occ = occ.to_host(nseg_all), blocks;
+        for (int b = 0; b < nseg_all; ++b)
+            if (h_occ[b]) blocks.push_back(b);
+        L.rg_nblocks = (int)blocks.size();
+        L.rg_blocks.alloc(std::max<size_t>(blocks.size(), 1), st);
+        L.rg_blocks.upload(blocks.data(), blocks.size());
+        // the 2-D grid would only serve mixed-length tiles (-> per point) and
+        // lengths beyond the rows / overflowing row cells (-> all centers)
+        L.cg.G = 0;
+    }
     L.tbox = tbox.p;
     L.ntiles = ntiles;
-    L.tlab.alloc(ntiles, st);
-    L.tnew.alloc(ntiles, st);
-    L.work.alloc(ntiles, st);
+    L.tlab.alloc(L.nstate(), st);
+    L.sbox.alloc(std::max<int64_t>(L.nsuper(), 1), st);
+    L.slenc.alloc(std::max<int64_t>(L.nsuper(), 1), st);
+    if (ntiles > 0)
+        k_super_boxes<<<(int)std::max<int64_t>(1, std::min<int64_t>((L.nsuper() + 7) / 8, kSMs * 8)),
+                        256, 0, st>>>(tbox.p, rows.len ? tlen.p : nullptr, ntiles, L.sbox.p,
+                                      L.slenc.p);
+    L.work.alloc(std::max<int64_t>(ntiles, 1), st);
+    L.tnew.alloc(std::max<int64_t>(ntiles, 1), st);
+    L.swork.alloc(std::max<int64_t>(L.nsuper(), 1), st);
+    L.nswork.alloc(1, st);
+    L.nswork.zero();
     L.nwork.alloc(1, st);
-    JB_CUDA(cudaMemsetAsync(L.tlab.p, 0xFF, sizeof(uint32_t) * ntiles, st));
-    JB_CUDA(cudaFuncSetAttribute(k_lloyd_work, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)L.smem()));
+    JB_CUDA(cudaMemsetAsync(L.tlab.p, 0xFF, sizeof(uint32_t) * L.nstate(), st));
+    JB_CUDA(cudaFuncSetAttribute(k_lloyd_work<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)L.smem(true)));
+    JB_CUDA(cudaFuncSetAttribute(k_lloyd_work<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)L.smem(false)));
 
     const int nblocks = (int)((n + D2_R - 1) / D2_R);
     DArr<uint32_t> d2_work(ntiles, st);
@@ -1296,14 +1536,16 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
         // syncs once per batch. Iterations launched after convergence are
         // no-ops; the count is taken on the device.
         L.acc.zero();
-        JB_CUDA(cudaMemsetAsync(L.tlab.p, 0xFF, sizeof(uint32_t) * ntiles, st));
+        JB_CUDA(cudaMemsetAsync(L.tlab.p, 0xFF, sizeof(uint32_t) * L.nstate(), st));
         JB_CUDA(cudaMemsetAsync(L.empties.p + L.k, 0, 3 * sizeof(int), st));
         L.diag.zero();
         JB_CUDA(cudaMemsetAsync(L.flags.p, 0, 8, st));
         JB_CUDA(cudaMemsetAsync(L.nwork.p, 0, 8, st));
+        JB_CUDA(cudaMemsetAsync(L.nswork.p, 0, 8, st));
         lloyd_assign(L, true, false);  // assign_all(points, seeds) (:204)
         JB_CUDA(cudaMemsetAsync(L.flags.p, 0, 8, st));
         JB_CUDA(cudaMemsetAsync(L.nwork.p, 0, 8, st));
+        JB_CUDA(cudaMemsetAsync(L.nswork.p, 0, 8, st));
         uint64_t it = 0;
         const uint64_t kBatch = dbg_on() ? 1 : 16;
         while (it < max_iters) {
@@ -1311,23 +1553,25 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
             for (uint64_t b = 0; b < B; ++b) {
                 lloyd_means(L, true);          // update_means ...
                 lloyd_assign(L, false, true);  // ... assign_all, label comparison
-                k_iter_end<<<1, 1, 0, st>>>(L.empties.p + L.k, L.flags.p, L.nwork.p, L.diag.p);
+                k_iter_end<<<1, 1, 0, st>>>(L.empties.p + L.k, L.flags.p, L.nwork.p, L.nswork.p,
+                                            L.diag.p);
                 JB_LAUNCH_CHECK();
             }
             LoopState h = lloyd_state(L);
             it = (uint64_t)h.iters;
             if (dbg_on()) {
                 auto cc = L.centers.to_host(2 * k);
-                auto dg = L.diag.to_host(2);
-                fprintf(stderr, "[jb] iter %d: empty=%d conv=%d cum_changed=%llu centers=%016llx\n",
-                        h.iters, h.n_empty, h.converged, dg[1],
+                auto dg = L.diag.to_host(4);
+                fprintf(stderr, "[jb] iter %d: empty=%d conv=%d cum_changed=%llu cum_tiles=%llu cum_need_supers=%llu centers=%016llx\n",
+                        h.iters, h.n_empty, h.converged, dg[1], dg[0], dg[2],
                         (unsigned long long)dbg_hash(cc.data(), 16 * k));
             }
             if (h.converged) break;
             if (h.n_empty) {  // empty clusters: re-seed on the host path, finish the iteration
                 lloyd_repair(L, h.n_empty);
                 lloyd_assign(L, false, true);
-                k_iter_end<<<1, 1, 0, st>>>(L.empties.p + L.k, L.flags.p, L.nwork.p, L.diag.p);
+                k_iter_end<<<1, 1, 0, st>>>(L.empties.p + L.k, L.flags.p, L.nwork.p, L.nswork.p,
+                                            L.diag.p);
                 JB_LAUNCH_CHECK();
                 h = lloyd_state(L);
                 it = (uint64_t)h.iters;
@@ -1432,36 +1676,32 @@ __global__ void k_last_positive(const uint32_t* __restrict__ gpos, const uint32_
     if ((threadIdx.x & 31) == 0) atomicMax(out, best);
 }
 
-// acc += delta (sx, sy as int128; counts as two's complement u64)
+// acc += delta, word by word (l3 limbs and two's complement counts are additive)
 __global__ void k_add_acc(unsigned long long* __restrict__ acc,
                           const unsigned long long* __restrict__ delta, int k) {
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < 2 * k; c += gridDim.x * blockDim.x) {
-        fx_atomic_add(acc + 2 * c, fx_load(delta + 2 * c));  // sx[k], sy[k] interleaved pairs
-    }
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < k; c += gridDim.x * blockDim.x)
-        acc[4 * k + c] += delta[4 * k + c];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 7 * k; i += gridDim.x * blockDim.x)
+        acc[i] += delta[i];
 }
 
 // re-seed empty cluster c at the globally chosen far point (update_means :193-196)
 __global__ void k_repair_dist(unsigned long long* __restrict__ acc, double* __restrict__ centers,
                               uint32_t* __restrict__ labs, uint32_t* __restrict__ tlab, int k,
                               int Ex, int Ey, int c, int donor, double px, double py,
-                              long long owner_r) {
+                              long long owner_r, int64_t ntiles) {
     const i128 fx = fx_from_double(px, Ex), fy = fx_from_double(py, Ey);
-    ClusterAcc a{acc, acc + 2 * k, acc + 4 * k};
-    fx_atomic_add(a.sx + 2 * donor, -fx);
-    fx_atomic_add(a.sy + 2 * donor, -fy);
+    ClusterAcc a{acc, acc + 3 * k, acc + 6 * k};
+    l3_store(a.sx + 3 * donor, l3_load(a.sx + 3 * donor) - fx);
+    l3_store(a.sy + 3 * donor, l3_load(a.sy + 3 * donor) - fy);
     a.cnt[donor] -= 1;
-    a.sx[2 * c] = a.sx[2 * c + 1] = 0;
-    a.sy[2 * c] = a.sy[2 * c + 1] = 0;
-    fx_atomic_add(a.sx + 2 * c, fx);
-    fx_atomic_add(a.sy + 2 * c, fy);
+    l3_store(a.sx + 3 * c, fx);
+    l3_store(a.sy + 3 * c, fy);
     a.cnt[c] = 1;
     centers[2 * c] = px;
     centers[2 * c + 1] = py;
     if (owner_r >= 0) {
         labs[owner_r] = (uint32_t)c;
         tlab[owner_r / TILE] = MIXED;
+        tlab[ntiles + owner_r / (TILE * 32)] = MIXED;
     }
 }
 
@@ -1478,7 +1718,7 @@ struct FarRec {
 void lloyd_best_dist(const Comm& cm, const double* d_pts, const uint64_t* d_lidx,
                      const uint32_t* d_gpos, int64_t n, uint64_t S, uint64_t k, uint64_t max_iters,
                      uint64_t n_init, const uint64_t* d_raw, uint64_t raw_count, uint64_t* cursor,
-                     const BBox& bb, KMeansOut& out, cudaStream_t st) {
+                     const BBox& bb, KMeansOut& out, cudaStream_t st, const PieceRows& rows) {
     if (k < 1) throw Error(INVALID_INPUT, "d2_seed: k must be >= 1");
     if (k > S) throw Error(INVALID_INPUT, "d2_seed: k exceeds points");
     if (k > 2048) throw Error(INVALID_INPUT, "k > 2048 is not supported by the Lloyd kernel");
@@ -1494,6 +1734,7 @@ void lloyd_best_dist(const Comm& cm, const double* d_pts, const uint64_t* d_lidx
     // ---- Morton order of this rank's points ----
     DArr<double2> spts(nn, st);
     DArr<uint32_t> orig(nn, st), pos(nn, st), gkey(nn, st);
+    DArr<int32_t> slen(rows.len ? nn : 0, st), tlen(std::max<int64_t>((n + TILE - 1) / TILE, 1), st);
     if (n > 0) {
         DArr<uint32_t> keys(n, st), skeys(n, st), vals(n, st);
         const double sx = wx > 0 ? 65535.0 / wx : 0.0, sy = wy > 0 ? 65535.0 / wy : 0.0;
@@ -1505,7 +1746,8 @@ void lloyd_best_dist(const Comm& cm, const double* d_pts, const uint64_t* d_lidx
                                         st);
         DArr<uint8_t> tmp(tb, st);
         cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.p, skeys.p, vals.p, orig.p, n, 0, 32, st);
-        k_sorted_gather<<<grid_cap(n), 256, 0, st>>>(pts, d_lidx, orig.p, n, spts.p, pos.p);
+        k_sorted_gather<<<grid_cap(n), 256, 0, st>>>(pts, d_lidx, orig.p, n, spts.p, pos.p,
+                                                     rows.len, slen.p);
         k_gkey<<<grid_cap(n), 256, 0, st>>>(d_gpos, orig.p, n, gkey.p);
         JB_LAUNCH_CHECK();
     }
@@ -1513,7 +1755,9 @@ void lloyd_best_dist(const Comm& cm, const double* d_pts, const uint64_t* d_lidx
     DArr<double4> tbox(std::max<int64_t>(ntiles, 1), st);
     DArr<double> tmax(std::max<int64_t>(ntiles, 1), st);
     const int tile_grid = (int)std::max<int64_t>(1, std::min<int64_t>((ntiles + 7) / 8, kSMs * 8));
-    if (n > 0) k_tile_boxes<<<tile_grid, 256, 0, st>>>(spts.p, n, tbox.p);
+    if (n > 0)
+        k_tile_boxes<<<tile_grid, 256, 0, st>>>(spts.p, n, tbox.p, rows.len ? slen.p : nullptr,
+                                                tlen.p);
     JB_LAUNCH_CHECK();
 
     LloydCtx L;
@@ -1527,13 +1771,13 @@ void lloyd_best_dist(const Comm& cm, const double* d_pts, const uint64_t* d_lidx
     L.st = st;
     L.centers.alloc(2 * k, st);
     L.labs.alloc(nn, st);
-    L.acc.alloc(5 * k, st);
-    L.dacc.alloc(5 * k, st);
+    L.acc.alloc(7 * k, st);
+    L.dacc.alloc(7 * k, st);
     L.use_dacc = true;
     L.flags.alloc(1, st);
     L.empties.alloc(k + 3, st);
     L.empties.zero();
-    L.diag.alloc(2, st);
+    L.diag.alloc(4, st);
     {
         const int G = grid_side_for(k), cap = 32;
         L.cg = make_grid_desc(bb.xmin, bb.xmax, bb.ymin, bb.ymax, G, cap);
@@ -1542,14 +1786,50 @@ void lloyd_best_dist(const Comm& cm, const double* d_pts, const uint64_t* d_lidx
         L.cg.cnt = L.cg_cnt.p;
         L.cg.cand = L.cg_cand.p;
     }
+    if (rows.len) {  // exact row grid over the integer piece lengths (jb_rowgrid.cuh)
+        L.rg = make_row_grid_desc(bb.ymin, bb.ymax, rows.scl, rows.sl, rows.max_len, 1 << 16);
+        L.rg_cell.alloc((size_t)L.rg.R * L.rg.Gy, st);
+        L.rg.cell = L.rg_cell.p;
+        L.slen = slen.p;
+        L.tlen = tlen.p;
+        // only segments holding points are rebuilt each iteration; the others
+        // stay "not built" (all ones) and send their queries to the fallback
+        JB_CUDA(cudaMemsetAsync(L.rg_cell.p, 0xFF, sizeof(uint64_t) * L.rg.R * L.rg.Gy, st));
+        const int nseg_all = row_grid_segments(L.rg);
+        DArr<int> occ(nseg_all, st);
+        occ.zero();
+        if (n > 0)
+            k_row_occupancy<<<grid_cap(n), 256, 0, st>>>(L.rg, spts.p, slen.p, n, occ.p);
+        JB_LAUNCH_CHECK();
+        std::vector<int> h_occ = occ.to_host(nseg_all), blocks;
+        for (int b = 0; b < nseg_all; ++b)
+            if (h_occ[b]) blocks.push_back(b);
+        L.rg_nblocks = (int)blocks.size();
+        L.rg_blocks.alloc(std::max<size_t>(blocks.size(), 1), st);
+        L.rg_blocks.upload(blocks.data(), blocks.size());
+        // the 2-D grid would only serve mixed-length tiles (-> per point) and
+        // lengths beyond the rows / overflowing row cells (-> all centers)
+        L.cg.G = 0;
+    }
     L.tbox = tbox.p;
     L.ntiles = ntiles;
-    L.tlab.alloc(std::max<int64_t>(ntiles, 1), st);
-    L.tnew.alloc(std::max<int64_t>(ntiles, 1), st);
+    L.tlab.alloc(L.nstate(), st);
+    L.sbox.alloc(std::max<int64_t>(L.nsuper(), 1), st);
+    L.slenc.alloc(std::max<int64_t>(L.nsuper(), 1), st);
+    if (ntiles > 0)
+        k_super_boxes<<<(int)std::max<int64_t>(1, std::min<int64_t>((L.nsuper() + 7) / 8, kSMs * 8)),
+                        256, 0, st>>>(tbox.p, rows.len ? tlen.p : nullptr, ntiles, L.sbox.p,
+                                      L.slenc.p);
     L.work.alloc(std::max<int64_t>(ntiles, 1), st);
+    L.tnew.alloc(std::max<int64_t>(ntiles, 1), st);
+    L.swork.alloc(std::max<int64_t>(L.nsuper(), 1), st);
+    L.nswork.alloc(1, st);
+    L.nswork.zero();
     L.nwork.alloc(1, st);
-    JB_CUDA(cudaFuncSetAttribute(k_lloyd_work, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)L.smem()));
+    JB_CUDA(cudaFuncSetAttribute(k_lloyd_work<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)L.smem(true)));
+    JB_CUDA(cudaFuncSetAttribute(k_lloyd_work<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)L.smem(false)));
 
     const uint64_t nblocks = (S + D2_R - 1) / D2_R;
     DArr<uint32_t> d2_work(std::max<int64_t>(ntiles, 1), st);
@@ -1603,30 +1883,24 @@ void lloyd_best_dist(const Comm& cm, const double* d_pts, const uint64_t* d_lidx
     };
 
     auto exchange_deltas = [&]() -> unsigned long long {  // returns global changed count
-        std::vector<unsigned long long> h(5 * k + 1);
-        L.dacc.download(h.data(), 5 * k);
-        L.flags.download(h.data() + 5 * k, 1);
+        std::vector<unsigned long long> h(7 * k + 1);
+        L.dacc.download(h.data(), 7 * k);
+        L.flags.download(h.data() + 7 * k, 1);
         JB_CUDA(cudaStreamSynchronize(st));
         const auto all = cm.gather(h);
-        std::vector<unsigned long long> sum(5 * k + 1, 0);
-        for (int r = 0; r < cm.world; ++r) {
-            const unsigned long long* o = &all[(size_t)r * (5 * k + 1)];
-            for (uint64_t i = 0; i < 4 * k; i += 2) {
-                const u128 a = ((u128)sum[i + 1] << 64) | sum[i];
-                const u128 b = ((u128)o[i + 1] << 64) | o[i];
-                const u128 c2 = a + b;
-                sum[i] = (unsigned long long)c2;
-                sum[i + 1] = (unsigned long long)(c2 >> 64);
-            }
-            for (uint64_t i = 4 * k; i < 5 * k + 1; ++i) sum[i] += o[i];
+        std::vector<unsigned long long> sum(7 * k + 1, 0);
+        for (int r = 0; r < cm.world; ++r) {  // every word is additive
+            const unsigned long long* o = &all[(size_t)r * (7 * k + 1)];
+            for (uint64_t i = 0; i < 7 * k + 1; ++i) sum[i] += o[i];
         }
-        L.dacc.upload(sum.data(), 5 * k);
+        L.dacc.upload(sum.data(), 7 * k);
         k_add_acc<<<1, 256, 0, st>>>(L.acc.p, L.dacc.p, (int)k);
         JB_LAUNCH_CHECK();
         L.dacc.zero();
         JB_CUDA(cudaMemsetAsync(L.flags.p, 0, 8, st));
         JB_CUDA(cudaMemsetAsync(L.nwork.p, 0, 8, st));
-        return sum[5 * k];
+        JB_CUDA(cudaMemsetAsync(L.nswork.p, 0, 8, st));
+        return sum[7 * k];
     };
 
     auto repair_dist = [&]() {  // update_means :181-197 across ranks
@@ -1708,7 +1982,7 @@ void lloyd_best_dist(const Comm& cm, const double* d_pts, const uint64_t* d_lidx
             }
             k_repair_dist<<<1, 1, 0, st>>>(L.acc.p, L.centers.p, L.labs.p, L.tlab.p, (int)k, L.Ex,
                                            L.Ey, c, (int)best.donor, best.x, best.y,
-                                           owner == cm.rank ? best.r : -1);
+                                           owner == cm.rank ? best.r : -1, L.ntiles);
             JB_LAUNCH_CHECK();
         }
         const int zero = 0;
@@ -1828,10 +2102,11 @@ void lloyd_best_dist(const Comm& cm, const double* d_pts, const uint64_t* d_lidx
         L.acc.zero();
         L.dacc.zero();
         L.diag.zero();
-        JB_CUDA(cudaMemsetAsync(L.tlab.p, 0xFF, sizeof(uint32_t) * std::max<int64_t>(ntiles, 1), st));
+        JB_CUDA(cudaMemsetAsync(L.tlab.p, 0xFF, sizeof(uint32_t) * L.nstate(), st));
         JB_CUDA(cudaMemsetAsync(L.empties.p + L.k, 0, 3 * sizeof(int), st));
         JB_CUDA(cudaMemsetAsync(L.flags.p, 0, 8, st));
         JB_CUDA(cudaMemsetAsync(L.nwork.p, 0, 8, st));
+        JB_CUDA(cudaMemsetAsync(L.nswork.p, 0, 8, st));
         lloyd_assign(L, true, false);
         exchange_deltas();
         uint64_t it = 0;
