@@ -17,9 +17,14 @@
 
 namespace jb {
 
-// Greedy piece end from `start` (compression.hpp:38-61), bit-exact.
+// Greedy piece end from `start` (compression.hpp:38-61), bit-exact. The
+// test at d = 1 cannot break (cand > start + 1 fails), so its deviation is not
+// evaluated; for d = 2^m the two divisions are multiplications by the exact
+// power of two 2^-m (a product and a quotient of the same real value round
+// identically). `bad` collects non-finite candidates (compression.hpp:73-74).
 __device__ __forceinline__ int64_t piece_end(const double* __restrict__ v, int64_t start,
-                                             int64_t last, double tol2, int64_t max_len) {
+                                             int64_t last, double tol2, int64_t max_len,
+                                             bool* bad = nullptr) {
     const double base = v[start];
     double s2 = 0.0, s3 = 0.0;
     // sum_{i<=d} i^2 kept as a running integer-valued double: identical to the
@@ -30,15 +35,31 @@ __device__ __forceinline__ int64_t piece_end(const double* __restrict__ v, int64
     for (;;) {
         const int64_t cand = end + 1;
         if (cand > last) break;
-        const double y = v[cand] - base;
-        const double d = (double)(cand - start);
-        const double ns2 = s2 + y * y;
+        const double vc = v[cand];
+        if (bad && !isfinite(vc)) *bad = true;
+        const double y = vc - base;
+        const int64_t L = cand - start;
+        const double d = (double)L;
+        const double yy = y * y;
+        const double ns2 = s2 + yy;
         const double ns3 = s3 + d * y;
         sq += d * d;
-        const double sum_d2 =
-            cand - start <= 165000 ? sq : d * (d + 1.0) * (2.0 * d + 1.0) / 6.0;
-        const double sq_dev = y * y / (d * d) * sum_d2 - 2.0 * y / d * ns3 + ns2;
-        if (sq_dev > (d - 1.0) * tol2 && cand > start + 1) break;
+        if (L > 1) {
+            double sum_d2 = sq;
+            if (L > 165000) sum_d2 = d * (d + 1.0) * (2.0 * d + 1.0) / 6.0;
+            double a, b;  // inc * inc / (len * len), 2.0 * inc / len
+            if ((L & (L - 1)) == 0) {
+                const int m = __ffsll(L) - 1;
+                const double inv = __longlong_as_double((long long)(1023 - m) << 52);
+                a = yy * (inv * inv);
+                b = (2.0 * y) * inv;
+            } else {
+                a = yy / (d * d);
+                b = 2.0 * y / d;
+            }
+            const double sq_dev = a * sum_d2 - b * ns3 + ns2;
+            if (sq_dev > (d - 1.0) * tol2) break;
+        }
         end = cand;
         s2 = ns2;
         s3 = ns3;
@@ -80,16 +101,17 @@ __global__ void k_spec(const double* __restrict__ v, ChunkGeom g, int64_t n_chun
     if (ch >= n_chunks) return;
     int64_t s, c, lo, hi, last;
     chunk_bounds(g, ch, s, c, lo, hi, last);
-    // compress() rejects non-finite samples (compression.hpp:73-74)
-    bool ok = true;
-    for (int64_t i = lo; i <= hi; ++i) ok &= isfinite(v[i]);
-    if (!ok) atomicExch(bad, 1);
+    // compress() rejects non-finite samples (compression.hpp:73-74): every
+    // sample in (lo, exit] is a candidate of this parse; lo itself is checked
+    // here (it is also a candidate of the previous chunk, unless first)
+    bool nonfinite = !isfinite(v[lo]);
     int64_t p = lo;
     while (p < hi) {
         flags[p] = 1;
-        p = piece_end(v, p, last, tol2, max_len);
+        p = piece_end(v, p, last, tol2, max_len, &nonfinite);
     }
     exit_spec[ch] = p;
+    if (nonfinite) atomicExch(bad, 1);
 }
 
 // Phase 2: E_out[c] = F_c(E_in[c-1]), F_c = exit of chunk c when the true

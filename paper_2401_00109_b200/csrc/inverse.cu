@@ -1,11 +1,15 @@
 // inverse.cu — inverse symbolization on sm_100a (inverse.hpp:32-132,
 // compression.hpp:87-103, 198-213).
 //
-// The reference's recurrences are sequential and stay sequential: one
-// thread per segment runs the carry / length-fix-up / start-value chains in
-// the reference's rounding (all segments are resident in one wave), then a
-// piece-parallel fill writes the interpolated samples v + inc * (i / len)
-// straight into the (optionally stitched, :198-213) output.
+// The reference's recurrences are sequential and stay sequential, but they
+// are split so that each runs with nothing else on its critical path: per
+// segment, one thread runs the length-carry chain (quantize_lengths :63-74)
+// and a thread of ANOTHER warp the start-value chain (inverse_compress
+// :94-101), both in the reference's rounding. Group sums, the residual
+// fix-up (match_total_length :81-93) and output positions are then exact
+// integer work, and a piece-parallel fill writes the interpolated samples
+// v + inc * (i / len) straight into the (optionally stitched, :198-213)
+// output.
 #include <algorithm>
 
 #include "jb_device.hpp"
@@ -35,29 +39,10 @@ __device__ __forceinline__ double llround_d(double x) {
     return r;
 }
 
-// Pass A -- one thread per segment runs the reference's sequential chains:
-//   quantize_lengths (:63-74): r = llround(l + carry), clamp >= 1,
-//     carry = (l + carry) - r  (r kept as an exact double: no int<->fp
-//     conversions on the ~90-cycle critical path);
-//   inverse_compress (:94-101): v += inc, and the running output position.
-// Only the rounded lengths (int32, 16-byte vector stores on the aligned
-// body) and, every GROUP pieces, checkpoints (v, position) leave the
-// thread, so the per-thread streams cost ~5 B/piece. Then the backward
-// fix-up (match_total_length :81-93) and a re-checkpoint of the tail.
-constexpr int GROUP = 32;
-
-struct ChainOut {
-    int32_t* qlen;      // N
-    double* vstart;     // N: start value of every piece
-    double* ck_v;       // one per group (unused)
-    int64_t* ck_pos;    // one per group
-    int64_t* grp_off;   // n_seg + 1: first group of each segment
-    int32_t* grp_seg;   // segment of every group
-};
+constexpr int GROUP = 32;  // pieces per fill unit
 
 // inverse_digitize_series (:41-44): the first segment holding a label >= k
-__global__ void k_inv_validate(InverseIn in, const int32_t* __restrict__ grp_seg,
-                               unsigned long long* __restrict__ err) {
+__global__ void k_inv_validate(InverseIn in, unsigned long long* __restrict__ err) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < in.N;
          j += (int64_t)gridDim.x * blockDim.x)
         if ((uint64_t)in.labels[j] >= in.k) {
@@ -87,112 +72,240 @@ __device__ __forceinline__ void chain_step(double l, double& carry, int32_t& q) 
     q = (int32_t)r;
 }
 
-__global__ void __launch_bounds__(32) k_inv_chain(InverseIn in, const double* __restrict__ rlen,
-                                                  const double* __restrict__ rinc, ChainOut co,
-                                                  double* __restrict__ out,
-                                                  unsigned long long* __restrict__ err) {
-    const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+constexpr size_t kInvTabSmem = 160 * 1024;  // larger codebooks read the tables from L1/L2
+
+__device__ __forceinline__ const double* inv_tables(const InverseIn& in, const double* rlen,
+                                                    const double* rinc, double* s_tabs) {
+    const int kk = (int)in.k;
+    const bool in_smem = rinc == rlen + kk && 2 * (size_t)kk * sizeof(double) <= kInvTabSmem;
+    if (in_smem) {
+        for (int c = threadIdx.x; c < kk; c += blockDim.x) {
+            s_tabs[c] = rlen[c];
+            s_tabs[kk + c] = rinc[c];
+        }
+    }
+    __syncthreads();
+    return in_smem ? s_tabs : rlen;  // global: rinc follows rlen
+}
+
+// Pass A -- the two chains of 32 segments: warp 0 the length carry
+// (qlen), warp 1 the start values (vstart), one segment per lane. A lane's
+// labels stream through a private shared-memory ring filled by asynchronous
+// 16-byte copies (cp.async) RD tiles ahead, so the in-order warp never waits
+// on memory: each step is its fp64 chain plus a shared-memory read.
+constexpr int RT = 16;                    // labels per ring tile
+constexpr int RD = 8;                     // tiles in flight
+constexpr int RSTRIDE = RT * RD * 4 + 16; // bytes per lane (padded: conflict-free LDS.128)
+
+__device__ __forceinline__ void ring_issue(unsigned char* my, const uint32_t* __restrict__ src,
+                                           int slot) {
+    const unsigned dst = (unsigned)__cvta_generic_to_shared(my + slot * RT * 4);
+#pragma unroll
+    for (int m = 0; m < RT / 4; ++m)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16 * m),
+                     "l"(src + 4 * m));
+}
+__device__ __forceinline__ void ring_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void ring_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+__global__ void __launch_bounds__(64) k_inv_chains(InverseIn in, const double* __restrict__ rlen,
+                                                   const double* __restrict__ rinc,
+                                                   int32_t* __restrict__ qlen,
+                                                   double* __restrict__ vstart) {
+    extern __shared__ double s_tabs[];  // rlen(k) | rinc(k)
+    __shared__ __align__(16) unsigned char ring[64 * RSTRIDE];
+    const double* tabs = inv_tables(in, rlen, rinc, s_tabs);
+    const int kk = (int)in.k;
+    const bool cwarp = threadIdx.x < 32;  // carry warp / start-value warp
+    const int64_t s = blockIdx.x * (int64_t)32 + (threadIdx.x & 31);
     if (s >= in.n_seg) return;
+    unsigned char* my = ring + threadIdx.x * RSTRIDE;
     const int64_t a = in.seg_offsets[s], b = in.seg_offsets[s + 1];
-    // (labels were validated by k_inv_validate)
-    const int64_t g0 = co.grp_off[s];
+    const double* tl = cwarp ? tabs : tabs + kk;
     double carry = 0.0, v = in.anchors[s];
-    int64_t pos = in.out_offsets[s], total = 0;
-    out[pos] = v;
-    auto step = [&](int64_t j, uint32_t lab, double& vs) -> int32_t {
-        if (((j - a) & (GROUP - 1)) == 0) co.ck_pos[g0 + ((j - a) >> 5)] = pos;
-        int32_t q;
-        chain_step(__ldg(rlen + lab), carry, q);
-        vs = v;
-        v += __ldg(rinc + lab);
-        pos += q;
-        total += q;
-        return q;
+    auto one = [&](int64_t j, uint32_t lab) {
+        if (cwarp) {
+            int32_t q;
+            chain_step(tl[lab], carry, q);
+            qlen[j] = q;
+        } else {
+            vstart[j] = v;
+            v += tl[lab];
+        }
     };
     int64_t j = a;
-    double vs0, vs1, vs2, vs3;
-    for (; j < b && (j & 3); ++j) {
-        co.qlen[j] = step(j, in.labels[j], vs0);
-        co.vstart[j] = vs0;
+    for (; j < b && (j & 3); ++j) one(j, in.labels[j]);
+    const int64_t jb = j;
+    const int64_t ntile = (b - jb) / RT;
+    for (int t = 0; t < RD - 1; ++t) {
+        if (t < ntile) ring_issue(my, in.labels + jb + (int64_t)t * RT, t);
+        ring_commit();
     }
-    for (; j + 4 <= b; j += 4) {
-        const uint4 L = *reinterpret_cast<const uint4*>(in.labels + j);
-        int4 Q;
-        Q.x = step(j, L.x, vs0);
-        Q.y = step(j + 1, L.y, vs1);
-        Q.z = step(j + 2, L.z, vs2);
-        Q.w = step(j + 3, L.w, vs3);
-        *reinterpret_cast<int4*>(co.qlen + j) = Q;
-        *reinterpret_cast<double2*>(co.vstart + j) = make_double2(vs0, vs1);
-        *reinterpret_cast<double2*>(co.vstart + j + 2) = make_double2(vs2, vs3);
+    for (int64_t t = 0; t < ntile; ++t) {
+        if (t + RD - 1 < ntile) ring_issue(my, in.labels + jb + (t + RD - 1) * RT, (int)((t + RD - 1) % RD));
+        ring_commit();
+        ring_wait<RD - 1>();  // tile t has landed
+        const uint4* src = reinterpret_cast<const uint4*>(my + (t % RD) * RT * 4);
+        const int64_t j0 = jb + t * RT;
+#pragma unroll
+        for (int m = 0; m < RT / 4; ++m) {
+            const uint4 L = src[m];
+            const int64_t jj = j0 + 4 * m;
+            if (cwarp) {
+                int4 Q;
+                chain_step(tl[L.x], carry, Q.x);
+                chain_step(tl[L.y], carry, Q.y);
+                chain_step(tl[L.z], carry, Q.z);
+                chain_step(tl[L.w], carry, Q.w);
+                *reinterpret_cast<int4*>(qlen + jj) = Q;
+            } else {
+                const double v0 = v;
+                const double v1 = v0 + tl[L.x];
+                const double v2 = v1 + tl[L.y];
+                const double v3 = v2 + tl[L.z];
+                v = v3 + tl[L.w];
+                *reinterpret_cast<double2*>(vstart + jj) = make_double2(v0, v1);
+                *reinterpret_cast<double2*>(vstart + jj + 2) = make_double2(v2, v3);
+            }
+        }
     }
-    for (; j < b; ++j) {
-        co.qlen[j] = step(j, in.labels[j], vs0);
-        co.vstart[j] = vs0;
+    for (j = jb + ntile * RT; j < b; ++j) one(j, in.labels[j]);
+}
+
+// quantized length of every group (warp per group)
+__global__ void k_inv_gsum(InverseIn in, const int32_t* __restrict__ qlen,
+                           const int64_t* __restrict__ grp_off, const int32_t* __restrict__ grp_seg,
+                           int64_t n_groups, int64_t* __restrict__ gsum) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; g < n_groups;
+         g += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t s = grp_seg[g];
+        const int64_t base = in.seg_offsets[s] + (g - grp_off[s]) * GROUP;
+        const int64_t j = base + lane;
+        long long q = j < in.seg_offsets[s + 1] ? qlen[j] : 0;
+        for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+        if (lane == 0) gsum[g] = q;
     }
-    // match_total_length: backward cascade
-    long long residual = in.source_lengths[s] - total;
-    int64_t first_mod = b;
-    for (int64_t t = b; t-- > a && residual != 0;) {
-        long long adj = (long long)co.qlen[t] + residual;
-        if (adj < 1) adj = 1;
-        residual -= adj - co.qlen[t];
-        co.qlen[t] = (int32_t)adj;
-        first_mod = t;
-    }
-    if (residual != 0 || b == a) {
-        atomicMin(err, (unsigned long long)(s * 16 + INVALID_PIECE));
-        return;
-    }
-    if (first_mod < b) {  // positions of the groups after the modified piece
-        const int64_t gm = (first_mod - a) >> 5;
-        int64_t p = co.ck_pos[g0 + gm];
-        for (int64_t t = a + gm * GROUP; t < b; ++t) {
-            if (((t - a) & (GROUP - 1)) == 0) co.ck_pos[g0 + ((t - a) >> 5)] = p;
-            p += co.qlen[t];
+}
+
+// Per segment (warp): match_total_length's backward cascade (lane 0), then
+// the output position of every group (exact scan of the group sums) and
+// the fill records. Errors: the lowest failing segment wins.
+struct GroupRec {
+    int64_t base;  // first piece
+    int64_t pos;   // output index of the sample before the group's first sample
+};
+
+__global__ void k_inv_segfix(InverseIn in, int32_t* __restrict__ qlen,
+                             const int64_t* __restrict__ grp_off, int64_t* __restrict__ gsum,
+                             GroupRec* __restrict__ rec, int32_t* __restrict__ gmeta,
+                             double* __restrict__ out, unsigned long long* __restrict__ err) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; s < in.n_seg;
+         s += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t a = in.seg_offsets[s], b = in.seg_offsets[s + 1];
+        const int64_t g0 = grp_off[s], g1 = grp_off[s + 1];
+        long long total = 0;
+        for (int64_t g = g0 + lane; g < g1; g += 32) total += gsum[g];
+        for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+        int bad = 0;
+        if (lane == 0) {
+            long long residual = in.source_lengths[s] - total;
+            for (int64_t t = b; t-- > a && residual != 0;) {
+                long long adj = (long long)qlen[t] + residual;
+                if (adj < 1) adj = 1;
+                const long long delta = adj - qlen[t];
+                residual -= delta;
+                qlen[t] = (int32_t)adj;
+                gsum[g0 + (t - a) / GROUP] += delta;
+            }
+            bad = residual != 0 || b == a;
+            if (bad) atomicMin(err, (unsigned long long)(s * 16 + INVALID_PIECE));
+            else out[in.out_offsets[s]] = in.anchors[s];
+        }
+        bad = __shfl_sync(0xffffffffu, bad, 0);
+        if (bad) continue;
+        __syncwarp();
+        // group positions: exclusive scan of the group sums
+        const bool drop = in.layout == 0 && (s + 1 < in.n_seg || in.drop_local_last);
+        long long run = in.out_offsets[s];
+        for (int64_t g = g0; g < g1; g += 32) {
+            const int64_t gg = g + lane;
+            const long long v = gg < g1 ? gsum[gg] : 0;
+            long long incl = v;
+            for (int o = 1; o < 32; o <<= 1) {
+                const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (gg < g1) {
+                const int64_t base = a + (gg - g0) * GROUP;
+                const int cnt = (int)(b - base < GROUP ? b - base : GROUP);
+                rec[gg] = GroupRec{base, run + incl - v};
+                gmeta[gg] = cnt | ((drop && gg == g1 - 1) ? 0x100 : 0);
+            }
+            run += __shfl_sync(0xffffffffu, incl, 31);
         }
     }
 }
 
-// Pass B -- one warp per group of GROUP pieces: v within the group replayed
-// sequentially from the checkpoint (shuffled, same rounding), positions by
-// an exact integer scan, then the group's samples v + inc * (i / len)
-// (inverse_compress :97-99) written contiguously into the output; a
-// non-final part of a univariate-partitioned fit drops its last sample
-// (stitch_partitions :198-213).
+// Pass B -- one warp per group of GROUP pieces. A lane writes its own
+// piece's samples v + inc * (i / len) (inverse_compress :97-99; positions
+// from the group's exact scan); a group holding a long piece switches to a
+// sample-parallel layout. A non-final part of a univariate-partitioned fit
+// drops its last sample (stitch_partitions :198-213).
 constexpr int DIV_MAX = 31;  // exact i/len table for len <= DIV_MAX (7.9 KB smem)
+constexpr int LANE_MAX = 16; // pieces up to this length: lane per piece
 
 __global__ void __launch_bounds__(256) k_inv_fill(InverseIn in, const double* __restrict__ rinc,
-                                                  ChainOut co, int64_t n_groups,
-                                                  double* __restrict__ out) {
+                                                  const int32_t* __restrict__ qlen,
+                                                  const double* __restrict__ vstart,
+                                                  const GroupRec* __restrict__ rec,
+                                                  const int32_t* __restrict__ gmeta,
+                                                  int64_t n_groups, double* __restrict__ out) {
     __shared__ double div_tab[(DIV_MAX + 1) * (DIV_MAX + 1)];
+    extern __shared__ double s_inc[];
+    const int kk = (int)in.k;
+    const bool inc_smem = (size_t)kk * sizeof(double) <= kInvTabSmem / 2;
     for (int t = threadIdx.x; t < (DIV_MAX + 1) * (DIV_MAX + 1); t += blockDim.x) {
         const int l = t / (DIV_MAX + 1), i = t % (DIV_MAX + 1);
         div_tab[t] = l > 0 ? (double)i / (double)l : 0.0;  // the same IEEE division
     }
+    if (inc_smem)
+        for (int c = threadIdx.x; c < kk; c += blockDim.x) s_inc[c] = rinc[c];
     __syncthreads();
+    const double* tinc = inc_smem ? s_inc : rinc;
     const int lane = threadIdx.x & 31;
     const unsigned FULL = 0xffffffffu;
     for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; g < n_groups;
          g += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        const int64_t s = co.grp_seg[g];
-        const int64_t a = in.seg_offsets[s], b = in.seg_offsets[s + 1];
-        const int64_t base = a + (g - co.grp_off[s]) * GROUP;
-        const int cnt = (int)((b - base) < GROUP ? (b - base) : GROUP);
-        const int64_t j = base + lane;
+        const GroupRec r = rec[g];
+        const int meta = gmeta[g];
+        const int cnt = meta & 0xFF;
+        const bool drop_last = (meta & 0x100) != 0;  // the group holds the dropped sample
+        const int64_t j = r.base + lane;
         const bool valid = lane < cnt;
-        const int len = valid ? co.qlen[j] : 0;
-        const double inc = valid ? __ldg(rinc + in.labels[j]) : 0.0;
-        const double myv = valid ? co.vstart[j] : 0.0;
+        const int len = valid ? qlen[j] : 0;
+        const double inc = valid ? tinc[in.labels[j]] : 0.0;
+        const double myv = valid ? vstart[j] : 0.0;
         long long incl = len;
         for (int o = 1; o < 32; o <<= 1) {
             const long long y = __shfl_up_sync(FULL, incl, o);
             if (lane >= o) incl += y;
         }
+        const int maxlen = __reduce_max_sync(FULL, len);
+        if (maxlen <= LANE_MAX) {
+            if (valid) {
+                const long long p0 = r.pos + incl - len;
+                const int nl = (drop_last && lane == cnt - 1) ? len - 1 : len;
+                for (int i = 1; i <= nl; ++i)
+                    out[p0 + i] = myv + inc * div_tab[len * (DIV_MAX + 1) + i];
+            }
+            continue;
+        }
         const long long L = __shfl_sync(FULL, incl, 31);
-        const int64_t pos = co.ck_pos[g];
-        const bool drop_last = in.layout == 0 && (s + 1 < in.n_seg || in.drop_local_last) &&
-                               base + GROUP >= b;
         for (long long q0 = 1; q0 <= L; q0 += 32) {
             const long long q = q0 + lane;  // 1-based sample within the group
             int last_below = -1;  // last piece with incl < q (fixed 5 steps)
@@ -211,7 +324,7 @@ __global__ void __launch_bounds__(256) k_inv_fill(InverseIn in, const double* __
                 // (double)i / l, IEEE-rounded; exact table for short pieces
                 const double frac = li <= DIV_MAX ? div_tab[li * (DIV_MAX + 1) + (int)i]
                                                   : (double)i / (double)li;
-                out[pos + q] = vi + ii * frac;
+                out[r.pos + q] = vi + ii * frac;
             }
         }
     }
@@ -244,17 +357,16 @@ void inverse_transform_device(const InverseIn& in, double* d_out, cudaStream_t s
     const int64_t n_groups = h_goff[in.n_seg];
     DArr<int64_t> goff(in.n_seg + 1, st);
     goff.upload(h_goff.data(), in.n_seg + 1);
-    DArr<int32_t> qlen(std::max<int64_t>(in.N, 1) + 4, st);
-    DArr<double> ck_v(1, st);
-    DArr<int64_t> ck_pos(std::max<int64_t>(n_groups, 1), st);
-    DArr<int32_t> gseg(std::max<int64_t>(n_groups, 1), st);
+    const int64_t ng = std::max<int64_t>(n_groups, 1);
+    DArr<int32_t> qlen(std::max<int64_t>(in.N, 1) + 4, st), gseg(ng, st), gmeta(ng, st);
     DArr<double> vstart(std::max<int64_t>(in.N, 1) + 4, st);
-    ChainOut co{qlen.p, vstart.p, ck_v.p, ck_pos.p, goff.p, gseg.p};
+    DArr<int64_t> gsum(ng, st);
+    DArr<GroupRec> rec(ng, st);
     k_group_segments<<<(int)((in.n_seg + 127) / 128), 128, 0, st>>>(goff.p, in.n_seg, gseg.p);
     JB_LAUNCH_CHECK();
     if (in.N > 0) {
         k_inv_validate<<<(int)std::max<int64_t>(1, std::min<int64_t>((in.N + 255) / 256, kSMs * 8)),
-                         256, 0, st>>>(in, gseg.p, err.p);
+                         256, 0, st>>>(in, err.p);
         JB_LAUNCH_CHECK();
         unsigned long long e0;
         err.download(&e0, 1);
@@ -263,12 +375,25 @@ void inverse_transform_device(const InverseIn& in, double* d_out, cudaStream_t s
             throw Error(UNKNOWN_SYMBOL, "label not in codebook of size " + std::to_string(in.k) +
                                             " (segment " + std::to_string(e0 / 16) + ")");
     }
+    const size_t tsmem = sizeof(double) * 2 * kk <= kInvTabSmem ? sizeof(double) * 2 * kk : 0;
     {
         JB_PROF("inverse_chain", st);
-        k_inv_chain<<<(int)((in.n_seg + 31) / 32), 32, 0, st>>>(in, tab.p, tab.p + kk, co, d_out,
-                                                                 err.p);
+        if (tsmem + 64 * RSTRIDE > 48 * 1024)
+            JB_CUDA(cudaFuncSetAttribute(k_inv_chains, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)tsmem));
+        k_inv_chains<<<(int)((in.n_seg + 31) / 32), 64, tsmem, st>>>(in, tab.p, tab.p + kk, qlen.p,
+                                                                      vstart.p);
+        JB_LAUNCH_CHECK();
+        const int wgrid = (int)std::max<int64_t>(
+            1, std::min<int64_t>((n_groups * 32 + 255) / 256, (int64_t)kSMs * 16));
+        if (n_groups > 0)
+            k_inv_gsum<<<wgrid, 256, 0, st>>>(in, qlen.p, goff.p, gseg.p, n_groups, gsum.p);
+        JB_LAUNCH_CHECK();
+        k_inv_segfix<<<(int)std::max<int64_t>(1, std::min<int64_t>((in.n_seg * 32 + 255) / 256,
+                                                                   (int64_t)kSMs * 16)),
+                       256, 0, st>>>(in, qlen.p, goff.p, gsum.p, rec.p, gmeta.p, d_out, err.p);
+        JB_LAUNCH_CHECK();
     }
-    JB_LAUNCH_CHECK();
     unsigned long long e;
     err.download(&e, 1);
     JB_CUDA(cudaStreamSynchronize(st));
@@ -284,9 +409,14 @@ void inverse_transform_device(const InverseIn& in, double* d_out, cudaStream_t s
     }
     if (n_groups > 0) {
         JB_PROF("inverse_fill", st);
+        const size_t fsmem = sizeof(double) * kk <= kInvTabSmem / 2 ? sizeof(double) * kk : 0;
+        if (fsmem > 40 * 1024)
+            JB_CUDA(cudaFuncSetAttribute(k_inv_fill, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)fsmem));
         const int grid = (int)std::max<int64_t>(
             1, std::min<int64_t>((n_groups * 32 + 255) / 256, (int64_t)kSMs * 16));
-        k_inv_fill<<<grid, 256, 0, st>>>(in, tab.p + kk, co, n_groups, d_out);
+        k_inv_fill<<<grid, 256, fsmem, st>>>(in, tab.p + kk, qlen.p, vstart.p, rec.p, gmeta.p,
+                                             n_groups, d_out);
         JB_LAUNCH_CHECK();
     }
 }

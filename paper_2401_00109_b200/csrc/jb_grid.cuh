@@ -75,7 +75,7 @@ struct BlockCands {
 };
 
 // block-wide: s.list/s.n := centers kept for box (bx0,bx1,by0,by1), index order
-__device__ inline void block_candidates(BlockCands& s, const double* __restrict__ centers, int k,
+__device__ inline void block_candidates(BlockCands& s, const double* centers, int k,
                                         double bx0, double bx1, double by0, double by1) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double M = INFINITY;
@@ -117,7 +117,7 @@ constexpr int kGridBlock = 16;  // cells per block side: one thread per cell
 
 // thread-wide candidate filter of one cell box over the block list (or all k
 // centers); writes up to cap indices in index order, returns the full count
-__device__ __forceinline__ int thread_cell_candidates(const double* __restrict__ centers, int k,
+__device__ __forceinline__ int thread_cell_candidates(const double* centers, int k,
                                                       const BlockCands& s, double bx0, double bx1,
                                                       double by0, double by1, uint16_t* out,
                                                       int cap) {
@@ -146,9 +146,13 @@ __device__ __forceinline__ int thread_cell_candidates(const double* __restrict__
 
 // one CTA per kGridBlock x kGridBlock block of cells, one thread per cell
 static __global__ void __launch_bounds__(kBuildTB) k_grid_build(CandGrid g,
-                                                                const double* __restrict__ centers,
+                                                                const double* centers,
                                                                 int k) {
     __shared__ BlockCands s;
+    extern __shared__ double s_centers[];  // 2k: every cell test reads them
+    for (int q = threadIdx.x; q < 2 * k; q += blockDim.x) s_centers[q] = centers[q];
+    __syncthreads();
+    centers = s_centers;
     const int Gb = (g.G + kGridBlock - 1) / kGridBlock;
     for (int blk = blockIdx.x; blk < Gb * Gb; blk += gridDim.x) {
         const int ix0 = (blk % Gb) * kGridBlock, iy0 = (blk / Gb) * kGridBlock;
@@ -170,7 +174,7 @@ static __global__ void __launch_bounds__(kBuildTB) k_grid_build(CandGrid g,
 
 inline void launch_grid_build(const CandGrid& g, const double* centers, int k, cudaStream_t st) {
     const int Gb = (g.G + kGridBlock - 1) / kGridBlock;
-    k_grid_build<<<Gb * Gb, kBuildTB, 0, st>>>(g, centers, k);
+    k_grid_build<<<Gb * Gb, kBuildTB, sizeof(double) * 2 * k, st>>>(g, centers, k);
 }
 
 // nearest_center (clustering.hpp:146-157) through the grid; cx/cy in smem

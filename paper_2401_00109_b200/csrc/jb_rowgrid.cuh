@@ -54,10 +54,14 @@ constexpr int kRowSeg = kBuildTB;  // y cells per CTA block, one thread per cell
 // one CTA per (length, kRowSeg y cells) segment; blocks: the segments to
 // build (null: all of them)
 static __global__ void __launch_bounds__(kBuildTB) k_row_grid_build(RowGrid g,
-                                                                    const double* __restrict__ centers,
+                                                                    const double* centers,
                                                                     int k, const int* __restrict__ blocks,
                                                                     int nblocks) {
     __shared__ BlockCands s;
+    extern __shared__ double s_centers[];  // 2k: every cell test reads them
+    for (int q = threadIdx.x; q < 2 * k; q += blockDim.x) s_centers[q] = centers[q];
+    __syncthreads();
+    centers = s_centers;
     const int nseg = (g.Gy + kRowSeg - 1) / kRowSeg;
     for (int bi = blockIdx.x; bi < nblocks; bi += gridDim.x) {
         const int blk = blocks ? blocks[bi] : bi;
@@ -92,7 +96,8 @@ inline void launch_row_grid_build(const RowGrid& g, const double* centers, int k
                                   const int* blocks = nullptr, int nblocks = -1) {
     if (nblocks < 0) nblocks = row_grid_segments(g);
     if (nblocks > 0)
-        k_row_grid_build<<<nblocks, kBuildTB, 0, st>>>(g, centers, k, blocks, nblocks);
+        k_row_grid_build<<<nblocks, kBuildTB, sizeof(double) * 2 * k, st>>>(g, centers, k, blocks,
+                                                                          nblocks);
 }
 
 // segments holding at least one point (length l <= R, y) -> flags[segment] = 1

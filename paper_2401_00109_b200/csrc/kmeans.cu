@@ -766,35 +766,43 @@ constexpr uint32_t MIXED = 0xFFFFFFFFu;
 // the candidate words of the row cells covering [y0, y1], pruned again with
 // the tile box. Returns false when a cell overflows or the span is long.
 __device__ __forceinline__ bool row_tile_single(const RowGrid& rg, int l, const double4& b,
-                                                const double* __restrict__ centers,
+                                                const double* centers,
                                                 uint32_t& single) {
     int iy0 = (int)((b.z - rg.y0) * rg.invh), iy1 = (int)((b.w - rg.y0) * rg.invh);
     iy0 = min(max(iy0, 0), rg.Gy - 1);
     iy1 = min(max(iy1, 0), rg.Gy - 1);
-    if (iy1 - iy0 >= 8) return false;
+    const int nc = iy1 - iy0 + 1;
+    if (nc > 8) return false;
     const unsigned long long* row =
-        reinterpret_cast<const unsigned long long*>(rg.cell) + (size_t)(l - 1) * rg.Gy;
+        reinterpret_cast<const unsigned long long*>(rg.cell) + (size_t)(l - 1) * rg.Gy + iy0;
+    uint64_t wv[8];  // all cell words first: independent loads
+#pragma unroll
+    for (int j = 0; j < 8; ++j) wv[j] = j < nc ? __ldg(row + j) : ~0ull;
     double M = INFINITY;
-    for (int iy = iy0; iy <= iy1; ++iy) {
-        const uint64_t w = __ldg(row + iy);
-        if ((w & 0xFFFF) >= kRowOverflow) return false;  // overflow / not built
-        for (int j = 0; j < 4; ++j) {
-            const uint32_t c = (uint32_t)((w >> (16 * j)) & 0xFFFF);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        if (j >= nc) break;
+        if ((wv[j] & 0xFFFF) >= kRowOverflow) return false;  // overflow / not built
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t c = (uint32_t)((wv[j] >> (16 * q)) & 0xFFFF);
             if (c == kRowEmpty) break;
             double dmn, dmx;
-            box_d2(__ldg(centers + 2 * c), __ldg(centers + 2 * c + 1), b, dmn, dmx);
+            box_d2(centers[2 * c], centers[2 * c + 1], b, dmn, dmx);
             M = fmin(M, dmx);
         }
     }
     const double thr = M * (1.0 + kKeepMargin) + 1e-300;
     uint32_t first = MIXED;
-    for (int iy = iy0; iy <= iy1; ++iy) {
-        const uint64_t w = __ldg(row + iy);
-        for (int j = 0; j < 4; ++j) {
-            const uint32_t c = (uint32_t)((w >> (16 * j)) & 0xFFFF);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        if (j >= nc) break;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t c = (uint32_t)((wv[j] >> (16 * q)) & 0xFFFF);
             if (c == kRowEmpty) break;
             double dmn, dmx;
-            box_d2(__ldg(centers + 2 * c), __ldg(centers + 2 * c + 1), b, dmn, dmx);
+            box_d2(centers[2 * c], centers[2 * c + 1], b, dmn, dmx);
             if (dmn <= thr) {
                 if (first == MIXED) first = c;
                 else if (c != first) {
@@ -812,7 +820,7 @@ __device__ __forceinline__ bool row_tile_single(const RowGrid& rg, int l, const 
 // l (0: mixed): the row grid when it applies, else the 2-D grid cells.
 __device__ __forceinline__ uint32_t box_single(const double4& b, int l, const CandGrid& g,
                                                const RowGrid& rg,
-                                               const double* __restrict__ centers) {
+                                               const double* centers) {
     uint32_t single;
     if (l >= 1 && l <= rg.R && row_tile_single(rg, l, b, centers, single)) return single;
     if (g.G == 0) return MIXED;  // no 2-D grid (row grid in use)
@@ -833,7 +841,7 @@ __device__ __forceinline__ uint32_t box_single(const double4& b, int l, const Ca
             for (int j = 0; j < n; ++j) {
                 const int c = __ldg(cl + j);
                 double dmn, dmx;
-                box_d2(__ldg(centers + 2 * c), __ldg(centers + 2 * c + 1), b, dmn, dmx);
+                box_d2(centers[2 * c], centers[2 * c + 1], b, dmn, dmx);
                 M = fmin(M, dmx);
             }
         }
@@ -847,7 +855,7 @@ __device__ __forceinline__ uint32_t box_single(const double4& b, int l, const Ca
             for (int j = 0; j < n; ++j) {
                 const uint32_t c = __ldg(cl + j);
                 double dmn, dmx;
-                box_d2(__ldg(centers + 2 * c), __ldg(centers + 2 * c + 1), b, dmn, dmx);
+                box_d2(centers[2 * c], centers[2 * c + 1], b, dmn, dmx);
                 if (dmn <= thr) {
                     if (first == MIXED) first = c;
                     else if (c != first) return MIXED;
@@ -863,11 +871,16 @@ __device__ __forceinline__ uint32_t box_single(const double4& b, int l, const Ca
 // whenever a point of it is relabeled outside this scheme, k_repair): it is
 // skipped. The others are listed for k_lloyd_work. State: tlab[ntiles + s].
 __global__ void k_super_check(const double4* __restrict__ sbox, const int32_t* __restrict__ slenc,
-                              int64_t ntiles, CandGrid g, const double* __restrict__ centers,
+                              int64_t ntiles, CandGrid g, const double* centers,
                               uint32_t* __restrict__ tlab, uint32_t* __restrict__ swork,
                               unsigned long long* __restrict__ nswork,
-                              const int* __restrict__ skip_flag, int force_all, RowGrid rg) {
+                              const int* __restrict__ skip_flag, int force_all, RowGrid rg,
+                              int k) {
     if (skip_flag && (skip_flag[0] | skip_flag[1])) return;
+    extern __shared__ double s_centers[];  // 2k: the candidate tests read them repeatedly
+    for (int i = threadIdx.x; i < 2 * k; i += blockDim.x) s_centers[i] = centers[i];
+    __syncthreads();
+    centers = s_centers;
     const int lane = threadIdx.x & 31;
     const int64_t nsuper = (ntiles + 31) / 32;
     uint32_t* stlab = tlab + ntiles;
@@ -897,11 +910,16 @@ __global__ void k_super_check(const double4* __restrict__ sbox, const int32_t* _
 __global__ void k_tile_expand(const uint32_t* __restrict__ swork,
                               const unsigned long long* __restrict__ nswork,
                               const double4* __restrict__ tbox, const int32_t* __restrict__ tlen,
-                              int64_t ntiles, CandGrid g, const double* __restrict__ centers,
+                              int64_t ntiles, CandGrid g, const double* centers,
                               const uint32_t* __restrict__ tlab, uint32_t* __restrict__ tnew,
                               uint32_t* __restrict__ work, unsigned long long* __restrict__ nwork,
-                              const int* __restrict__ skip_flag, int force_all, RowGrid rg) {
+                              const int* __restrict__ skip_flag, int force_all, RowGrid rg,
+                              int k) {
     if (skip_flag && (skip_flag[0] | skip_flag[1])) return;
+    extern __shared__ double s_centers[];
+    for (int i = threadIdx.x; i < 2 * k; i += blockDim.x) s_centers[i] = centers[i];
+    __syncthreads();
+    centers = s_centers;
     const int lane = threadIdx.x & 31;
     const int64_t nw = (int64_t)*nswork;
     for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nw;
@@ -1288,16 +1306,15 @@ void lloyd_assign(LloydCtx& L, bool full, bool gate_on_empties) {
         JB_PROF("lloyd_tile_check", L.st);
         k_super_check<<<(int)std::max<int64_t>(1, std::min<int64_t>((L.nsuper() + 255) / 256,
                                                                    kSMs * 16)),
-                        256, 0, L.st>>>(L.sbox.p, L.rg.R > 0 ? L.slenc.p : nullptr, L.ntiles, L.cg,
-                                        L.centers.p, L.tlab.p, L.swork.p, L.nswork.p, gate,
-                                        full ? 1 : 0, L.rg);
+                        256, sizeof(double) * 2 * L.k, L.st>>>(
+            L.sbox.p, L.rg.R > 0 ? L.slenc.p : nullptr, L.ntiles, L.cg, L.centers.p, L.tlab.p,
+            L.swork.p, L.nswork.p, gate, full ? 1 : 0, L.rg, L.k);
         k_tile_expand<<<full ? (int)std::max<int64_t>(1, std::min<int64_t>((L.nsuper() + 7) / 8,
                                                                             kSMs * 16))
                              : kSMs * 4,
-                        256, 0, L.st>>>(L.swork.p, L.nswork.p, L.tbox,
-                                        L.rg.R > 0 ? L.tlen : nullptr, L.ntiles, L.cg, L.centers.p,
-                                        L.tlab.p, L.tnew.p, L.work.p, L.nwork.p, gate,
-                                        full ? 1 : 0, L.rg);
+                        256, sizeof(double) * 2 * L.k, L.st>>>(
+            L.swork.p, L.nswork.p, L.tbox, L.rg.R > 0 ? L.tlen : nullptr, L.ntiles, L.cg,
+            L.centers.p, L.tlab.p, L.tnew.p, L.work.p, L.nwork.p, gate, full ? 1 : 0, L.rg, L.k);
     }
     JB_LAUNCH_CHECK();
     JB_PROF("lloyd_assign", L.st);
