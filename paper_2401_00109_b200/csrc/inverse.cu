@@ -29,15 +29,6 @@ __global__ void k_inv_tables(const double* __restrict__ centers,
     }
 }
 
-// llround (round half away from zero) of x, as a double, using only exact
-// fp64 operations: trunc, the exact remainder x - trunc(x), one compare.
-__device__ __forceinline__ double llround_d(double x) {
-    double r = trunc(x);
-    const double f = x - r;  // exact
-    if (f >= 0.5) r += 1.0;
-    else if (f <= -0.5) r -= 1.0;
-    return r;
-}
 
 constexpr int GROUP = 32;  // pieces per fill unit
 
@@ -64,29 +55,24 @@ __global__ void k_group_segments(const int64_t* __restrict__ grp_off, int64_t n_
     for (int64_t g = grp_off[s]; g < grp_off[s + 1]; ++g) grp_seg[g] = (int32_t)s;
 }
 
+// quantize_lengths' step (:68-70): r = max(1, llround(x)), x = l + carry,
+// carry = x - r (exact). For x >= 0.5, llround(x) == floor(fl(x + 0.5)):
+// the sum is exact except where the rounding cannot move the floor (it
+// only rounds when x + 0.5 lies in a binade above x's, i.e. at or above the
+// power of two that is the result); tests/test_round_identity.py checks the
+// identity. x < 0.5 clamps to 1. Five dependent fp64 operations per step
+// instead of eight.
 __device__ __forceinline__ void chain_step(double l, double& carry, int32_t& q) {
     const double x = l + carry;
-    double r = llround_d(x);
-    if (r < 1.0) r = 1.0;
+    double r = floor(x + 0.5);
+    if (x >= 0x1p52) r = x;  // already an integer
+    if (x < 0.5) r = 1.0;
     carry = x - r;
     q = (int32_t)r;
 }
 
 constexpr size_t kInvTabSmem = 160 * 1024;  // larger codebooks read the tables from L1/L2
 
-__device__ __forceinline__ const double* inv_tables(const InverseIn& in, const double* rlen,
-                                                    const double* rinc, double* s_tabs) {
-    const int kk = (int)in.k;
-    const bool in_smem = rinc == rlen + kk && 2 * (size_t)kk * sizeof(double) <= kInvTabSmem;
-    if (in_smem) {
-        for (int c = threadIdx.x; c < kk; c += blockDim.x) {
-            s_tabs[c] = rlen[c];
-            s_tabs[kk + c] = rinc[c];
-        }
-    }
-    __syncthreads();
-    return in_smem ? s_tabs : rlen;  // global: rinc follows rlen
-}
 
 // Pass A -- the two chains of 32 segments: warp 0 the length carry
 // (qlen), warp 1 the start values (vstart), one segment per lane. A lane's
@@ -111,13 +97,21 @@ __device__ __forceinline__ void ring_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+template <bool SMEM_TABS>
 __global__ void __launch_bounds__(64) k_inv_chains(InverseIn in, const double* __restrict__ rlen,
                                                    const double* __restrict__ rinc,
                                                    int32_t* __restrict__ qlen,
                                                    double* __restrict__ vstart) {
     extern __shared__ double s_tabs[];  // rlen(k) | rinc(k)
     __shared__ __align__(16) unsigned char ring[64 * RSTRIDE];
-    const double* tabs = inv_tables(in, rlen, rinc, s_tabs);
+    if (SMEM_TABS) {
+        for (int c = threadIdx.x; c < (int)in.k; c += blockDim.x) {
+            s_tabs[c] = rlen[c];
+            s_tabs[in.k + c] = rinc[c];
+        }
+        __syncthreads();
+    }
+    const double* tabs = SMEM_TABS ? s_tabs : rlen;  // global: rinc follows rlen
     const int kk = (int)in.k;
     const bool cwarp = threadIdx.x < 32;  // carry warp / start-value warp
     const int64_t s = blockIdx.x * (int64_t)32 + (threadIdx.x & 31);
@@ -378,11 +372,12 @@ void inverse_transform_device(const InverseIn& in, double* d_out, cudaStream_t s
     const size_t tsmem = sizeof(double) * 2 * kk <= kInvTabSmem ? sizeof(double) * 2 * kk : 0;
     {
         JB_PROF("inverse_chain", st);
+        auto kern = tsmem ? k_inv_chains<true> : k_inv_chains<false>;
         if (tsmem + 64 * RSTRIDE > 48 * 1024)
-            JB_CUDA(cudaFuncSetAttribute(k_inv_chains, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            JB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)tsmem));
-        k_inv_chains<<<(int)((in.n_seg + 31) / 32), 64, tsmem, st>>>(in, tab.p, tab.p + kk, qlen.p,
-                                                                      vstart.p);
+        kern<<<(int)((in.n_seg + 31) / 32), 64, tsmem, st>>>(in, tab.p, tab.p + kk, qlen.p,
+                                                              vstart.p);
         JB_LAUNCH_CHECK();
         const int wgrid = (int)std::max<int64_t>(
             1, std::min<int64_t>((n_groups * 32 + 255) / 256, (int64_t)kSMs * 16));
