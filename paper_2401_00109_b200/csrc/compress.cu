@@ -93,37 +93,134 @@ __device__ __forceinline__ void chunk_bounds(const ChunkGeom& g, int64_t ch, int
     hi = lo + g.C < last ? lo + g.C : last;
 }
 
-// Phase 1: speculative parse of every chunk from its first start position.
-__global__ void k_spec(const double* __restrict__ v, ChunkGeom g, int64_t n_chunks, double tol2,
-                       int64_t max_len, uint8_t* __restrict__ flags,
-                       int64_t* __restrict__ exit_spec, int* __restrict__ bad) {
+// Piece starts are kept as one bit per sample position, chunk-relative:
+// chunk ch owns words fb[ch * W .. ch * W + W), W = C / 32, bit (p - lo).
+__device__ __forceinline__ bool fbit(const uint32_t* __restrict__ fb, int64_t ch, int W,
+                                     int64_t rel) {
+    return (fb[ch * W + (rel >> 5)] >> (rel & 31)) & 1u;
+}
+
+// Phase 1: speculative parse of every chunk from its first start position,
+// streamed: each sample is loaded once (one register ahead) and tested once
+// against the open piece. When the test fails, the piece closes at the
+// previous sample, which opens the next piece, and the failing sample
+// becomes that piece's d = 1 candidate (always accepted, compression.hpp:54).
+// Identical decisions to piece_end, with no re-loads and a uniform
+// per-sample loop across the warp.
+__global__ void __launch_bounds__(128) k_spec(const double* __restrict__ v, ChunkGeom g,
+                                              int64_t n_chunks, double tol2, int64_t max_len,
+                                              uint32_t* __restrict__ fb,
+                                              int64_t* __restrict__ exit_spec,
+                                              int* __restrict__ bad) {
     const int64_t ch = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (ch >= n_chunks) return;
     int64_t s, c, lo, hi, last;
     chunk_bounds(g, ch, s, c, lo, hi, last);
-    // compress() rejects non-finite samples (compression.hpp:73-74): every
-    // sample in (lo, exit] is a candidate of this parse; lo itself is checked
-    // here (it is also a candidate of the previous chunk, unless first)
-    bool nonfinite = !isfinite(v[lo]);
-    int64_t p = lo;
-    while (p < hi) {
-        flags[p] = 1;
-        p = piece_end(v, p, last, tol2, max_len, &nonfinite);
+    const int W = (int)(g.C >> 5);
+    uint32_t* my = fb + ch * W;
+    uint32_t word = 1u;  // bit of lo: the chunk's first start
+    int wi = 0;
+    auto flag = [&](int64_t p) {
+        const int rel = (int)(p - lo);
+        while (wi < (rel >> 5)) {
+            my[wi++] = word;
+            word = 0;
+        }
+        word |= 1u << (rel & 31);
+    };
+    double prev = v[lo];            // v[i - 1]
+    bool nonfinite = !isfinite(prev);
+    double base = prev;             // v[start]
+    int64_t start = lo, L = 0;      // open piece: start, current length
+    double s2 = 0.0, s3 = 0.0, sq = 0.0;
+    int64_t i = lo + 1;
+    double vc = i <= last ? __ldg(v + i) : 0.0;
+    int64_t exit_p = -1;
+    for (;;) {
+        if (i > last) {  // every candidate accepted: the piece ends at last
+            exit_p = last;
+            break;
+        }
+        const double vn = i + 1 <= last ? __ldg(v + i + 1) : 0.0;  // next sample in flight
+        nonfinite |= !isfinite(vc);
+        const int64_t Ln = L + 1;
+        const double y = vc - base;
+        const double d = (double)Ln;
+        const double yy = y * y;
+        const double ns2 = s2 + yy;
+        const double ns3 = s3 + d * y;
+        const double nsq = sq + d * d;
+        bool brk = false;
+        if (Ln > 1) {
+            double sum_d2 = nsq;
+            if (Ln > 165000) sum_d2 = d * (d + 1.0) * (2.0 * d + 1.0) / 6.0;
+            double a, b;  // inc * inc / (len * len), 2.0 * inc / len
+            if ((Ln & (Ln - 1)) == 0) {
+                const int m = __ffsll(Ln) - 1;
+                const double inv = __longlong_as_double((long long)(1023 - m) << 52);
+                a = yy * (inv * inv);
+                b = (2.0 * y) * inv;
+            } else {
+                a = yy / (d * d);
+                b = 2.0 * y / d;
+            }
+            const double sq_dev = a * sum_d2 - b * ns3 + ns2;
+            brk = sq_dev > (d - 1.0) * tol2;
+        }
+        if (brk) {
+            // the piece ends at i - 1, which starts the next one
+            start = i - 1;
+            if (start >= hi) {
+                exit_p = start;
+                break;
+            }
+            flag(start);
+            base = prev;
+            const double y1 = vc - base;  // candidate i at d = 1 (same operations)
+            s2 = 0.0 + y1 * y1;
+            s3 = 0.0 + 1.0 * y1;
+            sq = 0.0 + 1.0;
+            L = 1;
+        } else {
+            s2 = ns2;
+            s3 = ns3;
+            sq = nsq;
+            L = Ln;
+        }
+        if (max_len > 0 && L >= max_len) {  // closes at i (compression.hpp:61-63)
+            start = i;
+            if (start >= hi) {
+                exit_p = start;
+                break;
+            }
+            flag(start);
+            base = vc;
+            s2 = s3 = sq = 0.0;
+            L = 0;
+        }
+        prev = vc;
+        vc = vn;
+        ++i;
     }
-    exit_spec[ch] = p;
+    for (; wi < W; ++wi) {
+        my[wi] = word;
+        word = 0;
+    }
+    exit_spec[ch] = exit_p;
     if (nonfinite) atomicExch(bad, 1);
 }
 
 // Phase 2: E_out[c] = F_c(E_in[c-1]), F_c = exit of chunk c when the true
 // orbit enters it at t.
 __global__ void k_fix(const double* __restrict__ v, ChunkGeom g, int64_t n_chunks, double tol2,
-                      int64_t max_len, const uint8_t* __restrict__ flags,
+                      int64_t max_len, const uint32_t* __restrict__ fb,
                       const int64_t* __restrict__ exit_spec, const int64_t* __restrict__ E_in,
                       int64_t* __restrict__ E_out, int* __restrict__ changed) {
     const int64_t ch = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (ch >= n_chunks) return;
     int64_t s, c, lo, hi, last;
     chunk_bounds(g, ch, s, c, lo, hi, last);
+    const int W = (int)(g.C >> 5);
     int64_t r;
     if (c == 0) {
         r = exit_spec[ch];
@@ -131,13 +228,13 @@ __global__ void k_fix(const double* __restrict__ v, ChunkGeom g, int64_t n_chunk
         const int64_t t = E_in[ch - 1];
         if (t >= hi) {
             r = t;
-        } else if (flags[t]) {
+        } else if (fbit(fb, ch, W, t - lo)) {
             r = exit_spec[ch];
         } else {
             int64_t q = t;
             do {
                 q = piece_end(v, q, last, tol2, max_len);
-            } while (q < hi && !flags[q]);
+            } while (q < hi && !fbit(fb, ch, W, q - lo));
             r = q < hi ? exit_spec[ch] : q;
         }
     }
@@ -145,102 +242,98 @@ __global__ void k_fix(const double* __restrict__ v, ChunkGeom g, int64_t n_chunk
     if (r != E_in[ch]) atomicExch(changed, 1);
 }
 
-// Phase 3: rewrite each chunk's flags to the true orbit and count its pieces.
+// Phase 3: rewrite each chunk's flags to the true orbit.
 __global__ void k_apply(const double* __restrict__ v, ChunkGeom g, int64_t n_chunks, double tol2,
-                        int64_t max_len, uint8_t* __restrict__ flags,
+                        int64_t max_len, uint32_t* __restrict__ fb,
                         const int64_t* __restrict__ E) {
     const int64_t ch = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (ch >= n_chunks) return;
     int64_t s, c, lo, hi, last;
     chunk_bounds(g, ch, s, c, lo, hi, last);
+    const int W = (int)(g.C >> 5);
+    uint32_t* my = fb + ch * W;
+    auto clear_range = [&](int64_t p0, int64_t p1) {  // bits of [p0, p1)
+        for (int64_t p = p0; p < p1; ++p) my[(p - lo) >> 5] &= ~(1u << ((p - lo) & 31));
+    };
     const int64_t T = c == 0 ? lo : E[ch - 1];
     if (T >= hi) {
-        for (int64_t i = lo; i < hi; ++i) flags[i] = 0;
+        for (int w = 0; w < W; ++w) my[w] = 0;
     } else {
-        for (int64_t i = lo; i < T; ++i) flags[i] = 0;
-        if (!flags[T]) {
+        clear_range(lo, T);
+        if (!fbit(fb, ch, W, T - lo)) {
             int64_t p = T;
-            flags[p] = 1;
+            my[(p - lo) >> 5] |= 1u << ((p - lo) & 31);
             for (;;) {
                 const int64_t q = piece_end(v, p, last, tol2, max_len);
                 const int64_t z = q < hi ? q : hi;
-                for (int64_t i = p + 1; i < z; ++i) flags[i] = 0;
-                if (q >= hi || flags[q]) break;
-                flags[q] = 1;
+                clear_range(p + 1, z);
+                if (q >= hi || fbit(fb, ch, W, q - lo)) break;
+                my[(q - lo) >> 5] |= 1u << ((q - lo) & 31);
                 p = q;
             }
         }
     }
 }
 
-// Phase 4a: pieces per chunk (one warp per chunk; lane l owns a contiguous
-// slice of C/32 start positions).
-__global__ void k_count(ChunkGeom g, int64_t n_chunks, const uint8_t* __restrict__ flags,
+// Phase 4a: pieces per chunk.
+__global__ void k_count(ChunkGeom g, int64_t n_chunks, const uint32_t* __restrict__ fb,
                         int64_t* __restrict__ count) {
-    const int lane = threadIdx.x & 31;
-    const int per = (int)(g.C / 32);
-    for (int64_t ch = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; ch < n_chunks;
-         ch += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        int64_t s, c, lo, hi, last;
-        chunk_bounds(g, ch, s, c, lo, hi, last);
+    const int W = (int)(g.C >> 5);
+    for (int64_t ch = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ch < n_chunks;
+         ch += (int64_t)gridDim.x * blockDim.x) {
         int n = 0;
-        const int64_t p0 = lo + (int64_t)lane * per;
-        for (int i = 0; i < per; ++i)
-            if (p0 + i < hi) n += flags[p0 + i];
-        for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
-        if (lane == 0) count[ch] = n;
+        for (int w = 0; w < W; ++w) n += __popc(fb[ch * W + w]);
+        count[ch] = n;
     }
 }
 
-// Phase 4b: emit (len, inc) pieces in input order, one warp per chunk. A
-// piece ends at the next start (same lane slice, a later lane's first start,
-// or the chunk's true exit E). Also max|inc| and max len for the fixed-point
-// exponents downstream.
+// Phase 4b: emit (len, inc) pieces in input order, one warp per chunk, a
+// lane per sample position of each 32-bit flag word: a flagged lane's piece
+// ends at the next set bit (this word, a later word, or the chunk's true exit
+// E); its output slot is the chunk base plus the set bits before it, so the
+// loads of v and the stores of len/inc are coalesced. Also max|inc| and max
+// len for the fixed-point exponents downstream.
 __global__ void k_emit(const double* __restrict__ v, ChunkGeom g, int64_t n_chunks,
-                       const uint8_t* __restrict__ flags, const int64_t* __restrict__ E,
+                       const uint32_t* __restrict__ fb, const int64_t* __restrict__ E,
                        const int64_t* __restrict__ base, int32_t* __restrict__ out_len,
                        double* __restrict__ out_inc, unsigned long long* __restrict__ max_inc_bits,
                        int* __restrict__ max_len) {
     const int lane = threadIdx.x & 31;
-    const int per = (int)(g.C / 32);
+    const int W = (int)(g.C >> 5);
     double mi = 0.0;
     int ml = 0;
     for (int64_t ch = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; ch < n_chunks;
          ch += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         int64_t s, c, lo, hi, last;
         chunk_bounds(g, ch, s, c, lo, hi, last);
-        const int64_t p0 = lo + (int64_t)lane * per;
-        unsigned bits = 0;  // flagged positions of this lane's slice
-        for (int i = 0; i < per; ++i)
-            if (p0 + i < hi && flags[p0 + i]) bits |= 1u << i;
-        const int cnt = __popc(bits);
-        int excl = cnt;
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, excl, o);
-            if (lane >= o) excl += y;
-        }
-        excl -= cnt;
-        // first start of any later lane (suffix min), else the chunk exit
-        int64_t first = bits ? p0 + (__ffs(bits) - 1) : INT64_MAX;
-        int64_t after = INT64_MAX;
-        for (int o = 1; o < 32; o <<= 1) {
-            const int64_t y = __shfl_down_sync(0xffffffffu, first, o);
-            if (lane + o < 32) after = min(after, y);
-            first = min(first, y);  // becomes suffix-min including self
-        }
-        if (after == INT64_MAX) after = E[ch];
-        int64_t j = base[ch] + excl;
-        while (bits) {
-            const int i = __ffs(bits) - 1;
-            bits &= bits - 1;
-            const int64_t p = p0 + i;
-            const int64_t e = bits ? p0 + (__ffs(bits) - 1) : after;
-            const double inc = v[e] - v[p];
-            out_len[j] = (int32_t)(e - p);
-            out_inc[j] = inc;
-            mi = fmax(mi, fabs(inc));
-            ml = max(ml, (int)(e - p));
-            ++j;
+        const uint32_t mine = lane < W ? fb[ch * W + lane] : 0u;  // all words of the chunk
+        const int64_t Ech = E[ch];
+        int64_t j = base[ch];
+        for (int w = 0; w < W; ++w) {
+            const uint32_t m = __shfl_sync(0xffffffffu, mine, w);
+            if (!m) continue;
+            // next start after this word: first set bit of a later word
+            uint32_t later = lane > w ? mine : 0u;
+            const unsigned nz = __ballot_sync(0xffffffffu, later != 0);
+            int64_t nxt = Ech;
+            if (nz) {
+                const int wl = __ffs(nz) - 1;
+                const uint32_t mw = __shfl_sync(0xffffffffu, mine, wl);
+                nxt = lo + 32 * wl + (__ffs(mw) - 1);
+            }
+            const bool f = (m >> lane) & 1u;
+            if (f) {
+                const int64_t p = lo + 32 * w + lane;
+                const uint32_t above = lane < 31 ? (m >> (lane + 1)) : 0u;
+                const int64_t e = above ? p + __ffs(above) : nxt;
+                const double inc = v[e] - v[p];
+                const int64_t k = j + __popc(m & ((1u << lane) - 1u));
+                out_len[k] = (int32_t)(e - p);
+                out_inc[k] = inc;
+                mi = fmax(mi, fabs(inc));
+                ml = max(ml, (int)(e - p));
+            }
+            j += __popc(m);
         }
     }
     for (int o = 16; o > 0; o >>= 1) {
@@ -280,8 +373,8 @@ void compress_segments(const double* d_values, const SegTable& seg, double tol,
     ChunkGeom g{seg.first.p, seg.steps.p, chunk_off.p, n_seg, C};
 
     const double tol2 = tol * tol;
-    DArr<uint8_t> flags(max_last + 1, st);
-    flags.zero();
+    const int W = (int)(C / 32);
+    DArr<uint32_t> flags(n_chunks * W, st);  // every word is written by k_spec
     DArr<int64_t> exit_spec(n_chunks, st), Ea(n_chunks, st), Eb(n_chunks, st), cnt(n_chunks, st);
     DArr<int> dflag(2, st);
     dflag.zero();
@@ -326,7 +419,7 @@ void compress_segments(const double* d_values, const SegTable& seg, double tol,
         1, std::min<int64_t>((n_chunks * 32 + 255) / 256, (int64_t)kSMs * 16));
     {
         JB_PROF("compress_count", st);
-        k_count<<<wgrid, 256, 0, st>>>(g, n_chunks, flags.p, cnt.p);
+        k_count<<<nb, TB, 0, st>>>(g, n_chunks, flags.p, cnt.p);
     }
     JB_LAUNCH_CHECK();
 
