@@ -31,29 +31,10 @@ __global__ void k_inv_tables(const double* __restrict__ centers,
 
 
 constexpr int GROUP = 32;  // pieces per fill unit
-
-// inverse_digitize_series (:41-44): the first segment holding a label >= k
-__global__ void k_inv_validate(InverseIn in, unsigned long long* __restrict__ err) {
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < in.N;
-         j += (int64_t)gridDim.x * blockDim.x)
-        if ((uint64_t)in.labels[j] >= in.k) {
-            // segment of piece j: binary search of the piece offsets
-            int64_t lo = 0, hi = in.n_seg;
-            while (hi - lo > 1) {
-                const int64_t m = (lo + hi) >> 1;
-                if (in.seg_offsets[m] <= j) lo = m;
-                else hi = m;
-            }
-            atomicMin(err, (unsigned long long)(lo * 16 + UNKNOWN_SYMBOL));
-        }
-}
-
-__global__ void k_group_segments(const int64_t* __restrict__ grp_off, int64_t n_seg,
-                                 int32_t* __restrict__ grp_seg) {
-    const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (s >= n_seg) return;
-    for (int64_t g = grp_off[s]; g < grp_off[s + 1]; ++g) grp_seg[g] = (int32_t)s;
-}
+// errors: lowest segment first, and within a segment the label check first
+// (reconstruct processes series in order; inverse_digitize_series checks
+// labels before quantize/match_total_length): code = segment * 4 + rank
+constexpr int kErrLabel = 0, kErrPiece = 1;
 
 // quantize_lengths' step (:68-70): r = max(1, llround(x)), x = l + carry,
 // carry = x - r (exact). For x >= 0.5, llround(x) == floor(fl(x + 0.5)):
@@ -101,7 +82,13 @@ template <bool SMEM_TABS>
 __global__ void __launch_bounds__(64) k_inv_chains(InverseIn in, const double* __restrict__ rlen,
                                                    const double* __restrict__ rinc,
                                                    int32_t* __restrict__ qlen,
-                                                   double* __restrict__ vstart) {
+                                                   double* __restrict__ vstart,
+                                                   const int64_t* __restrict__ grp_off,
+                                                   int64_t* __restrict__ gsum,
+                                                   unsigned long long* __restrict__ err) {
+    // The carry warp also validates every label (inverse_digitize_series
+    // :41-44) and sums the quantized lengths of each group of GROUP pieces;
+    // both are off its fp64 critical path.
     extern __shared__ double s_tabs[];  // rlen(k) | rinc(k)
     __shared__ __align__(16) unsigned char ring[64 * RSTRIDE];
     if (SMEM_TABS) {
@@ -120,14 +107,32 @@ __global__ void __launch_bounds__(64) k_inv_chains(InverseIn in, const double* _
     const int64_t a = in.seg_offsets[s], b = in.seg_offsets[s + 1];
     const double* tl = cwarp ? tabs : tabs + kk;
     double carry = 0.0, v = in.anchors[s];
+    bool badlab = false;
+    int64_t g = grp_off[s];
+    long long gacc = 0;
+    int gcnt = 0;
+    auto lab_ok = [&](uint32_t lab) -> uint32_t {  // invalid labels flag the segment
+        const bool bad = lab >= (uint32_t)kk;
+        badlab |= bad;
+        return bad ? 0u : lab;
+    };
+    auto gadd = [&](int32_t q) {
+        gacc += q;
+        if (++gcnt == GROUP) {
+            gsum[g++] = gacc;
+            gacc = 0;
+            gcnt = 0;
+        }
+    };
     auto one = [&](int64_t j, uint32_t lab) {
         if (cwarp) {
             int32_t q;
-            chain_step(tl[lab], carry, q);
+            chain_step(tl[lab_ok(lab)], carry, q);
             qlen[j] = q;
+            gadd(q);
         } else {
             vstart[j] = v;
-            v += tl[lab];
+            v += tl[lab < (uint32_t)kk ? lab : 0u];
         }
     };
     int64_t j = a;
@@ -150,38 +155,30 @@ __global__ void __launch_bounds__(64) k_inv_chains(InverseIn in, const double* _
             const int64_t jj = j0 + 4 * m;
             if (cwarp) {
                 int4 Q;
-                chain_step(tl[L.x], carry, Q.x);
-                chain_step(tl[L.y], carry, Q.y);
-                chain_step(tl[L.z], carry, Q.z);
-                chain_step(tl[L.w], carry, Q.w);
+                chain_step(tl[lab_ok(L.x)], carry, Q.x);
+                chain_step(tl[lab_ok(L.y)], carry, Q.y);
+                chain_step(tl[lab_ok(L.z)], carry, Q.z);
+                chain_step(tl[lab_ok(L.w)], carry, Q.w);
                 *reinterpret_cast<int4*>(qlen + jj) = Q;
+                gadd(Q.x);
+                gadd(Q.y);
+                gadd(Q.z);
+                gadd(Q.w);
             } else {
-                const double v0 = v;
-                const double v1 = v0 + tl[L.x];
-                const double v2 = v1 + tl[L.y];
-                const double v3 = v2 + tl[L.z];
-                v = v3 + tl[L.w];
+                const double v0 = v;  // invalid labels: the carry warp reports them
+                const double v1 = v0 + tl[L.x < (uint32_t)kk ? L.x : 0u];
+                const double v2 = v1 + tl[L.y < (uint32_t)kk ? L.y : 0u];
+                const double v3 = v2 + tl[L.z < (uint32_t)kk ? L.z : 0u];
+                v = v3 + tl[L.w < (uint32_t)kk ? L.w : 0u];
                 *reinterpret_cast<double2*>(vstart + jj) = make_double2(v0, v1);
                 *reinterpret_cast<double2*>(vstart + jj + 2) = make_double2(v2, v3);
             }
         }
     }
     for (j = jb + ntile * RT; j < b; ++j) one(j, in.labels[j]);
-}
-
-// quantized length of every group (warp per group)
-__global__ void k_inv_gsum(InverseIn in, const int32_t* __restrict__ qlen,
-                           const int64_t* __restrict__ grp_off, const int32_t* __restrict__ grp_seg,
-                           int64_t n_groups, int64_t* __restrict__ gsum) {
-    const int lane = threadIdx.x & 31;
-    for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; g < n_groups;
-         g += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        const int64_t s = grp_seg[g];
-        const int64_t base = in.seg_offsets[s] + (g - grp_off[s]) * GROUP;
-        const int64_t j = base + lane;
-        long long q = j < in.seg_offsets[s + 1] ? qlen[j] : 0;
-        for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-        if (lane == 0) gsum[g] = q;
+    if (cwarp) {
+        if (gcnt) gsum[g] = gacc;
+        if (badlab) atomicMin(err, (unsigned long long)(s * 4 + kErrLabel));
     }
 }
 
@@ -217,7 +214,7 @@ __global__ void k_inv_segfix(InverseIn in, int32_t* __restrict__ qlen,
                 gsum[g0 + (t - a) / GROUP] += delta;
             }
             bad = residual != 0 || b == a;
-            if (bad) atomicMin(err, (unsigned long long)(s * 16 + INVALID_PIECE));
+            if (bad) atomicMin(err, (unsigned long long)(s * 4 + kErrPiece));
             else out[in.out_offsets[s]] = in.anchors[s];
         }
         bad = __shfl_sync(0xffffffffu, bad, 0);
@@ -352,23 +349,10 @@ void inverse_transform_device(const InverseIn& in, double* d_out, cudaStream_t s
     DArr<int64_t> goff(in.n_seg + 1, st);
     goff.upload(h_goff.data(), in.n_seg + 1);
     const int64_t ng = std::max<int64_t>(n_groups, 1);
-    DArr<int32_t> qlen(std::max<int64_t>(in.N, 1) + 4, st), gseg(ng, st), gmeta(ng, st);
+    DArr<int32_t> qlen(std::max<int64_t>(in.N, 1) + 4, st), gmeta(ng, st);
     DArr<double> vstart(std::max<int64_t>(in.N, 1) + 4, st);
     DArr<int64_t> gsum(ng, st);
     DArr<GroupRec> rec(ng, st);
-    k_group_segments<<<(int)((in.n_seg + 127) / 128), 128, 0, st>>>(goff.p, in.n_seg, gseg.p);
-    JB_LAUNCH_CHECK();
-    if (in.N > 0) {
-        k_inv_validate<<<(int)std::max<int64_t>(1, std::min<int64_t>((in.N + 255) / 256, kSMs * 8)),
-                         256, 0, st>>>(in, err.p);
-        JB_LAUNCH_CHECK();
-        unsigned long long e0;
-        err.download(&e0, 1);
-        JB_CUDA(cudaStreamSynchronize(st));
-        if (e0 != ~0ULL)
-            throw Error(UNKNOWN_SYMBOL, "label not in codebook of size " + std::to_string(in.k) +
-                                            " (segment " + std::to_string(e0 / 16) + ")");
-    }
     const size_t tsmem = sizeof(double) * 2 * kk <= kInvTabSmem ? sizeof(double) * 2 * kk : 0;
     {
         JB_PROF("inverse_chain", st);
@@ -377,12 +361,7 @@ void inverse_transform_device(const InverseIn& in, double* d_out, cudaStream_t s
             JB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)tsmem));
         kern<<<(int)((in.n_seg + 31) / 32), 64, tsmem, st>>>(in, tab.p, tab.p + kk, qlen.p,
-                                                              vstart.p);
-        JB_LAUNCH_CHECK();
-        const int wgrid = (int)std::max<int64_t>(
-            1, std::min<int64_t>((n_groups * 32 + 255) / 256, (int64_t)kSMs * 16));
-        if (n_groups > 0)
-            k_inv_gsum<<<wgrid, 256, 0, st>>>(in, qlen.p, goff.p, gseg.p, n_groups, gsum.p);
+                                                              vstart.p, goff.p, gsum.p, err.p);
         JB_LAUNCH_CHECK();
         k_inv_segfix<<<(int)std::max<int64_t>(1, std::min<int64_t>((in.n_seg * 32 + 255) / 256,
                                                                    (int64_t)kSMs * 16)),
@@ -393,9 +372,8 @@ void inverse_transform_device(const InverseIn& in, double* d_out, cudaStream_t s
     err.download(&e, 1);
     JB_CUDA(cudaStreamSynchronize(st));
     if (e != ~0ULL) {
-        const int code = (int)(e % 16);
-        const long long seg = (long long)(e / 16);
-        if (code == UNKNOWN_SYMBOL)
+        const long long seg = (long long)(e / 4);
+        if (e % 4 == kErrLabel)
             throw Error(UNKNOWN_SYMBOL,
                         "label not in codebook of size " + std::to_string(in.k) +
                             " (segment " + std::to_string(seg) + ")");

@@ -398,12 +398,20 @@ __device__ __forceinline__ double2 load_pt(const double2* __restrict__ pts,
     return idx ? pts[idx[i]] : pts[i];
 }
 
+// Morton keys of the sample points; also gathers the points (and their
+// piece lengths) into sample order, so the sorted gather reads a compact
+// array instead of chasing idx into the full point array again.
 __global__ void k_morton(const double2* __restrict__ pts, const uint64_t* __restrict__ idx,
                          int64_t n, double x0, double sx, double y0, double sy,
-                         uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+                         uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                         double2* __restrict__ cpts, const int32_t* __restrict__ len,
+                         int32_t* __restrict__ clen) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const double2 p = load_pt(pts, idx, i);
+        const uint64_t src = idx ? idx[i] : (uint64_t)i;
+        const double2 p = pts[src];
+        cpts[i] = p;
+        if (len) clen[i] = len[src];
         const uint32_t qx = (uint32_t)fmin(fmax((p.x - x0) * sx, 0.0), 65535.0);
         const uint32_t qy = (uint32_t)fmin(fmax((p.y - y0) * sy, 0.0), 65535.0);
         keys[i] = spread16(qx) | (spread16(qy) << 1);
@@ -1396,8 +1404,10 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
     {
         DArr<uint32_t> keys(n, st), skeys(n, st), vals(n, st);
         const double sx = wx > 0 ? 65535.0 / wx : 0.0, sy = wy > 0 ? 65535.0 / wy : 0.0;
+        DArr<double2> cpts(n, st);
+        DArr<int32_t> clen(rows.len ? n : 0, st);
         k_morton<<<grid_cap(n), 256, 0, st>>>(pts, d_idx, n, bb.xmin, sx, bb.ymin, sy, keys.p,
-                                              vals.p);
+                                              vals.p, cpts.p, rows.len, clen.p);
         JB_LAUNCH_CHECK();
         size_t tb = 0;
         cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.p, skeys.p, vals.p, orig.p, n, 0, 32,
@@ -1405,8 +1415,8 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
         DArr<uint8_t> tmp(tb, st);
         cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.p, skeys.p, vals.p, orig.p, n, 0, 32, st);
         JB_LAUNCH_CHECK();
-        k_sorted_gather<<<grid_cap(n), 256, 0, st>>>(pts, d_idx, orig.p, n, spts.p, pos.p,
-                                                     rows.len, slen.p);
+        k_sorted_gather<<<grid_cap(n), 256, 0, st>>>(cpts.p, nullptr, orig.p, n, spts.p, pos.p,
+                                                     rows.len ? clen.p : nullptr, slen.p);
         JB_LAUNCH_CHECK();
     }
     JB_TRACE("kmeans: morton order", st);
@@ -1755,16 +1765,18 @@ void lloyd_best_dist(const Comm& cm, const double* d_pts, const uint64_t* d_lidx
     if (n > 0) {
         DArr<uint32_t> keys(n, st), skeys(n, st), vals(n, st);
         const double sx = wx > 0 ? 65535.0 / wx : 0.0, sy = wy > 0 ? 65535.0 / wy : 0.0;
+        DArr<double2> cpts(n, st);
+        DArr<int32_t> clen(rows.len ? n : 0, st);
         k_morton<<<grid_cap(n), 256, 0, st>>>(pts, d_lidx, n, bb.xmin, sx, bb.ymin, sy, keys.p,
-                                              vals.p);
+                                              vals.p, cpts.p, rows.len, clen.p);
         JB_LAUNCH_CHECK();
         size_t tb = 0;
         cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.p, skeys.p, vals.p, orig.p, n, 0, 32,
                                         st);
         DArr<uint8_t> tmp(tb, st);
         cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.p, skeys.p, vals.p, orig.p, n, 0, 32, st);
-        k_sorted_gather<<<grid_cap(n), 256, 0, st>>>(pts, d_lidx, orig.p, n, spts.p, pos.p,
-                                                     rows.len, slen.p);
+        k_sorted_gather<<<grid_cap(n), 256, 0, st>>>(cpts.p, nullptr, orig.p, n, spts.p, pos.p,
+                                                     rows.len ? clen.p : nullptr, slen.p);
         k_gkey<<<grid_cap(n), 256, 0, st>>>(d_gpos, orig.p, n, gkey.p);
         JB_LAUNCH_CHECK();
     }
