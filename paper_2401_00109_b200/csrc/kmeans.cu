@@ -630,9 +630,33 @@ __global__ void __launch_bounds__(256) k_d2_tiles(
 
 constexpr int PICK_TB = 1024;
 
+// warp-inclusive scan of int128 values (exact: integer adds with carries)
+__device__ __forceinline__ i128 warp_incl_scan_i128(i128 v) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long lo = (unsigned long long)(u128)v, hi = (unsigned long long)((u128)v >> 64);
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long plo = __shfl_up_sync(0xffffffffu, lo, o);
+        const unsigned long long phi = __shfl_up_sync(0xffffffffu, hi, o);
+        if (lane >= o) {
+            const unsigned long long nlo = lo + plo;
+            hi = hi + phi + (nlo < lo ? 1ULL : 0ULL);
+            lo = nlo;
+        }
+    }
+    return (i128)(((u128)hi << 64) | (u128)lo);
+}
+
+__device__ __forceinline__ i128 shfl_i128(i128 v, int src) {
+    const unsigned long long lo = __shfl_sync(0xffffffffu, (unsigned long long)(u128)v, src);
+    const unsigned long long hi = __shfl_sync(0xffffffffu, (unsigned long long)((u128)v >> 64), src);
+    return (i128)(((u128)hi << 64) | (u128)lo);
+}
+
 // One D^2 round pick: total > 0 ? weighted_index (:59-71) : first unchosen.
 // Finds the original-order partial-sum block holding the crossing, then the
-// element (d2 gathered through pos[]); all prefix arithmetic is exact.
+// element (d2 gathered through pos[]); all prefix arithmetic is exact. Warp w
+// owns a contiguous range of blocks read with coalesced loads; the warp
+// holding the crossing scans its range 32 blocks at a time.
 __global__ void __launch_bounds__(PICK_TB) k_pick(const uint64_t* __restrict__ raw,
                                                   const double* __restrict__ d2s,
                                                   const uint32_t* __restrict__ pos, int64_t n,
@@ -641,20 +665,30 @@ __global__ void __launch_bounds__(PICK_TB) k_pick(const uint64_t* __restrict__ r
                                                   int E, SeedState* ss,
                                                   int64_t* __restrict__ chosen, int c) {
     __shared__ unsigned long long s_lo[32], s_hi[32];
+    __shared__ unsigned long long s_wt_lo[32], s_wt_hi[32];
     __shared__ int s_found_block;
     __shared__ unsigned long long s_found_elem;
     __shared__ unsigned long long s_before[2];
-    const int t = threadIdx.x;
-    const int per = (nblocks + PICK_TB - 1) / PICK_TB;
-    const int b_lo = min(nblocks, t * per), b_hi = min(nblocks, b_lo + per);
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    constexpr int NW = PICK_TB / 32;
+    const int R = ((nblocks + NW - 1) / NW + 31) & ~31;  // blocks per warp, multiple of 32
+    const int b0 = min(nblocks, w * R), b1 = min(nblocks, b0 + R);
     i128 local = 0;
-    for (int b = b_lo; b < b_hi; ++b) local += fx_load(part + 2 * b);
+    for (int b = b0 + lane; b < b1; b += 32) local += fx_load(part + 2 * b);
+    local = fx_warp_sum(local);  // lane 0 holds the warp's total
+    if (lane == 0) {
+        s_wt_lo[w] = (unsigned long long)(u128)local;
+        s_wt_hi[w] = (unsigned long long)((u128)local >> 64);
+    }
     if (t == 0) {
         s_found_block = 0x7FFFFFFF;
         s_found_elem = ~0ULL;
     }
-    i128 total_fx;
-    const i128 excl = block_exscan_i128(local, &total_fx, s_lo, s_hi);
+    __syncthreads();
+    // every warp scans the NW warp totals (cheap; no extra barrier)
+    const i128 wt = (i128)(((u128)s_wt_hi[lane] << 64) | (u128)s_wt_lo[lane]);
+    const i128 wincl = warp_incl_scan_i128(wt);
+    const i128 total_fx = shfl_i128(wincl, 31);
     const double total = fx_to_double(total_fx, E);
     if (!(total > 0.0)) {
         // every remaining point duplicates a center: first free slot (:120-124)
@@ -677,19 +711,29 @@ __global__ void __launch_bounds__(PICK_TB) k_pick(const uint64_t* __restrict__ r
     if (canon >= 1.0) canon = 0x1.fffffffffffffp-1;  // nextafter(1, 0)
     const double u = canon * total + 0.0;             // uniform_real(0, total)
     const i128 U = fx_from_double(u, E);               // floor(u * 2^E), u >= 0
-    int my_block = 0x7FFFFFFF;
-    i128 my_before = 0;
-    {
-        i128 run = excl;
-        for (int b = b_lo; b < b_hi; ++b) {
-            const i128 v = fx_load(part + 2 * b);
-            if (U < run + v) {
-                my_block = b;
-                my_before = run;
-                atomicMin(&s_found_block, b);
+    // the warp range holding the crossing: first warp with U < inclusive prefix
+    const unsigned crossing = __ballot_sync(0xffffffffu, U < wincl);
+    if (w == 0 && crossing) {  // warp 0 resolves the block inside that range
+        const int fw = __ffs(crossing) - 1;
+        const i128 prev = shfl_i128(wincl, fw > 0 ? fw - 1 : 0);
+        i128 run = fw > 0 ? prev : (i128)0;  // exclusive prefix of warp fw's range
+        const int c0 = min(nblocks, fw * R), c1 = min(nblocks, c0 + R);
+        for (int bb = c0; bb < c1; bb += 32) {
+            const int b = bb + lane;
+            const i128 v = b < c1 ? fx_load(part + 2 * b) : (i128)0;
+            const i128 incl = warp_incl_scan_i128(v);
+            const unsigned hit = __ballot_sync(0xffffffffu, b < c1 && U < run + incl);
+            if (hit) {
+                const int hl = __ffs(hit) - 1;
+                const i128 before = run + shfl_i128(incl, hl) - shfl_i128(v, hl);
+                if (lane == 0) {
+                    s_found_block = bb + hl;
+                    s_before[0] = (unsigned long long)(u128)before;
+                    s_before[1] = (unsigned long long)((u128)before >> 64);
+                }
                 break;
             }
-            run += v;
+            run += shfl_i128(incl, 31);
         }
     }
     __syncthreads();
@@ -709,11 +753,6 @@ __global__ void __launch_bounds__(PICK_TB) k_pick(const uint64_t* __restrict__ r
         }
         return;
     }
-    if (my_block == fb) {
-        s_before[0] = (unsigned long long)(u128)my_before;
-        s_before[1] = (unsigned long long)((u128)my_before >> 64);
-    }
-    __syncthreads();
     const i128 before_block = fx_load(s_before);
     // within block fb: 1024 threads x 2 elements (original order)
     const int64_t e0 = (int64_t)fb * D2_R + 2 * t;
