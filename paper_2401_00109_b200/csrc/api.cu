@@ -472,7 +472,7 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
     std::vector<double> backend_centers;
     DArr<uint32_t> labels;
     DArr<uint64_t> sample;         // piece index (this rank's numbering) per sample entry
-    DArr<uint32_t> sample_labels;  // per sample entry
+    KMeansOut svq_km;              // svq: the sample's k-means (labels on demand)
     int64_t n_sample_local = 0;
     bool assign_needed = false;
     switch (c.backend) {
@@ -497,6 +497,7 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
             }
             k = c.k;
             backend_centers = km.centers;
+            kmeans_labels(km, N, st);
             labels = std::move(km.labels);
             fit->iterations = km.iterations;
             fit->draws = cursor;
@@ -546,12 +547,12 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
             }
             k = c.k;
             backend_centers = km.centers;
-            sample_labels = std::move(km.labels);
             fit->work_tiles = km.work_tiles;
             fit->changed_labels = km.changed_labels;
+            fit->iterations = km.iterations;
+            svq_km = std::move(km);  // sample labels: unsorted only if needed below
             labels.alloc(std::max<int64_t>(N, 1), st);
             assign_needed = true;
-            fit->iterations = km.iterations;
             fit->sample_size = S;
             fit->draws = cursor;
             break;
@@ -626,9 +627,11 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
     for (uint64_t g = 0; g < k; ++g) need_sample_stats |= gs.counts[g] == 0;
     std::vector<uint64_t> sls(k, 0), slc(k, 0);
     if (need_sample_stats && c.backend == JB_BACKEND_SVQ) {
-        if (n_sample_local > 0)
-            sample_len_stats(sample.p, sample_labels.p, n_sample_local, fit->pieces.len.p, k, sls,
+        if (n_sample_local > 0) {
+            kmeans_labels(svq_km, n_sample_local, st);
+            sample_len_stats(sample.p, svq_km.labels.p, n_sample_local, fit->pieces.len.p, k, sls,
                              slc, st);
+        }
         if (cm.dist()) {
             auto a = cm.gather(sls), b = cm.gather(slc);
             std::fill(sls.begin(), sls.end(), 0);

@@ -198,11 +198,16 @@ struct BBox {
 struct KMeansOut {
     uint64_t k = 0;
     std::vector<double> centers;  // 2k, backend cluster order
-    DArr<uint32_t> labels;        // per input point (lloyd labels)
+    DArr<uint32_t> labels;        // per input point, once kmeans_labels() ran
+    DArr<uint32_t> slabs, sorig;  // labels in the internal (Morton) order + its
+                                  // map to the input order: unsorted on demand
     uint64_t iterations = 0;
     double sse = 0.0;
     uint64_t work_tiles = 0, changed_labels = 0;  // Lloyd diagnostics (all iterations)
 };
+
+// Materialises out.labels (input order) from the internal order.
+void kmeans_labels(KMeansOut& out, int64_t n, cudaStream_t st);
 
 // sample_indices (clustering.hpp:74-85) on device; idx is S entries.
 // Returns the number of engine draws consumed (>= S).

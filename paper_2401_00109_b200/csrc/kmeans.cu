@@ -1667,14 +1667,29 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
             best_sse = sse;
             out.k = k;
             out.centers = L.centers.to_host(2 * k);
-            out.labels.alloc(n, st);
-            k_unsort_labels<<<grid_cap(n), 256, 0, st>>>(L.labs.p, orig.p, n, out.labels.p);
+            if (n_init == 1) {  // unsorted on demand (kmeans_labels)
+                out.slabs = std::move(L.labs);
+            } else {
+                out.slabs.alloc(n, st);
+                JB_CUDA(cudaMemcpyAsync(out.slabs.p, L.labs.p, sizeof(uint32_t) * n,
+                                        cudaMemcpyDeviceToDevice, st));
+            }
             JB_LAUNCH_CHECK();
             out.iterations = it;
             out.sse = sse;
         }
     }
+    out.sorig = std::move(orig);
     JB_CUDA(cudaStreamSynchronize(st));
+}
+
+void kmeans_labels(KMeansOut& out, int64_t n, cudaStream_t st) {
+    if (out.labels.p || !out.slabs.p) return;
+    out.labels.alloc(std::max<int64_t>(n, 1), st);
+    if (n > 0) {
+        k_unsort_labels<<<grid_cap(n), 256, 0, st>>>(out.slabs.p, out.sorig.p, n, out.labels.p);
+        JB_LAUNCH_CHECK();
+    }
 }
 
 }  // namespace jb
@@ -2207,15 +2222,17 @@ void lloyd_best_dist(const Comm& cm, const double* d_pts, const uint64_t* d_lidx
             best_sse = sse;
             out.k = k;
             out.centers = L.centers.to_host(2 * k);
-            out.labels.alloc(nn, st);
+            out.slabs.alloc(nn, st);
             if (n > 0) {
-                k_unsort_labels<<<grid_cap(n), 256, 0, st>>>(L.labs.p, orig.p, n, out.labels.p);
+                JB_CUDA(cudaMemcpyAsync(out.slabs.p, L.labs.p, sizeof(uint32_t) * n,
+                                        cudaMemcpyDeviceToDevice, st));
                 JB_LAUNCH_CHECK();
             }
             out.iterations = it;
             out.sse = sse;
         }
     }
+    out.sorig = std::move(orig);
     JB_CUDA(cudaStreamSynchronize(st));
 }
 
