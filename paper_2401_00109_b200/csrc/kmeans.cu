@@ -86,32 +86,32 @@ __global__ void __launch_bounds__(320) k_mt_generate(uint64_t seed, uint64_t cou
     }
 }
 
-// Multi-CTA engine: CTA c produces draws [c*B, (c+1)*B). Its starting window
-// (x_{cB} .. x_{cB+311}) is g_c(A) applied to the seeded window, g_c the
-// build-time jump polynomial (mt64_jump.c): XOR of the windows x_{i..i+311}
-// over the set coefficients i of g_c (64 batches of 312 windows). The 31 low
-// bits of the window's first word may differ from the sequential engine, but
-// the twist never reads them. buf[312+i] = twist(buf[i], buf[i+1], buf[i+156])
-// is x_{k+312} = f(x_k, x_{k+1}, x_{k+156}) on a 624-word sliding buffer.
+// Multi-CTA engine: CTA c produces draws [c*b, (c+1)*b). Its starting
+// window (x_{cb} .. x_{cb+311}) is p(A) applied to the seeded window, p the
+// build-time jump polynomial t^(cb) mod phi (mt64_jump.c): one table entry
+// when SUB == 1, else the product of a coarse jump (floor(c/SUB)*SUB*b) and
+// a fine one ((c%SUB)*b), applied in turn. Applying a polynomial is the XOR
+// of the windows x_{i..i+311} over its set coefficients i (64 batches of 312
+// windows; only set bits are visited). The 31 low bits of the window's first
+// word may differ from the sequential engine, but the twist never reads
+// them. buf[312+i] = twist(buf[i], buf[i+1], buf[i+156]) is x_{k+312} =
+// f(x_k, x_{k+1}, x_{k+156}) on a 624-word sliding buffer.
 __global__ void __launch_bounds__(320) k_mt_jump_generate(uint64_t seed, uint64_t count,
-                                                          uint64_t B,
+                                                          uint64_t b, int SUB,
                                                           const uint64_t* __restrict__ jump,
+                                                          const uint64_t* __restrict__ sub,
                                                           uint64_t* __restrict__ out) {
     __shared__ uint64_t buf[624];
     __shared__ uint64_t acc[312];
     __shared__ uint64_t gbits[312];
     const int t = threadIdx.x;
-    const uint64_t start = (uint64_t)blockIdx.x * B;
+    const uint64_t start = (uint64_t)blockIdx.x * b;
     if (start >= count) return;
-    const uint64_t nout = min(B, count - start);
+    const uint64_t nout = min(b, count - start);
     if (t == 0) {
         buf[0] = seed;
         for (int i = 1; i < 312; ++i)
             buf[i] = 6364136223846793005ULL * (buf[i - 1] ^ (buf[i - 1] >> 62)) + (uint64_t)i;
-    }
-    if (t < 312) {
-        gbits[t] = jump[(size_t)blockIdx.x * 312 + t];
-        acc[t] = 0;
     }
     __syncthreads();
     auto advance = [&]() {  // buf[312..623] from buf[0..311]
@@ -127,14 +127,27 @@ __global__ void __launch_bounds__(320) k_mt_jump_generate(uint64_t seed, uint64_
         if (t < 312) buf[t] = v;
         __syncthreads();
     };
-    if (blockIdx.x > 0) {
-        for (int b = 0; b < 64; ++b) {
+    auto apply = [&](const uint64_t* __restrict__ poly) {  // buf[0..311] := poly(A) buf
+        if (t < 312) {
+            gbits[t] = poly[t];
+            acc[t] = 0;
+        }
+        __syncthreads();
+        for (int bb = 0; bb < 64; ++bb) {
             advance();
             if (t < 312) {
                 uint64_t a = acc[t];
-                for (int tt = 0; tt < 312; ++tt) {
-                    const int bit = 312 * b + tt;
-                    if (bit < 19937 && ((gbits[bit >> 6] >> (bit & 63)) & 1ULL)) a ^= buf[tt + t];
+                const int b0 = 312 * bb, b1 = min(b0 + 312, 19937);
+                for (int bit = b0; bit < b1;) {  // set coefficients in [b0, b1)
+                    const int sh = bit & 63, take = min(64 - sh, b1 - bit);
+                    uint64_t m = gbits[bit >> 6] >> sh;
+                    if (take < 64) m &= (1ULL << take) - 1ULL;
+                    while (m) {
+                        const int k = __ffsll((long long)m) - 1;
+                        m &= m - 1ULL;
+                        a ^= buf[bit - b0 + k + t];
+                    }
+                    bit += take;
                 }
                 acc[t] = a;
             }
@@ -143,6 +156,13 @@ __global__ void __launch_bounds__(320) k_mt_jump_generate(uint64_t seed, uint64_
         }
         if (t < 312) buf[t] = acc[t];
         __syncthreads();
+    };
+    if (SUB == 1) {
+        if (blockIdx.x > 0) apply(sub + (size_t)blockIdx.x * 312);
+    } else {
+        const int big = (int)(blockIdx.x / SUB), small = (int)(blockIdx.x % SUB);
+        if (big > 0) apply(jump + (size_t)big * 312);
+        if (small > 0) apply(sub + (size_t)small * 312);
     }
     for (uint64_t base = 0; base < nout; base += 312) {
         advance();
@@ -239,30 +259,22 @@ int grid_cap(uint64_t n, int tb = 256, int per_sm = 8) {
 }  // namespace
 
 namespace {
-// jump table produced by mt64_jump at build time, next to libjabba_b200.so
+// jump tables produced by mt64_jump at build time, next to libjabba_b200.so
 struct JumpTable {
-    bool tried = false;
     uint64_t B = 0, count = 0;
     uint64_t* d = nullptr;  // device copy (process lifetime)
-    int device = -1;
 };
-JumpTable g_jump;
+struct JumpTables {
+    bool tried = false;
+    int device = -1;
+    JumpTable big, sub;  // sub: SUB = big.B / sub.B jumps inside one big block
+};
+JumpTables g_jump;
 std::mutex g_jump_mu;
 
-const JumpTable* jump_table() {
-    std::lock_guard<std::mutex> lk(g_jump_mu);
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (g_jump.tried && g_jump.device == dev) return g_jump.d ? &g_jump : nullptr;
-    g_jump.tried = true;
-    g_jump.device = dev;
-    g_jump.d = nullptr;
-    Dl_info info;
-    if (!dladdr((void*)&jump_table, &info) || !info.dli_fname) return nullptr;
-    std::string path(info.dli_fname);
-    path = path.substr(0, path.rfind('/') + 1) + "mt64_jump.bin";
+bool load_jump(const std::string& path, JumpTable& jt) {
     FILE* f = fopen(path.c_str(), "rb");
-    if (!f) return nullptr;
+    if (!f) return false;
     uint64_t hdr[4];
     std::vector<uint64_t> tab;
     bool ok = fread(hdr, 8, 4, f) == 4 && hdr[0] == 0x4A4D54364A4D5031ULL && hdr[3] == 312;
@@ -271,25 +283,55 @@ const JumpTable* jump_table() {
         ok = fread(tab.data(), 8, tab.size(), f) == tab.size();
     }
     fclose(f);
-    if (!ok) return nullptr;
-    if (cudaMalloc((void**)&g_jump.d, tab.size() * 8) != cudaSuccess) {
-        g_jump.d = nullptr;
-        return nullptr;
+    if (!ok) return false;
+    if (cudaMalloc((void**)&jt.d, tab.size() * 8) != cudaSuccess) {
+        jt.d = nullptr;
+        return false;
     }
-    cudaMemcpy(g_jump.d, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice);
-    g_jump.B = hdr[1];
-    g_jump.count = hdr[2];
+    cudaMemcpy(jt.d, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice);
+    jt.B = hdr[1];
+    jt.count = hdr[2];
+    return true;
+}
+
+const JumpTables* jump_tables() {
+    std::lock_guard<std::mutex> lk(g_jump_mu);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (g_jump.tried && g_jump.device == dev) return g_jump.big.d ? &g_jump : nullptr;
+    g_jump.tried = true;
+    g_jump.device = dev;
+    g_jump.big = JumpTable{};
+    g_jump.sub = JumpTable{};
+    Dl_info info;
+    if (!dladdr((void*)&jump_tables, &info) || !info.dli_fname) return nullptr;
+    std::string dir(info.dli_fname);
+    dir = dir.substr(0, dir.rfind('/') + 1);
+    if (!load_jump(dir + "mt64_jump.bin", g_jump.big)) return nullptr;
+    if (!load_jump(dir + "mt64_jump_small.bin", g_jump.sub) || g_jump.sub.B == 0 ||
+        g_jump.big.B % g_jump.sub.B || g_jump.big.B / g_jump.sub.B > g_jump.sub.count)
+        g_jump.sub = JumpTable{};  // big blocks only
     return &g_jump;
 }
 }  // namespace
 
 void mt19937_64_generate(uint64_t seed, uint64_t count, DArr<uint64_t>& out, cudaStream_t st) {
     out.alloc(count, st);
-    const JumpTable* jt = jump_table();
+    const JumpTables* jt = jump_tables();
     JB_PROF("mt19937_64", st);
-    if (jt && (count + jt->B - 1) / jt->B <= jt->count) {
-        const int ctas = (int)((count + jt->B - 1) / jt->B);
-        k_mt_jump_generate<<<ctas, 320, 0, st>>>(seed, count, jt->B, jt->d, out.p);
+    if (jt && jt->sub.d && (count + jt->sub.B - 1) / jt->sub.B <= jt->sub.count) {
+        // one fine jump per CTA: ~340 CTAs of 2^18 draws for config 4
+        const int ctas = (int)((count + jt->sub.B - 1) / jt->sub.B);
+        k_mt_jump_generate<<<ctas, 320, 0, st>>>(seed, count, jt->sub.B, 1, jt->big.d, jt->sub.d,
+                                                 out.p);
+    } else if (jt && (count + jt->big.B - 1) / jt->big.B <= jt->big.count) {
+        // coarse + fine jumps (fine table present) or coarse blocks only
+        // (SUB == 1 with the coarse table in the fine slot: coarse blocks only)
+        const int SUB = jt->sub.d ? (int)(jt->big.B / jt->sub.B) : 1;
+        const uint64_t b = jt->big.B / SUB;
+        const int ctas = (int)((count + b - 1) / b);
+        k_mt_jump_generate<<<ctas, 320, 0, st>>>(seed, count, b, SUB, jt->big.d,
+                                                 SUB > 1 ? jt->sub.d : jt->big.d, out.p);
     } else {  // no table (or beyond it): one CTA walks the engine
         k_mt_generate<<<1, 320, 0, st>>>(seed, count, out.p);
     }
