@@ -459,6 +459,7 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
     fit->scaling[1] = sc.sigma_len;
     fit->scaling[2] = sc.sigma_inc;
     const BBox bb{sc.xmin, sc.xmax, sc.ymin, sc.ymax};
+    PtsView pv = points_view(fit->pieces, sc);
     PieceRows rows;  // x = scl * len / sigma_len: exact row grids in k-means
     rows.len = fit->pieces.len.p;
     rows.scl = sc.scl;
@@ -489,10 +490,10 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
                 DArr<uint64_t> lidx(std::max<int64_t>(N, 1), st);
                 k_iota_pos<<<gsz(N), 256, 0, st>>>(gpos.p, lidx.p, N, (uint64_t)base);
                 JB_LAUNCH_CHECK();
-                lloyd_best_dist(cm, sc.pts.p, lidx.p, gpos.p, N, (uint64_t)N_glob, c.k, c.max_iters,
+                lloyd_best_dist(cm, pv, lidx.p, gpos.p, N, (uint64_t)N_glob, c.k, c.max_iters,
                                 c.n_init, raw.p, raw_count, &cursor, bb, km, st, rows);
             } else {
-                lloyd_best_device(sc.pts.p, nullptr, N, c.k, c.max_iters, c.n_init, raw.p,
+                lloyd_best_device(pv, nullptr, N, c.k, c.max_iters, c.n_init, raw.p,
                                   raw_count, &cursor, bb, km, st, rows);
             }
             k = c.k;
@@ -537,11 +538,11 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
                 k_local_idx<<<gsz(n_sample_local), 256, 0, st>>>(sample.p, gpos.p, n_sample_local,
                                                                  (uint64_t)base, lidx.p);
                 JB_LAUNCH_CHECK();
-                lloyd_best_dist(cm, sc.pts.p, lidx.p, gpos.p, n_sample_local, S, c.k, c.max_iters,
+                lloyd_best_dist(cm, pv, lidx.p, gpos.p, n_sample_local, S, c.k, c.max_iters,
                                 c.n_init, raw.p, raw_count, &cursor, bb, km, st, rows);
                 sample = std::move(lidx);
             } else {
-                lloyd_best_device(sc.pts.p, sample.p, (int64_t)S, c.k, c.max_iters, c.n_init,
+                lloyd_best_device(pv, sample.p, (int64_t)S, c.k, c.max_iters, c.n_init,
                                   raw.p, raw_count, &cursor, bb, km, st, rows);
                 n_sample_local = (int64_t)S;
             }
@@ -569,6 +570,8 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
             // GA is one sequential sweep over all points in key order (SURVEY
             // §8e): every rank runs it on the gathered points (replicated)
             DArr<double> all_pts;
+            materialize_points(fit->pieces, sc, st);  // GA sorts and sweeps the points
+            pv = points_view(fit->pieces, sc);
             const double* gpts = sc.pts.p;
             if (cm.dist()) {
                 int64_t mx = 0;
@@ -620,7 +623,7 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
     // ---- group statistics, ranking, codebook (digitization.hpp:217-291) ----
     auto t3 = Clock::now();
     GroupStats gs;
-    assign_and_stats(sc.pts.p, fit->pieces.len.p, N, backend_centers, k, bb, assign_needed,
+    assign_and_stats(pv, fit->pieces.len.p, N, backend_centers, k, bb, assign_needed,
                      labels.p, gs, st, sc.max_len_global, sc.scl, sc.sigma_len, &cm, base);
     std::vector<double> centers(2 * k), mean_lengths(k);
     bool need_sample_stats = false;

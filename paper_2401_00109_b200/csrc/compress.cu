@@ -297,11 +297,11 @@ __global__ void k_emit(const double* __restrict__ v, ChunkGeom g, int64_t n_chun
                        const uint32_t* __restrict__ fb, const int64_t* __restrict__ E,
                        const int64_t* __restrict__ base, int32_t* __restrict__ out_len,
                        double* __restrict__ out_inc, unsigned long long* __restrict__ max_inc_bits,
-                       int* __restrict__ max_len) {
+                       int* __restrict__ max_len) {  // [0] max, [1] min
     const int lane = threadIdx.x & 31;
     const int W = (int)(g.C >> 5);
     double mi = 0.0;
-    int ml = 0;
+    int ml = 0, mn = 0x7FFFFFFF;
     for (int64_t ch = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; ch < n_chunks;
          ch += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         int64_t s, c, lo, hi, last;
@@ -332,6 +332,7 @@ __global__ void k_emit(const double* __restrict__ v, ChunkGeom g, int64_t n_chun
                 out_inc[k] = inc;
                 mi = fmax(mi, fabs(inc));
                 ml = max(ml, (int)(e - p));
+                mn = min(mn, (int)(e - p));
             }
             j += __popc(m);
         }
@@ -339,10 +340,12 @@ __global__ void k_emit(const double* __restrict__ v, ChunkGeom g, int64_t n_chun
     for (int o = 16; o > 0; o >>= 1) {
         mi = fmax(mi, __shfl_down_sync(0xffffffffu, mi, o));
         ml = max(ml, __shfl_down_sync(0xffffffffu, ml, o));
+        mn = min(mn, __shfl_down_sync(0xffffffffu, mn, o));
     }
     if (lane == 0) {
         atomicMax(max_inc_bits, dbits(mi));
         atomicMax(max_len, ml);
+        atomicMin(max_len + 1, mn);
     }
 }
 
@@ -444,8 +447,11 @@ void compress_segments(const double* d_values, const SegTable& seg, double tol,
     out.seg_offsets.alloc(n_seg + 1, st);
     DArr<unsigned long long> mx(1, st);
     mx.zero();
-    DArr<int> ml(1, st);
-    ml.zero();
+    DArr<int> ml(2, st);
+    {
+        const int init[2] = {0, 0x7FFFFFFF};
+        ml.upload(init, 2);
+    }
     {
         JB_PROF("compress_emit", st);
         k_emit<<<wgrid, 256, 0, st>>>(d_values, g, n_chunks, flags.p, Ea.p, base.p, out.len.p,
@@ -456,12 +462,13 @@ void compress_segments(const double* d_values, const SegTable& seg, double tol,
                                                             out.seg_offsets.p);
     JB_LAUNCH_CHECK();
     unsigned long long hmx = 0;
-    int hml = 0;
+    int hml[2] = {0, 0};
     mx.download(&hmx, 1);
-    ml.download(&hml, 1);
+    ml.download(hml, 2);
     JB_CUDA(cudaStreamSynchronize(st));
     memcpy(&out.max_abs_inc, &hmx, 8);
-    out.max_len = hml;
+    out.max_len = hml[0];
+    out.min_len = N > 0 ? hml[1] : 0;
 }
 
 }  // namespace jb

@@ -48,12 +48,27 @@ __device__ __forceinline__ i128 block_sum_i128(i128 v) {
 
 constexpr int kTB = 256;
 
+// sum of inc (+ its extremes: with the piece-length extremes of k_emit they
+// give the points' bounding box, x = scl*len/sl and y = inc/si being monotone)
 __global__ void k_sum_inc(const double* __restrict__ inc, int64_t n, int E,
-                          unsigned long long* __restrict__ acc) {
+                          unsigned long long* __restrict__ acc, unsigned long long* __restrict__ mm) {
     i128 s = 0;
+    unsigned long long imn = ~0ULL, imx = 0;
     for (int64_t i = blockIdx.x * (int64_t)kTB + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * kTB)
-        s += fx_from_double(inc[i], E);
+         i += (int64_t)gridDim.x * kTB) {
+        const double v = inc[i];
+        s += fx_from_double(v, E);
+        imn = min(imn, ord_bits(v));
+        imx = max(imx, ord_bits(v));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        imn = min(imn, __shfl_xor_sync(0xffffffffu, imn, o));
+        imx = max(imx, __shfl_xor_sync(0xffffffffu, imx, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(mm, imn);
+        atomicMax(mm + 1, imx);
+    }
     s = block_sum_i128<kTB>(s);
     if (threadIdx.x == 0) fx_atomic_add(acc, s);
 }
@@ -91,48 +106,12 @@ __global__ void k_sum_var(const int32_t* __restrict__ len, const double* __restr
     }
 }
 
-// ScalingParams::apply (core.hpp:130-132) + bounding box
+// ScalingParams::apply (core.hpp:130-132): materialised points (GA only)
 __global__ void k_scale(const int32_t* __restrict__ len, const double* __restrict__ inc,
-                        int64_t n, double scl, double sl, double si, double* __restrict__ pts,
-                        unsigned long long* __restrict__ bb) {
-    unsigned long long xmn = ~0ULL, xmx = 0, ymn = ~0ULL, ymx = 0;
-    constexpr int U = 4;
-    for (int64_t b = blockIdx.x * (int64_t)kTB * U + threadIdx.x; b < n;
-         b += (int64_t)gridDim.x * kTB * U) {
-        int32_t L[U];
-        double I[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t i = b + (int64_t)u * kTB;
-            L[u] = i < n ? len[i] : 0;
-            I[u] = i < n ? inc[i] : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t i = b + (int64_t)u * kTB;
-            if (i >= n) break;
-            const double x = scl * (double)L[u] / sl;
-            const double y = I[u] / si;
-            reinterpret_cast<double2*>(pts)[i] = make_double2(x, y);
-            const unsigned long long ox = ord_bits(x), oy = ord_bits(y);
-            xmn = min(xmn, ox);
-            xmx = max(xmx, ox);
-            ymn = min(ymn, oy);
-            ymx = max(ymx, oy);
-        }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        xmn = min(xmn, __shfl_down_sync(0xffffffffu, xmn, o));
-        xmx = max(xmx, __shfl_down_sync(0xffffffffu, xmx, o));
-        ymn = min(ymn, __shfl_down_sync(0xffffffffu, ymn, o));
-        ymx = max(ymx, __shfl_down_sync(0xffffffffu, ymx, o));
-    }
-    if ((threadIdx.x & 31) == 0) {
-        atomicMin(bb + 0, xmn);
-        atomicMax(bb + 1, xmx);
-        atomicMin(bb + 2, ymn);
-        atomicMax(bb + 3, ymx);
-    }
+                        int64_t n, double scl, double sl, double si, double* __restrict__ pts) {
+    for (int64_t i = blockIdx.x * (int64_t)kTB + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * kTB)
+        reinterpret_cast<double2*>(pts)[i] = make_double2(scl * (double)len[i] / sl, inc[i] / si);
 }
 
 int grid_for(int64_t n) {
@@ -172,9 +151,14 @@ void scale_pieces(const Pieces& pc, int64_t total_steps, double scl, Scaled& out
     DArr<unsigned long long> acc(6, st);
     acc.zero();
     const int Einc = fx_exponent_for(max_abs_inc * n * 1.0000001 + 1e-300);
+    DArr<unsigned long long> mm(2, st);  // extremes of inc (order-preserving bits)
+    {
+        const unsigned long long init[2] = {~0ULL, 0ULL};
+        mm.upload(init, 2);
+    }
     if (pc.N > 0) {
         JB_PROF("scale_sum_inc", st);
-        k_sum_inc<<<grid_for(pc.N), kTB, 0, st>>>(pc.inc.p, pc.N, Einc, acc.p);
+        k_sum_inc<<<grid_for(pc.N), kTB, 0, st>>>(pc.inc.p, pc.N, Einc, acc.p, mm.p);
     }
     JB_LAUNCH_CHECK();
     JB_TRACE("scale: sum inc", st);
@@ -208,21 +192,14 @@ void scale_pieces(const Pieces& pc, int64_t total_steps, double scl, Scaled& out
     out.sigma_len = sl;
     out.sigma_inc = si;
 
-    out.pts.alloc(2 * pc.N, st);
-    JB_TRACE("scale: alloc points", st);
-    DArr<unsigned long long> bb(4, st);
-    unsigned long long init[4] = {~0ULL, 0ULL, ~0ULL, 0ULL};
-    bb.upload(init, 4);
-    if (pc.N > 0) {
-        JB_PROF("scale_points", st);
-        k_scale<<<grid_for(pc.N), kTB, 0, st>>>(pc.len.p, pc.inc.p, pc.N, scl, sl, si, out.pts.p,
-                                               bb.p);
-    }
-    JB_LAUNCH_CHECK();
-    std::vector<unsigned long long> hb = bb.to_host(4);
+    // bounding box of all points from the extremes of len and inc
+    std::vector<unsigned long long> hm = mm.to_host(2);
+    std::vector<unsigned long long> hb = {
+        pc.N > 0 ? (unsigned long long)pc.min_len : ~0ULL, (unsigned long long)pc.max_len,
+        hm[0], hm[1]};
     if (C.dist()) {
         auto all = C.gather(hb);
-        for (int j = 0; j < 4; ++j) hb[j] = all[j];  // rank 0's box, then the others
+        for (int j = 0; j < 4; ++j) hb[j] = all[j];  // rank 0's extremes, then the others
         for (int r = 1; r < C.world; ++r) {
             hb[0] = std::min(hb[0], all[4 * r]);
             hb[1] = std::max(hb[1], all[4 * r + 1]);
@@ -230,13 +207,34 @@ void scale_pieces(const Pieces& pc, int64_t total_steps, double scl, Scaled& out
             hb[3] = std::max(hb[3], all[4 * r + 3]);
         }
     }
-    out.xmin = ord_to_double(hb[0]);
-    out.xmax = ord_to_double(hb[1]);
-    out.ymin = ord_to_double(hb[2]);
-    out.ymax = ord_to_double(hb[3]);
+    out.xmin = scl * (double)(int32_t)hb[0] / sl;  // k_scale's expressions, monotone
+    out.xmax = scl * (double)(int32_t)hb[1] / sl;
+    out.ymin = ord_to_double(hb[2]) / si;
+    out.ymax = ord_to_double(hb[3]) / si;
     out.N_global = N;
     out.max_len_global = max_len;
 }
+
+PtsView points_view(const Pieces& pc, const Scaled& sc) {
+    PtsView v;
+    v.pts = sc.pts.p ? reinterpret_cast<const double2*>(sc.pts.p) : nullptr;
+    v.len = pc.len.p;
+    v.inc = pc.inc.p;
+    v.scl = sc.scl;
+    v.sl = sc.sigma_len;
+    v.si = sc.sigma_inc;
+    return v;
+}
+
+void materialize_points(const Pieces& pc, Scaled& sc, cudaStream_t st) {
+    if (sc.pts.p || pc.N == 0) return;
+    sc.pts.alloc(2 * pc.N, st);
+    JB_PROF("scale_points", st);
+    k_scale<<<grid_for(pc.N), kTB, 0, st>>>(pc.len.p, pc.inc.p, pc.N, sc.scl, sc.sigma_len,
+                                           sc.sigma_inc, sc.pts.p);
+    JB_LAUNCH_CHECK();
+}
+
 
 // ---------------------------------------------------------------------------
 // Nearest-center assignment + group statistics.
@@ -258,9 +256,10 @@ namespace {
 // atomics (native in L2). Everything is exact integer arithmetic, hence
 // independent of the schedule; the host removes the bias (count * B).
 constexpr int AS_TB = 256, AS_U = 4;
+constexpr int kXRow = 64;
 
 __global__ void __launch_bounds__(AS_TB) k_assign_stats(
-    const double2* __restrict__ pts, const int32_t* __restrict__ len, int64_t n,
+    const PtsView pv, const int32_t* __restrict__ len, int64_t n,
     const double* __restrict__ centers, int k, int do_assign, uint32_t* __restrict__ labels,
     int Ex, int Ey, unsigned long long Bx, unsigned long long By,
     unsigned long long* __restrict__ gacc, CandGrid cg, RowGrid rg, int RH) {
@@ -282,6 +281,8 @@ __global__ void __launch_bounds__(AS_TB) k_assign_stats(
         first[c] = 0xFFFFFFFFu;
     }
     for (int j = threadIdx.x; j < RH * k; j += AS_TB) hist[j] = 0;
+    __shared__ double s_xrow[kXRow];  // x of short pieces: k_scale's expression, once
+    for (int l = threadIdx.x; l < kXRow; l += AS_TB) s_xrow[l] = pv.scl * (double)l / pv.sl;
     __syncthreads();
     auto fold = [&]() {
         __syncthreads();
@@ -305,9 +306,21 @@ __global__ void __launch_bounds__(AS_TB) k_assign_stats(
             ll[u] = 0;
             lb[u] = 0;
             if (i < n) {
-                pp[u] = pts[i];
                 ll[u] = len[i];
+                if (pv.pts) {
+                    pp[u] = pv.pts[i];
+                } else {  // x from len (k_scale's expression), y = inc / si
+                    pp[u].y = pv.inc[i];
+                }
                 if (!do_assign) lb[u] = labels[i];
+            }
+        }
+        if (!pv.pts) {
+#pragma unroll
+            for (int u = 0; u < AS_U; ++u) {
+                const int32_t l = ll[u];
+                pp[u] = make_double2(l >= 0 && l < kXRow ? s_xrow[l] : pv.scl * (double)l / pv.sl,
+                                     pp[u].y / pv.si);
             }
         }
 #pragma unroll
@@ -362,14 +375,14 @@ __global__ void __launch_bounds__(AS_TB) k_assign_stats(
 
 // Large alphabets (GA can form thousands of groups; labels are given): the
 // same exact statistics with global 64-bit atomics (native in L2).
-__global__ void k_stats_global(const double2* __restrict__ pts, const int32_t* __restrict__ len,
+__global__ void k_stats_global(const PtsView pv, const int32_t* __restrict__ len,
                                int64_t n, const uint32_t* __restrict__ labels, int k, int Ex,
                                int Ey, unsigned long long Bx, unsigned long long By,
                                unsigned long long* __restrict__ gacc) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t lab = labels[i];
-        const double2 p = pts[i];
+        const double2 p = pv.at(i);
         atomicAdd(gacc + lab, 1ULL);
         atomicAdd(gacc + k + lab, (unsigned long long)len[i]);
         if ((unsigned long long)i < gacc[2 * k + lab]) atomicMin(gacc + 2 * k + lab, (unsigned long long)i);
@@ -416,7 +429,7 @@ __global__ void k_gather(const double2* __restrict__ pts, const uint64_t* __rest
 
 }  // namespace
 
-void assign_and_stats(const double* d_pts, const int32_t* d_len, int64_t n,
+void assign_and_stats(const PtsView& pv, const int32_t* d_len, int64_t n,
                       const std::vector<double>& centers, uint64_t k, const BBox& bb,
                       bool do_assign, uint32_t* d_labels, GroupStats& gs, cudaStream_t st,
                       int32_t max_len, double scl, double sigma_len, const Comm* cm,
@@ -475,7 +488,7 @@ void assign_and_stats(const double* d_pts, const int32_t* d_len, int64_t n,
         if (n > 0) {
             JB_PROF("assign_stats", st);
             k_stats_global<<<(int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, kSMs * 8)),
-                             256, 0, st>>>(reinterpret_cast<const double2*>(d_pts), d_len, n, d_labels,
+                             256, 0, st>>>(pv, d_len, n, d_labels,
                                            (int)k, Ex, Ey, Bx, By, acc.p);
         }
         JB_LAUNCH_CHECK();
@@ -487,7 +500,7 @@ void assign_and_stats(const double* d_pts, const int32_t* d_len, int64_t n,
                              (int64_t)kSMs * std::max(per_sm, 1)));
     if (n > 0) {
         JB_PROF("assign_stats", st);
-        k_assign_stats<<<grid, AS_TB, smem, st>>>(reinterpret_cast<const double2*>(d_pts), d_len, n,
+        k_assign_stats<<<grid, AS_TB, smem, st>>>(pv, d_len, n,
                                                   dc.p, (int)k, do_assign ? 1 : 0, d_labels, Ex, Ey,
                                                   Bx, By, acc.p, cg, rg, RH);
     }

@@ -164,7 +164,7 @@ struct Pieces {
     DArr<double> inc;
     DArr<int64_t> seg_offsets;  // n_seg + 1
     double max_abs_inc = 0.0;
-    int32_t max_len = 0;
+    int32_t max_len = 0, min_len = 0;
 };
 
 // Compresses every segment (compression.hpp:31-83, 167-193) with the
@@ -176,17 +176,35 @@ void compress_segments(const double* d_values, const SegTable& seg, double tol,
 // ---------------------------------------------------------------------------
 // Scaling (digitize.cu): scale_pieces digitization.hpp:25-59
 
+// The scaled points (x, y) = (scl * len / sigma_len, inc / sigma_inc)
+// (ScalingParams::apply core.hpp:130-132, k_scale's exact expressions),
+// either materialised or computed where they are read.
+struct PtsView {
+    const double2* pts = nullptr;  // materialised, or null: from len / inc
+    const int32_t* len = nullptr;
+    const double* inc = nullptr;
+    double scl = 1.0, sl = 1.0, si = 1.0;
+    __host__ __device__ __forceinline__ double2 at(uint64_t i) const {
+        if (pts) return pts[i];
+        return make_double2(scl * (double)len[i] / sl, inc[i] / si);
+    }
+};
+
 struct Scaled {
-    DArr<double> pts;  // 2N interleaved (x, y) (this rank's pieces)
+    DArr<double> pts;  // 2N interleaved (x, y): only when a backend needs them (GA)
     double scl = 1.0, sigma_len = 1.0, sigma_inc = 1.0;
     double xmin = 0, xmax = 0, ymin = 0, ymax = 0;  // bounding box of ALL points
     int64_t N_global = 0;
     int32_t max_len_global = 0;
 };
 
-// total_steps: of ALL ranks' segments; cm: null or world == 1 for one GPU
+// total_steps: of ALL ranks' segments; cm: null or world == 1 for one GPU.
+// Computes sigma and the bounding box; the points stay virtual.
 void scale_pieces(const Pieces& pc, int64_t total_steps, double scl, Scaled& out,
                   cudaStream_t st, const Comm* cm = nullptr);
+PtsView points_view(const Pieces& pc, const Scaled& sc);
+// materialises sc.pts (GA backends sort and sweep the points many times)
+void materialize_points(const Pieces& pc, Scaled& sc, cudaStream_t st);
 
 struct BBox {
     double xmin, xmax, ymin, ymax;
@@ -230,7 +248,7 @@ struct PieceRows {
 // d_pts[d_idx[i]] (or d_pts[i] when d_idx is null), i < n; 2-interleaved
 // device doubles. Draws are consumed from d_raw starting at *cursor (updated).
 // out.labels are in the original point order.
-void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, uint64_t k,
+void lloyd_best_device(const PtsView& pv, const uint64_t* d_idx, int64_t n, uint64_t k,
                        uint64_t max_iters, uint64_t n_init, const uint64_t* d_raw,
                        uint64_t raw_count, uint64_t* cursor, const BBox& bb, KMeansOut& out,
                        cudaStream_t st, const PieceRows& rows = PieceRows{});
@@ -239,7 +257,7 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
 // piece index d_lidx[i] and global sample position d_gpos[i] (ascending), n
 // entries -- of a global sample of S points. Same results on every rank,
 // equal to lloyd_best_device on the whole sample.
-void lloyd_best_dist(const Comm& cm, const double* d_pts, const uint64_t* d_lidx,
+void lloyd_best_dist(const Comm& cm, const PtsView& pv, const uint64_t* d_lidx,
                      const uint32_t* d_gpos, int64_t n, uint64_t S, uint64_t k, uint64_t max_iters,
                      uint64_t n_init, const uint64_t* d_raw, uint64_t raw_count, uint64_t* cursor,
                      const BBox& bb, KMeansOut& out, cudaStream_t st,
@@ -251,7 +269,7 @@ struct GroupStats {
     std::vector<uint64_t> counts, first_seen, len_sums;
     std::vector<double> sum_x, sum_y;  // rounded exact sums
 };
-void assign_and_stats(const double* d_pts, const int32_t* d_len, int64_t n,
+void assign_and_stats(const PtsView& pv, const int32_t* d_len, int64_t n,
                       const std::vector<double>& centers, uint64_t k, const BBox& bb,
                       bool do_assign, uint32_t* d_labels, GroupStats& gs, cudaStream_t st,
                       int32_t max_len, double scl, double sigma_len, const Comm* cm = nullptr,

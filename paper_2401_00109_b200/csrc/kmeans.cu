@@ -443,7 +443,7 @@ __device__ __forceinline__ double2 load_pt(const double2* __restrict__ pts,
 // Morton keys of the sample points; also gathers the points (and their
 // piece lengths) into sample order, so the sorted gather reads a compact
 // array instead of chasing idx into the full point array again.
-__global__ void k_morton(const double2* __restrict__ pts, const uint64_t* __restrict__ idx,
+__global__ void k_morton(const PtsView pv, const uint64_t* __restrict__ idx,
                          int64_t n, double x0, double sx, double y0, double sy,
                          uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
                          double2* __restrict__ cpts, const int32_t* __restrict__ len,
@@ -451,7 +451,7 @@ __global__ void k_morton(const double2* __restrict__ pts, const uint64_t* __rest
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t src = idx ? idx[i] : (uint64_t)i;
-        const double2 p = pts[src];
+        const double2 p = pv.at(src);
         cpts[i] = p;
         if (len) clen[i] = len[src];
         const uint32_t qx = (uint32_t)fmin(fmax((p.x - x0) * sx, 0.0), 65535.0);
@@ -1463,7 +1463,7 @@ void lloyd_update_means_sync(LloydCtx& L) {
 
 }  // namespace
 
-void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, uint64_t k,
+void lloyd_best_device(const PtsView& pv, const uint64_t* d_idx, int64_t n, uint64_t k,
                        uint64_t max_iters, uint64_t n_init, const uint64_t* d_raw,
                        uint64_t raw_count, uint64_t* cursor, const BBox& bb, KMeansOut& out,
                        cudaStream_t st, const PieceRows& rows) {
@@ -1471,7 +1471,6 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
     if ((int64_t)k > n) throw Error(INVALID_INPUT, "d2_seed: k exceeds points");
     if (k > 2048) throw Error(INVALID_INPUT, "k > 2048 is not supported by the Lloyd kernel");
     if (n >= (1LL << 32)) throw Error(INVALID_INPUT, "k-means on more than 2^32 points");
-    const double2* pts = reinterpret_cast<const double2*>(d_pts);
     const double mx = std::max(std::fabs(bb.xmin), std::fabs(bb.xmax));
     const double my = std::max(std::fabs(bb.ymin), std::fabs(bb.ymax));
     const double wx = bb.xmax - bb.xmin, wy = bb.ymax - bb.ymin;
@@ -1487,7 +1486,7 @@ void lloyd_best_device(const double* d_pts, const uint64_t* d_idx, int64_t n, ui
         const double sx = wx > 0 ? 65535.0 / wx : 0.0, sy = wy > 0 ? 65535.0 / wy : 0.0;
         DArr<double2> cpts(n, st);
         DArr<int32_t> clen(rows.len ? n : 0, st);
-        k_morton<<<grid_cap(n), 256, 0, st>>>(pts, d_idx, n, bb.xmin, sx, bb.ymin, sy, keys.p,
+        k_morton<<<grid_cap(n), 256, 0, st>>>(pv, d_idx, n, bb.xmin, sx, bb.ymin, sy, keys.p,
                                               vals.p, cpts.p, rows.len, clen.p);
         JB_LAUNCH_CHECK();
         size_t tb = 0;
@@ -1838,7 +1837,7 @@ struct FarRec {
 
 }  // namespace
 
-void lloyd_best_dist(const Comm& cm, const double* d_pts, const uint64_t* d_lidx,
+void lloyd_best_dist(const Comm& cm, const PtsView& pv, const uint64_t* d_lidx,
                      const uint32_t* d_gpos, int64_t n, uint64_t S, uint64_t k, uint64_t max_iters,
                      uint64_t n_init, const uint64_t* d_raw, uint64_t raw_count, uint64_t* cursor,
                      const BBox& bb, KMeansOut& out, cudaStream_t st, const PieceRows& rows) {
@@ -1846,7 +1845,6 @@ void lloyd_best_dist(const Comm& cm, const double* d_pts, const uint64_t* d_lidx
     if (k > S) throw Error(INVALID_INPUT, "d2_seed: k exceeds points");
     if (k > 2048) throw Error(INVALID_INPUT, "k > 2048 is not supported by the Lloyd kernel");
     if (S >= (1ULL << 32)) throw Error(INVALID_INPUT, "k-means on more than 2^32 points");
-    const double2* pts = reinterpret_cast<const double2*>(d_pts);
     const double mx = std::max(std::fabs(bb.xmin), std::fabs(bb.xmax));
     const double my = std::max(std::fabs(bb.ymin), std::fabs(bb.ymax));
     const double wx = bb.xmax - bb.xmin, wy = bb.ymax - bb.ymin;
@@ -1863,7 +1861,7 @@ void lloyd_best_dist(const Comm& cm, const double* d_pts, const uint64_t* d_lidx
         const double sx = wx > 0 ? 65535.0 / wx : 0.0, sy = wy > 0 ? 65535.0 / wy : 0.0;
         DArr<double2> cpts(n, st);
         DArr<int32_t> clen(rows.len ? n : 0, st);
-        k_morton<<<grid_cap(n), 256, 0, st>>>(pts, d_lidx, n, bb.xmin, sx, bb.ymin, sy, keys.p,
+        k_morton<<<grid_cap(n), 256, 0, st>>>(pv, d_lidx, n, bb.xmin, sx, bb.ymin, sy, keys.p,
                                               vals.p, cpts.p, rows.len, clen.p);
         JB_LAUNCH_CHECK();
         size_t tb = 0;
@@ -1995,8 +1993,17 @@ void lloyd_best_dist(const Comm& cm, const double* d_pts, const uint64_t* d_lidx
                 double2 p;
                 JB_CUDA(cudaMemcpyAsync(&li, d_lidx + i, 8, cudaMemcpyDeviceToHost, st));
                 JB_CUDA(cudaStreamSynchronize(st));
-                JB_CUDA(cudaMemcpyAsync(&p, pts + li, 16, cudaMemcpyDeviceToHost, st));
-                JB_CUDA(cudaStreamSynchronize(st));
+                if (pv.pts) {
+                    JB_CUDA(cudaMemcpyAsync(&p, pv.pts + li, 16, cudaMemcpyDeviceToHost, st));
+                    JB_CUDA(cudaStreamSynchronize(st));
+                } else {  // the point from its piece (k_scale's expressions, host IEEE)
+                    int32_t L;
+                    double I;
+                    JB_CUDA(cudaMemcpyAsync(&L, pv.len + li, 4, cudaMemcpyDeviceToHost, st));
+                    JB_CUDA(cudaMemcpyAsync(&I, pv.inc + li, 8, cudaMemcpyDeviceToHost, st));
+                    JB_CUDA(cudaStreamSynchronize(st));
+                    p = make_double2(pv.scl * (double)L / pv.sl, I / pv.si);
+                }
                 rec = Rec{1, p.x, p.y};
             }
         }
