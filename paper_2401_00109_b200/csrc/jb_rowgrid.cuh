@@ -53,7 +53,7 @@ constexpr int kRowSeg = kBuildTB;  // y cells per CTA block, one thread per cell
 
 // one CTA per (length, kRowSeg y cells) segment; blocks: the segments to
 // build (null: all of them)
-static __global__ void __launch_bounds__(kBuildTB) k_row_grid_build(RowGrid g,
+__device__ __forceinline__ void row_grid_build_body(RowGrid g,
                                                                     const double* centers,
                                                                     int k, const int* __restrict__ blocks,
                                                                     int nblocks) {
@@ -88,6 +88,13 @@ static __global__ void __launch_bounds__(kBuildTB) k_row_grid_build(RowGrid g,
         }
         __syncthreads();
     }
+}
+
+static __global__ void __launch_bounds__(kBuildTB) k_row_grid_build(RowGrid g,
+                                                                    const double* centers,
+                                                                    int k, const int* __restrict__ blocks,
+                                                                    int nblocks) {
+    row_grid_build_body(g, centers, k, blocks, nblocks);
 }
 
 inline int row_grid_segments(const RowGrid& g) { return g.R * ((g.Gy + kRowSeg - 1) / kRowSeg); }

@@ -34,6 +34,8 @@
 #include "jb_grid.cuh"
 #include "jb_rowgrid.cuh"
 
+#include <cooperative_groups.h>
+
 namespace jb {
 
 namespace {
@@ -959,7 +961,7 @@ __device__ __forceinline__ uint32_t box_single(const double4& b, int l, const Ca
 // time holds that label on all its points (its state is reset to MIXED
 // whenever a point of it is relabeled outside this scheme, k_repair): it is
 // skipped. The others are listed for k_lloyd_work. State: tlab[ntiles + s].
-__global__ void k_super_check(const double4* __restrict__ sbox, const int32_t* __restrict__ slenc,
+__device__ __forceinline__ void super_check_body(const double4* __restrict__ sbox, const int32_t* __restrict__ slenc,
                               int64_t ntiles, CandGrid g, const double* centers,
                               uint32_t* __restrict__ tlab, uint32_t* __restrict__ swork,
                               unsigned long long* __restrict__ nswork,
@@ -993,10 +995,19 @@ __global__ void k_super_check(const double4* __restrict__ sbox, const int32_t* _
     }
 }
 
+__global__ void k_super_check(const double4* __restrict__ sbox, const int32_t* __restrict__ slenc,
+                              int64_t ntiles, CandGrid g, const double* centers,
+                              uint32_t* __restrict__ tlab, uint32_t* __restrict__ swork,
+                              unsigned long long* __restrict__ nswork,
+                              const int* __restrict__ skip_flag, int force_all, RowGrid rg,
+                              int k) {
+    super_check_body(sbox, slenc, ntiles, g, centers, tlab, swork, nswork, skip_flag, force_all, rg, k);
+}
+
 // Tiles of the listed super-tiles (warp per super-tile, lane per tile): the
 // tiles whose single-center state changed or is MIXED are listed for
 // k_lloyd_work with their new state in tnew.
-__global__ void k_tile_expand(const uint32_t* __restrict__ swork,
+__device__ __forceinline__ void tile_expand_body(const uint32_t* __restrict__ swork,
                               const unsigned long long* __restrict__ nswork,
                               const double4* __restrict__ tbox, const int32_t* __restrict__ tlen,
                               int64_t ntiles, CandGrid g, const double* centers,
@@ -1027,6 +1038,17 @@ __global__ void k_tile_expand(const uint32_t* __restrict__ swork,
         base = __shfl_sync(0xffffffffu, base, 0);
         if (add) work[base + __popc(am & ((1u << lane) - 1u))] = (uint32_t)t;
     }
+}
+
+__global__ void k_tile_expand(const uint32_t* __restrict__ swork,
+                              const unsigned long long* __restrict__ nswork,
+                              const double4* __restrict__ tbox, const int32_t* __restrict__ tlen,
+                              int64_t ntiles, CandGrid g, const double* centers,
+                              const uint32_t* __restrict__ tlab, uint32_t* __restrict__ tnew,
+                              uint32_t* __restrict__ work, unsigned long long* __restrict__ nwork,
+                              const int* __restrict__ skip_flag, int force_all, RowGrid rg,
+                              int k) {
+    tile_expand_body(swork, nswork, tbox, tlen, ntiles, g, centers, tlab, tnew, work, nwork, skip_flag, force_all, rg, k);
 }
 
 // super-tile boxes and common lengths (32 tiles each)
@@ -1067,7 +1089,7 @@ __global__ void k_super_boxes(const double4* __restrict__ tbox, const int32_t* _
 // ones move few points, so each (old, new) label group of a warp adds its
 // deltas straight to the global accumulators (native 64-bit atomics in L2).
 template <bool FULL>
-__global__ void __launch_bounds__(LL_TB) k_lloyd_work(
+__device__ __forceinline__ void lloyd_work_body(
     const double2* __restrict__ spts, int64_t n, const double* __restrict__ centers, int k,
     CandGrid g, uint32_t* __restrict__ labs, const uint32_t* __restrict__ work,
     const unsigned long long* __restrict__ nwork, const uint32_t* __restrict__ tnew,
@@ -1165,9 +1187,20 @@ __global__ void __launch_bounds__(LL_TB) k_lloyd_work(
     if (threadIdx.x == 0 && s_changed) atomicAdd(changed, s_changed);
 }
 
+template <bool FULL>
+__global__ void __launch_bounds__(LL_TB) k_lloyd_work(
+    const double2* __restrict__ spts, int64_t n, const double* __restrict__ centers, int k,
+    CandGrid g, uint32_t* __restrict__ labs, const uint32_t* __restrict__ work,
+    const unsigned long long* __restrict__ nwork, const uint32_t* __restrict__ tnew,
+    uint32_t* __restrict__ tlab, int Ex, int Ey, ClusterAcc acc,
+    unsigned long long* __restrict__ changed, const int* __restrict__ skip_flag, RowGrid rg,
+    const int32_t* __restrict__ slen) {
+    lloyd_work_body<FULL>(spts, n, centers, k, g, labs, work, nwork, tnew, tlab, Ex, Ey, acc, changed, skip_flag, rg, slen);
+}
+
 // centers[c] = sums[c] / counts[c] for non-empty clusters (update_means
 // :177-180); reports the empty clusters in index order.
-__global__ void __launch_bounds__(256) k_means(ClusterAcc acc, int k, int Ex, int Ey,
+__device__ __forceinline__ void means_body(ClusterAcc acc, int k, int Ex, int Ey,
                                                double* __restrict__ centers,
                                                int* __restrict__ empties, int* __restrict__ n_empty,
                                                const int* __restrict__ gate) {
@@ -1205,6 +1238,13 @@ __global__ void __launch_bounds__(256) k_means(ClusterAcc acc, int k, int Ex, in
         __syncthreads();
     }
     if (threadIdx.x == 0) *n_empty = base;
+}
+
+__global__ void __launch_bounds__(256) k_means(ClusterAcc acc, int k, int Ex, int Ey,
+                                               double* __restrict__ centers,
+                                               int* __restrict__ empties, int* __restrict__ n_empty,
+                                               const int* __restrict__ gate) {
+    means_body(acc, k, Ex, Ey, centers, empties, n_empty, gate);
 }
 
 // farthest point among clusters with count > 1 (update_means :183-192):
@@ -1366,7 +1406,7 @@ struct LloydCtx {
 // end of one batched Lloyd iteration (lloyd_once :209-213): ++iterations,
 // stop when no label changed; resets the per-iteration counters. Gated like
 // the other kernels, so iterations launched past convergence are no-ops.
-__global__ void k_iter_end(int* __restrict__ state, unsigned long long* __restrict__ changed,
+__device__ __forceinline__ void iter_end_body(int* __restrict__ state, unsigned long long* __restrict__ changed,
                            unsigned long long* __restrict__ nwork,
                            unsigned long long* __restrict__ nswork,
                            unsigned long long* __restrict__ diag) {
@@ -1379,6 +1419,13 @@ __global__ void k_iter_end(int* __restrict__ state, unsigned long long* __restri
     *changed = 0;
     *nwork = 0;
     *nswork = 0;
+}
+
+__global__ void k_iter_end(int* __restrict__ state, unsigned long long* __restrict__ changed,
+                           unsigned long long* __restrict__ nwork,
+                           unsigned long long* __restrict__ nswork,
+                           unsigned long long* __restrict__ diag) {
+    iter_end_body(state, changed, nwork, nswork, diag);
 }
 
 void lloyd_assign(LloydCtx& L, bool full, bool gate_on_empties) {
@@ -1419,6 +1466,121 @@ void lloyd_means(LloydCtx& L, bool gated) {
     k_means<<<1, 256, 0, L.st>>>(L.cacc(), L.k, L.Ex, L.Ey, L.centers.p, L.empties.p,
                                   L.empties.p + L.k, gated ? L.empties.p + L.k : nullptr);
     JB_LAUNCH_CHECK();
+}
+
+// Persistent Lloyd loop (single GPU, row grid in use): every phase of an
+// iteration -- update_means (block 0), row-grid rebuild, super-tile check,
+// tile expansion, re-assignment, iteration end (block 0) -- runs in ONE
+// cooperative launch separated by grid-wide barriers, for up to `budget`
+// iterations, stopping at convergence or when update_means reports empty
+// clusters (re-seeded on the host path). Same phase bodies as the
+// multi-kernel path, so the same arithmetic.
+struct PersistArgs {
+    ClusterAcc acc;
+    int k, Ex, Ey;
+    double* centers;
+    int* empties;  // k entries, then state: n_empty | converged | iterations
+    RowGrid rg;
+    const int* rg_blocks;
+    int rg_nblocks;
+    const double4* sbox;
+    const int32_t* slenc;
+    int64_t ntiles;
+    CandGrid cg;
+    uint32_t* tlab;
+    uint32_t* swork;
+    unsigned long long* nswork;
+    const double4* tbox;
+    const int32_t* tlen;
+    uint32_t* tnew;
+    uint32_t* work;
+    unsigned long long* nwork;
+    const double2* spts;
+    int64_t n;
+    uint32_t* labs;
+    unsigned long long* changed;
+    const int32_t* slen;
+    unsigned long long* diag;
+    int budget;
+};
+
+__global__ void __launch_bounds__(256) k_lloyd_persistent(PersistArgs a) {
+    namespace cgx = cooperative_groups;
+    cgx::grid_group grid = cgx::this_grid();
+    int* state = a.empties + a.k;
+    for (int b = 0; b < a.budget; ++b) {
+        if (blockIdx.x == 0) means_body(a.acc, a.k, a.Ex, a.Ey, a.centers, a.empties, state, state);
+        grid.sync();
+        if (((volatile int*)state)[0] | ((volatile int*)state)[1]) break;
+        row_grid_build_body(a.rg, a.centers, a.k, a.rg_blocks, a.rg_nblocks);
+        grid.sync();
+        super_check_body(a.sbox, a.slenc, a.ntiles, a.cg, a.centers, a.tlab, a.swork, a.nswork,
+                         nullptr, 0, a.rg, a.k);
+        grid.sync();
+        tile_expand_body(a.swork, a.nswork, a.tbox, a.tlen, a.ntiles, a.cg, a.centers, a.tlab,
+                         a.tnew, a.work, a.nwork, nullptr, 0, a.rg, a.k);
+        grid.sync();
+        lloyd_work_body<false>(a.spts, a.n, a.centers, a.k, a.cg, a.labs, a.work, a.nwork, a.tnew,
+                               a.tlab, a.Ex, a.Ey, a.acc, a.changed, nullptr, a.rg, a.slen);
+        grid.sync();
+        if (blockIdx.x == 0) {
+            if (threadIdx.x == 0) iter_end_body(state, a.changed, a.nwork, a.nswork, a.diag);
+            __syncthreads();
+        }
+    }
+}
+
+// the persistent loop applies when the row grid carries the assignment
+// (no 2-D grid) and the device can co-schedule the grid
+bool lloyd_persistent(LloydCtx& L, int budget) {
+    if (L.rg.R == 0 || L.cg.G != 0 || L.n == 0 || dbg_on()) return false;
+    static int coop = -1;
+    if (coop < 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    }
+    if (!coop) return false;
+    const size_t smem = sizeof(double) * 2 * L.k;
+    JB_CUDA(cudaFuncSetAttribute(k_lloyd_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    int per_sm = 0;
+    JB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lloyd_persistent, 256, smem));
+    if (per_sm < 1) return false;
+    PersistArgs a;
+    a.acc = L.cacc();
+    a.k = L.k;
+    a.Ex = L.Ex;
+    a.Ey = L.Ey;
+    a.centers = L.centers.p;
+    a.empties = L.empties.p;
+    a.rg = L.rg;
+    a.rg_blocks = L.rg_blocks.p;
+    a.rg_nblocks = L.rg_nblocks;
+    a.sbox = L.sbox.p;
+    a.slenc = L.slenc.p;
+    a.ntiles = L.ntiles;
+    a.cg = L.cg;
+    a.tlab = L.tlab.p;
+    a.swork = L.swork.p;
+    a.nswork = L.nswork.p;
+    a.tbox = L.tbox;
+    a.tlen = L.tlen;
+    a.tnew = L.tnew.p;
+    a.work = L.work.p;
+    a.nwork = L.nwork.p;
+    a.spts = L.spts;
+    a.n = L.n;
+    a.labs = L.labs.p;
+    a.changed = L.flags.p;
+    a.slen = L.slen;
+    a.diag = L.diag.p;
+    a.budget = budget;
+    void* args[] = {&a};
+    JB_PROF("lloyd_persistent", L.st);
+    JB_CUDA(cudaLaunchCooperativeKernel((const void*)k_lloyd_persistent, dim3(kSMs * per_sm),
+                                        dim3(256), args, smem, L.st));
+    return true;
 }
 
 struct LoopState {
@@ -1657,12 +1819,14 @@ void lloyd_best_device(const PtsView& pv, const uint64_t* d_idx, int64_t n, uint
         const uint64_t kBatch = dbg_on() ? 1 : 16;
         while (it < max_iters) {
             const uint64_t B = std::min<uint64_t>(kBatch, max_iters - it);
-            for (uint64_t b = 0; b < B; ++b) {
-                lloyd_means(L, true);          // update_means ...
-                lloyd_assign(L, false, true);  // ... assign_all, label comparison
-                k_iter_end<<<1, 1, 0, st>>>(L.empties.p + L.k, L.flags.p, L.nwork.p, L.nswork.p,
-                                            L.diag.p);
-                JB_LAUNCH_CHECK();
+            if (!lloyd_persistent(L, (int)std::min<uint64_t>(max_iters - it, 1u << 30))) {
+                for (uint64_t b = 0; b < B; ++b) {
+                    lloyd_means(L, true);          // update_means ...
+                    lloyd_assign(L, false, true);  // ... assign_all, label comparison
+                    k_iter_end<<<1, 1, 0, st>>>(L.empties.p + L.k, L.flags.p, L.nwork.p,
+                                                L.nswork.p, L.diag.p);
+                    JB_LAUNCH_CHECK();
+                }
             }
             LoopState h = lloyd_state(L);
             it = (uint64_t)h.iters;
