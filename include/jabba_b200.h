@@ -10,6 +10,8 @@
  *                               + digitize digitization.hpp:207-293)
  *   jb_inverse_transform  <- jabba::reconstruct(const SymbolicResult&)        inverse.hpp:127-132
  *   jb_fit_inverse_transform  same, on a device-resident fit (no host copy)
+ *   jb_symbolize_with     <- jabba::symbolize_with(const Codebook&, const PieceSequence&)
+ *                                                                             digitization.hpp:297-307
  *   jb_plan_segments      <- Dataset::partitioned/multivariate/collection     core.hpp:73-98
  *                            + detail::split_series                           compression.hpp:140-160
  *   jb_config             <- JabbaConfig jabba.hpp:17-21, CompressionConfig compression.hpp:18-26,
@@ -163,6 +165,16 @@ jb_status jb_inverse_transform(jb_context* ctx, const double* centers,
                                const uint32_t* labels, const int64_t* piece_offsets,
                                const double* anchors, const int64_t* source_lengths,
                                int64_t n_seg, int32_t layout, double* out_values);
+
+/* symbolize_with: labels of n held-out pieces (len, inc) against a codebook
+ * (centers 2k interleaved, scaling {scl, sigma_len, sigma_inc}):
+ * Codebook::nearest(ScalingParams::apply(piece)), lowest index on ties
+ * (core.hpp:130-132, 147-160). pieces_on_device != 0: len/inc/labels are
+ * device pointers on the context's GPU; else host pointers. k == 0 ->
+ * JB_INVALID_INPUT ("symbolize_with: empty codebook"). */
+jb_status jb_symbolize_with(jb_context* ctx, const double* centers, uint64_t k,
+                            const double* scaling, const int64_t* len, const double* inc,
+                            int64_t n, int32_t pieces_on_device, uint32_t* labels);
 
 /* ---- Joint fit sharded over ranks (one process per GPU) -----------------
  * Every rank passes ITS contiguous range of the global segment table (and a

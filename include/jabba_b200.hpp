@@ -189,4 +189,31 @@ inline std::vector<jabba::TimeSeries> inverse_transform(const jabba::SymbolicRes
     return res;
 }
 
+// jabba::symbolize_with (digitization.hpp:297-307) on the GPU.
+inline jabba::SymbolicResult::Series symbolize_with(const jabba::Codebook& codebook,
+                                                    const jabba::PieceSequence& seq) {
+    if (codebook.size() == 0) throw jabba::invalid_input("symbolize_with: empty codebook");
+    std::vector<double> centers;
+    for (const auto& c : codebook.centers) {
+        centers.push_back(c[0]);
+        centers.push_back(c[1]);
+    }
+    const double scaling[3] = {codebook.scaling.scl, codebook.scaling.sigma_len,
+                               codebook.scaling.sigma_inc};
+    std::vector<int64_t> len;
+    std::vector<double> inc;
+    for (const auto& p : seq.pieces) {
+        len.push_back(p.len);
+        inc.push_back(p.inc);
+    }
+    jabba::SymbolicResult::Series s;
+    s.id = seq.source_id;
+    s.anchor = seq.anchor;
+    s.source_length = seq.source_length;
+    s.labels.resize(len.size());
+    check(jb_symbolize_with(context(), centers.data(), (uint64_t)codebook.size(), scaling,
+                            len.data(), inc.data(), (int64_t)len.size(), 0, s.labels.data()));
+    return s;
+}
+
 }  // namespace jabba_b200

@@ -140,6 +140,28 @@ int main() {
         cfg.compression.max_piece_len = 7;
         compare("random walk 2e5 svq max_piece_len 7", Dataset::partitioned(rw, 16), cfg);
     }
+    // symbolize_with (digitization.hpp:297-307): held-out pieces against a
+    // fitted codebook, as test_io.cpp:108-116 / acceptance.cpp:368 use it
+    for (Backend b : {Backend::vq, Backend::sampling_vq, Backend::ga}) {
+        JabbaConfig cfg;
+        cfg.compression.tol = 0.2;
+        cfg.digitize.backend = b;
+        cfg.digitize.vq.k = 16;
+        cfg.digitize.vq.r = 0.5;
+        cfg.digitize.ga.alpha = 0.3;
+        const JabbaFit fit = jabba_fit(Dataset::partitioned(oracle::walk(20000, 5), 4), cfg);
+        const PieceSequence held = compress(oracle::walk(30000, 99), {0.2, 0});
+        const auto ref = symbolize_with(fit.symbolic.codebook, held);
+        const auto got = jabba_b200::symbolize_with(fit.symbolic.codebook, held);
+        const bool same_labels = got.labels == ref.labels;
+        const bool ok = same_labels && got.anchor == ref.anchor &&
+                        got.source_length == ref.source_length;
+        report(std::string("symbolize_with held-out walk, ") + to_string(b) + " codebook", ok,
+               ok ? "" : (same_labels ? "metadata" : "labels"));
+    }
+    expect_throw<invalid_input>("symbolize_with: empty codebook", [] {
+        jabba_b200::symbolize_with(Codebook{}, compress(oracle::walk(100, 3), {0.2, 0}));
+    });
     // error classes at the reference's call sites
     expect_throw<invalid_partition>("oversized partition count", [] {
         jabba_b200::fit_transform(Dataset::partitioned(TimeSeries{{0, 1, 2, 3}, "tiny"}, 4),

@@ -953,6 +953,30 @@ int jo_inverse_compress(const int64_t* len, const double* inc, int64_t n, double
     return JO_OK;
 }
 
+/* symbolize_with digitization.hpp:297-307: ScalingParams::apply core.hpp:130-132,
+ * Codebook::nearest core.hpp:147-160 (dx = center - q, strict <, lowest index) */
+int jo_symbolize_with(const double* centers, uint64_t k, const double* scaling,
+                      const int64_t* len, const double* inc, int64_t n, uint32_t* labels) {
+    if (k == 0) return fail(JO_INVALID_INPUT, "symbolize_with: empty codebook");
+    for (int64_t i = 0; i < n; ++i) {
+        const double qx = scaling[0] * (double)len[i] / scaling[1];
+        const double qy = inc[i] / scaling[2];
+        uint64_t best = 0;
+        double best_d = INFINITY;
+        for (uint64_t c = 0; c < k; ++c) {
+            const double dx = centers[2 * c] - qx;
+            const double dy = centers[2 * c + 1] - qy;
+            const double d = dx * dx + dy * dy;
+            if (d < best_d) {
+                best_d = d;
+                best = c;
+            }
+        }
+        labels[i] = (uint32_t)best;
+    }
+    return JO_OK;
+}
+
 int64_t jo_reconstruct_size(const int64_t* source_lengths, int64_t n_seg, int32_t layout) {
     int64_t t = 0;
     for (int64_t s = 0; s < n_seg; ++s) t += source_lengths[s] + 1;

@@ -97,6 +97,9 @@ int jo_compress(const double* values, const int64_t* seg_first, const int64_t* s
 /* reconstruct (inverse.hpp:127-132). Output: univariate-partitioned ->
  * stitched single series of sum(steps)+1 values; else per-segment
  * (steps+1) values concatenated. out_values must hold jo_reconstruct_size(). */
+/* symbolize_with (digitization.hpp:297-307) of n pieces against a codebook */
+int jo_symbolize_with(const double* centers, uint64_t k, const double* scaling,
+                      const int64_t* len, const double* inc, int64_t n, uint32_t* labels);
 int64_t jo_reconstruct_size(const int64_t* source_lengths, int64_t n_seg, int32_t layout);
 int jo_reconstruct(const double* centers, const double* mean_lengths, uint64_t k,
                    const double* scaling, const uint32_t* labels, const int64_t* piece_offsets,

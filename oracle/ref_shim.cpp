@@ -177,6 +177,29 @@ int jref_reconstruct(const double* centers, const double* mean_lengths, uint64_t
     }
 }
 
+// symbolize_with (digitization.hpp:297-307) through the reference's own code
+int jref_symbolize_with(const double* centers, uint64_t k, const double* scaling,
+                        const int64_t* len, const double* inc, int64_t n, uint32_t* labels) {
+    try {
+        jabba::Codebook cb;
+        cb.scaling.scl = scaling[0];
+        cb.scaling.sigma_len = scaling[1];
+        cb.scaling.sigma_inc = scaling[2];
+        for (uint64_t g = 0; g < k; ++g) {
+            cb.centers.push_back({centers[2 * g], centers[2 * g + 1]});
+            cb.mean_lengths.push_back(1.0);
+            cb.symbols.push_back(jabba::symbol_token(g, k));
+        }
+        jabba::PieceSequence seq;
+        for (int64_t i = 0; i < n; ++i) seq.pieces.push_back(jabba::Piece{len[i], inc[i]});
+        const auto s = jabba::symbolize_with(cb, seq);
+        std::memcpy(labels, s.labels.data(), sizeof(uint32_t) * s.labels.size());
+        return 0;
+    } catch (const std::exception& e) {
+        return map_error(e);
+    }
+}
+
 // --- building blocks, for pinning the restatement ---
 
 void jref_mt_stream(uint64_t seed, uint64_t count, uint64_t* out) {

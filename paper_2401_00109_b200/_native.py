@@ -25,7 +25,7 @@ EXPORTS = [
     "jb_fit_inverse_transform", "jb_reconstruct_size", "jb_inverse_transform",
     "jb_symbol_token", "jb_profile_enable", "jb_profile_reset", "jb_profile_read",
     "jb_probe_fp64_tflops", "jb_mt19937_64_stream", "jb_sample_indices",
-    "jb_fit_transform_dist",
+    "jb_fit_transform_dist", "jb_symbolize_with",
 ]
 
 # int32_t (*allgather)(void* user, const void* send, uint64_t bytes, void* recv)
@@ -90,6 +90,9 @@ def lib() -> C.CDLL:
     L.jb_reconstruct_size.restype = C.c_int64
     L.jb_inverse_transform.argtypes = [vp, f64p, f64p, C.c_uint64, f64p, u32p, i64p, f64p, i64p,
                                        C.c_int64, C.c_int32, vp]
+    L.jb_symbolize_with.argtypes = [vp, f64p, C.c_uint64, f64p, vp, vp, C.c_int64, C.c_int32,
+                                    vp]
+    L.jb_symbolize_with.restype = C.c_int
     L.jb_symbol_token.argtypes = [C.c_uint64, C.c_uint64, C.c_char_p]
     L.jb_symbol_token.restype = C.c_int32
     L.jb_profile_enable.argtypes = [C.c_int32]

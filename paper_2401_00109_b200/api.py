@@ -481,6 +481,24 @@ class Engine:
             sl, len(sl), int(layout), out.ctypes.data))
         return out[:n]
 
+    def symbolize_arrays(self, centers, scaling, lens, incs, device_ptrs=None) -> np.ndarray:
+        """symbolize_with (digitization.hpp:297-307) on the GPU: labels of the
+        pieces (lens, incs) against the codebook (centers (k, 2), scaling).
+        device_ptrs = (len_i64_ptr, inc_ptr, labels_ptr, n): device arrays."""
+        cen = np.ascontiguousarray(centers, np.float64).reshape(-1)
+        sc = np.ascontiguousarray(scaling, np.float64)
+        if device_ptrs is not None:
+            lp, ip, op, n = device_ptrs
+            _check(N.lib().jb_symbolize_with(self.ctx, cen, len(cen) // 2, sc, C.c_void_p(lp),
+                                             C.c_void_p(ip), int(n), 1, C.c_void_p(op)))
+            return None
+        lens = np.ascontiguousarray(lens, np.int64)
+        incs = np.ascontiguousarray(incs, np.float64)
+        out = np.empty(max(len(lens), 1), np.uint32)
+        _check(N.lib().jb_symbolize_with(self.ctx, cen, len(cen) // 2, sc, lens.ctypes.data,
+                                         incs.ctypes.data, len(lens), 0, out.ctypes.data))
+        return out[: len(lens)]
+
 
 # ---------------------------------------------------------------------------
 # multi-GPU: one joint fit sharded over ranks (jb_fit_transform_dist)
@@ -655,3 +673,19 @@ def reconstruct(symbolic: SymbolicResult, engine: Optional[Engine] = None) -> Li
 
 
 inverse_transform = reconstruct
+
+
+def symbolize_with(codebook: Codebook, seq: PieceSequence,
+                   engine: Optional[Engine] = None) -> SymbolicSeries:
+    """symbolize_with (digitization.hpp:297-307): held-out pieces against a
+    fitted codebook, on the GPU (Codebook::nearest of ScalingParams::apply,
+    lowest index on ties)."""
+    eng = engine or default_engine()
+    if codebook.size() == 0:
+        raise InvalidInput("symbolize_with: empty codebook")
+    sc = codebook.scaling
+    lens = np.array([p.len for p in seq.pieces], np.int64)
+    incs = np.array([p.inc for p in seq.pieces], np.float64)
+    labels = eng.symbolize_arrays(np.asarray(codebook.centers, np.float64).reshape(-1, 2),
+                                  [sc.scl, sc.sigma_len, sc.sigma_inc], lens, incs)
+    return SymbolicSeries(seq.source_id, seq.anchor, seq.source_length, labels)

@@ -992,6 +992,56 @@ jb_status jb_inverse_transform(jb_context* ctx, const double* centers, const dou
     });
 }
 
+namespace jb_api {
+__global__ void k_len_to_i32(const int64_t* __restrict__ in, int64_t n, int32_t* __restrict__ out,
+                             int* __restrict__ bad) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = in[i];
+        if (v < INT32_MIN || v > INT32_MAX) *bad = 1;
+        out[i] = (int32_t)v;
+    }
+}
+}  // namespace jb_api
+
+jb_status jb_symbolize_with(jb_context* ctx, const double* centers, uint64_t k,
+                            const double* scaling, const int64_t* len, const double* inc,
+                            int64_t n, int32_t pieces_on_device, uint32_t* labels) {
+    return (jb_status)guarded([&] {
+        cudaStream_t st = ctx->stream;
+        JB_CUDA(cudaSetDevice(ctx->device));
+        if (k == 0) throw Error(INVALID_INPUT, "symbolize_with: empty codebook");
+        if (n < 0) throw Error(INVALID_INPUT, "negative piece count");
+        if (n == 0) return;
+        const std::vector<double> c(centers, centers + 2 * k);
+        DArr<int32_t> d_len(n, st);
+        DArr<int64_t> h2d_len;
+        DArr<double> d_inc;
+        DArr<uint32_t> d_lab;
+        DArr<int> bad(1, st);
+        bad.zero();
+        const int64_t* src_len = len;
+        if (!pieces_on_device) {
+            h2d_len.alloc(n, st);
+            h2d_len.upload(len, n);
+            src_len = h2d_len.p;
+            d_inc.alloc(n, st);
+            d_inc.upload(inc, n);
+            d_lab.alloc(n, st);
+        }
+        jb_api::k_len_to_i32<<<gsz(n), 256, 0, st>>>(src_len, n, d_len.p, bad.p);
+        JB_LAUNCH_CHECK();
+        int hb = 0;
+        bad.download(&hb, 1);
+        JB_CUDA(cudaStreamSynchronize(st));
+        if (hb) throw Error(INVALID_INPUT, "symbolize_with: piece length beyond 32 bits");
+        symbolize_pieces(d_len.p, pieces_on_device ? inc : d_inc.p, n, c, k, scaling,
+                         pieces_on_device ? labels : d_lab.p, st);
+        if (!pieces_on_device) d_lab.download(labels, n);
+        JB_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
 void jb_profile_enable(int32_t on) {
     prof_collect();
     if (on && g_pool.empty()) {

@@ -593,3 +593,113 @@ void gather_points(const double* d_pts, const uint64_t* d_idx, int64_t S, double
 }
 
 }  // namespace jb
+
+// ---------------------------------------------------------------------------
+// symbolize_with (digitization.hpp:297-307): held-out pieces against a
+// fitted codebook -- ScalingParams::apply (core.hpp:130-132) then
+// Codebook::nearest (core.hpp:147-160, lowest index on ties), through the
+// same exact grid assignment as the fit.
+
+namespace jb {
+namespace {
+
+__global__ void k_piece_extremes(const int32_t* __restrict__ len, const double* __restrict__ inc,
+                                 int64_t n, unsigned long long* __restrict__ mm,
+                                 int* __restrict__ nonfinite) {
+    unsigned long long lmn = ~0ULL, lmx = 0, imn = ~0ULL, imx = 0;
+    int bad = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        // order-preserving u64 of the signed len
+        const unsigned long long l = (unsigned long long)((long long)len[i]) ^ 0x8000000000000000ULL;
+        const double v = inc[i];
+        bad |= !isfinite(v);
+        lmn = min(lmn, l);
+        lmx = max(lmx, l);
+        imn = min(imn, ord_bits(v));
+        imx = max(imx, ord_bits(v));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lmn = min(lmn, __shfl_xor_sync(0xffffffffu, lmn, o));
+        lmx = max(lmx, __shfl_xor_sync(0xffffffffu, lmx, o));
+        imn = min(imn, __shfl_xor_sync(0xffffffffu, imn, o));
+        imx = max(imx, __shfl_xor_sync(0xffffffffu, imx, o));
+        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(mm + 0, lmn);
+        atomicMax(mm + 1, lmx);
+        atomicMin(mm + 2, imn);
+        atomicMax(mm + 3, imx);
+        if (bad) atomicExch(nonfinite, 1);
+    }
+}
+
+// Codebook::nearest over all centers (large or degenerate codebooks)
+__global__ void k_nearest_all(const PtsView pv, int64_t n, const double* __restrict__ centers,
+                              uint64_t k, uint32_t* __restrict__ labels) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double2 q = pv.at(i);
+        uint64_t best = 0;
+        double bd = __longlong_as_double(0x7FF0000000000000LL);  // +inf
+        for (uint64_t c = 0; c < k; ++c) {
+            const double d = dist2(q.x, q.y, centers[2 * c], centers[2 * c + 1]);
+            if (d < bd) {
+                bd = d;
+                best = c;
+            }
+        }
+        labels[i] = (uint32_t)best;
+    }
+}
+
+}  // namespace
+
+void symbolize_pieces(const int32_t* d_len, const double* d_inc, int64_t n,
+                      const std::vector<double>& centers, uint64_t k, const double scaling[3],
+                      uint32_t* d_labels, cudaStream_t st) {
+    if (k == 0) throw Error(INVALID_INPUT, "symbolize_with: empty codebook");
+    if (n == 0) return;
+    PtsView pv;
+    pv.len = d_len;
+    pv.inc = d_inc;
+    pv.scl = scaling[0];
+    pv.sl = scaling[1];
+    pv.si = scaling[2];
+    DArr<unsigned long long> mm(4, st);
+    const unsigned long long init[4] = {~0ULL, 0ULL, ~0ULL, 0ULL};
+    mm.upload(init, 4);
+    DArr<int> bad(1, st);
+    bad.zero();
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, kSMs * 8));
+    k_piece_extremes<<<grid, 256, 0, st>>>(d_len, d_inc, n, mm.p, bad.p);
+    JB_LAUNCH_CHECK();
+    std::vector<unsigned long long> h = mm.to_host(4);
+    int hbad = 0;
+    bad.download(&hbad, 1);
+    JB_CUDA(cudaStreamSynchronize(st));
+    const long long lmin = (long long)(h[0] ^ 0x8000000000000000ULL);
+    const long long lmax = (long long)(h[1] ^ 0x8000000000000000ULL);
+    BBox bb{pv.scl * (double)lmin / pv.sl, pv.scl * (double)lmax / pv.sl,
+            ord_to_double(h[2]) / pv.si, ord_to_double(h[3]) / pv.si};
+    bool grid_ok = !hbad && k <= 2048 && std::isfinite(pv.scl) && pv.scl >= 0.0 &&
+                   std::isfinite(pv.sl) && pv.sl > 0.0 && std::isfinite(pv.si) && pv.si > 0.0 &&
+                   std::isfinite(bb.xmin) && std::isfinite(bb.xmax) && std::isfinite(bb.ymin) &&
+                   std::isfinite(bb.ymax) && lmin >= INT32_MIN && lmax <= INT32_MAX;
+    for (uint64_t i = 0; i < 2 * k && grid_ok; ++i) grid_ok = std::isfinite(centers[i]);
+    if (grid_ok) {
+        GroupStats gs;
+        assign_and_stats(pv, d_len, n, centers, k, bb, true, d_labels, gs, st,
+                         (int32_t)std::max<long long>(lmax, 1), pv.scl, pv.sl);
+        return;
+    }
+    DArr<double> dc(2 * k, st);
+    dc.upload(centers.data(), 2 * k);
+    JB_PROF("symbolize_nearest_all", st);
+    k_nearest_all<<<grid, 256, 0, st>>>(pv, n, dc.p, k, d_labels);
+    JB_LAUNCH_CHECK();
+    JB_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace jb

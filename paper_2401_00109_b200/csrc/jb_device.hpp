@@ -275,6 +275,12 @@ void assign_and_stats(const PtsView& pv, const int32_t* d_len, int64_t n,
                       int32_t max_len, double scl, double sigma_len, const Comm* cm = nullptr,
                       int64_t first_base = 0);
 
+// symbolize_with (digitization.hpp:297-307) on device: labels of held-out
+// pieces (len, inc) against a codebook (centers 2k, scaling scl/sl/si).
+void symbolize_pieces(const int32_t* d_len, const double* d_inc, int64_t n,
+                      const std::vector<double>& centers, uint64_t k, const double scaling[3],
+                      uint32_t* d_labels, cudaStream_t st);
+
 void relabel(uint32_t* d_labels, int64_t n, const std::vector<uint32_t>& rank_of,
              cudaStream_t st);
 

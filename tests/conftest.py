@@ -20,6 +20,14 @@ def oracle():
 
 
 @pytest.fixture(scope="session")
+def reference():
+    from oracle_lib import REF_SO, Reference
+    if not os.path.exists(REF_SO):
+        pytest.skip("oracle/_ref not built (needs /root/reference)")
+    return Reference()
+
+
+@pytest.fixture(scope="session")
 def engine():
     from paper_2401_00109_b200 import api
     return api.Engine(0)

@@ -145,6 +145,18 @@ class Oracle(_Lib):
             build()
         super().__init__(ORACLE_SO, "jo_")
 
+    def symbolize_with(self, centers, scaling, lens, incs):
+        """symbolize_with (digitization.hpp:297-307) -> (status, labels)."""
+        c = np.ascontiguousarray(centers, np.float64).reshape(-1)
+        sc = np.ascontiguousarray(scaling, np.float64)
+        lens = np.ascontiguousarray(lens, np.int64)
+        incs = np.ascontiguousarray(incs, np.float64)
+        labels = np.zeros(max(len(lens), 1), np.uint32)
+        f = getattr(self.L, self.p + "symbolize_with")
+        f.argtypes = [f64p, C.c_uint64, f64p, i64p, f64p, C.c_int64, u32p]
+        st = f(c, len(c) // 2, sc, lens, incs, len(lens), labels)
+        return st, labels[: len(lens)]
+
     def plan_segments(self, series_lengths, layout, parts):
         sl = np.ascontiguousarray(series_lengths, np.int64)
         cap = int(len(sl) * max(parts, 1))
