@@ -74,9 +74,23 @@ struct BlockCands {
     double wmin[kBuildTB / 32];
 };
 
+// Keep threshold on dmin2. slack > 0 keeps, in addition, every center that
+// could become a candidate after the centers move by up to slack / 2 each:
+// c is dropped only if dmin(c) > sqrt(M) + slack, so after moves of at most
+// D = slack / 2, dmin'(c) >= dmin(c) - D > sqrt(M) + D >= sqrt(M') and c is
+// still not a candidate (M' <= (sqrt(M) + D)^2). The (1 + 1e-12) factors
+// cover the rounding of sqrt, the sum and the square. slack = 0: the exact
+// rule of the header comment.
+__device__ __forceinline__ double keep_threshold(double M, double slack) {
+    if (slack <= 0.0) return M * (1.0 + 1e-12) + 1e-300;
+    const double r = sqrt(M) * (1.0 + 1e-12) + slack;
+    return r * r * (1.0 + 1e-12) + 1e-300;
+}
+
 // block-wide: s.list/s.n := centers kept for box (bx0,bx1,by0,by1), index order
 __device__ inline void block_candidates(BlockCands& s, const double* centers, int k,
-                                        double bx0, double bx1, double by0, double by1) {
+                                        double bx0, double bx1, double by0, double by1,
+                                        double slack = 0.0) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double M = INFINITY;
     for (int c = threadIdx.x; c < k; c += kBuildTB) {
@@ -90,7 +104,7 @@ __device__ inline void block_candidates(BlockCands& s, const double* centers, in
     __syncthreads();
     M = s.wmin[0];
     for (int w = 1; w < kBuildTB / 32; ++w) M = fmin(M, s.wmin[w]);
-    const double thr = M * (1.0 + 1e-12) + 1e-300;
+    const double thr = keep_threshold(M, slack);
     for (int c0 = 0; c0 < k; c0 += kBuildTB) {
         const int c = c0 + threadIdx.x;
         bool keep = false;
@@ -120,7 +134,7 @@ constexpr int kGridBlock = 16;  // cells per block side: one thread per cell
 __device__ __forceinline__ int thread_cell_candidates(const double* centers, int k,
                                                       const BlockCands& s, double bx0, double bx1,
                                                       double by0, double by1, uint16_t* out,
-                                                      int cap) {
+                                                      int cap, double slack = 0.0) {
     const bool all = s.n > kBuildList;
     const int m = all ? k : s.n;
     double M = INFINITY;
@@ -130,7 +144,7 @@ __device__ __forceinline__ int thread_cell_candidates(const double* centers, int
         grid_box_d2(centers[2 * c], centers[2 * c + 1], bx0, bx1, by0, by1, dmn, dmx);
         M = fmin(M, dmx);
     }
-    const double thr = M * (1.0 + 1e-12) + 1e-300;
+    const double thr = keep_threshold(M, slack);
     int nc = 0;
     for (int j = 0; j < m; ++j) {
         const int c = all ? j : s.list[j];

@@ -25,6 +25,8 @@ struct RowGrid {
     double scl, sl;          // x_l = scl * (double)l / sl  (k_scale's expression)
     int R, Gy;               // lengths 1..R, Gy cells per length
     uint64_t* cell;          // R * Gy packed candidate words
+    double slack;            // build slack (jb_grid.cuh keep_threshold): valid while
+                             // every center stays within slack / 2 of its build position
 };
 
 __host__ inline RowGrid make_row_grid_desc(double ymin, double ymax, double scl, double sl,
@@ -42,6 +44,7 @@ __host__ inline RowGrid make_row_grid_desc(double ymin, double ymax, double scl,
     g.scl = scl;
     g.sl = sl;
     g.cell = nullptr;
+    g.slack = 0.0;
     return g;
 }
 
@@ -68,12 +71,13 @@ __device__ __forceinline__ void row_grid_build_body(RowGrid g,
         const int row = blk / nseg, iy0 = (blk % nseg) * kRowSeg;
         const int iy1 = min(iy0 + kRowSeg, g.Gy) - 1;
         const double x = row_x(g, row + 1);
-        block_candidates(s, centers, k, x, x, g.y0 + iy0 * g.h - g.mh, g.y0 + (iy1 + 1) * g.h + g.mh);
+        block_candidates(s, centers, k, x, x, g.y0 + iy0 * g.h - g.mh, g.y0 + (iy1 + 1) * g.h + g.mh,
+                         g.slack);
         const int iy = iy0 + (int)threadIdx.x;
         if (iy <= iy1) {
             uint16_t tmp[4];
             const int nc = thread_cell_candidates(centers, k, s, x, x, g.y0 + iy * g.h - g.mh,
-                                                  g.y0 + (iy + 1) * g.h + g.mh, tmp, 4);
+                                                  g.y0 + (iy + 1) * g.h + g.mh, tmp, 4, g.slack);
             uint64_t word;
             if (nc > 4) {
                 word = (~0ull << 16) | kRowOverflow;
@@ -121,6 +125,30 @@ static __global__ void k_row_occupancy(RowGrid g, const double2* __restrict__ pt
         const int f = (l - 1) * nseg + iy / kRowSeg;
         if (!flags[f]) flags[f] = 1;
     }
+}
+
+// nearest center from an already loaded row-cell word (~0: no row cell)
+__device__ __forceinline__ uint32_t row_pick(uint64_t w, const CandGrid& g, double px, double py,
+                                             const double* cx, const double* cy, int k) {
+    const uint32_t c0 = (uint32_t)(w & 0xFFFF);
+    if (c0 < kRowOverflow) {
+        uint32_t best = c0;
+        const uint32_t c1 = (uint32_t)((w >> 16) & 0xFFFF);
+        if (c1 == kRowEmpty) return best;  // the only possible argmin
+        double bd = dist2(px, py, cx[c0], cy[c0]);
+#pragma unroll
+        for (int j = 1; j < 4; ++j) {
+            const uint32_t c = (uint32_t)((w >> (16 * j)) & 0xFFFF);
+            if (c == kRowEmpty) break;
+            const double d = dist2(px, py, cx[c], cy[c]);
+            if (d < bd) {
+                bd = d;
+                best = c;
+            }
+        }
+        return best;
+    }
+    return grid_nearest(g, px, py, cx, cy, k);
 }
 
 // nearest_center (clustering.hpp:146-157) of a piece of length len at (px, py)

@@ -1131,21 +1131,46 @@ __device__ __forceinline__ void lloyd_work_body(
             const int64_t r = (int64_t)t * TILE + i * 32 + lane;
             old[i] = (r < n && !FULL) ? labs[r] : 0u;
         }
+        // all loads of the tile first (points, lengths, then row-cell words),
+        // so a tile costs about three dependent memory latencies, not twelve
+        double2 pt[TILE / 32];
+        int32_t ln[TILE / 32];
+        uint64_t cw[TILE / 32];
+        uint32_t bst[TILE / 32];
 #pragma unroll
         for (int i = 0; i < TILE / 32; ++i) {
             const int64_t r = (int64_t)t * TILE + i * 32 + lane;
             const bool valid = r < n;
-            double2 p = make_double2(0.0, 0.0);
-            uint32_t best = 0;
-            bool need_p = valid;
-            if (valid && single != MIXED) {
-                best = single;
-                need_p = FULL || old[i] != best;  // unchanged: point not needed
+            const bool need_p = valid && (single == MIXED || FULL || old[i] != single);
+            pt[i] = need_p ? spts[r] : make_double2(0.0, 0.0);
+            ln[i] = (valid && single == MIXED && slen) ? slen[r] : 0;
+        }
+        if (single == MIXED && slen) {
+#pragma unroll
+            for (int i = 0; i < TILE / 32; ++i) {
+                cw[i] = ~0ull;  // not built: fallback
+                if (ln[i] >= 1 && ln[i] <= rg.R) {
+                    int iy = (int)((pt[i].y - rg.y0) * rg.invh);
+                    iy = min(max(iy, 0), rg.Gy - 1);
+                    cw[i] = __ldg(reinterpret_cast<const unsigned long long*>(rg.cell) +
+                                  (size_t)(ln[i] - 1) * rg.Gy + iy);
+                }
             }
-            if (need_p) p = spts[r];
-            if (valid && single == MIXED)
-                best = slen ? row_nearest(rg, g, slen[r], p.x, p.y, cx, cy, k)
-                            : grid_nearest(g, p.x, p.y, cx, cy, k);
+        }
+#pragma unroll
+        for (int i = 0; i < TILE / 32; ++i) {
+            const int64_t r = (int64_t)t * TILE + i * 32 + lane;
+            bst[i] = single;
+            if (r < n && single == MIXED)
+                bst[i] = slen ? row_pick(cw[i], g, pt[i].x, pt[i].y, cx, cy, k)
+                              : grid_nearest(g, pt[i].x, pt[i].y, cx, cy, k);
+        }
+#pragma unroll
+        for (int i = 0; i < TILE / 32; ++i) {
+            const int64_t r = (int64_t)t * TILE + i * 32 + lane;
+            const bool valid = r < n;
+            const double2 p = pt[i];
+            const uint32_t best = valid ? bst[i] : 0u;
             const bool moved = valid && (FULL || old[i] != best);
             if (moved) labs[r] = best;
             if (!FULL && moved) ++my_changed;
@@ -1200,13 +1225,20 @@ __global__ void __launch_bounds__(LL_TB) k_lloyd_work(
 
 // centers[c] = sums[c] / counts[c] for non-empty clusters (update_means
 // :177-180); reports the empty clusters in index order.
+// mov (optional, persistent loop): [0] displacement accumulated since the
+// last row-grid build (double), [1] rebuild flag for this iteration (as
+// double), [2] the allowed displacement D = slack / 2. The row grid is rebuilt
+// only when a center may have moved more than D since the last build.
 __device__ __forceinline__ void means_body(ClusterAcc acc, int k, int Ex, int Ey,
                                                double* __restrict__ centers,
                                                int* __restrict__ empties, int* __restrict__ n_empty,
-                                               const int* __restrict__ gate) {
+                                               const int* __restrict__ gate,
+                                               double* __restrict__ mov = nullptr) {
     if (gate && (gate[0] | gate[1])) return;  // uniform over the block
     __shared__ int wc[32];
     __shared__ int base;
+    __shared__ double wmax[32];
+    double dmax = 0.0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) base = 0;
     __syncthreads();
@@ -1219,8 +1251,14 @@ __device__ __forceinline__ void means_body(ClusterAcc acc, int k, int Ex, int Ey
             l3_store(acc.sx + 3 * c, sx);  // renormalise the limbs once per iteration
             l3_store(acc.sy + 3 * c, sy);
             if (cnt > 0) {
-                centers[2 * c] = fx_to_double(sx, Ex) / (double)cnt;
-                centers[2 * c + 1] = fx_to_double(sy, Ey) / (double)cnt;
+                const double nx = fx_to_double(sx, Ex) / (double)cnt;
+                const double ny = fx_to_double(sy, Ey) / (double)cnt;
+                if (mov) {  // displacement, rounded up
+                    const double dx = nx - centers[2 * c], dy = ny - centers[2 * c + 1];
+                    dmax = fmax(dmax, sqrt(dx * dx + dy * dy) * (1.0 + 1e-12) + 1e-300);
+                }
+                centers[2 * c] = nx;
+                centers[2 * c + 1] = ny;
             } else {
                 empty = true;
             }
@@ -1238,6 +1276,22 @@ __device__ __forceinline__ void means_body(ClusterAcc acc, int k, int Ex, int Ey
         __syncthreads();
     }
     if (threadIdx.x == 0) *n_empty = base;
+    if (mov) {
+        for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+        if (lane == 0) wmax[warp] = dmax;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < (int)(blockDim.x >> 5); ++w) dmax = fmax(dmax, wmax[w]);
+            const double acc_d = mov[0] + dmax;  // triangle inequality: a bound
+            if (!(acc_d <= mov[2])) {  // also NaN / +inf (forced)
+                mov[0] = 0.0;
+                mov[1] = 1.0;
+            } else {
+                mov[0] = acc_d;
+                mov[1] = 0.0;
+            }
+        }
+    }
 }
 
 __global__ void __launch_bounds__(256) k_means(ClusterAcc acc, int k, int Ex, int Ey,
@@ -1365,6 +1419,7 @@ struct LloydCtx {
     int Ex, Ey;
     cudaStream_t st;
     DArr<double> centers;
+    DArr<double> mov;              // persistent loop: row-grid movement state
     DArr<uint32_t> labs;           // sorted order
     DArr<unsigned long long> acc;  // 5k: sx(2k) sy(2k) cnt(k)
     DArr<unsigned long long> flags;  // [0] changed
@@ -1502,27 +1557,45 @@ struct PersistArgs {
     const int32_t* slen;
     unsigned long long* diag;
     int budget;
+    unsigned long long* tstamp;  // optional: 6 globaltimer stamps per iteration (block 0)
+    double* mov;                 // row-grid movement state (means_body)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 __global__ void __launch_bounds__(256) k_lloyd_persistent(PersistArgs a) {
     namespace cgx = cooperative_groups;
     cgx::grid_group grid = cgx::this_grid();
     int* state = a.empties + a.k;
+    const bool ts = a.tstamp && blockIdx.x == 0 && threadIdx.x == 0;
     for (int b = 0; b < a.budget; ++b) {
-        if (blockIdx.x == 0) means_body(a.acc, a.k, a.Ex, a.Ey, a.centers, a.empties, state, state);
+        if (ts && b < 512) a.tstamp[6 * b] = gtimer();
+        if (blockIdx.x == 0)
+            means_body(a.acc, a.k, a.Ex, a.Ey, a.centers, a.empties, state, state, a.mov);
         grid.sync();
+        if (ts && b < 512) a.tstamp[6 * b + 1] = gtimer();
         if (((volatile int*)state)[0] | ((volatile int*)state)[1]) break;
-        row_grid_build_body(a.rg, a.centers, a.k, a.rg_blocks, a.rg_nblocks);
-        grid.sync();
+        if (((volatile double*)a.mov)[1] != 0.0) {  // centers moved too far: rebuild
+            row_grid_build_body(a.rg, a.centers, a.k, a.rg_blocks, a.rg_nblocks);
+            grid.sync();
+        }
+        if (ts && b < 512) a.tstamp[6 * b + 2] = gtimer();
         super_check_body(a.sbox, a.slenc, a.ntiles, a.cg, a.centers, a.tlab, a.swork, a.nswork,
                          nullptr, 0, a.rg, a.k);
         grid.sync();
+        if (ts && b < 512) a.tstamp[6 * b + 3] = gtimer();
         tile_expand_body(a.swork, a.nswork, a.tbox, a.tlen, a.ntiles, a.cg, a.centers, a.tlab,
                          a.tnew, a.work, a.nwork, nullptr, 0, a.rg, a.k);
         grid.sync();
+        if (ts && b < 512) a.tstamp[6 * b + 4] = gtimer();
         lloyd_work_body<false>(a.spts, a.n, a.centers, a.k, a.cg, a.labs, a.work, a.nwork, a.tnew,
                                a.tlab, a.Ex, a.Ey, a.acc, a.changed, nullptr, a.rg, a.slen);
         grid.sync();
+        if (ts && b < 512) a.tstamp[6 * b + 5] = gtimer();
         if (blockIdx.x == 0) {
             if (threadIdx.x == 0) iter_end_body(state, a.changed, a.nwork, a.nswork, a.diag);
             __syncthreads();
@@ -1533,6 +1606,7 @@ __global__ void __launch_bounds__(256) k_lloyd_persistent(PersistArgs a) {
 // the persistent loop applies when the row grid carries the assignment
 // (no 2-D grid) and the device can co-schedule the grid
 bool lloyd_persistent(LloydCtx& L, int budget) {
+    static const bool phase_times = getenv("JB_LLOYD_PHASES") != nullptr;
     if (L.rg.R == 0 || L.cg.G != 0 || L.n == 0 || dbg_on()) return false;
     static int coop = -1;
     if (coop < 0) {
@@ -1576,10 +1650,35 @@ bool lloyd_persistent(LloydCtx& L, int budget) {
     a.slen = L.slen;
     a.diag = L.diag.p;
     a.budget = budget;
+    // grid slack: centers may drift h / 2 (half a row-grid cell) between
+    // rebuilds; the first iteration of every launch rebuilds (+inf)
+    if (L.mov.n == 0) L.mov.alloc(3, L.st);
+    {
+        const double init[3] = {INFINITY, 1.0, 0.5 * L.rg.h};
+        L.mov.upload(init, 3);
+    }
+    a.mov = L.mov.p;
+    DArr<unsigned long long> tsb(phase_times ? 6 * 512 : 0, L.st);
+    if (phase_times) tsb.zero();
+    a.tstamp = phase_times ? tsb.p : nullptr;
     void* args[] = {&a};
-    JB_PROF("lloyd_persistent", L.st);
-    JB_CUDA(cudaLaunchCooperativeKernel((const void*)k_lloyd_persistent, dim3(kSMs * per_sm),
-                                        dim3(256), args, smem, L.st));
+    {
+        JB_PROF("lloyd_persistent", L.st);
+        JB_CUDA(cudaLaunchCooperativeKernel((const void*)k_lloyd_persistent, dim3(kSMs * per_sm),
+                                            dim3(256), args, smem, L.st));
+    }
+    if (phase_times) {  // JB_LLOYD_PHASES=1: mean phase latencies (us) on stderr
+        auto h = tsb.to_host(6 * 512);
+        double acc[5] = {0, 0, 0, 0, 0};
+        int cnt = 0;
+        for (int b = 0; b < 512 && h[6 * b + 5]; ++b, ++cnt)
+            for (int q = 0; q < 5; ++q) acc[q] += (double)(h[6 * b + q + 1] - h[6 * b + q]) * 1e-3;
+        if (cnt)
+            fprintf(stderr, "[jb] lloyd phases over %d iters (us): means %.1f grid %.1f super %.1f "
+                            "expand %.1f work %.1f (grid %d x 256)\n",
+                    cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt,
+                    kSMs * per_sm);
+    }
     return true;
 }
 
@@ -1696,6 +1795,7 @@ void lloyd_best_device(const PtsView& pv, const uint64_t* d_idx, int64_t n, uint
     }
     if (rows.len) {  // exact row grid over the integer piece lengths (jb_rowgrid.cuh)
         L.rg = make_row_grid_desc(bb.ymin, bb.ymax, rows.scl, rows.sl, rows.max_len, 1 << 16);
+        L.rg.slack = L.rg.h;  // persistent loop: rebuild only after h / 2 of movement
         L.rg_cell.alloc((size_t)L.rg.R * L.rg.Gy, st);
         L.rg.cell = L.rg_cell.p;
         L.slen = slen.p;
