@@ -138,8 +138,12 @@ def algorithmic_work(name, launches, info):
     """Algorithmic bytes or flops of ALL launches of `name`."""
     S, k, N, n = info["S"], info["k"], info["N"], info["n"]
     it = info["iterations"]
-    if name == "lloyd_assign":      # points of the tiles that need work: 16 B point + 4 B label r/w
-        return "hbm", 24.0 * 128 * info.get("lloyd_tiles", 0) + launches * 0.0
+    if name == "lloyd_assign":      # first (full) assignment: every sample point, 16 B + 4 B label out
+        return "hbm", launches * 20.0 * S
+    if name == "lloyd_persistent":  # iterations 1..I: points of the tiles that can change
+        # (16 B point + 4 B label r/w each); tiles of the full pass excluded
+        full_tiles = (S + 127) // 128
+        return "hbm", 24.0 * 128 * max(info.get("lloyd_tiles", 0) - full_tiles, 0)
     if name == "assign_stats":       # final assign + group stats: point 16 B + len 4 B in, label 4 B out
         return "hbm", launches * 24.0 * N
     if name == "d2_update":          # 16 B point + 8 B d2 read, 8 B d2 write per sample
@@ -151,6 +155,17 @@ def algorithmic_work(name, launches, info):
     if name == "inverse_fill":
         return "hbm", 8.0 * n + 28.0 * N
     return None, None
+
+
+def ncu_traffic(name):
+    """Per-launch DRAM bytes of `name` from an ncu --set full capture
+    (profiles/ncu_traffic.json, written by tools/ncu_traffic.py), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)[name]["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def fp64_peak(engine_lib, device):
@@ -374,7 +389,8 @@ def main():
             pk = peaks.get("hbm_gbs")
             ach = work / (kms * 1e-3) / 1e9
             roof = {"kernel": name, "bound": "hbm", "achieved": ach, "peak": pk, "unit": "GB/s",
-                    "frac": ach / pk if pk else None, "traffic": None,
+                    "frac": ach / pk if pk else None, "traffic": ncu_traffic(name),
+                    "algorithmic_bytes_per_launch": work / launches,
                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                     "launches": launches, "avg_launch_ms": kms / launches,
                     "share_of_step": kms / ms_profiled}

