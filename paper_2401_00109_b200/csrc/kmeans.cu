@@ -202,7 +202,7 @@ __device__ __forceinline__ bool lemire(uint64_t x, uint64_t erange, uint64_t& r)
 // host loop in sample_indices_device).
 __global__ void k_fy_map(const uint64_t* __restrict__ raw, uint64_t n, uint64_t S,
                          const uint64_t* __restrict__ bp_i, const uint64_t* __restrict__ bp_sh,
-                         int nbp, uint64_t* __restrict__ j_out, uint32_t* __restrict__ vals,
+                         int nbp, uint32_t* __restrict__ j_out, uint32_t* __restrict__ vals,
                          unsigned long long* __restrict__ first_reject) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < S;
          i += (uint64_t)gridDim.x * blockDim.x) {
@@ -216,19 +216,21 @@ __global__ void k_fy_map(const uint64_t* __restrict__ raw, uint64_t n, uint64_t 
         uint64_t r;
         const bool ok = lemire(raw[i + sh], erange, r);
         if (!ok && !fixed) atomicMin(first_reject, (unsigned long long)i);
-        j_out[i] = i + r;
+        j_out[i] = (uint32_t)(i + r);  // < n < 2^32
         vals[i] = (uint32_t)i;
     }
 }
 
-__global__ void k_fy_links(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+// P is pre-filled with "none": only the (few) swaps that share their j with an
+// earlier swap are written
+__global__ void k_fy_links(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
                            uint64_t S, uint32_t* __restrict__ P, uint32_t* __restrict__ L) {
     for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < S;
          r += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t key = keys[r];
         const uint32_t i = vals[r];
         const bool same_prev = r > 0 && keys[r - 1] == key;
-        P[i] = same_prev ? vals[r - 1] : 0xFFFFFFFFu;
+        if (same_prev) P[i] = vals[r - 1];
         const bool group_last = (r + 1 == S) || keys[r + 1] != key;
         if (group_last && key < S) {
             // last swap (< key) that wrote position `key`
@@ -238,7 +240,7 @@ __global__ void k_fy_links(const uint64_t* __restrict__ keys, const uint32_t* __
     }
 }
 
-__global__ void k_fy_resolve(const uint64_t* __restrict__ j, const uint32_t* __restrict__ P,
+__global__ void k_fy_resolve(const uint32_t* __restrict__ j, const uint32_t* __restrict__ P,
                              const uint32_t* __restrict__ L, uint64_t S,
                              uint64_t* __restrict__ idx) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < S;
@@ -343,7 +345,7 @@ void mt19937_64_generate(uint64_t seed, uint64_t count, DArr<uint64_t>& out, cud
 uint64_t sample_indices_device(uint64_t n, uint64_t S, const uint64_t* d_raw, uint64_t raw_count,
                                DArr<uint64_t>& idx, cudaStream_t st) {
     if (n >= (1ULL << 32)) throw Error(INVALID_INPUT, "sampling: more than 2^32 pieces");
-    DArr<uint64_t> j(S, st), keys_s(S, st);
+    DArr<uint32_t> j(S, st), keys_s(S, st);  // j_i < n < 2^32
     DArr<uint32_t> vals(S, st), vals_s(S, st);
     DArr<unsigned long long> rej(1, st);
     std::vector<uint64_t> bpi, bps;
@@ -392,7 +394,7 @@ uint64_t sample_indices_device(uint64_t n, uint64_t S, const uint64_t* d_raw, ui
     uint64_t total_shift = bps.empty() ? 0 : bps.back();
     // stable radix sort of (j, i) by j
     int end_bit = 1;
-    while (end_bit < 64 && (n >> end_bit) != 0) ++end_bit;
+    while (end_bit < 32 && (n >> end_bit) != 0) ++end_bit;
     size_t tb = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, tb, j.p, keys_s.p, vals.p, vals_s.p, (int64_t)S, 0,
                                     end_bit, st);
@@ -402,6 +404,7 @@ uint64_t sample_indices_device(uint64_t n, uint64_t S, const uint64_t* d_raw, ui
     JB_LAUNCH_CHECK();
     DArr<uint32_t> P(S, st), L(S, st);
     JB_CUDA(cudaMemsetAsync(L.p, 0xFF, sizeof(uint32_t) * S, st));
+    JB_CUDA(cudaMemsetAsync(P.p, 0xFF, sizeof(uint32_t) * S, st));
     k_fy_links<<<grid_cap(S), 256, 0, st>>>(keys_s.p, vals_s.p, S, P.p, L.p);
     JB_LAUNCH_CHECK();
     idx.alloc(S, st);
