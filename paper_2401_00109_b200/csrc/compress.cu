@@ -74,18 +74,13 @@ struct ChunkGeom {
     const int64_t* chunk_off;  // n_seg + 1
     int64_t n_seg;
     int64_t C;
+    const int32_t* chunk_seg;  // segment of every chunk (no binary search per chunk)
 };
 
 __device__ __forceinline__ void chunk_bounds(const ChunkGeom& g, int64_t ch, int64_t& s,
                                              int64_t& c, int64_t& lo, int64_t& hi,
                                              int64_t& last) {
-    int64_t a = 0, b = g.n_seg;  // find s: chunk_off[s] <= ch < chunk_off[s+1]
-    while (b - a > 1) {
-        const int64_t m = (a + b) >> 1;
-        if (g.chunk_off[m] <= ch) a = m;
-        else b = m;
-    }
-    s = a;
+    s = g.chunk_seg[ch];  // chunk_off[s] <= ch < chunk_off[s+1]
     c = ch - g.chunk_off[s];
     const int64_t first = g.seg_first[s];
     last = first + g.seg_steps[s];
@@ -349,6 +344,14 @@ __global__ void k_emit(const double* __restrict__ v, ChunkGeom g, int64_t n_chun
     }
 }
 
+__global__ void k_chunk_seg(const int64_t* __restrict__ chunk_off, int64_t n_seg,
+                            int32_t* __restrict__ chunk_seg) {
+    for (int64_t sidx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sidx < n_seg;
+         sidx += (int64_t)gridDim.x * blockDim.x)
+        for (int64_t ch = chunk_off[sidx]; ch < chunk_off[sidx + 1]; ++ch)
+            chunk_seg[ch] = (int32_t)sidx;
+}
+
 __global__ void k_seg_offsets(const int64_t* __restrict__ chunk_off,
                               const int64_t* __restrict__ base, int64_t n_seg, int64_t total,
                               int64_t* __restrict__ seg_off) {
@@ -373,7 +376,10 @@ void compress_segments(const double* d_values, const SegTable& seg, double tol,
     const int64_t n_chunks = h_chunk_off[n_seg];
     DArr<int64_t> chunk_off(n_seg + 1, st);
     chunk_off.upload(h_chunk_off.data(), n_seg + 1);
-    ChunkGeom g{seg.first.p, seg.steps.p, chunk_off.p, n_seg, C};
+    DArr<int32_t> chunk_seg(std::max<int64_t>(n_chunks, 1), st);
+    k_chunk_seg<<<ceil_div(n_seg, 256), 256, 0, st>>>(chunk_off.p, n_seg, chunk_seg.p);
+    JB_LAUNCH_CHECK();
+    ChunkGeom g{seg.first.p, seg.steps.p, chunk_off.p, n_seg, C, chunk_seg.p};
 
     const double tol2 = tol * tol;
     const int W = (int)(C / 32);
