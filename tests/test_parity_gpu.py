@@ -83,6 +83,26 @@ def test_configs_small_vs_oracle(engine, oracle, cid):
         assert nf.stats()["iterations"] == ref.iterations
 
 
+@pytest.mark.parametrize("cid,scale", [(1, 1.0), (2, 0.02), (3, 0.001), (4, 2e-3), (5, 2e-4)])
+def test_configs_vs_reference(engine, reference, cid, scale):
+    """The unmodified reference (oracle/_ref) on the same inputs, at larger
+    scales than the oracle cases: pieces and symbols bit-exact; centers,
+    scaling and the reconstruction within 1e-9."""
+    w = datasets.CONFIGS[cid](scale) if cid != 3 else datasets.config3(scale)
+    nf, off, ln, inc, sym, rec = _run(engine, w.values, w.series_lengths, w.layout, w.parts, w.cfg)
+    first, steps = api.plan_segments(w.series_lengths, w.layout, w.parts)
+    ref = reference.fit(w.values, first, steps, w.layout, make_config(**w.cfg))
+    assert ref.status == 0
+    st, rref = reference.reconstruct(ref, w.layout)
+    assert st == 0
+    want = dict(piece_offsets=ref.piece_offsets, piece_len=ref.piece_len,
+                piece_inc=ref.piece_inc, k=ref.k, labels=ref.labels, centers=ref.centers,
+                mean_lengths=ref.mean_lengths, scaling=ref.scaling, anchors=ref.anchors)
+    _check(nf, off, ln, inc, sym, rec, want, rref)
+    # (the reference's API exposes no iteration count; test_configs_small_vs_oracle
+    # pins iterations against the restatement)
+
+
 def test_compression_bit_exact_at_scale(engine, oracle):
     """1e7-sample partitioned walk (config 4 at 1%): boundaries + increments."""
     w = datasets.config4(0.01)
