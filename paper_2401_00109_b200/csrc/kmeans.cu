@@ -760,14 +760,63 @@ __global__ void __launch_bounds__(PICK_TB) k_pick(const uint64_t* __restrict__ r
     const i128 U = fx_from_double(u, E);               // floor(u * 2^E), u >= 0
     // the warp range holding the crossing: first warp with U < inclusive prefix
     const unsigned crossing = __ballot_sync(0xffffffffu, U < wincl);
+    // that range's block sums staged in shared memory by the whole block at
+    // once (one coalesced round trip), then walked by warp 0
+    constexpr int STAGE = 2048;
+    __shared__ unsigned long long s_rng[STAGE][2];
+    const int fwb = crossing ? __ffs(crossing) - 1 : 0;
+    const int r0 = min(nblocks, fwb * R), r1 = min(nblocks, r0 + R);
+    const bool staged = crossing && r1 - r0 <= STAGE;
+    constexpr int MAXCH = STAGE / 32;
+    __shared__ unsigned long long s_chk[MAXCH][2];  // 32-block chunk sums of the staged range
+    if (staged) {
+        for (int q = t; q < r1 - r0; q += PICK_TB) {
+            s_rng[q][0] = part[2 * (r0 + q)];
+            s_rng[q][1] = part[2 * (r0 + q) + 1];
+        }
+    }
+    __syncthreads();
+    const int nchk = (r1 - r0 + 31) / 32;
+    if (staged) {  // one warp per chunk sum, all in parallel
+        for (int j = w; j < nchk; j += NW) {
+            const int q = 32 * j + lane;
+            const i128 v = q < r1 - r0 ? (i128)(((u128)s_rng[q][1] << 64) | s_rng[q][0]) : (i128)0;
+            const i128 cs = fx_warp_sum(v);
+            if (lane == 0) {
+                s_chk[j][0] = (unsigned long long)(u128)cs;
+                s_chk[j][1] = (unsigned long long)((u128)cs >> 64);
+            }
+        }
+    }
+    __syncthreads();
     if (w == 0 && crossing) {  // warp 0 resolves the block inside that range
         const int fw = __ffs(crossing) - 1;
         const i128 prev = shfl_i128(wincl, fw > 0 ? fw - 1 : 0);
         i128 run = fw > 0 ? prev : (i128)0;  // exclusive prefix of warp fw's range
         const int c0 = min(nblocks, fw * R), c1 = min(nblocks, c0 + R);
-        for (int bb = c0; bb < c1; bb += 32) {
+        int start = c0;
+        if (staged) {  // the chunk holding the crossing, from the chunk sums
+            int jf = -1;
+            for (int j0 = 0; j0 < nchk && jf < 0; j0 += 32) {
+                const int j = j0 + lane;
+                const i128 v = j < nchk ? (i128)(((u128)s_chk[j][1] << 64) | s_chk[j][0]) : (i128)0;
+                const i128 incl = warp_incl_scan_i128(v);
+                const unsigned hit = __ballot_sync(0xffffffffu, j < nchk && U < run + incl);
+                if (hit) {
+                    const int hl = __ffs(hit) - 1;
+                    jf = j0 + hl;
+                    run += shfl_i128(incl, hl) - shfl_i128(v, hl);
+                } else {
+                    run += shfl_i128(incl, 31);
+                }
+            }
+            start = jf >= 0 ? c0 + 32 * jf : c1;
+        }
+        for (int bb = start; bb < c1; bb += 32) {
             const int b = bb + lane;
-            const i128 v = b < c1 ? fx_load(part + 2 * b) : (i128)0;
+            const i128 v = b >= c1 ? (i128)0
+                           : staged ? (i128)(((u128)s_rng[b - c0][1] << 64) | s_rng[b - c0][0])
+                                    : fx_load(part + 2 * b);
             const i128 incl = warp_incl_scan_i128(v);
             const unsigned hit = __ballot_sync(0xffffffffu, b < c1 && U < run + incl);
             if (hit) {
