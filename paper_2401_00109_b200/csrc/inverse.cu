@@ -249,14 +249,16 @@ __global__ void k_inv_segfix(InverseIn in, int32_t* __restrict__ qlen,
 // drops its last sample (stitch_partitions :198-213).
 constexpr int DIV_MAX = 31;  // exact i/len table for len <= DIV_MAX (7.9 KB smem)
 constexpr int LANE_MAX = 16; // pieces up to this length: lane per piece
+constexpr int FILL_TB = 256;
 
-__global__ void __launch_bounds__(256) k_inv_fill(InverseIn in, const double* __restrict__ rinc,
+__global__ void __launch_bounds__(FILL_TB) k_inv_fill(InverseIn in, const double* __restrict__ rinc,
                                                   const int32_t* __restrict__ qlen,
                                                   const double* __restrict__ vstart,
                                                   const GroupRec* __restrict__ rec,
                                                   const int32_t* __restrict__ gmeta,
                                                   int64_t n_groups, double* __restrict__ out) {
     __shared__ double div_tab[(DIV_MAX + 1) * (DIV_MAX + 1)];
+    __shared__ double s_stage[FILL_TB / 32][32 * LANE_MAX];
     extern __shared__ double s_inc[];
     const int kk = (int)in.k;
     const bool inc_smem = (size_t)kk * sizeof(double) <= kInvTabSmem / 2;
@@ -287,16 +289,21 @@ __global__ void __launch_bounds__(256) k_inv_fill(InverseIn in, const double* __
             if (lane >= o) incl += y;
         }
         const int maxlen = __reduce_max_sync(FULL, len);
+        const long long L = __shfl_sync(FULL, incl, 31);
         if (maxlen <= LANE_MAX) {
+            // lane per piece into the warp's staging row, then one coalesced copy
+            double* st = s_stage[threadIdx.x >> 5];
             if (valid) {
-                const long long p0 = r.pos + incl - len;
-                const int nl = (drop_last && lane == cnt - 1) ? len - 1 : len;
-                for (int i = 1; i <= nl; ++i)
-                    out[p0 + i] = myv + inc * div_tab[len * (DIV_MAX + 1) + i];
+                const int p0 = (int)(incl - len);
+                for (int i = 1; i <= len; ++i)
+                    st[p0 + i - 1] = myv + inc * div_tab[len * (DIV_MAX + 1) + i];
             }
+            __syncwarp();
+            const int Le = (int)L - (drop_last ? 1 : 0);
+            for (int q = lane; q < Le; q += 32) out[r.pos + 1 + q] = st[q];
+            __syncwarp();
             continue;
         }
-        const long long L = __shfl_sync(FULL, incl, 31);
         for (long long q0 = 1; q0 <= L; q0 += 32) {
             const long long q = q0 + lane;  // 1-based sample within the group
             int last_below = -1;  // last piece with incl < q (fixed 5 steps)
@@ -321,22 +328,305 @@ __global__ void __launch_bounds__(256) k_inv_fill(InverseIn in, const double* __
     }
 }
 
+// ---- fused path (the common case) ----
+// One block = 32 segments. Warp 0 runs, one lane per segment, both
+// sequential chains in the reference's rounding -- the length carry
+// (quantize_lengths :63-74) and the start values (inverse_compress :94-101),
+// independent of each other so they overlap -- into rings of per-piece
+// quantized lengths and start values, plus each tile's first output
+// position. The writer warps trail it by FD tiles and emit every sample at
+// its final position: a half-warp per (segment, tile), lane m holding piece
+// m, samples assigned to lanes 16 at a time (coalesced stores), the piece of
+// a sample found by a 4-step search over the tile's exclusive length scan.
+// When a segment's last tile is done, warp 0 applies match_total_length's
+// backward cascade (:81-93) to the pieces still in the ring -- the cascade
+// only moves the tail, so every piece already written sits at its final
+// position -- and recomputes the window's tile positions. A cascade that
+// reaches past the window sends the call to the general path (err[1]).
+constexpr int FD = 4;                    // tiles between warp 0 and the writers (cascade window)
+constexpr int FRD = 6;                   // label tiles in flight
+constexpr int FS = FRD + FD;             // label ring tiles
+constexpr int FLSTR = FS * RT * 4 + 16;  // label ring bytes per lane
+constexpr int FQ = (FD + 1) * RT;        // ring entries per lane
+constexpr int FWW = 7;                   // writer warps
+constexpr int FUSED_TB = 32 * (1 + FWW);
+constexpr long long kTileSamplesMax = 1LL << 30;  // larger tiles: general path
+constexpr int kLanePiece = 8;  // pieces up to this length: lane per piece; longer: warp per piece
+
+struct FusedSmem {
+    double div[(DIV_MAX + 1) * (DIV_MAX + 1)];
+    double vs[32 * FQ];       // start value of each piece
+    int32_t q[32 * FQ];       // quantized length of each piece (0: outside the segment)
+    int32_t ex[32 * FQ];      // its first sample's offset from the tile's first sample
+    long long pos[FD + 1][32];// output position of each tile's first sample
+    long long E[32];          // last output position of each segment
+    int ntile[32];
+    int bail[32];
+    unsigned char lab[32 * FLSTR];
+};
+
+__device__ __forceinline__ void ring_issue_z(unsigned char* my, const uint32_t* __restrict__ labels,
+                                             int64_t idx, int64_t n, int slot) {
+    const unsigned dst = (unsigned)__cvta_generic_to_shared(my + slot * RT * 4);
+#pragma unroll
+    for (int m = 0; m < RT / 4; ++m) {
+        const int64_t i = idx + 4 * m;  // 16-byte chunk: zero-filled past the label array
+        const int64_t rem = n - i;
+        const unsigned nb = rem >= 4 ? 16u : rem > 0 ? (unsigned)rem * 4u : 0u;
+        const uint32_t* src = nb ? labels + i : labels;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst + 16 * m),
+                     "l"(src), "r"(nb));
+    }
+}
+
+template <bool SMEM_TABS>
+__global__ void __launch_bounds__(FUSED_TB) k_inv_fused(InverseIn in, const double* __restrict__ rlen,
+                                                        const double* __restrict__ rinc,
+                                                        double* __restrict__ out,
+                                                        unsigned long long* __restrict__ err) {
+    extern __shared__ __align__(128) unsigned char dsm[];
+    const int kk = (int)in.k;
+    const size_t toff = SMEM_TABS ? ((size_t)2 * kk * sizeof(double) + 127) & ~(size_t)127 : 0;
+    double* s_tabs = reinterpret_cast<double*>(dsm);
+    FusedSmem& S = *reinterpret_cast<FusedSmem*>(dsm + toff);
+    if (SMEM_TABS)
+        for (int c = threadIdx.x; c < kk; c += blockDim.x) {
+            s_tabs[c] = rlen[c];
+            s_tabs[kk + c] = rinc[c];
+        }
+    for (int t = threadIdx.x; t < (DIV_MAX + 1) * (DIV_MAX + 1); t += blockDim.x) {
+        const int l = t / (DIV_MAX + 1), i = t % (DIV_MAX + 1);
+        S.div[t] = l > 0 ? (double)i / (double)l : 0.0;  // the same IEEE division
+    }
+    const double* tlen = SMEM_TABS ? s_tabs : rlen;
+    const double* tinc = SMEM_TABS ? s_tabs + kk : rinc;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned FULL = 0xffffffffu;
+
+    // warp 0: lane = segment
+    const int64_t s = blockIdx.x * (int64_t)32 + lane;
+    int64_t a = 0, b = 0, base = 0;
+    int ntile = 0;
+    double carry = 0.0, v = 0.0;
+    long long total = 0, pos = 0;
+    bool badlab = false;
+    unsigned char* lrow = S.lab + lane * FLSTR;
+    int32_t* qrow = S.q + lane * FQ;
+    int32_t* xrow = S.ex + lane * FQ;
+    double* vrow = S.vs + lane * FQ;
+    if (warp == 0) {
+        const bool live = s < in.n_seg;
+        long long E = -1;
+        if (live) {
+            a = in.seg_offsets[s];
+            b = in.seg_offsets[s + 1];
+            const long long o = in.out_offsets[s];
+            const bool drop = in.layout == 0 && (s + 1 < in.n_seg || in.drop_local_last);
+            E = o + in.source_lengths[s] - (drop ? 1 : 0);
+            v = in.anchors[s];
+            if (E >= o) out[o] = v;
+            pos = o + 1;
+        }
+        base = a & ~(int64_t)3;  // 16-byte aligned label tiles
+        ntile = b > a ? (int)((b - base + RT - 1) / RT) : 0;
+        S.E[lane] = E;
+        S.ntile[lane] = ntile;
+        S.bail[lane] = 0;
+        for (int t = 0; t < FRD - 1; ++t) {
+            if (t < ntile) ring_issue_z(lrow, in.labels, base + (int64_t)t * RT, in.N, t % FS);
+            ring_commit();
+        }
+    }
+    __syncthreads();
+    int maxT = 0;
+    for (int l = 0; l < 32; ++l) maxT = max(maxT, S.ntile[l]);
+    auto lab_ok = [&](uint32_t lab) -> uint32_t {
+        const bool bad = lab >= (uint32_t)kk;
+        badlab |= bad;
+        return bad ? 0u : lab;
+    };
+
+    for (int it = 0; it < maxT + FD; ++it) {
+        if (warp == 0) {
+            if (it < ntile) {
+                const int tn = it + FRD - 1;
+                if (tn < ntile) ring_issue_z(lrow, in.labels, base + (int64_t)tn * RT, in.N, tn % FS);
+                ring_commit();
+                ring_wait<FRD - 1>();  // tile it has landed
+                const uint32_t* lt = reinterpret_cast<const uint32_t*>(lrow + (it % FS) * RT * 4);
+                const int slot = it % (FD + 1);
+                int32_t* qt = qrow + slot * RT;
+                int32_t* xt = xrow + slot * RT;
+                double* vt = vrow + slot * RT;
+                const int64_t jt = base + (int64_t)it * RT;
+                S.pos[slot][lane] = pos;
+                long long tsum = 0;
+                if (jt >= a && jt + RT <= b) {
+#pragma unroll
+                    for (int m = 0; m < RT / 4; ++m) {
+                        const uint4 L = reinterpret_cast<const uint4*>(lt)[m];
+                        const uint32_t l0 = lab_ok(L.x), l1 = lab_ok(L.y), l2 = lab_ok(L.z),
+                                       l3 = lab_ok(L.w);
+                        int4 Q;
+                        chain_step(tlen[l0], carry, Q.x);
+                        chain_step(tlen[l1], carry, Q.y);
+                        chain_step(tlen[l2], carry, Q.z);
+                        chain_step(tlen[l3], carry, Q.w);
+                        reinterpret_cast<int4*>(qt)[m] = Q;
+                        int4 X;
+                        X.x = (int)tsum;
+                        X.y = X.x + Q.x;
+                        X.z = X.y + Q.y;
+                        X.w = X.z + Q.z;
+                        reinterpret_cast<int4*>(xt)[m] = X;
+                        tsum += (long long)Q.x + Q.y + Q.z + Q.w;
+                        const double v0 = v, v1 = v0 + tinc[l0], v2 = v1 + tinc[l1],
+                                     v3 = v2 + tinc[l2];
+                        v = v3 + tinc[l3];
+                        reinterpret_cast<double2*>(vt)[2 * m] = make_double2(v0, v1);
+                        reinterpret_cast<double2*>(vt)[2 * m + 1] = make_double2(v2, v3);
+                    }
+                } else {
+                    for (int m = 0; m < RT; ++m) {
+                        const int64_t j = jt + m;
+                        int32_t q = 0;
+                        vt[m] = v;
+                        if (j >= a && j < b) {
+                            const uint32_t l = lab_ok(lt[m]);
+                            chain_step(tlen[l], carry, q);
+                            v += tinc[l];
+                        }
+                        qt[m] = q;
+                        xt[m] = (int)tsum;
+                        tsum += q;
+                    }
+                }
+                total += tsum;
+                pos += tsum;
+                if (tsum > kTileSamplesMax && !S.bail[lane]) {  // the writers count in int
+                    S.bail[lane] = 1;
+                    atomicAdd(err + 1, 1ULL);
+                }
+                if (it == ntile - 1) {  // match_total_length on the window
+                    long long residual = in.source_lengths[s] - total;
+                    const int t0 = ntile - FD > 0 ? ntile - FD : 0;
+                    const int64_t jlo = max(a, base + (int64_t)t0 * RT);
+                    for (int64_t j = b - 1; j >= jlo && residual != 0; --j) {
+                        const int64_t r = j - base;
+                        int32_t* qp = qrow + (int)((r / RT) % (FD + 1)) * RT + (int)(r % RT);
+                        long long adj = (long long)*qp + residual;
+                        if (adj < 1) adj = 1;
+                        residual -= adj - *qp;
+                        *qp = (int32_t)adj;
+                    }
+                    if (residual != 0) {
+                        if (jlo == a) {
+                            atomicMin(err, (unsigned long long)(s * 4 + kErrPiece));
+                        } else {
+                            S.bail[lane] = 1;
+                            atomicAdd(err + 1, 1ULL);
+                        }
+                    }
+                    // the window's tile positions after the cascade
+                    long long pp = S.pos[t0 % (FD + 1)][lane];
+                    for (int t = t0; t < ntile; ++t) {
+                        S.pos[t % (FD + 1)][lane] = pp;
+                        const int32_t* qq = qrow + (t % (FD + 1)) * RT;
+                        int32_t* xx = xrow + (t % (FD + 1)) * RT;
+                        long long ts = 0;
+                        for (int m = 0; m < RT; ++m) {
+                            xx[m] = (int)ts;
+                            ts += qq[m];
+                        }
+                        pp += ts;
+                        if (ts > kTileSamplesMax && !S.bail[lane]) {
+                            S.bail[lane] = 1;
+                            atomicAdd(err + 1, 1ULL);
+                        }
+                    }
+                }
+            }
+        } else {
+            const int t = it - FD;
+            if (t >= 0) {
+                const int h = lane >> 4, m = lane & 15;
+                const int slot = t % (FD + 1);
+                for (int L0 = 2 * (warp - 1); L0 < 32; L0 += 2 * FWW) {
+                    // lane per piece: a half-warp per segment
+                    const int L = L0 + h;
+                    const bool act = t < S.ntile[L] && !S.bail[L];
+                    const int r = L * FQ + slot * RT + m;
+                    const int q = act ? S.q[r] : 0;
+                    double vv = 0.0, inc = 0.0;
+                    long long P0 = 0, E = -1;
+                    if (q > 0) {
+                        vv = S.vs[r];
+                        const uint32_t lab = reinterpret_cast<const uint32_t*>(
+                            S.lab + L * FLSTR + (t % FS) * RT * 4)[m];
+                        inc = tinc[lab < (uint32_t)kk ? lab : 0u];
+                        P0 = S.pos[slot][L] + S.ex[r];
+                        E = S.E[L];
+                    }
+                    const int qmax = __reduce_max_sync(FULL, q);
+                    const int lim = min(qmax, kLanePiece);
+                    for (int i = 1; i <= lim; ++i) {
+                        const long long P = P0 + i - 1;
+                        if (i <= q && P <= E) {
+                            const double fr = q <= DIV_MAX ? S.div[q * (DIV_MAX + 1) + i]
+                                                           : (double)i / (double)q;
+                            out[P] = vv + inc * fr;
+                        }
+                    }
+                    if (qmax > kLanePiece) {  // long pieces: the warp writes 32 samples at a time
+                        unsigned lm = __ballot_sync(FULL, q > kLanePiece);
+                        while (lm) {
+                            const int src = __ffs(lm) - 1;
+                            lm &= lm - 1;
+                            const int qs = __shfl_sync(FULL, q, src);
+                            const long long ps = __shfl_sync(FULL, P0, src);
+                            const long long es = __shfl_sync(FULL, E, src);
+                            const double vs = __shfl_sync(FULL, vv, src);
+                            const double is = __shfl_sync(FULL, inc, src);
+                            for (int i = kLanePiece + 1 + lane; i <= qs; i += 32) {
+                                const long long P = ps + i - 1;
+                                if (P <= es) {
+                                    const double fr = qs <= DIV_MAX
+                                                          ? S.div[qs * (DIV_MAX + 1) + i]
+                                                          : (double)i / (double)qs;
+                                    out[P] = vs + is * fr;
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (warp == 0) {
+        if (s < in.n_seg && b == a) atomicMin(err, (unsigned long long)(s * 4 + kErrPiece));
+        if (badlab) atomicMin(err, (unsigned long long)(s * 4 + kErrLabel));
+    }
+}
+
 }  // namespace
 
-void inverse_transform_device(const InverseIn& in, double* d_out, cudaStream_t st) {
-    if (in.layout == 0 && in.n_seg == 0)
-        throw Error(INVALID_INPUT, "stitch_partitions: no segments");
-    const uint64_t kk = std::max<uint64_t>(in.k, 1);
-    DArr<double> tab(2 * kk, st);
-    DArr<unsigned long long> err(1, st);
-    const unsigned long long none = ~0ULL;
-    err.upload(&none, 1);
-    if (in.k > 0) {
-        k_inv_tables<<<(int)std::min<uint64_t>((in.k + 255) / 256, 1024), 256, 0, st>>>(
-            in.centers, in.mean_lengths, in.k, in.scl, in.sigma_len, in.sigma_inc, tab.p,
-            tab.p + kk);
-        JB_LAUNCH_CHECK();
-    }
+static void throw_inverse_error(unsigned long long e, uint64_t k) {
+    if (e == ~0ULL) return;
+    const long long seg = (long long)(e / 4);
+    if (e % 4 == kErrLabel)
+        throw Error(UNKNOWN_SYMBOL, "label not in codebook of size " + std::to_string(k) +
+                                        " (segment " + std::to_string(seg) + ")");
+    throw Error(INVALID_PIECE, "cannot fit pieces into the segment's steps (segment " +
+                                   std::to_string(seg) + ")");
+}
+
+// The general path: both chains write per-piece state (qlen, vstart), the
+// cascade and positions run per segment, and a piece-parallel pass fills.
+// Used when some segment's cascade reaches further back than the fused
+// kernel's window.
+static void inverse_general(const InverseIn& in, const double* tabp, uint64_t kk,
+                            DArr<unsigned long long>& err, double* d_out, cudaStream_t st) {
     // group layout (host: segment piece counts are needed anyway for the offsets)
     std::vector<int64_t> h_off(in.n_seg + 1), h_goff(in.n_seg + 1);
     JB_CUDA(cudaMemcpyAsync(h_off.data(), in.seg_offsets, sizeof(int64_t) * (in.n_seg + 1),
@@ -360,7 +650,7 @@ void inverse_transform_device(const InverseIn& in, double* d_out, cudaStream_t s
         if (tsmem + 64 * RSTRIDE > 48 * 1024)
             JB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)tsmem));
-        kern<<<(int)((in.n_seg + 31) / 32), 64, tsmem, st>>>(in, tab.p, tab.p + kk, qlen.p,
+        kern<<<(int)((in.n_seg + 31) / 32), 64, tsmem, st>>>(in, tabp, tabp + kk, qlen.p,
                                                               vstart.p, goff.p, gsum.p, err.p);
         JB_LAUNCH_CHECK();
         k_inv_segfix<<<(int)std::max<int64_t>(1, std::min<int64_t>((in.n_seg * 32 + 255) / 256,
@@ -371,27 +661,54 @@ void inverse_transform_device(const InverseIn& in, double* d_out, cudaStream_t s
     unsigned long long e;
     err.download(&e, 1);
     JB_CUDA(cudaStreamSynchronize(st));
-    if (e != ~0ULL) {
-        const long long seg = (long long)(e / 4);
-        if (e % 4 == kErrLabel)
-            throw Error(UNKNOWN_SYMBOL,
-                        "label not in codebook of size " + std::to_string(in.k) +
-                            " (segment " + std::to_string(seg) + ")");
-        throw Error(INVALID_PIECE, "cannot fit pieces into the segment's steps (segment " +
-                                       std::to_string(seg) + ")");
-    }
+    throw_inverse_error(e, in.k);
     if (n_groups > 0) {
         JB_PROF("inverse_fill", st);
         const size_t fsmem = sizeof(double) * kk <= kInvTabSmem / 2 ? sizeof(double) * kk : 0;
-        if (fsmem > 40 * 1024)
+        if (fsmem > 8 * 1024)  // 40 KB static (division table + staging rows)
             JB_CUDA(cudaFuncSetAttribute(k_inv_fill, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)fsmem));
         const int grid = (int)std::max<int64_t>(
-            1, std::min<int64_t>((n_groups * 32 + 255) / 256, (int64_t)kSMs * 16));
-        k_inv_fill<<<grid, 256, fsmem, st>>>(in, tab.p + kk, qlen.p, vstart.p, rec.p, gmeta.p,
+            1, std::min<int64_t>((n_groups * 32 + FILL_TB - 1) / FILL_TB, (int64_t)kSMs * 16));
+        k_inv_fill<<<grid, FILL_TB, fsmem, st>>>(in, tabp + kk, qlen.p, vstart.p, rec.p, gmeta.p,
                                              n_groups, d_out);
         JB_LAUNCH_CHECK();
     }
+}
+
+void inverse_transform_device(const InverseIn& in, double* d_out, cudaStream_t st) {
+    if (in.layout == 0 && in.n_seg == 0)
+        throw Error(INVALID_INPUT, "stitch_partitions: no segments");
+    const uint64_t kk = std::max<uint64_t>(in.k, 1);
+    DArr<double> tab(2 * kk, st);
+    DArr<unsigned long long> err(2, st);  // [0] lowest error code, [1] segments needing the general path
+    const unsigned long long init[2] = {~0ULL, 0ULL};
+    err.upload(init, 2);
+    if (in.k > 0) {
+        k_inv_tables<<<(int)std::min<uint64_t>((in.k + 255) / 256, 1024), 256, 0, st>>>(
+            in.centers, in.mean_lengths, in.k, in.scl, in.sigma_len, in.sigma_inc, tab.p,
+            tab.p + kk);
+        JB_LAUNCH_CHECK();
+    }
+    if (in.n_seg == 0) return;
+    unsigned long long h[2];
+    {
+        JB_PROF("inverse_fused", st);
+        const size_t tsmem = sizeof(double) * 2 * kk <= kInvTabSmem ? sizeof(double) * 2 * kk : 0;
+        const size_t smem = tsmem + sizeof(FusedSmem) + 128;
+        auto kern = tsmem ? k_inv_fused<true> : k_inv_fused<false>;
+        JB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<(int)((in.n_seg + 31) / 32), FUSED_TB, smem, st>>>(in, tab.p, tab.p + kk, d_out, err.p);
+        JB_LAUNCH_CHECK();
+        err.download(h, 2);
+        JB_CUDA(cudaStreamSynchronize(st));
+    }
+    if (h[1] != 0) {  // a cascade outside the window: redo everything on the general path
+        err.upload(init, 2);
+        inverse_general(in, tab.p, kk, err, d_out, st);
+        return;
+    }
+    throw_inverse_error(h[0], in.k);
 }
 
 }  // namespace jb
