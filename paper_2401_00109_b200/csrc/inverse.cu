@@ -12,6 +12,8 @@
 // output.
 #include <algorithm>
 
+#include <cub/device/device_scan.cuh>
+
 #include "jb_device.hpp"
 
 namespace jb {
@@ -329,41 +331,87 @@ __global__ void __launch_bounds__(FILL_TB) k_inv_fill(InverseIn in, const double
 }
 
 // ---- fused path (the common case) ----
-// One block = 32 segments. Warp 0 runs, one lane per segment, both
-// sequential chains in the reference's rounding -- the length carry
-// (quantize_lengths :63-74) and the start values (inverse_compress :94-101),
-// independent of each other so they overlap -- into rings of per-piece
-// quantized lengths and start values, plus each tile's first output
-// position. The writer warps trail it by FD tiles and emit every sample at
-// its final position: a half-warp per (segment, tile), lane m holding piece
-// m, samples assigned to lanes 16 at a time (coalesced stores), the piece of
-// a sample found by a 4-step search over the tile's exclusive length scan.
-// When a segment's last tile is done, warp 0 applies match_total_length's
-// backward cascade (:81-93) to the pieces still in the ring -- the cascade
-// only moves the tail, so every piece already written sits at its final
-// position -- and recomputes the window's tile positions. A cascade that
-// reaches past the window sends the call to the general path (err[1]).
-constexpr int FD = 4;                    // tiles between warp 0 and the writers (cascade window)
-constexpr int FRD = 6;                   // label tiles in flight
-constexpr int FS = FRD + FD;             // label ring tiles
-constexpr int FLSTR = FS * RT * 4 + 16;  // label ring bytes per lane
-constexpr int FQ = (FD + 1) * RT;        // ring entries per lane
-constexpr int FWW = 7;                   // writer warps
-constexpr int FUSED_TB = 32 * (1 + FWW);
-constexpr long long kTileSamplesMax = 1LL << 30;  // larger tiles: general path
-constexpr int kLanePiece = 8;  // pieces up to this length: lane per piece; longer: warp per piece
+// One block = 32 segments, three warp-specialized roles connected by
+// shared-memory rings with mbarrier full/empty handshakes, so each role runs
+// at its own pace and the carry chain -- the latency-bound critical path --
+// never waits on the others while the rings have room:
+//  * the value warp (warp 1), lane = segment, streams the labels through a
+//    cp.async ring, checks them (inverse_digitize_series :41-44), runs the
+//    start-value chain (inverse_compress :94-101) and looks up each piece's
+//    real length and increment;
+//  * the carry warp (warp 0), lane = segment, runs only the length-carry
+//    chain (quantize_lengths :63-74) on real lengths waiting in shared
+//    memory and records each piece's quantized length and last output
+//    position;
+//  * the writer warps store every sample at its final position, lane per
+//    piece: a piece's last sample v + inc * (q / q) is the next piece's start
+//    value (inc * 1.0 == inc), so the common one-sample piece costs a
+//    shared-memory load and a store; the other samples of longer pieces
+//    (v + inc * (i / q)) go through a flattened per-warp queue.
+// The last TAILT tiles of a segment are not written in the loop: their
+// lengths, start values and increments go to a global scratch, the carry warp
+// applies match_total_length's backward cascade (:81-93) there once the
+// segment's chain is done (the cascade moves only the tail, so every piece
+// written in the loop sits at its final position), and all warps write the
+// tails after the loop. A cascade reaching past the tail sends the call to
+// the general path (counted in err[1]).
+#ifndef JB_FUSED_NOWRITE
+#define JB_FUSED_NOWRITE 0
+#endif
+constexpr int FRD = 4;                    // label tiles in flight (value warp)
+constexpr int FLSTR = FRD * RT * 4 + 16;  // label ring bytes per lane
+constexpr int DL = 2, DQ = 2, DV = 4;     // ring depths: real lengths, quantized, start values
+constexpr int LVS = RT + 2;               // real-length row (padded: conflict-free 128-bit)
+constexpr int QPS = RT + 4;               // quantized-length / last-position row (padded)
+constexpr int VSS = RT + 1;               // (start value, increment) x RT + the value after
+constexpr int FDIV = 16;                  // exact i / q table for q <= FDIV
+constexpr int FWW = 4;                    // writer warps
+constexpr int FUSED_TB = 32 * (2 + FWW);
+constexpr int TAILT = 16;                 // tiles per segment left to the tail pass
+constexpr int WP = 16 / FWW;              // (segment, tile) half-warp pairs per writer warp
+constexpr int WQ = WP * 32;               // queue entries per writer warp
+constexpr int NBAR = 2 * (DL + DQ + DV);
 
-struct FusedSmem {
-    double div[(DIV_MAX + 1) * (DIV_MAX + 1)];
-    double vs[32 * FQ];       // start value of each piece
-    int32_t q[32 * FQ];       // quantized length of each piece (0: outside the segment)
-    int32_t ex[32 * FQ];      // its first sample's offset from the tile's first sample
-    long long pos[FD + 1][32];// output position of each tile's first sample
-    long long E[32];          // last output position of each segment
+struct FusedSmem {  // rows 16-byte aligned (cp.async, 128-bit accesses)
+    unsigned long long bar[NBAR];  // full / empty mbarriers of the three rings
+    unsigned char lab[32 * FLSTR];
+    double2 vs[DV][32 * VSS];
+    double lv[DL][32 * LVS];
+    int32_t q[DQ][32 * QPS];       // quantized length (0: nothing to write in the loop)
+    int32_t pe[DQ][32 * QPS];      // last output position, from the segment's anchor
+    double div[(FDIV + 1) * (FDIV + 1)];
+    double* ob[32];                // output address of each segment's anchor
+    int32_t E[32];                 // the segment's last position (-1: none)
     int ntile[32];
     int bail[32];
-    unsigned char lab[32 * FLSTR];
+    uint16_t wq[FWW][WQ];          // queued pieces: segment << 4 | piece
 };
+static_assert(32 * FLSTR % 16 == 0 && LVS * 8 % 16 == 0 && QPS * 4 % 16 == 0 && NBAR % 2 == 0,
+              "fused ring rows must stay 16-byte aligned");
+
+struct TailScratch {  // per segment (from off[s]): its tail pieces + 1
+    const int64_t* off;
+    int32_t* q;
+    int32_t* pe;
+    double* inc;
+    double* v;  // start values; the entry after the last piece: the value after it
+};
+
+// tail layout: the same integer expressions as k_inv_fused
+__device__ __forceinline__ int64_t tail_first_piece(int64_t a, int64_t b) {
+    const int64_t base = a & ~(int64_t)3;
+    const int ntile = b > a ? (int)((b - base + RT - 1) / RT) : 0;
+    const int tt0 = ntile > TAILT ? ntile - TAILT : 0;
+    return max(a, base + (int64_t)tt0 * RT);
+}
+__global__ void k_tail_sizes(const int64_t* __restrict__ seg_offsets, int64_t n_seg,
+                             int64_t* __restrict__ sz) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n_seg;
+         s += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a = seg_offsets[s], b = seg_offsets[s + 1];
+        sz[s] = b - tail_first_piece(a, b) + 1;
+    }
+}
 
 __device__ __forceinline__ void ring_issue_z(unsigned char* my, const uint32_t* __restrict__ labels,
                                              int64_t idx, int64_t n, int slot) {
@@ -379,11 +427,62 @@ __device__ __forceinline__ void ring_issue_z(unsigned char* my, const uint32_t* 
     }
 }
 
+__device__ __forceinline__ void mb_init(unsigned long long* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(b)),
+                 "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mb_arrive(unsigned long long* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(b))
+                 : "memory");
+}
+__device__ __forceinline__ void mb_wait(unsigned long long* b, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"((unsigned)__cvta_generic_to_shared(b)),
+        "r"(parity)
+        : "memory");
+}
+
+// A warp writes the samples of up to 32 pieces, lane per piece: q samples
+// ending at position pe (from the segment anchor at ob), the last one vnext,
+// the others vv + inc * (i / q); positions beyond E are dropped. (Tail pass.)
+__device__ __forceinline__ void emit_pieces(int q, int pe, int E, double* ob, double vnext,
+                                            double vv, double inc, const double* div) {
+    const unsigned FULL = 0xffffffffu;
+    if (q > 0 && pe <= E) ob[pe] = vnext;
+    const int qmax = __reduce_max_sync(FULL, q);
+    if (qmax <= 1) return;
+    const int lane = threadIdx.x & 31;
+    const unsigned mq = __ballot_sync(FULL, q > 1);
+    unsigned lm = mq;
+    while (lm) {  // a piece at a time, its other samples across the warp
+        const int src = __ffs(lm) - 1;
+        lm &= lm - 1;
+        const int qs = __shfl_sync(FULL, q, src);
+        const int ps = __shfl_sync(FULL, pe - q + 1, src);
+        const int es = __shfl_sync(FULL, E, src);
+        const double vs = __shfl_sync(FULL, vv, src);
+        const double is = __shfl_sync(FULL, inc, src);
+        double* os =
+            reinterpret_cast<double*>(__shfl_sync(FULL, reinterpret_cast<unsigned long long>(ob), src));
+        for (int i = 1 + lane; i < qs; i += 32)
+            if (ps + i - 1 <= es) {
+                const double fr = qs <= FDIV ? div[qs * (FDIV + 1) + i] : (double)i / (double)qs;
+                os[ps + i - 1] = vs + is * fr;
+            }
+    }
+}
+
 template <bool SMEM_TABS>
-__global__ void __launch_bounds__(FUSED_TB) k_inv_fused(InverseIn in, const double* __restrict__ rlen,
-                                                        const double* __restrict__ rinc,
-                                                        double* __restrict__ out,
-                                                        unsigned long long* __restrict__ err) {
+__global__ void __launch_bounds__(FUSED_TB, 3) k_inv_fused(InverseIn in, const double* __restrict__ rlen,
+                                                           const double* __restrict__ rinc,
+                                                           double* __restrict__ out, TailScratch tail,
+                                                           unsigned long long* __restrict__ err) {
     extern __shared__ __align__(128) unsigned char dsm[];
     const int kk = (int)in.k;
     const size_t toff = SMEM_TABS ? ((size_t)2 * kk * sizeof(double) + 127) & ~(size_t)127 : 0;
@@ -394,218 +493,348 @@ __global__ void __launch_bounds__(FUSED_TB) k_inv_fused(InverseIn in, const doub
             s_tabs[c] = rlen[c];
             s_tabs[kk + c] = rinc[c];
         }
-    for (int t = threadIdx.x; t < (DIV_MAX + 1) * (DIV_MAX + 1); t += blockDim.x) {
-        const int l = t / (DIV_MAX + 1), i = t % (DIV_MAX + 1);
+    for (int t = threadIdx.x; t < (FDIV + 1) * (FDIV + 1); t += blockDim.x) {
+        const int l = t / (FDIV + 1), i = t % (FDIV + 1);
         S.div[t] = l > 0 ? (double)i / (double)l : 0.0;  // the same IEEE division
+    }
+    unsigned long long* LVF = S.bar;
+    unsigned long long* LVE = LVF + DL;
+    unsigned long long* QF = LVE + DL;
+    unsigned long long* QE = QF + DQ;
+    unsigned long long* VF = QE + DQ;
+    unsigned long long* VE = VF + DV;
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < DL; ++k) {
+            mb_init(LVF + k, 32);
+            mb_init(LVE + k, 32);
+        }
+        for (int k = 0; k < DQ; ++k) {
+            mb_init(QF + k, 32);
+            mb_init(QE + k, 32 * FWW);
+        }
+        for (int k = 0; k < DV; ++k) {
+            mb_init(VF + k, 32);
+            mb_init(VE + k, 32 * FWW);
+        }
     }
     const double* tlen = SMEM_TABS ? s_tabs : rlen;
     const double* tinc = SMEM_TABS ? s_tabs + kk : rinc;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const unsigned FULL = 0xffffffffu;
 
-    // warp 0: lane = segment
+    // segment of this lane (carry and value warps)
     const int64_t s = blockIdx.x * (int64_t)32 + lane;
-    int64_t a = 0, b = 0, base = 0;
-    int ntile = 0;
-    double carry = 0.0, v = 0.0;
-    long long total = 0, pos = 0;
-    bool badlab = false;
-    unsigned char* lrow = S.lab + lane * FLSTR;
-    int32_t* qrow = S.q + lane * FQ;
-    int32_t* xrow = S.ex + lane * FQ;
-    double* vrow = S.vs + lane * FQ;
+    const bool live = s < in.n_seg;
+    int64_t a = 0, b = 0;
+    if (warp < 2 && live) {
+        a = in.seg_offsets[s];
+        b = in.seg_offsets[s + 1];
+    }
+    const int64_t base = a & ~(int64_t)3;  // 16-byte aligned label tiles
+    const int ntile = b > a ? (int)((b - base + RT - 1) / RT) : 0;
+    const int tt0 = ntile > TAILT ? ntile - TAILT : 0;    // first tail tile
+    const int64_t jlo = max(a, base + (int64_t)tt0 * RT);  // first tail piece
+    const int64_t tofs = live && warp < 2 ? tail.off[s] - jlo : 0;  // scratch index of piece j
     if (warp == 0) {
-        const bool live = s < in.n_seg;
         long long E = -1;
         if (live) {
-            a = in.seg_offsets[s];
-            b = in.seg_offsets[s + 1];
             const long long o = in.out_offsets[s];
             const bool drop = in.layout == 0 && (s + 1 < in.n_seg || in.drop_local_last);
-            E = o + in.source_lengths[s] - (drop ? 1 : 0);
-            v = in.anchors[s];
-            if (E >= o) out[o] = v;
-            pos = o + 1;
+            E = in.source_lengths[s] - (drop ? 1 : 0);
+            if (E >= 0) out[o] = in.anchors[s];
+            S.ob[lane] = out + o;
+        } else {
+            S.ob[lane] = out;
         }
-        base = a & ~(int64_t)3;  // 16-byte aligned label tiles
-        ntile = b > a ? (int)((b - base + RT - 1) / RT) : 0;
-        S.E[lane] = E;
+        S.E[lane] = (int32_t)(E < 0x7FFFFFFFLL ? E : 0);
         S.ntile[lane] = ntile;
-        S.bail[lane] = 0;
-        for (int t = 0; t < FRD - 1; ++t) {
-            if (t < ntile) ring_issue_z(lrow, in.labels, base + (int64_t)t * RT, in.N, t % FS);
-            ring_commit();
-        }
+        S.bail[lane] = E >= 0x7FFFFFFFLL;  // positions from the anchor are ints
     }
     __syncthreads();
     int maxT = 0;
     for (int l = 0; l < 32; ++l) maxT = max(maxT, S.ntile[l]);
-    auto lab_ok = [&](uint32_t lab) -> uint32_t {
-        const bool bad = lab >= (uint32_t)kk;
-        badlab |= bad;
-        return bad ? 0u : lab;
-    };
 
-    for (int it = 0; it < maxT + FD; ++it) {
-        if (warp == 0) {
+    if (warp == 1) {
+        // ---- value warp ----
+        unsigned char* lrow = S.lab + lane * FLSTR;
+        double v = live ? in.anchors[s] : 0.0;
+        bool badlab = false;
+        for (int t = 0; t < FRD - 1; ++t) {
+            if (t < ntile) ring_issue_z(lrow, in.labels, base + (int64_t)t * RT, in.N, t);
+            ring_commit();
+        }
+        for (int it = 0; it < maxT; ++it) {
+            const int k = it % DL, kv = it % DV;
+            mb_wait(LVE + k, ((it / DL) & 1) ^ 1);
+            mb_wait(VE + kv, ((it / DV) & 1) ^ 1);
+            const int tn = it + FRD - 1;
+            if (tn < ntile) ring_issue_z(lrow, in.labels, base + (int64_t)tn * RT, in.N, tn % FRD);
+            ring_commit();
+            ring_wait<FRD - 1>();  // tile it has landed
             if (it < ntile) {
-                const int tn = it + FRD - 1;
-                if (tn < ntile) ring_issue_z(lrow, in.labels, base + (int64_t)tn * RT, in.N, tn % FS);
-                ring_commit();
-                ring_wait<FRD - 1>();  // tile it has landed
-                const uint32_t* lt = reinterpret_cast<const uint32_t*>(lrow + (it % FS) * RT * 4);
-                const int slot = it % (FD + 1);
-                int32_t* qt = qrow + slot * RT;
-                int32_t* xt = xrow + slot * RT;
-                double* vt = vrow + slot * RT;
+                const uint32_t* lt = reinterpret_cast<const uint32_t*>(lrow + (it % FRD) * RT * 4);
+                double2* vt = S.vs[kv] + lane * VSS;
+                double* lv = S.lv[k] + lane * LVS;
                 const int64_t jt = base + (int64_t)it * RT;
-                S.pos[slot][lane] = pos;
-                long long tsum = 0;
                 if (jt >= a && jt + RT <= b) {
 #pragma unroll
-                    for (int m = 0; m < RT / 4; ++m) {
-                        const uint4 L = reinterpret_cast<const uint4*>(lt)[m];
-                        const uint32_t l0 = lab_ok(L.x), l1 = lab_ok(L.y), l2 = lab_ok(L.z),
-                                       l3 = lab_ok(L.w);
-                        int4 Q;
-                        chain_step(tlen[l0], carry, Q.x);
-                        chain_step(tlen[l1], carry, Q.y);
-                        chain_step(tlen[l2], carry, Q.z);
-                        chain_step(tlen[l3], carry, Q.w);
-                        reinterpret_cast<int4*>(qt)[m] = Q;
-                        int4 X;
-                        X.x = (int)tsum;
-                        X.y = X.x + Q.x;
-                        X.z = X.y + Q.y;
-                        X.w = X.z + Q.z;
-                        reinterpret_cast<int4*>(xt)[m] = X;
-                        tsum += (long long)Q.x + Q.y + Q.z + Q.w;
-                        const double v0 = v, v1 = v0 + tinc[l0], v2 = v1 + tinc[l1],
-                                     v3 = v2 + tinc[l2];
-                        v = v3 + tinc[l3];
-                        reinterpret_cast<double2*>(vt)[2 * m] = make_double2(v0, v1);
-                        reinterpret_cast<double2*>(vt)[2 * m + 1] = make_double2(v2, v3);
+                    for (int mm = 0; mm < RT / 4; ++mm) {
+                        const uint4 L = reinterpret_cast<const uint4*>(lt)[mm];
+                        uint32_t l[4] = {L.x, L.y, L.z, L.w};
+                        double inc[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            badlab |= l[e] >= (uint32_t)kk;
+                            l[e] = l[e] < (uint32_t)kk ? l[e] : 0u;
+                            inc[e] = tinc[l[e]];
+                        }
+                        reinterpret_cast<double2*>(lv)[2 * mm] = make_double2(tlen[l[0]], tlen[l[1]]);
+                        reinterpret_cast<double2*>(lv)[2 * mm + 1] =
+                            make_double2(tlen[l[2]], tlen[l[3]]);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            vt[4 * mm + e] = make_double2(v, inc[e]);
+                            v += inc[e];
+                        }
                     }
                 } else {
-                    for (int m = 0; m < RT; ++m) {
-                        const int64_t j = jt + m;
-                        int32_t q = 0;
-                        vt[m] = v;
+                    for (int mm = 0; mm < RT; ++mm) {
+                        const int64_t j = jt + mm;
+                        double inc = 0.0;
+                        lv[mm] = 0.0;
                         if (j >= a && j < b) {
-                            const uint32_t l = lab_ok(lt[m]);
-                            chain_step(tlen[l], carry, q);
-                            v += tinc[l];
+                            uint32_t l = lt[mm];
+                            badlab |= l >= (uint32_t)kk;
+                            l = l < (uint32_t)kk ? l : 0u;
+                            lv[mm] = tlen[l];
+                            inc = tinc[l];
                         }
-                        qt[m] = q;
-                        xt[m] = (int)tsum;
-                        tsum += q;
+                        vt[mm] = make_double2(v, inc);
+                        v += inc;
                     }
                 }
-                total += tsum;
-                pos += tsum;
-                if (tsum > kTileSamplesMax && !S.bail[lane]) {  // the writers count in int
-                    S.bail[lane] = 1;
-                    atomicAdd(err + 1, 1ULL);
+                vt[RT] = make_double2(v, 0.0);  // the start value after the tile
+                if (it >= tt0) {  // tail tile: start values and increments to the scratch
+                    for (int mm = 0; mm < RT; ++mm) {
+                        const int64_t j = jt + mm;
+                        if (j >= jlo && j < b) {
+                            tail.v[tofs + j] = vt[mm].x;
+                            tail.inc[tofs + j] = vt[mm].y;
+                        }
+                    }
+                    if (it == ntile - 1) tail.v[tofs + b] = v;
                 }
-                if (it == ntile - 1) {  // match_total_length on the window
-                    long long residual = in.source_lengths[s] - total;
-                    const int t0 = ntile - FD > 0 ? ntile - FD : 0;
-                    const int64_t jlo = max(a, base + (int64_t)t0 * RT);
-                    for (int64_t j = b - 1; j >= jlo && residual != 0; --j) {
-                        const int64_t r = j - base;
-                        int32_t* qp = qrow + (int)((r / RT) % (FD + 1)) * RT + (int)(r % RT);
-                        long long adj = (long long)*qp + residual;
-                        if (adj < 1) adj = 1;
-                        residual -= adj - *qp;
-                        *qp = (int32_t)adj;
-                    }
-                    if (residual != 0) {
-                        if (jlo == a) {
-                            atomicMin(err, (unsigned long long)(s * 4 + kErrPiece));
-                        } else {
-                            S.bail[lane] = 1;
-                            atomicAdd(err + 1, 1ULL);
-                        }
-                    }
-                    // the window's tile positions after the cascade
-                    long long pp = S.pos[t0 % (FD + 1)][lane];
-                    for (int t = t0; t < ntile; ++t) {
-                        S.pos[t % (FD + 1)][lane] = pp;
-                        const int32_t* qq = qrow + (t % (FD + 1)) * RT;
-                        int32_t* xx = xrow + (t % (FD + 1)) * RT;
-                        long long ts = 0;
-                        for (int m = 0; m < RT; ++m) {
-                            xx[m] = (int)ts;
-                            ts += qq[m];
-                        }
-                        pp += ts;
-                        if (ts > kTileSamplesMax && !S.bail[lane]) {
-                            S.bail[lane] = 1;
-                            atomicAdd(err + 1, 1ULL);
-                        }
+            }
+            mb_arrive(LVF + k);
+            mb_arrive(VF + kv);
+        }
+        if (badlab) atomicMin(err, (unsigned long long)(s * 4 + kErrLabel));
+    } else if (warp == 0) {
+        // ---- carry warp ----
+        double carry = 0.0;
+        long long total = 0, pos = 1, pos_tail = 1;  // positions from the anchor
+        bool bail = S.bail[lane];
+        if (bail) atomicAdd(err + 1, 1ULL);
+        auto do_bail = [&]() {
+            if (!bail) {
+                bail = true;
+                atomicAdd(err + 1, 1ULL);
+            }
+        };
+        for (int it = 0; it < maxT; ++it) {
+            const int k = it % DL, kq = it % DQ;
+            mb_wait(LVF + k, (it / DL) & 1);
+            double l[RT];
+            const double* lv = S.lv[k] + lane * LVS;
+#pragma unroll
+            for (int mm = 0; mm < RT / 2; ++mm) {
+                const double2 d = reinterpret_cast<const double2*>(lv)[mm];
+                l[2 * mm] = d.x;
+                l[2 * mm + 1] = d.y;
+            }
+            mb_arrive(LVE + k);
+            int32_t* qt = S.q[kq] + lane * QPS;
+            int32_t* pt = S.pe[kq] + lane * QPS;
+            int32_t Q[RT];
+            const int64_t jt = base + (int64_t)it * RT;
+            if (it < ntile) {
+                if (it == tt0) pos_tail = pos;
+                if (jt >= a && jt + RT <= b) {
+#pragma unroll
+                    for (int mm = 0; mm < RT; ++mm) chain_step(l[mm], carry, Q[mm]);
+                } else {
+                    for (int mm = 0; mm < RT; ++mm) {
+                        const int64_t j = jt + mm;
+                        Q[mm] = 0;
+                        if (j >= a && j < b) chain_step(l[mm], carry, Q[mm]);
                     }
                 }
             }
-        } else {
-            const int t = it - FD;
-            if (t >= 0) {
-                const int h = lane >> 4, m = lane & 15;
-                const int slot = t % (FD + 1);
-                for (int L0 = 2 * (warp - 1); L0 < 32; L0 += 2 * FWW) {
-                    // lane per piece: a half-warp per segment
-                    const int L = L0 + h;
-                    const bool act = t < S.ntile[L] && !S.bail[L];
-                    const int r = L * FQ + slot * RT + m;
-                    const int q = act ? S.q[r] : 0;
-                    double vv = 0.0, inc = 0.0;
-                    long long P0 = 0, E = -1;
-                    if (q > 0) {
-                        vv = S.vs[r];
-                        const uint32_t lab = reinterpret_cast<const uint32_t*>(
-                            S.lab + L * FLSTR + (t % FS) * RT * 4)[m];
-                        inc = tinc[lab < (uint32_t)kk ? lab : 0u];
-                        P0 = S.pos[slot][L] + S.ex[r];
-                        E = S.E[L];
+            mb_wait(QE + kq, ((it / DQ) & 1) ^ 1);
+            if (it < tt0 && !bail) {
+#pragma unroll
+                for (int mm = 0; mm < RT / 4; ++mm) {
+                    int4 q4, p4;
+                    q4.x = Q[4 * mm];
+                    q4.y = Q[4 * mm + 1];
+                    q4.z = Q[4 * mm + 2];
+                    q4.w = Q[4 * mm + 3];
+                    p4.x = (int)(pos += q4.x) - 1;
+                    p4.y = (int)(pos += q4.y) - 1;
+                    p4.z = (int)(pos += q4.z) - 1;
+                    p4.w = (int)(pos += q4.w) - 1;
+                    reinterpret_cast<int4*>(qt)[mm] = q4;
+                    reinterpret_cast<int4*>(pt)[mm] = p4;
+                }
+            } else {  // tail tile, finished or bailed segment: nothing to write in the loop
+#pragma unroll
+                for (int mm = 0; mm < RT / 4; ++mm)
+                    reinterpret_cast<int4*>(qt)[mm] = make_int4(0, 0, 0, 0);
+                if (it < ntile) {
+#pragma unroll
+                    for (int mm = 0; mm < RT; ++mm) {
+                        const int64_t j = jt + mm;
+                        if (it >= tt0 && j >= jlo && j < b) tail.q[tofs + j] = Q[mm];
+                        pos += Q[mm];
                     }
-                    const int qmax = __reduce_max_sync(FULL, q);
-                    const int lim = min(qmax, kLanePiece);
-                    for (int i = 1; i <= lim; ++i) {
-                        const long long P = P0 + i - 1;
-                        if (i <= q && P <= E) {
-                            const double fr = q <= DIV_MAX ? S.div[q * (DIV_MAX + 1) + i]
-                                                           : (double)i / (double)q;
-                            out[P] = vv + inc * fr;
-                        }
+                }
+            }
+            mb_arrive(QF + kq);
+            if (it < ntile) {
+                if (pos > 0x7FFFFFFFLL) do_bail();
+                if (it == ntile - 1) {  // match_total_length on the tail
+                    total = pos - 1;
+                    long long residual = in.source_lengths[s] - total;
+                    int32_t* tq = tail.q + tofs;  // indexed by piece
+                    for (int64_t j = b - 1; j >= jlo && residual != 0; --j) {
+                        long long adj = (long long)tq[j] + residual;
+                        if (adj < 1) adj = 1;
+                        residual -= adj - tq[j];
+                        tq[j] = (int32_t)adj;
                     }
-                    if (qmax > kLanePiece) {  // long pieces: the warp writes 32 samples at a time
-                        unsigned lm = __ballot_sync(FULL, q > kLanePiece);
-                        while (lm) {
-                            const int src = __ffs(lm) - 1;
-                            lm &= lm - 1;
-                            const int qs = __shfl_sync(FULL, q, src);
-                            const long long ps = __shfl_sync(FULL, P0, src);
-                            const long long es = __shfl_sync(FULL, E, src);
-                            const double vs = __shfl_sync(FULL, vv, src);
-                            const double is = __shfl_sync(FULL, inc, src);
-                            for (int i = kLanePiece + 1 + lane; i <= qs; i += 32) {
-                                const long long P = ps + i - 1;
-                                if (P <= es) {
-                                    const double fr = qs <= DIV_MAX
-                                                          ? S.div[qs * (DIV_MAX + 1) + i]
-                                                          : (double)i / (double)qs;
-                                    out[P] = vs + is * fr;
-                                }
-                            }
-                        }
+                    if (residual != 0) {
+                        if (jlo == a) atomicMin(err, (unsigned long long)(s * 4 + kErrPiece));
+                        else do_bail();
                     }
+                    long long pp = pos_tail;
+                    int32_t* tp = tail.pe + tofs;
+                    for (int64_t j = jlo; j < b; ++j) {
+                        pp += tq[j];
+                        tp[j] = (int32_t)(pp - 1);
+                    }
+                    if (pp > 0x7FFFFFFFLL) do_bail();
                 }
             }
         }
-        __syncthreads();
+        (void)total;
+        if (live && b == a) atomicMin(err, (unsigned long long)(s * 4 + kErrPiece));
+        S.bail[lane] = bail;
+    } else if (!JB_FUSED_NOWRITE) {
+        // ---- writer warps: lane m of half h holds piece m of segment L ----
+        const int wi = warp - 2, m = lane & 15;
+        int wE[WP];
+        double* wout[WP];
+#pragma unroll
+        for (int k = 0; k < WP; ++k) {
+            const int L = 2 * wi + (lane >> 4) + 2 * FWW * k;
+            wE[k] = S.E[L];
+            wout[k] = S.ob[L];
+        }
+        for (int it = 0; it < maxT; ++it) {
+            const int kq = it % DQ, kv = it % DV;
+            mb_wait(QF + kq, (it / DQ) & 1);
+            mb_wait(VF + kv, (it / DV) & 1);
+            int nq = 0;
+#pragma unroll
+            for (int k = 0; k < WP; ++k) {
+                const int L = 2 * wi + (lane >> 4) + 2 * FWW * k;
+                const int q = S.q[kq][L * QPS + m];
+                if (q > 0) {
+                    const int pe = S.pe[kq][L * QPS + m];
+                    if (pe <= wE[k]) wout[k][pe] = S.vs[kv][L * VSS + m + 1].x;
+                }
+                const unsigned mq = __ballot_sync(0xffffffffu, q > 1);
+                if (q > 1) S.wq[wi][nq + __popc(mq & ((1u << lane) - 1u))] = (uint16_t)(L << 4 | m);
+                nq += __popc(mq);
+            }
+            __syncwarp();
+            // the other samples of the queued pieces, flattened over the warp
+            for (int e0 = 0; e0 < nq; e0 += 32) {
+                const int e = e0 + lane;
+                const int ent = e < nq ? S.wq[wi][e] : 0;
+                const int cnt = e < nq ? S.q[kq][(ent >> 4) * QPS + (ent & 15)] - 1 : 0;
+                int incl = cnt;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                const int ex = incl - cnt;
+                const int tot = __shfl_sync(0xffffffffu, incl, 31);
+                for (int c0 = 0; c0 < tot; c0 += 32) {
+                    const int c = c0 + lane;
+                    int p = 0;  // last entry with ex <= c: the one holding sample c
+#pragma unroll
+                    for (int st = 16; st > 0; st >>= 1) {
+                        const int x = __shfl_sync(0xffffffffu, ex, p + st);
+                        if (x <= c) p += st;
+                    }
+                    const int xp = __shfl_sync(0xffffffffu, ex, p);
+                    const int en = __shfl_sync(0xffffffffu, ent, p);
+                    if (c < tot) {
+                        const int L = en >> 4, mm = en & 15;
+                        const int q = S.q[kq][L * QPS + mm];
+                        const int P0 = S.pe[kq][L * QPS + mm] - q + 1;
+                        const int i = c - xp + 1;  // 1 .. q-1
+                        if (P0 + i - 1 <= S.E[L]) {
+                            const double2 vi = S.vs[kv][L * VSS + mm];
+                            const double fr =
+                                q <= FDIV ? S.div[q * (FDIV + 1) + i] : (double)i / (double)q;
+                            S.ob[L][P0 + i - 1] = vi.x + vi.y * fr;
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            mb_arrive(QE + kq);
+            mb_arrive(VE + kv);
+        }
     }
-    if (warp == 0) {
-        if (s < in.n_seg && b == a) atomicMin(err, (unsigned long long)(s * 4 + kErrPiece));
-        if (badlab) atomicMin(err, (unsigned long long)(s * 4 + kErrLabel));
+    if (JB_FUSED_NOWRITE && warp >= 2) {  // keep the handshakes balanced
+        for (int it = 0; it < maxT; ++it) {
+            mb_wait(QF + it % DQ, (it / DQ) & 1);
+            mb_wait(VF + it % DV, (it / DV) & 1);
+            mb_arrive(QE + it % DQ);
+            mb_arrive(VE + it % DV);
+        }
+    }
+    __syncthreads();
+    if (warp == 0) S.ntile[lane] = (int)(live && b > a ? b - jlo : 0);  // tail pieces
+    __syncthreads();
+    if (JB_FUSED_NOWRITE) return;
+    // tail pass: a warp per segment, lane per piece
+    constexpr int NW = FUSED_TB / 32;
+    for (int L = warp; L < 32; L += NW) {
+        const int64_t sg = blockIdx.x * (int64_t)32 + L;
+        const int cnt = S.ntile[L];
+        if (S.bail[L] || cnt == 0) continue;
+        const int E = S.E[L];
+        double* ob = S.ob[L];
+        const int64_t so = tail.off[sg];
+        for (int c = 0; c < cnt; c += 32) {
+            const int64_t u = so + c + lane;
+            int q = 0, pe = 0;
+            double vn = 0.0, vv = 0.0, inc = 0.0;
+            if (c + lane < cnt) {
+                q = tail.q[u];
+                pe = tail.pe[u];
+                vn = tail.v[u + 1];
+                if (q > 1) {
+                    vv = tail.v[u];
+                    inc = tail.inc[u];
+                }
+            }
+            emit_pieces(q, pe, E, ob, vn, vv, inc, S.div);
+        }
     }
 }
 
@@ -698,7 +927,24 @@ void inverse_transform_device(const InverseIn& in, double* d_out, cudaStream_t s
         const size_t smem = tsmem + sizeof(FusedSmem) + 128;
         auto kern = tsmem ? k_inv_fused<true> : k_inv_fused<false>;
         JB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kern<<<(int)((in.n_seg + 31) / 32), FUSED_TB, smem, st>>>(in, tab.p, tab.p + kk, d_out, err.p);
+        // tail scratch offsets: exclusive scan of (tail pieces + 1)
+        DArr<int64_t> tsz(in.n_seg + 1, st), toff(in.n_seg + 1, st);
+        k_tail_sizes<<<(int)std::min<int64_t>((in.n_seg + 255) / 256, 4096), 256, 0, st>>>(
+            in.seg_offsets, in.n_seg, tsz.p);
+        JB_LAUNCH_CHECK();
+        JB_CUDA(cudaMemsetAsync(tsz.p + in.n_seg, 0, sizeof(int64_t), st));
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, tsz.p, toff.p, in.n_seg + 1, st);
+        DArr<uint8_t> tmp(tb, st);
+        cub::DeviceScan::ExclusiveSum(tmp.p, tb, tsz.p, toff.p, in.n_seg + 1, st);
+        int64_t ntail = 0;
+        JB_CUDA(cudaMemcpyAsync(&ntail, toff.p + in.n_seg, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        JB_CUDA(cudaStreamSynchronize(st));
+        DArr<int32_t> tq(ntail, st), tpe(ntail, st);
+        DArr<double> tinc(ntail, st), tv(ntail, st);
+        const TailScratch tail{toff.p, tq.p, tpe.p, tinc.p, tv.p};
+        kern<<<(int)((in.n_seg + 31) / 32), FUSED_TB, smem, st>>>(in, tab.p, tab.p + kk, d_out,
+                                                                   tail, err.p);
         JB_LAUNCH_CHECK();
         err.download(h, 2);
         JB_CUDA(cudaStreamSynchronize(st));

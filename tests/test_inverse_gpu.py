@@ -61,6 +61,8 @@ def test_inverse_deep_cascade(engine, oracle, layout):
     rng = np.random.default_rng(7 + layout)
     f = _case(rng, 64, 400, 30, 0.0, lambda q, n: max(n, q // 3))
     _compare(engine, oracle, f, layout)
+    f = _case(rng, 40, 3000, 30, 0.0, lambda q, n: max(n, q - int(rng.integers(0, 400))))
+    _compare(engine, oracle, f, layout)
 
 
 def test_inverse_long_pieces(engine, oracle):

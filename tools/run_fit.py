@@ -18,6 +18,8 @@ ap.add_argument("--scale", type=float, default=0.1)
 ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--profile", action="store_true")
 a = ap.parse_args()
+if os.environ.get("JB_LIB"):  # an experimental build of the library
+    _native.LIB_PATH = os.environ["JB_LIB"]
 n = int(round(1e9 * a.scale))
 m = max(1, int(round(10000 * a.scale)))
 x = make_series_gpu(n, 0, torch.device("cuda", 0))
