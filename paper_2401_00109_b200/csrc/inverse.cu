@@ -358,6 +358,20 @@ __global__ void __launch_bounds__(FILL_TB) k_inv_fill(InverseIn in, const double
 #ifndef JB_FUSED_NOWRITE
 #define JB_FUSED_NOWRITE 0
 #endif
+#ifndef JB_FUSED_PROF  // experiment builds: per-role busy / waiting cycles
+#define JB_FUSED_PROF 0
+#endif
+#if JB_FUSED_PROF
+__device__ unsigned long long g_fused_prof[8];
+#define FP_WAIT(call)                                \
+    do {                                             \
+        const long long t0_ = clock64();             \
+        call;                                        \
+        fp_wait += clock64() - t0_;                  \
+    } while (0)
+#else
+#define FP_WAIT(call) call
+#endif
 constexpr int FRD = 4;                    // label tiles in flight (value warp)
 constexpr int FLSTR = FRD * RT * 4 + 16;  // label ring bytes per lane
 constexpr int DL = 2, DQ = 2, DV = 4;     // ring depths: real lengths, quantized, start values
@@ -380,7 +394,7 @@ struct FusedSmem {  // rows 16-byte aligned (cp.async, 128-bit accesses)
     int32_t q[DQ][32 * QPS];       // quantized length (0: nothing to write in the loop)
     int32_t pe[DQ][32 * QPS];      // last output position, from the segment's anchor
     double div[(FDIV + 1) * (FDIV + 1)];
-    double* ob[32];                // output address of each segment's anchor
+    long long oo[32];              // output index of each segment's anchor
     int32_t E[32];                 // the segment's last position (-1: none)
     int ntile[32];
     int bail[32];
@@ -442,9 +456,9 @@ __device__ __forceinline__ void mb_wait(unsigned long long* b, unsigned parity) 
     asm volatile(
         "{\n .reg .pred p;\n"
         "WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
         " @!p bra WAIT_%=;\n}\n" ::"r"((unsigned)__cvta_generic_to_shared(b)),
-        "r"(parity)
+        "r"(parity), "r"(0x989680u)  // suspend-time hint: sleep instead of spinning
         : "memory");
 }
 
@@ -541,9 +555,9 @@ __global__ void __launch_bounds__(FUSED_TB, 3) k_inv_fused(InverseIn in, const d
             const bool drop = in.layout == 0 && (s + 1 < in.n_seg || in.drop_local_last);
             E = in.source_lengths[s] - (drop ? 1 : 0);
             if (E >= 0) out[o] = in.anchors[s];
-            S.ob[lane] = out + o;
+            S.oo[lane] = o;
         } else {
-            S.ob[lane] = out;
+            S.oo[lane] = 0;
         }
         S.E[lane] = (int32_t)(E < 0x7FFFFFFFLL ? E : 0);
         S.ntile[lane] = ntile;
@@ -553,6 +567,9 @@ __global__ void __launch_bounds__(FUSED_TB, 3) k_inv_fused(InverseIn in, const d
     int maxT = 0;
     for (int l = 0; l < 32; ++l) maxT = max(maxT, S.ntile[l]);
 
+    long long fp_wait = 0, fp_t0 = clock64();
+    (void)fp_wait;
+    (void)fp_t0;
     if (warp == 1) {
         // ---- value warp ----
         unsigned char* lrow = S.lab + lane * FLSTR;
@@ -564,8 +581,8 @@ __global__ void __launch_bounds__(FUSED_TB, 3) k_inv_fused(InverseIn in, const d
         }
         for (int it = 0; it < maxT; ++it) {
             const int k = it % DL, kv = it % DV;
-            mb_wait(LVE + k, ((it / DL) & 1) ^ 1);
-            mb_wait(VE + kv, ((it / DV) & 1) ^ 1);
+            FP_WAIT(mb_wait(LVE + k, ((it / DL) & 1) ^ 1));
+            FP_WAIT(mb_wait(VE + kv, ((it / DV) & 1) ^ 1));
             const int tn = it + FRD - 1;
             if (tn < ntile) ring_issue_z(lrow, in.labels, base + (int64_t)tn * RT, in.N, tn % FRD);
             ring_commit();
@@ -642,7 +659,7 @@ __global__ void __launch_bounds__(FUSED_TB, 3) k_inv_fused(InverseIn in, const d
         };
         for (int it = 0; it < maxT; ++it) {
             const int k = it % DL, kq = it % DQ;
-            mb_wait(LVF + k, (it / DL) & 1);
+            FP_WAIT(mb_wait(LVF + k, (it / DL) & 1));
             double l[RT];
             const double* lv = S.lv[k] + lane * LVS;
 #pragma unroll
@@ -669,7 +686,7 @@ __global__ void __launch_bounds__(FUSED_TB, 3) k_inv_fused(InverseIn in, const d
                     }
                 }
             }
-            mb_wait(QE + kq, ((it / DQ) & 1) ^ 1);
+            FP_WAIT(mb_wait(QE + kq, ((it / DQ) & 1) ^ 1));
             if (it < tt0 && !bail) {
 #pragma unroll
                 for (int mm = 0; mm < RT / 4; ++mm) {
@@ -737,12 +754,12 @@ __global__ void __launch_bounds__(FUSED_TB, 3) k_inv_fused(InverseIn in, const d
         for (int k = 0; k < WP; ++k) {
             const int L = 2 * wi + (lane >> 4) + 2 * FWW * k;
             wE[k] = S.E[L];
-            wout[k] = S.ob[L];
+            wout[k] = out + S.oo[L];  // derived from the kernel argument: global stores
         }
         for (int it = 0; it < maxT; ++it) {
             const int kq = it % DQ, kv = it % DV;
-            mb_wait(QF + kq, (it / DQ) & 1);
-            mb_wait(VF + kv, (it / DV) & 1);
+            FP_WAIT(mb_wait(QF + kq, (it / DQ) & 1));
+            FP_WAIT(mb_wait(VF + kv, (it / DV) & 1));
             int nq = 0;
 #pragma unroll
             for (int k = 0; k < WP; ++k) {
@@ -789,7 +806,7 @@ __global__ void __launch_bounds__(FUSED_TB, 3) k_inv_fused(InverseIn in, const d
                             const double2 vi = S.vs[kv][L * VSS + mm];
                             const double fr =
                                 q <= FDIV ? S.div[q * (FDIV + 1) + i] : (double)i / (double)q;
-                            S.ob[L][P0 + i - 1] = vi.x + vi.y * fr;
+                            out[S.oo[L] + P0 + i - 1] = vi.x + vi.y * fr;
                         }
                     }
                 }
@@ -807,6 +824,13 @@ __global__ void __launch_bounds__(FUSED_TB, 3) k_inv_fused(InverseIn in, const d
             mb_arrive(VE + it % DV);
         }
     }
+#if JB_FUSED_PROF
+    if (lane == 0) {
+        const int role = warp < 2 ? warp : 2;
+        atomicAdd(&g_fused_prof[2 * role], (unsigned long long)(clock64() - fp_t0));
+        atomicAdd(&g_fused_prof[2 * role + 1], (unsigned long long)fp_wait);
+    }
+#endif
     __syncthreads();
     if (warp == 0) S.ntile[lane] = (int)(live && b > a ? b - jlo : 0);  // tail pieces
     __syncthreads();
@@ -818,7 +842,7 @@ __global__ void __launch_bounds__(FUSED_TB, 3) k_inv_fused(InverseIn in, const d
         const int cnt = S.ntile[L];
         if (S.bail[L] || cnt == 0) continue;
         const int E = S.E[L];
-        double* ob = S.ob[L];
+        double* ob = out + S.oo[L];
         const int64_t so = tail.off[sg];
         for (int c = 0; c < cnt; c += 32) {
             const int64_t u = so + c + lane;
@@ -949,6 +973,18 @@ void inverse_transform_device(const InverseIn& in, double* d_out, cudaStream_t s
         err.download(h, 2);
         JB_CUDA(cudaStreamSynchronize(st));
     }
+#if JB_FUSED_PROF
+    {
+        unsigned long long pr[8];
+        JB_CUDA(cudaMemcpyFromSymbol(pr, g_fused_prof, sizeof(pr)));
+        const double nb = (double)((in.n_seg + 31) / 32);
+        fprintf(stderr, "[jb] fused roles (Mcycles per block): carry %.2f (wait %.2f) value %.2f (wait %.2f) writers %.2f (wait %.2f)\n",
+                pr[0] / nb / 1e6, pr[1] / nb / 1e6, pr[2] / nb / 1e6, pr[3] / nb / 1e6,
+                pr[4] / nb / FWW / 1e6, pr[5] / nb / FWW / 1e6);
+        const unsigned long long z[8] = {};
+        JB_CUDA(cudaMemcpyToSymbol(g_fused_prof, z, sizeof(z)));
+    }
+#endif
     if (h[1] != 0) {  // a cascade outside the window: redo everything on the general path
         err.upload(init, 2);
         inverse_general(in, tab.p, kk, err, d_out, st);
