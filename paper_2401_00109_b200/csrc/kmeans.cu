@@ -451,14 +451,14 @@ __device__ __forceinline__ double2 load_pt(const double2* __restrict__ pts,
 __global__ void k_morton(const PtsView pv, const uint64_t* __restrict__ idx,
                          int64_t n, double x0, double sx, double y0, double sy,
                          uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                         double2* __restrict__ cpts, const int32_t* __restrict__ len,
-                         int32_t* __restrict__ clen) {
+                         double2* __restrict__ cpts, const int32_t* __restrict__ len) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t src = idx ? idx[i] : (uint64_t)i;
         const double2 p = pv.at(src);
-        cpts[i] = p;
-        if (len) clen[i] = len[src];
+        // with piece lengths the record carries (length, y): x is the length's
+        // row coordinate (pv.at's expression), recomputed in the sorted gather
+        cpts[i] = len ? make_double2((double)len[src], p.y) : p;
         const uint32_t qx = (uint32_t)fmin(fmax((p.x - x0) * sx, 0.0), 65535.0);
         const uint32_t qy = (uint32_t)fmin(fmax((p.y - y0) * sy, 0.0), 65535.0);
         keys[i] = spread16(qx) | (spread16(qy) << 1);
@@ -466,16 +466,22 @@ __global__ void k_morton(const PtsView pv, const uint64_t* __restrict__ idx,
     }
 }
 
-__global__ void k_sorted_gather(const double2* __restrict__ pts, const uint64_t* __restrict__ idx,
-                                const uint32_t* __restrict__ orig, int64_t n,
-                                double2* __restrict__ spts, uint32_t* __restrict__ pos,
-                                const int32_t* __restrict__ len, int32_t* __restrict__ slen) {
+// one random 16-byte record read per point (plus the pos scatter)
+__global__ void k_sorted_gather(const double2* __restrict__ cpts, const uint32_t* __restrict__ orig,
+                                int64_t n, double2* __restrict__ spts, uint32_t* __restrict__ pos,
+                                double scl, double sl, int32_t* __restrict__ slen) {
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
          r += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t o = orig[r];
-        spts[r] = load_pt(pts, idx, o);
+        const double2 c = cpts[o];
+        if (slen) {
+            const int32_t l = (int32_t)c.x;
+            spts[r] = make_double2(scl * (double)l / sl, c.y);
+            slen[r] = l;
+        } else {
+            spts[r] = c;
+        }
         pos[o] = (uint32_t)r;
-        if (len) slen[r] = len[idx ? idx[o] : o];
     }
 }
 
@@ -1798,9 +1804,8 @@ void lloyd_best_device(const PtsView& pv, const uint64_t* d_idx, int64_t n, uint
         DArr<uint32_t> keys(n, st), skeys(n, st), vals(n, st);
         const double sx = wx > 0 ? 65535.0 / wx : 0.0, sy = wy > 0 ? 65535.0 / wy : 0.0;
         DArr<double2> cpts(n, st);
-        DArr<int32_t> clen(rows.len ? n : 0, st);
         k_morton<<<grid_cap(n), 256, 0, st>>>(pv, d_idx, n, bb.xmin, sx, bb.ymin, sy, keys.p,
-                                              vals.p, cpts.p, rows.len, clen.p);
+                                              vals.p, cpts.p, rows.len);
         JB_LAUNCH_CHECK();
         size_t tb = 0;
         cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.p, skeys.p, vals.p, orig.p, n, 0, 32,
@@ -1808,8 +1813,8 @@ void lloyd_best_device(const PtsView& pv, const uint64_t* d_idx, int64_t n, uint
         DArr<uint8_t> tmp(tb, st);
         cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.p, skeys.p, vals.p, orig.p, n, 0, 32, st);
         JB_LAUNCH_CHECK();
-        k_sorted_gather<<<grid_cap(n), 256, 0, st>>>(cpts.p, nullptr, orig.p, n, spts.p, pos.p,
-                                                     rows.len ? clen.p : nullptr, slen.p);
+        k_sorted_gather<<<grid_cap(n), 256, 0, st>>>(cpts.p, orig.p, n, spts.p, pos.p, pv.scl,
+                                                     pv.sl, rows.len ? slen.p : nullptr);
         JB_LAUNCH_CHECK();
     }
     JB_TRACE("kmeans: morton order", st);
@@ -2176,17 +2181,16 @@ void lloyd_best_dist(const Comm& cm, const PtsView& pv, const uint64_t* d_lidx,
         DArr<uint32_t> keys(n, st), skeys(n, st), vals(n, st);
         const double sx = wx > 0 ? 65535.0 / wx : 0.0, sy = wy > 0 ? 65535.0 / wy : 0.0;
         DArr<double2> cpts(n, st);
-        DArr<int32_t> clen(rows.len ? n : 0, st);
         k_morton<<<grid_cap(n), 256, 0, st>>>(pv, d_lidx, n, bb.xmin, sx, bb.ymin, sy, keys.p,
-                                              vals.p, cpts.p, rows.len, clen.p);
+                                              vals.p, cpts.p, rows.len);
         JB_LAUNCH_CHECK();
         size_t tb = 0;
         cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.p, skeys.p, vals.p, orig.p, n, 0, 32,
                                         st);
         DArr<uint8_t> tmp(tb, st);
         cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.p, skeys.p, vals.p, orig.p, n, 0, 32, st);
-        k_sorted_gather<<<grid_cap(n), 256, 0, st>>>(cpts.p, nullptr, orig.p, n, spts.p, pos.p,
-                                                     rows.len ? clen.p : nullptr, slen.p);
+        k_sorted_gather<<<grid_cap(n), 256, 0, st>>>(cpts.p, orig.p, n, spts.p, pos.p, pv.scl,
+                                                     pv.sl, rows.len ? slen.p : nullptr);
         k_gkey<<<grid_cap(n), 256, 0, st>>>(d_gpos, orig.p, n, gkey.p);
         JB_LAUNCH_CHECK();
     }
