@@ -1731,11 +1731,24 @@ bool lloyd_persistent(LloydCtx& L, int budget) {
         int cnt = 0;
         for (int b = 0; b < 512 && h[6 * b + 5]; ++b, ++cnt)
             for (int q = 0; q < 5; ++q) acc[q] += (double)(h[6 * b + q + 1] - h[6 * b + q]) * 1e-3;
-        if (cnt)
+        if (cnt) {
+            int rebuilds = 0;
+            double quart[4][5] = {};
+            for (int b = 0; b < cnt; ++b) {
+                rebuilds += (h[6 * b + 2] - h[6 * b + 1]) > 1500;
+                for (int q = 0; q < 5; ++q)
+                    quart[4 * b / cnt][q] += (double)(h[6 * b + q + 1] - h[6 * b + q]) * 1e-3;
+            }
             fprintf(stderr, "[jb] lloyd phases over %d iters (us): means %.1f grid %.1f super %.1f "
-                            "expand %.1f work %.1f (grid %d x 256)\n",
+                            "expand %.1f work %.1f (grid %d x 256), %d grid rebuilds\n",
                     cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt,
-                    kSMs * per_sm);
+                    kSMs * per_sm, rebuilds);
+            for (int qq = 0; qq < 4; ++qq)
+                fprintf(stderr, "[jb]   quarter %d: means %.1f grid %.1f super %.1f expand %.1f work %.1f\n",
+                        qq, quart[qq][0] / (cnt / 4.0), quart[qq][1] / (cnt / 4.0),
+                        quart[qq][2] / (cnt / 4.0), quart[qq][3] / (cnt / 4.0),
+                        quart[qq][4] / (cnt / 4.0));
+        }
     }
     return true;
 }
