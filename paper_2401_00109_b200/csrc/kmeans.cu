@@ -1199,8 +1199,9 @@ __device__ __forceinline__ void lloyd_work_body(
         for (int i = 0; i < TILE / 32; ++i) {
             const int64_t r = (int64_t)t * TILE + i * 32 + lane;
             const bool valid = r < n;
-            const bool need_p = valid && (single == MIXED || FULL || old[i] != single);
-            pt[i] = need_p ? spts[r] : make_double2(0.0, 0.0);
+            // not gated on old[i]: the point loads go out with the label loads
+            // (one memory round trip instead of two; unused points cost 2 KB)
+            pt[i] = valid ? spts[r] : make_double2(0.0, 0.0);
             ln[i] = (valid && single == MIXED && slen) ? slen[r] : 0;
         }
         if (single == MIXED && slen) {
@@ -1223,35 +1224,64 @@ __device__ __forceinline__ void lloyd_work_body(
                 bst[i] = slen ? row_pick(cw[i], g, pt[i].x, pt[i].y, cx, cy, k)
                               : grid_nearest(g, pt[i].x, pt[i].y, cx, cy, k);
         }
+        auto flush = [&](uint32_t kk, u128 sa, u128 sb, unsigned long long, int cnt) {
+            if (FULL) {
+                fx_atomic_add(s_sx + 2 * kk, (i128)sa);
+                fx_atomic_add(s_sy + 2 * kk, (i128)sb);
+                atomicAdd(s_cnt + kk, (unsigned long long)cnt);
+            } else {
+                const uint32_t nb = kk & 0xFFFFu, ob = kk >> 16;
+                l3_add(acc.sx + 3 * nb, (i128)sa);
+                l3_add(acc.sy + 3 * nb, (i128)sb);
+                atomicAdd(acc.cnt + nb, (unsigned long long)cnt);
+                l3_add(acc.sx + 3 * ob, -(i128)sa);
+                l3_add(acc.sy + 3 * ob, -(i128)sb);
+                atomicAdd(acc.cnt + ob, (unsigned long long)(-(long long)cnt));
+            }
+        };
+        bool mv[TILE / 32];
+        uint32_t key[TILE / 32];
+        uint32_t key0 = 0xFFFFFFFFu;  // the first moved point's key (lane order, round order)
 #pragma unroll
         for (int i = 0; i < TILE / 32; ++i) {
             const int64_t r = (int64_t)t * TILE + i * 32 + lane;
             const bool valid = r < n;
-            const double2 p = pt[i];
             const uint32_t best = valid ? bst[i] : 0u;
-            const bool moved = valid && (FULL || old[i] != best);
-            if (moved) labs[r] = best;
-            if (!FULL && moved) ++my_changed;
+            mv[i] = valid && (FULL || old[i] != best);
+            if (mv[i]) labs[r] = best;
+            if (!FULL && mv[i]) ++my_changed;
+            key[i] = FULL ? best : ((old[i] << 16) | best);
+            const unsigned bm = __ballot_sync(0xffffffffu, mv[i]);
+            if (key0 == 0xFFFFFFFFu && bm) key0 = __shfl_sync(0xffffffffu, key[i], __ffs(bm) - 1);
+        }
+        bool uni = true;  // every moved point shares one (old, new) pair: the SINGLE-tile case
+#pragma unroll
+        for (int i = 0; i < TILE / 32; ++i) uni &= !mv[i] || key[i] == key0;
+        uni = __all_sync(0xffffffffu, uni);
+        if (uni) {
+            if (key0 != 0xFFFFFFFFu) {  // one tree reduction and one set of atomics per tile
+                i128 sa = 0, sb = 0;
+                int cnt = 0;
+#pragma unroll
+                for (int i = 0; i < TILE / 32; ++i)
+                    if (mv[i]) {
+                        sa += fx_from_double(pt[i].x, Ex);
+                        sb += fx_from_double(pt[i].y, Ey);
+                        ++cnt;
+                    }
+                sa = fx_warp_sum(sa);
+                sb = fx_warp_sum(sb);
+                for (int o = 16; o > 0; o >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, o);
+                if (lane == 0) flush(key0, (u128)sa, (u128)sb, 0ULL, cnt);
+            }
+        } else {
             // group lanes by (old, new) label pair; one set of atomics per group
-            const uint32_t key = FULL ? best : ((old[i] << 16) | best);
-            const i128 fx = moved ? fx_from_double(p.x, Ex) : (i128)0;
-            const i128 fy = moved ? fx_from_double(p.y, Ey) : (i128)0;
-            warp_aggregate(moved, key, (u128)fx, (u128)fy, 0ULL, agg,
-                           [&](uint32_t kk, u128 sa, u128 sb, unsigned long long, int cnt) {
-                               if (FULL) {
-                                   fx_atomic_add(s_sx + 2 * kk, (i128)sa);
-                                   fx_atomic_add(s_sy + 2 * kk, (i128)sb);
-                                   atomicAdd(s_cnt + kk, (unsigned long long)cnt);
-                               } else {
-                                   const uint32_t nb = kk & 0xFFFFu, ob = kk >> 16;
-                                   l3_add(acc.sx + 3 * nb, (i128)sa);
-                                   l3_add(acc.sy + 3 * nb, (i128)sb);
-                                   atomicAdd(acc.cnt + nb, (unsigned long long)cnt);
-                                   l3_add(acc.sx + 3 * ob, -(i128)sa);
-                                   l3_add(acc.sy + 3 * ob, -(i128)sb);
-                                   atomicAdd(acc.cnt + ob, (unsigned long long)(-(long long)cnt));
-                               }
-                           });
+#pragma unroll
+            for (int i = 0; i < TILE / 32; ++i) {
+                const i128 fx = mv[i] ? fx_from_double(pt[i].x, Ex) : (i128)0;
+                const i128 fy = mv[i] ? fx_from_double(pt[i].y, Ey) : (i128)0;
+                warp_aggregate(mv[i], key[i], (u128)fx, (u128)fy, 0ULL, agg, flush);
+            }
         }
         if (lane == 0) tlab[t] = single;
       }
