@@ -1742,7 +1742,7 @@ bool lloyd_persistent(LloydCtx& L, int budget) {
     // rebuilds; the first iteration of every launch rebuilds (+inf)
     if (L.mov.n == 0) L.mov.alloc(3, L.st);
     {
-        const double init[3] = {INFINITY, 1.0, 0.5 * L.rg.h};
+        const double init[3] = {INFINITY, 1.0, 0.5 * L.rg.slack};
         L.mov.upload(init, 3);
     }
     a.mov = L.mov.p;
@@ -1895,7 +1895,8 @@ void lloyd_best_device(const PtsView& pv, const uint64_t* d_idx, int64_t n, uint
     }
     if (rows.len) {  // exact row grid over the integer piece lengths (jb_rowgrid.cuh)
         L.rg = make_row_grid_desc(bb.ymin, bb.ymax, rows.scl, rows.sl, rows.max_len, 1 << 16);
-        L.rg.slack = L.rg.h;  // persistent loop: rebuild only after h / 2 of movement
+        static const double slack_h = getenv("JB_RG_SLACK") ? atof(getenv("JB_RG_SLACK")) : 4.0;
+        L.rg.slack = slack_h * L.rg.h;  // persistent loop: rebuild only after slack / 2 of movement
         L.rg_cell.alloc((size_t)L.rg.R * L.rg.Gy, st);
         L.rg.cell = L.rg_cell.p;
         L.slen = slen.p;
