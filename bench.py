@@ -337,38 +337,40 @@ def main():
     value = n / (ms_step / 1e3)  # the whole series, all ranks together
 
     # ---- e2e through the C ABI with host buffers ----
-    host_in = torch.empty(n_local, dtype=torch.float64, pin_memory=True)
-    host_in.copy_(x)
-    host_out = torch.empty(n_local, dtype=torch.float64, pin_memory=True)
-    host_lab = torch.empty(N, dtype=torch.int32, pin_memory=True)
-    hin, hout, hlab = host_in.numpy(), host_out.numpy(), host_lab.numpy().view(np.uint32)
-    del x
-    torch.cuda.empty_cache()
+    e2e = None
+    if args.e2e_steps > 0:
+        host_in = torch.empty(n_local, dtype=torch.float64, pin_memory=True)
+        host_in.copy_(x)
+        host_out = torch.empty(n_local, dtype=torch.float64, pin_memory=True)
+        host_lab = torch.empty(N, dtype=torch.int32, pin_memory=True)
+        hin, hout, hlab = host_in.numpy(), host_out.numpy(), host_lab.numpy().view(np.uint32)
+        del x
+        torch.cuda.empty_cache()
 
-    def e2e_step():
-        nf2 = fit(values=hin)
-        nf2.labels_into(hlab)
-        nf2.inverse(out=hout)
-        return nf2
+        def e2e_step():
+            nf2 = fit(values=hin)
+            nf2.labels_into(hlab)
+            nf2.inverse(out=hout)
+            return nf2
 
-    e2e_step()  # warm
-    barrier()
-    t0 = time.perf_counter()
-    e2 = torch.cuda.Event(enable_timing=True)
-    e3 = torch.cuda.Event(enable_timing=True)
-    e2.record()
-    for _ in range(args.e2e_steps):
-        nf2 = e2e_step()
-    e3.record()
-    barrier()
-    e2e_ms = e2.elapsed_time(e3) / args.e2e_steps
-    t_e = torch.tensor([e2e_ms], dtype=torch.float64, device=red_dev)
-    if world > 1:
-        dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
-    e2e_ms = float(t_e.item())
-    e2e = {"value": n / (e2e_ms / 1e3), "unit": "points/s",
-           "h2d_bytes_per_step": 8 * n_local, "d2h_bytes_per_step": 8 * n_local + 4 * nf2.n_pieces,
-           "per": "rank" if world > 1 else "step"}
+        e2e_step()  # warm
+        barrier()
+        t0 = time.perf_counter()
+        e2 = torch.cuda.Event(enable_timing=True)
+        e3 = torch.cuda.Event(enable_timing=True)
+        e2.record()
+        for _ in range(args.e2e_steps):
+            nf2 = e2e_step()
+        e3.record()
+        barrier()
+        e2e_ms = e2.elapsed_time(e3) / args.e2e_steps
+        t_e = torch.tensor([e2e_ms], dtype=torch.float64, device=red_dev)
+        if world > 1:
+            dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t_e.item())
+        e2e = {"value": n / (e2e_ms / 1e3), "unit": "points/s",
+               "h2d_bytes_per_step": 8 * n_local, "d2h_bytes_per_step": 8 * n_local + 4 * nf2.n_pieces,
+               "per": "rank" if world > 1 else "step"}
 
     # ---- roofline of the dominant kernel ----
     peaks, peak_kind = measured_peaks()
