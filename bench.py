@@ -157,6 +157,41 @@ def algorithmic_work(name, launches, info):
     return None, None
 
 
+def step_roofline(info, ms_step, hbm_gbs, fp64_tflops):
+    """Whole-step roofline of SURVEY.md §8(d): per phase T_roof = max(bytes /
+    HBM, flops / FP64 peak) with the reference algorithm's compulsory work
+    (brute-force D^2 / Lloyd / final assignment over all k centers), summed;
+    frac = T_roof / T_measured. T (candidate tests) = steps + N: every step is
+    one accepted test and every piece but a segment's last ends on a failed
+    one (T/step 1.89 at cfg4). A frac above 1 means the exact
+    candidate pruning does less work than the reference
+    algorithm's compulsory minimum."""
+    n, N, S, k, I = info["n"], info["N"], info["S"], info["k"], info["iterations"]
+    T = info["steps"] + N
+    phases = {  # (flops, bytes)
+        "compress": (23.0 * T, 8.0 * n + 16.0 * N),
+        "scale": (11.0 * N, 32.0 * N),
+        "d2_seed": (9.0 * S * k, 32.0 * S * k),
+        "lloyd": (I * (6.0 * S * k + 2.0 * S), I * 24.0 * S),
+        "final_assign": (6.0 * N * k + 3.0 * N, 20.0 * N),
+        "inverse": (6.0 * N + 3.0 * n, 4.0 * N + 8.0 * n),
+    }
+    out, tot = {}, 0.0
+    for ph, (fl, by) in phases.items():
+        t_b = by / (hbm_gbs * 1e9)
+        t_f = fl / (fp64_tflops * 1e12) if fp64_tflops else 0.0
+        t = max(t_b, t_f)
+        tot += t
+        out[ph] = {"flops": fl, "bytes": by, "t_roof_ms": t * 1e3,
+                   "bound": "fp64" if t_f > t_b else "hbm"}
+    return {"definition": "SURVEY.md §8(d): sum over phases of max(bytes/HBM, flops/FP64), "
+                          "reference algorithm's compulsory work; frac = T_roof / T_measured",
+            "hbm_gbs": hbm_gbs, "fp64_tflops": fp64_tflops,
+            "fp64_peak_source": "measured DFMA-chain probe on this GPU (jb_probe_fp64_tflops, 2 flop/DFMA)",
+            "t_roof_ms": tot * 1e3, "t_measured_ms": ms_step, "frac": tot * 1e3 / ms_step,
+            "phases": out}
+
+
 def ncu_traffic(name):
     """Per-launch DRAM bytes of `name` from an ncu --set full capture
     (profiles/ncu_traffic.json, written by tools/ncu_traffic.py), or None."""
@@ -418,6 +453,8 @@ def main():
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": workload_desc(n, m, args.scale, world),
             "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
+            "step_roofline": step_roofline(dict(info, steps=int(sum(steps_g))), ms_step,
+                                           peaks.get("hbm_gbs"), fp64_peak(_native.lib(), local)),
             "clocks": clk.summary(), "gpu_launches": gpu_launches,
             "phase_ms": st["ms"], "profiled_step_ms": ms_profiled, "fit_stats": {k: st[k] for k in ("iterations", "sample_size",
                                                                     "fix_rounds")},

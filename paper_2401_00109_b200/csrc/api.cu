@@ -515,8 +515,9 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
             const uint64_t raw_count = S + (c.k + 1) * c.n_init + 4096;
             mt19937_64_generate(c.seed, raw_count, raw, st);
             JB_TRACE("svq: engine draws", st);
-            uint64_t cursor =
-                sample_indices_device((uint64_t)N_glob, S, raw.p, raw_count, sample, st);
+            SampleOrder jorder;  // single GPU: gather-friendly Morton pass
+            uint64_t cursor = sample_indices_device((uint64_t)N_glob, S, raw.p, raw_count, sample,
+                                                    st, cm.dist() ? nullptr : &jorder);
             JB_TRACE("svq: sample indices", st);
             KMeansOut km;
             if (cm.dist()) {  // the entries this rank owns, in sample order
@@ -543,7 +544,7 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
                 sample = std::move(lidx);
             } else {
                 lloyd_best_device(pv, sample.p, (int64_t)S, c.k, c.max_iters, c.n_init,
-                                  raw.p, raw_count, &cursor, bb, km, st, rows);
+                                  raw.p, raw_count, &cursor, bb, km, st, rows, &jorder);
                 n_sample_local = (int64_t)S;
             }
             k = c.k;

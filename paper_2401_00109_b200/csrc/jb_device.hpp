@@ -229,8 +229,15 @@ void kmeans_labels(KMeansOut& out, int64_t n, cudaStream_t st);
 
 // sample_indices (clustering.hpp:74-85) on device; idx is S entries.
 // Returns the number of engine draws consumed (>= S).
+// jorder (optional): the swap targets j_i sorted (stable) and the swap
+// indices i in that order -- the sample in ascending piece order except the
+// ~S^2/2n entries of repeated targets -- for the gather-friendly Morton pass.
+struct SampleOrder {
+    DArr<uint32_t> j, i;
+};
 uint64_t sample_indices_device(uint64_t n, uint64_t S, const uint64_t* d_raw, uint64_t raw_count,
-                               DArr<uint64_t>& idx, cudaStream_t st);
+                               DArr<uint64_t>& idx, cudaStream_t st,
+                               SampleOrder* jorder = nullptr);
 
 // Raw std::mt19937_64 stream on device.
 void mt19937_64_generate(uint64_t seed, uint64_t count, DArr<uint64_t>& out, cudaStream_t st);
@@ -251,7 +258,8 @@ struct PieceRows {
 void lloyd_best_device(const PtsView& pv, const uint64_t* d_idx, int64_t n, uint64_t k,
                        uint64_t max_iters, uint64_t n_init, const uint64_t* d_raw,
                        uint64_t raw_count, uint64_t* cursor, const BBox& bb, KMeansOut& out,
-                       cudaStream_t st, const PieceRows& rows = PieceRows{});
+                       cudaStream_t st, const PieceRows& rows = PieceRows{},
+                       const SampleOrder* jorder = nullptr);
 
 // Distributed variant: this rank holds the sample entries it owns -- local
 // piece index d_lidx[i] and global sample position d_gpos[i] (ascending), n

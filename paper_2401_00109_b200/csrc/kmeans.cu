@@ -343,7 +343,7 @@ void mt19937_64_generate(uint64_t seed, uint64_t count, DArr<uint64_t>& out, cud
 }
 
 uint64_t sample_indices_device(uint64_t n, uint64_t S, const uint64_t* d_raw, uint64_t raw_count,
-                               DArr<uint64_t>& idx, cudaStream_t st) {
+                               DArr<uint64_t>& idx, cudaStream_t st, SampleOrder* jorder) {
     if (n >= (1ULL << 32)) throw Error(INVALID_INPUT, "sampling: more than 2^32 pieces");
     DArr<uint32_t> j(S, st), keys_s(S, st);  // j_i < n < 2^32
     DArr<uint32_t> vals(S, st), vals_s(S, st);
@@ -413,6 +413,10 @@ uint64_t sample_indices_device(uint64_t n, uint64_t S, const uint64_t* d_raw, ui
         k_fy_resolve<<<grid_cap(S), 256, 0, st>>>(j.p, P.p, L.p, S, idx.p);
     }
     JB_LAUNCH_CHECK();
+    if (jorder) {
+        jorder->j = std::move(keys_s);
+        jorder->i = std::move(vals_s);
+    }
     return S + total_shift;
 }
 
@@ -482,6 +486,52 @@ __global__ void k_sorted_gather(const double2* __restrict__ cpts, const uint32_t
             spts[r] = c;
         }
         pos[o] = (uint32_t)r;
+    }
+}
+
+// Morton pass in swap-target order (SampleOrder): r-th entry = swap i =
+// order_i[r]; the first of a run of equal targets has idx[i] = j (no earlier
+// swap touched position j: k_fy_links), the rest take the resolved idx[i].
+// Piece reads follow ascending j, so len/inc stream instead of two random
+// reads per point. Record r carries (y, len, i) for the sorted gather.
+struct SRec {
+    double y;
+    int32_t len;
+    uint32_t i;
+};
+
+__global__ void k_morton_jorder(const PtsView pv, const uint64_t* __restrict__ idx,
+                                const uint32_t* __restrict__ oj, const uint32_t* __restrict__ oi,
+                                int64_t n, double x0, double sx, double y0, double sy,
+                                uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                                SRec* __restrict__ rec) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t j = oj[r], i = oi[r];
+        const bool first = r == 0 || oj[r - 1] != j;
+        const uint64_t src = first ? (uint64_t)j : idx[i];
+        const int32_t l = pv.len[src];
+        const double2 p = make_double2(pv.scl * (double)l / pv.sl, pv.inc[src] / pv.si);  // pv.at
+        rec[r] = SRec{p.y, l, i};
+        const uint32_t qx = (uint32_t)fmin(fmax((p.x - x0) * sx, 0.0), 65535.0);
+        const uint32_t qy = (uint32_t)fmin(fmax((p.y - y0) * sy, 0.0), 65535.0);
+        keys[r] = spread16(qx) | (spread16(qy) << 1);
+        vals[r] = (uint32_t)r;
+    }
+}
+
+// one random 16-byte record read per point (plus the pos scatter)
+__global__ void k_sorted_gather_rec(const SRec* __restrict__ rec, const uint32_t* __restrict__ ordr,
+                                    int64_t n, double2* __restrict__ spts,
+                                    uint32_t* __restrict__ orig, uint32_t* __restrict__ pos,
+                                    double scl, double sl, int32_t* __restrict__ slen) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n;
+         s += (int64_t)gridDim.x * blockDim.x) {
+        const SRec c = rec[ordr[s]];
+        spts[s] = make_double2(scl * (double)c.len / sl, c.y);
+        slen[s] = c.len;
+        orig[s] = c.i;
+        pos[c.i] = (uint32_t)s;
     }
 }
 
@@ -1014,7 +1064,71 @@ __device__ __forceinline__ uint32_t box_single(const double4& b, int l, const Ca
     return first;
 }
 
-// Super-tile check (32 consecutive tiles = 4096 points), one thread each. A
+// box_single by a group of 8 lanes (lane `sub` takes row cell word sub, its
+// <= 4 candidates): the same candidate set, the same M (fmin is exact and
+// order free), the same threshold and the same dmn <= thr tests as the
+// serial loop, and SINGLE iff every passing candidate is one center -- so
+// the same answer with a short critical path. Every lane of the warp must
+// call it (shuffles over the full mask); l and b are uniform per group.
+__device__ __forceinline__ uint32_t box_single_g8(const double4& b, int l, const CandGrid& g,
+                                                  const RowGrid& rg, const double* centers,
+                                                  int sub) {
+    bool row = l >= 1 && l <= rg.R;
+    int iy0 = 0, nc = 0;
+    if (row) {
+        iy0 = (int)((b.z - rg.y0) * rg.invh);
+        int iy1 = (int)((b.w - rg.y0) * rg.invh);
+        iy0 = min(max(iy0, 0), rg.Gy - 1);
+        iy1 = min(max(iy1, 0), rg.Gy - 1);
+        nc = iy1 - iy0 + 1;
+        row = nc <= 8;
+    }
+    uint64_t wv = ~0ull;
+    if (row && sub < nc)
+        wv = __ldg(reinterpret_cast<const unsigned long long*>(rg.cell) + (size_t)(l - 1) * rg.Gy +
+                   iy0 + sub);
+    bool bad = row && sub < nc && (wv & 0xFFFF) >= kRowOverflow;
+    double dmn[4];
+    double M = INFINITY;
+    int ncand = 0;
+    if (row && sub < nc && !bad) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t c = (uint32_t)((wv >> (16 * q)) & 0xFFFF);
+            if (c == kRowEmpty) break;
+            double dmx;
+            box_d2(centers[2 * c], centers[2 * c + 1], b, dmn[q], dmx);
+            M = fmin(M, dmx);
+            ncand = q + 1;
+        }
+    }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+        M = fmin(M, __shfl_xor_sync(0xffffffffu, M, o));
+        bad |= __shfl_xor_sync(0xffffffffu, (int)bad, o) != 0;
+    }
+    const double thr = M * (1.0 + kKeepMargin) + 1e-300;
+    uint32_t cmin = MIXED, cmax = 0;  // passing candidates (cmax: c + 1)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        if (q >= ncand) break;
+        if (dmn[q] <= thr) {
+            const uint32_t c = (uint32_t)((wv >> (16 * q)) & 0xFFFF);
+            cmin = min(cmin, c);
+            cmax = max(cmax, c + 1);
+        }
+    }
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) {
+        cmin = min(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
+        cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+    }
+    if (row && !bad) return (cmax != 0 && cmin + 1 == cmax) ? cmin : MIXED;
+    if (g.G == 0) return MIXED;
+    return box_single(b, l, g, rg, centers);  // 2-D grid: every lane the serial test
+}
+
+// Super-tile check (32 consecutive tiles = 4096 points), 8 lanes each. A
 // super-tile whose box is SINGLE with the center it was SINGLE with last
 // time holds that label on all its points (its state is reset to MIXED
 // whenever a point of it is relabeled outside this scheme, k_repair): it is
@@ -1030,18 +1144,20 @@ __device__ __forceinline__ void super_check_body(const double4* __restrict__ sbo
     for (int i = threadIdx.x; i < 2 * k; i += blockDim.x) s_centers[i] = centers[i];
     __syncthreads();
     centers = s_centers;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, grp = lane >> 3, sub = lane & 7;
     const int64_t nsuper = (ntiles + 31) / 32;
     uint32_t* stlab = tlab + ntiles;
-    const int64_t wstride = (((int64_t)gridDim.x * blockDim.x) >> 5) * 32;
-    for (int64_t s0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * 32; s0 < nsuper;
-         s0 += wstride) {
-        const int64_t sidx = s0 + lane;
+    // 8 lanes per super-tile (box_single_g8), 4 super-tiles per warp pass
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t wstride = (((int64_t)gridDim.x * blockDim.x) >> 5) * 4;
+    for (int64_t s0 = warp * 4; s0 < nsuper; s0 += wstride) {
+        const int64_t sidx = s0 + grp;
+        const bool valid = sidx < nsuper;
+        const double4 b = valid ? sbox[sidx] : make_double4(0.0, 0.0, 0.0, 0.0);
+        const int l = valid && slenc ? slenc[sidx] : 0;
+        const uint32_t ss = force_all ? MIXED : box_single_g8(b, l, g, rg, centers, sub);
         bool need = false;
-        if (sidx < nsuper) {
-            const uint32_t ss = force_all ? MIXED
-                                          : box_single(sbox[sidx], slenc ? slenc[sidx] : 0, g, rg,
-                                                       centers);
+        if (valid && sub == 0) {
             need = force_all || ss == MIXED || ss != stlab[sidx];
             if (need) stlab[sidx] = ss;  // all its points carry ss after this iteration
         }
@@ -1062,7 +1178,8 @@ __global__ void k_super_check(const double4* __restrict__ sbox, const int32_t* _
     super_check_body(sbox, slenc, ntiles, g, centers, tlab, swork, nswork, skip_flag, force_all, rg, k);
 }
 
-// Tiles of the listed super-tiles (warp per super-tile, lane per tile): the
+// Tiles of the listed super-tiles (8 lanes per tile over the flattened
+// (super-tile, tile) list): the
 // tiles whose single-center state changed or is MIXED are listed for
 // k_lloyd_work with their new state in tnew.
 __device__ __forceinline__ void tile_expand_body(const uint32_t* __restrict__ swork,
@@ -1078,15 +1195,19 @@ __device__ __forceinline__ void tile_expand_body(const uint32_t* __restrict__ sw
     for (int i = threadIdx.x; i < 2 * k; i += blockDim.x) s_centers[i] = centers[i];
     __syncthreads();
     centers = s_centers;
-    const int lane = threadIdx.x & 31;
-    const int64_t nw = (int64_t)*nswork;
-    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nw;
-         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        const int64_t t = (int64_t)swork[w] * 32 + lane;
+    const int lane = threadIdx.x & 31, grp = lane >> 3, sub = lane & 7;
+    const int64_t items = (int64_t)*nswork * 32;  // (listed super-tile, tile) pairs
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t wstride = (((int64_t)gridDim.x * blockDim.x) >> 5) * 4;
+    for (int64_t i0 = warp * 4; i0 < items; i0 += wstride) {  // 8 lanes per tile
+        const int64_t it = i0 + grp;
+        const int64_t t = it < items ? (int64_t)swork[it >> 5] * 32 + (it & 31) : ntiles;
+        const bool valid = t < ntiles;
+        const double4 b = valid ? tbox[t] : make_double4(0.0, 0.0, 0.0, 0.0);
+        const int l = valid && tlen ? tlen[t] : 0;
+        const uint32_t single = force_all ? MIXED : box_single_g8(b, l, g, rg, centers, sub);
         bool add = false;
-        if (t < ntiles) {
-            const uint32_t single =
-                force_all ? MIXED : box_single(tbox[t], tlen ? tlen[t] : 0, g, rg, centers);
+        if (valid && sub == 0) {
             tnew[t] = single;
             add = force_all || single == MIXED || single != tlab[t];
         }
@@ -1828,7 +1949,7 @@ void lloyd_update_means_sync(LloydCtx& L) {
 void lloyd_best_device(const PtsView& pv, const uint64_t* d_idx, int64_t n, uint64_t k,
                        uint64_t max_iters, uint64_t n_init, const uint64_t* d_raw,
                        uint64_t raw_count, uint64_t* cursor, const BBox& bb, KMeansOut& out,
-                       cudaStream_t st, const PieceRows& rows) {
+                       cudaStream_t st, const PieceRows& rows, const SampleOrder* jorder) {
     if (k < 1) throw Error(INVALID_INPUT, "d2_seed: k must be >= 1");
     if ((int64_t)k > n) throw Error(INVALID_INPUT, "d2_seed: k exceeds points");
     if (k > 2048) throw Error(INVALID_INPUT, "k > 2048 is not supported by the Lloyd kernel");
@@ -1846,19 +1967,41 @@ void lloyd_best_device(const PtsView& pv, const uint64_t* d_idx, int64_t n, uint
     {
         DArr<uint32_t> keys(n, st), skeys(n, st), vals(n, st);
         const double sx = wx > 0 ? 65535.0 / wx : 0.0, sy = wy > 0 ? 65535.0 / wy : 0.0;
-        DArr<double2> cpts(n, st);
-        k_morton<<<grid_cap(n), 256, 0, st>>>(pv, d_idx, n, bb.xmin, sx, bb.ymin, sy, keys.p,
-                                              vals.p, cpts.p, rows.len);
-        JB_LAUNCH_CHECK();
-        size_t tb = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.p, skeys.p, vals.p, orig.p, n, 0, 32,
-                                        st);
-        DArr<uint8_t> tmp(tb, st);
-        cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.p, skeys.p, vals.p, orig.p, n, 0, 32, st);
-        JB_LAUNCH_CHECK();
-        k_sorted_gather<<<grid_cap(n), 256, 0, st>>>(cpts.p, orig.p, n, spts.p, pos.p, pv.scl,
-                                                     pv.sl, rows.len ? slen.p : nullptr);
-        JB_LAUNCH_CHECK();
+        const bool jo = jorder && d_idx && rows.len && !pv.pts && pv.len == rows.len &&
+                        jorder->j.n >= (size_t)n && jorder->i.n >= (size_t)n;
+        if (jo) {  // piece reads in ascending piece order (k_morton_jorder)
+            DArr<SRec> rec(n, st);
+            DArr<uint32_t> ordr(n, st);
+            k_morton_jorder<<<grid_cap(n), 256, 0, st>>>(pv, d_idx, jorder->j.p, jorder->i.p, n,
+                                                         bb.xmin, sx, bb.ymin, sy, keys.p, vals.p,
+                                                         rec.p);
+            JB_LAUNCH_CHECK();
+            size_t tb = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.p, skeys.p, vals.p, ordr.p, n, 0, 32,
+                                            st);
+            DArr<uint8_t> tmp(tb, st);
+            cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.p, skeys.p, vals.p, ordr.p, n, 0, 32,
+                                            st);
+            JB_LAUNCH_CHECK();
+            k_sorted_gather_rec<<<grid_cap(n), 256, 0, st>>>(rec.p, ordr.p, n, spts.p, orig.p,
+                                                             pos.p, pv.scl, pv.sl, slen.p);
+            JB_LAUNCH_CHECK();
+        } else {
+            DArr<double2> cpts(n, st);
+            k_morton<<<grid_cap(n), 256, 0, st>>>(pv, d_idx, n, bb.xmin, sx, bb.ymin, sy, keys.p,
+                                                  vals.p, cpts.p, rows.len);
+            JB_LAUNCH_CHECK();
+            size_t tb = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.p, skeys.p, vals.p, orig.p, n, 0, 32,
+                                            st);
+            DArr<uint8_t> tmp(tb, st);
+            cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.p, skeys.p, vals.p, orig.p, n, 0, 32,
+                                            st);
+            JB_LAUNCH_CHECK();
+            k_sorted_gather<<<grid_cap(n), 256, 0, st>>>(cpts.p, orig.p, n, spts.p, pos.p, pv.scl,
+                                                         pv.sl, rows.len ? slen.p : nullptr);
+            JB_LAUNCH_CHECK();
+        }
     }
     JB_TRACE("kmeans: morton order", st);
     const int64_t ntiles = (n + TILE - 1) / TILE;
