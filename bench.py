@@ -144,12 +144,24 @@ def algorithmic_work(name, launches, info):
         # (16 B point + 4 B label r/w each); tiles of the full pass excluded
         full_tiles = (S + 127) // 128
         return "hbm", 24.0 * 128 * max(info.get("lloyd_tiles", 0) - full_tiles, 0)
-    if name == "assign_stats":       # final assign + group stats: point 16 B + len 4 B in, label 4 B out
-        return "hbm", launches * 24.0 * N
-    if name == "d2_update":          # 16 B point + 8 B d2 read, 8 B d2 write per sample
-        return "hbm", launches * 32.0 * S
+    if name == "assign_stats":       # final assign + group stats: len 4 B + inc 8 B in (points
+        return "hbm", launches * 16.0 * N  # are virtual), label 4 B out
+    if name == "d2_update":          # points of the tiles not culled: 16 B point + 8 B d2 read
+        # + 8 B d2 write; the cull reads 40 B (box + max d2) per tile per round
+        ntiles = (S + 127) // 128
+        return "hbm", 32.0 * 128 * info.get("d2_tiles", 0) + 40.0 * ntiles * max(k - 1, 0)
     if name == "compress_spec":      # 23 flops per candidate test, T ~ 1.89 n (cfg4)
         return "fp64", 23.0 * info.get("tests", 1.89 * n)
+    if name == "inverse_fused":      # label 4 B per piece in, 8 B per reconstructed sample out
+        return "hbm", launches * (4.0 * N + 8.0 * n)
+    if name == "sample_order":       # j 4 + i 4 + len 4 + inc 8 in; key 4 + record 16 out
+        return "hbm", launches * 40.0 * S
+    if name == "sample_unpack":      # record 16 in; point 16 + len 4 + orig 4 + pos 4 out
+        return "hbm", launches * 44.0 * S
+    if name == "compress_emit":      # samples 8 B in; len 4 + inc 8 B per piece out
+        return "hbm", launches * (8.0 * n + 12.0 * N)
+    if name in ("scale_sum_var", "scale_sum_inc"):  # len 4 + inc 8 B per piece
+        return "hbm", launches * 12.0 * N
     if name == "inverse_chain":      # label 4 B in; quantized length 4 B + start value 8 B out
         return "hbm", 16.0 * N
     if name == "inverse_fill":
@@ -363,7 +375,8 @@ def main():
     st = nf.stats()
     N = nf.n_pieces
     info = dict(S=st["sample_size"], k=nf.k, N=N, n=n, iterations=st["iterations"],
-                lloyd_tiles=st.get("lloyd_tiles_processed", 0))
+                lloyd_tiles=st.get("lloyd_tiles_processed", 0),
+                d2_tiles=st.get("d2_tiles_updated", 0))
     red_dev = dev if world == 1 or dist.get_backend() == "nccl" else "cpu"
     t_local = torch.tensor([ms_total], dtype=torch.float64, device=red_dev)
     if world > 1:

@@ -149,7 +149,8 @@ jb_status jb_fit_copy_symbolic(const jb_fit* fit, uint32_t* labels, double* cent
  * (compress, scale, backend, stats, total) */
 jb_status jb_fit_stats(const jb_fit* fit, uint64_t* iterations, uint64_t* sample_size,
                        uint64_t* draws, int32_t* fix_rounds, int32_t* ga_rounds,
-                       double* phase_ms /* 7: 5 phases, Lloyd tiles processed, labels changed */);
+                       double* phase_ms /* 8: 5 phases, Lloyd tiles processed, labels changed,
+                                          D^2 tiles updated */);
 
 /* inverse_transform on the device-resident fit. out_values: host
  * (out_on_device == 0) or device pointer with jb_fit_reconstruct_size()

@@ -394,13 +394,14 @@ class NativeFit:
     def stats(self):
         it, ss, dr = C.c_uint64(), C.c_uint64(), C.c_uint64()
         fr, gr = C.c_int32(), C.c_int32()
-        ph = np.zeros(7, np.float64)
+        ph = np.zeros(8, np.float64)
         _check(N.lib().jb_fit_stats(self.h, C.byref(it), C.byref(ss), C.byref(dr), C.byref(fr),
                                     C.byref(gr), ph.ctypes.data))
         return dict(iterations=it.value, sample_size=ss.value, draws=dr.value,
                     fix_rounds=fr.value, ga_rounds=gr.value,
                     ms=dict(zip(["compress", "scale", "backend", "stats", "total"], ph[:5])),
-                    lloyd_tiles_processed=int(ph[5]), lloyd_labels_changed=int(ph[6]))
+                    lloyd_tiles_processed=int(ph[5]), lloyd_labels_changed=int(ph[6]),
+                    d2_tiles_updated=int(ph[7]))
 
     def reconstruct_size(self) -> int:
         return N.lib().jb_fit_reconstruct_size(self.h)

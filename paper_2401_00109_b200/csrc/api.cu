@@ -218,6 +218,7 @@ struct jb_fit {
     double scaling[3] = {1.0, 1.0, 1.0};
     // diagnostics
     uint64_t iterations = 0, sample_size = 0, draws = 0, work_tiles = 0, changed_labels = 0;
+    uint64_t d2_tiles = 0;
     int32_t fix_rounds = 0, ga_rounds = 0;
     double phase_ms[5] = {0, 0, 0, 0, 0};
 };
@@ -551,6 +552,7 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
             backend_centers = km.centers;
             fit->work_tiles = km.work_tiles;
             fit->changed_labels = km.changed_labels;
+            fit->d2_tiles = km.d2_tiles;
             fit->iterations = km.iterations;
             svq_km = std::move(km);  // sample labels: unsorted only if needed below
             labels.alloc(std::max<int64_t>(N, 1), st);
@@ -898,6 +900,7 @@ jb_status jb_fit_stats(const jb_fit* f, uint64_t* iterations, uint64_t* sample_s
     if (phase_ms) {  // extended diagnostics after the 5 phase timings
         phase_ms[5] = (double)f->work_tiles;
         phase_ms[6] = (double)f->changed_labels;
+        phase_ms[7] = (double)f->d2_tiles;
     }
     return JB_OK;
 }

@@ -222,6 +222,7 @@ struct KMeansOut {
     uint64_t iterations = 0;
     double sse = 0.0;
     uint64_t work_tiles = 0, changed_labels = 0;  // Lloyd diagnostics (all iterations)
+    uint64_t d2_tiles = 0;                        // D^2 rounds: tiles updated (persistent path)
 };
 
 // Materialises out.labels (input order) from the internal order.

@@ -489,45 +489,47 @@ __global__ void k_sorted_gather(const double2* __restrict__ cpts, const uint32_t
     }
 }
 
-// Morton pass in swap-target order (SampleOrder): r-th entry = swap i =
-// order_i[r]; the first of a run of equal targets has idx[i] = j (no earlier
-// swap touched position j: k_fy_links), the rest take the resolved idx[i].
-// Piece reads follow ascending j, so len/inc stream instead of two random
-// reads per point. Record r carries (y, len, i) for the sorted gather.
+// Spatial pass in swap-target order (SampleOrder), for points on the row
+// grid's vertical lines: the r-th entry is swap i = order_i[r]; the first of
+// a run of equal targets has idx[i] = j (no earlier swap touched position j:
+// k_fy_links), the rest take the resolved idx[i]. Piece reads follow
+// ascending j, so len/inc stream instead of two random reads per point. The
+// key orders by (piece length, y): every tile lies on one line (x is a
+// function of the length) with the smallest y extent a sort can give. The
+// (y, len, i) record rides through the radix sort as its value, so the
+// sorted order needs no random gather.
 struct SRec {
     double y;
     int32_t len;
     uint32_t i;
 };
 
-__global__ void k_morton_jorder(const PtsView pv, const uint64_t* __restrict__ idx,
+__global__ void k_rowkey_jorder(const PtsView pv, const uint64_t* __restrict__ idx,
                                 const uint32_t* __restrict__ oj, const uint32_t* __restrict__ oi,
-                                int64_t n, double x0, double sx, double y0, double sy,
-                                uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                                SRec* __restrict__ rec) {
+                                int64_t n, int qbits, uint32_t lcap, double y0, double sy,
+                                uint32_t* __restrict__ keys, SRec* __restrict__ rec) {
+    const double qmax = (double)((1u << qbits) - 1u);
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
          r += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t j = oj[r], i = oi[r];
         const bool first = r == 0 || oj[r - 1] != j;
         const uint64_t src = first ? (uint64_t)j : idx[i];
         const int32_t l = pv.len[src];
-        const double2 p = make_double2(pv.scl * (double)l / pv.sl, pv.inc[src] / pv.si);  // pv.at
-        rec[r] = SRec{p.y, l, i};
-        const uint32_t qx = (uint32_t)fmin(fmax((p.x - x0) * sx, 0.0), 65535.0);
-        const uint32_t qy = (uint32_t)fmin(fmax((p.y - y0) * sy, 0.0), 65535.0);
-        keys[r] = spread16(qx) | (spread16(qy) << 1);
-        vals[r] = (uint32_t)r;
+        const double y = pv.inc[src] / pv.si;  // pv.at's y
+        rec[r] = SRec{y, l, i};
+        const uint32_t qy = (uint32_t)fmin(fmax((y - y0) * sy, 0.0), qmax);
+        keys[r] = (min((uint32_t)l, lcap) << qbits) | qy;
     }
 }
 
-// one random 16-byte record read per point (plus the pos scatter)
-__global__ void k_sorted_gather_rec(const SRec* __restrict__ rec, const uint32_t* __restrict__ ordr,
-                                    int64_t n, double2* __restrict__ spts,
-                                    uint32_t* __restrict__ orig, uint32_t* __restrict__ pos,
-                                    double scl, double sl, int32_t* __restrict__ slen) {
+// sorted records -> points (pv.at's x from the length), lengths, original
+// sample positions, and the inverse permutation
+__global__ void k_rec_unpack(const SRec* __restrict__ srec, int64_t n, double2* __restrict__ spts,
+                             uint32_t* __restrict__ orig, uint32_t* __restrict__ pos, double scl,
+                             double sl, int32_t* __restrict__ slen) {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n;
          s += (int64_t)gridDim.x * blockDim.x) {
-        const SRec c = rec[ordr[s]];
+        const SRec c = srec[s];
         spts[s] = make_double2(scl * (double)c.len / sl, c.y);
         slen[s] = c.len;
         orig[s] = c.i;
@@ -681,12 +683,14 @@ __global__ void __launch_bounds__(256) k_d2_tiles(
     const unsigned long long* __restrict__ nwork, double* __restrict__ tmax,
     double* __restrict__ d2s, const SeedState* __restrict__ ss, int init, int E,
     unsigned long long* __restrict__ part, const double2* __restrict__ cur,
-    const uint32_t* __restrict__ gkey) {
+    const uint32_t* __restrict__ gkey, unsigned long long* __restrict__ diag) {
     // cur: center given directly (distributed fit); gkey: partial-sum block
-    // key per sorted point (global sample position) instead of orig
+    // key per sorted point (global sample position) instead of orig; diag:
+    // tiles updated (diagnostics)
     const int lane = threadIdx.x & 31;
     const int64_t ntiles = (n + TILE - 1) / TILE;
     const int64_t nw = init ? ntiles : (int64_t)*nwork;
+    if (diag && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(diag, (unsigned long long)nw);
     const double2 c = cur ? *cur : spts[pos[ss->last]];
     const uint32_t* key = gkey ? gkey : orig;
     for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nw;
@@ -1969,22 +1973,32 @@ void lloyd_best_device(const PtsView& pv, const uint64_t* d_idx, int64_t n, uint
         const double sx = wx > 0 ? 65535.0 / wx : 0.0, sy = wy > 0 ? 65535.0 / wy : 0.0;
         const bool jo = jorder && d_idx && rows.len && !pv.pts && pv.len == rows.len &&
                         jorder->j.n >= (size_t)n && jorder->i.n >= (size_t)n;
-        if (jo) {  // piece reads in ascending piece order (k_morton_jorder)
-            DArr<SRec> rec(n, st);
-            DArr<uint32_t> ordr(n, st);
-            k_morton_jorder<<<grid_cap(n), 256, 0, st>>>(pv, d_idx, jorder->j.p, jorder->i.p, n,
-                                                         bb.xmin, sx, bb.ymin, sy, keys.p, vals.p,
-                                                         rec.p);
+        if (jo) {  // piece reads in ascending piece order, (length, y) key (k_rowkey_jorder)
+            int lbits = 1;
+            const uint32_t lcap = (uint32_t)std::min<int32_t>(std::max<int32_t>(rows.max_len, 1), 255);
+            while ((1u << lbits) <= lcap) ++lbits;
+            const int end_bit = lbits + 18 <= 24 ? 24 : 32;
+            const int qbits = end_bit - lbits;
+            const double syq = wy > 0 ? (double)((1u << qbits) - 1u) / wy : 0.0;
+            DArr<SRec> rec(n, st), srec(n, st);
+            {
+                JB_PROF("sample_order", st);
+                k_rowkey_jorder<<<grid_cap(n), 256, 0, st>>>(pv, d_idx, jorder->j.p, jorder->i.p, n,
+                                                             qbits, lcap, bb.ymin, syq, keys.p, rec.p);
+            }
             JB_LAUNCH_CHECK();
             size_t tb = 0;
-            cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.p, skeys.p, vals.p, ordr.p, n, 0, 32,
-                                            st);
+            cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.p, skeys.p, rec.p, srec.p, n, 0,
+                                            end_bit, st);
             DArr<uint8_t> tmp(tb, st);
-            cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.p, skeys.p, vals.p, ordr.p, n, 0, 32,
-                                            st);
+            cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys.p, skeys.p, rec.p, srec.p, n, 0,
+                                            end_bit, st);
             JB_LAUNCH_CHECK();
-            k_sorted_gather_rec<<<grid_cap(n), 256, 0, st>>>(rec.p, ordr.p, n, spts.p, orig.p,
-                                                             pos.p, pv.scl, pv.sl, slen.p);
+            {
+                JB_PROF("sample_unpack", st);
+                k_rec_unpack<<<grid_cap(n), 256, 0, st>>>(srec.p, n, spts.p, orig.p, pos.p, pv.scl,
+                                                          pv.sl, slen.p);
+            }
             JB_LAUNCH_CHECK();
         } else {
             DArr<double2> cpts(n, st);
@@ -2093,6 +2107,8 @@ void lloyd_best_device(const PtsView& pv, const uint64_t* d_idx, int64_t n, uint
     DArr<unsigned long long> part(2 * nblocks, st);
     DArr<SeedState> ss(1, st);
     DArr<int64_t> chosen(k, st);
+    DArr<unsigned long long> d2_diag(1, st);
+    d2_diag.zero();
 
     double best_sse = 0.0;
     for (uint64_t restart = 0; restart < n_init; ++restart) {
@@ -2106,7 +2122,7 @@ void lloyd_best_device(const PtsView& pv, const uint64_t* d_idx, int64_t n, uint
             JB_PROF("d2_update", st);
             k_d2_tiles<<<tile_grid, 256, 0, st>>>(spts.p, orig.p, pos.p, n, nullptr, nullptr,
                                                   tmax.p, d2s.p, ss.p, 1, Ed2, part.p, nullptr,
-                                                  nullptr);
+                                                  nullptr, d2_diag.p);
         }
         JB_LAUNCH_CHECK();
         for (uint64_t c = 1; c < k; ++c) {
@@ -2123,7 +2139,7 @@ void lloyd_best_device(const PtsView& pv, const uint64_t* d_idx, int64_t n, uint
                                                      d2_work.p, d2_nwork.p, nullptr);
                 k_d2_tiles<<<tile_grid, 256, 0, st>>>(spts.p, orig.p, pos.p, n, d2_work.p,
                                                       d2_nwork.p, tmax.p, d2s.p, ss.p, 0, Ed2,
-                                                      part.p, nullptr, nullptr);
+                                                      part.p, nullptr, nullptr, d2_diag.p);
                 JB_LAUNCH_CHECK();
             }
         }
@@ -2200,6 +2216,9 @@ void lloyd_best_device(const PtsView& pv, const uint64_t* d_idx, int64_t n, uint
             JB_CUDA(cudaStreamSynchronize(st));
             out.work_tiles = diag[0];
             out.changed_labels = diag[1];
+            JB_CUDA(cudaMemcpyAsync(diag, d2_diag.p, 8, cudaMemcpyDeviceToHost, st));
+            JB_CUDA(cudaStreamSynchronize(st));
+            out.d2_tiles = diag[0];
         }
         lloyd_update_means_sync(L);
         JB_TRACE("kmeans: lloyd", st);
@@ -2647,7 +2666,7 @@ void lloyd_best_dist(const Comm& cm, const PtsView& pv, const uint64_t* d_lidx,
             JB_PROF("d2_update", st);
             k_d2_tiles<<<tile_grid, 256, 0, st>>>(spts.p, orig.p, pos.p, n, nullptr, nullptr,
                                                   tmax.p, d2s.p, ss.p, 1, Ed2, part.p, cur.p,
-                                                  gkey.p);
+                                                  gkey.p, nullptr);
         }
         JB_LAUNCH_CHECK();
         for (uint64_t c = 1; c < k; ++c) {
@@ -2724,7 +2743,7 @@ void lloyd_best_dist(const Comm& cm, const PtsView& pv, const uint64_t* d_lidx,
                                                      d2_work.p, d2_nwork.p, cur.p);
                 k_d2_tiles<<<tile_grid, 256, 0, st>>>(spts.p, orig.p, pos.p, n, d2_work.p,
                                                       d2_nwork.p, tmax.p, d2s.p, ss.p, 0, Ed2,
-                                                      part.p, cur.p, gkey.p);
+                                                      part.p, cur.p, gkey.p, nullptr);
                 JB_LAUNCH_CHECK();
             }
         }
