@@ -29,8 +29,10 @@ using jb_api::MaxOp;
 // ---------------------------------------------------------------------------
 // kernel-level event profiler (jb_device.hpp: prof_begin / prof_end)
 
+#include <exception>
 #include <map>
 #include <mutex>
+#include <thread>
 
 namespace jb {
 namespace prof_detail {
@@ -201,6 +203,8 @@ double ms_since(Clock::time_point t0) {
 struct jb_context {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;  // svq sampling, concurrent with scale_pieces
+    cudaEvent_t side_done = nullptr;
 };
 
 struct jb_fit {
@@ -451,6 +455,49 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
     }
     fit->piece_base = base;
 
+    // svq on one GPU: the engine draws and the sample (sampling_kmeans
+    // clustering.hpp:251-262) depend only on N and the seed, so they run on
+    // a side stream from a helper thread while scale_pieces runs here; the
+    // backend joins them (and rethrows their error after scale's own).
+    struct SvqPre {
+        DArr<uint64_t> raw, sample;
+        SampleOrder jorder;
+        uint64_t S = 0, raw_count = 0, cursor = 0;
+        std::exception_ptr err;
+        std::thread th;
+        ~SvqPre() {
+            if (th.joinable()) th.join();
+        }
+    } pre;
+    if (c.backend == JB_BACKEND_SVQ && !cm.dist()) {
+        if (!ctx->side) {
+            JB_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+            JB_CUDA(cudaEventCreateWithFlags(&ctx->side_done, cudaEventDisableTiming));
+        }
+        const int dev = ctx->device;
+        cudaStream_t s2 = ctx->side;
+        cudaEvent_t ev = ctx->side_done;
+        const int64_t Ng = N_glob;
+        pre.th = std::thread([&pre, &c, dev, s2, ev, Ng] {
+            try {
+                JB_CUDA(cudaSetDevice(dev));
+                validate_vq(c, c.r);
+                pre.S = (uint64_t)std::llround(c.r * (double)Ng);
+                if (pre.S < c.k)
+                    throw Error(INVALID_INPUT, "sampling_kmeans: sample of " + std::to_string(pre.S) +
+                                                   " points is smaller than k=" +
+                                                   std::to_string(c.k) + " (increase r)");
+                pre.raw_count = pre.S + (c.k + 1) * c.n_init + 4096;
+                mt19937_64_generate(c.seed, pre.raw_count, pre.raw, s2);
+                pre.cursor = sample_indices_device((uint64_t)Ng, pre.S, pre.raw.p, pre.raw_count,
+                                                   pre.sample, s2, &pre.jorder);
+                JB_CUDA(cudaEventRecord(ev, s2));
+            } catch (...) {
+                pre.err = std::current_exception();
+            }
+        });
+    }
+
     // ---- digitize: scale_pieces ----
     auto t1 = Clock::now();
     Scaled sc;
@@ -506,19 +553,32 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
             break;
         }
         case JB_BACKEND_SVQ: {
-            validate_vq(c, c.r);
-            const uint64_t S = (uint64_t)std::llround(c.r * (double)N_glob);
-            if (S < c.k)
-                throw Error(INVALID_INPUT, "sampling_kmeans: sample of " + std::to_string(S) +
-                                               " points is smaller than k=" +
-                                               std::to_string(c.k) + " (increase r)");
             DArr<uint64_t> raw;
-            const uint64_t raw_count = S + (c.k + 1) * c.n_init + 4096;
-            mt19937_64_generate(c.seed, raw_count, raw, st);
-            JB_TRACE("svq: engine draws", st);
-            SampleOrder jorder;  // single GPU: gather-friendly Morton pass
-            uint64_t cursor = sample_indices_device((uint64_t)N_glob, S, raw.p, raw_count, sample,
-                                                    st, cm.dist() ? nullptr : &jorder);
+            SampleOrder jorder;  // single GPU: gather-friendly spatial pass
+            uint64_t S = 0, raw_count = 0, cursor = 0;
+            if (pre.th.joinable()) {  // sampled on the side stream (above)
+                pre.th.join();
+                if (pre.err) std::rethrow_exception(pre.err);
+                JB_CUDA(cudaStreamWaitEvent(st, ctx->side_done, 0));
+                S = pre.S;
+                raw_count = pre.raw_count;
+                cursor = pre.cursor;
+                raw = std::move(pre.raw);
+                sample = std::move(pre.sample);
+                jorder = std::move(pre.jorder);
+            } else {
+                validate_vq(c, c.r);
+                S = (uint64_t)std::llround(c.r * (double)N_glob);
+                if (S < c.k)
+                    throw Error(INVALID_INPUT, "sampling_kmeans: sample of " + std::to_string(S) +
+                                                   " points is smaller than k=" +
+                                                   std::to_string(c.k) + " (increase r)");
+                raw_count = S + (c.k + 1) * c.n_init + 4096;
+                mt19937_64_generate(c.seed, raw_count, raw, st);
+                JB_TRACE("svq: engine draws", st);
+                cursor = sample_indices_device((uint64_t)N_glob, S, raw.p, raw_count, sample, st,
+                                               cm.dist() ? nullptr : &jorder);
+            }
             JB_TRACE("svq: sample indices", st);
             KMeansOut km;
             if (cm.dist()) {  // the entries this rank owns, in sample order
@@ -753,6 +813,12 @@ void jb_context_destroy(jb_context* ctx) {
     cudaStreamSynchronize(ctx->stream);
     jb::dev_cache_drop(ctx->stream);
     cudaStreamSynchronize(ctx->stream);
+    if (ctx->side) {
+        cudaStreamSynchronize(ctx->side);
+        jb::dev_cache_drop(ctx->side);
+        cudaStreamSynchronize(ctx->side);
+        cudaEventDestroy(ctx->side_done);
+    }
     // buffers of fits that outlive the context stay valid (the stream handle
     // is not destroyed: a jb_fit still references it)
     delete ctx;

@@ -533,7 +533,18 @@ __global__ void k_rec_unpack(const SRec* __restrict__ srec, int64_t n, double2* 
         spts[s] = make_double2(scl * (double)c.len / sl, c.y);
         slen[s] = c.len;
         orig[s] = c.i;
-        pos[c.i] = (uint32_t)s;
+    }
+}
+
+// pos = inverse of orig, scattered in passes over ranges [lo, hi) of the
+// original index small enough to stay resident in L2 (the full 4n-byte
+// scatter would miss to DRAM on every 4-byte write)
+__global__ void k_pos_scatter(const uint32_t* __restrict__ orig, int64_t n, uint32_t lo,
+                              uint32_t hi, uint32_t* __restrict__ pos) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n;
+         s += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t o = orig[s];
+        if (o >= lo && o < hi) pos[o] = (uint32_t)s;
     }
 }
 
@@ -666,11 +677,22 @@ __global__ void k_d2_cull(const double4* __restrict__ tbox, const double* __rest
                           uint32_t* __restrict__ work, unsigned long long* __restrict__ nwork,
                           const double2* __restrict__ cur) {
     const double2 c = cur ? *cur : spts[pos[ss->last]];
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntiles;
+    const int lane = threadIdx.x & 31;
+    // warp-uniform trip count (t - lane is the warp's first tile)
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t - lane < ntiles;
          t += (int64_t)gridDim.x * blockDim.x) {
-        double dmin2, dmax2;
-        box_d2(c.x, c.y, tbox[t], dmin2, dmax2);
-        if (!(dmin2 * (1.0 - kKeepMargin) > tmax[t])) work[atomicAdd(nwork, 1ULL)] = (uint32_t)t;
+        bool need = false;
+        if (t < ntiles) {
+            double dmin2, dmax2;
+            box_d2(c.x, c.y, tbox[t], dmin2, dmax2);
+            need = !(dmin2 * (1.0 - kKeepMargin) > tmax[t]);
+        }
+        // one atomic per warp (a per-tile atomic on one counter serialises)
+        const unsigned m = __ballot_sync(0xffffffffu, need);
+        unsigned long long base = 0;
+        if (lane == 0 && m) base = atomicAdd(nwork, (unsigned long long)__popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (need) work[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)t;
     }
 }
 
@@ -781,7 +803,19 @@ __global__ void __launch_bounds__(PICK_TB) k_pick(const uint64_t* __restrict__ r
     const int R = ((nblocks + NW - 1) / NW + 31) & ~31;  // blocks per warp, multiple of 32
     const int b0 = min(nblocks, w * R), b1 = min(nblocks, b0 + R);
     i128 local = 0;
-    for (int b = b0 + lane; b < b1; b += 32) local += fx_load(part + 2 * b);
+    // 8 independent loads in flight per lane (a plain strided loop would wait
+    // one L2 round trip per block: ~42 per lane at config 4)
+    for (int b = b0 + lane; b < b1; b += 32 * 8) {
+        unsigned long long lo[8], hi[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int bb = b + 32 * u;
+            lo[u] = bb < b1 ? part[2 * bb] : 0ULL;
+            hi[u] = bb < b1 ? part[2 * bb + 1] : 0ULL;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) local += (i128)(((u128)hi[u] << 64) | (u128)lo[u]);
+    }
     local = fx_warp_sum(local);  // lane 0 holds the warp's total
     if (lane == 0) {
         s_wt_lo[w] = (unsigned long long)(u128)local;
@@ -1998,6 +2032,11 @@ void lloyd_best_device(const PtsView& pv, const uint64_t* d_idx, int64_t n, uint
                 JB_PROF("sample_unpack", st);
                 k_rec_unpack<<<grid_cap(n), 256, 0, st>>>(srec.p, n, spts.p, orig.p, pos.p, pv.scl,
                                                           pv.sl, slen.p);
+                // ~48 MB of pos per pass: resident in the 126 MB L2 while scattered
+                const int64_t span = (int64_t)12 << 20;
+                for (int64_t lo = 0; lo < n; lo += span)
+                    k_pos_scatter<<<grid_cap(n), 256, 0, st>>>(
+                        orig.p, n, (uint32_t)lo, (uint32_t)std::min<int64_t>(n, lo + span), pos.p);
             }
             JB_LAUNCH_CHECK();
         } else {
