@@ -20,7 +20,8 @@ NAMES = {
     "assign_stats": r"k_assign_stats", "inverse_chain": r"k_inv_chains",
     "inverse_fill": r"k_inv_fill", "d2_update": r"k_d2_tiles", "d2_pick": r"k_pick\b",
     "compress_spec": r"k_spec", "compress_emit": r"k_emit", "scale_sum_var": r"k_sum_var",
-    "scale_sum_inc": r"k_sum_inc",
+    "scale_sum_inc": r"k_sum_inc", "inverse_fused": r"k_inv_fused", "sample_order": r"k_rowkey_jorder",
+    "sample_unpack": r"k_rec_unpack",
 }
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
