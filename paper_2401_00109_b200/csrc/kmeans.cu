@@ -22,12 +22,15 @@
 #include <cub/cub.cuh>
 
 #include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <map>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "jb_device.hpp"
@@ -2319,6 +2322,116 @@ void kmeans_labels(KMeansOut& out, int64_t n, cudaStream_t st) {
 namespace jb {
 namespace {
 
+// ---------------------------------------------------------------------------
+// Device-side exchanges of the joint fit. Every exchanged quantity is a
+// vector of u64 words whose word-wise sum over ranks is the wanted result
+// (l3 limbs, 32-bit halves of int128 partials, or one owner's bits with
+// zeros elsewhere), so a sum all-reduce is exact and identical on every
+// rank. Transport: NCCL on the fit's stream when every rank drives its own
+// GPU (the libnccl the process already loaded -- torch's -- else the
+// system's, found at run time), else staged through the caller's host
+// allgather (jb_comm), e.g. gloo ranks sharing one GPU in the tests.
+
+struct NcclApi {
+    bool tried = false;
+    void* h = nullptr;
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+std::mutex g_nccl_mu;
+std::map<std::tuple<const void*, int, int, int>, ncclComm_t> g_nccl_comms;
+
+const NcclApi* nccl_api() {
+    if (!g_nccl.tried) {
+        g_nccl.tried = true;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+        if (h) {
+            g_nccl.get_unique_id = (decltype(g_nccl.get_unique_id))dlsym(h, "ncclGetUniqueId");
+            g_nccl.comm_init_rank = (decltype(g_nccl.comm_init_rank))dlsym(h, "ncclCommInitRank");
+            g_nccl.all_reduce = (decltype(g_nccl.all_reduce))dlsym(h, "ncclAllReduce");
+            g_nccl.error_string = (decltype(g_nccl.error_string))dlsym(h, "ncclGetErrorString");
+            if (g_nccl.get_unique_id && g_nccl.comm_init_rank && g_nccl.all_reduce &&
+                g_nccl.error_string)
+                g_nccl.h = h;
+        }
+    }
+    return g_nccl.h ? &g_nccl : nullptr;
+}
+
+struct DevComm {
+    const Comm* cm = nullptr;
+    ncclComm_t nc = nullptr;  // null: staged through cm's host allgather
+
+    // a collective call: the same on every rank (the bus-id exchange and the
+    // NCCL bootstrap go through the host allgather)
+    void init(const Comm& c, cudaStream_t st) {
+        cm = &c;
+        if (!c.dist() || getenv("JB_DIST_STAGED")) return;
+        int dev = 0;
+        JB_CUDA(cudaGetDevice(&dev));
+        char bus[32] = {0};
+        JB_CUDA(cudaDeviceGetPCIBusId(bus, sizeof bus, dev));
+        std::vector<char> all(32 * (size_t)c.world);
+        c.allgather(bus, 32, all.data());
+        bool distinct = true;  // NCCL needs one GPU per rank
+        for (int a = 0; a < c.world && distinct; ++a)
+            for (int b = a + 1; b < c.world; ++b)
+                if (!strncmp(&all[32 * a], &all[32 * b], 32)) distinct = false;
+        int ok = distinct && nccl_api() != nullptr;
+        std::vector<int> oks(c.world);
+        c.allgather(&ok, sizeof ok, oks.data());
+        for (int v : oks) ok &= v;
+        if (!ok) return;
+        std::lock_guard<std::mutex> lk(g_nccl_mu);
+        const auto key = std::make_tuple((const void*)c.c, c.rank, c.world, dev);
+        auto it = g_nccl_comms.find(key);
+        if (it != g_nccl_comms.end()) {
+            nc = it->second;
+            return;
+        }
+        ncclUniqueId id;
+        memset(&id, 0, sizeof id);
+        if (c.rank == 0 && g_nccl.get_unique_id(&id) != ncclSuccess)
+            throw Error(NCCL_ERROR, "ncclGetUniqueId failed");
+        std::vector<ncclUniqueId> ids(c.world);
+        c.allgather(&id, sizeof id, ids.data());
+        const ncclResult_t r = g_nccl.comm_init_rank(&nc, c.world, ids[0], c.rank);
+        if (r != ncclSuccess)
+            throw Error(NCCL_ERROR, std::string("ncclCommInitRank: ") + g_nccl.error_string(r));
+        g_nccl_comms[key] = nc;
+        (void)st;
+    }
+
+    // p[0..count) = word-wise sum over ranks (mod 2^64), in stream order
+    void allreduce_u64(unsigned long long* p, size_t count, cudaStream_t st) const {
+        if (!cm->dist() || count == 0) return;
+        if (nc) {
+            const ncclResult_t r =
+                g_nccl.all_reduce(p, p, count, ncclUint64, ncclSum, nc, st);
+            if (r != ncclSuccess)
+                throw Error(NCCL_ERROR, std::string("ncclAllReduce: ") + g_nccl.error_string(r));
+            return;
+        }
+        std::vector<unsigned long long> h(count);
+        JB_CUDA(cudaMemcpyAsync(h.data(), p, 8 * count, cudaMemcpyDeviceToHost, st));
+        JB_CUDA(cudaStreamSynchronize(st));
+        const auto all = cm->gather(h);
+        for (size_t i = 0; i < count; ++i) {
+            unsigned long long v = 0;
+            for (int r = 0; r < cm->world; ++r) v += all[(size_t)r * count + i];
+            h[i] = v;
+        }
+        JB_CUDA(cudaMemcpyAsync(p, h.data(), 8 * count, cudaMemcpyHostToDevice, st));
+        JB_CUDA(cudaStreamSynchronize(st));
+    }
+    bool nccl() const { return nc != nullptr; }
+};
+
 __global__ void k_gkey(const uint32_t* __restrict__ gpos, const uint32_t* __restrict__ orig,
                        int64_t n, uint32_t* __restrict__ gkey) {
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
@@ -2364,13 +2477,6 @@ __global__ void k_last_positive(const uint32_t* __restrict__ gpos, const uint32_
     if ((threadIdx.x & 31) == 0) atomicMax(out, best);
 }
 
-// acc += delta, word by word (l3 limbs and two's complement counts are additive)
-__global__ void k_add_acc(unsigned long long* __restrict__ acc,
-                          const unsigned long long* __restrict__ delta, int k) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 7 * k; i += gridDim.x * blockDim.x)
-        acc[i] += delta[i];
-}
-
 // re-seed empty cluster c at the globally chosen far point (update_means :193-196)
 __global__ void k_repair_dist(unsigned long long* __restrict__ acc, double* __restrict__ centers,
                               uint32_t* __restrict__ labs, uint32_t* __restrict__ tlab, int k,
@@ -2390,6 +2496,207 @@ __global__ void k_repair_dist(unsigned long long* __restrict__ acc, double* __re
         labs[owner_r] = (uint32_t)c;
         tlab[owner_r / TILE] = MIXED;
         tlab[ntiles + owner_r / (TILE * 32)] = MIXED;
+    }
+}
+
+// ---- device-side distributed D^2 round (no host round trip) ----
+
+// int128 (lo, hi) partials <-> three additive words (bits 0-31 and 32-63 of
+// lo, and hi): a word-wise sum over ranks recombines to the exact total
+__global__ void k_part_split(const unsigned long long* __restrict__ part, int nblocks,
+                             unsigned long long* __restrict__ p3) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nblocks; b += gridDim.x * blockDim.x) {
+        const unsigned long long lo = part[2 * b], hi = part[2 * b + 1];
+        p3[3 * b] = lo & 0xFFFFFFFFull;
+        p3[3 * b + 1] = lo >> 32;
+        p3[3 * b + 2] = hi;
+    }
+}
+
+__global__ void k_part_join(const unsigned long long* __restrict__ p3, int nblocks,
+                            unsigned long long* __restrict__ gpart) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nblocks; b += gridDim.x * blockDim.x) {
+        const u128 v = (u128)p3[3 * b] + ((u128)p3[3 * b + 1] << 32) + ((u128)p3[3 * b + 2] << 64);
+        gpart[2 * b] = (unsigned long long)v;
+        gpart[2 * b + 1] = (unsigned long long)(v >> 64);
+    }
+}
+
+struct DPick {
+    unsigned long long U[2], before[2];
+    long long fb;  // crossing block, -1: none (degenerate round or spill)
+    int deg;       // this round: every remaining point duplicates a center
+    int spill;     // sticky: a roundoff spill happened (host re-runs the seeding)
+};
+
+// total, u and the crossing block of the global partial sums (k_pick's
+// arithmetic): 1024 threads over contiguous block ranges, one exact scan
+__global__ void __launch_bounds__(PICK_TB) k_dpick_block(const uint64_t* __restrict__ raw,
+                                                         const unsigned long long* __restrict__ gpart,
+                                                         int nblocks, int E, SeedState* ss,
+                                                         int64_t* __restrict__ chosen, int c,
+                                                         DPick* dp) {
+    __shared__ unsigned long long s_lo[32], s_hi[32];
+    __shared__ unsigned long long s_found;
+    const int t = threadIdx.x;
+    const int per = (nblocks + PICK_TB - 1) / PICK_TB;
+    const int b0 = min(nblocks, t * per), b1 = min(nblocks, b0 + per);
+    i128 local = 0;
+    for (int b = b0; b < b1; ++b) local += fx_load(gpart + 2 * b);
+    if (t == 0) s_found = ~0ULL;
+    i128 total;
+    const i128 ex = block_exscan_i128(local, &total, s_lo, s_hi);
+    const double total_d = fx_to_double(total, E);
+    if (!(total_d > 0.0)) {  // every remaining point duplicates a center (:120-124)
+        if (t == 0) {
+            int64_t next = 0;
+            for (;;) {
+                bool taken = false;
+                for (int q = 0; q < c; ++q) taken |= chosen[q] == next;
+                if (!taken) break;
+                ++next;
+            }
+            chosen[c] = next;
+            ss->degenerate = 1;
+            dp->deg = 1;
+            dp->fb = -1;
+        }
+        return;
+    }
+    const uint64_t x = raw[ss->cursor];
+    double canon = __ull2double_rn(x) * 0x1p-64;  // generate_canonical<double,53>
+    if (canon >= 1.0) canon = 0x1.fffffffffffffp-1;
+    const double u = canon * total_d + 0.0;
+    const i128 U = fx_from_double(u, E);
+    i128 run = ex;
+    int mine = -1;
+    for (int b = b0; b < b1; ++b) {
+        const i128 v = fx_load(gpart + 2 * b);
+        if (U < run + v) {
+            mine = b;
+            break;
+        }
+        run += v;
+    }
+    if (mine >= 0) atomicMin(&s_found, (unsigned long long)mine);
+    __syncthreads();
+    if (t == 0) {
+        dp->deg = 0;
+        dp->fb = s_found == ~0ULL ? -1 : (long long)s_found;
+        dp->U[0] = (unsigned long long)(u128)U;
+        dp->U[1] = (unsigned long long)((u128)U >> 64);
+        if (s_found == ~0ULL) dp->spill = 1;
+    }
+    if (mine >= 0 && (unsigned long long)mine == s_found) {
+        dp->before[0] = (unsigned long long)(u128)run;
+        dp->before[1] = (unsigned long long)((u128)run >> 64);
+    }
+}
+
+// this rank's d2 bits of the crossing block's entries (zeros elsewhere)
+__global__ void k_dblock_weights(const uint32_t* __restrict__ gpos, const uint32_t* __restrict__ pos,
+                                 int64_t n, const double* __restrict__ d2s, const DPick* dp,
+                                 unsigned long long* __restrict__ w) {
+    if (dp->fb < 0) return;
+    const uint64_t q0 = (uint64_t)dp->fb * D2_R, q1 = q0 + D2_R;
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t m = (lo + hi) >> 1;
+        if (gpos[m] < q0) lo = m + 1;
+        else hi = m;
+    }
+    for (int64_t i = lo + threadIdx.x; i < n && gpos[i] < q1; i += blockDim.x)
+        w[gpos[i] - q0] = (unsigned long long)__double_as_longlong(d2s[pos[i]]);
+}
+
+// the element inside the crossing block from the gathered weights
+__global__ void __launch_bounds__(PICK_TB) k_dpick_elem(const unsigned long long* __restrict__ w,
+                                                        DPick* dp, int E, SeedState* ss,
+                                                        int64_t* __restrict__ chosen, int c,
+                                                        uint64_t S) {
+    __shared__ unsigned long long s_lo[32], s_hi[32];
+    __shared__ unsigned long long s_found;
+    if (dp->deg) return;
+    const int t = threadIdx.x;
+    if (dp->fb < 0) {  // roundoff spill (:67-70): the host re-runs the seeding
+        if (t == 0) chosen[c] = (int64_t)S - 1;
+        return;
+    }
+    if (t == 0) s_found = ~0ULL;
+    const uint64_t e0 = (uint64_t)dp->fb * D2_R + 2 * t;
+    i128 a = 0, b = 0;
+    if (e0 < S) a = fx_from_double(__longlong_as_double((long long)w[2 * t]), E);
+    if (e0 + 1 < S) b = fx_from_double(__longlong_as_double((long long)w[2 * t + 1]), E);
+    i128 dummy;
+    const i128 ex2 = block_exscan_i128(a + b, &dummy, s_lo, s_hi);
+    const i128 U = fx_load(dp->U), before = fx_load(dp->before) + ex2;
+    unsigned long long hit = ~0ULL;
+    if (e0 < S && U < before + a) hit = e0;
+    else if (e0 + 1 < S && U < before + a + b) hit = e0 + 1;
+    if (hit != ~0ULL) atomicMin(&s_found, hit);
+    __syncthreads();
+    if (t == 0) {
+        if (s_found == ~0ULL) {
+            dp->spill = 1;
+            chosen[c] = (int64_t)S - 1;
+        } else {
+            chosen[c] = (int64_t)s_found;
+        }
+        ss->cursor += 1;
+    }
+}
+
+// the chosen point's bits from its owner (zeros on the other ranks)
+__global__ void k_dcenter_bits(const uint32_t* __restrict__ gpos, const uint32_t* __restrict__ pos,
+                               const double2* __restrict__ spts, int64_t n,
+                               const int64_t* __restrict__ chosen, int c,
+                               unsigned long long* __restrict__ cb) {
+    const uint64_t q = (uint64_t)chosen[c];
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t m = (lo + hi) >> 1;
+        if (gpos[m] < q) lo = m + 1;
+        else hi = m;
+    }
+    cb[0] = cb[1] = 0;
+    if (lo < n && gpos[lo] == q) {
+        const double2 p = spts[pos[lo]];
+        cb[0] = (unsigned long long)__double_as_longlong(p.x);
+        cb[1] = (unsigned long long)__double_as_longlong(p.y);
+    }
+}
+
+__global__ void k_dstore_center(const unsigned long long* __restrict__ cb, double* __restrict__ centers,
+                                int c) {
+    centers[2 * c] = __longlong_as_double((long long)cb[0]);
+    centers[2 * c + 1] = __longlong_as_double((long long)cb[1]);
+}
+
+// Lloyd iteration end of the joint fit (device loop): acc += the all-reduced
+// deltas; ++iterations; converged when no label changed anywhere. Gated like
+// k_iter_end (pending empty-cluster repair / converged: no-op).
+__global__ void k_dist_accum(unsigned long long* __restrict__ acc,
+                             unsigned long long* __restrict__ dacc, int k,
+                             int* __restrict__ state, unsigned long long* __restrict__ changed,
+                             unsigned long long* __restrict__ nwork,
+                             unsigned long long* __restrict__ nswork,
+                             unsigned long long* __restrict__ diag, int count_iter) {
+    if (count_iter && (state[0] | state[1])) return;
+    for (int i = threadIdx.x; i < 7 * k; i += blockDim.x) {
+        acc[i] += dacc[i];
+        dacc[i] = 0;
+    }
+    if (threadIdx.x == 0) {
+        if (count_iter) {
+            state[2] += 1;
+            diag[0] += *nwork;
+            diag[2] += *nswork;
+            diag[1] += *changed;
+            if (*changed == 0) state[1] = 1;
+        }
+        *changed = 0;
+        *nwork = 0;
+        *nswork = 0;
     }
 }
 
@@ -2579,27 +2886,6 @@ void lloyd_best_dist(const Comm& cm, const PtsView& pv, const uint64_t* d_lidx,
         throw Error(INTERNAL, "distributed seeding: no owner for a sample position");
     };
 
-    auto exchange_deltas = [&]() -> unsigned long long {  // returns global changed count
-        std::vector<unsigned long long> h(7 * k + 1);
-        L.dacc.download(h.data(), 7 * k);
-        L.flags.download(h.data() + 7 * k, 1);
-        JB_CUDA(cudaStreamSynchronize(st));
-        const auto all = cm.gather(h);
-        std::vector<unsigned long long> sum(7 * k + 1, 0);
-        for (int r = 0; r < cm.world; ++r) {  // every word is additive
-            const unsigned long long* o = &all[(size_t)r * (7 * k + 1)];
-            for (uint64_t i = 0; i < 7 * k + 1; ++i) sum[i] += o[i];
-        }
-        L.dacc.upload(sum.data(), 7 * k);
-        k_add_acc<<<1, 256, 0, st>>>(L.acc.p, L.dacc.p, (int)k);
-        JB_LAUNCH_CHECK();
-        L.dacc.zero();
-        JB_CUDA(cudaMemsetAsync(L.flags.p, 0, 8, st));
-        JB_CUDA(cudaMemsetAsync(L.nwork.p, 0, 8, st));
-        JB_CUDA(cudaMemsetAsync(L.nswork.p, 0, 8, st));
-        return sum[7 * k];
-    };
-
     auto repair_dist = [&]() {  // update_means :181-197 across ranks
         lloyd_means(L, false);
         int ne = 0;
@@ -2686,116 +2972,208 @@ void lloyd_best_dist(const Comm& cm, const PtsView& pv, const uint64_t* d_lidx,
         JB_CUDA(cudaMemcpyAsync(L.empties.p + L.k, &zero, sizeof(int), cudaMemcpyHostToDevice, st));
     };
 
-    double best_sse = 0.0;
-    for (uint64_t restart = 0; restart < n_init; ++restart) {
-        // ---- d2_seed (clustering.hpp:92-131) ----
-        std::vector<uint64_t> chosen;
-        std::vector<double> ch_xy;
-        uint64_t cur_draw = *cursor, r0;
-        while (!lemire_host(draw(cur_draw), S, r0)) ++cur_draw;
-        cur_draw += 1;
-        chosen.push_back(r0);
-        auto xy = center_of(r0);
-        ch_xy.push_back(xy.first);
-        ch_xy.push_back(xy.second);
-        double2 hc = make_double2(xy.first, xy.second);
-        cur.upload(&hc, 1);
+    // host-driven seeding: every decision on the host from allgathered
+    // partials (kept as the fallback of the device path's roundoff spill)
+    auto seed_host = [&]() {
+            std::vector<uint64_t> chosen;
+            std::vector<double> ch_xy;
+            uint64_t cur_draw = *cursor, r0;
+            while (!lemire_host(draw(cur_draw), S, r0)) ++cur_draw;
+            cur_draw += 1;
+            chosen.push_back(r0);
+            auto xy = center_of(r0);
+            ch_xy.push_back(xy.first);
+            ch_xy.push_back(xy.second);
+            double2 hc = make_double2(xy.first, xy.second);
+            cur.upload(&hc, 1);
+            part.zero();
+            if (n > 0) {
+                JB_PROF("d2_update", st);
+                k_d2_tiles<<<tile_grid, 256, 0, st>>>(spts.p, orig.p, pos.p, n, nullptr, nullptr,
+                                                      tmax.p, d2s.p, ss.p, 1, Ed2, part.p, cur.p,
+                                                      gkey.p, nullptr);
+            }
+            JB_LAUNCH_CHECK();
+            for (uint64_t c = 1; c < k; ++c) {
+                std::vector<unsigned long long> hp = part.to_host(2 * nblocks);
+                hp = cm.sum_i128(hp);
+                i128 total = 0;
+                for (uint64_t b = 0; b < nblocks; ++b) total += fx_load(&hp[2 * b]);
+                const double total_d = fx_to_double(total, Ed2);
+                uint64_t next;
+                if (!(total_d > 0.0)) {  // every remaining point duplicates a center (:120-124)
+                    next = 0;
+                    while (std::find(chosen.begin(), chosen.end(), next) != chosen.end()) ++next;
+                } else {
+                    const uint64_t x = draw(cur_draw);
+                    double canon = (double)x * 0x1p-64;  // generate_canonical<double,53>
+                    if (canon >= 1.0) canon = 0x1.fffffffffffffp-1;
+                    const double u = canon * total_d + 0.0;
+                    const i128 U = fx_from_double(u, Ed2);
+                    i128 run = 0;
+                    uint64_t fb = nblocks;
+                    for (uint64_t b = 0; b < nblocks; ++b) {
+                        const i128 v = fx_load(&hp[2 * b]);
+                        if (U < run + v) {
+                            fb = b;
+                            break;
+                        }
+                        run += v;
+                    }
+                    if (fb == nblocks) {  // roundoff spill: last positive-weight index (:67-70)
+                        long long lp = -1;
+                        if (n > 0) {
+                            dll.upload(&lp, 1);
+                            k_last_positive<<<1, 256, 0, st>>>(d_gpos, pos.p, n, d2s.p, dll.p);
+                            dll.download(&lp, 1);
+                            JB_CUDA(cudaStreamSynchronize(st));
+                        }
+                        std::vector<long long> all(cm.world);
+                        cm.allgather(&lp, sizeof lp, all.data());
+                        long long m = (long long)S - 1, best = -1;
+                        for (auto v : all) best = std::max(best, v);
+                        next = best >= 0 ? (uint64_t)best : (uint64_t)m;
+                    } else {
+                        wblk.zero();
+                        if (n > 0) k_block_weights<<<1, 256, 0, st>>>(d_gpos, pos.p, n, d2s.p, fb, wblk.p);
+                        JB_LAUNCH_CHECK();
+                        std::vector<double> w = wblk.to_host(D2_R);
+                        const auto all = cm.gather(w);  // every position owned by exactly one rank
+                        next = UINT64_MAX;
+                        i128 before = run;
+                        for (uint64_t e = 0; e < D2_R && fb * D2_R + e < S; ++e) {
+                            double we = 0.0;
+                            for (int r = 0; r < cm.world; ++r) we += all[(size_t)r * D2_R + e];
+                            const i128 a = fx_from_double(we, Ed2);
+                            if (U < before + a) {
+                                next = fb * D2_R + e;
+                                break;
+                            }
+                            before += a;
+                        }
+                        if (next == UINT64_MAX) throw Error(INTERNAL, "distributed D2 pick failed");
+                    }
+                    cur_draw += 1;
+                }
+                chosen.push_back(next);
+                xy = center_of(next);
+                ch_xy.push_back(xy.first);
+                ch_xy.push_back(xy.second);
+                if (c + 1 < k && n > 0) {
+                    hc = make_double2(xy.first, xy.second);
+                    cur.upload(&hc, 1);
+                    JB_PROF("d2_update", st);
+                    JB_CUDA(cudaMemsetAsync(d2_nwork.p, 0, 8, st));
+                    k_d2_cull<<<cull_grid, 256, 0, st>>>(tbox.p, tmax.p, ntiles, spts.p, pos.p, ss.p,
+                                                         d2_work.p, d2_nwork.p, cur.p);
+                    k_d2_tiles<<<tile_grid, 256, 0, st>>>(spts.p, orig.p, pos.p, n, d2_work.p,
+                                                          d2_nwork.p, tmax.p, d2s.p, ss.p, 0, Ed2,
+                                                          part.p, cur.p, gkey.p, nullptr);
+                    JB_LAUNCH_CHECK();
+                }
+            }
+            *cursor = cur_draw;
+            L.centers.upload(ch_xy.data(), 2 * k);
+            if (dbg_on())
+                fprintf(stderr, "[jb r%d] dist seeds: S=%llu n=%lld Ed2=%d Ex=%d Ey=%d chosen[0..3]=%llu %llu %llu %llu hash=%016llx cursor=%llu\n",
+                        cm.rank, (unsigned long long)S, (long long)n, Ed2, L.Ex, L.Ey,
+                        (unsigned long long)chosen[0], (unsigned long long)chosen[std::min<uint64_t>(1, k - 1)],
+                        (unsigned long long)chosen[std::min<uint64_t>(2, k - 1)], (unsigned long long)chosen[k - 1],
+                        (unsigned long long)dbg_hash(ch_xy.data(), 16 * k), (unsigned long long)cur_draw);
+    };
+
+    // device-driven seeding: partials all-reduced on the stream (DevComm),
+    // every rank picks the same point on device; false on a roundoff spill
+    DevComm dc;
+    dc.init(cm, st);
+    if (dbg_on())
+        fprintf(stderr, "[jb r%d] dist exchanges: %s\n", cm.rank,
+                dc.nccl() ? "NCCL on the stream" : "staged through the host allgather");
+    auto seed_device = [&]() -> bool {
+        DArr<SeedState> dss(1, st);
+        const SeedState h0{*cursor, 0, 0, 0};
+        dss.upload(&h0, 1);
+        DArr<int64_t> dch(k, st);
+        DArr<DPick> dp(1, st);
+        dp.zero();
+        DArr<unsigned long long> p3(3 * nblocks, st), gpart(2 * nblocks, st), w(D2_R, st), cb(2, st);
+        const double2* curp = reinterpret_cast<const double2*>(cb.p);
+        const int pg = (int)std::max<uint64_t>(1, std::min<uint64_t>((nblocks + 255) / 256, kSMs * 4));
         part.zero();
+        k_pick_first<<<1, 1, 0, st>>>(d_raw, S, dss.p, dch.p);
+        k_dcenter_bits<<<1, 1, 0, st>>>(d_gpos, pos.p, spts.p, n, dch.p, 0, cb.p);
+        JB_LAUNCH_CHECK();
+        dc.allreduce_u64(cb.p, 2, st);
+        k_dstore_center<<<1, 1, 0, st>>>(cb.p, L.centers.p, 0);
         if (n > 0) {
             JB_PROF("d2_update", st);
             k_d2_tiles<<<tile_grid, 256, 0, st>>>(spts.p, orig.p, pos.p, n, nullptr, nullptr,
-                                                  tmax.p, d2s.p, ss.p, 1, Ed2, part.p, cur.p,
+                                                  tmax.p, d2s.p, ss.p, 1, Ed2, part.p, curp,
                                                   gkey.p, nullptr);
         }
         JB_LAUNCH_CHECK();
         for (uint64_t c = 1; c < k; ++c) {
-            std::vector<unsigned long long> hp = part.to_host(2 * nblocks);
-            hp = cm.sum_i128(hp);
-            i128 total = 0;
-            for (uint64_t b = 0; b < nblocks; ++b) total += fx_load(&hp[2 * b]);
-            const double total_d = fx_to_double(total, Ed2);
-            uint64_t next;
-            if (!(total_d > 0.0)) {  // every remaining point duplicates a center (:120-124)
-                next = 0;
-                while (std::find(chosen.begin(), chosen.end(), next) != chosen.end()) ++next;
-            } else {
-                const uint64_t x = draw(cur_draw);
-                double canon = (double)x * 0x1p-64;  // generate_canonical<double,53>
-                if (canon >= 1.0) canon = 0x1.fffffffffffffp-1;
-                const double u = canon * total_d + 0.0;
-                const i128 U = fx_from_double(u, Ed2);
-                i128 run = 0;
-                uint64_t fb = nblocks;
-                for (uint64_t b = 0; b < nblocks; ++b) {
-                    const i128 v = fx_load(&hp[2 * b]);
-                    if (U < run + v) {
-                        fb = b;
-                        break;
-                    }
-                    run += v;
-                }
-                if (fb == nblocks) {  // roundoff spill: last positive-weight index (:67-70)
-                    long long lp = -1;
-                    if (n > 0) {
-                        dll.upload(&lp, 1);
-                        k_last_positive<<<1, 256, 0, st>>>(d_gpos, pos.p, n, d2s.p, dll.p);
-                        dll.download(&lp, 1);
-                        JB_CUDA(cudaStreamSynchronize(st));
-                    }
-                    std::vector<long long> all(cm.world);
-                    cm.allgather(&lp, sizeof lp, all.data());
-                    long long m = (long long)S - 1, best = -1;
-                    for (auto v : all) best = std::max(best, v);
-                    next = best >= 0 ? (uint64_t)best : (uint64_t)m;
-                } else {
-                    wblk.zero();
-                    if (n > 0) k_block_weights<<<1, 256, 0, st>>>(d_gpos, pos.p, n, d2s.p, fb, wblk.p);
-                    JB_LAUNCH_CHECK();
-                    std::vector<double> w = wblk.to_host(D2_R);
-                    const auto all = cm.gather(w);  // every position owned by exactly one rank
-                    next = UINT64_MAX;
-                    i128 before = run;
-                    for (uint64_t e = 0; e < D2_R && fb * D2_R + e < S; ++e) {
-                        double we = 0.0;
-                        for (int r = 0; r < cm.world; ++r) we += all[(size_t)r * D2_R + e];
-                        const i128 a = fx_from_double(we, Ed2);
-                        if (U < before + a) {
-                            next = fb * D2_R + e;
-                            break;
-                        }
-                        before += a;
-                    }
-                    if (next == UINT64_MAX) throw Error(INTERNAL, "distributed D2 pick failed");
-                }
-                cur_draw += 1;
+            {
+                JB_PROF("d2_pick", st);
+                k_part_split<<<pg, 256, 0, st>>>(part.p, (int)nblocks, p3.p);
+                dc.allreduce_u64(p3.p, 3 * nblocks, st);
+                k_part_join<<<pg, 256, 0, st>>>(p3.p, (int)nblocks, gpart.p);
+                k_dpick_block<<<1, PICK_TB, 0, st>>>(d_raw, gpart.p, (int)nblocks, Ed2, dss.p,
+                                                     dch.p, (int)c, dp.p);
+                w.zero();
+                if (n > 0) k_dblock_weights<<<1, 256, 0, st>>>(d_gpos, pos.p, n, d2s.p, dp.p, w.p);
+                JB_LAUNCH_CHECK();
+                dc.allreduce_u64(w.p, D2_R, st);
+                k_dpick_elem<<<1, PICK_TB, 0, st>>>(w.p, dp.p, Ed2, dss.p, dch.p, (int)c, S);
+                k_dcenter_bits<<<1, 1, 0, st>>>(d_gpos, pos.p, spts.p, n, dch.p, (int)c, cb.p);
+                JB_LAUNCH_CHECK();
+                dc.allreduce_u64(cb.p, 2, st);
+                k_dstore_center<<<1, 1, 0, st>>>(cb.p, L.centers.p, (int)c);
             }
-            chosen.push_back(next);
-            xy = center_of(next);
-            ch_xy.push_back(xy.first);
-            ch_xy.push_back(xy.second);
             if (c + 1 < k && n > 0) {
-                hc = make_double2(xy.first, xy.second);
-                cur.upload(&hc, 1);
                 JB_PROF("d2_update", st);
                 JB_CUDA(cudaMemsetAsync(d2_nwork.p, 0, 8, st));
                 k_d2_cull<<<cull_grid, 256, 0, st>>>(tbox.p, tmax.p, ntiles, spts.p, pos.p, ss.p,
-                                                     d2_work.p, d2_nwork.p, cur.p);
+                                                     d2_work.p, d2_nwork.p, curp);
                 k_d2_tiles<<<tile_grid, 256, 0, st>>>(spts.p, orig.p, pos.p, n, d2_work.p,
                                                       d2_nwork.p, tmax.p, d2s.p, ss.p, 0, Ed2,
-                                                      part.p, cur.p, gkey.p, nullptr);
-                JB_LAUNCH_CHECK();
+                                                      part.p, curp, gkey.p, nullptr);
+            }
+            JB_LAUNCH_CHECK();
+        }
+        SeedState hs;
+        DPick hp;
+        dss.download(&hs, 1);
+        dp.download(&hp, 1);
+        JB_CUDA(cudaStreamSynchronize(st));
+        if (hp.spill) return false;
+        if (hs.cursor > raw_count) throw Error(INTERNAL, "rng stream exhausted");
+        *cursor = hs.cursor;
+        return true;
+    };
+
+    double best_sse = 0.0;
+    for (uint64_t restart = 0; restart < n_init; ++restart) {
+        // ---- d2_seed (clustering.hpp:92-131) ----
+        {
+            const uint64_t cursor0 = *cursor;
+            if (getenv("JB_DIST_HOST_SEED") || !seed_device()) {
+                *cursor = cursor0;
+                seed_host();
             }
         }
-        *cursor = cur_draw;
-        L.centers.upload(ch_xy.data(), 2 * k);
-        if (dbg_on())
-            fprintf(stderr, "[jb r%d] dist seeds: S=%llu n=%lld Ed2=%d Ex=%d Ey=%d chosen[0..3]=%llu %llu %llu %llu hash=%016llx cursor=%llu\n",
-                    cm.rank, (unsigned long long)S, (long long)n, Ed2, L.Ex, L.Ey,
-                    (unsigned long long)chosen[0], (unsigned long long)chosen[std::min<uint64_t>(1, k - 1)],
-                    (unsigned long long)chosen[std::min<uint64_t>(2, k - 1)], (unsigned long long)chosen[k - 1],
-                    (unsigned long long)dbg_hash(ch_xy.data(), 16 * k), (unsigned long long)cur_draw);
 
-        // ---- Lloyd (lloyd_once :200-220), one exchange per iteration ----
+
+        // ---- Lloyd (lloyd_once :200-220): device loop, one all-reduce of the
+        // exact cluster-sum deltas + change count per iteration, host sync
+        // once per batch (empty clusters: re-seeded on the host path) ----
+        auto exchange_dev = [&](bool count_iter) {
+            dc.allreduce_u64(L.dacc.p, 7 * k, st);
+            dc.allreduce_u64(L.flags.p, 1, st);
+            k_dist_accum<<<1, 256, 0, st>>>(L.acc.p, L.dacc.p, (int)k, L.empties.p + L.k, L.flags.p,
+                                             L.nwork.p, L.nswork.p, L.diag.p, count_iter ? 1 : 0);
+            JB_LAUNCH_CHECK();
+        };
         L.acc.zero();
         L.dacc.zero();
         L.diag.zero();
@@ -2804,21 +3182,33 @@ void lloyd_best_dist(const Comm& cm, const PtsView& pv, const uint64_t* d_lidx,
         JB_CUDA(cudaMemsetAsync(L.flags.p, 0, 8, st));
         JB_CUDA(cudaMemsetAsync(L.nwork.p, 0, 8, st));
         JB_CUDA(cudaMemsetAsync(L.nswork.p, 0, 8, st));
-        lloyd_assign(L, true, false);
-        exchange_deltas();
+        lloyd_assign(L, true, false);  // assign_all(points, seeds) (:204)
+        exchange_dev(false);
         uint64_t it = 0;
-        for (; it < max_iters; ++it) {
-            repair_dist();                 // update_means (+ empty-cluster re-seeding)
-            lloyd_assign(L, false, false); // assign_all
-            const unsigned long long ch = exchange_deltas();
+        const uint64_t kBatch = dbg_on() ? 1 : 16;
+        while (it < max_iters) {
+            const uint64_t B = std::min<uint64_t>(kBatch, max_iters - it);
+            for (uint64_t b = 0; b < B; ++b) {
+                lloyd_means(L, true);          // update_means ...
+                lloyd_assign(L, false, true);  // ... assign_all, label comparison
+                exchange_dev(true);
+            }
+            LoopState h = lloyd_state(L);
+            it = (uint64_t)h.iters;
             if (dbg_on()) {
                 auto cc = L.centers.to_host(2 * k);
-                fprintf(stderr, "[jb r%d] dist iter %llu: changed=%llu centers=%016llx\n", cm.rank,
-                        (unsigned long long)it, ch, (unsigned long long)dbg_hash(cc.data(), 16 * k));
+                fprintf(stderr, "[jb r%d] dist iter %d: empty=%d conv=%d centers=%016llx\n", cm.rank,
+                        h.iters, h.n_empty, h.converged,
+                        (unsigned long long)dbg_hash(cc.data(), 16 * k));
             }
-            if (ch == 0) {
-                ++it;
-                break;
+            if (h.converged) break;
+            if (h.n_empty) {  // re-seed the empty clusters, finish the iteration
+                repair_dist();
+                lloyd_assign(L, false, true);
+                exchange_dev(true);
+                h = lloyd_state(L);
+                it = (uint64_t)h.iters;
+                if (h.converged) break;
             }
         }
         repair_dist();  // final update_means
