@@ -1696,6 +1696,9 @@ struct LloydCtx {
     DArr<unsigned long long> dacc;  // distributed fit: this rank's deltas (5k)
     bool use_dacc = false;
     ClusterAcc cacc() { return ClusterAcc{acc.p, acc.p + 3 * k, acc.p + 6 * k}; }
+    // label-change counter: in the distributed fit it trails the deltas
+    // (dacc[7k]) so one all-reduce carries both
+    unsigned long long* changed_ptr() { return use_dacc ? dacc.p + 7 * k : flags.p; }
     ClusterAcc tacc() {  // where the assignment writes
         return use_dacc ? ClusterAcc{dacc.p, dacc.p + 3 * k, dacc.p + 6 * k} : cacc();
     }
@@ -1762,7 +1765,7 @@ void lloyd_assign(LloydCtx& L, bool full, bool gate_on_empties) {
     auto kern = full ? k_lloyd_work<true> : k_lloyd_work<false>;
     kern<<<L.grid(), LL_TB, L.smem(full), L.st>>>(
         L.spts, L.n, L.centers.p, L.k, L.cg, L.labs.p, L.work.p, L.nwork.p, L.tnew.p, L.tlab.p,
-        L.Ex, L.Ey, L.tacc(), L.flags.p, gate, L.rg, L.rg.R > 0 ? L.slen : nullptr);
+        L.Ex, L.Ey, L.tacc(), L.changed_ptr(), gate, L.rg, L.rg.R > 0 ? L.slen : nullptr);
     JB_LAUNCH_CHECK();
 }
 
@@ -2767,7 +2770,7 @@ void lloyd_best_dist(const Comm& cm, const PtsView& pv, const uint64_t* d_lidx,
     L.centers.alloc(2 * k, st);
     L.labs.alloc(nn, st);
     L.acc.alloc(7 * k, st);
-    L.dacc.alloc(7 * k, st);
+    L.dacc.alloc(7 * k + 1, st);  // deltas + change count (changed_ptr)
     L.use_dacc = true;
     L.flags.alloc(1, st);
     L.empties.alloc(k + 3, st);
@@ -3168,9 +3171,9 @@ void lloyd_best_dist(const Comm& cm, const PtsView& pv, const uint64_t* d_lidx,
         // exact cluster-sum deltas + change count per iteration, host sync
         // once per batch (empty clusters: re-seeded on the host path) ----
         auto exchange_dev = [&](bool count_iter) {
-            dc.allreduce_u64(L.dacc.p, 7 * k, st);
-            dc.allreduce_u64(L.flags.p, 1, st);
-            k_dist_accum<<<1, 256, 0, st>>>(L.acc.p, L.dacc.p, (int)k, L.empties.p + L.k, L.flags.p,
+            dc.allreduce_u64(L.dacc.p, 7 * k + 1, st);
+            k_dist_accum<<<1, 256, 0, st>>>(L.acc.p, L.dacc.p, (int)k, L.empties.p + L.k,
+                                             L.changed_ptr(),
                                              L.nwork.p, L.nswork.p, L.diag.p, count_iter ? 1 : 0);
             JB_LAUNCH_CHECK();
         };
