@@ -95,6 +95,23 @@ __device__ __forceinline__ bool fbit(const uint32_t* __restrict__ fb, int64_t ch
     return (fb[ch * W + (rel >> 5)] >> (rel & 31)) & 1u;
 }
 
+// Correctly rounded quotient a / b (b a positive integer-valued double,
+// ry = RN(1 / b)) by FMA corrections: q0 = RN(a ry), then twice
+// q <- RN(q + RN(a - b q) ry), the remainder a - b q being exact under an
+// FMA. After the first correction q is faithful, and Markstein's theorem
+// makes the second one RN(a / b): the IEEE quotient the reference computes,
+// in 5 fp64 operations instead of the division sequence. Valid for
+// 2^-900 <= |a| <= 2^1000 (no underflow or overflow of the remainder);
+// callers fall back to the division outside that range.
+// tests/test_div_identity.py checks the identity against a / b.
+__device__ __forceinline__ double div_cr(double a, double b, double ry) {
+    const double q0 = __dmul_rn(a, ry);
+    const double q1 = __fma_rn(__fma_rn(-q0, b, a), ry, q0);
+    return __fma_rn(__fma_rn(-q1, b, a), ry, q1);
+}
+
+constexpr int kRcp = 256;  // k_spec reciprocal tables cover d <= kRcp
+
 // Phase 1: speculative parse of every chunk from its first start position,
 // streamed: each sample is loaded once (one register ahead) and tested once
 // against the open piece. When the test fails, the piece closes at the
@@ -107,6 +124,14 @@ __global__ void __launch_bounds__(128) k_spec(const double* __restrict__ v, Chun
                                               uint32_t* __restrict__ fb,
                                               int64_t* __restrict__ exit_spec,
                                               int* __restrict__ bad) {
+    // RN(1/d) and RN(1/d^2) for the FMA quotients (div_cr)
+    __shared__ double s_r1[kRcp + 1], s_r2[kRcp + 1];
+    for (int t = threadIdx.x; t <= kRcp; t += blockDim.x) {
+        const double dd = (double)(t > 0 ? t : 1);
+        s_r1[t] = 1.0 / dd;
+        s_r2[t] = 1.0 / (dd * dd);
+    }
+    __syncthreads();
     const int64_t ch = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (ch >= n_chunks) return;
     int64_t s, c, lo, hi, last;
@@ -150,14 +175,14 @@ __global__ void __launch_bounds__(128) k_spec(const double* __restrict__ v, Chun
             double sum_d2 = nsq;
             if (Ln > 165000) sum_d2 = d * (d + 1.0) * (2.0 * d + 1.0) / 6.0;
             double a, b;  // inc * inc / (len * len), 2.0 * inc / len
-            if ((Ln & (Ln - 1)) == 0) {
-                const int m = __ffsll(Ln) - 1;
-                const double inv = __longlong_as_double((long long)(1023 - m) << 52);
-                a = yy * (inv * inv);
-                b = (2.0 * y) * inv;
+            const double y2 = 2.0 * y, ay = fabs(y);
+            if (Ln <= kRcp && ((ay >= 0x1p-450 && ay <= 0x1p500) || y == 0.0)) {
+                // warp-uniform in practice: no divergent division sequence
+                a = yy == 0.0 ? yy : div_cr(yy, d * d, s_r2[Ln]);
+                b = y2 == 0.0 ? y2 : div_cr(y2, d, s_r1[Ln]);  // 0 / d keeps the zero's sign
             } else {
                 a = yy / (d * d);
-                b = 2.0 * y / d;
+                b = y2 / d;
             }
             const double sq_dev = a * sum_d2 - b * ns3 + ns2;
             brk = sq_dev > (d - 1.0) * tol2;

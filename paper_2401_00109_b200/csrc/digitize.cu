@@ -396,8 +396,17 @@ __global__ void k_relabel(uint32_t* __restrict__ labels, int64_t n,
     extern __shared__ uint32_t rk[];
     for (int c = threadIdx.x; c < k; c += blockDim.x) rk[c] = rank_of[c];
     __syncthreads();
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
+    // 16-byte accesses, two in flight per thread (labels are 256-byte aligned)
+    uint4* l4 = reinterpret_cast<uint4*>(labels);
+    const int64_t n4 = n >> 2, stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += 2 * stride) {
+        uint4 a = l4[i], b = make_uint4(0, 0, 0, 0);
+        const bool two = i + stride < n4;
+        if (two) b = l4[i + stride];
+        l4[i] = make_uint4(rk[a.x], rk[a.y], rk[a.z], rk[a.w]);
+        if (two) l4[i + stride] = make_uint4(rk[b.x], rk[b.y], rk[b.z], rk[b.w]);
+    }
+    for (int64_t i = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
         labels[i] = rk[labels[i]];
 }
 
@@ -560,7 +569,8 @@ void relabel(uint32_t* d_labels, int64_t n, const std::vector<uint32_t>& rank_of
     DArr<uint32_t> rk(k, st);
     rk.upload(rank_of.data(), k);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, kSMs * 8));
-    if ((size_t)k * 4 <= 48 * 1024)
+    JB_PROF("relabel", st);
+    if ((size_t)k * 4 <= 48 * 1024 && ((uintptr_t)d_labels & 15) == 0)
         k_relabel<<<grid, 256, k * 4, st>>>(d_labels, n, rk.p, k);
     else
         k_relabel_global<<<grid, 256, 0, st>>>(d_labels, n, rk.p);
