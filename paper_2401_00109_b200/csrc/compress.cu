@@ -95,21 +95,6 @@ __device__ __forceinline__ bool fbit(const uint32_t* __restrict__ fb, int64_t ch
     return (fb[ch * W + (rel >> 5)] >> (rel & 31)) & 1u;
 }
 
-// Correctly rounded quotient a / b (b a positive integer-valued double,
-// ry = RN(1 / b)) by FMA corrections: q0 = RN(a ry), then twice
-// q <- RN(q + RN(a - b q) ry), the remainder a - b q being exact under an
-// FMA. After the first correction q is faithful, and Markstein's theorem
-// makes the second one RN(a / b): the IEEE quotient the reference computes,
-// in 5 fp64 operations instead of the division sequence. Valid for
-// 2^-900 <= |a| <= 2^1000 (no underflow or overflow of the remainder);
-// callers fall back to the division outside that range.
-// tests/test_div_identity.py checks the identity against a / b.
-__device__ __forceinline__ double div_cr(double a, double b, double ry) {
-    const double q0 = __dmul_rn(a, ry);
-    const double q1 = __fma_rn(__fma_rn(-q0, b, a), ry, q0);
-    return __fma_rn(__fma_rn(-q1, b, a), ry, q1);
-}
-
 constexpr int kRcp = 256;  // k_spec reciprocal tables cover d <= kRcp
 
 // Phase 1: speculative parse of every chunk from its first start position,

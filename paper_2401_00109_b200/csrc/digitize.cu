@@ -223,6 +223,7 @@ PtsView points_view(const Pieces& pc, const Scaled& sc) {
     v.scl = sc.scl;
     v.sl = sc.sigma_len;
     v.si = sc.sigma_inc;
+    v.rsi = div_by_recip(sc.sigma_inc);
     return v;
 }
 
@@ -320,7 +321,7 @@ __global__ void __launch_bounds__(AS_TB) k_assign_stats(
             for (int u = 0; u < AS_U; ++u) {
                 const int32_t l = ll[u];
                 pp[u] = make_double2(l >= 0 && l < kXRow ? s_xrow[l] : pv.scl * (double)l / pv.sl,
-                                     pp[u].y / pv.si);
+                                     div_by(pp[u].y, pv.si, pv.rsi));
             }
         }
 #pragma unroll
@@ -677,6 +678,7 @@ void symbolize_pieces(const int32_t* d_len, const double* d_inc, int64_t n,
     pv.scl = scaling[0];
     pv.sl = scaling[1];
     pv.si = scaling[2];
+    pv.rsi = div_by_recip(pv.si);
     DArr<unsigned long long> mm(4, st);
     const unsigned long long init[4] = {~0ULL, 0ULL, ~0ULL, 0ULL};
     mm.upload(init, 4);

@@ -71,6 +71,34 @@ __host__ __device__ inline int fx_exponent_for(double max_abs_sum) {
     return E;
 }
 
+// Correctly rounded quotient a / b from ry = RN(1 / b) by FMA corrections:
+// q0 = RN(a ry), then twice q <- RN(q + RN(a - b q) ry); the remainder of a
+// faithful quotient is exact under an FMA, the first correction makes q
+// faithful and Markstein's theorem makes the second one RN(a / b) -- the
+// IEEE quotient -- in 5 fp64 operations instead of the division sequence
+// (whose slow-path branch also diverges warps). Needs no underflow or
+// overflow on the way: 2^-900 <= |a| <= 2^900 and 2^-50 <= b <= 2^50 (the
+// caller checks b once and passes ry = 0 outside that range).
+// tests/test_div_identity.py checks the identity against a / b.
+__device__ __forceinline__ double div_cr(double a, double b, double ry) {
+    const double q0 = __dmul_rn(a, ry);
+    const double q1 = __fma_rn(__fma_rn(-q0, b, a), ry, q0);
+    return __fma_rn(__fma_rn(-q1, b, a), ry, q1);
+}
+
+// a / b (IEEE, round to nearest) for a divisor b > 0 with ry = RN(1/b), or
+// ry = 0 when b is outside div_cr's range
+__device__ __forceinline__ double div_by(double a, double b, double ry) {
+    if (ry == 0.0) return a / b;
+    const double aa = fabs(a);
+    if (aa == 0.0) return a;  // +-0 / b (b > 0 here) keeps the zero's sign
+    return (aa >= 0x1p-900 && aa <= 0x1p900) ? div_cr(a, b, ry) : a / b;
+}
+
+__host__ inline double div_by_recip(double b) {  // ry for div_by
+    return (b >= 0x1p-50 && b <= 0x1p50) ? 1.0 / b : 0.0;
+}
+
 // |x| * 2^E truncated to an integer, with x's sign.
 __host__ __device__ __forceinline__ i128 fx_from_double(double x, int E) {
 #ifdef __CUDA_ARCH__

@@ -184,9 +184,14 @@ struct PtsView {
     const int32_t* len = nullptr;
     const double* inc = nullptr;
     double scl = 1.0, sl = 1.0, si = 1.0;
+    double rsi = 0.0;  // div_by_recip(si): y = inc / si by div_by on device
     __host__ __device__ __forceinline__ double2 at(uint64_t i) const {
         if (pts) return pts[i];
+#ifdef __CUDA_ARCH__
+        return make_double2(scl * (double)len[i] / sl, div_by(inc[i], si, rsi));
+#else
         return make_double2(scl * (double)len[i] / sl, inc[i] / si);
+#endif
     }
 };
 

@@ -518,7 +518,7 @@ __global__ void k_rowkey_jorder(const PtsView pv, const uint64_t* __restrict__ i
         const bool first = r == 0 || oj[r - 1] != j;
         const uint64_t src = first ? (uint64_t)j : idx[i];
         const int32_t l = pv.len[src];
-        const double y = pv.inc[src] / pv.si;  // pv.at's y
+        const double y = div_by(pv.inc[src], pv.si, pv.rsi);  // pv.at's y
         rec[r] = SRec{y, l, i};
         const uint32_t qy = (uint32_t)fmin(fmax((y - y0) * sy, 0.0), qmax);
         keys[r] = (min((uint32_t)l, lcap) << qbits) | qy;

@@ -1,8 +1,11 @@
-"""The FMA-corrected quotient k_spec uses for the reference's divisions
-(compress.cu div_cr: yy / (d*d) and 2y / d of compression.hpp:52) equals the
+"""The FMA-corrected quotient (jb_common.cuh div_cr) that replaces the
+reference's divisions on the hot path -- yy / (d*d) and 2y / d of the
+compression test (compression.hpp:52, k_spec) and y = inc / sigma_inc of
+scale_pieces (digitization.hpp:50, PtsView / k_assign_stats) -- equals the
 IEEE quotient: checked in C (gcc, libm fma, no contraction) on random
-numerators over the guarded range 2^-900..2^1000, near-multiples of b, and
-integers, for every d <= 256 with b = d and b = d^2."""
+numerators over the guarded range, near-multiples of b, and integers, for
+every d <= 256 with b = d and b = d^2, and for random divisors in
+[2^-50, 2^50] (including all-ones significands)."""
 import os
 import shutil
 import subprocess
@@ -41,6 +44,23 @@ int main(int argc, char** argv) {
                 if (memcmp(&want, &got, 8)) ++bad;
             }
         }
+    for (long t = 0; t < per / 10; ++t) {  /* general divisors (sigma_inc) */
+        double b = ldexp(1.0 + (double)(xr() >> 11) * 0x1p-53, (int)(xr() % 100) - 50);
+        if (t % 7 == 0) b = nextafter(ldexp(1.0, (int)(xr() % 40) - 20), 0.0);
+        const double ry = 1.0 / b;
+        for (int k = 0; k < 1000; ++k) {
+            const int e = (int)(xr() % 1800) - 900;
+            double a = ldexp(1.0 + (double)(xr() >> 11) * 0x1p-53, e);
+            if (xr() & 1) a = -a;
+            if (k % 3 == 1) {
+                a = ldexp(1.0 + (double)(xr() >> 11) * 0x1p-53, e % 100) * b;
+                if (k & 4) a = nextafter(a, 0.0);
+            }
+            const double want = a / b, got = div_cr(a, b, ry);
+            ++n;
+            if (memcmp(&want, &got, 8)) ++bad;
+        }
+    }
     printf("%ld %ld\n", n, bad);
     return 0;
 }
@@ -56,5 +76,5 @@ def test_fma_quotient_equals_ieee_division():
         subprocess.run(["gcc", "-O2", "-ffp-contract=off", "-o", exe, c, "-lm"], check=True)
         out = subprocess.run([exe, "40000"], capture_output=True, text=True, check=True).stdout
         n, bad = map(int, out.split())
-        assert n == 256 * 2 * 40000
+        assert n == 256 * 2 * 40000 + 4000 * 1000
         assert bad == 0
