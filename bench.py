@@ -147,9 +147,9 @@ def algorithmic_work(name, launches, info):
     if name == "assign_stats":       # final assign + group stats: len 4 B + inc 8 B in (points
         return "hbm", launches * 16.0 * N  # are virtual), label 4 B out
     if name == "d2_update":          # points of the tiles not culled: 16 B point + 8 B d2 read
-        # + 8 B d2 write; the cull reads 40 B (box + max d2) per tile per round
+        # + 8 B d2 write; the cull reads 20 B (fp32 box + max d2) per tile per round
         ntiles = (S + 127) // 128
-        return "hbm", 32.0 * 128 * info.get("d2_tiles", 0) + 40.0 * ntiles * max(k - 1, 0)
+        return "hbm", 32.0 * 128 * info.get("d2_tiles", 0) + 20.0 * ntiles * max(k - 1, 0)
     if name == "compress_spec":      # 23 flops per candidate test, T ~ 1.89 n (cfg4)
         return "fp64", 23.0 * info.get("tests", 1.89 * n)
     if name == "inverse_fused":      # label 4 B per piece in, 8 B per reconstructed sample out

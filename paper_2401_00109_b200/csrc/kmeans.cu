@@ -674,7 +674,20 @@ __global__ void k_pick_first(const uint64_t* __restrict__ raw, uint64_t n, SeedS
 // of its box can come closer to the new center than the tile's current max
 // d2; every other tile keeps all its d2 (the rounded distances of its points
 // are all > max d2 >= d2, so std::min leaves them unchanged).
-__global__ void k_d2_cull(const double4* __restrict__ tbox, const double* __restrict__ tmax,
+// tile boxes for the D^2 cull in fp32, rounded outward (a superset box): the
+// cull reads 20 B per tile instead of 40; with tmax rounded up, the test can
+// only keep more tiles, never skip one the exact test keeps
+__global__ void k_cull_boxes(const double4* __restrict__ tbox, int64_t ntiles,
+                             float4* __restrict__ cbox) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntiles;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const double4 b = tbox[t];
+        cbox[t] = make_float4(__double2float_rd(b.x), __double2float_ru(b.y),
+                              __double2float_rd(b.z), __double2float_ru(b.w));
+    }
+}
+
+__global__ void k_d2_cull(const float4* __restrict__ cbox, const float* __restrict__ tmax,
                           int64_t ntiles, const double2* __restrict__ spts,
                           const uint32_t* __restrict__ pos, const SeedState* __restrict__ ss,
                           uint32_t* __restrict__ work, unsigned long long* __restrict__ nwork,
@@ -686,9 +699,10 @@ __global__ void k_d2_cull(const double4* __restrict__ tbox, const double* __rest
          t += (int64_t)gridDim.x * blockDim.x) {
         bool need = false;
         if (t < ntiles) {
+            const float4 f = cbox[t];
             double dmin2, dmax2;
-            box_d2(c.x, c.y, tbox[t], dmin2, dmax2);
-            need = !(dmin2 * (1.0 - kKeepMargin) > tmax[t]);
+            box_d2(c.x, c.y, make_double4(f.x, f.y, f.z, f.w), dmin2, dmax2);
+            need = !(dmin2 * (1.0 - kKeepMargin) > (double)tmax[t]);
         }
         // one atomic per warp (a per-tile atomic on one counter serialises)
         const unsigned m = __ballot_sync(0xffffffffu, need);
@@ -705,7 +719,7 @@ __global__ void k_d2_cull(const double4* __restrict__ tbox, const double* __rest
 __global__ void __launch_bounds__(256) k_d2_tiles(
     const double2* __restrict__ spts, const uint32_t* __restrict__ orig,
     const uint32_t* __restrict__ pos, int64_t n, const uint32_t* __restrict__ work,
-    const unsigned long long* __restrict__ nwork, double* __restrict__ tmax,
+    const unsigned long long* __restrict__ nwork, float* __restrict__ tmax,
     double* __restrict__ d2s, const SeedState* __restrict__ ss, int init, int E,
     unsigned long long* __restrict__ part, const double2* __restrict__ cur,
     const uint32_t* __restrict__ gkey, unsigned long long* __restrict__ diag) {
@@ -756,7 +770,7 @@ __global__ void __launch_bounds__(256) k_d2_tiles(
             mx = fmax(mx, v);
         }
         for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-        if (lane == 0) tmax[t] = mx;
+        if (lane == 0) tmax[t] = __double2float_ru(mx);  // an upper bound for the cull
     }
 }
 
@@ -2065,10 +2079,12 @@ void lloyd_best_device(const PtsView& pv, const uint64_t* d_idx, int64_t n, uint
     JB_TRACE("kmeans: morton order", st);
     const int64_t ntiles = (n + TILE - 1) / TILE;
     DArr<double4> tbox(ntiles, st);
-    DArr<double> tmax(ntiles, st);
+    DArr<float> tmax(ntiles, st);  // per-tile max d2, rounded up (D^2 cull)
     const int tile_grid = (int)std::max<int64_t>(1, std::min<int64_t>((ntiles + 7) / 8, kSMs * 8));
     k_tile_boxes<<<tile_grid, 256, 0, st>>>(spts.p, n, tbox.p, rows.len ? slen.p : nullptr,
                                             tlen.p);
+    DArr<float4> cbox(ntiles, st);
+    k_cull_boxes<<<grid_cap(ntiles), 256, 0, st>>>(tbox.p, ntiles, cbox.p);
     JB_LAUNCH_CHECK();
 
     LloydCtx L;
@@ -2180,7 +2196,7 @@ void lloyd_best_device(const PtsView& pv, const uint64_t* d_idx, int64_t n, uint
             if (c + 1 < k) {
                 JB_PROF("d2_update", st);
                 JB_CUDA(cudaMemsetAsync(d2_nwork.p, 0, 8, st));
-                k_d2_cull<<<cull_grid, 256, 0, st>>>(tbox.p, tmax.p, ntiles, spts.p, pos.p, ss.p,
+                k_d2_cull<<<cull_grid, 256, 0, st>>>(cbox.p, tmax.p, ntiles, spts.p, pos.p, ss.p,
                                                      d2_work.p, d2_nwork.p, nullptr);
                 k_d2_tiles<<<tile_grid, 256, 0, st>>>(spts.p, orig.p, pos.p, n, d2_work.p,
                                                       d2_nwork.p, tmax.p, d2s.p, ss.p, 0, Ed2,
@@ -2751,11 +2767,13 @@ void lloyd_best_dist(const Comm& cm, const PtsView& pv, const uint64_t* d_lidx,
     }
     const int64_t ntiles = (n + TILE - 1) / TILE;
     DArr<double4> tbox(std::max<int64_t>(ntiles, 1), st);
-    DArr<double> tmax(std::max<int64_t>(ntiles, 1), st);
+    DArr<float> tmax(std::max<int64_t>(ntiles, 1), st);  // per-tile max d2, rounded up
     const int tile_grid = (int)std::max<int64_t>(1, std::min<int64_t>((ntiles + 7) / 8, kSMs * 8));
     if (n > 0)
         k_tile_boxes<<<tile_grid, 256, 0, st>>>(spts.p, n, tbox.p, rows.len ? slen.p : nullptr,
                                                 tlen.p);
+    DArr<float4> cbox(std::max<int64_t>(ntiles, 1), st);
+    if (n > 0) k_cull_boxes<<<grid_cap(ntiles), 256, 0, st>>>(tbox.p, ntiles, cbox.p);
     JB_LAUNCH_CHECK();
 
     LloydCtx L;
@@ -3067,7 +3085,7 @@ void lloyd_best_dist(const Comm& cm, const PtsView& pv, const uint64_t* d_lidx,
                     cur.upload(&hc, 1);
                     JB_PROF("d2_update", st);
                     JB_CUDA(cudaMemsetAsync(d2_nwork.p, 0, 8, st));
-                    k_d2_cull<<<cull_grid, 256, 0, st>>>(tbox.p, tmax.p, ntiles, spts.p, pos.p, ss.p,
+                    k_d2_cull<<<cull_grid, 256, 0, st>>>(cbox.p, tmax.p, ntiles, spts.p, pos.p, ss.p,
                                                          d2_work.p, d2_nwork.p, cur.p);
                     k_d2_tiles<<<tile_grid, 256, 0, st>>>(spts.p, orig.p, pos.p, n, d2_work.p,
                                                           d2_nwork.p, tmax.p, d2s.p, ss.p, 0, Ed2,
@@ -3136,7 +3154,7 @@ void lloyd_best_dist(const Comm& cm, const PtsView& pv, const uint64_t* d_lidx,
             if (c + 1 < k && n > 0) {
                 JB_PROF("d2_update", st);
                 JB_CUDA(cudaMemsetAsync(d2_nwork.p, 0, 8, st));
-                k_d2_cull<<<cull_grid, 256, 0, st>>>(tbox.p, tmax.p, ntiles, spts.p, pos.p, ss.p,
+                k_d2_cull<<<cull_grid, 256, 0, st>>>(cbox.p, tmax.p, ntiles, spts.p, pos.p, ss.p,
                                                      d2_work.p, d2_nwork.p, curp);
                 k_d2_tiles<<<tile_grid, 256, 0, st>>>(spts.p, orig.p, pos.p, n, d2_work.p,
                                                       d2_nwork.p, tmax.p, d2s.p, ss.p, 0, Ed2,
