@@ -292,6 +292,8 @@ __global__ void k_count(ChunkGeom g, int64_t n_chunks, const uint32_t* __restric
     }
 }
 
+constexpr int kEmitW = 8;  // flag words per chunk at most (C <= 256)
+
 // Phase 4b: emit (len, inc) pieces in input order, one warp per chunk, a
 // lane per sample position of each 32-bit flag word: a flagged lane's piece
 // ends at the next set bit (this word, a later word, or the chunk's true exit
@@ -312,9 +314,20 @@ __global__ void k_emit(const double* __restrict__ v, ChunkGeom g, int64_t n_chun
         int64_t s, c, lo, hi, last;
         chunk_bounds(g, ch, s, c, lo, hi, last);
         const uint32_t mine = lane < W ? fb[ch * W + lane] : 0u;  // all words of the chunk
+        // the chunk's samples, one per (word, lane), all loads in flight at
+        // once: v[p] is a register and v[e] a shuffle when e lies in the same
+        // or the next word (a load otherwise: pieces longer than a word)
+        double vr[kEmitW];
+#pragma unroll
+        for (int w = 0; w < kEmitW; ++w) {
+            const int64_t q = lo + 32 * w + lane;
+            vr[w] = (w < W && q <= last) ? __ldg(v + q) : 0.0;
+        }
         const int64_t Ech = E[ch];
         int64_t j = base[ch];
-        for (int w = 0; w < W; ++w) {
+#pragma unroll
+        for (int w = 0; w < kEmitW; ++w) {
+            if (w >= W) break;
             const uint32_t m = __shfl_sync(0xffffffffu, mine, w);
             if (!m) continue;
             // next start after this word: first set bit of a later word
@@ -327,11 +340,16 @@ __global__ void k_emit(const double* __restrict__ v, ChunkGeom g, int64_t n_chun
                 nxt = lo + 32 * wl + (__ffs(mw) - 1);
             }
             const bool f = (m >> lane) & 1u;
+            const int64_t p = lo + 32 * w + lane;
+            const uint32_t above = lane < 31 ? (m >> (lane + 1)) : 0u;
+            const int64_t e = above ? p + __ffs(above) : nxt;
+            const int64_t re = e - lo - 32 * w;  // e relative to this word
+            const double e0 = __shfl_sync(0xffffffffu, vr[w], (int)(re & 31));
+            const double e1 = w + 1 < kEmitW ? __shfl_sync(0xffffffffu, vr[(w + 1) % kEmitW], (int)(re & 31))
+                                             : 0.0;
             if (f) {
-                const int64_t p = lo + 32 * w + lane;
-                const uint32_t above = lane < 31 ? (m >> (lane + 1)) : 0u;
-                const int64_t e = above ? p + __ffs(above) : nxt;
-                const double inc = v[e] - v[p];
+                const double ve = re < 32 ? e0 : (re < 64 && w + 1 < W ? e1 : __ldg(v + e));
+                const double inc = ve - vr[w];
                 const int64_t k = j + __popc(m & ((1u << lane) - 1u));
                 out_len[k] = (int32_t)(e - p);
                 out_inc[k] = inc;
