@@ -54,12 +54,22 @@ __global__ void k_sum_inc(const double* __restrict__ inc, int64_t n, int E,
                           unsigned long long* __restrict__ acc, unsigned long long* __restrict__ mm) {
     i128 s = 0;
     unsigned long long imn = ~0ULL, imx = 0;
-    for (int64_t i = blockIdx.x * (int64_t)kTB + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * kTB) {
-        const double v = inc[i];
-        s += fx_from_double(v, E);
-        imn = min(imn, ord_bits(v));
-        imx = max(imx, ord_bits(v));
+    constexpr int U = 4;  // independent loads in flight per thread
+    for (int64_t b = blockIdx.x * (int64_t)kTB * U + threadIdx.x; b < n;
+         b += (int64_t)gridDim.x * kTB * U) {
+        double V[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = b + (int64_t)u * kTB;
+            V[u] = i < n ? inc[i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (b + (int64_t)u * kTB >= n) break;
+            s += fx_from_double(V[u], E);
+            imn = min(imn, ord_bits(V[u]));
+            imx = max(imx, ord_bits(V[u]));
+        }
     }
     for (int o = 16; o > 0; o >>= 1) {
         imn = min(imn, __shfl_xor_sync(0xffffffffu, imn, o));

@@ -151,35 +151,47 @@ __device__ __forceinline__ uint32_t row_pick(uint64_t w, const CandGrid& g, doub
     return grid_nearest(g, px, py, cx, cy, k);
 }
 
+// the row-cell word of a piece of length len at y = py (~0: no row cell,
+// which row_nearest_w sends to the 2-D grid fallback)
+__device__ __forceinline__ uint64_t row_cell_word(const RowGrid& rg, int32_t len, double py) {
+    if (len < 1 || len > rg.R) return ~0ull;
+    int iy = (int)((py - rg.y0) * rg.invh);
+    iy = min(max(iy, 0), rg.Gy - 1);
+    return __ldg(reinterpret_cast<const unsigned long long*>(rg.cell) + (size_t)(len - 1) * rg.Gy +
+                 iy);
+}
+
+// nearest_center (clustering.hpp:146-157) of a piece at (px, py) whose row
+// cell word w was loaded ahead (row_cell_word)
+__device__ __forceinline__ uint32_t row_nearest_w(const CandGrid& g, uint64_t w, double px,
+                                                  double py, const double* cx, const double* cy,
+                                                  int k) {
+    const uint32_t c0 = (uint32_t)(w & 0xFFFF);
+    if (c0 < kRowOverflow) {
+        uint32_t best = c0;
+        const uint32_t c1 = (uint32_t)((w >> 16) & 0xFFFF);
+        if (c1 == kRowEmpty) return best;  // the only possible argmin
+        double bd = dist2(px, py, cx[c0], cy[c0]);
+#pragma unroll
+        for (int j = 1; j < 4; ++j) {
+            const uint32_t c = (uint32_t)((w >> (16 * j)) & 0xFFFF);
+            if (c == kRowEmpty) break;
+            const double d = dist2(px, py, cx[c], cy[c]);
+            if (d < bd) {
+                bd = d;
+                best = c;
+            }
+        }
+        return best;
+    }
+    return grid_nearest(g, px, py, cx, cy, k);
+}
+
 // nearest_center (clustering.hpp:146-157) of a piece of length len at (px, py)
 __device__ __forceinline__ uint32_t row_nearest(const RowGrid& rg, const CandGrid& g, int32_t len,
                                                 double px, double py, const double* cx,
                                                 const double* cy, int k) {
-    if (len >= 1 && len <= rg.R) {
-        int iy = (int)((py - rg.y0) * rg.invh);
-        iy = min(max(iy, 0), rg.Gy - 1);
-        const uint64_t w = __ldg(reinterpret_cast<const unsigned long long*>(rg.cell) +
-                                 (size_t)(len - 1) * rg.Gy + iy);
-        const uint32_t c0 = (uint32_t)(w & 0xFFFF);
-        if (c0 < kRowOverflow) {
-            uint32_t best = c0;
-            const uint32_t c1 = (uint32_t)((w >> 16) & 0xFFFF);
-            if (c1 == kRowEmpty) return best;  // the only possible argmin
-            double bd = dist2(px, py, cx[c0], cy[c0]);
-#pragma unroll
-            for (int j = 1; j < 4; ++j) {
-                const uint32_t c = (uint32_t)((w >> (16 * j)) & 0xFFFF);
-                if (c == kRowEmpty) break;
-                const double d = dist2(px, py, cx[c], cy[c]);
-                if (d < bd) {
-                    bd = d;
-                    best = c;
-                }
-            }
-            return best;
-        }
-    }
-    return grid_nearest(g, px, py, cx, cy, k);
+    return row_nearest_w(g, row_cell_word(rg, len, py), px, py, cx, cy, k);
 }
 
 }  // namespace jb
