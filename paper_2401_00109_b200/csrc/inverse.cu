@@ -760,17 +760,26 @@ __global__ void __launch_bounds__(FUSED_TB, 3) k_inv_fused(InverseIn in, const d
             const int kq = it % DQ, kv = it % DV;
             FP_WAIT(mb_wait(QF + kq, (it / DQ) & 1));
             FP_WAIT(mb_wait(VF + kv, (it / DV) & 1));
+            // all shared-memory reads of the WP segment pairs first (independent,
+            // in flight together), then the stores, then the queue of longer pieces
+            int qk[WP], pek[WP];
+            double vk[WP];
+#pragma unroll
+            for (int k = 0; k < WP; ++k) {
+                const int L = 2 * wi + (lane >> 4) + 2 * FWW * k;
+                qk[k] = S.q[kq][L * QPS + m];
+                pek[k] = S.pe[kq][L * QPS + m];
+                vk[k] = S.vs[kv][L * VSS + m + 1].x;
+            }
+#pragma unroll
+            for (int k = 0; k < WP; ++k)
+                if (qk[k] > 0 && pek[k] <= wE[k]) wout[k][pek[k]] = vk[k];
             int nq = 0;
 #pragma unroll
             for (int k = 0; k < WP; ++k) {
                 const int L = 2 * wi + (lane >> 4) + 2 * FWW * k;
-                const int q = S.q[kq][L * QPS + m];
-                if (q > 0) {
-                    const int pe = S.pe[kq][L * QPS + m];
-                    if (pe <= wE[k]) wout[k][pe] = S.vs[kv][L * VSS + m + 1].x;
-                }
-                const unsigned mq = __ballot_sync(0xffffffffu, q > 1);
-                if (q > 1) S.wq[wi][nq + __popc(mq & ((1u << lane) - 1u))] = (uint16_t)(L << 4 | m);
+                const unsigned mq = __ballot_sync(0xffffffffu, qk[k] > 1);
+                if (qk[k] > 1) S.wq[wi][nq + __popc(mq & ((1u << lane) - 1u))] = (uint16_t)(L << 4 | m);
                 nq += __popc(mq);
             }
             __syncwarp();
