@@ -809,13 +809,17 @@ __global__ void __launch_bounds__(PICK_TB) k_pick(const uint64_t* __restrict__ r
                                                   int nblocks,
                                                   const unsigned long long* __restrict__ part,
                                                   int E, SeedState* ss,
-                                                  int64_t* __restrict__ chosen, int c) {
+                                                  int64_t* __restrict__ chosen, int c,
+                                                  unsigned long long* __restrict__ nwork_reset) {
     __shared__ unsigned long long s_lo[32], s_hi[32];
     __shared__ unsigned long long s_wt_lo[32], s_wt_hi[32];
     __shared__ int s_found_block;
     __shared__ unsigned long long s_found_elem;
     __shared__ unsigned long long s_before[2];
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    // the next cull's counter (the previous round's k_d2_tiles, which read
+    // it, finished before this launch): no separate memset per round
+    if (t == 0 && nwork_reset) *nwork_reset = 0;
     constexpr int NW = PICK_TB / 32;
     const int R = ((nblocks + NW - 1) / NW + 31) & ~31;  // blocks per warp, multiple of 32
     const int b0 = min(nblocks, w * R), b1 = min(nblocks, b0 + R);
@@ -2190,12 +2194,11 @@ void lloyd_best_device(const PtsView& pv, const uint64_t* d_idx, int64_t n, uint
             {
                 JB_PROF("d2_pick", st);
                 k_pick<<<1, PICK_TB, 0, st>>>(d_raw, d2s.p, pos.p, n, nblocks, part.p, Ed2, ss.p,
-                                              chosen.p, (int)c);
+                                              chosen.p, (int)c, d2_nwork.p);
             }
             JB_LAUNCH_CHECK();
             if (c + 1 < k) {
                 JB_PROF("d2_update", st);
-                JB_CUDA(cudaMemsetAsync(d2_nwork.p, 0, 8, st));
                 k_d2_cull<<<cull_grid, 256, 0, st>>>(cbox.p, tmax.p, ntiles, spts.p, pos.p, ss.p,
                                                      d2_work.p, d2_nwork.p, nullptr);
                 k_d2_tiles<<<tile_grid, 256, 0, st>>>(spts.p, orig.p, pos.p, n, d2_work.p,
