@@ -1847,10 +1847,13 @@ __global__ void __launch_bounds__(256) k_lloyd_persistent(PersistArgs a) {
         if (ts && b < 512) a.tstamp[6 * b] = gtimer();
         if (blockIdx.x == 0)
             means_body(a.acc, a.k, a.Ex, a.Ey, a.centers, a.empties, state, state, a.mov);
+        if (blockIdx.x == 0 && threadIdx.x == 0)  // one word for the other blocks to read
+            state[3] = ((state[0] | state[1]) ? 1 : 0) | (a.mov[1] != 0.0 ? 2 : 0);
         grid.sync();
         if (ts && b < 512) a.tstamp[6 * b + 1] = gtimer();
-        if (((volatile int*)state)[0] | ((volatile int*)state)[1]) break;
-        if (((volatile double*)a.mov)[1] != 0.0) {  // centers moved too far: rebuild
+        const int gate = ((volatile int*)state)[3];  // bit 0: stop, bit 1: rebuild
+        if (gate & 1) break;
+        if (gate & 2) {  // centers moved too far: rebuild
             row_grid_build_body(a.rg, a.centers, a.k, a.rg_blocks, a.rg_nblocks);
             grid.sync();
         }
@@ -2104,7 +2107,7 @@ void lloyd_best_device(const PtsView& pv, const uint64_t* d_idx, int64_t n, uint
     L.labs.alloc(n, st);
     L.acc.alloc(7 * k, st);
     L.flags.alloc(1, st);
-    L.empties.alloc(k + 3, st);  // list | n_empty | converged | iterations
+    L.empties.alloc(k + 4, st);  // list | n_empty | converged | iterations | gate
     L.diag.alloc(4, st);
     L.empties.zero();
     {
@@ -2794,7 +2797,7 @@ void lloyd_best_dist(const Comm& cm, const PtsView& pv, const uint64_t* d_lidx,
     L.dacc.alloc(7 * k + 1, st);  // deltas + change count (changed_ptr)
     L.use_dacc = true;
     L.flags.alloc(1, st);
-    L.empties.alloc(k + 3, st);
+    L.empties.alloc(k + 4, st);
     L.empties.zero();
     L.diag.alloc(4, st);
     {
