@@ -694,22 +694,39 @@ __global__ void k_d2_cull(const float4* __restrict__ cbox, const float* __restri
                           const double2* __restrict__ cur) {
     const double2 c = cur ? *cur : spts[pos[ss->last]];
     const int lane = threadIdx.x & 31;
-    // warp-uniform trip count (t - lane is the warp's first tile)
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t - lane < ntiles;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        bool need = false;
-        if (t < ntiles) {
-            const float4 f = cbox[t];
-            double dmin2, dmax2;
-            box_d2(c.x, c.y, make_double4(f.x, f.y, f.z, f.w), dmin2, dmax2);
-            need = !(dmin2 * (1.0 - kKeepMargin) > (double)tmax[t]);
+    constexpr int U = 4;  // tiles per thread per pass, loads issued together
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    // warp-uniform trip count (t0 - lane is the warp's first tile)
+    for (int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t0 - lane < ntiles;
+         t0 += U * stride) {
+        float4 f[U];
+        float tm[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t t = t0 + u * stride;
+            f[u] = t < ntiles ? cbox[t] : make_float4(0.f, 0.f, 0.f, 0.f);
+            tm[u] = t < ntiles ? tmax[t] : -INFINITY;  // -inf: never needed
         }
-        // one atomic per warp (a per-tile atomic on one counter serialises)
-        const unsigned m = __ballot_sync(0xffffffffu, need);
+        unsigned m[U];
+        int cnt = 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            double dmin2, dmax2;
+            box_d2(c.x, c.y, make_double4(f[u].x, f[u].y, f[u].z, f[u].w), dmin2, dmax2);
+            m[u] = __ballot_sync(0xffffffffu, !(dmin2 * (1.0 - kKeepMargin) > (double)tm[u]));
+            cnt += __popc(m[u]);
+        }
+        if (!cnt) continue;  // warp-uniform
+        // one atomic per warp and pass (a per-tile atomic on one counter serialises)
         unsigned long long base = 0;
-        if (lane == 0 && m) base = atomicAdd(nwork, (unsigned long long)__popc(m));
+        if (lane == 0) base = atomicAdd(nwork, (unsigned long long)cnt);
         base = __shfl_sync(0xffffffffu, base, 0);
-        if (need) work[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)t;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if ((m[u] >> lane) & 1u)
+                work[base + __popc(m[u] & ((1u << lane) - 1u))] = (uint32_t)(t0 + u * stride);
+            base += __popc(m[u]);
+        }
     }
 }
 
@@ -2170,7 +2187,7 @@ void lloyd_best_device(const PtsView& pv, const uint64_t* d_idx, int64_t n, uint
     DArr<uint32_t> d2_work(ntiles, st);
     DArr<unsigned long long> d2_nwork(1, st);
     const int cull_grid =
-        (int)std::max<int64_t>(1, std::min<int64_t>((ntiles + 255) / 256, kSMs * 16));
+        (int)std::max<int64_t>(1, std::min<int64_t>((ntiles + 1023) / 1024, kSMs * 8));
     DArr<double> d2s(n, st);
     DArr<unsigned long long> part(2 * nblocks, st);
     DArr<SeedState> ss(1, st);
@@ -2857,7 +2874,7 @@ void lloyd_best_dist(const Comm& cm, const PtsView& pv, const uint64_t* d_lidx,
     DArr<uint32_t> d2_work(std::max<int64_t>(ntiles, 1), st);
     DArr<unsigned long long> d2_nwork(1, st);
     const int cull_grid =
-        (int)std::max<int64_t>(1, std::min<int64_t>((ntiles + 255) / 256, kSMs * 16));
+        (int)std::max<int64_t>(1, std::min<int64_t>((ntiles + 1023) / 1024, kSMs * 8));
     DArr<double> d2s(nn, st);
     DArr<unsigned long long> part(2 * nblocks, st);
     DArr<SeedState> ss(1, st);
