@@ -424,6 +424,37 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
         d_values = dvals.p;
     }
 
+    // svq on one GPU: the engine draws and the sample (sampling_kmeans
+    // clustering.hpp:251-262) depend only on N and the seed, so they run on
+    // a side stream: the draws from the start of the fit (a bound on their
+    // count, S <= r * steps, is known before compression: the stream is the
+    // same prefix for any count), the sample from a helper thread while
+    // scale_pieces runs here; the backend joins them (and rethrows their
+    // error after scale's own).
+    struct SvqPre {
+        DArr<uint64_t> raw, sample;
+        SampleOrder jorder;
+        uint64_t S = 0, raw_count = 0, cursor = 0;
+        std::exception_ptr err;
+        std::thread th;
+        ~SvqPre() {
+            if (th.joinable()) th.join();
+        }
+    } pre;
+    const bool svq_side = c.backend == JB_BACKEND_SVQ && !cm.dist();
+    if (svq_side) {
+        if (!ctx->side) {
+            JB_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+            JB_CUDA(cudaEventCreateWithFlags(&ctx->side_done, cudaEventDisableTiming));
+        }
+        if (c.r > 0.0 && c.r <= 1.0 && c.k >= 1 && c.n_init >= 1 && c.n_init < 1000000 &&
+            c.k < (1ULL << 40)) {  // the helper validates again and reports errors in order
+            pre.raw_count = (uint64_t)std::llround(c.r * (double)seg.total_steps) +
+                            (c.k + 1) * c.n_init + 4096;
+            mt19937_64_generate(c.seed, pre.raw_count, pre.raw, ctx->side);
+        }
+    }
+
     // ---- compression (local segments) ----
     JB_TRACE("fit: values on device", st);
     compress_segments(d_values, seg, c.tol, c.max_piece_len, fit->pieces, st, &fit->fix_rounds);
@@ -455,25 +486,7 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
     }
     fit->piece_base = base;
 
-    // svq on one GPU: the engine draws and the sample (sampling_kmeans
-    // clustering.hpp:251-262) depend only on N and the seed, so they run on
-    // a side stream from a helper thread while scale_pieces runs here; the
-    // backend joins them (and rethrows their error after scale's own).
-    struct SvqPre {
-        DArr<uint64_t> raw, sample;
-        SampleOrder jorder;
-        uint64_t S = 0, raw_count = 0, cursor = 0;
-        std::exception_ptr err;
-        std::thread th;
-        ~SvqPre() {
-            if (th.joinable()) th.join();
-        }
-    } pre;
-    if (c.backend == JB_BACKEND_SVQ && !cm.dist()) {
-        if (!ctx->side) {
-            JB_CUDA(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
-            JB_CUDA(cudaEventCreateWithFlags(&ctx->side_done, cudaEventDisableTiming));
-        }
+    if (svq_side) {
         const int dev = ctx->device;
         cudaStream_t s2 = ctx->side;
         cudaEvent_t ev = ctx->side_done;
@@ -487,8 +500,11 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
                     throw Error(INVALID_INPUT, "sampling_kmeans: sample of " + std::to_string(pre.S) +
                                                    " points is smaller than k=" +
                                                    std::to_string(c.k) + " (increase r)");
-                pre.raw_count = pre.S + (c.k + 1) * c.n_init + 4096;
-                mt19937_64_generate(c.seed, pre.raw_count, pre.raw, s2);
+                const uint64_t need = pre.S + (c.k + 1) * c.n_init + 4096;
+                if (pre.raw.p == nullptr || pre.raw_count < need) {  // no early draws
+                    pre.raw_count = need;
+                    mt19937_64_generate(c.seed, pre.raw_count, pre.raw, s2);
+                }
                 pre.cursor = sample_indices_device((uint64_t)Ng, pre.S, pre.raw.p, pre.raw_count,
                                                    pre.sample, s2, &pre.jorder);
                 JB_CUDA(cudaEventRecord(ev, s2));
