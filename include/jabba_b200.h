@@ -221,6 +221,14 @@ jb_status jb_mt19937_64_stream(jb_context* ctx, uint64_t seed, uint64_t count, u
 jb_status jb_sample_indices(jb_context* ctx, uint64_t n, uint64_t sample_size, uint64_t seed,
                             uint64_t* out);
 
+/* The reference's left-to-right fp64 accumulation `s += w` from s = 0 of
+ * non-negative terms (scale_pieces var_len digitization.hpp:39-45, group sums
+ * :224-231), reproduced bit-exactly by the parallel emulation the fit uses
+ * (seqsum.cu): out[g] = sequential sum of terms[seg_off[g] .. seg_off[g+1]).
+ * Terms must be >= 0 (the result is exact for any finite non-negative input). */
+jb_status jb_seq_sum_nonneg(jb_context* ctx, const double* terms, const int64_t* seg_off,
+                            int64_t n_seg, double* out);
+
 /* symbol token of cluster rank r in an alphabet of size k (core.hpp:186-193);
  * writes a NUL-terminated string into buf (>= 24 bytes); returns its length */
 int32_t jb_symbol_token(uint64_t rank, uint64_t alphabet_size, char* buf);

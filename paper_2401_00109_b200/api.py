@@ -469,6 +469,16 @@ class Engine:
         _check(N.lib().jb_sample_indices(self.ctx, n, sample_size, seed, out.ctypes.data))
         return out[:sample_size]
 
+    def seq_sum_nonneg(self, terms, seg_off=None) -> np.ndarray:
+        """The reference's sequential ``s += w`` over non-negative terms
+        (digitization.hpp:39-45, 224-231), per segment, bit-exact on device."""
+        w = np.ascontiguousarray(terms, np.float64)
+        off = np.ascontiguousarray([0, len(w)] if seg_off is None else seg_off, np.int64)
+        out = np.zeros(max(len(off) - 1, 1), np.float64)
+        _check(N.lib().jb_seq_sum_nonneg(self.ctx, w.ctypes.data, off.ctypes.data, len(off) - 1,
+                                         out.ctypes.data))
+        return out[: len(off) - 1]
+
     def inverse_arrays(self, centers, mean_lengths, scaling, labels, piece_offsets, anchors,
                        source_lengths, layout: int) -> np.ndarray:
         sl = np.ascontiguousarray(source_lengths, np.int64)

@@ -704,6 +704,13 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
     GroupStats gs;
     assign_and_stats(pv, fit->pieces.len.p, N, backend_centers, k, bb, assign_needed,
                      labels.p, gs, st, sc.max_len_global, sc.scl, sc.sigma_len, &cm, base);
+    // the x sums bit-exact as the reference accumulates them: then the
+    // codebook's x and every reconstructed length match (inverse.hpp:46,63-74)
+    if (k > 0) {
+        const std::vector<double> sx = exact_group_sum_x(fit->pieces.len.p, labels.p, N, k, sc.scl,
+                                                         sc.sigma_len, st, &cm);
+        for (uint64_t g = 0; g < k; ++g) gs.sum_x[g] = sx[g];
+    }
     std::vector<double> centers(2 * k), mean_lengths(k);
     bool need_sample_stats = false;
     for (uint64_t g = 0; g < k; ++g) need_sample_stats |= gs.counts[g] == 0;
@@ -1179,6 +1186,26 @@ jb_status jb_sample_indices(jb_context* ctx, uint64_t n, uint64_t sample_size, u
         sample_indices_device(n, sample_size, raw.p, raw_count, idx, ctx->stream);
         idx.download(out, sample_size);
         JB_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+jb_status jb_seq_sum_nonneg(jb_context* ctx, const double* terms, const int64_t* seg_off,
+                            int64_t n_seg, double* out) {
+    return (jb_status)guarded([&] {
+        JB_CUDA(cudaSetDevice(ctx->device));
+        if (n_seg < 0) throw Error(INVALID_INPUT, "negative segment count");
+        std::vector<int64_t> off(seg_off, seg_off + n_seg + 1);
+        for (int64_t g = 0; g < n_seg; ++g)
+            if (off[g + 1] < off[g] || off[0] < 0)
+                throw Error(INVALID_INPUT, "segment offsets must be non-decreasing");
+        const int64_t n = n_seg > 0 ? off[n_seg] : 0;
+        DArr<double> w(std::max<int64_t>(n, 1), ctx->stream);
+        w.upload(terms, n);
+        SeqTerms t;
+        t.kind = SeqTerms::DIRECT;
+        t.w = w.p;
+        const std::vector<double> r = seq_sum_nonneg(t, off, ctx->stream);
+        std::copy(r.begin(), r.end(), out);
     });
 }
 

@@ -184,7 +184,7 @@ void scale_pieces(const Pieces& pc, int64_t total_steps, double scl, Scaled& out
     const int Ei = fx_exponent_for(dimax * dimax * n * 1.001 + 1e-300);
     acc.zero();
     if (pc.N > 0) {
-        JB_PROF("scale_sum_var", st);
+        JB_PROF("scale_sum_var", st);  // var_inc (var_len: exact sequential below)
         k_sum_var<<<grid_for(pc.N), kTB, 0, st>>>(pc.len.p, pc.inc.p, pc.N, mean_len, mean_inc, El,
                                                  Ei, acc.p);
     }
@@ -192,7 +192,14 @@ void scale_pieces(const Pieces& pc, int64_t total_steps, double scl, Scaled& out
     h = acc.to_host(4);
     h = C.sum_i128(h);
     JB_TRACE("scale: variances", st);
-    const double var_len = fx_to_double(fx_load(h.data()), El);
+    // var_len: the reference's left-to-right sum of (len - mean_len)^2,
+    // bit-exact (seqsum.cu); sigma_len then fixes every x = scl*len/sigma_len
+    // and every reconstructed length (inverse.hpp:46)
+    SeqTerms vt;
+    vt.len = pc.len.p;
+    vt.kind = SeqTerms::VAR_LEN;
+    vt.a = mean_len;
+    const double var_len = seq_sum_nonneg(vt, {0, pc.N}, st, cm)[0];
     const double var_inc = fx_to_double(fx_load(h.data() + 2), Ei);
     double sl = N > 1 ? std::sqrt(var_len / (n - 1.0)) : 0.0;
     double si = N > 1 ? std::sqrt(var_inc / (n - 1.0)) : 0.0;
@@ -572,6 +579,56 @@ void assign_and_stats(const PtsView& pv, const int32_t* d_len, int64_t n,
         gs.sum_x[c] = fx_to_double((i128)(((u128)rec[7 * c + 4] << 64) | rec[7 * c + 3]), Ex);
         gs.sum_y[c] = fx_to_double((i128)(((u128)rec[7 * c + 6] << 64) | rec[7 * c + 5]), Ey);
     }
+}
+
+namespace {
+// first position of each key in a sorted key array (k + 1 offsets)
+__global__ void k_key_offsets(const uint32_t* __restrict__ keys, int64_t n, int64_t k,
+                              int64_t* __restrict__ off) {
+    const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (g > k) return;
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((int64_t)keys[mid] < g) lo = mid + 1;
+        else hi = mid;
+    }
+    off[g] = lo;
+}
+}  // namespace
+
+std::vector<double> exact_group_sum_x(const int32_t* d_len, const uint32_t* d_labels, int64_t n,
+                                      uint64_t k, double scl, double sigma_len, cudaStream_t st,
+                                      const Comm* cm) {
+    // the pieces of each group in index order: a stable sort of the lengths
+    // by label, then the groups' sequential sums (digitization.hpp:224-231)
+    std::vector<int64_t> off(k + 1, 0);
+    DArr<int32_t> slen(std::max<int64_t>(n, 1), st);
+    if (n > 0) {
+        DArr<uint32_t> skey(n, st);
+        int bits = 1;
+        while (bits < 32 && (1ULL << bits) < k) ++bits;
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, d_labels, skey.p, d_len, slen.p, n, 0, bits, st);
+        DArr<uint8_t> tmp(std::max<size_t>(tb, 1), st);
+        {
+            JB_PROF("group_sort", st);
+            cub::DeviceRadixSort::SortPairs(tmp.p, tb, d_labels, skey.p, d_len, slen.p, n, 0, bits,
+                                            st);
+        }
+        JB_LAUNCH_CHECK();
+        DArr<int64_t> doff(k + 1, st);
+        k_key_offsets<<<(int)((k + 256) / 256), 256, 0, st>>>(skey.p, n, (int64_t)k, doff.p);
+        JB_LAUNCH_CHECK();
+        doff.download(off.data(), k + 1);
+        JB_CUDA(cudaStreamSynchronize(st));
+    }
+    SeqTerms t;
+    t.len = slen.p;
+    t.kind = SeqTerms::X;
+    t.a = scl;
+    t.b = sigma_len;
+    return seq_sum_nonneg(t, off, st, cm);
 }
 
 void relabel(uint32_t* d_labels, int64_t n, const std::vector<uint32_t>& rank_of,

@@ -216,6 +216,43 @@ struct BBox {
 };
 
 // ---------------------------------------------------------------------------
+// Exact emulation of the reference's sequential fp64 sums of non-negative
+// terms (seqsum.cu): var_len (digitization.hpp:39-45) and the per-group sum
+// of x (digitization.hpp:224-231).
+
+struct SeqTerms {
+    enum Kind : int { VAR_LEN = 0, X = 1, DIRECT = 2 };
+    const int32_t* len = nullptr;  // term i from len[i]
+    const double* w = nullptr;     // DIRECT: the terms themselves
+    int kind = VAR_LEN;
+    double a = 0.0, b = 1.0;       // VAR_LEN: (len - a)^2;  X: a * len / b
+};
+
+// Segment g is the terms [seg_off[g], seg_off[g+1]); each is summed
+// s = s_in[g]; s = fl(s + term) in index order, bit-exactly.
+struct SeqSum {
+    SeqTerms terms;
+    cudaStream_t stream = 0;
+    int64_t n_seg = 0, nblk = 0, n2 = 0, n3 = 0;
+    std::vector<int64_t> h_off, h_blk;
+    std::vector<double> local_total;  // approximate per-segment sums (prediction)
+    DArr<int64_t> d_blk, d_off;
+    DArr<double> bsum, gpre;
+    DArr<int> bseg, be, e2, s2, e3, s3;
+    DArr<unsigned long long> pe, po, pe2, po2, pe3, po3;
+    void setup(const SeqTerms& t, const std::vector<int64_t>& seg_off, cudaStream_t st);
+    // s_in_approx: approximate start values; terms_before: terms of the
+    // sequence preceding this part (other ranks), for the error bound
+    void predict(const std::vector<double>& s_in_approx, const std::vector<int64_t>& terms_before);
+    std::vector<double> resolve(const std::vector<double>& s_in);
+};
+
+// One call for all ranks (cm null or world 1: single GPU); rank r's terms of
+// segment g follow ranks 0..r-1's. Returns the exact sums from s = 0.
+std::vector<double> seq_sum_nonneg(const SeqTerms& t, const std::vector<int64_t>& seg_off,
+                                   cudaStream_t st, const Comm* cm = nullptr);
+
+// ---------------------------------------------------------------------------
 // k-means family (kmeans.cu)
 
 struct KMeansOut {
@@ -297,6 +334,13 @@ void symbolize_pieces(const int32_t* d_len, const double* d_inc, int64_t n,
 
 void relabel(uint32_t* d_labels, int64_t n, const std::vector<uint32_t>& rank_of,
              cudaStream_t st);
+
+// The reference's sequential per-group sums of x = scl*len/sigma_len over the
+// pieces in index order (digitization.hpp:224-231), bit-exact: labels are the
+// backend's cluster ids (< k) of this rank's pieces.
+std::vector<double> exact_group_sum_x(const int32_t* d_len, const uint32_t* d_labels, int64_t n,
+                                      uint64_t k, double scl, double sigma_len, cudaStream_t st,
+                                      const Comm* cm = nullptr);
 
 // Sum of len and count over sample labels (svq empty-cluster fallback,
 // digitization.hpp:240-252).

@@ -1,0 +1,461 @@
+// seqsum.cu — exact emulation of the reference's left-to-right fp64
+// accumulation of NON-NEGATIVE terms, in parallel.
+//
+// The reference sums several non-negative quantities with a plain loop,
+// `s += w` from s = 0 in index order:
+//   * var_len of scale_pieces, w = (len - mean_len)^2   digitization.hpp:39-45
+//   * the per-group sum of x = scl*len/sigma_len        digitization.hpp:224-231
+// Both feed discrete decisions of the inverse (rlen = c_x*sigma_len/scl,
+// inverse.hpp:46, then llround with carry, :63-74), so the device must produce
+// the SAME double, not a more accurate one.
+//
+// Method. For s in the binade [2^e, 2^(e+1)) the grid is u_e = 2^(e-52), and
+// as long as the result stays in that binade, fl(s + w) = s + u_e * inc(w)
+// where inc(w) = w / u_e rounded to nearest; a tie (w / u_e = a + 1/2) rounds
+// to the even significand, i.e. depends on the parity of M = s / u_e. Each term
+// is therefore the map M -> M + (M even ? i_even : i_odd), and such maps
+// compose associatively as pairs (i_even, i_odd). The sum is cut into blocks
+// of kB terms; a block whose accumulator provably stays in one binade e
+// (predicted from an approximate prefix, then VERIFIED while resolving) is
+// summarised by its composed pair, blocks of 32 and 1024 into uniform parent
+// pairs. One warp per segment then walks the blocks from the exact start
+// value: a uniform node whose binade matches and whose result stays below
+// 2^(e+1) is applied in O(1) -- exactly, by the argument above, since the
+// accumulator is monotone -- and everything else (the first terms, binade
+// crossings, mispredictions) is summed 32 terms at a time, falling back to
+// the hardware fp64 add (the reference's own operation) term by term where a
+// chunk crosses a binade or holds a tie. The prediction only decides speed:
+// every O(1) step is checked, so the result is the sequential sum for any
+// input (subnormal accumulators and zero included).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "jb_device.hpp"
+
+namespace jb {
+
+namespace {
+
+constexpr int kB = 2048;       // terms per block (64 per lane)
+constexpr int kNone = -100000; // "no uniform binade"
+
+struct Pair {
+    unsigned long long e, o;  // increments (units of u) for even / odd entry significand
+};
+
+__device__ __forceinline__ Pair compose(Pair f, Pair g) {
+    Pair r;
+    r.e = f.e + ((f.e & 1ULL) ? g.o : g.e);
+    r.o = f.o + (((1ULL + f.o) & 1ULL) ? g.o : g.e);
+    return r;
+}
+
+__device__ __forceinline__ double term_at(const SeqTerms& t, int64_t i) {
+    if (t.kind == SeqTerms::DIRECT) return t.w[i];
+    const double l = (double)t.len[i];
+    if (t.kind == SeqTerms::VAR_LEN) {
+        const double dl = l - t.a;  // digitization.hpp:41,43
+        return dl * dl;
+    }
+    return t.a * l / t.b;  // ScalingParams::apply core.hpp:131 (x)
+}
+
+// w / 2^(e-52): the integer part a and the class of the remainder
+// (0: below half, 1: above half, 2: exactly half). w >= 0 finite.
+// Saturates at 2^57 (callers then fail the < 2^53 check; 32 saturated
+// lanes still sum without wrapping).
+__device__ __forceinline__ unsigned long long grid_units(double w, int e, int& cls) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(w);
+    const int bexp = (int)((b >> 52) & 0x7FF);
+    unsigned long long m = b & 0x000FFFFFFFFFFFFFULL;
+    int ew;  // w = m * 2^(ew - 52)
+    if (bexp == 0) {
+        ew = -1022;
+    } else {
+        m |= 0x0010000000000000ULL;
+        ew = bexp - 1023;
+    }
+    cls = 0;
+    if (m == 0) return 0;
+    const int up = ew - e;  // w / u_e = m * 2^up
+    if (up >= 0) return up >= 5 ? (1ULL << 57) : (m << up);
+    const int sh = -up;
+    if (sh >= 55) return 0;  // < 1/2
+    const unsigned long long a = sh >= 64 ? 0 : (m >> sh);
+    const unsigned long long rem = m & ((1ULL << sh) - 1ULL);
+    const unsigned long long half = 1ULL << (sh - 1);
+    cls = rem > half ? 1 : (rem == half ? 2 : 0);
+    return a;
+}
+
+__device__ __forceinline__ Pair term_pair(double w, int e) {
+    int cls;
+    const unsigned long long a = grid_units(w, e, cls);
+    if (cls == 2) return Pair{a + (a & 1ULL), a + 1ULL - (a & 1ULL)};
+    return Pair{a + (unsigned long long)cls, a + (unsigned long long)cls};
+}
+
+// binade exponent of a positive normal double, kNone otherwise
+__device__ __forceinline__ int binade(double s) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(s);
+    const int bexp = (int)((b >> 52) & 0x7FF);
+    if ((b >> 63) || bexp == 0 || bexp == 0x7FF) return kNone;
+    return bexp - 1023;
+}
+
+// s (binade e) advanced by the pair p: true and s updated iff the result stays
+// in the binade (then it is exactly the sequential result)
+__device__ __forceinline__ bool apply_pair(double& s, int e, Pair p) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(s);
+    const unsigned long long M = (b & 0x000FFFFFFFFFFFFFULL) | 0x0010000000000000ULL;
+    const unsigned long long inc = (M & 1ULL) ? p.o : p.e;
+    if (inc >= (1ULL << 53)) return false;
+    const unsigned long long Mn = M + inc;
+    if (Mn >= (1ULL << 53)) return false;
+    s = __longlong_as_double((long long)(((unsigned long long)(e + 1023) << 52) |
+                                         (Mn & 0x000FFFFFFFFFFFFFULL)));
+    return true;
+}
+
+struct SegDesc {
+    const int64_t* blk;   // n_seg + 1: first block of each segment
+    const int64_t* off;   // n_seg + 1: first term of each segment
+    int64_t n_seg;
+};
+
+__device__ __forceinline__ int64_t seg_of_block(const SegDesc& sd, int64_t b) {
+    int64_t lo = 0, hi = sd.n_seg;  // largest g with blk[g] <= b
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (sd.blk[mid] <= b) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// pass 1: approximate block sums (prediction only)
+__global__ void k_ss_bsum(SeqTerms t, SegDesc sd, int64_t nblk, double* __restrict__ bsum,
+                          int* __restrict__ bseg) {
+    const int lane = threadIdx.x & 31;
+    const int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (b >= nblk) return;
+    const int64_t g = seg_of_block(sd, b);
+    const int64_t i0 = sd.off[g] + (b - sd.blk[g]) * kB;
+    const int64_t i1 = min(i0 + kB, sd.off[g + 1]);
+    double s = 0.0;
+    for (int64_t i = i0 + lane; i < i1; i += 32) s += term_at(t, i);
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+        bsum[b] = s;
+        bseg[b] = (int)g;
+    }
+}
+
+// pass 2: predicted binade of every block and its composed pair
+__global__ void k_ss_pairs(SeqTerms t, SegDesc sd, int64_t nblk, const double* __restrict__ bsum,
+                           const double* __restrict__ gpre, const int* __restrict__ bseg,
+                           const double* __restrict__ s_in, const int64_t* __restrict__ gbase,
+                           int* __restrict__ be, unsigned long long* __restrict__ pe,
+                           unsigned long long* __restrict__ po) {
+    const int lane = threadIdx.x & 31;
+    const int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (b >= nblk) return;
+    const int g = bseg[b];
+    const int64_t b0 = sd.blk[g];
+    const double P0 = s_in[g] + (gpre[b] - gpre[b0]);
+    const double P1 = P0 + bsum[b];
+    // |sequential - exact| <= (terms so far) * 2^-52 * s, plus slack for the
+    // approximate (double) prefix; a misprediction only costs the fallback
+    const int64_t i0 = sd.off[g] + (b - b0) * kB;
+    const int64_t i1 = min(i0 + kB, sd.off[g + 1]);
+    const double d = (double)(gbase[g] + (i1 - sd.off[g]) + (int64_t)(b - b0 + 2) * 64) * 0x1p-52 +
+                     0x1p-40;
+    const int e0 = binade(P0 * (1.0 - d)), e1 = binade(P1 * (1.0 + d));
+    int e = (e0 != kNone && e0 == e1) ? e0 : kNone;
+    Pair acc{0, 0};
+    if (e != kNone) {
+        unsigned long long sum = 0;
+        bool tie = false, big = false;
+        for (int64_t i = i0 + lane; i < i1; i += 32) {
+            int cls;
+            const unsigned long long a = grid_units(term_at(t, i), e, cls);
+            big |= a >= (1ULL << 53);  // one term alone leaves the binade
+            sum += a + (cls == 1 ? 1ULL : 0ULL);
+            tie |= cls == 2;
+        }
+        big |= sum >= (1ULL << 54);  // (64 terms per lane: no wrap before this test)
+        for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (__any_sync(0xffffffffu, big)) {
+            e = kNone;
+        } else if (__any_sync(0xffffffffu, tie)) {
+            // ordered composition: chunks of 32 by a shuffle scan, in order
+            Pair run{0, 0};
+            for (int64_t c = i0; c < i1; c += 32) {
+                const int64_t i = c + lane;
+                Pair p = i < i1 ? term_pair(term_at(t, i), e) : Pair{0, 0};
+                for (int o = 1; o < 32; o <<= 1) {
+                    Pair q;
+                    q.e = __shfl_up_sync(0xffffffffu, p.e, o);
+                    q.o = __shfl_up_sync(0xffffffffu, p.o, o);
+                    if (lane >= o) p = compose(q, p);
+                }
+                Pair tot;
+                tot.e = __shfl_sync(0xffffffffu, p.e, 31);
+                tot.o = __shfl_sync(0xffffffffu, p.o, 31);
+                run = compose(run, tot);
+            }
+            acc = run;
+        } else {
+            acc = Pair{sum, sum};
+        }
+        if (acc.e >= (1ULL << 53) || acc.o >= (1ULL << 53)) e = kNone;
+    }
+    if (lane == 0) {
+        be[b] = e;
+        pe[b] = acc.e;
+        po[b] = acc.o;
+    }
+}
+
+// parents of 32 consecutive nodes: uniform iff all 32 children are uniform in
+// the same binade and segment
+__global__ void k_ss_level(int64_t nchild, const int* __restrict__ ce, const int* __restrict__ cseg,
+                           const unsigned long long* __restrict__ cpe,
+                           const unsigned long long* __restrict__ cpo, int64_t npar,
+                           int* __restrict__ e_out, int* __restrict__ seg_out,
+                           unsigned long long* __restrict__ pe_out,
+                           unsigned long long* __restrict__ po_out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (p >= npar) return;
+    const int64_t c = p * 32 + lane;
+    const bool have = c < nchild;
+    const int e = have ? ce[c] : kNone;
+    const int sg = have ? cseg[c] : -1;
+    Pair q = have ? Pair{cpe[c], cpo[c]} : Pair{0, 0};
+    const int e0 = __shfl_sync(0xffffffffu, e, 0);
+    const int s0 = __shfl_sync(0xffffffffu, sg, 0);
+    const bool uni = __all_sync(0xffffffffu, have && e == e0 && sg == s0 && e != kNone);
+    for (int o = 1; o < 32; o <<= 1) {
+        Pair r;
+        r.e = __shfl_up_sync(0xffffffffu, q.e, o);
+        r.o = __shfl_up_sync(0xffffffffu, q.o, o);
+        if (lane >= o) q = compose(r, q);
+    }
+    if (lane == 31) {
+        const bool fits = q.e < (1ULL << 53) && q.o < (1ULL << 53);
+        e_out[p] = uni && fits ? e0 : kNone;
+        seg_out[p] = s0;
+        pe_out[p] = q.e;
+        po_out[p] = q.o;
+    }
+}
+
+struct Level {
+    const int* e;
+    const int* seg;
+    const unsigned long long* pe;
+    const unsigned long long* po;
+};
+
+// the chunk fallback: terms [i0, i1) from s, 32 at a time (warp-uniform s)
+__device__ void ss_terms(const SeqTerms& t, int64_t i0, int64_t i1, double& s) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t c = i0; c < i1; c += 32) {
+        const int64_t i = c + lane;
+        const int n = (int)(i1 - c < 32 ? i1 - c : 32);
+        const double w = i < i1 ? term_at(t, i) : 0.0;
+        const int e = binade(s);
+        if (e != kNone) {
+            int cls;
+            unsigned long long a = grid_units(w, e, cls);
+            a += cls == 1 ? 1ULL : 0ULL;
+            const bool tie = cls == 2;
+            for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+            if (!__any_sync(0xffffffffu, tie) && apply_pair(s, e, Pair{a, a})) continue;
+        }
+        for (int j = 0; j < n; ++j) s = s + __shfl_sync(0xffffffffu, w, j);  // the reference's add
+    }
+}
+
+// one warp per segment: s_out[g] = sequential sum of the segment from s_in[g]
+__global__ void k_ss_resolve(SeqTerms t, SegDesc sd, int64_t nblk, Level L1, Level L2, int64_t n2,
+                             Level L3, int64_t n3, const double* __restrict__ s_in,
+                             double* __restrict__ s_out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (g >= sd.n_seg) return;
+    double s = s_in[g];
+    const int64_t bend = sd.blk[g + 1];
+    int64_t b = sd.blk[g];
+    while (b < bend) {
+        const int e = binade(s);
+        if (e != kNone) {
+            if ((b & 1023) == 0 && b + 1024 <= bend && (b >> 10) < n3) {
+                const int64_t p = b >> 10;
+                if (L3.e[p] == e && L3.seg[p] == (int)g && apply_pair(s, e, Pair{L3.pe[p], L3.po[p]})) {
+                    b += 1024;
+                    continue;
+                }
+            }
+            if ((b & 31) == 0 && b + 32 <= bend && (b >> 5) < n2) {
+                const int64_t p = b >> 5;
+                if (L2.e[p] == e && L2.seg[p] == (int)g && apply_pair(s, e, Pair{L2.pe[p], L2.po[p]})) {
+                    b += 32;
+                    continue;
+                }
+            }
+            if (L1.e[b] == e && apply_pair(s, e, Pair{L1.pe[b], L1.po[b]})) {
+                ++b;
+                continue;
+            }
+        }
+        const int64_t i0 = sd.off[g] + (b - sd.blk[g]) * kB;
+        const int64_t i1 = min(i0 + kB, sd.off[g + 1]);
+        ss_terms(t, i0, i1, s);
+        ++b;
+    }
+    if (lane == 0) s_out[g] = s;
+}
+
+int blocks_for_warps(int64_t warps) { return (int)std::max<int64_t>(1, (warps + 7) / 8); }
+
+}  // namespace
+
+void SeqSum::setup(const SeqTerms& t, const std::vector<int64_t>& seg_off, cudaStream_t st) {
+    terms = t;
+    stream = st;
+    n_seg = (int64_t)seg_off.size() - 1;
+    h_off = seg_off;
+    h_blk.assign(n_seg + 1, 0);
+    for (int64_t g = 0; g < n_seg; ++g)
+        h_blk[g + 1] = h_blk[g] + (seg_off[g + 1] - seg_off[g] + kB - 1) / kB;
+    nblk = h_blk[n_seg];
+    d_blk.alloc(n_seg + 1, st);
+    d_off.alloc(n_seg + 1, st);
+    d_blk.upload(h_blk.data(), n_seg + 1);
+    d_off.upload(h_off.data(), n_seg + 1);
+    const size_t nb = (size_t)std::max<int64_t>(nblk, 1);
+    bsum.alloc(nb, st);
+    gpre.alloc(nb, st);
+    bseg.alloc(nb, st);
+    local_total.assign(n_seg, 0.0);
+    if (nblk == 0) return;
+    const SegDesc sd{d_blk.p, d_off.p, n_seg};
+    {
+        JB_PROF("seqsum_blocks", st);
+        k_ss_bsum<<<blocks_for_warps(nblk), 256, 0, st>>>(t, sd, nblk, bsum.p, bseg.p);
+    }
+    JB_LAUNCH_CHECK();
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, bsum.p, gpre.p, nblk, st);
+    DArr<uint8_t> tmp(std::max<size_t>(tb, 1), st);
+    cub::DeviceScan::ExclusiveSum(tmp.p, tb, bsum.p, gpre.p, nblk, st);
+    JB_LAUNCH_CHECK();
+    // per-segment totals (approximate): for the start-value predictions of
+    // the following ranks / for diagnostics
+    std::vector<double> g(nblk), bs(nblk);
+    gpre.download(g.data(), nblk);
+    bsum.download(bs.data(), nblk);
+    JB_CUDA(cudaStreamSynchronize(st));
+    for (int64_t s = 0; s < n_seg; ++s) {
+        if (h_blk[s + 1] == h_blk[s]) continue;
+        local_total[s] = g[h_blk[s + 1] - 1] + bs[h_blk[s + 1] - 1] - g[h_blk[s]];
+    }
+}
+
+void SeqSum::predict(const std::vector<double>& s_in_approx, const std::vector<int64_t>& terms_before) {
+    cudaStream_t st = stream;
+    const size_t nb = (size_t)std::max<int64_t>(nblk, 1);
+    be.alloc(nb, st);
+    pe.alloc(nb, st);
+    po.alloc(nb, st);
+    n2 = (nblk + 31) / 32;
+    n3 = (n2 + 31) / 32;
+    e2.alloc(std::max<int64_t>(n2, 1), st);
+    s2.alloc(std::max<int64_t>(n2, 1), st);
+    pe2.alloc(std::max<int64_t>(n2, 1), st);
+    po2.alloc(std::max<int64_t>(n2, 1), st);
+    e3.alloc(std::max<int64_t>(n3, 1), st);
+    s3.alloc(std::max<int64_t>(n3, 1), st);
+    pe3.alloc(std::max<int64_t>(n3, 1), st);
+    po3.alloc(std::max<int64_t>(n3, 1), st);
+    if (nblk == 0) return;
+    DArr<double> sin_d(n_seg, st);
+    sin_d.upload(s_in_approx.data(), n_seg);
+    DArr<int64_t> gb(n_seg, st);
+    gb.upload(terms_before.data(), n_seg);
+    const SegDesc sd{d_blk.p, d_off.p, n_seg};
+    {
+        JB_PROF("seqsum_pairs", st);
+        k_ss_pairs<<<blocks_for_warps(nblk), 256, 0, st>>>(terms, sd, nblk, bsum.p, gpre.p, bseg.p,
+                                                           sin_d.p, gb.p, be.p, pe.p, po.p);
+        JB_LAUNCH_CHECK();
+        k_ss_level<<<blocks_for_warps(n2), 256, 0, st>>>(nblk, be.p, bseg.p, pe.p, po.p, n2, e2.p,
+                                                         s2.p, pe2.p, po2.p);
+        JB_LAUNCH_CHECK();
+        k_ss_level<<<blocks_for_warps(n3), 256, 0, st>>>(n2, e2.p, s2.p, pe2.p, po2.p, n3, e3.p,
+                                                         s3.p, pe3.p, po3.p);
+        JB_LAUNCH_CHECK();
+    }
+    JB_CUDA(cudaStreamSynchronize(st));  // sin_d / gb are released on return
+}
+
+std::vector<double> SeqSum::resolve(const std::vector<double>& s_in) {
+    cudaStream_t st = stream;
+    std::vector<double> out(s_in);
+    if (n_seg == 0) return out;
+    DArr<double> din(n_seg, st), dout(n_seg, st);
+    din.upload(s_in.data(), n_seg);
+    const SegDesc sd{d_blk.p, d_off.p, n_seg};
+    const Level L1{be.p, bseg.p, pe.p, po.p}, L2{e2.p, s2.p, pe2.p, po2.p},
+        L3{e3.p, s3.p, pe3.p, po3.p};
+    {
+        JB_PROF("seqsum_resolve", st);
+        k_ss_resolve<<<blocks_for_warps(n_seg), 256, 0, st>>>(terms, sd, nblk, L1, L2, n2, L3, n3,
+                                                              din.p, dout.p);
+    }
+    JB_LAUNCH_CHECK();
+    dout.download(out.data(), n_seg);
+    JB_CUDA(cudaStreamSynchronize(st));
+    return out;
+}
+
+std::vector<double> seq_sum_nonneg(const SeqTerms& t, const std::vector<int64_t>& seg_off,
+                                   cudaStream_t st, const Comm* cm) {
+    const int64_t n_seg = (int64_t)seg_off.size() - 1;
+    SeqSum ss;
+    ss.setup(t, seg_off, st);
+    std::vector<double> s_in(n_seg, 0.0);
+    std::vector<int64_t> before(n_seg, 0);
+    if (!cm || !cm->dist()) {
+        ss.predict(s_in, before);
+        return ss.resolve(s_in);
+    }
+    // ranks hold consecutive pieces of every segment: rank r's terms follow
+    // ranks 0..r-1's. Predictions from the gathered approximate totals, then
+    // the exact start values are handed down the ranks one at a time.
+    std::vector<double> tot = cm->gather(ss.local_total);
+    std::vector<int64_t> cnt(n_seg);
+    for (int64_t g = 0; g < n_seg; ++g) cnt[g] = seg_off[g + 1] - seg_off[g];
+    std::vector<int64_t> cnts = cm->gather(cnt);
+    std::vector<double> approx(n_seg, 0.0);
+    for (int r = 0; r < cm->rank; ++r)
+        for (int64_t g = 0; g < n_seg; ++g) {
+            approx[g] += tot[(size_t)r * n_seg + g];
+            before[g] += cnts[(size_t)r * n_seg + g];
+        }
+    ss.predict(approx, before);
+    std::vector<double> cur(n_seg, 0.0);
+    for (int r = 0; r < cm->world; ++r) {
+        std::vector<double> mine = r == cm->rank ? ss.resolve(cur) : cur;
+        std::vector<double> all = cm->gather(mine);
+        std::copy(all.begin() + (size_t)r * n_seg, all.begin() + (size_t)(r + 1) * n_seg, cur.begin());
+    }
+    return cur;
+}
+
+}  // namespace jb
