@@ -131,6 +131,109 @@ def make_series_gpu(n: int, seed: int, device):
     return x
 
 
+def _znorm_rows(x):
+    import torch
+    mu = x.mean(dim=-1, keepdim=True)
+    sd = x.std(dim=-1, unbiased=False, keepdim=True)
+    sd[sd == 0] = 1.0
+    return (x - mu) / sd
+
+
+def _sines_gpu(g, rows, length, dev):
+    import torch
+    t = torch.arange(length, dtype=torch.float64, device=dev)
+    P = torch.rand(rows, 3, 1, dtype=torch.float64, device=dev, generator=g) * 480 + 20
+    A = torch.rand(rows, 3, 1, dtype=torch.float64, device=dev, generator=g) * 1.5 + 0.5
+    ph = torch.rand(rows, 3, 1, dtype=torch.float64, device=dev, generator=g) * 2 * np.pi
+    x = (A * torch.sin(2 * np.pi * t / P + ph)).sum(1)
+    x += 0.1 * torch.randn(rows, length, dtype=torch.float64, device=dev, generator=g)
+    return _znorm_rows(x)
+
+
+def _walks_gpu(g, rows, length, dev):
+    import torch
+    x = torch.zeros(rows, length, dtype=torch.float64, device=dev)
+    x[:, 1:] = torch.cumsum(torch.randn(rows, length - 1, dtype=torch.float64, device=dev,
+                                        generator=g), 1)
+    return _znorm_rows(x)
+
+
+def make_config_gpu(cid: int, dev):
+    """BASELINE.json configs 1, 2, 3, 5 at full scale, generated on the GPU
+    (torch as plumbing; same shapes and distributions as datasets.py, not its
+    draws). Returns (values, series_lengths, layout, parts, cfg)."""
+    import torch
+    g = torch.Generator(device=dev)
+    g.manual_seed(1000 + cid)
+    if cid == 1:
+        x = _walks_gpu(g, 64, 2000, dev)
+        return x.reshape(-1), [2000] * 64, 2, 1, dict(tol=0.05, backend="svq", k=50, r=0.5,
+                                                       seed=0, scl=1.0)
+    if cid == 2:
+        x = _sines_gpu(g, 1000, 10000, dev)
+        return x.reshape(-1), [10000] * 1000, 2, 4, dict(tol=0.1, backend="ga", alpha=0.1,
+                                                          sort_key=1, early_stop=1, scl=1.0)
+    if cid == 3:
+        S, C, T = 1000, 64, 4096
+        x = torch.empty(S, C, T, dtype=torch.float64, device=dev)
+        for s0 in range(0, S, 100):  # AR(1) phi .95 with a shared N(0,1) factor
+            f = torch.randn(100, 1, T, dtype=torch.float64, device=dev, generator=g)
+            e = np.sqrt(0.5) * f + np.sqrt(0.5) * torch.randn(100, C, T, dtype=torch.float64,
+                                                              device=dev, generator=g)
+            e = e.permute(2, 0, 1).contiguous()
+            for t in range(1, T):
+                e[t].add_(e[t - 1], alpha=0.95)
+            x[s0:s0 + 100] = _znorm_rows(e.permute(1, 2, 0))
+            del e, f
+        return x.reshape(-1), [T] * (S * C), 2, 1, dict(tol=0.05, backend="svq", k=100, r=0.3,
+                                                         seed=0, scl=1.0)
+    if cid == 5:
+        R, L = 10000, 100000
+        x = torch.empty(R, L, dtype=torch.float64, device=dev)
+        for r0 in range(0, R, 500):
+            x[r0:r0 + 500:2] = _walks_gpu(g, 250, L, dev)
+            x[r0 + 1:r0 + 500:2] = _sines_gpu(g, 250, L, dev)
+        return x.reshape(-1), [L] * R, 2, 8, dict(tol=0.05, backend="svq", k=500, r=0.2,
+                                                   seed=0, scl=1.0)
+    raise ValueError(cid)
+
+
+def time_config(cid, eng, api, dev, steps, warmup):
+    """Device-resident fit_transform + inverse_transform of one config."""
+    import torch
+    x, lengths, layout, parts, cfgd = make_config_gpu(cid, dev)
+    n = x.numel()
+    first, st = api.plan_segments(lengths, layout, parts)
+    cfg = api.JabbaConfig.of(**cfgd)
+    out = torch.empty(n + len(first), dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+
+    def one():
+        nf = eng.fit_arrays(None, first, st, layout, cfg, device_ptr=x.data_ptr(), n_values=n)
+        nf.inverse(out_ptr=out.data_ptr(), on_device=True)
+        return nf
+
+    for _ in range(warmup):
+        nf = one()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        nf = one()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    res = {"n_points": n, "segments": len(first), "pieces": nf.n_pieces, "k": nf.k,
+           "backend": cfgd["backend"], "ms_per_step": ms, "value": n / (ms / 1e3),
+           "unit": "points/s", "steps": steps, "warmup": warmup,
+           "iterations": nf.stats()["iterations"],
+           "data": "synthetic on device (torch), config shapes of BASELINE.json"}
+    nf.close()
+    del x, out
+    torch.cuda.empty_cache()
+    return res
+
+
 # ---------------------------------------------------------------------------
 # roofline bookkeeping for the dominant kernel
 
@@ -169,49 +272,53 @@ def algorithmic_work(name, launches, info):
     return None, None
 
 
-def step_roofline(info, ms_step, hbm_gbs, fp64_tflops):
-    """Whole-step roofline of SURVEY.md §8(d): per phase T_roof = max(bytes /
-    HBM, flops / FP64 peak) with the reference algorithm's compulsory work
-    (brute-force D^2 / Lloyd / final assignment over all k centers), summed;
-    frac = T_roof / T_measured. T (candidate tests) = steps + N: every step is
-    one accepted test and every piece but a segment's last ends on a failed
-    one (T/step 1.89 at cfg4). A frac above 1 means the exact
-    candidate pruning does less work than the reference
-    algorithm's compulsory minimum."""
-    n, N, S, k, I = info["n"], info["N"], info["S"], info["k"], info["iterations"]
-    T = info["steps"] + N
-    phases = {  # (flops, bytes)
-        "compress": (23.0 * T, 8.0 * n + 16.0 * N),
-        "scale": (11.0 * N, 32.0 * N),
-        "d2_seed": (9.0 * S * k, 32.0 * S * k),
-        "lloyd": (I * (6.0 * S * k + 2.0 * S), I * 24.0 * S),
-        "final_assign": (6.0 * N * k + 3.0 * N, 20.0 * N),
-        "inverse": (6.0 * N + 3.0 * n, 4.0 * N + 8.0 * n),
-    }
-    out, tot = {}, 0.0
-    for ph, (fl, by) in phases.items():
-        t_b = by / (hbm_gbs * 1e9)
-        t_f = fl / (fp64_tflops * 1e12) if fp64_tflops else 0.0
-        t = max(t_b, t_f)
-        tot += t
-        out[ph] = {"flops": fl, "bytes": by, "t_roof_ms": t * 1e3,
-                   "bound": "fp64" if t_f > t_b else "hbm"}
-    return {"definition": "SURVEY.md §8(d): sum over phases of max(bytes/HBM, flops/FP64), "
-                          "reference algorithm's compulsory work; frac = T_roof / T_measured",
-            "hbm_gbs": hbm_gbs, "fp64_tflops": fp64_tflops,
-            "fp64_peak_source": "measured DFMA-chain probe on this GPU (jb_probe_fp64_tflops, 2 flop/DFMA)",
-            "t_roof_ms": tot * 1e3, "t_measured_ms": ms_step, "frac": tot * 1e3 / ms_step,
-            "phases": out}
+def work_roofline(ms_step, hbm_gbs, fp64_tflops):
+    """Work-done roofline of one step: sum over the kernels of one config-4
+    step of max(DRAM bytes / HBM peak, fp64 flops / FP64 peak), each kernel's
+    bytes and flops MEASURED by ncu (profiles/ncu_work.json, tools/ncu_work.py:
+    dram__bytes_read+write, dadd + dmul + 2 dfma thread instructions), divided
+    by the measured step time. frac = 1 would mean every kernel runs at the
+    bound of the traffic and arithmetic it actually does."""
+    p = os.path.join(ROOT, "profiles", "ncu_work.json")
+    try:
+        with open(p) as f:
+            w = json.load(f)
+    except (OSError, ValueError):
+        return None
+    t = 0.0
+    top = []
+    for name, k in w["kernels"].items():
+        tb = k["dram_bytes"] / (hbm_gbs * 1e9)
+        tf = k["fp64_flops"] / (fp64_tflops * 1e12) if fp64_tflops else 0.0
+        t += max(tb, tf)
+        top.append((max(tb, tf), name, "fp64" if tf > tb else "hbm", k["time_ms"]))
+    top.sort(reverse=True)
+    return {"definition": "sum over kernels of max(ncu DRAM bytes / HBM, ncu fp64 flops / FP64) "
+                          "per step, / measured step time",
+            "source": os.path.basename(p) + " (" + w.get("report", "?") + ")",
+            "t_work_ms": t * 1e3, "t_measured_ms": ms_step, "frac": t * 1e3 / ms_step,
+            "ncu_kernel_ms_sum": w.get("t_kernels_ms"),
+            "top": [{"kernel": n, "bound": b, "t_roof_ms": round(x * 1e3, 3),
+                     "ncu_ms": round(m, 3)} for x, n, b, m in top[:8]]}
+
+
+def io_floor(n, N, ms_step, hbm_gbs):
+    """Compulsory I/O of the round trip: read the samples once (8 B), write
+    the reconstruction (8 B/sample) and the labels (4 B/piece)."""
+    b = 16.0 * n + 4.0 * N
+    t = b / (hbm_gbs * 1e9) * 1e3
+    return {"bytes": b, "t_ms": t, "frac_of_step": t / ms_step}
 
 
 def ncu_traffic(name):
-    """Per-launch DRAM bytes of `name` from an ncu --set full capture
-    (profiles/ncu_traffic.json, written by tools/ncu_traffic.py), or None."""
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    """Per-launch DRAM bytes of `name` averaged over ALL its launches in one
+    step (profiles/ncu_work.json, tools/ncu_work.py), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_work.json")
     try:
         with open(p) as f:
-            return json.load(f)[name]["dram_bytes_per_launch"]
-    except (OSError, KeyError, ValueError):
+            b = json.load(f)["bench_names"][name]
+        return b["dram_bytes"] / b["launches"]
+    except (OSError, KeyError, ValueError, ZeroDivisionError):
         return None
 
 
@@ -233,12 +340,52 @@ def measured_peaks():
 # ---------------------------------------------------------------------------
 # CPU baseline: the reference itself on a bounded sample
 
+def load_generators():
+    """paper_2401_00109_b200/datasets.py (numpy generators) loaded by path, so
+    the reference arm never imports the package (whose native library must not
+    be mapped in that process)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "jb_bench_datasets", os.path.join(ROOT, "paper_2401_00109_b200", "datasets.py"))
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules[spec.name] = mod  # (dataclasses look their module up)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def split_plan(series_lengths, parts):
+    """Segment table of detail::split_series (compression.hpp:140-160): each
+    series' steps split into `parts` near-equal parts, the first steps % parts
+    parts one step longer; a part starts at the previous part's last sample."""
+    first, steps, start = [], [], 0
+    for n in series_lengths:
+        total = int(n) - 1
+        base, extra = divmod(total, parts)
+        b = start
+        for s in range(parts):
+            st = base + (1 if s < extra else 0)
+            first.append(b)
+            steps.append(st)
+            b += st
+        start += int(n)
+    return np.array(first, np.int64), np.array(steps, np.int64)
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_reference_run(scale: float, steps: int = 1):
     from oracle_lib import Reference, make_config
-    from paper_2401_00109_b200 import datasets
-    from paper_2401_00109_b200.api import plan_segments
-    w = datasets.config4(scale)
-    first, st = plan_segments(w.series_lengths, w.layout, w.parts)
+    w = load_generators().config4(scale)
+    first, st = split_plan(w.series_lengths, w.parts)
     cores = os.cpu_count() or 1
     cfg = make_config(threads=cores, **CFG4)
     R = Reference()
@@ -266,6 +413,8 @@ def main():
                     help="bounded CPU sample (fraction of config 4) for cpu_baseline")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--configs", default="1,2,3,5",
+                    help="other BASELINE configs timed after the headline (empty: none)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -279,15 +428,25 @@ def main():
         timed = times[args.warmup:] or times
         t = sum(timed) / len(timed)
         v = n / t
-        sample = (f"cfg4 at {args.cpu_scale:g} scale: {n} samples, {nseg} partitions, "
-                  "tol 0.1, svq k=200 r=0.1; jabba_fit + reconstruct of the unmodified "
-                  "reference headers (oracle/_ref), compression threads = nproc")
+        sample = (f"BOUNDED SLICE of the workload: cfg4 at {args.cpu_scale:g} scale, {n} samples "
+                  f"in {nseg} partitions of 1e5 (the full config's partition size), tol 0.1, "
+                  "svq k=200 r=0.1; one step = jabba_fit + reconstruct of the unmodified "
+                  "reference headers (oracle/_ref), compression threads = nproc "
+                  "(digitization and inverse are single-threaded in the reference)")
+        n_full = int(round(1e9 * args.scale))
         print(json.dumps({
             "metric": METRIC, "value": v, "unit": "points/s", "n_gpus": args.gpus,
             "steps": len(timed), "warmup": args.warmup, "ms_per_step": t * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": workload_desc(n, nseg, args.cpu_scale),
+            "config": workload_desc(n_full, max(1, int(round(10000 * args.scale))), args.scale),
+            "slice": {"n_points": n, "partitions": nseg, "scale": args.cpu_scale,
+                      "ms_per_step": t * 1e3,
+                      "extrapolated_ms_per_step_full": t * 1e3 * n_full / n,
+                      "extrapolation": "linear in samples at fixed partition size, k, r "
+                                       "(Lloyd cost is linear in the sample size at I=300; "
+                                       "SURVEY.md §6 measured 1% -> full as linear)"},
+            "cpu_model": cpu_model(),
             "cpu_baseline": {"value": v, "unit": "points/s", "cores": cores,
                              "kind": "reference", "sample": sample},
             "e2e": {"value": v, "unit": "points/s", "h2d_bytes_per_step": 0,
@@ -456,6 +615,16 @@ def main():
                          "unmodified reference (oracle/_ref), 1 jabba_fit + reconstruct, "
                          f"{ctimes[0]:.1f} s"}
 
+    configs = {}
+    if rank == 0 and world == 1 and args.configs:
+        del out
+        torch.cuda.empty_cache()
+        for c in [int(v) for v in args.configs.split(",") if v]:
+            try:
+                configs[f"cfg{c}"] = time_config(c, eng, api, dev, max(2, min(args.steps, 5)), 2)
+            except Exception as ex:  # report, never hide
+                configs[f"cfg{c}"] = {"error": repr(ex)}
+
     # launches per step of the instrumented kernels (every hot kernel is)
     gpu_launches = int(sum(c for _, c in prof.values())) * args.steps if prof else 0
     if rank == 0:
@@ -466,8 +635,10 @@ def main():
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": workload_desc(n, m, args.scale, world),
             "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
-            "step_roofline": step_roofline(dict(info, steps=int(sum(steps_g))), ms_step,
-                                           peaks.get("hbm_gbs"), fp64_peak(_native.lib(), local)),
+            "work_roofline": work_roofline(ms_step, peaks.get("hbm_gbs"),
+                                           fp64_peak(_native.lib(), local)),
+            "io_floor": io_floor(n, N, ms_step, peaks.get("hbm_gbs")),
+            "configs": configs, "cpu_model": cpu_model(),
             "clocks": clk.summary(), "gpu_launches": gpu_launches,
             "phase_ms": st["ms"], "profiled_step_ms": ms_profiled, "fit_stats": {k: st[k] for k in ("iterations", "sample_size",
                                                                     "fix_rounds")},

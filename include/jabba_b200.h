@@ -221,6 +221,13 @@ jb_status jb_mt19937_64_stream(jb_context* ctx, uint64_t seed, uint64_t count, u
 jb_status jb_sample_indices(jb_context* ctx, uint64_t n, uint64_t sample_size, uint64_t seed,
                             uint64_t* out);
 
+/* jabba::kmeans (clustering.hpp:224-236) on 2-D points (host, interleaved
+ * x,y): D^2 seeding, Lloyd iterations and restarts on the device with the
+ * reference's RNG stream; labels (n), centers (2k), iterations of the best run. */
+jb_status jb_kmeans(jb_context* ctx, const double* points, int64_t n, uint64_t k,
+                    uint64_t max_iters, uint64_t n_init, uint64_t seed, uint32_t* labels,
+                    double* centers, uint64_t* iterations);
+
 /* The reference's left-to-right fp64 accumulation `s += w` from s = 0 of
  * non-negative terms (scale_pieces var_len digitization.hpp:39-45, group sums
  * :224-231), reproduced bit-exactly by the parallel emulation the fit uses

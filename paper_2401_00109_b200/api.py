@@ -469,6 +469,17 @@ class Engine:
         _check(N.lib().jb_sample_indices(self.ctx, n, sample_size, seed, out.ctypes.data))
         return out[:sample_size]
 
+    def kmeans(self, points, k: int, max_iters: int = 300, n_init: int = 1, seed: int = 0):
+        """jabba::kmeans (clustering.hpp:224-236) on device: (labels, centers, iterations)."""
+        p = np.ascontiguousarray(points, np.float64).reshape(-1, 2)
+        n = len(p)
+        labels = np.zeros(max(n, 1), np.uint32)
+        centers = np.zeros(max(2 * k, 1), np.float64)
+        it = C.c_uint64(0)
+        _check(N.lib().jb_kmeans(self.ctx, p.ctypes.data, n, k, max_iters, n_init, seed,
+                                 labels.ctypes.data, centers.ctypes.data, C.byref(it)))
+        return labels[:n], centers[: 2 * k].reshape(-1, 2), it.value
+
     def seq_sum_nonneg(self, terms, seg_off=None) -> np.ndarray:
         """The reference's sequential ``s += w`` over non-negative terms
         (digitization.hpp:39-45, 224-231), per segment, bit-exact on device."""

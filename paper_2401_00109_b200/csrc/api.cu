@@ -1189,6 +1189,50 @@ jb_status jb_sample_indices(jb_context* ctx, uint64_t n, uint64_t sample_size, u
     });
 }
 
+jb_status jb_kmeans(jb_context* ctx, const double* points, int64_t n, uint64_t k,
+                    uint64_t max_iters, uint64_t n_init, uint64_t seed, uint32_t* labels,
+                    double* centers, uint64_t* iterations) {
+    return (jb_status)guarded([&] {
+        JB_CUDA(cudaSetDevice(ctx->device));
+        cudaStream_t st = ctx->stream;
+        // VQConfig::validate (clustering.hpp:26-31) through the fit's checks
+        jb_config c;
+        jb_config_default(&c);
+        c.k = k;
+        c.max_iters = max_iters;
+        c.n_init = n_init;
+        validate_vq(c, 1.0);
+        if (n <= 0) throw Error(INVALID_INPUT, "kmeans: no points");
+        if ((int64_t)k > n) throw Error(INVALID_INPUT, "kmeans: k exceeds points");
+        BBox bb{points[0], points[0], points[1], points[1]};
+        for (int64_t i = 0; i < n; ++i) {
+            const double x = points[2 * i], y = points[2 * i + 1];
+            if (!std::isfinite(x) || !std::isfinite(y))
+                throw Error(INVALID_INPUT, "kmeans: non-finite point");
+            bb.xmin = std::min(bb.xmin, x);
+            bb.xmax = std::max(bb.xmax, x);
+            bb.ymin = std::min(bb.ymin, y);
+            bb.ymax = std::max(bb.ymax, y);
+        }
+        DArr<double> dp(2 * n, st);
+        dp.upload(points, 2 * n);
+        PtsView pv;
+        pv.pts = reinterpret_cast<const double2*>(dp.p);
+        DArr<uint64_t> raw;
+        const uint64_t raw_count = (k + 1) * n_init + 4096;
+        mt19937_64_generate(seed, raw_count, raw, st);
+        uint64_t cursor = 0;
+        KMeansOut km;
+        lloyd_best_device(pv, nullptr, n, k, max_iters, n_init, raw.p, raw_count, &cursor, bb, km,
+                          st);
+        kmeans_labels(km, n, st);
+        km.labels.download(labels, n);
+        JB_CUDA(cudaStreamSynchronize(st));
+        std::copy(km.centers.begin(), km.centers.begin() + 2 * k, centers);
+        *iterations = km.iterations;
+    });
+}
+
 jb_status jb_seq_sum_nonneg(jb_context* ctx, const double* terms, const int64_t* seg_off,
                             int64_t n_seg, double* out) {
     return (jb_status)guarded([&] {
