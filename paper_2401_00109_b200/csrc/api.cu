@@ -702,13 +702,24 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
     // ---- group statistics, ranking, codebook (digitization.hpp:217-291) ----
     auto t3 = Clock::now();
     GroupStats gs;
+    RangeHist xh;  // per-range (length, group) counts: the exact x sums below
     assign_and_stats(pv, fit->pieces.len.p, N, backend_centers, k, bb, assign_needed,
-                     labels.p, gs, st, sc.max_len_global, sc.scl, sc.sigma_len, &cm, base);
+                     labels.p, gs, st, sc.max_len_global, sc.scl, sc.sigma_len, &cm, base,
+                     k <= 2048 ? &xh : nullptr);
     // the x sums bit-exact as the reference accumulates them: then the
     // codebook's x and every reconstructed length match (inverse.hpp:46,63-74)
     if (k > 0) {
-        const std::vector<double> sx = exact_group_sum_x(fit->pieces.len.p, labels.p, N, k, sc.scl,
-                                                         sc.sigma_len, st, &cm);
+        std::vector<double> sx;
+        if (k <= 2048) {
+            SeqTerms xt;
+            xt.len = fit->pieces.len.p;
+            xt.kind = SeqTerms::X;
+            xt.a = sc.scl;
+            xt.b = sc.sigma_len;
+            sx = range_seq_sums(xh, xt, labels.p, st, &cm);
+        } else {  // large alphabets (GA): sort the lengths by group, then sum
+            sx = exact_group_sum_x(fit->pieces.len.p, labels.p, N, k, sc.scl, sc.sigma_len, st, &cm);
+        }
         for (uint64_t g = 0; g < k; ++g) gs.sum_x[g] = sx[g];
     }
     std::vector<double> centers(2 * k), mean_lengths(k);

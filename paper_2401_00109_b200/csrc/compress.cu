@@ -216,13 +216,22 @@ __global__ void __launch_bounds__(128) k_spec(const double* __restrict__ v, Chun
 }
 
 // Phase 2: E_out[c] = F_c(E_in[c-1]), F_c = exit of chunk c when the true
-// orbit enters it at t.
+// orbit enters it at t. Only chunks whose entry changed in the previous round
+// (dirty_in[c-1]) are re-evaluated: long pieces make chains of chunks whose
+// orbits merge late (config 5: ~50 rounds), and a full re-parse of every
+// chunk per round would cost a whole compression pass each time.
 __global__ void k_fix(const double* __restrict__ v, ChunkGeom g, int64_t n_chunks, double tol2,
                       int64_t max_len, const uint32_t* __restrict__ fb,
                       const int64_t* __restrict__ exit_spec, const int64_t* __restrict__ E_in,
-                      int64_t* __restrict__ E_out, int* __restrict__ changed) {
+                      int64_t* __restrict__ E_out, int* __restrict__ changed,
+                      const uint8_t* __restrict__ dirty_in, uint8_t* __restrict__ dirty_out) {
     const int64_t ch = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (ch >= n_chunks) return;
+    if (dirty_in && !(ch > 0 && dirty_in[ch - 1])) {  // entry unchanged: so is the exit
+        E_out[ch] = E_in[ch];
+        dirty_out[ch] = 0;
+        return;
+    }
     int64_t s, c, lo, hi, last;
     chunk_bounds(g, ch, s, c, lo, hi, last);
     const int W = (int)(g.C >> 5);
@@ -244,7 +253,44 @@ __global__ void k_fix(const double* __restrict__ v, ChunkGeom g, int64_t n_chunk
         }
     }
     E_out[ch] = r;
-    if (r != E_in[ch]) atomicExch(changed, 1);
+    const bool ch_ = r != E_in[ch];
+    if (dirty_out) dirty_out[ch] = ch_ ? 1 : 0;
+    if (ch_) atomicExch(changed, 1);
+}
+
+// Phase 2b (chains that merge late): one thread per segment walks its chunks
+// in order from the true entry -- the exact sequential fixed point, O(1) per
+// chunk whose entry is a speculative start or lies beyond it -- instead of
+// one more parallel round per chunk of the longest chain (config 5's long
+// pieces: ~50 rounds).
+__global__ void k_fix_walk(const double* __restrict__ v, ChunkGeom g, double tol2,
+                           int64_t max_len, const uint32_t* __restrict__ fb,
+                           const int64_t* __restrict__ exit_spec, int64_t* __restrict__ E) {
+    const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (s >= g.n_seg) return;
+    const int64_t c0 = g.chunk_off[s], c1 = g.chunk_off[s + 1];
+    if (c0 >= c1) return;
+    const int W = (int)(g.C >> 5);
+    int64_t t = exit_spec[c0];
+    E[c0] = t;
+    for (int64_t ch = c0 + 1; ch < c1; ++ch) {
+        int64_t ss, c, lo, hi, last;
+        chunk_bounds(g, ch, ss, c, lo, hi, last);
+        int64_t r;
+        if (t >= hi) {
+            r = t;
+        } else if (fbit(fb, ch, W, t - lo)) {
+            r = exit_spec[ch];
+        } else {
+            int64_t q = t;
+            do {
+                q = piece_end(v, q, last, tol2, max_len);
+            } while (q < hi && !fbit(fb, ch, W, q - lo));
+            r = q < hi ? exit_spec[ch] : q;
+        }
+        E[ch] = r;
+        t = r;
+    }
 }
 
 // Phase 3: rewrite each chunk's flags to the true orbit.
@@ -431,20 +477,31 @@ void compress_segments(const double* d_values, const SegTable& seg, double tol,
     JB_CUDA(cudaMemcpyAsync(Ea.p, exit_spec.p, sizeof(int64_t) * n_chunks,
                             cudaMemcpyDeviceToDevice, st));
     int iters = 0;
+    DArr<uint8_t> dirty_a(n_chunks, st), dirty_b(n_chunks, st);
     for (;;) {
         JB_CUDA(cudaMemsetAsync(dflag.p + 1, 0, sizeof(int), st));
         {
             JB_PROF("compress_fix", st);
             k_fix<<<nb, TB, 0, st>>>(d_values, g, n_chunks, tol2, max_piece_len, flags.p,
-                                 exit_spec.p, Ea.p, Eb.p, dflag.p + 1);
+                                 exit_spec.p, Ea.p, Eb.p, dflag.p + 1,
+                                 iters == 0 ? nullptr : dirty_a.p, dirty_b.p);
         }
         JB_LAUNCH_CHECK();
+        std::swap(dirty_a, dirty_b);
         ++iters;
         int ch;
         JB_CUDA(cudaMemcpyAsync(&ch, dflag.p + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
         JB_CUDA(cudaStreamSynchronize(st));
         std::swap(Ea, Eb);
         if (!ch) break;
+        if (iters == 2) {  // still moving: walk the segments sequentially (exact)
+            JB_PROF("compress_fix", st);
+            k_fix_walk<<<ceil_div(n_seg, 128), 128, 0, st>>>(d_values, g, tol2, max_piece_len,
+                                                              flags.p, exit_spec.p, Ea.p);
+            JB_LAUNCH_CHECK();
+            ++iters;
+            break;
+        }
     }
     if (n_fix_iters) *n_fix_iters = iters;
     {

@@ -83,37 +83,69 @@ __global__ void k_sum_inc(const double* __restrict__ inc, int64_t n, int E,
     if (threadIdx.x == 0) fx_atomic_add(acc, s);
 }
 
-// var_len / var_inc accumulations of scale_pieces (digitization.hpp:39-45)
-__global__ void k_sum_var(const int32_t* __restrict__ len, const double* __restrict__ inc,
-                          int64_t n, double mean_len, double mean_inc, int El, int Ei,
-                          unsigned long long* __restrict__ acc) {
-    i128 sl = 0, si = 0;
-    constexpr int U = 4;
-    for (int64_t b = blockIdx.x * (int64_t)kTB * U + threadIdx.x; b < n;
-         b += (int64_t)gridDim.x * kTB * U) {
-        int32_t L[U];
-        double I[U];
+// scale_pieces' second pass (digitization.hpp:39-45): var_inc as an exact
+// fixed-point sum, and var_len's range histogram (seqsum.cu: ranges of
+// VB_R pieces, counts per length <= RH, longer pieces listed) from which the
+// reference's sequential var_len is reproduced bit for bit. Warp per range.
+constexpr int VB_R = 2048;
+
+__global__ void __launch_bounds__(256) k_var_blocks(
+    const int32_t* __restrict__ len, const double* __restrict__ inc, int64_t n, double mean_len,
+    double mean_inc, int Ei, unsigned long long* __restrict__ acc, uint16_t* __restrict__ hist,
+    double* __restrict__ lx, uint32_t* __restrict__ long_idx,
+    unsigned long long* __restrict__ long_n, int RH) {
+    __shared__ uint32_t sh[8][64];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t nr = (n + VB_R - 1) / VB_R;
+    i128 si = 0;
+    for (int64_t r = (int64_t)blockIdx.x * 8 + w; r < nr; r += (int64_t)gridDim.x * 8) {
+        for (int l = lane; l < RH; l += 32) sh[w][l] = 0;
+        __syncwarp();
+        double lsum = 0.0;
+        const int64_t i0 = r * VB_R, i1 = min(i0 + VB_R, n);
+        for (int64_t c = i0; c < i1; c += 32 * 8) {
+            int32_t L[8];
+            double I[8];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t i = b + (int64_t)u * kTB;
-            L[u] = i < n ? len[i] : 0;
-            I[u] = i < n ? inc[i] : 0.0;
-        }
+            for (int u = 0; u < 8; ++u) {
+                const int64_t i = c + u * 32 + lane;
+                L[u] = i < i1 ? len[i] : 0;
+                I[u] = i < i1 ? inc[i] : 0.0;
+            }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if (b + (int64_t)u * kTB >= n) break;
-            const double dl = (double)L[u] - mean_len;  // digitization.hpp:41-44
-            const double di = I[u] - mean_inc;
-            sl += fx_from_double(dl * dl, El);
-            si += fx_from_double(di * di, Ei);
+            for (int u = 0; u < 8; ++u) {
+                const int64_t i = c + u * 32 + lane;
+                const bool v = i < i1;
+                if (v) {
+                    const double di = I[u] - mean_inc;  // digitization.hpp:42,44
+                    si += fx_from_double(di * di, Ei);
+                }
+                const int l = L[u];
+                const bool in = v && l >= 1 && l <= RH;
+                const unsigned grp = __match_any_sync(0xffffffffu, in ? l : -1);
+                if (in && (__ffs(grp) - 1) == lane) atomicAdd(&sh[w][l - 1], (uint32_t)__popc(grp));
+                const bool lg = v && !in;
+                const unsigned lm = __ballot_sync(0xffffffffu, lg);
+                if (lm) {
+                    unsigned long long b = 0;
+                    if (lane == __ffs(lm) - 1) b = atomicAdd(long_n, (unsigned long long)__popc(lm));
+                    b = __shfl_sync(0xffffffffu, b, __ffs(lm) - 1);
+                    if (lg) {
+                        long_idx[b + __popc(lm & ((1u << lane) - 1u))] = (uint32_t)i;
+                        const double dl = (double)l - mean_len;
+                        lsum += dl * dl;
+                    }
+                }
+            }
         }
+        __syncwarp();
+        for (int l = lane; l < RH; l += 32) hist[r * RH + l] = (uint16_t)sh[w][l];
+        for (int o = 16; o; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+        if (lane == 0) lx[r] = lsum;
+        __syncwarp();
     }
-    sl = block_sum_i128<kTB>(sl);
-    si = block_sum_i128<kTB>(si);
-    if (threadIdx.x == 0) {
-        fx_atomic_add(acc, sl);
-        fx_atomic_add(acc + 2, si);
-    }
+    si = block_sum_i128<256>(si);
+    if (threadIdx.x == 0) fx_atomic_add(acc + 2, si);
 }
 
 // ScalingParams::apply (core.hpp:130-132): materialised points (GA only)
@@ -178,15 +210,18 @@ void scale_pieces(const Pieces& pc, int64_t total_steps, double scl, Scaled& out
     const double mean_len = (double)total_steps / n;
     const double mean_inc = fx_to_double(fx_load(h.data()), Einc) / n;
 
-    const double dlmax = std::max((double)max_len - mean_len, mean_len - 1.0) + 1.0;
     const double dimax = max_abs_inc + std::fabs(mean_inc) + 1e-300;
-    const int El = fx_exponent_for(dlmax * dlmax * n * 1.001 + 1e-300);
     const int Ei = fx_exponent_for(dimax * dimax * n * 1.001 + 1e-300);
     acc.zero();
+    RangeHist vh;  // var_len's range histogram (seqsum.cu)
+    const int RH = (int)std::min<int32_t>(std::max<int32_t>(pc.max_len, 1), 64);
+    vh.alloc(pc.N, VB_R, 1, RH, pc.max_len > RH, st);
     if (pc.N > 0) {
-        JB_PROF("scale_sum_var", st);  // var_inc (var_len: exact sequential below)
-        k_sum_var<<<grid_for(pc.N), kTB, 0, st>>>(pc.len.p, pc.inc.p, pc.N, mean_len, mean_inc, El,
-                                                 Ei, acc.p);
+        JB_PROF("scale_sum_var", st);
+        const int64_t nr = vh.nr;
+        k_var_blocks<<<(int)std::max<int64_t>(1, std::min<int64_t>((nr + 7) / 8, (int64_t)kSMs * 8)),
+                       256, 0, st>>>(pc.len.p, pc.inc.p, pc.N, mean_len, mean_inc, Ei, acc.p,
+                                     vh.hist.p, vh.lx.p, vh.long_idx.p, vh.long_n.p, RH);
     }
     JB_LAUNCH_CHECK();
     h = acc.to_host(4);
@@ -199,7 +234,7 @@ void scale_pieces(const Pieces& pc, int64_t total_steps, double scl, Scaled& out
     vt.len = pc.len.p;
     vt.kind = SeqTerms::VAR_LEN;
     vt.a = mean_len;
-    const double var_len = seq_sum_nonneg(vt, {0, pc.N}, st, cm)[0];
+    const double var_len = range_seq_sums(vh, vt, nullptr, st, cm)[0];
     const double var_inc = fx_to_double(fx_load(h.data() + 2), Ei);
     double sl = N > 1 ? std::sqrt(var_len / (n - 1.0)) : 0.0;
     double si = N > 1 ? std::sqrt(var_inc / (n - 1.0)) : 0.0;
@@ -276,17 +311,30 @@ namespace {
 constexpr int AS_TB = 256, AS_U = 4;
 constexpr int kXRow = 64;
 
+// Per-range output of the group statistics (seqsum.cu RangeHist): per range
+// of R pieces (a multiple of AS_TB * AS_U) the (length, cluster) counts and
+// the long pieces' approximate x sums; long pieces listed. hist == null: none.
+struct RangeOut {
+    uint16_t* hist = nullptr;
+    double* lx = nullptr;
+    uint32_t* long_idx = nullptr;
+    unsigned long long* long_n = nullptr;
+    int64_t R = 1024;
+};
+
 __global__ void __launch_bounds__(AS_TB) k_assign_stats(
     const PtsView pv, const int32_t* __restrict__ len, int64_t n,
     const double* __restrict__ centers, int k, int do_assign, uint32_t* __restrict__ labels,
     int Ex, int Ey, unsigned long long Bx, unsigned long long By,
-    unsigned long long* __restrict__ gacc, CandGrid cg, RowGrid rg, int RH) {
+    unsigned long long* __restrict__ gacc, CandGrid cg, RowGrid rg, int RH, RangeOut ro) {
     // gacc layout: count(k) len(k) first(k) sx(2k) sy(2k), sums biased
     extern __shared__ unsigned long long smem64[];
     double* cx = reinterpret_cast<double*>(smem64);
     double* cy = cx + k;
     unsigned long long* yacc = smem64 + (do_assign ? 2 * k : 0);  // 3k limb totals
-    uint32_t* hist = reinterpret_cast<uint32_t*>(yacc + 3 * k);    // RH x k
+    unsigned long long* tot = yacc + 3 * k;                        // 4k: count, len, x (lo, hi)
+    double* lxr = reinterpret_cast<double*>(tot + 4 * k);          // k: this range's long x
+    uint32_t* hist = reinterpret_cast<uint32_t*>(lxr + k);         // RH x k (this range)
     uint32_t* ylimb = hist + (size_t)RH * k;                        // 3k
     uint32_t* first = ylimb + 3 * k;                                // k
     for (int c = threadIdx.x; c < k; c += AS_TB) {
@@ -295,6 +343,8 @@ __global__ void __launch_bounds__(AS_TB) k_assign_stats(
             cy[c] = centers[2 * c + 1];
         }
         yacc[c] = yacc[k + c] = yacc[2 * k + c] = 0;
+        tot[c] = tot[k + c] = tot[2 * k + c] = tot[3 * k + c] = 0;
+        lxr[c] = 0.0;
         ylimb[c] = ylimb[k + c] = ylimb[2 * k + c] = 0;
         first[c] = 0xFFFFFFFFu;
     }
@@ -310,80 +360,116 @@ __global__ void __launch_bounds__(AS_TB) k_assign_stats(
         }
         __syncthreads();
     };
-    const int64_t stride = (int64_t)gridDim.x * AS_TB * AS_U;
+    const int64_t R = ro.R, nr = (n + R - 1) / R;
     int round = 0;
-    for (int64_t base0 = blockIdx.x * (int64_t)AS_TB * AS_U; base0 < n; base0 += stride) {
-        const int64_t base = base0 + threadIdx.x;
-        double2 pp[AS_U];
-        int32_t ll[AS_U];
-        uint32_t lb[AS_U];
-#pragma unroll
-        for (int u = 0; u < AS_U; ++u) {
-            const int64_t i = base + (int64_t)u * AS_TB;
-            pp[u] = make_double2(0.0, 0.0);
-            ll[u] = 0;
-            lb[u] = 0;
-            if (i < n) {
-                ll[u] = len[i];
-                if (pv.pts) {
-                    pp[u] = pv.pts[i];
-                } else {  // x from len (k_scale's expression), y = inc / si
-                    pp[u].y = pv.inc[i];
-                }
-                if (!do_assign) lb[u] = labels[i];
-            }
-        }
-        if (!pv.pts) {
+    for (int64_t r = blockIdx.x; r < nr; r += gridDim.x) {
+        const int64_t rend = min(n, (r + 1) * R);
+        for (int64_t base0 = r * R; base0 < rend; base0 += (int64_t)AS_TB * AS_U) {
+            const int64_t base = base0 + threadIdx.x;
+            double2 pp[AS_U];
+            int32_t ll[AS_U];
+            uint32_t lb[AS_U];
 #pragma unroll
             for (int u = 0; u < AS_U; ++u) {
-                const int32_t l = ll[u];
-                pp[u] = make_double2(l >= 0 && l < kXRow ? s_xrow[l] : pv.scl * (double)l / pv.sl,
-                                     div_by(pp[u].y, pv.si, pv.rsi));
+                const int64_t i = base + (int64_t)u * AS_TB;
+                pp[u] = make_double2(0.0, 0.0);
+                ll[u] = 0;
+                lb[u] = 0;
+                if (i < rend) {
+                    ll[u] = len[i];
+                    if (pv.pts) {
+                        pp[u] = pv.pts[i];
+                    } else {  // x from len (k_scale's expression), y = inc / si
+                        pp[u].y = pv.inc[i];
+                    }
+                    if (!do_assign) lb[u] = labels[i];
+                }
             }
-        }
+            if (!pv.pts) {
 #pragma unroll
-        for (int u = 0; u < AS_U; ++u) {
-            const int64_t i = base + (int64_t)u * AS_TB;
-            if (i >= n) continue;
-            const double2 p = pp[u];
-            const int32_t l = ll[u];
-            uint32_t lab = lb[u];
-            if (do_assign) {
-                lab = row_nearest(rg, cg, l, p.x, p.y, cx, cy, k);
-                labels[i] = lab;
+                for (int u = 0; u < AS_U; ++u) {
+                    const int32_t l = ll[u];
+                    pp[u] = make_double2(l >= 0 && l < kXRow ? s_xrow[l] : pv.scl * (double)l / pv.sl,
+                                         div_by(pp[u].y, pv.si, pv.rsi));
+                }
             }
-            if ((uint32_t)i < first[lab]) atomicMin(first + lab, (uint32_t)i);
-            if (l >= 1 && l <= RH) {
-                atomicAdd(hist + (size_t)(l - 1) * k + lab, 1u);
-            } else {  // rare: long piece
-                atomicAdd(gacc + lab, 1ULL);
-                atomicAdd(gacc + k + lab, (unsigned long long)l);
-                fx_atomic_add_small(gacc + 3 * k + 2 * lab, (u128)(fx_from_double(p.x, Ex) + (i128)Bx));
+#pragma unroll
+            for (int u = 0; u < AS_U; ++u) {
+                const int64_t i = base + (int64_t)u * AS_TB;
+                const bool valid = i < rend;
+                const double2 p = pp[u];
+                const int32_t l = ll[u];
+                uint32_t lab = lb[u];
+                bool lg = false;
+                if (valid) {
+                    if (do_assign) {
+                        lab = row_nearest(rg, cg, l, p.x, p.y, cx, cy, k);
+                        labels[i] = lab;
+                    }
+                    if ((uint32_t)i < first[lab]) atomicMin(first + lab, (uint32_t)i);
+                    if (l >= 1 && l <= RH) {
+                        atomicAdd(hist + (size_t)(l - 1) * k + lab, 1u);
+                    } else {  // rare: long piece
+                        lg = true;
+                        atomicAdd(gacc + lab, 1ULL);
+                        atomicAdd(gacc + k + lab, (unsigned long long)l);
+                        fx_atomic_add_small(gacc + 3 * k + 2 * lab,
+                                            (u128)(fx_from_double(p.x, Ex) + (i128)Bx));
+                        if (ro.hist) atomicAdd(lxr + lab, p.x);
+                    }
+                    const unsigned long long yb = (unsigned long long)(fx_from_double(p.y, Ey) + (i128)By);
+                    atomicAdd(ylimb + lab, (uint32_t)(yb & 0x1FFFFFu));
+                    atomicAdd(ylimb + k + lab, (uint32_t)((yb >> 21) & 0x1FFFFFu));
+                    atomicAdd(ylimb + 2 * k + lab, (uint32_t)(yb >> 42));
+                }
+                if (ro.hist) {  // list the long pieces (one counter atomic per warp)
+                    const unsigned lm = __ballot_sync(0xffffffffu, lg);
+                    if (lm) {
+                        const int lane = threadIdx.x & 31;
+                        unsigned long long b = 0;
+                        if (lane == __ffs(lm) - 1) b = atomicAdd(ro.long_n, (unsigned long long)__popc(lm));
+                        b = __shfl_sync(0xffffffffu, b, __ffs(lm) - 1);
+                        if (lg) ro.long_idx[b + __popc(lm & ((1u << lane) - 1u))] = (uint32_t)i;
+                    }
+                }
             }
-            const unsigned long long yb = (unsigned long long)(fx_from_double(p.y, Ey) + (i128)By);
-            atomicAdd(ylimb + lab, (uint32_t)(yb & 0x1FFFFFu));
-            atomicAdd(ylimb + k + lab, (uint32_t)((yb >> 21) & 0x1FFFFFu));
-            atomicAdd(ylimb + 2 * k + lab, (uint32_t)(yb >> 42));
+            if (++round & 1) continue;
+            fold();
         }
-        if (++round & 1) continue;
-        fold();
+        // end of range r: fold its counts into the block totals, write its record
+        __syncthreads();
+        for (int c = threadIdx.x; c < k; c += AS_TB) {
+            unsigned long long cnt = 0, ls = 0;
+            u128 sx = 0;
+            for (int l = 1; l <= RH; ++l) {
+                const uint32_t h = hist[(size_t)(l - 1) * k + c];
+                if (!h) continue;
+                cnt += h;
+                ls += (unsigned long long)h * (unsigned long long)l;
+                const u128 xb = (u128)(fx_from_double(row_x(rg, l), Ex) + (i128)Bx);
+                sx += xb * (u128)h;
+            }
+            tot[c] += cnt;
+            tot[k + c] += ls;
+            const u128 t0 = ((u128)tot[3 * k + c] << 64 | tot[2 * k + c]) + sx;
+            tot[2 * k + c] = (unsigned long long)t0;
+            tot[3 * k + c] = (unsigned long long)(t0 >> 64);
+            if (ro.hist) ro.lx[r * k + c] = lxr[c];
+            lxr[c] = 0.0;
+        }
+        __syncthreads();
+        for (int j = threadIdx.x; j < RH * k; j += AS_TB) {
+            if (ro.hist) ro.hist[r * RH * k + j] = (uint16_t)hist[j];
+            hist[j] = 0;
+        }
+        __syncthreads();
     }
     fold();
     for (int c = threadIdx.x; c < k; c += AS_TB) {
-        unsigned long long cnt = 0, ls = 0;
-        u128 sx = 0;
-        for (int l = 1; l <= RH; ++l) {
-            const uint32_t h = hist[(size_t)(l - 1) * k + c];
-            if (!h) continue;
-            cnt += h;
-            ls += (unsigned long long)h * (unsigned long long)l;
-            const u128 xb = (u128)(fx_from_double(row_x(rg, l), Ex) + (i128)Bx);
-            sx += xb * (u128)h;
-        }
-        if (cnt) {
-            atomicAdd(gacc + c, cnt);
-            atomicAdd(gacc + k + c, ls);
-            fx_atomic_add(gacc + 3 * k + 2 * c, (i128)sx);
+        if (tot[c]) {
+            atomicAdd(gacc + c, tot[c]);
+            atomicAdd(gacc + k + c, tot[k + c]);
+            fx_atomic_add(gacc + 3 * k + 2 * c, (i128)(((u128)tot[3 * k + c] << 64) | tot[2 * k + c]));
         }
         const u128 sy = (u128)yacc[c] + ((u128)yacc[k + c] << 21) + ((u128)yacc[2 * k + c] << 42);
         if (sy) fx_atomic_add(gacc + 5 * k + 2 * c, (i128)sy);
@@ -460,7 +546,7 @@ void assign_and_stats(const PtsView& pv, const int32_t* d_len, int64_t n,
                       const std::vector<double>& centers, uint64_t k, const BBox& bb,
                       bool do_assign, uint32_t* d_labels, GroupStats& gs, cudaStream_t st,
                       int32_t max_len, double scl, double sigma_len, const Comm* cm,
-                      int64_t first_base) {
+                      int64_t first_base, RangeHist* rh) {
     DArr<double> dc(std::max<uint64_t>(2 * k, 1), st);
     if (centers.size() >= 2 * k) dc.upload(centers.data(), 2 * k);  // GA: no centers needed
     else if (do_assign) throw Error(INTERNAL, "assignment without centers");
@@ -482,11 +568,11 @@ void assign_and_stats(const PtsView& pv, const int32_t* d_len, int64_t n,
     if (k > 2048 && do_assign)
         throw Error(INVALID_INPUT, "k > 2048 is not supported by the assignment kernel");
     // histogram rows: piece lengths 1..RH (longer pieces take the global path)
-    int64_t rh = std::min<int64_t>(std::max<int32_t>(max_len, 1), 64);
-    rh = std::min<int64_t>(rh, std::max<int64_t>(1, 8192 / (int64_t)std::max<uint64_t>(k, 1)));
-    const int RH = (int)rh;
-    const size_t smem = (do_assign ? sizeof(double) * 2 * k : 0) + sizeof(unsigned long long) * 3 * k +
-                        sizeof(uint32_t) * ((size_t)RH * k + 4 * k);
+    int64_t rh_ = std::min<int64_t>(std::max<int32_t>(max_len, 1), 64);
+    rh_ = std::min<int64_t>(rh_, std::max<int64_t>(1, 8192 / (int64_t)std::max<uint64_t>(k, 1)));
+    const int RH = (int)rh_;
+    const size_t smem = (do_assign ? sizeof(double) * 2 * k : 0) + sizeof(unsigned long long) * 7 * k +
+                        sizeof(double) * k + sizeof(uint32_t) * ((size_t)RH * k + 4 * k);
     if (k <= 2048)
         JB_CUDA(cudaFuncSetAttribute(k_assign_stats, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)std::max<size_t>(smem, 1)));
@@ -494,6 +580,7 @@ void assign_and_stats(const PtsView& pv, const int32_t* d_len, int64_t n,
     CandGrid cg{};
     DArr<uint16_t> cg_cnt, cg_cand;
     DArr<uint64_t> rg_cell;
+    DArr<uint16_t> rg_spill;
     if (do_assign) {
         // exact candidate grids over the points' bounding box (jb_grid.cuh,
         // jb_rowgrid.cuh): rows for short pieces, 2-D for the rest
@@ -505,6 +592,8 @@ void assign_and_stats(const PtsView& pv, const int32_t* d_len, int64_t n,
         cg.cand = cg_cand.p;
         rg_cell.alloc((size_t)rg.R * rg.Gy, st);
         rg.cell = rg_cell.p;
+        rg_spill.alloc((size_t)rg.R * rg.Gy * kSpill, st);
+        rg.spill = rg_spill.p;
         JB_PROF("assign_grid", st);
         launch_grid_build(cg, dc.p, (int)k, st);
         JB_LAUNCH_CHECK();
@@ -525,11 +614,24 @@ void assign_and_stats(const PtsView& pv, const int32_t* d_len, int64_t n,
     const int grid = (int)std::max<int64_t>(
         1, std::min<int64_t>((n + AS_TB * AS_U - 1) / (AS_TB * AS_U),
                              (int64_t)kSMs * std::max(per_sm, 1)));
+    // ranges: about one per block, at most 32768 pieces (u16 counts), a
+    // multiple of the 1024-piece chunk
+    constexpr int64_t kChunk = (int64_t)AS_TB * AS_U;
+    const int64_t R = std::min<int64_t>(32768, std::max<int64_t>(kChunk, (n / grid) / kChunk * kChunk));
+    RangeOut ro;
+    ro.R = R;
+    if (rh) {
+        rh->alloc(n, R, (int)k, RH, max_len > RH, st);
+        ro.hist = rh->hist.p;
+        ro.lx = rh->lx.p;
+        ro.long_idx = rh->long_idx.p;
+        ro.long_n = rh->long_n.p;
+    }
     if (n > 0) {
         JB_PROF("assign_stats", st);
         k_assign_stats<<<grid, AS_TB, smem, st>>>(pv, d_len, n,
                                                   dc.p, (int)k, do_assign ? 1 : 0, d_labels, Ex, Ey,
-                                                  Bx, By, acc.p, cg, rg, RH);
+                                                  Bx, By, acc.p, cg, rg, RH, ro);
     }
     JB_LAUNCH_CHECK();
     }

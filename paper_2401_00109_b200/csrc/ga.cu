@@ -1,20 +1,21 @@
 // ga.cu — greedy aggregation (clustering.hpp:292-375) on sm_100a.
 //
-// The reference sweep visits points in stable key order; an unassigned point
-// becomes a starting point and claims every unassigned later point inside its
-// key window (early stop on key gap > alpha) within distance alpha. Equivalently
-// (the lexicographically-first maximal independent set in sorted order):
-//   * the earlier neighbours of sorted position j form N-(j) = {i in [lo(j), j):
-//     dist2(p_i, p_j) <= alpha^2}, where lo(j) is the first i whose window
-//     reaches j (windows are monotone in i because keys are sorted);
-//   * j is claimed by the FIRST starting point in N-(j); j is a starting point
-//     iff N-(j) holds none.
-// Each round, every undecided j scans N-(j) in order from where it last
-// stopped, skipping claimed neighbours: a start decides it (claimed), an
-// undecided neighbour suspends it, reaching j makes it a start. Decisions are
-// final, so rounds repeat until none is undecided; the result is exactly the
-// sequential sweep's. Keys are sorted with a stable CUB radix sort on
-// (key, index), matching std::stable_sort (:335-338).
+// The reference sweeps points in stable key order: an unassigned point
+// becomes a starting point and claims every unassigned later point of its key
+// window (early stop on key gap > alpha) within distance alpha. The sweep is
+// reproduced exactly in BATCHES of starts by one cooperative kernel:
+//   A. (one block) the next GA_M unassigned points in key order are the
+//      candidates; every earlier point is decided, so a candidate is a start
+//      iff no earlier candidate that is a start claims it (window and
+//      distance test). Their GA_M x GA_M adjacency bits are built in parallel
+//      and resolved by one sequential pass over the bitmasks.
+//   B. (whole grid) every new start claims the unassigned points of its
+//      window within alpha; a point reached by several takes the FIRST start
+//      (atomicMin on the sorted position), exactly as the sequential sweep.
+// Work is the sequential sweep's (the starts' windows) plus the candidates'
+// pairwise tests; a batch costs two grid barriers. Keys are sorted with a
+// stable CUB radix sort on (key, index), matching std::stable_sort (:335-338).
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <cmath>
@@ -108,57 +109,147 @@ __global__ void k_windows(const double2* __restrict__ pts, const unsigned long l
     }
 }
 
-// lo(j) = first i with wend[i] > j (wend is non-decreasing)
-__global__ void k_lo(const int64_t* __restrict__ wend, int64_t n, int64_t* __restrict__ resume) {
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
-         j += (int64_t)gridDim.x * blockDim.x) {
-        int64_t a = 0, b = j;
-        while (a < b) {
-            const int64_t m = (a + b) >> 1;
-            if (wend[m] > j) b = m;
-            else a = m + 1;
+constexpr int GA_M = 256;  // candidates per batch (= block size of the sweep)
+constexpr unsigned long long kNoOwner = ~0ULL;
+
+struct GaSweep {
+    const double2* spt;
+    const int64_t* wend;
+    int64_t n;
+    double alpha2;
+    uint8_t* status;             // 0 unassigned, 1 start, 2 claimed
+    unsigned long long* owner;   // claiming start (sorted position), kNoOwner: none yet
+    int64_t* real;               // GA_M: the batch's starts
+    int64_t* wpre;               // GA_M + 1: prefix of their window sizes
+    int* ctl;                    // [0] done, [1] starts in this batch, [2] batches
+    int64_t* cursor;             // every position before it is decided
+};
+
+__device__ void ga_phase_a(const GaSweep& a) {
+    __shared__ int64_t cand[GA_M];
+    __shared__ uint32_t adj[GA_M][GA_M / 32];
+    __shared__ int wcnt[GA_M / 32];
+    __shared__ int s_m, s_nreal;
+    __shared__ int64_t s_real[GA_M], s_pre[GA_M + 1];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    if (t == 0) s_m = 0;
+    __syncthreads();
+    int64_t p0 = *a.cursor;
+    // the next GA_M unassigned points in key order (those the last claims
+    // reached are decided: marked here)
+    while (s_m < GA_M && p0 < a.n) {
+        const int64_t p = p0 + t;
+        bool c = false;
+        if (p < a.n && a.status[p] == 0) {
+            if (a.owner[p] != kNoOwner) a.status[p] = 2;
+            else c = true;
         }
-        resume[j] = a;
+        const unsigned m = __ballot_sync(0xffffffffu, c);
+        if (lane == 0) wcnt[w] = __popc(m);
+        __syncthreads();
+        int off = s_m;
+        for (int q = 0; q < w; ++q) off += wcnt[q];
+        off += __popc(m & ((1u << lane) - 1u));
+        if (c && off < GA_M) cand[off] = p;
+        __syncthreads();
+        if (t == 0) {
+            int tot = s_m;
+            for (int q = 0; q < GA_M / 32; ++q) tot += wcnt[q];
+            s_m = tot < GA_M ? tot : GA_M;
+        }
+        p0 += GA_M;
+        __syncthreads();
+    }
+    const int m = s_m;
+    if (m == 0) {
+        if (t == 0) a.ctl[0] = 1;
+        return;
+    }
+    // row t: the earlier candidates whose start would claim cand[t]
+    for (int q = 0; q < GA_M / 32; ++q) adj[t][q] = 0u;
+    if (t < m) {
+        const int64_t j = cand[t];
+        const double2 pj = a.spt[j];
+        for (int i = 0; i < t; ++i) {
+            const int64_t ci = cand[i];
+            if (j < a.wend[ci]) {
+                const double2 pi = a.spt[ci];
+                if (dist2(pi.x, pi.y, pj.x, pj.y) <= a.alpha2) adj[t][i >> 5] |= 1u << (i & 31);
+            }
+        }
+    }
+    __syncthreads();
+    if (t == 0) {  // in order: a start unless an earlier start claims it
+        uint32_t realm[GA_M / 32];
+        for (int q = 0; q < GA_M / 32; ++q) realm[q] = 0u;
+        int nr = 0;
+        for (int c = 0; c < m; ++c) {
+            int first = -1;
+            for (int q = 0; q < GA_M / 32 && first < 0; ++q) {
+                const uint32_t hit = adj[c][q] & realm[q];
+                if (hit) first = 32 * q + __ffs(hit) - 1;
+            }
+            const int64_t j = cand[c];
+            if (first < 0) {
+                realm[c >> 5] |= 1u << (c & 31);
+                a.status[j] = 1;
+                a.owner[j] = (unsigned long long)j;
+                s_real[nr++] = j;
+            } else {
+                a.status[j] = 2;
+                a.owner[j] = (unsigned long long)cand[first];
+            }
+        }
+        s_nreal = nr;
+        s_pre[0] = 0;
+        for (int r = 0; r < nr; ++r) s_pre[r + 1] = s_pre[r] + (a.wend[s_real[r]] - s_real[r] - 1);
+        *a.cursor = cand[m - 1] + 1;
+        a.ctl[1] = nr;
+        a.ctl[2] += 1;
+    }
+    __syncthreads();
+    for (int r = t; r < s_nreal; r += GA_M) a.real[r] = s_real[r];
+    for (int r = t; r <= s_nreal; r += GA_M) a.wpre[r] = s_pre[r];
+}
+
+// every new start claims the unassigned points of its window within alpha
+__device__ void ga_phase_b(const GaSweep& a) {
+    const int nr = ((volatile int*)a.ctl)[1];
+    const int64_t total = ((volatile int64_t*)a.wpre)[nr];
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        int lo = 0, hi = nr;  // the start whose window slice holds q
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (((volatile int64_t*)a.wpre)[mid] <= q) lo = mid;
+            else hi = mid;
+        }
+        const int64_t s = ((volatile int64_t*)a.real)[lo];
+        const int64_t j = s + 1 + (q - ((volatile int64_t*)a.wpre)[lo]);
+        if (((volatile uint8_t*)a.status)[j] != 0) continue;
+        const double2 ps = a.spt[s], pj = a.spt[j];
+        if (dist2(ps.x, ps.y, pj.x, pj.y) <= a.alpha2)
+            atomicMin(a.owner + j, (unsigned long long)s);  // the first start claims it
     }
 }
 
-// status: 0 undecided, 1 starting point, 2 claimed (owner = claiming start)
-__global__ void k_round(const double2* __restrict__ spt, int64_t n, double alpha2,
-                        const int64_t* __restrict__ list, int64_t n_list,
-                        uint8_t* __restrict__ status, int64_t* __restrict__ resume,
-                        int64_t* __restrict__ owner, unsigned long long* __restrict__ pending) {
-    unsigned long long my_pending = 0;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_list;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t j = list ? list[t] : t;
-        if (*(volatile const uint8_t*)(status + j)) continue;
-        const double2 pj = spt[j];
-        int64_t i = resume[j];
-        int decided = 0;
-        for (; i < j; ++i) {
-            const double2 pi = spt[i];
-            if (dist2(pi.x, pi.y, pj.x, pj.y) <= alpha2) {
-                const uint8_t si = *(volatile const uint8_t*)(status + i);
-                if (si == 0) break;  // wait for i
-                if (si == 1) {
-                    owner[j] = i;
-                    decided = 2;
-                    break;
-                }
-            }
-        }
-        if (!decided && i == j) decided = 1;
-        if (decided) {
-            if (decided == 1) owner[j] = j;
-            __threadfence();
-            *(volatile uint8_t*)(status + j) = (uint8_t)decided;
-        } else {
-            resume[j] = i;
-            ++my_pending;
-        }
+__global__ void __launch_bounds__(GA_M) k_ga_sweep(GaSweep a) {
+    namespace cgx = cooperative_groups;
+    cgx::grid_group grid = cgx::this_grid();
+    for (;;) {
+        if (blockIdx.x == 0) ga_phase_a(a);
+        grid.sync();
+        if (((volatile int*)a.ctl)[0]) break;
+        ga_phase_b(a);
+        grid.sync();
     }
-    for (int o = 16; o > 0; o >>= 1) my_pending += __shfl_down_sync(0xffffffffu, my_pending, o);
-    if ((threadIdx.x & 31) == 0 && my_pending) atomicAdd(pending, my_pending);
+}
+
+__global__ void k_ga_finish(uint8_t* __restrict__ status,
+                            const unsigned long long* __restrict__ owner, int64_t n) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+         j += (int64_t)gridDim.x * blockDim.x)
+        if (status[j] == 0 && owner[j] != kNoOwner) status[j] = 2;
 }
 
 __global__ void k_start_flags(const uint8_t* __restrict__ status, int64_t n,
@@ -168,22 +259,13 @@ __global__ void k_start_flags(const uint8_t* __restrict__ status, int64_t n,
         is_start[j] = status[j] == 1 ? 1 : 0;
 }
 
-__global__ void k_ga_labels(const int64_t* __restrict__ owner, const int64_t* __restrict__ gid,
+__global__ void k_ga_labels(const unsigned long long* __restrict__ owner,
+                            const int64_t* __restrict__ gid,
                             const uint32_t* __restrict__ sidx, int64_t n,
                             uint32_t* __restrict__ labels) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
          j += (int64_t)gridDim.x * blockDim.x)
         labels[sidx[j]] = (uint32_t)gid[owner[j]];
-}
-
-__global__ void k_compact_pending(const uint8_t* __restrict__ status,
-                                  const int64_t* __restrict__ list, int64_t n_list,
-                                  int64_t* __restrict__ out, unsigned long long* __restrict__ cnt) {
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_list;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t j = list ? list[t] : t;
-        if (status[j] == 0) out[atomicAdd(cnt, 1ULL)] = j;
-    }
 }
 
 int gcap(int64_t n) {
@@ -244,48 +326,39 @@ void greedy_aggregate_device(const double* d_pts, int64_t n, double alpha, int s
     }
     DArr<double2> spt(n, st);
     DArr<double> skey(n, st);
-    DArr<int64_t> wend(n, st), resume(n, st), owner(n, st);
+    DArr<int64_t> wend(n, st);
+    DArr<unsigned long long> owner(n, st);
     {
         JB_PROF("ga_windows", st);
         k_windows<<<gcap(n), 256, 0, st>>>(pts, skb.p, sidx.p, n, alpha, early_stop ? 1 : 0, spt.p,
                                        skey.p, wend.p);
     }
     JB_LAUNCH_CHECK();
-    k_lo<<<gcap(n), 256, 0, st>>>(wend.p, n, resume.p);
-    JB_LAUNCH_CHECK();
     DArr<uint8_t> status(n, st);
     status.zero();
-    DArr<unsigned long long> pend(2, st);
-    DArr<int64_t> listA(n, st), listB(n, st);
-    int64_t* list = nullptr;  // nullptr = all positions
-    int64_t n_list = n;
-    int rounds = 0;
-    for (;;) {
-        pend.zero();
-        {
-            JB_PROF("ga_round", st);
-            k_round<<<gcap(n_list), 256, 0, st>>>(spt.p, n, alpha2, list, n_list, status.p,
-                                              resume.p, owner.p, pend.p);
-        }
-        JB_LAUNCH_CHECK();
-        ++rounds;
-        unsigned long long p = 0;
-        pend.download(&p, 1);
-        JB_CUDA(cudaStreamSynchronize(st));
-        if (p == 0) break;
-        if ((int64_t)p * 4 < n_list) {  // shrink the work list
-            int64_t* dst = (list == listA.p) ? listB.p : listA.p;
-            JB_CUDA(cudaMemsetAsync(pend.p + 1, 0, 8, st));
-            k_compact_pending<<<gcap(n_list), 256, 0, st>>>(status.p, list, n_list, dst,
-                                                            pend.p + 1);
-            JB_LAUNCH_CHECK();
-            unsigned long long c = 0;
-            JB_CUDA(cudaMemcpyAsync(&c, pend.p + 1, 8, cudaMemcpyDeviceToHost, st));
-            JB_CUDA(cudaStreamSynchronize(st));
-            list = dst;
-            n_list = (int64_t)c;
-        }
+    JB_CUDA(cudaMemsetAsync(owner.p, 0xFF, sizeof(unsigned long long) * n, st));
+    DArr<int64_t> real(GA_M, st), wpre(GA_M + 1, st), cursor(1, st);
+    DArr<int> ctl(3, st);
+    ctl.zero();
+    cursor.zero();
+    GaSweep a{spt.p, wend.p, n, alpha2, status.p, owner.p, real.p, wpre.p, ctl.p, cursor.p};
+    int per_sm = 0;
+    JB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ga_sweep, GA_M, 0));
+    if (per_sm < 1) throw Error(INTERNAL, "greedy_aggregate: sweep kernel does not fit");
+    void* args[] = {&a};
+    {
+        JB_PROF("ga_sweep", st);
+        JB_CUDA(cudaLaunchCooperativeKernel((const void*)k_ga_sweep,
+                                            dim3(kSMs * std::min(per_sm, 2)), dim3(GA_M), args, 0,
+                                            st));
     }
+    JB_LAUNCH_CHECK();
+    k_ga_finish<<<gcap(n), 256, 0, st>>>(status.p, owner.p, n);
+    JB_LAUNCH_CHECK();
+    int hctl[3];
+    ctl.download(hctl, 3);
+    JB_CUDA(cudaStreamSynchronize(st));
+    const int rounds = hctl[2];
     // group ids in sorted order of their starting points
     DArr<int64_t> flg(n + 1, st), gid(n + 1, st);
     k_start_flags<<<gcap(n), 256, 0, st>>>(status.p, n, flg.p);

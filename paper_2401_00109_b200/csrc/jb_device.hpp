@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <algorithm>
 #include <cstdlib>
 #include <utility>
 #include <vector>
@@ -247,6 +248,42 @@ struct SeqSum {
     std::vector<double> resolve(const std::vector<double>& s_in);
 };
 
+// Range-histogram input of an exact sum whose terms are a function of the
+// piece length (seqsum.cu): for every range r of R consecutive pieces, the
+// pieces of group g with length l in 1..RH are counted in
+// hist[(r * RH + l - 1) * k + g]; longer pieces are listed (long_idx, any
+// order) and their terms' approximate sums kept in lx[r * k + g]. k == 1:
+// every piece is in the one group. Written by the producer kernels
+// (k_var_blocks, k_assign_stats), consumed by range_seq_sums.
+struct RangeHist {
+    int64_t n = 0, R = 0, nr = 0;
+    int k = 1, RH = 0;
+    DArr<uint16_t> hist;
+    DArr<double> lx;
+    DArr<uint32_t> long_idx;
+    DArr<unsigned long long> long_n;
+    void alloc(int64_t n_, int64_t R_, int k_, int RH_, bool longs, cudaStream_t st) {
+        n = n_;
+        R = R_;
+        k = k_;
+        RH = RH_;
+        nr = (n + R - 1) / R;
+        hist.alloc(std::max<int64_t>(nr * RH * k, 1), st);
+        lx.alloc(std::max<int64_t>(nr * k, 1), st);
+        lx.zero();
+        long_n.alloc(1, st);
+        long_n.zero();
+        if (longs) long_idx.alloc(std::max<int64_t>(n, 1), st);
+        else long_idx.release();
+    }
+};
+
+// Exact sequential sums of the terms of every group's pieces in index order
+// (d_labels: group of each piece, null when k == 1); multi-GPU as below.
+std::vector<double> range_seq_sums(const RangeHist& h, const SeqTerms& t,
+                                   const uint32_t* d_labels, cudaStream_t st,
+                                   const Comm* cm = nullptr);
+
 // One call for all ranks (cm null or world 1: single GPU); rank r's terms of
 // segment g follow ranks 0..r-1's. Returns the exact sums from s = 0.
 std::vector<double> seq_sum_nonneg(const SeqTerms& t, const std::vector<int64_t>& seg_off,
@@ -324,7 +361,7 @@ void assign_and_stats(const PtsView& pv, const int32_t* d_len, int64_t n,
                       const std::vector<double>& centers, uint64_t k, const BBox& bb,
                       bool do_assign, uint32_t* d_labels, GroupStats& gs, cudaStream_t st,
                       int32_t max_len, double scl, double sigma_len, const Comm* cm = nullptr,
-                      int64_t first_base = 0);
+                      int64_t first_base = 0, RangeHist* rh = nullptr);
 
 // symbolize_with (digitization.hpp:297-307) on device: labels of held-out
 // pieces (len, inc) against a codebook (centers 2k, scaling scl/sl/si).

@@ -17,22 +17,30 @@
 
 namespace jb {
 
+constexpr uint64_t kRowSpill = 0xFFFDull;     // low half-word of a spilled cell (5..kSpill)
 constexpr uint64_t kRowOverflow = 0xFFFEull;  // low half-word of an overflowing cell
 constexpr uint64_t kRowEmpty = 0xFFFFull;     // unused candidate slot
+// A cell with 5..kSpill candidates keeps them in spill[cell * kSpill ..] and
+// its word holds (kRowSpill | count << 16 | cell << 32): dense clusters of
+// centers (config 5, k = 500 around the short rows) would otherwise send
+// whole cells to the all-centers fallback.
+constexpr int kSpill = 16;
 
 struct RowGrid {
     double y0, h, invh, mh;  // y cells (same inflation rule as CandGrid)
     double scl, sl;          // x_l = scl * (double)l / sl  (k_scale's expression)
     int R, Gy;               // lengths 1..R, Gy cells per length
     uint64_t* cell;          // R * Gy packed candidate words
+    uint16_t* spill;         // R * Gy * kSpill, or null (no spilling: overflow)
     double slack;            // build slack (jb_grid.cuh keep_threshold): valid while
                              // every center stays within slack / 2 of its build position
 };
 
 __host__ inline RowGrid make_row_grid_desc(double ymin, double ymax, double scl, double sl,
-                                           int32_t max_len, int64_t cell_budget) {
+                                           int32_t max_len, int64_t cell_budget,
+                                           int32_t max_rows = 256) {
     RowGrid g{};
-    g.R = (int)std::max<int64_t>(1, std::min<int64_t>(max_len, 256));
+    g.R = (int)std::max<int64_t>(1, std::min<int64_t>(max_len, max_rows));
     int64_t gy = 256;
     while (gy < 16384 && gy * 2 * g.R <= cell_budget) gy *= 2;
     g.Gy = (int)gy;
@@ -44,6 +52,7 @@ __host__ inline RowGrid make_row_grid_desc(double ymin, double ymax, double scl,
     g.scl = scl;
     g.sl = sl;
     g.cell = nullptr;
+    g.spill = nullptr;
     g.slack = 0.0;
     return g;
 }
@@ -75,11 +84,16 @@ __device__ __forceinline__ void row_grid_build_body(RowGrid g,
                          g.slack);
         const int iy = iy0 + (int)threadIdx.x;
         if (iy <= iy1) {
-            uint16_t tmp[4];
+            uint16_t tmp[kSpill];
             const int nc = thread_cell_candidates(centers, k, s, x, x, g.y0 + iy * g.h - g.mh,
-                                                  g.y0 + (iy + 1) * g.h + g.mh, tmp, 4, g.slack);
+                                                  g.y0 + (iy + 1) * g.h + g.mh, tmp, kSpill,
+                                                  g.slack);
+            const size_t cidx = (size_t)row * g.Gy + iy;
             uint64_t word;
-            if (nc > 4) {
+            if (nc > 4 && nc <= kSpill && g.spill) {
+                for (int j = 0; j < nc; ++j) g.spill[cidx * kSpill + j] = tmp[j];
+                word = kRowSpill | ((uint64_t)nc << 16) | ((uint64_t)cidx << 32);
+            } else if (nc > 4) {
                 word = (~0ull << 16) | kRowOverflow;
             } else {
                 word = ~0ull;
@@ -88,7 +102,7 @@ __device__ __forceinline__ void row_grid_build_body(RowGrid g,
                     word |= (uint64_t)tmp[j] << (16 * j);
                 }
             }
-            g.cell[(size_t)row * g.Gy + iy] = word;
+            g.cell[cidx] = word;
         }
         __syncthreads();
     }
@@ -128,10 +142,16 @@ static __global__ void k_row_occupancy(RowGrid g, const double2* __restrict__ pt
 }
 
 // nearest center from an already loaded row-cell word (~0: no row cell)
-__device__ __forceinline__ uint32_t row_pick(uint64_t w, const CandGrid& g, double px, double py,
-                                             const double* cx, const double* cy, int k) {
+__device__ __forceinline__ uint32_t row_nearest_w(const CandGrid& g, const uint16_t* spill,
+                                                  uint64_t w, double px, double py,
+                                                  const double* cx, const double* cy, int k);
+
+__device__ __forceinline__ uint32_t row_pick(uint64_t w, const CandGrid& g, const uint16_t* spill,
+                                             double px, double py, const double* cx,
+                                             const double* cy, int k) {
     const uint32_t c0 = (uint32_t)(w & 0xFFFF);
-    if (c0 < kRowOverflow) {
+    if (c0 == kRowSpill) return row_nearest_w(g, spill, w, px, py, cx, cy, k);
+    if (c0 < kRowSpill) {
         uint32_t best = c0;
         const uint32_t c1 = (uint32_t)((w >> 16) & 0xFFFF);
         if (c1 == kRowEmpty) return best;  // the only possible argmin
@@ -151,6 +171,20 @@ __device__ __forceinline__ uint32_t row_pick(uint64_t w, const CandGrid& g, doub
     return grid_nearest(g, px, py, cx, cy, k);
 }
 
+// candidates of a built cell word: 1..4 inline, 5..kSpill spilled, 0 otherwise
+__device__ __forceinline__ int row_word_count(uint64_t w) {
+    const uint64_t c0 = w & 0xFFFF;
+    if (c0 == kRowSpill) return (int)((w >> 16) & 0xFFFF);
+    if (c0 >= kRowOverflow) return 0;
+    int n = 1;
+    while (n < 4 && ((w >> (16 * n)) & 0xFFFF) != kRowEmpty) ++n;
+    return n;
+}
+__device__ __forceinline__ uint32_t row_word_cand(const uint16_t* spill, uint64_t w, int j) {
+    if ((w & 0xFFFF) == kRowSpill) return __ldg(spill + (size_t)(w >> 32) * kSpill + j);
+    return (uint32_t)((w >> (16 * j)) & 0xFFFF);
+}
+
 // the row-cell word of a piece of length len at y = py (~0: no row cell,
 // which row_nearest_w sends to the 2-D grid fallback)
 __device__ __forceinline__ uint64_t row_cell_word(const RowGrid& rg, int32_t len, double py) {
@@ -163,11 +197,26 @@ __device__ __forceinline__ uint64_t row_cell_word(const RowGrid& rg, int32_t len
 
 // nearest_center (clustering.hpp:146-157) of a piece at (px, py) whose row
 // cell word w was loaded ahead (row_cell_word)
-__device__ __forceinline__ uint32_t row_nearest_w(const CandGrid& g, uint64_t w, double px,
-                                                  double py, const double* cx, const double* cy,
-                                                  int k) {
+__device__ __forceinline__ uint32_t row_nearest_w(const CandGrid& g, const uint16_t* spill,
+                                                  uint64_t w, double px, double py,
+                                                  const double* cx, const double* cy, int k) {
     const uint32_t c0 = (uint32_t)(w & 0xFFFF);
-    if (c0 < kRowOverflow) {
+    if (c0 == kRowSpill) {
+        const uint16_t* sl = spill + (size_t)(w >> 32) * kSpill;
+        const int nc = (int)((w >> 16) & 0xFFFF);
+        uint32_t best = __ldg(sl);
+        double bd = dist2(px, py, cx[best], cy[best]);
+        for (int j = 1; j < nc; ++j) {
+            const uint32_t c = __ldg(sl + j);
+            const double d = dist2(px, py, cx[c], cy[c]);
+            if (d < bd) {
+                bd = d;
+                best = c;
+            }
+        }
+        return best;
+    }
+    if (c0 < kRowSpill) {
         uint32_t best = c0;
         const uint32_t c1 = (uint32_t)((w >> 16) & 0xFFFF);
         if (c1 == kRowEmpty) return best;  // the only possible argmin
@@ -191,7 +240,7 @@ __device__ __forceinline__ uint32_t row_nearest_w(const CandGrid& g, uint64_t w,
 __device__ __forceinline__ uint32_t row_nearest(const RowGrid& rg, const CandGrid& g, int32_t len,
                                                 double px, double py, const double* cx,
                                                 const double* cy, int k) {
-    return row_nearest_w(g, row_cell_word(rg, len, py), px, py, cx, cy, k);
+    return row_nearest_w(g, rg.spill, row_cell_word(rg, len, py), px, py, cx, cy, k);
 }
 
 }  // namespace jb

@@ -1054,14 +1054,12 @@ __device__ __forceinline__ bool row_tile_single(const RowGrid& rg, int l, const 
 #pragma unroll
     for (int j = 0; j < 8; ++j) wv[j] = j < nc ? __ldg(row + j) : ~0ull;
     double M = INFINITY;
-#pragma unroll
     for (int j = 0; j < 8; ++j) {
         if (j >= nc) break;
         if ((wv[j] & 0xFFFF) >= kRowOverflow) return false;  // overflow / not built
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint32_t c = (uint32_t)((wv[j] >> (16 * q)) & 0xFFFF);
-            if (c == kRowEmpty) break;
+        const int m = row_word_count(wv[j]);
+        for (int q = 0; q < m; ++q) {
+            const uint32_t c = row_word_cand(rg.spill, wv[j], q);
             double dmn, dmx;
             box_d2(centers[2 * c], centers[2 * c + 1], b, dmn, dmx);
             M = fmin(M, dmx);
@@ -1069,13 +1067,11 @@ __device__ __forceinline__ bool row_tile_single(const RowGrid& rg, int l, const 
     }
     const double thr = M * (1.0 + kKeepMargin) + 1e-300;
     uint32_t first = MIXED;
-#pragma unroll
     for (int j = 0; j < 8; ++j) {
         if (j >= nc) break;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint32_t c = (uint32_t)((wv[j] >> (16 * q)) & 0xFFFF);
-            if (c == kRowEmpty) break;
+        const int m = row_word_count(wv[j]);
+        for (int q = 0; q < m; ++q) {
+            const uint32_t c = row_word_cand(rg.spill, wv[j], q);
             double dmn, dmx;
             box_d2(centers[2 * c], centers[2 * c + 1], b, dmn, dmx);
             if (dmn <= thr) {
@@ -1164,18 +1160,15 @@ __device__ __forceinline__ uint32_t box_single_g8(const double4& b, int l, const
         wv = __ldg(reinterpret_cast<const unsigned long long*>(rg.cell) + (size_t)(l - 1) * rg.Gy +
                    iy0 + sub);
     bool bad = row && sub < nc && (wv & 0xFFFF) >= kRowOverflow;
-    double dmn[4];
     double M = INFINITY;
     int ncand = 0;
     if (row && sub < nc && !bad) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint32_t c = (uint32_t)((wv >> (16 * q)) & 0xFFFF);
-            if (c == kRowEmpty) break;
-            double dmx;
-            box_d2(centers[2 * c], centers[2 * c + 1], b, dmn[q], dmx);
+        ncand = row_word_count(wv);
+        for (int q = 0; q < ncand; ++q) {
+            const uint32_t c = row_word_cand(rg.spill, wv, q);
+            double dmn, dmx;
+            box_d2(centers[2 * c], centers[2 * c + 1], b, dmn, dmx);
             M = fmin(M, dmx);
-            ncand = q + 1;
         }
     }
 #pragma unroll
@@ -1185,11 +1178,11 @@ __device__ __forceinline__ uint32_t box_single_g8(const double4& b, int l, const
     }
     const double thr = M * (1.0 + kKeepMargin) + 1e-300;
     uint32_t cmin = MIXED, cmax = 0;  // passing candidates (cmax: c + 1)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        if (q >= ncand) break;
-        if (dmn[q] <= thr) {
-            const uint32_t c = (uint32_t)((wv >> (16 * q)) & 0xFFFF);
+    for (int q = 0; q < ncand; ++q) {
+        const uint32_t c = row_word_cand(rg.spill, wv, q);
+        double dmn, dmx;
+        box_d2(centers[2 * c], centers[2 * c + 1], b, dmn, dmx);
+        if (dmn <= thr) {
             cmin = min(cmin, c);
             cmax = max(cmax, c + 1);
         }
@@ -1418,7 +1411,7 @@ __device__ __forceinline__ void lloyd_work_body(
             const int64_t r = (int64_t)t * TILE + i * 32 + lane;
             bst[i] = single;
             if (r < n && single == MIXED)
-                bst[i] = slen ? row_pick(cw[i], g, pt[i].x, pt[i].y, cx, cy, k)
+                bst[i] = slen ? row_pick(cw[i], g, rg.spill, pt[i].x, pt[i].y, cx, cy, k)
                               : grid_nearest(g, pt[i].x, pt[i].y, cx, cy, k);
         }
         auto flush = [&](uint32_t kk, u128 sa, u128 sb, unsigned long long, int cnt) {
@@ -1720,6 +1713,7 @@ struct LloydCtx {
     DArr<unsigned long long> nwork, diag;
     RowGrid rg{};                   // rg.R == 0: no row grid
     DArr<uint64_t> rg_cell;
+    DArr<uint16_t> rg_spill;
     DArr<int> rg_blocks;            // row-grid segments holding points
     int rg_nblocks = 0;
     const int32_t* slen = nullptr;  // piece length per sorted point
@@ -2136,11 +2130,18 @@ void lloyd_best_device(const PtsView& pv, const uint64_t* d_idx, int64_t n, uint
         L.cg.cand = L.cg_cand.p;
     }
     if (rows.len) {  // exact row grid over the integer piece lengths (jb_rowgrid.cuh)
-        L.rg = make_row_grid_desc(bb.ymin, bb.ymax, rows.scl, rows.sl, rows.max_len, 1 << 16);
+        // every piece length up to 4096 gets a row (a length beyond the rows
+        // is compared with all k centers, every iteration); long rows hold
+        // few points, and only the occupied segments are ever built
+        const int32_t R = std::min<int32_t>(std::max<int32_t>(rows.max_len, 1), 4096);
+        const int64_t budget = std::min<int64_t>(1 << 23, std::max<int64_t>(1 << 16, (int64_t)R * 2048));
+        L.rg = make_row_grid_desc(bb.ymin, bb.ymax, rows.scl, rows.sl, rows.max_len, budget, 4096);
         static const double slack_h = getenv("JB_RG_SLACK") ? atof(getenv("JB_RG_SLACK")) : 4.0;
         L.rg.slack = slack_h * L.rg.h;  // persistent loop: rebuild only after slack / 2 of movement
         L.rg_cell.alloc((size_t)L.rg.R * L.rg.Gy, st);
         L.rg.cell = L.rg_cell.p;
+        L.rg_spill.alloc((size_t)L.rg.R * L.rg.Gy * kSpill, st);
+        L.rg.spill = L.rg_spill.p;
         L.slen = slen.p;
         L.tlen = tlen.p;
         // only segments holding points are rebuilt each iteration; the others
@@ -2826,9 +2827,13 @@ void lloyd_best_dist(const Comm& cm, const PtsView& pv, const uint64_t* d_lidx,
         L.cg.cand = L.cg_cand.p;
     }
     if (rows.len) {  // exact row grid over the integer piece lengths (jb_rowgrid.cuh)
-        L.rg = make_row_grid_desc(bb.ymin, bb.ymax, rows.scl, rows.sl, rows.max_len, 1 << 16);
+        const int32_t R = std::min<int32_t>(std::max<int32_t>(rows.max_len, 1), 4096);
+        const int64_t budget = std::min<int64_t>(1 << 23, std::max<int64_t>(1 << 16, (int64_t)R * 2048));
+        L.rg = make_row_grid_desc(bb.ymin, bb.ymax, rows.scl, rows.sl, rows.max_len, budget, 4096);
         L.rg_cell.alloc((size_t)L.rg.R * L.rg.Gy, st);
         L.rg.cell = L.rg_cell.p;
+        L.rg_spill.alloc((size_t)L.rg.R * L.rg.Gy * kSpill, st);
+        L.rg.spill = L.rg_spill.p;
         L.slen = slen.p;
         L.tlen = tlen.p;
         // only segments holding points are rebuilt each iteration; the others

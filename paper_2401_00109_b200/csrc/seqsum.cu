@@ -53,6 +53,15 @@ __device__ __forceinline__ Pair compose(Pair f, Pair g) {
     return r;
 }
 
+__device__ __forceinline__ double term_of_len(const SeqTerms& t, int32_t len) {
+    const double l = (double)len;
+    if (t.kind == SeqTerms::VAR_LEN) {
+        const double dl = l - t.a;  // digitization.hpp:41,43
+        return dl * dl;
+    }
+    return t.a * l / t.b;  // ScalingParams::apply core.hpp:131 (x)
+}
+
 __device__ __forceinline__ double term_at(const SeqTerms& t, int64_t i) {
     if (t.kind == SeqTerms::DIRECT) return t.w[i];
     const double l = (double)t.len[i];
@@ -222,7 +231,8 @@ __global__ void k_ss_pairs(SeqTerms t, SegDesc sd, int64_t nblk, const double* _
 
 // parents of 32 consecutive nodes: uniform iff all 32 children are uniform in
 // the same binade and segment
-__global__ void k_ss_level(int64_t nchild, const int* __restrict__ ce, const int* __restrict__ cseg,
+__global__ void k_ss_level(int64_t nchild, int64_t seg_div, const int* __restrict__ ce,
+                           const int* __restrict__ cseg,
                            const unsigned long long* __restrict__ cpe,
                            const unsigned long long* __restrict__ cpo, int64_t npar,
                            int* __restrict__ e_out, int* __restrict__ seg_out,
@@ -234,7 +244,7 @@ __global__ void k_ss_level(int64_t nchild, const int* __restrict__ ce, const int
     const int64_t c = p * 32 + lane;
     const bool have = c < nchild;
     const int e = have ? ce[c] : kNone;
-    const int sg = have ? cseg[c] : -1;
+    const int sg = have ? (cseg ? cseg[c] : (int)(c / seg_div)) : -1;
     Pair q = have ? Pair{cpe[c], cpo[c]} : Pair{0, 0};
     const int e0 = __shfl_sync(0xffffffffu, e, 0);
     const int s0 = __shfl_sync(0xffffffffu, sg, 0);
@@ -394,10 +404,10 @@ void SeqSum::predict(const std::vector<double>& s_in_approx, const std::vector<i
         k_ss_pairs<<<blocks_for_warps(nblk), 256, 0, st>>>(terms, sd, nblk, bsum.p, gpre.p, bseg.p,
                                                            sin_d.p, gb.p, be.p, pe.p, po.p);
         JB_LAUNCH_CHECK();
-        k_ss_level<<<blocks_for_warps(n2), 256, 0, st>>>(nblk, be.p, bseg.p, pe.p, po.p, n2, e2.p,
+        k_ss_level<<<blocks_for_warps(n2), 256, 0, st>>>(nblk, 1, be.p, bseg.p, pe.p, po.p, n2, e2.p,
                                                          s2.p, pe2.p, po2.p);
         JB_LAUNCH_CHECK();
-        k_ss_level<<<blocks_for_warps(n3), 256, 0, st>>>(n2, e2.p, s2.p, pe2.p, po2.p, n3, e3.p,
+        k_ss_level<<<blocks_for_warps(n3), 256, 0, st>>>(n2, 1, e2.p, s2.p, pe2.p, po2.p, n3, e3.p,
                                                          s3.p, pe3.p, po3.p);
         JB_LAUNCH_CHECK();
     }
@@ -454,6 +464,381 @@ std::vector<double> seq_sum_nonneg(const SeqTerms& t, const std::vector<int64_t>
         std::vector<double> mine = r == cm->rank ? ss.resolve(cur) : cur;
         std::vector<double> all = cm->gather(mine);
         std::copy(all.begin() + (size_t)r * n_seg, all.begin() + (size_t)(r + 1) * n_seg, cur.begin());
+    }
+    return cur;
+}
+
+
+// ---------------------------------------------------------------------------
+// Range-histogram form (no pass over the data of its own): the producer
+// kernel (scale's k_var_blocks for var_len, k_assign_stats for the group
+// sums) counts, for every range of R consecutive pieces, the pieces of each
+// group by length l <= RH and lists the longer ones. A record (r, g) -- the
+// pieces of group g in range r, in index order -- then gets its binade
+// prediction and its pair from the counts alone: sum_l h[l] * inc(T(l), e),
+// order-free unless some present length is a tie at e (then the record is
+// left to the fallback). Records are range-major (r * k + g, the layout the
+// producer writes, so every pass reads it coalesced across groups); level
+// nodes group 32 consecutive ranges of one group. One CTA per group walks its
+// records from the exact start value; the fallback re-reads the range and
+// keeps the members of g in order.
+
+namespace {
+
+// K1: approximate sum of every record (thread per record, range-major:
+// the histogram is read coalesced across groups)
+__global__ void k_rs_bsum(SeqTerms t, const uint16_t* __restrict__ hist,
+                          const double* __restrict__ lx, int64_t nr, int k, int RH,
+                          double* __restrict__ bsum) {
+    __shared__ double T[64];
+    if (threadIdx.x < RH) T[threadIdx.x] = term_of_len(t, threadIdx.x + 1);
+    __syncthreads();
+    const int64_t nrec = nr * k;
+    for (int64_t rec = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; rec < nrec;
+         rec += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = rec / k, g = rec - r * k;
+        const uint16_t* h = hist + (r * RH) * k + g;
+        double v = lx[rec];
+        for (int l = 0; l < RH; ++l) v += (double)h[(int64_t)l * k] * T[l];
+        bsum[rec] = v;
+    }
+}
+
+// range-major (nr x k) -> group-major (k x nr), 32 x 32 tiles through shared memory
+__global__ void k_rs_transpose(const double* __restrict__ in, int64_t nr, int k,
+                               double* __restrict__ out) {
+    __shared__ double tile[32][33];
+    const int64_t r0 = (int64_t)blockIdx.x * 32, g0 = (int64_t)blockIdx.y * 32;
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const int64_t r = r0 + j, g = g0 + threadIdx.x;
+        if (r < nr && g < k) tile[j][threadIdx.x] = in[r * k + g];
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const int64_t g = g0 + j, r = r0 + threadIdx.x;
+        if (r < nr && g < k) out[g * nr + r] = tile[threadIdx.x][j];
+    }
+}
+
+// K3: every record's predicted binade and pair (thread per record)
+__global__ void k_rs_pairs(SeqTerms t, const uint16_t* __restrict__ hist,
+                           const double* __restrict__ bsum, int64_t nr, int k, int RH,
+                           const double* __restrict__ gpre, const double* __restrict__ s_in,
+                           double rel, int* __restrict__ be, unsigned long long* __restrict__ pe,
+                           unsigned long long* __restrict__ po) {
+    __shared__ double T[64];
+    if (threadIdx.x < RH) T[threadIdx.x] = term_of_len(t, threadIdx.x + 1);
+    __syncthreads();
+    const int64_t nrec = nr * k;
+    for (int64_t rec = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; rec < nrec;
+         rec += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = rec / k, g = rec - r * k;
+        // gpre: exclusive prefix over ALL records in group-major order
+        const double P0 = s_in[g] + (gpre[g * nr + r] - gpre[g * nr]);
+        const double P1 = P0 + bsum[rec];
+        const int e0 = binade(P0 * (1.0 - rel)), e1 = binade(P1 * (1.0 + rel));
+        int e = (e0 != kNone && e0 == e1) ? e0 : kNone;
+        unsigned long long A = 0;
+        const uint16_t* h = hist + (r * RH) * k + g;
+        for (int l = 0; l < RH && e != kNone; ++l) {
+            const unsigned long long c = h[(int64_t)l * k];
+            if (!c) continue;
+            int cls;
+            const unsigned long long a = grid_units(T[l], e, cls);
+            const unsigned long long inc = a + (unsigned long long)cls;
+            if (cls == 2 || inc > ((1ULL << 53) - A) / c) e = kNone;  // tie / leaves the binade
+            else A += c * inc;
+        }
+        be[rec] = e;
+        pe[rec] = A;
+        po[rec] = A;
+    }
+}
+
+// the listed long pieces: their increments, atomically (order-free)
+__global__ void k_rs_long(SeqTerms t, const uint32_t* __restrict__ idx,
+                          const unsigned long long* __restrict__ count, int64_t R, int k,
+                          const uint32_t* __restrict__ labels, int* __restrict__ be,
+                          unsigned long long* __restrict__ pe, unsigned long long* __restrict__ po) {
+    const int64_t n = (int64_t)*count;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = idx[j];
+        const int64_t g = labels ? labels[i] : 0;
+        const int64_t rec = (i / R) * k + g;
+        const int e = be[rec];
+        if (e == kNone) continue;
+        int cls;
+        const unsigned long long a = grid_units(term_of_len(t, t.len[i]), e, cls);
+        if (cls == 2 || a >= (1ULL << 53)) {
+            atomicExch(be + rec, kNone);
+            continue;
+        }
+        const unsigned long long inc = a + (unsigned long long)cls;
+        const unsigned long long old = atomicAdd(pe + rec, inc);
+        atomicAdd(po + rec, inc);
+        // past 2^53 the record leaves its binade: drop it (before any wrap)
+        if (old + inc >= (1ULL << 53)) atomicExch(be + rec, kNone);
+    }
+}
+
+// parent (j, g) of the 32 children (32 j .. 32 j + 31, g), range-major
+__global__ void k_rs_level(int64_t nchild, int k, const int* __restrict__ ce,
+                           const unsigned long long* __restrict__ cpe,
+                           const unsigned long long* __restrict__ cpo, int64_t npar,
+                           int* __restrict__ e_out, unsigned long long* __restrict__ pe_out,
+                           unsigned long long* __restrict__ po_out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (q >= npar * k) return;
+    const int64_t j = q / k, g = q - j * k;
+    const int64_t c = j * 32 + lane;
+    const bool have = c < nchild;
+    const int e = have ? ce[c * k + g] : kNone;
+    Pair p = have ? Pair{cpe[c * k + g], cpo[c * k + g]} : Pair{0, 0};
+    const int e0 = __shfl_sync(0xffffffffu, e, 0);
+    const bool uni = __all_sync(0xffffffffu, have && e == e0 && e != kNone);
+    for (int o = 1; o < 32; o <<= 1) {
+        Pair r;
+        r.e = __shfl_up_sync(0xffffffffu, p.e, o);
+        r.o = __shfl_up_sync(0xffffffffu, p.o, o);
+        if (lane >= o) p = compose(r, p);
+    }
+    if (lane == 31) {
+        const bool fits = p.e < (1ULL << 53) && p.o < (1ULL << 53);
+        e_out[q] = uni && fits ? e0 : kNone;
+        pe_out[q] = p.e;
+        po_out[q] = p.o;
+    }
+}
+
+struct RLevel {
+    const int* e;
+    const unsigned long long* pe;
+    const unsigned long long* po;
+    int64_t n;  // nodes per group
+};
+
+// a window of 32 consecutive nodes of one group held by a warp's lanes: the
+// walk pays one load per 32 steps instead of one dependent load per step
+struct Window {
+    int64_t base = -1;
+    int e = 0;
+    unsigned long long pe = 0, po = 0;
+    __device__ __forceinline__ void get(const RLevel& L, int k, int64_t g, int64_t p, int& oe,
+                                        Pair& pr) {
+        const int lane = threadIdx.x & 31;
+        if (base < 0 || p < base || p >= base + 32) {
+            base = p;
+            const int64_t q = p + lane;
+            e = q < L.n ? L.e[q * k + g] : kNone;
+            pe = q < L.n ? L.pe[q * k + g] : 0;
+            po = q < L.n ? L.po[q * k + g] : 0;
+        }
+        const int src = (int)(p - base);
+        oe = __shfl_sync(0xffffffffu, e, src);
+        pr.e = __shfl_sync(0xffffffffu, pe, src);
+        pr.o = __shfl_sync(0xffffffffu, po, src);
+    }
+};
+
+__device__ void ss_lens(const SeqTerms& t, const int32_t* lens, int cnt, double& s) {
+    const int lane = threadIdx.x & 31;
+    for (int c = 0; c < cnt; c += 32) {
+        const int n = cnt - c < 32 ? cnt - c : 32;
+        const double w = lane < n ? term_of_len(t, lens[c + lane]) : 0.0;
+        const int e = binade(s);
+        if (e != kNone) {
+            int cls;
+            unsigned long long a = grid_units(w, e, cls);
+            a += cls == 1 ? 1ULL : 0ULL;
+            const bool tie = cls == 2;
+            for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+            if (!__any_sync(0xffffffffu, tie) && apply_pair(s, e, Pair{a, a})) continue;
+        }
+        for (int j = 0; j < n; ++j) s = s + __shfl_sync(0xffffffffu, w, j);  // the reference's add
+    }
+}
+
+constexpr int RS_TB = 256, RS_SUB = 1024;  // pieces per warp per fallback sub-range
+
+// one CTA per group: walk its records; a record that cannot be applied in
+// O(1) is summed from the range's pieces (members of g gathered in order)
+__global__ void __launch_bounds__(RS_TB) k_rs_resolve(SeqTerms t, const uint32_t* __restrict__ labels,
+                                                      int64_t n, int64_t R, int k, RLevel L1,
+                                                      RLevel L2, RLevel L3,
+                                                      const double* __restrict__ s_in,
+                                                      double* __restrict__ s_out) {
+    __shared__ int32_t s_len[RS_TB / 32][RS_SUB];
+    __shared__ int s_cnt[RS_TB / 32];
+    __shared__ double s_val;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t g = blockIdx.x;
+    const int64_t nr = L1.n;
+    double s = s_in[g];
+    Window W1, W2, W3;
+    int64_t r = 0;
+    while (r < nr) {
+        const int e = binade(s);
+        if (e != kNone) {
+            int ne;
+            Pair pr;
+            if ((r & 1023) == 0 && r + 1024 <= nr) {
+                W3.get(L3, k, g, r >> 10, ne, pr);
+                if (ne == e && apply_pair(s, e, pr)) {
+                    r += 1024;
+                    continue;
+                }
+            }
+            if ((r & 31) == 0 && r + 32 <= nr) {
+                W2.get(L2, k, g, r >> 5, ne, pr);
+                if (ne == e && apply_pair(s, e, pr)) {
+                    r += 32;
+                    continue;
+                }
+            }
+            W1.get(L1, k, g, r, ne, pr);
+            if (ne == e && apply_pair(s, e, pr)) {
+                ++r;
+                continue;
+            }
+        }
+        // fallback: the pieces of range r, the members of g in index order
+        const int64_t i0 = r * R, i1 = min(i0 + R, n);
+        for (int64_t sub = i0; sub < i1; sub += (int64_t)RS_SUB * (RS_TB / 32)) {
+            const int64_t w0 = sub + (int64_t)w * RS_SUB;
+            uint32_t lab[RS_SUB / 32];
+            int32_t ln[RS_SUB / 32];
+#pragma unroll
+            for (int j = 0; j < RS_SUB / 32; ++j) {  // every load in flight at once
+                const int64_t i = w0 + j * 32 + lane;
+                lab[j] = i < i1 && labels ? labels[i] : 0u;
+                ln[j] = i < i1 ? t.len[i] : 0;
+            }
+            int cnt = 0;
+#pragma unroll
+            for (int j = 0; j < RS_SUB / 32; ++j) {
+                const int64_t i = w0 + j * 32 + lane;
+                const bool in = i < i1 && lab[j] == (uint32_t)g;
+                const unsigned m = __ballot_sync(0xffffffffu, in);
+                if (in) s_len[w][cnt + __popc(m & ((1u << lane) - 1u))] = ln[j];
+                cnt += __popc(m);
+            }
+            if (lane == 0) s_cnt[w] = cnt;
+            __syncthreads();
+            if (w == 0)
+                for (int q = 0; q < RS_TB / 32; ++q) ss_lens(t, s_len[q], s_cnt[q], s);
+            if (threadIdx.x == 0) s_val = s;
+            __syncthreads();
+            s = s_val;
+            __syncthreads();
+        }
+        ++r;
+    }
+    if (threadIdx.x == 0) s_out[g] = s;
+}
+
+}  // namespace
+
+std::vector<double> range_seq_sums(const RangeHist& h, const SeqTerms& t,
+                                   const uint32_t* d_labels, cudaStream_t st, const Comm* cm) {
+    const int k = h.k;
+    const int64_t nr = h.nr, nrec = nr * (int64_t)k;
+    std::vector<double> cur(k, 0.0);
+    if (h.RH > 64) throw Error(INTERNAL, "range histogram wider than 64 lengths");
+    DArr<double> bsum(std::max<int64_t>(nrec, 1), st), gpre(std::max<int64_t>(nrec, 1), st);
+    auto grid_for_n = [](int64_t m) {
+        return (int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, kSMs * 16));
+    };
+    std::vector<double> local_total(k, 0.0);
+    if (nrec > 0) {
+        JB_PROF("seqsum_blocks", st);
+        k_rs_bsum<<<grid_for_n(nrec), 256, 0, st>>>(t, h.hist.p, h.lx.p, nr, k, h.RH, bsum.p);
+        JB_LAUNCH_CHECK();
+        // per-group prefix: group-major copy, one scan over all records (each
+        // group's base subtracted where it is read)
+        DArr<double> gm(k > 1 ? nrec : 0, st);
+        const double* src = bsum.p;
+        if (k > 1) {
+            k_rs_transpose<<<dim3((unsigned)((nr + 31) / 32), (unsigned)((k + 31) / 32)), dim3(32, 8),
+                             0, st>>>(bsum.p, nr, k, gm.p);
+            JB_LAUNCH_CHECK();
+            src = gm.p;
+        }
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, src, gpre.p, nrec, st);
+        DArr<uint8_t> tmp(std::max<size_t>(tb, 1), st);
+        cub::DeviceScan::ExclusiveSum(tmp.p, tb, src, gpre.p, nrec, st);
+        JB_LAUNCH_CHECK();
+        if (cm && cm->dist()) {  // this rank's approximate group totals
+            std::vector<double> pre = gpre.to_host(nrec);
+            std::vector<double> last(k);
+            for (int g = 0; g < k; ++g) {
+                JB_CUDA(cudaMemcpyAsync(&last[g], src + (int64_t)g * nr + nr - 1, 8,
+                                        cudaMemcpyDeviceToHost, st));
+            }
+            JB_CUDA(cudaStreamSynchronize(st));
+            for (int g = 0; g < k; ++g)
+                local_total[g] = pre[(int64_t)g * nr + nr - 1] + last[g] - pre[(int64_t)g * nr];
+        }
+    }
+    std::vector<double> approx(k, 0.0);
+    int64_t n_all = h.n;
+    if (cm && cm->dist()) {  // predictions from the gathered approximate totals
+        const std::vector<double> all = cm->gather(local_total);
+        const std::vector<int64_t> ns = cm->gather(std::vector<int64_t>{h.n});
+        n_all = 0;
+        for (int r = 0; r < cm->world; ++r) {
+            n_all += ns[r];
+            if (r < cm->rank)
+                for (int g = 0; g < k; ++g) approx[g] += all[(size_t)r * k + g];
+        }
+    }
+    // |sequential - exact| <= (terms so far) * 2^-52 * s; plus the double prefix's slack
+    const double rel = (double)(n_all + 64) * 0x1p-52 + 0x1p-40;
+    const int64_t n2 = (nr + 31) / 32, n3 = (n2 + 31) / 32;
+    auto mx1 = [](int64_t v) { return std::max<int64_t>(v, 1); };
+    DArr<int> be(mx1(nrec), st), e2(mx1(n2 * k), st), e3(mx1(n3 * k), st);
+    DArr<unsigned long long> pe(mx1(nrec), st), po(mx1(nrec), st), pe2(mx1(n2 * k), st),
+        po2(mx1(n2 * k), st), pe3(mx1(n3 * k), st), po3(mx1(n3 * k), st);
+    DArr<double> sin_d(k, st), sout_d(k, st);
+    if (nrec > 0) {
+        sin_d.upload(approx.data(), k);
+        JB_PROF("seqsum_pairs", st);
+        k_rs_pairs<<<grid_for_n(nrec), 256, 0, st>>>(t, h.hist.p, bsum.p, nr, k, h.RH, gpre.p,
+                                                     sin_d.p, rel, be.p, pe.p, po.p);
+        JB_LAUNCH_CHECK();
+        if (h.long_idx.p)
+            k_rs_long<<<kSMs * 4, 256, 0, st>>>(t, h.long_idx.p, h.long_n.p, h.R, k, d_labels, be.p,
+                                                pe.p, po.p);
+        JB_LAUNCH_CHECK();
+        k_rs_level<<<blocks_for_warps(n2 * k), 256, 0, st>>>(nr, k, be.p, pe.p, po.p, n2, e2.p,
+                                                             pe2.p, po2.p);
+        JB_LAUNCH_CHECK();
+        k_rs_level<<<blocks_for_warps(n3 * k), 256, 0, st>>>(n2, k, e2.p, pe2.p, po2.p, n3, e3.p,
+                                                             pe3.p, po3.p);
+        JB_LAUNCH_CHECK();
+    }
+    const RLevel L1{be.p, pe.p, po.p, nr}, L2{e2.p, pe2.p, po2.p, n2}, L3{e3.p, pe3.p, po3.p, n3};
+    auto resolve = [&](const std::vector<double>& sin) {
+        std::vector<double> out(sin);
+        if (nrec == 0) return out;
+        sin_d.upload(sin.data(), k);
+        {
+            JB_PROF(k == 1 ? "seqsum_resolve_one" : "seqsum_resolve_groups", st);
+            k_rs_resolve<<<k, RS_TB, 0, st>>>(t, d_labels, h.n, h.R, k, L1, L2, L3, sin_d.p,
+                                              sout_d.p);
+        }
+        JB_LAUNCH_CHECK();
+        sout_d.download(out.data(), k);
+        JB_CUDA(cudaStreamSynchronize(st));
+        return out;
+    };
+    if (!cm || !cm->dist()) return resolve(cur);
+    for (int r = 0; r < cm->world; ++r) {  // exact start values handed down the ranks
+        std::vector<double> mine = r == cm->rank ? resolve(cur) : cur;
+        std::vector<double> all = cm->gather(mine);
+        std::copy(all.begin() + (size_t)r * k, all.begin() + (size_t)(r + 1) * k, cur.begin());
     }
     return cur;
 }
