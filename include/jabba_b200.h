@@ -236,6 +236,14 @@ jb_status jb_kmeans(jb_context* ctx, const double* points, int64_t n, uint64_t k
 jb_status jb_seq_sum_nonneg(jb_context* ctx, const double* terms, const int64_t* seg_off,
                             int64_t n_seg, double* out);
 
+/* jabba::mse (metrics.hpp:18-29) on the GPU, bit-exact: the reference's
+ * left-to-right sum of (a_i - b_i)^2 (the same emulation as
+ * jb_seq_sum_nonneg) divided by n. on_device != 0: a and b are device
+ * pointers on the context's GPU; else host pointers. n == 0 ->
+ * JB_INVALID_INPUT. */
+jb_status jb_mse(jb_context* ctx, const double* a, const double* b, int64_t n, int32_t on_device,
+                 double* out);
+
 /* symbol token of cluster rank r in an alphabet of size k (core.hpp:186-193);
  * writes a NUL-terminated string into buf (>= 24 bytes); returns its length */
 int32_t jb_symbol_token(uint64_t rank, uint64_t alphabet_size, char* buf);

@@ -25,7 +25,7 @@ EXPORTS = [
     "jb_fit_inverse_transform", "jb_reconstruct_size", "jb_inverse_transform",
     "jb_symbol_token", "jb_profile_enable", "jb_profile_reset", "jb_profile_read",
     "jb_probe_fp64_tflops", "jb_mt19937_64_stream", "jb_sample_indices",
-    "jb_fit_transform_dist", "jb_symbolize_with", "jb_seq_sum_nonneg", "jb_kmeans",
+    "jb_fit_transform_dist", "jb_symbolize_with", "jb_seq_sum_nonneg", "jb_kmeans", "jb_mse",
 ]
 
 # int32_t (*allgather)(void* user, const void* send, uint64_t bytes, void* recv)
@@ -107,6 +107,8 @@ def lib() -> C.CDLL:
     L.jb_kmeans.argtypes = [vp, vp, C.c_int64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, vp,
                             vp, C.POINTER(C.c_uint64)]
     L.jb_kmeans.restype = C.c_int
+    L.jb_mse.argtypes = [vp, vp, vp, C.c_int64, C.c_int32, C.POINTER(C.c_double)]
+    L.jb_mse.restype = C.c_int
     L.jb_fit_transform_dist.argtypes = [vp, C.POINTER(JbComm), vp, C.c_int64, C.c_int32, i64p,
                                         i64p, C.c_int64, C.c_int64, C.c_int32,
                                         C.POINTER(JbConfig), C.POINTER(vp)]

@@ -480,6 +480,16 @@ class Engine:
                                  labels.ctypes.data, centers.ctypes.data, C.byref(it)))
         return labels[:n], centers[: 2 * k].reshape(-1, 2), it.value
 
+    def mse(self, a, b) -> float:
+        """jabba::mse (metrics.hpp:18-29) on device, bit-exact."""
+        a = np.ascontiguousarray(a, np.float64)
+        b = np.ascontiguousarray(b, np.float64)
+        if len(a) != len(b):
+            raise InvalidInput(f"mse: length mismatch ({len(a)} vs {len(b)})")
+        out = C.c_double(0)
+        _check(N.lib().jb_mse(self.ctx, a.ctypes.data, b.ctypes.data, len(a), 0, C.byref(out)))
+        return out.value
+
     def seq_sum_nonneg(self, terms, seg_off=None) -> np.ndarray:
         """The reference's sequential ``s += w`` over non-negative terms
         (digitization.hpp:39-45, 224-231), per segment, bit-exact on device."""

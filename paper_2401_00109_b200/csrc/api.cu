@@ -1244,6 +1244,30 @@ jb_status jb_kmeans(jb_context* ctx, const double* points, int64_t n, uint64_t k
     });
 }
 
+jb_status jb_mse(jb_context* ctx, const double* a, const double* b, int64_t n, int32_t on_device,
+                 double* out) {
+    return (jb_status)guarded([&] {
+        JB_CUDA(cudaSetDevice(ctx->device));
+        if (n <= 0) throw Error(INVALID_INPUT, "mse: empty series");
+        DArr<double> da, db;
+        const double* pa = a;
+        const double* pb = b;
+        if (!on_device) {
+            da.alloc(n, ctx->stream);
+            db.alloc(n, ctx->stream);
+            da.upload(a, n);
+            db.upload(b, n);
+            pa = da.p;
+            pb = db.p;
+        }
+        SeqTerms t;
+        t.kind = SeqTerms::SQDIFF;
+        t.w = pa;
+        t.w2 = pb;
+        *out = seq_sum_nonneg(t, {0, n}, ctx->stream)[0] / (double)n;
+    });
+}
+
 jb_status jb_seq_sum_nonneg(jb_context* ctx, const double* terms, const int64_t* seg_off,
                             int64_t n_seg, double* out) {
     return (jb_status)guarded([&] {

@@ -13,9 +13,56 @@
 // compiled with -fmad=false, so boundaries and increments are bit-exact.
 #include <cub/cub.cuh>
 
+#include <algorithm>
+#include <mutex>
+#include <vector>
+
 #include "jb_device.hpp"
 
 namespace jb {
+
+// RN(1/d) and RN(1/d^2) for d <= kRcpG (L1-resident through __ldg): the
+// FMA-corrected quotients (div_cr) of the deviation test for long pieces
+// (config 5: pieces up to ~3000 samples), instead of the division sequence.
+constexpr int kRcpG = 4096;
+__device__ double g_rcp1[kRcpG + 1], g_rcp2[kRcpG + 1];
+
+void upload_recips(cudaStream_t st) {  // once per device
+    static std::mutex mu;
+    static std::vector<int> done;
+    static std::vector<double> r1(kRcpG + 1), r2(kRcpG + 1);
+    int dev = 0;
+    JB_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (std::find(done.begin(), done.end(), dev) != done.end()) return;
+    for (int t = 0; t <= kRcpG; ++t) {
+        const double dd = (double)(t > 0 ? t : 1);
+        r1[t] = 1.0 / dd;  // IEEE, as the device's 1.0 / dd
+        r2[t] = 1.0 / (dd * dd);
+    }
+    JB_CUDA(cudaMemcpyToSymbolAsync(g_rcp1, r1.data(), sizeof(double) * (kRcpG + 1), 0,
+                                    cudaMemcpyHostToDevice, st));
+    JB_CUDA(cudaMemcpyToSymbolAsync(g_rcp2, r2.data(), sizeof(double) * (kRcpG + 1), 0,
+                                    cudaMemcpyHostToDevice, st));
+    JB_CUDA(cudaStreamSynchronize(st));
+    done.push_back(dev);
+}
+
+// a = yy / (d d), b = 2 y / d as the reference rounds them (compression.hpp:52)
+__device__ __forceinline__ void dev_quotients(double y, double yy, double d, int64_t L,
+                                              const double* r1s, const double* r2s, int rs,
+                                              double& a, double& b) {
+    const double y2 = 2.0 * y, ay = fabs(y);
+    if (L <= kRcpG && ((ay >= 0x1p-450 && ay <= 0x1p500) || y == 0.0)) {
+        const double q1 = L <= rs ? r1s[L] : __ldg(g_rcp1 + L);
+        const double q2 = L <= rs ? r2s[L] : __ldg(g_rcp2 + L);
+        a = yy == 0.0 ? yy : div_cr(yy, d * d, q2);
+        b = y2 == 0.0 ? y2 : div_cr(y2, d, q1);  // 0 / d keeps the zero's sign
+    } else {
+        a = yy / (d * d);
+        b = y2 / d;
+    }
+}
 
 // Greedy piece end from `start` (compression.hpp:38-61), bit-exact. The
 // test at d = 1 cannot break (cand > start + 1 fails), so its deviation is not
@@ -54,8 +101,7 @@ __device__ __forceinline__ int64_t piece_end(const double* __restrict__ v, int64
                 a = yy * (inv * inv);
                 b = (2.0 * y) * inv;
             } else {
-                a = yy / (d * d);
-                b = 2.0 * y / d;
+                dev_quotients(y, yy, d, L, nullptr, nullptr, 0, a, b);
             }
             const double sq_dev = a * sum_d2 - b * ns3 + ns2;
             if (sq_dev > (d - 1.0) * tol2) break;
@@ -160,15 +206,7 @@ __global__ void __launch_bounds__(128) k_spec(const double* __restrict__ v, Chun
             double sum_d2 = nsq;
             if (Ln > 165000) sum_d2 = d * (d + 1.0) * (2.0 * d + 1.0) / 6.0;
             double a, b;  // inc * inc / (len * len), 2.0 * inc / len
-            const double y2 = 2.0 * y, ay = fabs(y);
-            if (Ln <= kRcp && ((ay >= 0x1p-450 && ay <= 0x1p500) || y == 0.0)) {
-                // warp-uniform in practice: no divergent division sequence
-                a = yy == 0.0 ? yy : div_cr(yy, d * d, s_r2[Ln]);
-                b = y2 == 0.0 ? y2 : div_cr(y2, d, s_r1[Ln]);  // 0 / d keeps the zero's sign
-            } else {
-                a = yy / (d * d);
-                b = y2 / d;
-            }
+            dev_quotients(y, yy, d, Ln, s_r1, s_r2, kRcp, a, b);
             const double sq_dev = a * sum_d2 - b * ns3 + ns2;
             brk = sq_dev > (d - 1.0) * tol2;
         }
@@ -437,6 +475,7 @@ __global__ void k_seg_offsets(const int64_t* __restrict__ chunk_off,
 void compress_segments(const double* d_values, const SegTable& seg, double tol,
                        int64_t max_piece_len, Pieces& out, cudaStream_t st, int* n_fix_iters) {
     const int64_t n_seg = seg.n_seg;
+    upload_recips(st);
     // chunk size: enough chunks to fill 148 SMs, clamped to [32, 256] steps
     int64_t C = 256;
     while (C > 32 && seg.total_steps / C < (int64_t)kSMs * 1024) C >>= 1;

@@ -222,9 +222,10 @@ struct BBox {
 // of x (digitization.hpp:224-231).
 
 struct SeqTerms {
-    enum Kind : int { VAR_LEN = 0, X = 1, DIRECT = 2 };
+    enum Kind : int { VAR_LEN = 0, X = 1, DIRECT = 2, SQDIFF = 3 };
     const int32_t* len = nullptr;  // term i from len[i]
-    const double* w = nullptr;     // DIRECT: the terms themselves
+    const double* w = nullptr;     // DIRECT: the terms themselves; SQDIFF: (w[i] - w2[i])^2
+    const double* w2 = nullptr;
     int kind = VAR_LEN;
     double a = 0.0, b = 1.0;       // VAR_LEN: (len - a)^2;  X: a * len / b
 };

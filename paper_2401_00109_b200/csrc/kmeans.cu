@@ -1906,6 +1906,8 @@ bool lloyd_persistent(LloydCtx& L, int budget) {
     int per_sm = 0;
     JB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lloyd_persistent, 256, smem));
     if (per_sm < 1) return false;
+    static const int per_sm_cap = getenv("JB_LLOYD_PER_SM") ? atoi(getenv("JB_LLOYD_PER_SM")) : 3;
+    if (per_sm_cap > 0) per_sm = std::min(per_sm, per_sm_cap);  // grid barriers: fewer blocks
     PersistArgs a;
     a.acc = L.cacc();
     a.k = L.k;

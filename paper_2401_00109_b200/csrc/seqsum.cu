@@ -64,6 +64,10 @@ __device__ __forceinline__ double term_of_len(const SeqTerms& t, int32_t len) {
 
 __device__ __forceinline__ double term_at(const SeqTerms& t, int64_t i) {
     if (t.kind == SeqTerms::DIRECT) return t.w[i];
+    if (t.kind == SeqTerms::SQDIFF) {
+        const double d = t.w[i] - t.w2[i];  // metrics.hpp:25-26
+        return d * d;
+    }
     const double l = (double)t.len[i];
     if (t.kind == SeqTerms::VAR_LEN) {
         const double dl = l - t.a;  // digitization.hpp:41,43
@@ -668,7 +672,9 @@ __global__ void __launch_bounds__(RS_TB) k_rs_resolve(SeqTerms t, const uint32_t
                                                       int64_t n, int64_t R, int k, RLevel L1,
                                                       RLevel L2, RLevel L3,
                                                       const double* __restrict__ s_in,
-                                                      double* __restrict__ s_out) {
+                                                      double* __restrict__ s_out,
+                                                      unsigned long long* __restrict__ diag) {
+    // diag (optional): steps applied at level 3 / 2 / 1, fallbacks
     __shared__ int32_t s_len[RS_TB / 32][RS_SUB];
     __shared__ int s_cnt[RS_TB / 32];
     __shared__ double s_val;
@@ -687,6 +693,7 @@ __global__ void __launch_bounds__(RS_TB) k_rs_resolve(SeqTerms t, const uint32_t
                 W3.get(L3, k, g, r >> 10, ne, pr);
                 if (ne == e && apply_pair(s, e, pr)) {
                     r += 1024;
+                    if (diag && threadIdx.x == 0) atomicAdd(diag + 0, 1ULL);
                     continue;
                 }
             }
@@ -694,15 +701,18 @@ __global__ void __launch_bounds__(RS_TB) k_rs_resolve(SeqTerms t, const uint32_t
                 W2.get(L2, k, g, r >> 5, ne, pr);
                 if (ne == e && apply_pair(s, e, pr)) {
                     r += 32;
+                    if (diag && threadIdx.x == 0) atomicAdd(diag + 1, 1ULL);
                     continue;
                 }
             }
             W1.get(L1, k, g, r, ne, pr);
             if (ne == e && apply_pair(s, e, pr)) {
                 ++r;
+                if (diag && threadIdx.x == 0) atomicAdd(diag + 2, 1ULL);
                 continue;
             }
         }
+        if (diag && threadIdx.x == 0) atomicAdd(diag + 3, 1ULL);
         // fallback: the pieces of range r, the members of g in index order
         const int64_t i0 = r * R, i1 = min(i0 + R, n);
         for (int64_t sub = i0; sub < i1; sub += (int64_t)RS_SUB * (RS_TB / 32)) {
@@ -824,12 +834,20 @@ std::vector<double> range_seq_sums(const RangeHist& h, const SeqTerms& t,
         std::vector<double> out(sin);
         if (nrec == 0) return out;
         sin_d.upload(sin.data(), k);
+        static const bool stats = getenv("JB_SEQSUM_STATS") != nullptr;
+        DArr<unsigned long long> diag(stats ? 4 : 0, st);
+        if (stats) diag.zero();
         {
             JB_PROF(k == 1 ? "seqsum_resolve_one" : "seqsum_resolve_groups", st);
             k_rs_resolve<<<k, RS_TB, 0, st>>>(t, d_labels, h.n, h.R, k, L1, L2, L3, sin_d.p,
-                                              sout_d.p);
+                                              sout_d.p, stats ? diag.p : nullptr);
         }
         JB_LAUNCH_CHECK();
+        if (stats) {
+            const auto d = diag.to_host(4);
+            fprintf(stderr, "[jb] seqsum k=%d records=%lld R=%lld: L3 %llu L2 %llu L1 %llu fallbacks %llu\n",
+                    k, (long long)nrec, (long long)h.R, d[0], d[1], d[2], d[3]);
+        }
         sout_d.download(out.data(), k);
         JB_CUDA(cudaStreamSynchronize(st));
         return out;
