@@ -92,7 +92,7 @@ constexpr int VB_R = 2048;
 __global__ void __launch_bounds__(256) k_var_blocks(
     const int32_t* __restrict__ len, const double* __restrict__ inc, int64_t n, double mean_len,
     double mean_inc, int Ei, unsigned long long* __restrict__ acc, uint16_t* __restrict__ hist,
-    double* __restrict__ lx, uint32_t* __restrict__ long_idx,
+    double* __restrict__ approx, uint32_t* __restrict__ long_idx,
     unsigned long long* __restrict__ long_n, int RH) {
     __shared__ uint32_t sh[8][64];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -139,9 +139,13 @@ __global__ void __launch_bounds__(256) k_var_blocks(
             }
         }
         __syncwarp();
-        for (int l = lane; l < RH; l += 32) hist[r * RH + l] = (uint16_t)sh[w][l];
+        for (int l = lane; l < RH; l += 32) {
+            hist[r * RH + l] = (uint16_t)sh[w][l];
+            const double dl = (double)(l + 1) - mean_len;
+            lsum += (double)sh[w][l] * (dl * dl);  // the record's approximate sum
+        }
         for (int o = 16; o; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
-        if (lane == 0) lx[r] = lsum;
+        if (lane == 0) approx[r] = lsum;
         __syncwarp();
     }
     si = block_sum_i128<256>(si);
@@ -206,6 +210,7 @@ void scale_pieces(const Pieces& pc, int64_t total_steps, double scl, Scaled& out
     JB_TRACE("scale: sum inc", st);
     std::vector<unsigned long long> h = acc.to_host(2);
     h = C.sum_i128(h);
+    const std::vector<unsigned long long> hm = mm.to_host(2);
     // mean_len: sequential double sum of integer lens is exact (< 2^53)
     const double mean_len = (double)total_steps / n;
     const double mean_inc = fx_to_double(fx_load(h.data()), Einc) / n;
@@ -221,7 +226,7 @@ void scale_pieces(const Pieces& pc, int64_t total_steps, double scl, Scaled& out
         const int64_t nr = vh.nr;
         k_var_blocks<<<(int)std::max<int64_t>(1, std::min<int64_t>((nr + 7) / 8, (int64_t)kSMs * 8)),
                        256, 0, st>>>(pc.len.p, pc.inc.p, pc.N, mean_len, mean_inc, Ei, acc.p,
-                                     vh.hist.p, vh.lx.p, vh.long_idx.p, vh.long_n.p, RH);
+                                     vh.hist.p, vh.approx.p, vh.long_idx.p, vh.long_n.p, RH);
     }
     JB_LAUNCH_CHECK();
     h = acc.to_host(4);
@@ -245,7 +250,6 @@ void scale_pieces(const Pieces& pc, int64_t total_steps, double scl, Scaled& out
     out.sigma_inc = si;
 
     // bounding box of all points from the extremes of len and inc
-    std::vector<unsigned long long> hm = mm.to_host(2);
     std::vector<unsigned long long> hb = {
         pc.N > 0 ? (unsigned long long)pc.min_len : ~0ULL, (unsigned long long)pc.max_len,
         hm[0], hm[1]};
@@ -316,7 +320,7 @@ constexpr int kXRow = 64;
 // the long pieces' approximate x sums; long pieces listed. hist == null: none.
 struct RangeOut {
     uint16_t* hist = nullptr;
-    double* lx = nullptr;
+    double* approx = nullptr;  // per (range, cluster): approximate sum of the pieces' x
     uint32_t* long_idx = nullptr;
     unsigned long long* long_n = nullptr;
     int64_t R = 1024;
@@ -441,20 +445,23 @@ __global__ void __launch_bounds__(AS_TB) k_assign_stats(
         for (int c = threadIdx.x; c < k; c += AS_TB) {
             unsigned long long cnt = 0, ls = 0;
             u128 sx = 0;
+            double ax = lxr[c];
             for (int l = 1; l <= RH; ++l) {
                 const uint32_t h = hist[(size_t)(l - 1) * k + c];
                 if (!h) continue;
                 cnt += h;
                 ls += (unsigned long long)h * (unsigned long long)l;
-                const u128 xb = (u128)(fx_from_double(row_x(rg, l), Ex) + (i128)Bx);
+                const double xl = row_x(rg, l);
+                const u128 xb = (u128)(fx_from_double(xl, Ex) + (i128)Bx);
                 sx += xb * (u128)h;
+                ax += (double)h * xl;
             }
             tot[c] += cnt;
             tot[k + c] += ls;
             const u128 t0 = ((u128)tot[3 * k + c] << 64 | tot[2 * k + c]) + sx;
             tot[2 * k + c] = (unsigned long long)t0;
             tot[3 * k + c] = (unsigned long long)(t0 >> 64);
-            if (ro.hist) ro.lx[r * k + c] = lxr[c];
+            if (ro.hist) ro.approx[r * k + c] = ax;
             lxr[c] = 0.0;
         }
         __syncthreads();
@@ -623,7 +630,7 @@ void assign_and_stats(const PtsView& pv, const int32_t* d_len, int64_t n,
     if (rh) {
         rh->alloc(n, R, (int)k, RH, max_len > RH, st);
         ro.hist = rh->hist.p;
-        ro.lx = rh->lx.p;
+        ro.approx = rh->approx.p;
         ro.long_idx = rh->long_idx.p;
         ro.long_n = rh->long_n.p;
     }

@@ -253,14 +253,15 @@ struct SeqSum {
 // piece length (seqsum.cu): for every range r of R consecutive pieces, the
 // pieces of group g with length l in 1..RH are counted in
 // hist[(r * RH + l - 1) * k + g]; longer pieces are listed (long_idx, any
-// order) and their terms' approximate sums kept in lx[r * k + g]. k == 1:
+// order); approx[r * k + g] is an approximate sum of the record's terms (a
+// binade prediction only: any rounding is fine). k == 1:
 // every piece is in the one group. Written by the producer kernels
 // (k_var_blocks, k_assign_stats), consumed by range_seq_sums.
 struct RangeHist {
     int64_t n = 0, R = 0, nr = 0;
     int k = 1, RH = 0;
     DArr<uint16_t> hist;
-    DArr<double> lx;
+    DArr<double> approx;
     DArr<uint32_t> long_idx;
     DArr<unsigned long long> long_n;
     void alloc(int64_t n_, int64_t R_, int k_, int RH_, bool longs, cudaStream_t st) {
@@ -270,8 +271,8 @@ struct RangeHist {
         RH = RH_;
         nr = (n + R - 1) / R;
         hist.alloc(std::max<int64_t>(nr * RH * k, 1), st);
-        lx.alloc(std::max<int64_t>(nr * k, 1), st);
-        lx.zero();
+        approx.alloc(std::max<int64_t>(nr * k, 1), st);
+        approx.zero();
         long_n.alloc(1, st);
         long_n.zero();
         if (longs) long_idx.alloc(std::max<int64_t>(n, 1), st);

@@ -1005,6 +1005,174 @@ __global__ void __launch_bounds__(PICK_TB) k_pick(const uint64_t* __restrict__ r
     }
 }
 
+
+// The same pick by a thread-block CLUSTER of PC CTAs: CTA r stages its
+// contiguous share of the block partials in shared memory and sums them; the
+// PC range totals are exchanged through distributed shared memory; the CTA
+// whose range holds u finds the block from its staged partials and the
+// element inside it exactly as k_pick. One CTA read ~700 KB of partials per
+// round (config 4); eight read 87 KB each, in parallel.
+constexpr int PC = 8;
+constexpr size_t kPickClusterSmem = 200 * 1024;  // staged partials per CTA
+
+__global__ void __cluster_dims__(PC, 1, 1) __launch_bounds__(PICK_TB)
+    k_pick_cluster(const uint64_t* __restrict__ raw, const double* __restrict__ d2s,
+                   const uint32_t* __restrict__ pos, int64_t n, int nblocks,
+                   const unsigned long long* __restrict__ part, int E, SeedState* ss,
+                   int64_t* __restrict__ chosen, int c, unsigned long long* __restrict__ nwork_reset) {
+    namespace cgx = cooperative_groups;
+    cgx::cluster_group cl = cgx::this_cluster();
+    extern __shared__ unsigned long long s_part[];  // my blocks: (lo, hi) pairs
+    __shared__ unsigned long long s_lo[32], s_hi[32];
+    __shared__ unsigned long long s_tot[2];
+    __shared__ int s_fb;
+    __shared__ unsigned long long s_before[2];
+    __shared__ unsigned long long s_found_elem;
+    const int t = threadIdx.x, lane = t & 31;
+    const int r = (int)cl.block_rank();
+    const int per = (nblocks + PC - 1) / PC;
+    const int b0 = min(nblocks, r * per), b1 = min(nblocks, b0 + per), nb = b1 - b0;
+    if (r == 0 && t == 0 && nwork_reset) *nwork_reset = 0;
+    // stage my partials (8 independent 16-byte loads in flight per thread)
+    const ulonglong2* p2 = reinterpret_cast<const ulonglong2*>(part) + b0;
+    ulonglong2* s2 = reinterpret_cast<ulonglong2*>(s_part);
+    for (int q0 = t; q0 < nb; q0 += PICK_TB * 8) {
+        ulonglong2 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int q = q0 + u * PICK_TB;
+            v[u] = q < nb ? p2[q] : make_ulonglong2(0ULL, 0ULL);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int q = q0 + u * PICK_TB;
+            if (q < nb) s2[q] = v[u];
+        }
+    }
+    __syncthreads();
+    // thread t owns blocks [b0 + t*qn, ...) of my range: its sum, then a block scan
+    const int qn = (nb + PICK_TB - 1) / PICK_TB;
+    const int q0 = min(nb, t * qn), q1 = min(nb, q0 + qn);
+    i128 mine = 0;
+    for (int q = q0; q < q1; ++q) mine += (i128)(((u128)s2[q].y << 64) | (u128)s2[q].x);
+    i128 range_total;
+    const i128 excl = block_exscan_i128(mine, &range_total, s_lo, s_hi);
+    if (t == 0) {
+        s_tot[0] = (unsigned long long)(u128)range_total;
+        s_tot[1] = (unsigned long long)((u128)range_total >> 64);
+        s_fb = 0x7FFFFFFF;
+        s_found_elem = ~0ULL;
+    }
+    cl.sync();
+    // the PC range totals (DSMEM): prefix, total, u -- identical on every CTA
+    i128 pre_r = 0, total_fx = 0;
+    int rc = -1;
+    for (int q = 0; q < PC; ++q) {
+        const unsigned long long* rt = cl.map_shared_rank(s_tot, q);
+        const i128 v = (i128)(((u128)rt[1] << 64) | (u128)rt[0]);
+        if (q < r) pre_r += v;
+        total_fx += v;
+    }
+    const double total = fx_to_double(total_fx, E);
+    bool spill = false;
+    i128 U = 0;
+    if (total > 0.0) {
+        const uint64_t x = raw[ss->cursor];
+        double canon = __ull2double_rn(x) * 0x1p-64;  // generate_canonical<double,53>
+        if (canon >= 1.0) canon = 0x1.fffffffffffffp-1;
+        const double u = canon * total + 0.0;  // uniform_real(0, total)
+        U = fx_from_double(u, E);
+        i128 run = 0;
+        for (int q = 0; q < PC && rc < 0; ++q) {
+            const unsigned long long* rt = cl.map_shared_rank(s_tot, q);
+            run += (i128)(((u128)rt[1] << 64) | (u128)rt[0]);
+            if (U < run) rc = q;
+        }
+        spill = rc < 0;
+    }
+    cl.sync();  // no CTA leaves while its totals may still be read
+    if (!(total > 0.0) || spill) {  // rare paths, serially as k_pick
+        if (r == 0 && t == 0) {
+            int64_t next;
+            if (!(total > 0.0)) {  // every remaining point duplicates a center (:120-124)
+                next = 0;
+                for (;;) {
+                    bool taken = false;
+                    for (int q = 0; q < c; ++q) taken |= chosen[q] == next;
+                    if (!taken) break;
+                    ++next;
+                }
+                ss->degenerate = 1;
+            } else {  // roundoff spill: last positive-weight index (:67-70)
+                next = n - 1;
+                for (int64_t i = n - 1; i >= 0; --i)
+                    if (d2s[pos[i]] > 0.0) {
+                        next = i;
+                        break;
+                    }
+                ss->cursor += 1;
+            }
+            chosen[c] = next;
+            ss->last = next;
+        }
+        return;
+    }
+    if (r != rc) return;
+    // my range holds the crossing: the owning thread finds the block
+    const i128 lo_t = pre_r + excl;
+    if (U >= lo_t && U < lo_t + mine) {
+        i128 run = lo_t;
+        for (int q = q0; q < q1; ++q) {
+            const i128 v = (i128)(((u128)s2[q].y << 64) | (u128)s2[q].x);
+            if (U < run + v) {
+                s_fb = b0 + q;
+                s_before[0] = (unsigned long long)(u128)run;
+                s_before[1] = (unsigned long long)((u128)run >> 64);
+                break;
+            }
+            run += v;
+        }
+    }
+    __syncthreads();
+    const int fb = s_fb;
+    if (fb == 0x7FFFFFFF) {  // cannot happen for U < total; stay safe: spill rule
+        if (t == 0) {
+            int64_t next = n - 1;
+            for (int64_t i = n - 1; i >= 0; --i)
+                if (d2s[pos[i]] > 0.0) {
+                    next = i;
+                    break;
+                }
+            chosen[c] = next;
+            ss->last = next;
+            ss->cursor += 1;
+        }
+        return;
+    }
+    const i128 before_block = fx_load(s_before);
+    const int64_t e0 = (int64_t)fb * D2_R + 2 * t;  // 1024 threads x 2 elements
+    i128 a = 0, bsum = 0;
+    if (e0 < n) a = fx_from_double(d2s[pos[e0]], E);
+    if (e0 + 1 < n) bsum = fx_from_double(d2s[pos[e0 + 1]], E);
+    i128 dummy;
+    const i128 ex2 = block_exscan_i128(a + bsum, &dummy, s_lo, s_hi);
+    {
+        const i128 before = before_block + ex2;
+        unsigned long long hit = ~0ULL;
+        if (e0 < n && U < before + a) hit = (unsigned long long)e0;
+        else if (e0 + 1 < n && U < before + a + bsum) hit = (unsigned long long)(e0 + 1);
+        if (hit != ~0ULL) atomicMin(&s_found_elem, hit);
+    }
+    __syncthreads();
+    if (t == 0) {
+        const int64_t next = (int64_t)s_found_elem;
+        chosen[c] = next;
+        ss->last = next;
+        ss->cursor += 1;
+    }
+    (void)lane;
+}
+
 __global__ void k_copy_center(const double2* __restrict__ spts, const uint32_t* __restrict__ pos,
                               const int64_t* __restrict__ chosen, int k,
                               double* __restrict__ centers) {
@@ -2213,11 +2381,22 @@ void lloyd_best_device(const PtsView& pv, const uint64_t* d_idx, int64_t n, uint
                                                   nullptr, d2_diag.p);
         }
         JB_LAUNCH_CHECK();
+        // cluster pick when every CTA's share of the partials fits its smem
+        const size_t pick_smem = 16 * (size_t)((nblocks + PC - 1) / PC);
+        const bool cluster_pick = pick_smem <= kPickClusterSmem;
+        if (cluster_pick)
+            JB_CUDA(cudaFuncSetAttribute(k_pick_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)std::max<size_t>(pick_smem, 16)));
         for (uint64_t c = 1; c < k; ++c) {
             {
                 JB_PROF("d2_pick", st);
-                k_pick<<<1, PICK_TB, 0, st>>>(d_raw, d2s.p, pos.p, n, nblocks, part.p, Ed2, ss.p,
-                                              chosen.p, (int)c, d2_nwork.p);
+                if (cluster_pick)
+                    k_pick_cluster<<<PC, PICK_TB, std::max<size_t>(pick_smem, 16), st>>>(
+                        d_raw, d2s.p, pos.p, n, nblocks, part.p, Ed2, ss.p, chosen.p, (int)c,
+                        d2_nwork.p);
+                else
+                    k_pick<<<1, PICK_TB, 0, st>>>(d_raw, d2s.p, pos.p, n, nblocks, part.p, Ed2,
+                                                  ss.p, chosen.p, (int)c, d2_nwork.p);
             }
             JB_LAUNCH_CHECK();
             if (c + 1 < k) {

@@ -489,25 +489,6 @@ std::vector<double> seq_sum_nonneg(const SeqTerms& t, const std::vector<int64_t>
 
 namespace {
 
-// K1: approximate sum of every record (thread per record, range-major:
-// the histogram is read coalesced across groups)
-__global__ void k_rs_bsum(SeqTerms t, const uint16_t* __restrict__ hist,
-                          const double* __restrict__ lx, int64_t nr, int k, int RH,
-                          double* __restrict__ bsum) {
-    __shared__ double T[64];
-    if (threadIdx.x < RH) T[threadIdx.x] = term_of_len(t, threadIdx.x + 1);
-    __syncthreads();
-    const int64_t nrec = nr * k;
-    for (int64_t rec = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; rec < nrec;
-         rec += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = rec / k, g = rec - r * k;
-        const uint16_t* h = hist + (r * RH) * k + g;
-        double v = lx[rec];
-        for (int l = 0; l < RH; ++l) v += (double)h[(int64_t)l * k] * T[l];
-        bsum[rec] = v;
-    }
-}
-
 // range-major (nr x k) -> group-major (k x nr), 32 x 32 tiles through shared memory
 __global__ void k_rs_transpose(const double* __restrict__ in, int64_t nr, int k,
                                double* __restrict__ out) {
@@ -550,8 +531,10 @@ __global__ void k_rs_pairs(SeqTerms t, const uint16_t* __restrict__ hist,
             int cls;
             const unsigned long long a = grid_units(T[l], e, cls);
             const unsigned long long inc = a + (unsigned long long)cls;
-            if (cls == 2 || inc > ((1ULL << 53) - A) / c) e = kNone;  // tie / leaves the binade
-            else A += c * inc;
+            // tie, or the record leaves the binade (128-bit product: no wrap)
+            const u128 add = (u128)c * (u128)inc;
+            if (cls == 2 || add >= (u128)((1ULL << 53) - A)) e = kNone;
+            else A += (unsigned long long)add;
         }
         be[rec] = e;
         pe[rec] = A;
@@ -646,7 +629,32 @@ struct Window {
     }
 };
 
+__device__ void ss_chunks(const SeqTerms& t, const int32_t* lens, int cnt, double& s);
+
 __device__ void ss_lens(const SeqTerms& t, const int32_t* lens, int cnt, double& s) {
+    const int lane = threadIdx.x & 31;
+    for (int c0 = 0; c0 < cnt; c0 += 1024) {
+        // 1024 terms at once when none of them crosses a binade or ties:
+        // lane-local sums, one warp reduction (one per 32 chunks)
+        const int nb = cnt - c0 < 1024 ? cnt - c0 : 1024;
+        const int e = binade(s);
+        if (e != kNone && nb > 64) {
+            unsigned long long a = 0;
+            bool bad = false;
+            for (int j = lane; j < nb; j += 32) {
+                int cls;
+                const unsigned long long q = grid_units(term_of_len(t, lens[c0 + j]), e, cls);
+                bad |= cls == 2 || q >= (1ULL << 53);
+                a += q + (cls == 1 ? 1ULL : 0ULL);
+            }
+            for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+            if (!__any_sync(0xffffffffu, bad) && apply_pair(s, e, Pair{a, a})) continue;
+        }
+        ss_chunks(t, lens + c0, nb, s);
+    }
+}
+
+__device__ void ss_chunks(const SeqTerms& t, const int32_t* lens, int cnt, double& s) {
     const int lane = threadIdx.x & 31;
     for (int c = 0; c < cnt; c += 32) {
         const int n = cnt - c < 32 ? cnt - c : 32;
@@ -736,8 +744,12 @@ __global__ void __launch_bounds__(RS_TB) k_rs_resolve(SeqTerms t, const uint32_t
             }
             if (lane == 0) s_cnt[w] = cnt;
             __syncthreads();
-            if (w == 0)
-                for (int q = 0; q < RS_TB / 32; ++q) ss_lens(t, s_len[q], s_cnt[q], s);
+            if (w == 0) {  // the regions in order; small ones chunk by chunk
+                int tot = 0;
+                for (int q = 0; q < RS_TB / 32; ++q) tot += s_cnt[q];
+                for (int q = 0; q < RS_TB / 32; ++q)
+                    if (s_cnt[q]) (tot > 256 ? ss_lens : ss_chunks)(t, s_len[q], s_cnt[q], s);
+            }
             if (threadIdx.x == 0) s_val = s;
             __syncthreads();
             s = s_val;
@@ -756,22 +768,21 @@ std::vector<double> range_seq_sums(const RangeHist& h, const SeqTerms& t,
     const int64_t nr = h.nr, nrec = nr * (int64_t)k;
     std::vector<double> cur(k, 0.0);
     if (h.RH > 64) throw Error(INTERNAL, "range histogram wider than 64 lengths");
-    DArr<double> bsum(std::max<int64_t>(nrec, 1), st), gpre(std::max<int64_t>(nrec, 1), st);
+    const double* bsum = h.approx.p;  // the producer's per-record approximate sums
+    DArr<double> gpre(std::max<int64_t>(nrec, 1), st);
     auto grid_for_n = [](int64_t m) {
         return (int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, kSMs * 16));
     };
     std::vector<double> local_total(k, 0.0);
     if (nrec > 0) {
         JB_PROF("seqsum_blocks", st);
-        k_rs_bsum<<<grid_for_n(nrec), 256, 0, st>>>(t, h.hist.p, h.lx.p, nr, k, h.RH, bsum.p);
-        JB_LAUNCH_CHECK();
         // per-group prefix: group-major copy, one scan over all records (each
         // group's base subtracted where it is read)
         DArr<double> gm(k > 1 ? nrec : 0, st);
-        const double* src = bsum.p;
+        const double* src = bsum;
         if (k > 1) {
             k_rs_transpose<<<dim3((unsigned)((nr + 31) / 32), (unsigned)((k + 31) / 32)), dim3(32, 8),
-                             0, st>>>(bsum.p, nr, k, gm.p);
+                             0, st>>>(bsum, nr, k, gm.p);
             JB_LAUNCH_CHECK();
             src = gm.p;
         }
@@ -815,7 +826,7 @@ std::vector<double> range_seq_sums(const RangeHist& h, const SeqTerms& t,
     if (nrec > 0) {
         sin_d.upload(approx.data(), k);
         JB_PROF("seqsum_pairs", st);
-        k_rs_pairs<<<grid_for_n(nrec), 256, 0, st>>>(t, h.hist.p, bsum.p, nr, k, h.RH, gpre.p,
+        k_rs_pairs<<<grid_for_n(nrec), 256, 0, st>>>(t, h.hist.p, bsum, nr, k, h.RH, gpre.p,
                                                      sin_d.p, rel, be.p, pe.p, po.p);
         JB_LAUNCH_CHECK();
         if (h.long_idx.p)
