@@ -296,37 +296,130 @@ __global__ void k_fix(const double* __restrict__ v, ChunkGeom g, int64_t n_chunk
     if (ch_) atomicExch(changed, 1);
 }
 
-// Phase 2b (chains that merge late): one thread per segment walks its chunks
-// in order from the true entry -- the exact sequential fixed point, O(1) per
-// chunk whose entry is a speculative start or lies beyond it -- instead of
-// one more parallel round per chunk of the longest chain (config 5's long
-// pieces: ~50 rounds).
-__global__ void k_fix_walk(const double* __restrict__ v, ChunkGeom g, double tol2,
-                           int64_t max_len, const uint32_t* __restrict__ fb,
-                           const int64_t* __restrict__ exit_spec, int64_t* __restrict__ E) {
-    const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+// Greedy piece end from `start` (compression.hpp:38-61) evaluated by a whole
+// warp, 32 candidates per step: lane j tests d = c0 + j - start. The running
+// sums s2 = sum y^2 and s3 = sum d*y stay the reference's sequential fp64
+// sums: each lane adds the step's terms of lanes 0..j to the carried sum in
+// order (predicated adds over a shared-memory broadcast of the terms), which
+// is the same chain of roundings. The piece ends before the first lane that
+// fails the test, passes `last` or exceeds max_len (all three give
+// end = cand - 1). Uniform result.
+__device__ __forceinline__ int64_t piece_end_warp(const double* __restrict__ v, int64_t start,
+                                                  int64_t last, double tol2, int64_t max_len,
+                                                  double* sh /* 64 doubles per warp */) {
+    const int lane = threadIdx.x & 31;
+    const double base = __ldg(v + start);
+    double s2 = 0.0, s3 = 0.0;  // carried sums through the previous step
+    for (int64_t c0 = start + 1;; c0 += 32) {
+        const int64_t cand = c0 + lane;
+        const int64_t L = cand - start;
+        const bool in = cand <= last && (max_len <= 0 || L <= max_len);
+        const double vc = in ? __ldg(v + cand) : base;
+        const double y = vc - base;
+        const double d = (double)L;
+        const double yy = y * y, dy = d * y;
+        sh[lane] = yy;
+        sh[32 + lane] = dy;
+        __syncwarp();
+        double n2 = s2, n3 = s3;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            const double a2 = sh[i], a3 = sh[32 + i];
+            if (i <= lane) {
+                n2 += a2;
+                n3 += a3;
+            }
+        }
+        __syncwarp();
+        bool stop = !in;
+        if (in && L > 1) {
+            // sum_{i<=d} i^2: the exact integer while d(d+1)(2d+1) < 2^53,
+            // where the reference's formula is exact too; the formula beyond
+            const double sum_d2 = L <= 165000 ? (double)(L * (L + 1) * (2 * L + 1) / 6)
+                                              : d * (d + 1.0) * (2.0 * d + 1.0) / 6.0;
+            double a, b;  // inc * inc / (len * len), 2.0 * inc / len
+            dev_quotients(y, yy, d, L, nullptr, nullptr, 0, a, b);
+            const double sq_dev = a * sum_d2 - b * n3 + n2;
+            stop = sq_dev > (d - 1.0) * tol2;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, stop);
+        if (m) return c0 + (__ffs(m) - 1) - 1;
+        s2 = __shfl_sync(0xffffffffu, n2, 31);
+        s3 = __shfl_sync(0xffffffffu, n3, 31);
+    }
+}
+
+// Phase 2b (chains that merge late, config 5's long pieces): one WARP per
+// segment walks its chunks in order from the true entry -- the exact
+// sequential fixed point -- and rewrites each chunk's flags to the true orbit
+// on the way (so Phase 3 is skipped). A chunk whose entry is a speculative
+// start costs O(1); otherwise the warp parses from the entry until the true
+// orbit meets a speculative start or leaves the chunk. The chunk's W flag
+// words live in lanes 0..W-1.
+constexpr int kWalkTB = 128;
+__global__ void __launch_bounds__(kWalkTB) k_walk(const double* __restrict__ v, ChunkGeom g,
+                                                  double tol2, int64_t max_len,
+                                                  uint32_t* __restrict__ fb,
+                                                  const int64_t* __restrict__ exit_spec,
+                                                  int64_t* __restrict__ E) {
+    __shared__ double s_terms[kWalkTB / 32][64];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     if (s >= g.n_seg) return;
     const int64_t c0 = g.chunk_off[s], c1 = g.chunk_off[s + 1];
-    if (c0 >= c1) return;
     const int W = (int)(g.C >> 5);
-    int64_t t = exit_spec[c0];
-    E[c0] = t;
-    for (int64_t ch = c0 + 1; ch < c1; ++ch) {
+    int64_t t = g.seg_first[s];  // true entry of the current chunk
+    for (int64_t ch = c0; ch < c1; ++ch) {
         int64_t ss, c, lo, hi, last;
         chunk_bounds(g, ch, ss, c, lo, hi, last);
+        uint32_t word = lane < W ? fb[ch * W + lane] : 0u;
+        // clear bits of positions [p0, p1) (chunk-relative)
+        auto clear = [&](int64_t p0, int64_t p1) {
+            const int64_t w0 = 32 * (int64_t)lane;
+            const int64_t a = p0 - lo > w0 ? p0 - lo - w0 : 0;
+            const int64_t b = p1 - lo - w0 < 32 ? p1 - lo - w0 : 32;
+            if (a < b) {
+                const uint32_t hm = b >= 32 ? 0xffffffffu : ((1u << b) - 1u);
+                word &= ~(hm & ~((1u << a) - 1u));
+            }
+        };
+        auto test = [&](int64_t p) {
+            const int rel = (int)(p - lo);
+            return (__shfl_sync(0xffffffffu, word, rel >> 5) >> (rel & 31)) & 1u;
+        };
+        auto set = [&](int64_t p) {
+            const int rel = (int)(p - lo);
+            if (lane == (rel >> 5)) word |= 1u << (rel & 31);
+        };
         int64_t r;
         if (t >= hi) {
+            word = 0;
             r = t;
-        } else if (fbit(fb, ch, W, t - lo)) {
-            r = exit_spec[ch];
         } else {
-            int64_t q = t;
-            do {
-                q = piece_end(v, q, last, tol2, max_len);
-            } while (q < hi && !fbit(fb, ch, W, q - lo));
-            r = q < hi ? exit_spec[ch] : q;
+            clear(lo, t);
+            if (test(t)) {
+                r = exit_spec[ch];
+            } else {
+                set(t);
+                int64_t p = t;
+                for (;;) {
+                    const int64_t q = piece_end_warp(v, p, last, tol2, max_len, s_terms[wib]);
+                    clear(p + 1, q < hi ? q : hi);
+                    if (q >= hi) {
+                        r = q;
+                        break;
+                    }
+                    if (test(q)) {
+                        r = exit_spec[ch];
+                        break;
+                    }
+                    set(q);
+                    p = q;
+                }
+            }
         }
-        E[ch] = r;
+        if (lane < W) fb[ch * W + lane] = word;
+        if (lane == 0) E[ch] = r;
         t = r;
     }
 }
@@ -516,6 +609,12 @@ void compress_segments(const double* d_values, const SegTable& seg, double tol,
     JB_CUDA(cudaMemcpyAsync(Ea.p, exit_spec.p, sizeof(int64_t) * n_chunks,
                             cudaMemcpyDeviceToDevice, st));
     int iters = 0;
+    // the warp walk is sequential per segment: used unless one segment is so
+    // long that its walk would outlast the parallel rounds
+    int64_t max_steps = 0;
+    for (int64_t s = 0; s < n_seg; ++s) max_steps = std::max(max_steps, seg.h_steps[s]);
+    const bool walk_ok = max_steps <= (int64_t(1) << 22) && !getenv("JB_NO_WALK");
+    bool walked = false;
     DArr<uint8_t> dirty_a(n_chunks, st), dirty_b(n_chunks, st);
     for (;;) {
         JB_CUDA(cudaMemsetAsync(dflag.p + 1, 0, sizeof(int), st));
@@ -533,21 +632,22 @@ void compress_segments(const double* d_values, const SegTable& seg, double tol,
         JB_CUDA(cudaStreamSynchronize(st));
         std::swap(Ea, Eb);
         if (!ch) break;
-        if (iters == 2) {  // still moving: walk the segments sequentially (exact)
-            JB_PROF("compress_fix", st);
-            k_fix_walk<<<ceil_div(n_seg, 128), 128, 0, st>>>(d_values, g, tol2, max_piece_len,
-                                                              flags.p, exit_spec.p, Ea.p);
+        if (walk_ok) {  // still moving: walk the segments sequentially (exact)
+            JB_PROF("compress_walk", st);
+            k_walk<<<ceil_div(n_seg * 32, kWalkTB), kWalkTB, 0, st>>>(
+                d_values, g, tol2, max_piece_len, flags.p, exit_spec.p, Ea.p);
             JB_LAUNCH_CHECK();
             ++iters;
+            walked = true;
             break;
         }
     }
     if (n_fix_iters) *n_fix_iters = iters;
-    {
+    if (!walked) {
         JB_PROF("compress_apply", st);
         k_apply<<<nb, TB, 0, st>>>(d_values, g, n_chunks, tol2, max_piece_len, flags.p, Ea.p);
+        JB_LAUNCH_CHECK();
     }
-    JB_LAUNCH_CHECK();
     const int wgrid = (int)std::max<int64_t>(
         1, std::min<int64_t>((n_chunks * 32 + 255) / 256, (int64_t)kSMs * 16));
     {
