@@ -306,7 +306,7 @@ __global__ void k_pair_labels(const uint32_t* __restrict__ sidx,
 
 
 int gsz(int64_t n) {
-    return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)kSMs * 8));
+    return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8));
 }
 
 // ga-hier (digitization.hpp:168-195): two 1-D aggregations, pieces labeled by

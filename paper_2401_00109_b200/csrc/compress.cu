@@ -571,7 +571,7 @@ void compress_segments(const double* d_values, const SegTable& seg, double tol,
     upload_recips(st);
     // chunk size: enough chunks to fill 148 SMs, clamped to [32, 256] steps
     int64_t C = 256;
-    while (C > 32 && seg.total_steps / C < (int64_t)kSMs * 1024) C >>= 1;
+    while (C > 32 && seg.total_steps / C < (int64_t)num_sms() * 1024) C >>= 1;
     std::vector<int64_t> h_chunk_off(n_seg + 1);
     int64_t max_last = 0;
     h_chunk_off[0] = 0;
@@ -649,7 +649,7 @@ void compress_segments(const double* d_values, const SegTable& seg, double tol,
         JB_LAUNCH_CHECK();
     }
     const int wgrid = (int)std::max<int64_t>(
-        1, std::min<int64_t>((n_chunks * 32 + 255) / 256, (int64_t)kSMs * 16));
+        1, std::min<int64_t>((n_chunks * 32 + 255) / 256, (int64_t)num_sms() * 16));
     {
         JB_PROF("compress_count", st);
         k_count<<<nb, TB, 0, st>>>(g, n_chunks, flags.p, cnt.p);

@@ -162,7 +162,7 @@ __global__ void k_scale(const int32_t* __restrict__ len, const double* __restric
 
 int grid_for(int64_t n) {
     const int64_t b = (n + kTB - 1) / kTB;
-    return (int)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)kSMs * 8));
+    return (int)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)num_sms() * 8));
 }
 
 }  // namespace
@@ -224,7 +224,7 @@ void scale_pieces(const Pieces& pc, int64_t total_steps, double scl, Scaled& out
     if (pc.N > 0) {
         JB_PROF("scale_sum_var", st);
         const int64_t nr = vh.nr;
-        k_var_blocks<<<(int)std::max<int64_t>(1, std::min<int64_t>((nr + 7) / 8, (int64_t)kSMs * 8)),
+        k_var_blocks<<<(int)std::max<int64_t>(1, std::min<int64_t>((nr + 7) / 8, (int64_t)num_sms() * 8)),
                        256, 0, st>>>(pc.len.p, pc.inc.p, pc.N, mean_len, mean_inc, Ei, acc.p,
                                      vh.hist.p, vh.approx.p, vh.long_idx.p, vh.long_n.p, RH);
     }
@@ -610,7 +610,7 @@ void assign_and_stats(const PtsView& pv, const int32_t* d_len, int64_t n,
     if (k > 2048) {
         if (n > 0) {
             JB_PROF("assign_stats", st);
-            k_stats_global<<<(int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, kSMs * 8)),
+            k_stats_global<<<(int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, num_sms() * 8)),
                              256, 0, st>>>(pv, d_len, n, d_labels,
                                            (int)k, Ex, Ey, Bx, By, acc.p);
         }
@@ -620,7 +620,7 @@ void assign_and_stats(const PtsView& pv, const int32_t* d_len, int64_t n,
     JB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_assign_stats, AS_TB, smem));
     const int grid = (int)std::max<int64_t>(
         1, std::min<int64_t>((n + AS_TB * AS_U - 1) / (AS_TB * AS_U),
-                             (int64_t)kSMs * std::max(per_sm, 1)));
+                             (int64_t)num_sms() * std::max(per_sm, 1)));
     // ranges: about one per block, at most 32768 pieces (u16 counts), a
     // multiple of the 1024-piece chunk
     constexpr int64_t kChunk = (int64_t)AS_TB * AS_U;
@@ -745,7 +745,7 @@ void relabel(uint32_t* d_labels, int64_t n, const std::vector<uint32_t>& rank_of
     const int k = (int)rank_of.size();
     DArr<uint32_t> rk(k, st);
     rk.upload(rank_of.data(), k);
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, kSMs * 8));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, num_sms() * 8));
     JB_PROF("relabel", st);
     if ((size_t)k * 4 <= 48 * 1024 && ((uintptr_t)d_labels & 15) == 0)
         k_relabel<<<grid, 256, k * 4, st>>>(d_labels, n, rk.p, k);
@@ -760,7 +760,7 @@ void sample_len_stats(const uint64_t* d_sample, const uint32_t* d_sample_labels,
                       std::vector<uint64_t>& count, cudaStream_t st) {
     DArr<unsigned long long> acc(2 * k, st);
     acc.zero();
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((S + 255) / 256, kSMs * 8));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((S + 255) / 256, num_sms() * 8));
     k_sample_len<<<grid, 256, 0, st>>>(d_sample, d_sample_labels, S, d_len, acc.p, acc.p + k);
     JB_LAUNCH_CHECK();
     auto h = acc.to_host(2 * k);
@@ -770,7 +770,7 @@ void sample_len_stats(const uint64_t* d_sample, const uint32_t* d_sample_labels,
 
 void gather_points(const double* d_pts, const uint64_t* d_idx, int64_t S, double* d_out,
                    cudaStream_t st) {
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((S + 255) / 256, kSMs * 8));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((S + 255) / 256, num_sms() * 8));
     {
         JB_PROF("sample_gather", st);
         k_gather<<<grid, 256, 0, st>>>(reinterpret_cast<const double2*>(d_pts), d_idx, S,
@@ -860,7 +860,7 @@ void symbolize_pieces(const int32_t* d_len, const double* d_inc, int64_t n,
     mm.upload(init, 4);
     DArr<int> bad(1, st);
     bad.zero();
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, kSMs * 8));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, num_sms() * 8));
     k_piece_extremes<<<grid, 256, 0, st>>>(d_len, d_inc, n, mm.p, bad.p);
     JB_LAUNCH_CHECK();
     std::vector<unsigned long long> h = mm.to_host(4);

@@ -269,7 +269,7 @@ __global__ void k_ga_labels(const unsigned long long* __restrict__ owner,
 }
 
 int gcap(int64_t n) {
-    return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)kSMs * 8));
+    return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8));
 }
 
 }  // namespace
@@ -349,7 +349,7 @@ void greedy_aggregate_device(const double* d_pts, int64_t n, double alpha, int s
     {
         JB_PROF("ga_sweep", st);
         JB_CUDA(cudaLaunchCooperativeKernel((const void*)k_ga_sweep,
-                                            dim3(kSMs * std::min(per_sm, 2)), dim3(GA_M), args, 0,
+                                            dim3(num_sms() * std::min(per_sm, 2)), dim3(GA_M), args, 0,
                                             st));
     }
     JB_LAUNCH_CHECK();

@@ -916,7 +916,7 @@ static void inverse_general(const InverseIn& in, const double* tabp, uint64_t kk
                                                               vstart.p, goff.p, gsum.p, err.p);
         JB_LAUNCH_CHECK();
         k_inv_segfix<<<(int)std::max<int64_t>(1, std::min<int64_t>((in.n_seg * 32 + 255) / 256,
-                                                                   (int64_t)kSMs * 16)),
+                                                                   (int64_t)num_sms() * 16)),
                        256, 0, st>>>(in, qlen.p, goff.p, gsum.p, rec.p, gmeta.p, d_out, err.p);
         JB_LAUNCH_CHECK();
     }
@@ -931,7 +931,7 @@ static void inverse_general(const InverseIn& in, const double* tabp, uint64_t kk
             JB_CUDA(cudaFuncSetAttribute(k_inv_fill, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)fsmem));
         const int grid = (int)std::max<int64_t>(
-            1, std::min<int64_t>((n_groups * 32 + FILL_TB - 1) / FILL_TB, (int64_t)kSMs * 16));
+            1, std::min<int64_t>((n_groups * 32 + FILL_TB - 1) / FILL_TB, (int64_t)num_sms() * 16));
         k_inv_fill<<<grid, FILL_TB, fsmem, st>>>(in, tabp + kk, qlen.p, vstart.p, rec.p, gmeta.p,
                                              n_groups, d_out);
         JB_LAUNCH_CHECK();

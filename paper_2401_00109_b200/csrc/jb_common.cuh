@@ -310,6 +310,22 @@ __device__ __forceinline__ unsigned long long dbits(double x) {
 
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 
-constexpr int kSMs = 148;
+// SMs of the current device, for grid sizing and cooperative launches (148
+// on a full B200; a MIG slice or an MPS SM limit exposes fewer)
+inline int num_sms() {
+    static int cache[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int& c = cache[dev & 63];
+    if (!c) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v < 1) {
+            cudaGetLastError();
+            v = 148;
+        }
+        c = v;
+    }
+    return c;
+}
 
 }  // namespace jb

@@ -260,7 +260,7 @@ __global__ void k_fy_resolve(const uint32_t* __restrict__ j, const uint32_t* __r
 }
 
 int grid_cap(uint64_t n, int tb = 256, int per_sm = 8) {
-    return (int)std::max<uint64_t>(1, std::min<uint64_t>((n + tb - 1) / tb, (uint64_t)kSMs * per_sm));
+    return (int)std::max<uint64_t>(1, std::min<uint64_t>((n + tb - 1) / tb, (uint64_t)num_sms() * per_sm));
 }
 
 }  // namespace
@@ -608,7 +608,7 @@ __device__ __forceinline__ void box_d2(double cx, double cy, const double4& b, d
 
 constexpr double kKeepMargin = 1e-12;
 
-// block-wide exclusive scan of int128 values (blockDim.x == 1024)
+// block-wide exclusive scan of int128 values (blockDim.x a multiple of 32)
 __device__ __forceinline__ i128 block_exscan_i128(i128 v, i128* total,
                                                   unsigned long long* s_lo,
                                                   unsigned long long* s_hi) {
@@ -629,7 +629,8 @@ __device__ __forceinline__ i128 block_exscan_i128(i128 v, i128* total,
     }
     __syncthreads();
     if (w == 0) {
-        unsigned long long a = s_lo[lane], b = s_hi[lane];
+        const bool in = lane < (int)(blockDim.x >> 5);
+        unsigned long long a = in ? s_lo[lane] : 0ULL, b = in ? s_hi[lane] : 0ULL;
         for (int o = 1; o < 32; o <<= 1) {
             const unsigned long long plo = __shfl_up_sync(0xffffffffu, a, o);
             const unsigned long long phi = __shfl_up_sync(0xffffffffu, b, o);
@@ -774,7 +775,7 @@ __global__ void __launch_bounds__(256) k_d2_tiles(
             if (init) {
                 v = dd;
                 d2s[r] = v;
-                fx_atomic_add(part + 2 * (o[i] / D2_R), fx_from_double(v, E));
+                if (part) fx_atomic_add(part + 2 * (o[i] / D2_R), fx_from_double(v, E));
             } else {
                 v = old[i];
                 if (dd < v) {  // std::min(d2, dd)
@@ -1171,6 +1172,419 @@ __global__ void __cluster_dims__(PC, 1, 1) __launch_bounds__(PICK_TB)
         ss->cursor += 1;
     }
     (void)lane;
+}
+
+// ---- persistent D^2 seeding: every round of d2_seed in ONE cooperative
+// launch (clustering.hpp:112-129). Per round:
+//   (1) CTA b sums its contiguous range of the original-order block
+//       partials into rtot[b], keeping the partials in shared memory;
+//       grid barrier;
+//   (2) every CTA scans the range totals (u, total: identical everywhere)
+//       and so knows the range holding the crossing; ITS CTA alone finds the
+//       block (from its staged partials) and the element (d2 of the block's
+//       2048 points) and publishes it through a round-tagged flag -- the
+//       others wait on the flag instead of a grid barrier, so nothing
+//       changes the d2 values while they are being read;
+//   (3) CTA b culls its own tiles (t = b, b + G, ...: a compact set of kept
+//       tiles spreads over all CTAs) against the new center and updates the
+//       kept ones with its warps; grid barrier.
+// Tile -> CTA ownership is static: each CTA keeps its tiles' cull boxes and
+// max d2 in shared memory for the whole launch, and d2 of a tile is only
+// ever written by one SM; data other CTAs wrote inside the launch is read
+// with ld.global.cg (L2).
+//
+// Fixed point: d2 -> floor(d2 * 2^E) with E chosen so the initial total is
+// < 2^107 (18 bits below the per-round path's scale, still ~2^-100 of the
+// total per unit), so every block partial lies in [0, 2^107) and is known
+// from its value mod 2^108. A block partial is two u64 limbs, L (bits 0-43
+// of each addend) and H (bits 44-107, wrapping): a changed point adds
+// (new - old) mod 2^108 as two fire-and-forget atomics, with no carry round
+// trip (a (lo, hi) int128 add must learn the low word's carry). The range
+// owner folds L into H every round, before any add, so L never overflows.
+// The prefix arithmetic is exact on these integers, as in k_pick. If the
+// total reaches 0 (every remaining point duplicates a center), the launch
+// stops before that round (flag[1]) and the per-round path finishes.
+constexpr int D2P_TB = 1024;
+
+struct D2Seed {
+    const double2* spts;
+    const uint32_t* orig;
+    const uint32_t* pos;
+    int64_t n;
+    const float4* cbox;
+    float* tmax;
+    int64_t ntiles;
+    double* d2s;
+    const unsigned long long* part;  // (lo, hi) partials after the init round
+    unsigned long long* part2;       // this launch's block partials: (L, H) limbs
+    int nblocks;
+    int E;
+    const uint64_t* raw;
+    SeedState* ss;
+    int64_t* chosen;
+    int k;
+    unsigned long long* rtot;  // (lo, hi) per CTA
+    int* flag;                 // [0] last published round (0 before launch), [1] exit round
+    unsigned long long* diag;
+    unsigned long long* phase;  // optional (JB_D2_PHASES): summed ns of 5 phases, CTAs 0 and 1
+    int ntl;                    // tiles per CTA (shared-memory arrays)
+};
+
+constexpr unsigned long long kM44 = (1ULL << 44) - 1;
+
+__device__ __forceinline__ i128 ldcg_i128(const unsigned long long* p) {
+    const unsigned long long lo = __ldcg(p), hi = __ldcg(p + 1);
+    return (i128)(((u128)hi << 64) | (u128)lo);
+}
+
+__global__ void __launch_bounds__(D2P_TB, 1) k_d2_seed(D2Seed P) {
+    namespace cgx = cooperative_groups;
+    cgx::grid_group grid = cgx::this_grid();
+    extern __shared__ unsigned long long s_dyn[];
+    const int ntl = P.ntl;
+    const int G = (int)gridDim.x, b = (int)blockIdx.x;
+    const int BR = (P.nblocks + G - 1) / G;  // blocks per range
+    float4* s_box = reinterpret_cast<float4*>(s_dyn);                      // my tiles' cull boxes
+    unsigned long long* s_part = s_dyn + 2 * ntl;                          // my range's partials (lo, hi)
+    float* s_tmax = reinterpret_cast<float*>(s_part + 2 * BR);             // my tiles' max d2
+    uint32_t* s_list = reinterpret_cast<uint32_t*>(s_tmax + ntl);          // kept tiles (local)
+    __shared__ unsigned long long s_lo[32], s_hi[32];
+    __shared__ int s_cnt, s_rc, s_fb;
+    __shared__ unsigned long long s_before[2], s_bbefore[2];
+    __shared__ long long s_next;
+    constexpr int NW = D2P_TB / 32;
+    constexpr int EP = D2_R / D2P_TB;  // elements of a block per thread
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    uint64_t cursor = P.ss->cursor;
+    int64_t last = P.ss->last;
+    const int QB = (BR + D2P_TB - 1) / D2P_TB;  // blocks per thread
+    const int r0 = min(P.nblocks, b * BR), r1 = min(P.nblocks, r0 + BR);
+    const int q0 = min(r1, r0 + t * QB), q1 = min(r1, q0 + QB);
+    for (int i = t; i < ntl; i += D2P_TB) {
+        const int64_t tt = (int64_t)b + (int64_t)i * G;
+        s_box[i] = tt < P.ntiles ? P.cbox[tt] : make_float4(0.f, 0.f, 0.f, 0.f);
+        s_tmax[i] = tt < P.ntiles ? P.tmax[tt] : -INFINITY;  // -inf: never kept
+    }
+    unsigned long long kept = 0;
+    unsigned long long tprev = 0;
+    auto stamp = [&](int i) {  // JB_D2_PHASES: CTA 0 and 1 sum their phase times
+        if (P.phase && t == 0 && b < 2) {
+            unsigned long long v;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+            if (i > 0) atomicAdd(P.phase + 5 * b + i - 1, v - tprev);
+            tprev = v;
+        }
+    };
+    int c = 1;
+    for (; c < P.k; ++c) {
+        stamp(0);
+        // ---- (1) my range total; partials normalised and staged ----
+        i128 mine = 0;
+        for (int j = q0; j < q1; ++j) {
+            u128 v;
+            if (c == 1) {
+                v = (u128)fx_load(P.part + 2 * j);  // the init round's sums, < 2^107
+            } else {
+                const unsigned long long L = __ldcg(P.part2 + 2 * j), H = __ldcg(P.part2 + 2 * j + 1);
+                v = ((u128)L + ((u128)H << 44)) & (((u128)1 << 108) - 1);
+            }
+            __stcg(P.part2 + 2 * j, (unsigned long long)v & kM44);
+            __stcg(P.part2 + 2 * j + 1, (unsigned long long)(v >> 44));
+            s_part[2 * (j - r0)] = (unsigned long long)v;
+            s_part[2 * (j - r0) + 1] = (unsigned long long)(v >> 64);
+            mine += (i128)v;
+        }
+        {
+            i128 rt;
+            block_exscan_i128(mine, &rt, s_lo, s_hi);
+            if (t == 0) {
+                __stcg(P.rtot + 2 * b, (unsigned long long)(u128)rt);
+                __stcg(P.rtot + 2 * b + 1, (unsigned long long)((u128)rt >> 64));
+            }
+        }
+        stamp(1);
+        grid.sync();
+        stamp(2);
+        // ---- (2) the pick ----
+        const i128 vr = t < G ? ldcg_i128(P.rtot + 2 * t) : (i128)0;
+        i128 total_fx;
+        const i128 exr = block_exscan_i128(vr, &total_fx, s_lo, s_hi);
+        if (total_fx == 0) break;  // uniform: the per-round path finishes
+        const double total = fx_to_double(total_fx, P.E);
+        const uint64_t x = P.raw[cursor];
+        double canon = __ull2double_rn(x) * 0x1p-64;  // generate_canonical<double,53>
+        if (canon >= 1.0) canon = 0x1.fffffffffffffp-1;
+        const double u = canon * total + 0.0;  // uniform_real(0, total)
+        const i128 U = fx_from_double(u, P.E);
+        if (t == 0) s_rc = -1;
+        __syncthreads();
+        if (t < G && U >= exr && U < exr + vr) {  // unique: vr > 0 there
+            s_rc = t;
+            s_before[0] = (unsigned long long)(u128)exr;
+            s_before[1] = (unsigned long long)((u128)exr >> 64);
+        }
+        __syncthreads();
+        const int rc = s_rc;
+        // the owner: the crossing range's CTA, or CTA 0 on a roundoff spill
+        // (U >= total): the same decision on every CTA
+        const int owner = rc >= 0 ? rc : 0;
+        int64_t next;
+        if (b == owner) {
+            if (t == 0) {
+                s_fb = -1;
+                s_next = -1;
+            }
+            __syncthreads();
+            if (rc >= 0) {
+                i128 dummy;
+                const i128 ex = fx_load(s_before) + block_exscan_i128(mine, &dummy, s_lo, s_hi);
+                if (U >= ex && U < ex + mine) {
+                    i128 run = ex;
+                    for (int j = q0; j < q1; ++j) {
+                        const i128 v = fx_load(s_part + 2 * (j - r0));
+                        if (U < run + v) {
+                            s_fb = j;
+                            s_bbefore[0] = (unsigned long long)(u128)run;
+                            s_bbefore[1] = (unsigned long long)((u128)run >> 64);
+                            break;
+                        }
+                        run += v;
+                    }
+                }
+                __syncthreads();
+                const int fb = s_fb;  // found: U lies inside this range
+                const int64_t e0 = (int64_t)fb * D2_R + (int64_t)EP * t;
+                i128 a[EP];
+                i128 ts = 0;
+#pragma unroll
+                for (int i = 0; i < EP; ++i) {
+                    const int64_t e = e0 + i;
+                    a[i] = (fb >= 0 && e < P.n) ? fx_from_double(__ldcg(P.d2s + P.pos[e]), P.E)
+                                                : (i128)0;
+                    ts += a[i];
+                }
+                const i128 ex3 = fx_load(s_bbefore) + block_exscan_i128(ts, &dummy, s_lo, s_hi);
+                if (fb >= 0 && U >= ex3 && U < ex3 + ts) {
+                    i128 run = ex3;
+#pragma unroll
+                    for (int i = 0; i < EP; ++i) {
+                        run += a[i];
+                        if (U < run) {
+                            s_next = e0 + i;
+                            break;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+            if (t == 0) {
+                long long nx = s_next;
+                if (nx < 0) {  // roundoff spill: last positive-weight index (:67-70)
+                    nx = P.n - 1;
+                    for (int64_t i = P.n - 1; i >= 0; --i)
+                        if (__ldcg(P.d2s + P.pos[i]) > 0.0) {
+                            nx = i;
+                            break;
+                        }
+                }
+                P.chosen[c] = nx;
+                s_next = nx;
+                __threadfence();
+                atomicExch(P.flag, c);  // publish round c
+            }
+            __syncthreads();
+            next = s_next;
+        } else {
+            if (t == 0) {
+                while (*(volatile int*)P.flag < c) {
+                }
+                __threadfence();
+                s_next = __ldcg((const long long*)P.chosen + c);
+            }
+            __syncthreads();
+            next = s_next;
+        }
+        cursor += 1;
+        last = next;
+        stamp(3);
+        if (c + 1 >= P.k) {
+            c = P.k;
+            break;
+        }
+        // ---- (3) cull + update my tiles against the new center ----
+        const double2 cc = P.spts[P.pos[next]];
+        if (t == 0) s_cnt = 0;
+        __syncthreads();
+        for (int i0 = 0; i0 < ntl; i0 += D2P_TB) {  // block-uniform trip count
+            const int i = i0 + t;
+            bool keep = false;
+            if (i < ntl) {
+                const float4 f = s_box[i];
+                double dmin2, dmax2;
+                box_d2(cc.x, cc.y, make_double4(f.x, f.y, f.z, f.w), dmin2, dmax2);
+                keep = !(dmin2 * (1.0 - kKeepMargin) > (double)s_tmax[i]);
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            if (m) {
+                int base = 0;
+                if (lane == 0) base = atomicAdd(&s_cnt, __popc(m));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (keep) s_list[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)i;
+            }
+        }
+        __syncthreads();
+        const int cnt = s_cnt;
+        if (t == 0) kept += (unsigned long long)cnt;
+        for (int li = w; li < cnt; li += NW) {
+            const int il = (int)s_list[li];
+            const int64_t tl = (int64_t)b + (int64_t)il * G;
+            double2 p[TILE / 32];
+            double old[TILE / 32];
+            uint32_t o[TILE / 32];
+#pragma unroll
+            for (int ii = 0; ii < TILE / 32; ++ii) {
+                const int64_t r = tl * TILE + ii * 32 + lane;
+                if (r < P.n) {
+                    p[ii] = P.spts[r];
+                    old[ii] = __ldcg(P.d2s + r);
+                    o[ii] = P.orig[r];
+                }
+            }
+            double mx = 0.0;
+#pragma unroll
+            for (int ii = 0; ii < TILE / 32; ++ii) {
+                const int64_t r = tl * TILE + ii * 32 + lane;
+                if (r >= P.n) break;
+                const double dd = dist2(p[ii].x, p[ii].y, cc.x, cc.y);
+                double v = old[ii];
+                if (dd < v) {  // std::min(d2, dd)
+                    const u128 dl = (u128)(fx_from_double(dd, P.E) - fx_from_double(v, P.E));
+                    unsigned long long* q2 = P.part2 + 2 * (o[ii] / D2_R);
+                    atomicAdd(q2, (unsigned long long)dl & kM44);
+                    atomicAdd(q2 + 1, (unsigned long long)(dl >> 44));  // bits 44-107 (mod 2^64)
+                    v = dd;
+                    __stcg(P.d2s + r, v);
+                }
+                mx = fmax(mx, v);
+            }
+            for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+            if (lane == 0) s_tmax[il] = __double2float_ru(mx);
+        }
+        stamp(4);
+        grid.sync();
+        stamp(5);
+    }
+    if (c < P.k) {  // early exit before round c: the tile maxima back for the per-round path
+        for (int i = t; i < ntl; i += D2P_TB) {
+            const int64_t tt = (int64_t)b + (int64_t)i * G;
+            if (tt < P.ntiles) P.tmax[tt] = s_tmax[i];
+        }
+    }
+    if (b == 0 && t == 0) {
+        P.ss->cursor = cursor;
+        P.ss->last = last;
+        P.flag[1] = c;
+    }
+    if (t == 0 && P.diag && kept) atomicAdd(P.diag, kept);
+}
+
+// the device supports cooperative launches (cached per process)
+bool coop_ok() {
+    static int coop = -1;
+    if (coop < 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev) != cudaSuccess) {
+            cudaGetLastError();
+            coop = 0;
+        }
+    }
+    return coop != 0;
+}
+
+// (lo, hi) partials of every block from the current d2 (the per-round
+// path's 128-bit scale), after an early exit of k_d2_seed
+__global__ void k_part_rebuild(const double* __restrict__ d2s, const uint32_t* __restrict__ orig,
+                               int64_t n, int E, unsigned long long* __restrict__ part) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x)
+        fx_atomic_add_small(part + 2 * (orig[r] / D2_R), (u128)fx_from_double(d2s[r], E));
+}
+
+struct D2Plan {
+    int G = 0;  // 0: no persistent launch
+    int ntl = 0;
+    size_t smem = 0;
+};
+
+// the persistent seeding grid: one 1024-thread CTA per SM, its tiles' cull
+// state and its range of partials in shared memory
+D2Plan d2_plan(int64_t ntiles, int nblocks) {
+    D2Plan p;
+    if (!coop_ok()) return p;
+    const int G = num_sms();
+    if (G > D2P_TB) return p;
+    const int ntl = (int)((ntiles + G - 1) / G);
+    const int BR = (nblocks + G - 1) / G;
+    const size_t smem = 24 * (size_t)ntl + 16 * (size_t)BR;
+    if (smem > 200 * 1024) return p;
+    if (cudaFuncSetAttribute(k_d2_seed, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess) {
+        cudaGetLastError();
+        return p;
+    }
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_d2_seed, D2P_TB, smem) != cudaSuccess ||
+        occ < 1) {
+        cudaGetLastError();
+        return p;
+    }
+    p.G = G;
+    p.ntl = ntl;
+    p.smem = smem;
+    return p;
+}
+
+// Rounds 1.. of d2_seed in one cooperative launch; returns the round the
+// per-round path continues from (k when done; 1 when the launch failed).
+uint64_t d2_seed_persistent(const D2Plan& pl, const double2* spts, const uint32_t* orig,
+                            const uint32_t* pos, int64_t n, const float4* cbox, float* tmax,
+                            int64_t ntiles, double* d2s, unsigned long long* part, int nblocks,
+                            int E, const uint64_t* raw, SeedState* ss, int64_t* chosen, int k,
+                            unsigned long long* diag, cudaStream_t st) {
+    static const bool phases = getenv("JB_D2_PHASES") != nullptr;
+    const int G = pl.G;
+    DArr<unsigned long long> part2(2 * (size_t)std::max(nblocks, 1), st);
+    DArr<unsigned long long> aux(2 * G + 1 + 10, st);  // range totals, flags, phase sums
+    JB_CUDA(cudaMemsetAsync(aux.p + 2 * G, 0, 8 * 11, st));
+    int* flag = reinterpret_cast<int*>(aux.p + 2 * G);
+    D2Seed a{spts, orig, pos, n, cbox, tmax, ntiles, d2s, part, part2.p, nblocks, E, raw, ss,
+             chosen, k, aux.p, flag, diag, phases ? aux.p + 2 * G + 1 : nullptr, pl.ntl};
+    void* args[] = {&a};
+    {
+        JB_PROF("d2_seed", st);
+        const cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_d2_seed, dim3(G),
+                                                          dim3(D2P_TB), args, pl.smem, st);
+        if (e != cudaSuccess) {  // cannot co-schedule: the per-round path from round 1
+            cudaGetLastError();
+            return 1;
+        }
+    }
+    JB_LAUNCH_CHECK();
+    int hf[2];
+    JB_CUDA(cudaMemcpyAsync(hf, flag, 8, cudaMemcpyDeviceToHost, st));
+    JB_CUDA(cudaStreamSynchronize(st));
+    if (phases) {
+        unsigned long long h[10];
+        JB_CUDA(cudaMemcpy(h, aux.p + 2 * G + 1, 80, cudaMemcpyDeviceToHost));
+        const double r = std::max(k - 1, 1), r2 = std::max(k - 2, 1);
+        for (int q = 0; q < 2; ++q)
+            fprintf(stderr, "[jb] d2 phases CTA %d (us/round, G=%d): sums %.2f sync1 %.2f "
+                            "pick %.2f cull+update %.2f sync2 %.2f\n",
+                    q, G, h[5 * q] * 1e-3 / r, h[5 * q + 1] * 1e-3 / r, h[5 * q + 2] * 1e-3 / r,
+                    h[5 * q + 3] * 1e-3 / r2, h[5 * q + 4] * 1e-3 / r2);
+    }
+    return (uint64_t)hf[1];
 }
 
 __global__ void k_copy_center(const double2* __restrict__ spts, const uint32_t* __restrict__ pos,
@@ -1904,7 +2318,7 @@ struct LloydCtx {
     }
     int grid() const {
         return (int)std::max<int64_t>(1, std::min<int64_t>((n + LL_TB - 1) / LL_TB,
-                                                           (int64_t)kSMs * 6));
+                                                           (int64_t)num_sms() * 6));
     }
 };
 
@@ -1946,13 +2360,13 @@ void lloyd_assign(LloydCtx& L, bool full, bool gate_on_empties) {
     {
         JB_PROF("lloyd_tile_check", L.st);
         k_super_check<<<(int)std::max<int64_t>(1, std::min<int64_t>((L.nsuper() + 255) / 256,
-                                                                   kSMs * 16)),
+                                                                   num_sms() * 16)),
                         256, sizeof(double) * 2 * L.k, L.st>>>(
             L.sbox.p, L.rg.R > 0 ? L.slenc.p : nullptr, L.ntiles, L.cg, L.centers.p, L.tlab.p,
             L.swork.p, L.nswork.p, gate, full ? 1 : 0, L.rg, L.k);
         k_tile_expand<<<full ? (int)std::max<int64_t>(1, std::min<int64_t>((L.nsuper() + 7) / 8,
-                                                                            kSMs * 16))
-                             : kSMs * 4,
+                                                                            num_sms() * 16))
+                             : num_sms() * 4,
                         256, sizeof(double) * 2 * L.k, L.st>>>(
             L.swork.p, L.nswork.p, L.tbox, L.rg.R > 0 ? L.tlen : nullptr, L.ntiles, L.cg,
             L.centers.p, L.tlab.p, L.tnew.p, L.work.p, L.nwork.p, gate, full ? 1 : 0, L.rg, L.k);
@@ -2119,8 +2533,12 @@ bool lloyd_persistent(LloydCtx& L, int budget) {
     void* args[] = {&a};
     {
         JB_PROF("lloyd_persistent", L.st);
-        JB_CUDA(cudaLaunchCooperativeKernel((const void*)k_lloyd_persistent, dim3(kSMs * per_sm),
-                                            dim3(256), args, smem, L.st));
+        const cudaError_t e = cudaLaunchCooperativeKernel(
+            (const void*)k_lloyd_persistent, dim3(num_sms() * per_sm), dim3(256), args, smem, L.st);
+        if (e != cudaSuccess) {  // cannot co-schedule (MPS/MIG limits): multi-kernel path
+            cudaGetLastError();
+            return false;
+        }
     }
     if (phase_times) {  // JB_LLOYD_PHASES=1: mean phase latencies (us) on stderr
         auto h = tsb.to_host(6 * 512);
@@ -2139,7 +2557,7 @@ bool lloyd_persistent(LloydCtx& L, int budget) {
             fprintf(stderr, "[jb] lloyd phases over %d iters (us): means %.1f grid %.1f super %.1f "
                             "expand %.1f work %.1f (grid %d x 256), %d grid rebuilds\n",
                     cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt,
-                    kSMs * per_sm, rebuilds);
+                    num_sms() * per_sm, rebuilds);
             for (int qq = 0; qq < 4; ++qq)
                 fprintf(stderr, "[jb]   quarter %d: means %.1f grid %.1f super %.1f expand %.1f work %.1f\n",
                         qq, quart[qq][0] / (cnt / 4.0), quart[qq][1] / (cnt / 4.0),
@@ -2167,7 +2585,7 @@ void lloyd_repair(LloydCtx& L, int ne) {
     JB_CUDA(cudaMemcpyAsync(em.data(), L.empties.p, sizeof(int) * ne, cudaMemcpyDeviceToHost,
                             L.st));
     JB_CUDA(cudaStreamSynchronize(L.st));
-    const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>((L.n + 255) / 256, kSMs * 4));
+    const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>((L.n + 255) / 256, num_sms() * 4));
     if (L.far_blk.n < (size_t)(3 * nblk)) L.far_blk.alloc(3 * nblk, L.st);
     for (int c : em) {
         k_far_block<<<nblk, 256, 0, L.st>>>(L.spts, L.orig, L.n, L.labs.p, L.centers.p,
@@ -2268,7 +2686,7 @@ void lloyd_best_device(const PtsView& pv, const uint64_t* d_idx, int64_t n, uint
     const int64_t ntiles = (n + TILE - 1) / TILE;
     DArr<double4> tbox(ntiles, st);
     DArr<float> tmax(ntiles, st);  // per-tile max d2, rounded up (D^2 cull)
-    const int tile_grid = (int)std::max<int64_t>(1, std::min<int64_t>((ntiles + 7) / 8, kSMs * 8));
+    const int tile_grid = (int)std::max<int64_t>(1, std::min<int64_t>((ntiles + 7) / 8, num_sms() * 8));
     k_tile_boxes<<<tile_grid, 256, 0, st>>>(spts.p, n, tbox.p, rows.len ? slen.p : nullptr,
                                             tlen.p);
     DArr<float4> cbox(ntiles, st);
@@ -2339,7 +2757,7 @@ void lloyd_best_device(const PtsView& pv, const uint64_t* d_idx, int64_t n, uint
     L.sbox.alloc(std::max<int64_t>(L.nsuper(), 1), st);
     L.slenc.alloc(std::max<int64_t>(L.nsuper(), 1), st);
     if (ntiles > 0)
-        k_super_boxes<<<(int)std::max<int64_t>(1, std::min<int64_t>((L.nsuper() + 7) / 8, kSMs * 8)),
+        k_super_boxes<<<(int)std::max<int64_t>(1, std::min<int64_t>((L.nsuper() + 7) / 8, num_sms() * 8)),
                         256, 0, st>>>(tbox.p, rows.len ? tlen.p : nullptr, ntiles, L.sbox.p,
                                       L.slenc.p);
     L.work.alloc(std::max<int64_t>(ntiles, 1), st);
@@ -2358,7 +2776,7 @@ void lloyd_best_device(const PtsView& pv, const uint64_t* d_idx, int64_t n, uint
     DArr<uint32_t> d2_work(ntiles, st);
     DArr<unsigned long long> d2_nwork(1, st);
     const int cull_grid =
-        (int)std::max<int64_t>(1, std::min<int64_t>((ntiles + 1023) / 1024, kSMs * 8));
+        (int)std::max<int64_t>(1, std::min<int64_t>((ntiles + 1023) / 1024, num_sms() * 8));
     DArr<double> d2s(n, st);
     DArr<unsigned long long> part(2 * nblocks, st);
     DArr<SeedState> ss(1, st);
@@ -2372,22 +2790,40 @@ void lloyd_best_device(const PtsView& pv, const uint64_t* d_idx, int64_t n, uint
         SeedState h{*cursor, 0, 0, 0};
         ss.upload(&h, 1);
         part.zero();
+        // all rounds in one cooperative launch when the device can co-schedule
+        // it (two-limb partials, E - 18: k_d2_seed), else -- or from the
+        // round where it stops -- one pick + cull + update launch per round
+        // on the 128-bit scale
+        const D2Plan plan = (k > 1 && !getenv("JB_D2_NO_PERSIST")) ? d2_plan(ntiles, nblocks)
+                                                                    : D2Plan{};
+        const int Einit = plan.G ? Ed2 - 18 : Ed2;
         k_pick_first<<<1, 1, 0, st>>>(d_raw, (uint64_t)n, ss.p, chosen.p);
         JB_LAUNCH_CHECK();
         {
             JB_PROF("d2_update", st);
             k_d2_tiles<<<tile_grid, 256, 0, st>>>(spts.p, orig.p, pos.p, n, nullptr, nullptr,
-                                                  tmax.p, d2s.p, ss.p, 1, Ed2, part.p, nullptr,
+                                                  tmax.p, d2s.p, ss.p, 1, Einit, part.p, nullptr,
                                                   nullptr, d2_diag.p);
         }
         JB_LAUNCH_CHECK();
+        uint64_t c_from = 1;
+        if (plan.G) {
+            c_from = d2_seed_persistent(plan, spts.p, orig.p, pos.p, n, cbox.p, tmax.p, ntiles,
+                                        d2s.p, part.p, nblocks, Ed2 - 18, d_raw, ss.p, chosen.p,
+                                        (int)k, d2_diag.p, st);
+            if (c_from < k) {  // rebuild the partials on the 128-bit scale
+                part.zero();
+                k_part_rebuild<<<grid_cap(n), 256, 0, st>>>(d2s.p, orig.p, n, Ed2, part.p);
+                JB_LAUNCH_CHECK();
+            }
+        }
         // cluster pick when every CTA's share of the partials fits its smem
         const size_t pick_smem = 16 * (size_t)((nblocks + PC - 1) / PC);
         const bool cluster_pick = pick_smem <= kPickClusterSmem;
-        if (cluster_pick)
+        if (cluster_pick && c_from < k)
             JB_CUDA(cudaFuncSetAttribute(k_pick_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)std::max<size_t>(pick_smem, 16)));
-        for (uint64_t c = 1; c < k; ++c) {
+        for (uint64_t c = c_from; c < k; ++c) {
             {
                 JB_PROF("d2_pick", st);
                 if (cluster_pick)
@@ -2973,7 +3409,7 @@ void lloyd_best_dist(const Comm& cm, const PtsView& pv, const uint64_t* d_lidx,
     const int64_t ntiles = (n + TILE - 1) / TILE;
     DArr<double4> tbox(std::max<int64_t>(ntiles, 1), st);
     DArr<float> tmax(std::max<int64_t>(ntiles, 1), st);  // per-tile max d2, rounded up
-    const int tile_grid = (int)std::max<int64_t>(1, std::min<int64_t>((ntiles + 7) / 8, kSMs * 8));
+    const int tile_grid = (int)std::max<int64_t>(1, std::min<int64_t>((ntiles + 7) / 8, num_sms() * 8));
     if (n > 0)
         k_tile_boxes<<<tile_grid, 256, 0, st>>>(spts.p, n, tbox.p, rows.len ? slen.p : nullptr,
                                                 tlen.p);
@@ -3042,7 +3478,7 @@ void lloyd_best_dist(const Comm& cm, const PtsView& pv, const uint64_t* d_lidx,
     L.sbox.alloc(std::max<int64_t>(L.nsuper(), 1), st);
     L.slenc.alloc(std::max<int64_t>(L.nsuper(), 1), st);
     if (ntiles > 0)
-        k_super_boxes<<<(int)std::max<int64_t>(1, std::min<int64_t>((L.nsuper() + 7) / 8, kSMs * 8)),
+        k_super_boxes<<<(int)std::max<int64_t>(1, std::min<int64_t>((L.nsuper() + 7) / 8, num_sms() * 8)),
                         256, 0, st>>>(tbox.p, rows.len ? tlen.p : nullptr, ntiles, L.sbox.p,
                                       L.slenc.p);
     L.work.alloc(std::max<int64_t>(ntiles, 1), st);
@@ -3060,7 +3496,7 @@ void lloyd_best_dist(const Comm& cm, const PtsView& pv, const uint64_t* d_lidx,
     DArr<uint32_t> d2_work(std::max<int64_t>(ntiles, 1), st);
     DArr<unsigned long long> d2_nwork(1, st);
     const int cull_grid =
-        (int)std::max<int64_t>(1, std::min<int64_t>((ntiles + 1023) / 1024, kSMs * 8));
+        (int)std::max<int64_t>(1, std::min<int64_t>((ntiles + 1023) / 1024, num_sms() * 8));
     DArr<double> d2s(nn, st);
     DArr<unsigned long long> part(2 * nblocks, st);
     DArr<SeedState> ss(1, st);
@@ -3125,7 +3561,7 @@ void lloyd_best_dist(const Comm& cm, const PtsView& pv, const uint64_t* d_lidx,
         std::vector<int> em(ne);
         L.empties.download(em.data(), ne);
         JB_CUDA(cudaStreamSynchronize(st));
-        const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, kSMs * 4));
+        const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, num_sms() * 4));
         if (L.far_blk.n < (size_t)(3 * nblk)) L.far_blk.alloc(3 * nblk, st);
         for (int c : em) {
             FarRec mine{-1.0, INT64_MAX, -1, 0.0, 0.0, -1};
@@ -3328,7 +3764,7 @@ void lloyd_best_dist(const Comm& cm, const PtsView& pv, const uint64_t* d_lidx,
         dp.zero();
         DArr<unsigned long long> p3(3 * nblocks, st), gpart(2 * nblocks, st), w(D2_R, st), cb(2, st);
         const double2* curp = reinterpret_cast<const double2*>(cb.p);
-        const int pg = (int)std::max<uint64_t>(1, std::min<uint64_t>((nblocks + 255) / 256, kSMs * 4));
+        const int pg = (int)std::max<uint64_t>(1, std::min<uint64_t>((nblocks + 255) / 256, num_sms() * 4));
         part.zero();
         k_pick_first<<<1, 1, 0, st>>>(d_raw, S, dss.p, dch.p);
         k_dcenter_bits<<<1, 1, 0, st>>>(d_gpos, pos.p, spts.p, n, dch.p, 0, cb.p);

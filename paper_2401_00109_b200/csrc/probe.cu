@@ -30,7 +30,7 @@ extern "C" jb_status jb_probe_fp64_tflops(int device, double* tflops) {
     try {
         JB_CUDA(cudaSetDevice(device));
         DArr<double> out(1, 0);
-        const int grid = kSMs * 8, tb = 256, iters = 20000;
+        const int grid = num_sms() * 8, tb = 256, iters = 20000;
         k_dfma_chain<<<grid, tb>>>(out.p, 100, 0.999999, 1e-9);  // warm-up
         cudaEvent_t a, b;
         JB_CUDA(cudaEventCreate(&a));

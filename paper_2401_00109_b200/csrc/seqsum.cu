@@ -771,7 +771,7 @@ std::vector<double> range_seq_sums(const RangeHist& h, const SeqTerms& t,
     const double* bsum = h.approx.p;  // the producer's per-record approximate sums
     DArr<double> gpre(std::max<int64_t>(nrec, 1), st);
     auto grid_for_n = [](int64_t m) {
-        return (int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, kSMs * 16));
+        return (int)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, num_sms() * 16));
     };
     std::vector<double> local_total(k, 0.0);
     if (nrec > 0) {
@@ -830,7 +830,7 @@ std::vector<double> range_seq_sums(const RangeHist& h, const SeqTerms& t,
                                                      sin_d.p, rel, be.p, pe.p, po.p);
         JB_LAUNCH_CHECK();
         if (h.long_idx.p)
-            k_rs_long<<<kSMs * 4, 256, 0, st>>>(t, h.long_idx.p, h.long_n.p, h.R, k, d_labels, be.p,
+            k_rs_long<<<num_sms() * 4, 256, 0, st>>>(t, h.long_idx.p, h.long_n.p, h.R, k, d_labels, be.p,
                                                 pe.p, po.p);
         JB_LAUNCH_CHECK();
         k_rs_level<<<blocks_for_warps(n2 * k), 256, 0, st>>>(nr, k, be.p, pe.p, po.p, n2, e2.p,
