@@ -181,7 +181,7 @@ __device__ __forceinline__ int row_word_count(uint64_t w) {
     return n;
 }
 __device__ __forceinline__ uint32_t row_word_cand(const uint16_t* spill, uint64_t w, int j) {
-    if ((w & 0xFFFF) == kRowSpill) return __ldg(spill + (size_t)(w >> 32) * kSpill + j);
+    if ((w & 0xFFFF) == kRowSpill) return __ldcg(spill + (size_t)(w >> 32) * kSpill + j);
     return (uint32_t)((w >> (16 * j)) & 0xFFFF);
 }
 
@@ -191,8 +191,8 @@ __device__ __forceinline__ uint64_t row_cell_word(const RowGrid& rg, int32_t len
     if (len < 1 || len > rg.R) return ~0ull;
     int iy = (int)((py - rg.y0) * rg.invh);
     iy = min(max(iy, 0), rg.Gy - 1);
-    return __ldg(reinterpret_cast<const unsigned long long*>(rg.cell) + (size_t)(len - 1) * rg.Gy +
-                 iy);
+    return __ldcg(reinterpret_cast<const unsigned long long*>(rg.cell) + (size_t)(len - 1) * rg.Gy +
+                  iy);
 }
 
 // nearest_center (clustering.hpp:146-157) of a piece at (px, py) whose row
@@ -204,10 +204,10 @@ __device__ __forceinline__ uint32_t row_nearest_w(const CandGrid& g, const uint1
     if (c0 == kRowSpill) {
         const uint16_t* sl = spill + (size_t)(w >> 32) * kSpill;
         const int nc = (int)((w >> 16) & 0xFFFF);
-        uint32_t best = __ldg(sl);
+        uint32_t best = __ldcg(sl);
         double bd = dist2(px, py, cx[best], cy[best]);
         for (int j = 1; j < nc; ++j) {
-            const uint32_t c = __ldg(sl + j);
+            const uint32_t c = __ldcg(sl + j);
             const double d = dist2(px, py, cx[c], cy[c]);
             if (d < bd) {
                 bd = d;

@@ -1634,7 +1634,7 @@ __device__ __forceinline__ bool row_tile_single(const RowGrid& rg, int l, const 
         reinterpret_cast<const unsigned long long*>(rg.cell) + (size_t)(l - 1) * rg.Gy + iy0;
     uint64_t wv[8];  // all cell words first: independent loads
 #pragma unroll
-    for (int j = 0; j < 8; ++j) wv[j] = j < nc ? __ldg(row + j) : ~0ull;
+    for (int j = 0; j < 8; ++j) wv[j] = j < nc ? __ldcg(row + j) : ~0ull;
     double M = INFINITY;
     for (int j = 0; j < 8; ++j) {
         if (j >= nc) break;
@@ -1739,8 +1739,8 @@ __device__ __forceinline__ uint32_t box_single_g8(const double4& b, int l, const
     }
     uint64_t wv = ~0ull;
     if (row && sub < nc)
-        wv = __ldg(reinterpret_cast<const unsigned long long*>(rg.cell) + (size_t)(l - 1) * rg.Gy +
-                   iy0 + sub);
+        wv = __ldcg(reinterpret_cast<const unsigned long long*>(rg.cell) + (size_t)(l - 1) * rg.Gy +
+                    iy0 + sub);
     bool bad = row && sub < nc && (wv & 0xFFFF) >= kRowOverflow;
     double M = INFINITY;
     int ncand = 0;
@@ -1918,6 +1918,126 @@ __global__ void k_super_boxes(const double4* __restrict__ tbox, const int32_t* _
 // (full) assignment accumulates per block in shared memory; the incremental
 // ones move few points, so each (old, new) label group of a warp adds its
 // deltas straight to the global accumulators (native 64-bit atomics in L2).
+// One listed tile, one warp: labels := the single center, or nearest_center
+// through the grids; exact integer deltas of the cluster sums (FULL: into
+// the block's shared accumulators s_sx/s_sy/s_cnt; else (old, new) groups
+// straight to the global limbs).
+template <bool FULL>
+__device__ __forceinline__ void lloyd_tile(
+    uint32_t t, uint32_t single, const double2* __restrict__ spts, int64_t n,
+    const double* __restrict__ cx, const double* __restrict__ cy, int k, CandGrid g,
+    uint32_t* __restrict__ labs, uint32_t* __restrict__ tlab, int Ex, int Ey, ClusterAcc acc,
+    RowGrid rg, const int32_t* __restrict__ slen, AggScratch* agg,
+    unsigned long long* s_sx, unsigned long long* s_sy, unsigned long long* s_cnt,
+    unsigned long long& my_changed) {
+    const int lane = threadIdx.x & 31;
+    uint32_t old[TILE / 32];
+#pragma unroll
+    for (int i = 0; i < TILE / 32; ++i) {
+        const int64_t r = (int64_t)t * TILE + i * 32 + lane;
+        old[i] = (r < n && !FULL) ? __ldcg(labs + r) : 0u;  // written by other SMs in-kernel
+    }
+    // all loads of the tile first (points, lengths, then row-cell words),
+    // so a tile costs about three dependent memory latencies, not twelve
+    double2 pt[TILE / 32];
+    int32_t ln[TILE / 32];
+    uint64_t cw[TILE / 32];
+    uint32_t bst[TILE / 32];
+#pragma unroll
+    for (int i = 0; i < TILE / 32; ++i) {
+        const int64_t r = (int64_t)t * TILE + i * 32 + lane;
+        const bool valid = r < n;
+        // not gated on old[i]: the point loads go out with the label loads
+        // (one memory round trip instead of two; unused points cost 2 KB)
+        pt[i] = valid ? spts[r] : make_double2(0.0, 0.0);
+        ln[i] = (valid && single == MIXED && slen) ? slen[r] : 0;
+    }
+    if (single == MIXED && slen) {
+#pragma unroll
+        for (int i = 0; i < TILE / 32; ++i) {
+            cw[i] = ~0ull;  // not built: fallback
+            if (ln[i] >= 1 && ln[i] <= rg.R) {
+                int iy = (int)((pt[i].y - rg.y0) * rg.invh);
+                iy = min(max(iy, 0), rg.Gy - 1);
+                cw[i] = __ldcg(reinterpret_cast<const unsigned long long*>(rg.cell) +
+                               (size_t)(ln[i] - 1) * rg.Gy + iy);
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < TILE / 32; ++i) {
+        const int64_t r = (int64_t)t * TILE + i * 32 + lane;
+        bst[i] = single;
+        if (r < n && single == MIXED)
+            bst[i] = slen ? row_pick(cw[i], g, rg.spill, pt[i].x, pt[i].y, cx, cy, k)
+                          : grid_nearest(g, pt[i].x, pt[i].y, cx, cy, k);
+    }
+    auto flush = [&](uint32_t kk, u128 sa, u128 sb, unsigned long long, int cnt) {
+        if (FULL) {
+            fx_atomic_add(s_sx + 2 * kk, (i128)sa);
+            fx_atomic_add(s_sy + 2 * kk, (i128)sb);
+            atomicAdd(s_cnt + kk, (unsigned long long)cnt);
+        } else {
+            const uint32_t nb = kk & 0xFFFFu, ob = kk >> 16;
+            l3_add(acc.sx + 3 * nb, (i128)sa);
+            l3_add(acc.sy + 3 * nb, (i128)sb);
+            atomicAdd(acc.cnt + nb, (unsigned long long)cnt);
+            l3_add(acc.sx + 3 * ob, -(i128)sa);
+            l3_add(acc.sy + 3 * ob, -(i128)sb);
+            atomicAdd(acc.cnt + ob, (unsigned long long)(-(long long)cnt));
+        }
+    };
+    bool mv[TILE / 32];
+    uint32_t key[TILE / 32];
+    uint32_t key0 = 0xFFFFFFFFu;  // the first moved point's key (lane order, round order)
+#pragma unroll
+    for (int i = 0; i < TILE / 32; ++i) {
+        const int64_t r = (int64_t)t * TILE + i * 32 + lane;
+        const bool valid = r < n;
+        const uint32_t best = valid ? bst[i] : 0u;
+        mv[i] = valid && (FULL || old[i] != best);
+        if (mv[i]) labs[r] = best;
+        if (!FULL && mv[i]) ++my_changed;
+        key[i] = FULL ? best : ((old[i] << 16) | best);
+        const unsigned bm = __ballot_sync(0xffffffffu, mv[i]);
+        if (key0 == 0xFFFFFFFFu && bm) key0 = __shfl_sync(0xffffffffu, key[i], __ffs(bm) - 1);
+    }
+    bool uni = true;  // every moved point shares one (old, new) pair: the SINGLE-tile case
+#pragma unroll
+    for (int i = 0; i < TILE / 32; ++i) uni &= !mv[i] || key[i] == key0;
+    uni = __all_sync(0xffffffffu, uni);
+    if (uni) {
+        if (key0 != 0xFFFFFFFFu) {  // one tree reduction and one set of atomics per tile
+            i128 sa = 0, sb = 0;
+            int cnt = 0;
+#pragma unroll
+            for (int i = 0; i < TILE / 32; ++i)
+                if (mv[i]) {
+                    sa += fx_from_double(pt[i].x, Ex);
+                    sb += fx_from_double(pt[i].y, Ey);
+                    ++cnt;
+                }
+            sa = fx_warp_sum(sa);
+            sb = fx_warp_sum(sb);
+            for (int o = 16; o > 0; o >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, o);
+            if (lane == 0) flush(key0, (u128)sa, (u128)sb, 0ULL, cnt);
+        }
+    } else {
+        // group lanes by (old, new) label pair; one set of atomics per group
+#pragma unroll
+        for (int i = 0; i < TILE / 32; ++i) {
+            const i128 fx = mv[i] ? fx_from_double(pt[i].x, Ex) : (i128)0;
+            const i128 fy = mv[i] ? fx_from_double(pt[i].y, Ey) : (i128)0;
+            warp_aggregate(mv[i], key[i], (u128)fx, (u128)fy, 0ULL, agg, flush);
+        }
+    }
+    if (lane == 0) tlab[t] = single;
+}
+
+// One warp per listed tile (lloyd_tile). The first (full) assignment
+// accumulates per block in shared memory; the incremental ones move few
+// points, so each (old, new) label group of a warp adds its deltas straight
+// to the global accumulators (native 64-bit atomics in L2).
 template <bool FULL>
 __device__ __forceinline__ void lloyd_work_body(
     const double2* __restrict__ spts, int64_t n, const double* __restrict__ centers, int k,
@@ -1952,111 +2072,9 @@ __device__ __forceinline__ void lloyd_work_body(
     unsigned long long my_changed = 0;
     for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < nw;
          w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-      {
         const uint32_t t = work[w];
-        const uint32_t single = tnew[t];
-        uint32_t old[TILE / 32];
-#pragma unroll
-        for (int i = 0; i < TILE / 32; ++i) {
-            const int64_t r = (int64_t)t * TILE + i * 32 + lane;
-            old[i] = (r < n && !FULL) ? labs[r] : 0u;
-        }
-        // all loads of the tile first (points, lengths, then row-cell words),
-        // so a tile costs about three dependent memory latencies, not twelve
-        double2 pt[TILE / 32];
-        int32_t ln[TILE / 32];
-        uint64_t cw[TILE / 32];
-        uint32_t bst[TILE / 32];
-#pragma unroll
-        for (int i = 0; i < TILE / 32; ++i) {
-            const int64_t r = (int64_t)t * TILE + i * 32 + lane;
-            const bool valid = r < n;
-            // not gated on old[i]: the point loads go out with the label loads
-            // (one memory round trip instead of two; unused points cost 2 KB)
-            pt[i] = valid ? spts[r] : make_double2(0.0, 0.0);
-            ln[i] = (valid && single == MIXED && slen) ? slen[r] : 0;
-        }
-        if (single == MIXED && slen) {
-#pragma unroll
-            for (int i = 0; i < TILE / 32; ++i) {
-                cw[i] = ~0ull;  // not built: fallback
-                if (ln[i] >= 1 && ln[i] <= rg.R) {
-                    int iy = (int)((pt[i].y - rg.y0) * rg.invh);
-                    iy = min(max(iy, 0), rg.Gy - 1);
-                    cw[i] = __ldg(reinterpret_cast<const unsigned long long*>(rg.cell) +
-                                  (size_t)(ln[i] - 1) * rg.Gy + iy);
-                }
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < TILE / 32; ++i) {
-            const int64_t r = (int64_t)t * TILE + i * 32 + lane;
-            bst[i] = single;
-            if (r < n && single == MIXED)
-                bst[i] = slen ? row_pick(cw[i], g, rg.spill, pt[i].x, pt[i].y, cx, cy, k)
-                              : grid_nearest(g, pt[i].x, pt[i].y, cx, cy, k);
-        }
-        auto flush = [&](uint32_t kk, u128 sa, u128 sb, unsigned long long, int cnt) {
-            if (FULL) {
-                fx_atomic_add(s_sx + 2 * kk, (i128)sa);
-                fx_atomic_add(s_sy + 2 * kk, (i128)sb);
-                atomicAdd(s_cnt + kk, (unsigned long long)cnt);
-            } else {
-                const uint32_t nb = kk & 0xFFFFu, ob = kk >> 16;
-                l3_add(acc.sx + 3 * nb, (i128)sa);
-                l3_add(acc.sy + 3 * nb, (i128)sb);
-                atomicAdd(acc.cnt + nb, (unsigned long long)cnt);
-                l3_add(acc.sx + 3 * ob, -(i128)sa);
-                l3_add(acc.sy + 3 * ob, -(i128)sb);
-                atomicAdd(acc.cnt + ob, (unsigned long long)(-(long long)cnt));
-            }
-        };
-        bool mv[TILE / 32];
-        uint32_t key[TILE / 32];
-        uint32_t key0 = 0xFFFFFFFFu;  // the first moved point's key (lane order, round order)
-#pragma unroll
-        for (int i = 0; i < TILE / 32; ++i) {
-            const int64_t r = (int64_t)t * TILE + i * 32 + lane;
-            const bool valid = r < n;
-            const uint32_t best = valid ? bst[i] : 0u;
-            mv[i] = valid && (FULL || old[i] != best);
-            if (mv[i]) labs[r] = best;
-            if (!FULL && mv[i]) ++my_changed;
-            key[i] = FULL ? best : ((old[i] << 16) | best);
-            const unsigned bm = __ballot_sync(0xffffffffu, mv[i]);
-            if (key0 == 0xFFFFFFFFu && bm) key0 = __shfl_sync(0xffffffffu, key[i], __ffs(bm) - 1);
-        }
-        bool uni = true;  // every moved point shares one (old, new) pair: the SINGLE-tile case
-#pragma unroll
-        for (int i = 0; i < TILE / 32; ++i) uni &= !mv[i] || key[i] == key0;
-        uni = __all_sync(0xffffffffu, uni);
-        if (uni) {
-            if (key0 != 0xFFFFFFFFu) {  // one tree reduction and one set of atomics per tile
-                i128 sa = 0, sb = 0;
-                int cnt = 0;
-#pragma unroll
-                for (int i = 0; i < TILE / 32; ++i)
-                    if (mv[i]) {
-                        sa += fx_from_double(pt[i].x, Ex);
-                        sb += fx_from_double(pt[i].y, Ey);
-                        ++cnt;
-                    }
-                sa = fx_warp_sum(sa);
-                sb = fx_warp_sum(sb);
-                for (int o = 16; o > 0; o >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, o);
-                if (lane == 0) flush(key0, (u128)sa, (u128)sb, 0ULL, cnt);
-            }
-        } else {
-            // group lanes by (old, new) label pair; one set of atomics per group
-#pragma unroll
-            for (int i = 0; i < TILE / 32; ++i) {
-                const i128 fx = mv[i] ? fx_from_double(pt[i].x, Ex) : (i128)0;
-                const i128 fy = mv[i] ? fx_from_double(pt[i].y, Ey) : (i128)0;
-                warp_aggregate(mv[i], key[i], (u128)fx, (u128)fy, 0ULL, agg, flush);
-            }
-        }
-        if (lane == 0) tlab[t] = single;
-      }
+        lloyd_tile<FULL>(t, tnew[t], spts, n, cx, cy, k, g, labs, tlab, Ex, Ey, acc, rg, slen, agg,
+                         s_sx, s_sy, s_cnt, my_changed);
     }
     for (int o = 16; o > 0; o >>= 1) my_changed += __shfl_down_sync(0xffffffffu, my_changed, o);
     if (lane == 0 && my_changed) atomicAdd(&s_changed, my_changed);
@@ -2423,6 +2441,7 @@ struct PersistArgs {
     int budget;
     unsigned long long* tstamp;  // optional: 6 globaltimer stamps per iteration (block 0)
     double* mov;                 // row-grid movement state (means_body)
+    unsigned long long* cnt2;    // persistent loop: changed[2], listed super-tiles[2] (by parity)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -2431,42 +2450,195 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
+// update_means (clustering.hpp:177-180) computed by EVERY block from the
+// global limbs into its shared copy of the centers (identical on every
+// block: the same integers, the same operations), so no block waits for
+// another to publish them. Returns the number of empty clusters (listed in
+// index order into empties when non-null) and the largest center
+// displacement (rounded up), both uniform over the block.
+__device__ __forceinline__ void means_local(ClusterAcc acc, int k, int Ex, int Ey, double* s_c,
+                                            int* __restrict__ empties, int& n_empty,
+                                            double& dmax_out) {
+    __shared__ int wc[32];
+    __shared__ int base;
+    __shared__ double wmax[32];
+    double dmax = 0.0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) base = 0;
+    __syncthreads();
+    for (int c0 = 0; c0 < k; c0 += blockDim.x) {
+        const int c = c0 + threadIdx.x;
+        bool empty = false;
+        if (c < k) {
+            const long long cnt = (long long)__ldcg(acc.cnt + c);
+            const i128 sx = (i128)((u128)__ldcg(acc.sx + 3 * c) + ((u128)__ldcg(acc.sx + 3 * c + 1) << 32) +
+                                   ((u128)__ldcg(acc.sx + 3 * c + 2) << 64));
+            const i128 sy = (i128)((u128)__ldcg(acc.sy + 3 * c) + ((u128)__ldcg(acc.sy + 3 * c + 1) << 32) +
+                                   ((u128)__ldcg(acc.sy + 3 * c + 2) << 64));
+            if (cnt > 0) {
+                const double nx = fx_to_double(sx, Ex) / (double)cnt;
+                const double ny = fx_to_double(sy, Ey) / (double)cnt;
+                const double dx = nx - s_c[2 * c], dy = ny - s_c[2 * c + 1];
+                dmax = fmax(dmax, sqrt(dx * dx + dy * dy) * (1.0 + 1e-12) + 1e-300);
+                s_c[2 * c] = nx;
+                s_c[2 * c + 1] = ny;
+            } else {
+                empty = true;
+            }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, empty);
+        if (lane == 0) wc[warp] = __popc(m);
+        __syncthreads();
+        int off = base;
+        for (int w = 0; w < warp; ++w) off += wc[w];
+        if (empty && empties) empties[off + __popc(m & ((1u << lane) - 1u))] = c;
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) base += wc[w];
+        __syncthreads();
+    }
+    for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+    if (lane == 0) wmax[warp] = dmax;
+    __syncthreads();
+    double d = wmax[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) d = fmax(d, wmax[w]);
+    n_empty = base;
+    dmax_out = d;
+    __syncthreads();
+}
+
+// Lloyd iterations (lloyd_once :200-220) in one cooperative launch, two grid
+// barriers per iteration:
+//   every block: update_means into its shared centers (means_local); stop on
+//     an empty cluster (host repair); row-grid rebuild when the centers may
+//     have moved more than half a cell since the last one (+ barrier);
+//     super-tile check -> global list of super-tiles;       barrier B1
+//   (listed super-tile, 4 of its tiles) per warp: the tiles' single-center
+//     tests (tile_expand_body), then the tiles that need it reassigned by
+//     the same warp (lloyd_tile);                             barrier B2
+//   every block: iteration end (count, stop when no label changed).
+// Counters alternate by iteration parity, so a counter is cleared only once
+// every block is past reading it. Block 0 folds the low limbs of the cluster
+// sums upward with atomics while the other blocks add to them.
 __global__ void __launch_bounds__(256) k_lloyd_persistent(PersistArgs a) {
     namespace cgx = cooperative_groups;
     cgx::grid_group grid = cgx::this_grid();
-    int* state = a.empties + a.k;
+    extern __shared__ double s_cen[];  // [0, 2k) centers (x, y); [2k, 4k) cx | cy
+    const int k = a.k;
+    double* cx = s_cen + 2 * k;
+    double* cy = cx + k;
+    __shared__ AggScratch agg_all[8];
+    AggScratch* agg = agg_all + (threadIdx.x >> 5);
+    __shared__ unsigned long long s_changed;
+    __shared__ unsigned long long s_q[32];  // block tile queue: (single << 32) | tile
+    __shared__ int s_qn;
+    if (threadIdx.x == 0) s_qn = 0;
+    int* state = a.empties + k;
+    if (state[0] | state[1]) return;  // pending repair / converged (uniform)
+    for (int i = threadIdx.x; i < 2 * k; i += blockDim.x) s_cen[i] = a.centers[i];
+    double mov0 = a.mov[0];  // displacement since the last row-grid build (+inf: build now)
+    const double movD = a.mov[2];
     const bool ts = a.tstamp && blockIdx.x == 0 && threadIdx.x == 0;
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    __syncthreads();
     for (int b = 0; b < a.budget; ++b) {
+        const int par = b & 1;
         if (ts && b < 512) a.tstamp[6 * b] = gtimer();
-        if (blockIdx.x == 0)
-            means_body(a.acc, a.k, a.Ex, a.Ey, a.centers, a.empties, state, state, a.mov);
-        if (blockIdx.x == 0 && threadIdx.x == 0)  // one word for the other blocks to read
-            state[3] = ((state[0] | state[1]) ? 1 : 0) | (a.mov[1] != 0.0 ? 2 : 0);
-        grid.sync();
+        int n_empty;
+        double dmax;
+        means_local(a.acc, k, a.Ex, a.Ey, s_cen, blockIdx.x == 0 ? a.empties : nullptr, n_empty, dmax);
+        if (n_empty > 0) {
+            if (lead) state[0] = n_empty;
+            break;
+        }
+        const double acc_d = mov0 + dmax;  // triangle inequality: a bound
+        const bool rebuild = !(acc_d <= movD);
+        mov0 = rebuild ? 0.0 : acc_d;
+        for (int c = threadIdx.x; c < k; c += blockDim.x) {
+            cx[c] = s_cen[2 * c];
+            cy[c] = s_cen[2 * c + 1];
+        }
+        __syncthreads();
         if (ts && b < 512) a.tstamp[6 * b + 1] = gtimer();
-        const int gate = ((volatile int*)state)[3];  // bit 0: stop, bit 1: rebuild
-        if (gate & 1) break;
-        if (gate & 2) {  // centers moved too far: rebuild
-            row_grid_build_body(a.rg, a.centers, a.k, a.rg_blocks, a.rg_nblocks);
+        if (rebuild) {
+            row_grid_build_body(a.rg, s_cen, k, a.rg_blocks, a.rg_nblocks);
             grid.sync();
         }
         if (ts && b < 512) a.tstamp[6 * b + 2] = gtimer();
-        super_check_body(a.sbox, a.slenc, a.ntiles, a.cg, a.centers, a.tlab, a.swork, a.nswork,
-                         nullptr, 0, a.rg, a.k);
-        grid.sync();
+        super_check_body(a.sbox, a.slenc, a.ntiles, a.cg, s_cen, a.tlab, a.swork, a.cnt2 + 2 + par,
+                         nullptr, 0, a.rg, k);
+        if (threadIdx.x == 0) s_changed = 0;
+        grid.sync();  // B1
         if (ts && b < 512) a.tstamp[6 * b + 3] = gtimer();
-        tile_expand_body(a.swork, a.nswork, a.tbox, a.tlen, a.ntiles, a.cg, a.centers, a.tlab,
-                         a.tnew, a.work, a.nwork, nullptr, 0, a.rg, a.k);
-        grid.sync();
-        if (ts && b < 512) a.tstamp[6 * b + 4] = gtimer();
-        lloyd_work_body<false>(a.spts, a.n, a.centers, a.k, a.cg, a.labs, a.work, a.nwork, a.tnew,
-                               a.tlab, a.Ex, a.Ey, a.acc, a.changed, nullptr, a.rg, a.slen);
-        grid.sync();
-        if (ts && b < 512) a.tstamp[6 * b + 5] = gtimer();
-        if (blockIdx.x == 0) {
-            if (threadIdx.x == 0) iter_end_body(state, a.changed, a.nwork, a.nswork, a.diag);
-            __syncthreads();
+        if (lead) {  // counters of the other parity: last read before B2 of b - 1
+            a.cnt2[par ^ 1] = 0;
+            a.cnt2[2 + (par ^ 1)] = 0;
         }
+        if (blockIdx.x == 0) {  // fold the low limbs of the cluster sums (value-preserving)
+            for (int q = threadIdx.x; q < 2 * k; q += blockDim.x) {
+                unsigned long long* l3 = (q < k ? a.acc.sx : a.acc.sy) + 3 * (q % k);
+                const unsigned long long L = atomicExch(l3, 0ULL);
+                atomicAdd(l3, L & 0xFFFFFFFFull);
+                atomicAdd(l3 + 1, L >> 32);
+                const unsigned long long M = atomicExch(l3 + 1, 0ULL);
+                atomicAdd(l3 + 1, M & 0xFFFFFFFFull);
+                atomicAdd(l3 + 2, M >> 32);
+            }
+        }
+        const int64_t items = (int64_t)__ldcg(a.cnt2 + 2 + par) * 8;
+        unsigned long long my_changed = 0, my_tiles = 0;
+        {
+            // block b takes items b*8 .. b*8+7, then (b+G)*8 ..: one item per warp;
+            // the tiles to reassign go to a block queue drained by all 8 warps
+            const int lane = threadIdx.x & 31, grp = lane >> 3, sub = lane & 7;
+            const int wib = threadIdx.x >> 5;
+            for (int64_t b0 = (int64_t)blockIdx.x * 8; b0 < items; b0 += (int64_t)gridDim.x * 8) {
+                const int64_t it = b0 + wib;
+                if (it < items) {
+                    const int64_t t = (int64_t)__ldcg(a.swork + (it >> 3)) * 32 + (it & 7) * 4 + grp;
+                    const bool tv = t < a.ntiles;
+                    const double4 tb = tv ? a.tbox[t] : make_double4(0.0, 0.0, 0.0, 0.0);
+                    const int tl = tv && a.tlen ? a.tlen[t] : 0;
+                    const uint32_t single = box_single_g8(tb, tl, a.cg, a.rg, s_cen, sub);
+                    const bool add = tv && sub == 0 && (single == MIXED || single != __ldcg(a.tlab + t));
+                    if (add) s_q[atomicAdd(&s_qn, 1)] = ((unsigned long long)single << 32) | (unsigned long long)t;
+                }
+                __syncthreads();
+                const int nq = s_qn;
+                for (int q = wib; q < nq; q += 8) {
+                    const unsigned long long v = s_q[q];
+                    lloyd_tile<false>((uint32_t)v, (uint32_t)(v >> 32), a.spts, a.n, cx, cy, k, a.cg,
+                                      a.labs, a.tlab, a.Ex, a.Ey, a.acc, a.rg, a.slen, agg, nullptr,
+                                      nullptr, nullptr, my_changed);
+                    ++my_tiles;
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) s_qn = 0;
+                __syncthreads();
+            }
+        }
+        if ((threadIdx.x & 31) == 0 && my_tiles) atomicAdd(a.diag, my_tiles);
+        for (int o = 16; o > 0; o >>= 1) my_changed += __shfl_down_sync(0xffffffffu, my_changed, o);
+        if ((threadIdx.x & 31) == 0 && my_changed) atomicAdd(&s_changed, my_changed);
+        __syncthreads();
+        if (threadIdx.x == 0 && s_changed) atomicAdd(a.cnt2 + par, s_changed);
+        if (ts && b < 512) a.tstamp[6 * b + 4] = gtimer();
+        grid.sync();  // B2
+        if (ts && b < 512) a.tstamp[6 * b + 5] = gtimer();
+        // iteration end (iter_end_body), on every block
+        const unsigned long long chg = __ldcg(a.cnt2 + par);
+        if (lead) {
+            state[2] += 1;
+            a.diag[1] += chg;  // labels changed
+            a.diag[2] += __ldcg(a.cnt2 + 2 + par);  // super-tiles listed
+        }
+        if (chg == 0) {
+            if (lead) state[1] = 1;
+            break;
+        }
+    }
+    if (blockIdx.x == 0) {
+        for (int i = threadIdx.x; i < 2 * k; i += blockDim.x) a.centers[i] = s_cen[i];
     }
 }
 
@@ -2482,11 +2654,19 @@ bool lloyd_persistent(LloydCtx& L, int budget) {
         cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
     }
     if (!coop) return false;
-    const size_t smem = sizeof(double) * 2 * L.k;
-    JB_CUDA(cudaFuncSetAttribute(k_lloyd_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
+    const size_t smem = sizeof(double) * 4 * L.k;  // centers (x, y) + cx | cy
+    if (smem > 200 * 1024 ||
+        cudaFuncSetAttribute(k_lloyd_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
     int per_sm = 0;
-    JB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lloyd_persistent, 256, smem));
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lloyd_persistent, 256, smem) !=
+        cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
     if (per_sm < 1) return false;
     static const int per_sm_cap = getenv("JB_LLOYD_PER_SM") ? atoi(getenv("JB_LLOYD_PER_SM")) : 3;
     if (per_sm_cap > 0) per_sm = std::min(per_sm, per_sm_cap);  // grid barriers: fewer blocks
@@ -2530,6 +2710,9 @@ bool lloyd_persistent(LloydCtx& L, int budget) {
     DArr<unsigned long long> tsb(phase_times ? 6 * 512 : 0, L.st);
     if (phase_times) tsb.zero();
     a.tstamp = phase_times ? tsb.p : nullptr;
+    DArr<unsigned long long> cnt2(4, L.st);
+    cnt2.zero();
+    a.cnt2 = cnt2.p;
     void* args[] = {&a};
     {
         JB_PROF("lloyd_persistent", L.st);
@@ -2554,12 +2737,12 @@ bool lloyd_persistent(LloydCtx& L, int budget) {
                 for (int q = 0; q < 5; ++q)
                     quart[4 * b / cnt][q] += (double)(h[6 * b + q + 1] - h[6 * b + q]) * 1e-3;
             }
-            fprintf(stderr, "[jb] lloyd phases over %d iters (us): means %.1f grid %.1f super %.1f "
-                            "expand %.1f work %.1f (grid %d x 256), %d grid rebuilds\n",
+            fprintf(stderr, "[jb] lloyd phases over %d iters (us): means %.1f grid %.1f check+B1 %.1f "
+                            "work %.1f B2 %.1f (grid %d x 256), %d grid rebuilds\n",
                     cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt,
                     num_sms() * per_sm, rebuilds);
             for (int qq = 0; qq < 4; ++qq)
-                fprintf(stderr, "[jb]   quarter %d: means %.1f grid %.1f super %.1f expand %.1f work %.1f\n",
+                fprintf(stderr, "[jb]   quarter %d: means %.1f grid %.1f check+B1 %.1f work %.1f B2 %.1f\n",
                         qq, quart[qq][0] / (cnt / 4.0), quart[qq][1] / (cnt / 4.0),
                         quart[qq][2] / (cnt / 4.0), quart[qq][3] / (cnt / 4.0),
                         quart[qq][4] / (cnt / 4.0));
