@@ -397,6 +397,11 @@ __global__ void __launch_bounds__(AS_TB) k_assign_stats(
                                          div_by(pp[u].y, pv.si, pv.rsi));
                 }
             }
+            uint64_t cw[AS_U];  // row-cell words, all in flight before the searches
+            if (do_assign) {
+#pragma unroll
+                for (int u = 0; u < AS_U; ++u) cw[u] = row_cell_word<true>(rg, ll[u], pp[u].y);
+            }
 #pragma unroll
             for (int u = 0; u < AS_U; ++u) {
                 const int64_t i = base + (int64_t)u * AS_TB;
@@ -407,7 +412,7 @@ __global__ void __launch_bounds__(AS_TB) k_assign_stats(
                 bool lg = false;
                 if (valid) {
                     if (do_assign) {
-                        lab = row_nearest(rg, cg, l, p.x, p.y, cx, cy, k);
+                        lab = row_nearest_w(cg, rg.spill, cw[u], p.x, p.y, cx, cy, k);
                         labels[i] = lab;
                     }
                     if ((uint32_t)i < first[lab]) atomicMin(first + lab, (uint32_t)i);

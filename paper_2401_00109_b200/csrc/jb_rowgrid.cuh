@@ -186,13 +186,17 @@ __device__ __forceinline__ uint32_t row_word_cand(const uint16_t* spill, uint64_
 }
 
 // the row-cell word of a piece of length len at y = py (~0: no row cell,
-// which row_nearest_w sends to the 2-D grid fallback)
+// which row_nearest_w sends to the 2-D grid fallback). RO: the grid is
+// read-only for the whole kernel, so the word may come through L1 (the final
+// assignment); otherwise (grids rebuilt inside a persistent kernel) L2 only.
+template <bool RO = false>
 __device__ __forceinline__ uint64_t row_cell_word(const RowGrid& rg, int32_t len, double py) {
     if (len < 1 || len > rg.R) return ~0ull;
     int iy = (int)((py - rg.y0) * rg.invh);
     iy = min(max(iy, 0), rg.Gy - 1);
-    return __ldcg(reinterpret_cast<const unsigned long long*>(rg.cell) + (size_t)(len - 1) * rg.Gy +
-                  iy);
+    const unsigned long long* w =
+        reinterpret_cast<const unsigned long long*>(rg.cell) + (size_t)(len - 1) * rg.Gy + iy;
+    return RO ? __ldg(w) : __ldcg(w);
 }
 
 // nearest_center (clustering.hpp:146-157) of a piece at (px, py) whose row
