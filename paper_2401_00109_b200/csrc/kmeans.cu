@@ -1460,8 +1460,8 @@ __global__ void __launch_bounds__(D2P_TB, 1) k_d2_seed(D2Seed P) {
                 if (dd < v) {  // std::min(d2, dd)
                     const u128 dl = (u128)(fx_from_double(dd, P.E) - fx_from_double(v, P.E));
                     unsigned long long* q2 = P.part2 + 2 * (o[ii] / D2_R);
-                    atomicAdd(q2, (unsigned long long)dl & kM44);
-                    atomicAdd(q2 + 1, (unsigned long long)(dl >> 44));  // bits 44-107 (mod 2^64)
+                    red_add_u64(q2, (unsigned long long)dl & kM44);
+                    red_add_u64(q2 + 1, (unsigned long long)(dl >> 44));  // bits 44-107 (mod 2^64)
                     v = dd;
                     __stcg(P.d2s + r, v);
                 }
