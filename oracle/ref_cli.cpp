@@ -10,6 +10,7 @@
 #include <sstream>
 #include <string>
 
+#include "jabba/bench.hpp"
 #include "jabba/jabba.hpp"
 
 namespace {
@@ -68,6 +69,22 @@ int main(int argc, char** argv) {
                                          : jabba::symbolic_to_text(fit.symbolic);
             if (kv.count("--out")) put(kv.at("--out"), out);
             else std::cout << out;
+            return 0;
+        }
+        if (cmd == "bench-multivariate") {  // run_multivariate_protocol (bench.hpp:297-420)
+            jabba::Dataset ds = jabba::load_dataset(
+                get(kv, "--input", ""), jabba::data_format_from_string(get(kv, "--format", "ts-lite")));
+            if (ds.layout == jabba::Layout::collection)
+                ds = jabba::Dataset::multivariate(std::move(ds.series));
+            jabba::MultivariateOptions opt;
+            opt.eta = std::stod(get(kv, "--eta", "1"));
+            opt.sampling_r = std::stod(get(kv, "--r", "0.5"));
+            opt.scl = std::stod(get(kv, "--scl", "1"));
+            opt.seed = std::stoull(get(kv, "--seed", "0"));
+            const jabba::BenchReport report =
+                jabba::run_multivariate_protocol(ds, std::stod(get(kv, "--tol", "0.01")), opt);
+            if (kv.count("--json-out")) put(kv.at("--json-out"), report.to_json());
+            std::cout << report.to_text();
             return 0;
         }
         if (cmd == "reconstruct") {

@@ -7,6 +7,8 @@
 //   jabba_b200 inspect     --model F
 //   jabba_b200 bench partition-sweep [--n] [--tol] [--alpha] [--partitions 1,2,4] [--seed]
 //                          [--out F] [--json-out F]
+//   jabba_b200 bench multivariate --input F [--format] [--tol] [--eta] [--r] [--scl] [--seed]
+//                          [--out F] [--json-out F]
 // Exit codes as the reference (jabba_cli.cpp:2): 0 success, 2 usage error, 1
 // data / validation error. File formats are those of io.hpp (dataset
 // loaders :70-144, model / symbolic JSON :160-289, symbols text :293-338),
@@ -24,6 +26,7 @@
 #include <fstream>
 #include <iomanip>
 #include <iostream>
+#include <limits>
 #include <map>
 #include <memory>
 #include <random>
@@ -638,7 +641,9 @@ const char* kUsage =
     "       jabba_b200 reconstruct --symbols F [--model F] [--out F] [--ref F] [--ref-format FMT]\n"
     "       jabba_b200 inspect --model F\n"
     "       jabba_b200 bench partition-sweep [--n N] [--tol X] [--alpha X] [--partitions 1,2,4]\n"
-    "                  [--seed S] [--out F] [--json-out F]\n";
+    "                  [--seed S] [--out F] [--json-out F]\n"
+    "       jabba_b200 bench multivariate --input F [--format FMT] [--tol X] [--eta X] [--r X]\n"
+    "                  [--scl X] [--seed S] [--out F] [--json-out F]\n";
 
 // ---------------------------------------------------------------------------
 // subcommands
@@ -728,11 +733,17 @@ int run_inspect(const Args& a) {
 // series with m partitions; compression / digitization times from the GPU
 // fit's phase clocks, MSE of the reconstruction on the GPU (bit-exact),
 // scaled-space SSE, tau_c, and the invariants re-checked before reporting.
-struct Row {
+struct Row {  // BenchRow core.hpp:220-239
     std::string method;
     int partitions = 1, threads = 1;
     size_t symbols = 0;
     double mse = 0, sse = 0, tau_c = 1, t_compress = 0, t_digitize = 0, t_total = 0, speedup = 1;
+    double dtw = std::numeric_limits<double>::quiet_NaN();  // NaN: not measured
+    void validate() const {
+        if (mse < 0 || sse < 0) throw DataError("bench row: negative metric");
+        if (!(tau_c > 0.0 && tau_c <= 1.0)) throw DataError("bench row: tau_c outside (0,1]");
+        if (!std::isnan(dtw) && dtw < 0) throw DataError("bench row: negative dtw");
+    }
 };
 
 std::vector<double> gaussian_noise(size_t n, uint64_t seed) {  // bench.hpp:27-36
@@ -749,9 +760,13 @@ std::string rows_csv(const std::vector<Row>& rows) {  // BenchReport::to_csv ben
     out << "method,partitions,threads,symbols,mse,dtw,sse,tau_c,t_compress,t_digitize,t_total,"
            "speedup\n";
     for (const auto& r : rows)
+    {
         out << r.method << ',' << r.partitions << ',' << r.threads << ',' << r.symbols << ','
-            << r.mse << ",," << r.sse << ',' << r.tau_c << ',' << r.t_compress << ','
-            << r.t_digitize << ',' << r.t_total << ',' << r.speedup << '\n';
+            << r.mse << ',';
+        if (!std::isnan(r.dtw)) out << r.dtw;
+        out << ',' << r.sse << ',' << r.tau_c << ',' << r.t_compress << ',' << r.t_digitize
+            << ',' << r.t_total << ',' << r.speedup << '\n';
+    }
     return out.str();
 }
 
@@ -764,8 +779,10 @@ std::string rows_text(const std::vector<Row>& rows) {  // BenchReport::to_text b
     for (const auto& r : rows) {
         out << std::left << std::setw(14) << r.method << std::right << std::setw(6) << r.partitions
             << std::setw(8) << r.threads << std::setw(9) << r.symbols << std::setw(13)
-            << std::setprecision(4) << std::scientific << r.mse << std::setw(13) << "-"
-            << std::setw(11) << std::setprecision(5) << std::fixed << r.tau_c << std::setw(12)
+            << std::setprecision(4) << std::scientific << r.mse;
+        if (std::isnan(r.dtw)) out << std::setw(13) << "-";
+        else out << std::setw(13) << std::setprecision(4) << std::scientific << r.dtw;
+        out << std::setw(11) << std::setprecision(5) << std::fixed << r.tau_c << std::setw(12)
             << std::setprecision(4) << std::fixed << r.t_compress << std::setw(12) << r.t_digitize
             << std::setw(9) << std::setprecision(2) << std::fixed << r.speedup << '\n';
     }
@@ -781,6 +798,7 @@ std::string rows_json(const std::vector<Row>& rows) {  // BenchReport::to_json b
         e["threads"] = r.threads;
         e["symbols"] = r.symbols;
         e["mse"] = r.mse;
+        if (!std::isnan(r.dtw)) e["dtw"] = r.dtw;
         e["sse"] = r.sse;
         e["tau_c"] = r.tau_c;
         e["t_compress"] = r.t_compress;
@@ -898,6 +916,214 @@ int run_partition_sweep(const Args& a) {
     return 0;
 }
 
+// dtw (metrics.hpp:33-50): O(n m) dynamic programming, on the host
+double dtw(const std::vector<double>& x, const std::vector<double>& y) {
+    if (x.empty() || y.empty()) throw DataError("dtw: empty series");
+    const double inf = std::numeric_limits<double>::infinity();
+    std::vector<double> prev(y.size() + 1, inf), cur(y.size() + 1, inf);
+    prev[0] = 0.0;
+    for (size_t i = 1; i <= x.size(); ++i) {
+        cur[0] = inf;
+        for (size_t j = 1; j <= y.size(); ++j) {
+            const double d = x[i - 1] - y[j - 1];
+            cur[j] = d * d + std::min({prev[j], cur[j - 1], prev[j - 1]});
+        }
+        std::swap(prev, cur);
+    }
+    return prev[y.size()];
+}
+
+// auto_alpha (digitization.hpp:66-75), the same expression with the host libm
+double auto_alpha(int64_t n, int64_t N, double tol, double eta) {
+    if (N < 1 || n <= N) throw DataError("auto_alpha: requires n > N >= 1");
+    if (!(tol > 0.0)) throw DataError("auto_alpha: tol must be > 0");
+    if (!(eta > 0.0)) throw DataError("auto_alpha: eta must be > 0");
+    const double dn = (double)n, dN = (double)N;
+    const double poly = 3.0 * dn * dn * dn * dn + 2.0 - 5.0 * dn * dn;
+    const double num = 60.0 * dn * (dn - dN) * tol * tol;
+    return std::pow(num / (dN * eta * eta * poly), 0.25);
+}
+
+// check_pinned_endpoints (bench.hpp:140-152): the reconstructed increments of
+// a joint fit sum to the original ones
+void check_pinned(const Fit& f) {
+    double orig = 0.0, recon = 0.0;
+    const auto& cb = f.sym.cb;
+    for (size_t s = 0; s < f.sym.series.size(); ++s) {
+        for (int64_t i = f.off[s]; i < f.off[s + 1]; ++i) orig += f.inc[i];
+        for (uint32_t l : f.sym.series[s].labels) recon += cb.centers[l][1] * cb.sigma_inc;
+    }
+    if (std::abs(orig - recon) > 1e-9 * std::max({1.0, std::abs(orig), std::abs(recon)}))
+        throw DataError("bench: pinned-endpoint identity violated");
+}
+
+// check_compression_bound (bench.hpp:112-138) of segment s of a fit
+void check_segment_bound(const std::vector<double>& series, const Fit& f, size_t s, double tol) {
+    size_t start = 0;
+    double total_dev = 0.0;
+    for (int64_t i = f.off[s]; i < f.off[s + 1]; ++i) {
+        const size_t end = start + (size_t)f.len[i];
+        const double base = series[start], inc = series[end] - base, len = (double)f.len[i];
+        double dev = 0.0;
+        for (size_t q = start; q <= end; ++q) {
+            const double d = base + inc * ((double)(q - start) / len) - series[q];
+            dev += d * d;
+        }
+        const double bound = (len - 1.0) * tol * tol;
+        if (dev > bound + 1e-9 * std::max(1.0, bound))
+            throw DataError("bench: compression piece bound violated");
+        total_dev += dev;
+        start = end;
+    }
+    const double n = (double)f.sym.series[s].source_length, N = (double)(f.off[s + 1] - f.off[s]);
+    const double global = (n - N) * tol * tol;
+    if (total_dev > global + 1e-9 * std::max(1.0, global))
+        throw DataError("bench: global compression bound violated");
+}
+
+// bench multivariate (run_multivariate_protocol bench.hpp:297-420): a ga-auto
+// joint fit fixes alpha and the symbol budget k_m; a joint sampling-VQ fit
+// gets k_m symbols, per-dimension GA fits get alpha, per-dimension full VQ
+// fits share k_m. Each method: symbols, MSE (GPU, bit-exact) and DTW (host)
+// of the reconstruction per dimension, scaled-space SSE, tau_c; times are
+// medians of 3 runs from the GPU fits' phase clocks.
+int run_multivariate(const Args& a) {
+    Dataset ds = load_dataset(a.req("--input"), a.str("--format", "ts-lite"));
+    if (ds.layout == JB_LAYOUT_COLLECTION) {  // promote an equal-length collection (csv-cols)
+        for (const auto& x : ds.series)
+            if (x.values.size() != ds.series.front().values.size())
+                throw DataError("multivariate dataset: dimensions must have equal length");
+        ds.layout = JB_LAYOUT_MULTIVARIATE;
+        ds.m = (int64_t)ds.series.size();
+    }
+    if (ds.layout != JB_LAYOUT_MULTIVARIATE)
+        throw DataError("multivariate protocol needs a multivariate dataset");
+    const size_t d = ds.series.size();
+    if (d == 0) throw DataError("empty dataset");
+    const double tol = a.num<double>("--tol", 0.01), eta = a.num<double>("--eta", 1.0);
+    const double r_opt = a.num<double>("--r", 0.5), scl = a.num<double>("--scl", 1.0);
+    const uint64_t seed = a.num<uint64_t>("--seed", 0);
+    const uint64_t max_iters = 300;
+    int64_t total_samples = 0;
+    for (const auto& x : ds.series) total_samples += (int64_t)x.values.size();
+
+    auto base_cfg = [&](int32_t backend) {
+        jb_config c;
+        jb_config_default(&c);
+        c.tol = tol;
+        c.backend = backend;
+        c.scl = scl;
+        return c;
+    };
+    struct Timed {
+        std::vector<Fit> fits;  // one joint fit, or one per dimension
+        double t_compress = 0.0, t_digitize = 0.0;
+    };
+    // median of 3 runs (median_runtime bench.hpp:94-106) of a list of fits
+    auto timed = [&](const std::vector<std::pair<Dataset, jb_config>>& runs) {
+        Timed t;
+        std::vector<double> tc, td;
+        for (int rep = 0; rep < 3; ++rep) {
+            std::vector<Fit> fits;
+            double c = 0.0, g = 0.0;
+            for (const auto& [dd, cfg] : runs) {
+                fits.push_back(fit_transform(dd, cfg));
+                c += fits.back().ms_compress * 1e-3;
+                g += fits.back().ms_digitize * 1e-3;
+            }
+            tc.push_back(c);
+            td.push_back(g);
+            t.fits = std::move(fits);
+        }
+        std::sort(tc.begin(), tc.end());
+        std::sort(td.begin(), td.end());
+        t.t_compress = tc[1];
+        t.t_digitize = td[1];
+        return t;
+    };
+
+    // 1) joint GA with auto alpha fixes the budget
+    jb_config ga_cfg = base_cfg(JB_BACKEND_GA_AUTO);
+    ga_cfg.eta = eta;
+    const Timed joint_ga = timed({{ds, ga_cfg}});
+    const Fit& jg = joint_ga.fits.front();
+    for (size_t i = 0; i < d; ++i) check_segment_bound(ds.series[i].values, jg, i, tol);
+    check_pinned(jg);
+    const double alpha = auto_alpha(jg.total_steps, jg.pieces, tol, eta);
+    const uint64_t k_m = jg.sym.cb.size();
+
+    // 2) joint VQ (sampling k-means) with the same symbol count; the sample
+    // must still hold at least k_m points
+    jb_config vq_cfg = base_cfg(JB_BACKEND_SVQ);
+    vq_cfg.k = k_m;
+    vq_cfg.r = std::min(1.0, std::max(r_opt, ((double)k_m + 1.0) / (double)jg.pieces));
+    vq_cfg.seed = seed;
+    vq_cfg.max_iters = max_iters;
+    const Timed joint_vq = timed({{ds, vq_cfg}});
+    check_pinned(joint_vq.fits.front());
+
+    // 3) per-dimension GA with the same alpha; 4) per-dimension VQ sharing
+    // k_m (the first k_m % d dimensions get the extra center)
+    std::vector<std::pair<Dataset, jb_config>> pga, pvq;
+    for (size_t i = 0; i < d; ++i) {
+        const Dataset one = collection({ds.series[i]});
+        jb_config g = base_cfg(JB_BACKEND_GA);
+        g.alpha = alpha;
+        pga.emplace_back(one, g);
+        jb_config v = base_cfg(JB_BACKEND_VQ);
+        uint64_t k = std::max<uint64_t>(1, k_m / d + (i < k_m % d ? 1 : 0));
+        k = std::min<uint64_t>(k, (uint64_t)(jg.off[i + 1] - jg.off[i]));
+        v.k = k;
+        v.seed = seed;
+        v.max_iters = max_iters;
+        pvq.emplace_back(one, v);
+    }
+    const Timed per_ga = timed(pga);
+    const Timed per_vq = timed(pvq);
+
+    // the compression phase alone: the joint GA runs' compression clocks
+    const double t_compress = joint_ga.t_compress;
+    std::vector<Row> rows;
+    auto evaluate = [&](const std::string& method, const Timed& t) {
+        std::vector<std::vector<double>> recons;
+        double sse = 0.0;
+        size_t symbols = 0;
+        for (const auto& f : t.fits) {
+            symbols += f.sym.cb.size();
+            for (auto& x : reconstruct(f.sym)) recons.push_back(std::move(x.values));
+            sse += fit_sse(f);
+        }
+        Row r;
+        r.method = method;
+        r.partitions = (int)d;
+        r.threads = 1;
+        r.symbols = symbols;
+        r.t_compress = t_compress;
+        r.t_digitize = t.t_digitize;
+        r.t_total = r.t_compress + r.t_digitize;
+        double mse_acc = 0.0, dtw_acc = 0.0;
+        for (size_t i = 0; i < d; ++i) {
+            mse_acc += mse(ds.series[i].values, recons[i]);
+            dtw_acc += dtw(ds.series[i].values, recons[i]);
+        }
+        r.mse = mse_acc / (double)d;
+        r.dtw = dtw_acc / (double)d;
+        r.sse = sse;
+        if ((int64_t)symbols >= total_samples) throw DataError("bench: alphabet larger than the dataset");
+        r.tau_c = 1.0 - (double)symbols / (double)total_samples;
+        r.validate();
+        rows.push_back(r);
+    };
+    evaluate("abba-vq", per_vq);
+    evaluate("fabba-ga", per_ga);
+    evaluate("jabba-vq", joint_vq);
+    evaluate("jabba-ga", joint_ga);
+    std::cout << rows_text(rows);
+    if (a.has("--out")) write_file(a.str("--out"), rows_csv(rows));
+    if (a.has("--json-out")) write_file(a.str("--json-out"), rows_json(rows));
+    return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -920,12 +1146,18 @@ int main(int argc, char** argv) {
                                         {}));
         if (cmd == "inspect") return run_inspect(Args(argc, argv, 2, {"--model"}, {}));
         if (cmd == "bench") {
-            if (argc < 3 || std::string(argv[2]) != "partition-sweep")
-                throw UsageError("bench needs a protocol: partition-sweep");
-            return run_partition_sweep(Args(argc, argv, 3,
-                                            {"--n", "--tol", "--alpha", "--partitions", "--seed",
-                                             "--out", "--json-out"},
-                                            {}));
+            const std::string proto = argc >= 3 ? argv[2] : "";
+            if (proto == "partition-sweep")
+                return run_partition_sweep(Args(argc, argv, 3,
+                                                {"--n", "--tol", "--alpha", "--partitions",
+                                                 "--seed", "--out", "--json-out"},
+                                                {}));
+            if (proto == "multivariate")
+                return run_multivariate(Args(argc, argv, 3,
+                                             {"--input", "--format", "--tol", "--eta", "--r",
+                                              "--scl", "--seed", "--out", "--json-out"},
+                                             {}));
+            throw UsageError("bench needs a protocol: partition-sweep | multivariate");
         }
         throw UsageError("unknown subcommand: " + cmd);
     } catch (const UsageError& e) {

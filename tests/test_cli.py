@@ -171,3 +171,52 @@ def test_gpu_mse_bit_exact(engine):
         d = a - b
         want = np.cumsum(d * d)[-1] / n
         assert engine.mse(a, b) == want
+
+
+def _multivariate(path, d=4, n=600, seed=3):
+    """One multivariate sample in ts-lite (series id, dimension id, values):
+    AR(1) channels with a shared factor, as config 3, z-normalised."""
+    rng = np.random.default_rng(seed)
+    x = np.zeros((d, n))
+    for t in range(1, n):
+        f = rng.standard_normal()
+        x[:, t] = 0.95 * x[:, t - 1] + np.sqrt(0.5) * f + np.sqrt(0.5) * rng.standard_normal(d)
+    x = (x - x.mean(axis=1, keepdims=True)) / x.std(axis=1, keepdims=True)
+    with open(path, "w") as fh:
+        for c in range(d):
+            fh.write("s0," + str(c) + "," + ",".join(repr(float(v)) for v in x[c]) + "\n")
+
+
+@pytest.mark.gpu
+def test_bench_multivariate_vs_reference(tmp_path):
+    """bench multivariate (run_multivariate_protocol, bench.hpp:297-420): the
+    four methods' rows -- symbol counts exact; MSE, DTW, SSE and tau_c to
+    1e-9 -- against the unmodified reference protocol on the same file."""
+    need_ref()
+    data = tmp_path / "mv.ts"
+    _multivariate(data)
+    args = ["--input", str(data), "--format", "ts-lite", "--tol", "0.05", "--eta", "1",
+            "--r", "0.5", "--seed", "0"]
+    r = run(CLI, "bench", "multivariate", *args, "--json-out", str(tmp_path / "g.json"),
+            "--out", str(tmp_path / "g.csv"))
+    assert r.returncode == 0, r.stderr
+    r = run(REF_CLI, "bench-multivariate", *args, "--json-out", str(tmp_path / "r.json"))
+    assert r.returncode == 0, r.stderr
+    got = json.loads((tmp_path / "g.json").read_text())
+    want = json.loads((tmp_path / "r.json").read_text())
+    assert [x["method"] for x in got] == [x["method"] for x in want] == \
+        ["abba-vq", "fabba-ga", "jabba-vq", "jabba-ga"]
+    for g, w in zip(got, want):
+        assert g["symbols"] == w["symbols"] and g["partitions"] == w["partitions"] == 4
+        for key in ("mse", "dtw", "sse", "tau_c"):
+            assert g[key] == pytest.approx(w[key], rel=1e-9, abs=1e-12), (g["method"], key)
+    assert (tmp_path / "g.csv").read_text().splitlines()[1].count(",") == 11
+
+
+def test_bench_multivariate_usage(tmp_path):
+    assert run(CLI, "bench").returncode == 2
+    assert run(CLI, "bench", "multivariate").returncode == 2          # --input required
+    ragged = tmp_path / "rag.ts"
+    ragged.write_text("s0,0,1,2,3\ns0,1,1,2\n")
+    r = run(CLI, "bench", "multivariate", "--input", str(ragged))
+    assert r.returncode == 1
