@@ -437,6 +437,7 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
         uint64_t S = 0, raw_count = 0, cursor = 0;
         std::exception_ptr err;
         std::thread th;
+        bool inline_done = false;  // JB_SERIAL_SIDE: ran on the calling thread (profilers)
         ~SvqPre() {
             if (th.joinable()) th.join();
         }
@@ -491,7 +492,7 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
         cudaStream_t s2 = ctx->side;
         cudaEvent_t ev = ctx->side_done;
         const int64_t Ng = N_glob;
-        pre.th = std::thread([&pre, &c, dev, s2, ev, Ng] {
+        auto side_work = [&pre, &c, dev, s2, ev, Ng] {
             try {
                 JB_CUDA(cudaSetDevice(dev));
                 validate_vq(c, c.r);
@@ -511,7 +512,16 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
             } catch (...) {
                 pre.err = std::current_exception();
             }
-        });
+        };
+        // JB_SERIAL_SIDE=1: no helper thread (ncu cannot replay a kernel while
+        // another host thread launches); same work, same streams
+        static const bool serial = getenv("JB_SERIAL_SIDE") != nullptr;
+        if (serial) {
+            side_work();
+            pre.inline_done = true;
+        } else {
+            pre.th = std::thread(side_work);
+        }
     }
 
     // ---- digitize: scale_pieces ----
@@ -572,8 +582,8 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
             DArr<uint64_t> raw;
             SampleOrder jorder;  // single GPU: gather-friendly spatial pass
             uint64_t S = 0, raw_count = 0, cursor = 0;
-            if (pre.th.joinable()) {  // sampled on the side stream (above)
-                pre.th.join();
+            if (pre.th.joinable() || pre.inline_done) {  // sampled on the side stream (above)
+                if (pre.th.joinable()) pre.th.join();
                 if (pre.err) std::rethrow_exception(pre.err);
                 JB_CUDA(cudaStreamWaitEvent(st, ctx->side_done, 0));
                 S = pre.S;

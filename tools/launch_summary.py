@@ -33,6 +33,8 @@ def main():
     for row in csv.DictReader(lines):
         if row.get("Metric Name") != "gpu__time_duration.sum":
             continue
+        if "at::" in row["Kernel Name"] or "at_cuda_detail" in row["Kernel Name"]:
+            continue  # torch kernels: the harness's input generation, not the step
         v = float(row["Metric Value"].replace(",", "")) * UNIT[row["Metric Unit"]]
         k = short(row["Kernel Name"])
         agg[k][0] += 1

@@ -20,6 +20,7 @@ OUT = os.path.join(ROOT, "profiles", "ncu_work.json")
 # bench profile name -> kernel-name regex (every kernel of the JB_PROF site)
 BENCH = {
     "lloyd_persistent": r"k_lloyd_persistent", "lloyd_assign": r"k_lloyd_work",
+    "d2_seed": r"k_d2_seed",
     "assign_stats": r"k_assign_stats", "d2_update": r"k_d2_tiles|k_d2_cull",
     "d2_pick": r"k_pick\b", "compress_spec": r"k_spec", "compress_emit": r"k_emit",
     "scale_sum_var": r"k_sum_var", "scale_sum_inc": r"k_sum_inc", "inverse_fused": r"k_inv_fused",
@@ -59,6 +60,8 @@ def main():
         d[1][r[im]] = v
     ks = {}
     for name, m in per.values():
+        if "at::" in name or "at_cuda_detail" in name:  # torch: the harness's input generation
+            continue
         b = base_name(name)
         k = ks.setdefault(b, {"launches": 0, "time_ms": 0.0, "dram_bytes": 0.0, "fp64_flops": 0.0})
         k["launches"] += 1
