@@ -740,10 +740,11 @@ __global__ void __launch_bounds__(256) k_d2_tiles(
     const unsigned long long* __restrict__ nwork, float* __restrict__ tmax,
     double* __restrict__ d2s, const SeedState* __restrict__ ss, int init, int E,
     unsigned long long* __restrict__ part, const double2* __restrict__ cur,
-    const uint32_t* __restrict__ gkey, unsigned long long* __restrict__ diag) {
+    const uint32_t* __restrict__ gkey, unsigned long long* __restrict__ diag, int limbs44 = 0) {
     // cur: center given directly (distributed fit); gkey: partial-sum block
     // key per sorted point (global sample position) instead of orig; diag:
-    // tiles updated (diagnostics)
+    // tiles updated (diagnostics); limbs44: the init round's partials as
+    // k_d2_seed's (bits 0-43, bits 44-107) limbs, fire-and-forget REDs
     const int lane = threadIdx.x & 31;
     const int64_t ntiles = (n + TILE - 1) / TILE;
     const int64_t nw = init ? ntiles : (int64_t)*nwork;
@@ -775,7 +776,14 @@ __global__ void __launch_bounds__(256) k_d2_tiles(
             if (init) {
                 v = dd;
                 d2s[r] = v;
-                if (part) fx_atomic_add(part + 2 * (o[i] / D2_R), fx_from_double(v, E));
+                if (part && limbs44) {
+                    const u128 f = (u128)fx_from_double(v, E);
+                    unsigned long long* q2 = part + 2 * (o[i] / D2_R);
+                    red_add_u64(q2, (unsigned long long)f & ((1ULL << 44) - 1));
+                    red_add_u64(q2 + 1, (unsigned long long)(f >> 44));
+                } else if (part) {
+                    fx_atomic_add(part + 2 * (o[i] / D2_R), fx_from_double(v, E));
+                }
             } else {
                 v = old[i];
                 if (dd < v) {  // std::min(d2, dd)
@@ -1281,13 +1289,9 @@ __global__ void __launch_bounds__(D2P_TB, 1) k_d2_seed(D2Seed P) {
         // ---- (1) my range total; partials normalised and staged ----
         i128 mine = 0;
         for (int j = q0; j < q1; ++j) {
-            u128 v;
-            if (c == 1) {
-                v = (u128)fx_load(P.part + 2 * j);  // the init round's sums, < 2^107
-            } else {
-                const unsigned long long L = __ldcg(P.part2 + 2 * j), H = __ldcg(P.part2 + 2 * j + 1);
-                v = ((u128)L + ((u128)H << 44)) & (((u128)1 << 108) - 1);
-            }
+            // (the init round wrote the same limbs: k_d2_tiles, limbs44)
+            const unsigned long long L = __ldcg(P.part2 + 2 * j), H = __ldcg(P.part2 + 2 * j + 1);
+            const u128 v = ((u128)L + ((u128)H << 44)) & (((u128)1 << 108) - 1);
             __stcg(P.part2 + 2 * j, (unsigned long long)v & kM44);
             __stcg(P.part2 + 2 * j + 1, (unsigned long long)(v >> 44));
             s_part[2 * (j - r0)] = (unsigned long long)v;
@@ -1549,16 +1553,16 @@ D2Plan d2_plan(int64_t ntiles, int nblocks) {
 // per-round path continues from (k when done; 1 when the launch failed).
 uint64_t d2_seed_persistent(const D2Plan& pl, const double2* spts, const uint32_t* orig,
                             const uint32_t* pos, int64_t n, const float4* cbox, float* tmax,
-                            int64_t ntiles, double* d2s, unsigned long long* part, int nblocks,
+                            int64_t ntiles, double* d2s, unsigned long long* part,
+                            unsigned long long* part2, int nblocks,
                             int E, const uint64_t* raw, SeedState* ss, int64_t* chosen, int k,
                             unsigned long long* diag, cudaStream_t st) {
     static const bool phases = getenv("JB_D2_PHASES") != nullptr;
     const int G = pl.G;
-    DArr<unsigned long long> part2(2 * (size_t)std::max(nblocks, 1), st);
     DArr<unsigned long long> aux(2 * G + 1 + 10, st);  // range totals, flags, phase sums
     JB_CUDA(cudaMemsetAsync(aux.p + 2 * G, 0, 8 * 11, st));
     int* flag = reinterpret_cast<int*>(aux.p + 2 * G);
-    D2Seed a{spts, orig, pos, n, cbox, tmax, ntiles, d2s, part, part2.p, nblocks, E, raw, ss,
+    D2Seed a{spts, orig, pos, n, cbox, tmax, ntiles, d2s, part, part2, nblocks, E, raw, ss,
              chosen, k, aux.p, flag, diag, phases ? aux.p + 2 * G + 1 : nullptr, pl.ntl};
     void* args[] = {&a};
     {
@@ -2982,18 +2986,22 @@ void lloyd_best_device(const PtsView& pv, const uint64_t* d_idx, int64_t n, uint
         const int Einit = plan.G ? Ed2 - 18 : Ed2;
         k_pick_first<<<1, 1, 0, st>>>(d_raw, (uint64_t)n, ss.p, chosen.p);
         JB_LAUNCH_CHECK();
+        // the cooperative kernel's partials (two-limb layout), filled by the init round
+        DArr<unsigned long long> part2(plan.G ? 2 * (size_t)std::max(nblocks, 1) : 0, st);
+        if (plan.G) part2.zero();
         {
             JB_PROF("d2_update", st);
             k_d2_tiles<<<tile_grid, 256, 0, st>>>(spts.p, orig.p, pos.p, n, nullptr, nullptr,
-                                                  tmax.p, d2s.p, ss.p, 1, Einit, part.p, nullptr,
-                                                  nullptr, d2_diag.p);
+                                                  tmax.p, d2s.p, ss.p, 1, Einit,
+                                                  plan.G ? part2.p : part.p, nullptr, nullptr,
+                                                  d2_diag.p, plan.G ? 1 : 0);
         }
         JB_LAUNCH_CHECK();
         uint64_t c_from = 1;
         if (plan.G) {
             c_from = d2_seed_persistent(plan, spts.p, orig.p, pos.p, n, cbox.p, tmax.p, ntiles,
-                                        d2s.p, part.p, nblocks, Ed2 - 18, d_raw, ss.p, chosen.p,
-                                        (int)k, d2_diag.p, st);
+                                        d2s.p, part.p, part2.p, nblocks, Ed2 - 18, d_raw, ss.p,
+                                        chosen.p, (int)k, d2_diag.p, st);
             if (c_from < k) {  // rebuild the partials on the 128-bit scale
                 part.zero();
                 k_part_rebuild<<<grid_cap(n), 256, 0, st>>>(d2s.p, orig.p, n, Ed2, part.p);
