@@ -14,7 +14,7 @@
  * (128-bit Lemire "nearly divisionless" downscaling for a full 64-bit engine)
  * and uniform_real_distribution (generate_canonical<double,53>: one engine
  * draw, double(x) / 2^64, clamped below 1). Pinned draw-for-draw against the
- * real std:: implementation by tests/test_oracle_vs_ref.py.
+ * real std:: implementation by tests/test_oracle_golden.py (test_rng_matches_libstdcxx).
  */
 #include "jabba_oracle.h"
 

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <climits>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -406,6 +407,11 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
             throw Error(INVALID_INPUT, "compression needs at least 2 samples (segment " +
                                            std::to_string(s) + ")");
         if (seg_first[s] < 0) throw Error(INVALID_INPUT, "negative segment offset");
+        // piece lengths are 32-bit on the device: a segment longer than that
+        // needs max_piece_len to bound them (the reference's are 64-bit)
+        if (seg_steps[s] > INT32_MAX && !(c.max_piece_len > 0 && c.max_piece_len <= INT32_MAX))
+            throw Error(INVALID_INPUT, "segment " + std::to_string(s) + " has more than 2^31-1 "
+                                       "steps: set max_piece_len <= 2^31-1");
         max_last = std::max(max_last, seg_first[s] + seg_steps[s]);
         seg.total_steps += seg_steps[s];
     }
