@@ -447,11 +447,6 @@ __device__ __forceinline__ uint32_t spread16(uint32_t v) {
     return v;
 }
 
-__device__ __forceinline__ double2 load_pt(const double2* __restrict__ pts,
-                                           const uint64_t* __restrict__ idx, int64_t i) {
-    return idx ? pts[idx[i]] : pts[i];
-}
-
 // Morton keys of the sample points; also gathers the points (and their
 // piece lengths) into sample order, so the sorted gather reads a compact
 // array instead of chasing idx into the full point array again.
