@@ -87,10 +87,13 @@ __global__ void __launch_bounds__(64) k_inv_chains(InverseIn in, const double* _
                                                    double* __restrict__ vstart,
                                                    const int64_t* __restrict__ grp_off,
                                                    int64_t* __restrict__ gsum,
-                                                   unsigned long long* __restrict__ err) {
+                                                   unsigned long long* __restrict__ err,
+                                                   const int64_t* __restrict__ list,
+                                                   int64_t nlist) {
     // The carry warp also validates every label (inverse_digitize_series
     // :41-44) and sums the quantized lengths of each group of GROUP pieces;
-    // both are off its fp64 critical path.
+    // both are off its fp64 critical path. list: the segments to process
+    // (null: all); grp_off is indexed by list position.
     extern __shared__ double s_tabs[];  // rlen(k) | rinc(k)
     __shared__ __align__(16) unsigned char ring[64 * RSTRIDE];
     if (SMEM_TABS) {
@@ -103,14 +106,15 @@ __global__ void __launch_bounds__(64) k_inv_chains(InverseIn in, const double* _
     const double* tabs = SMEM_TABS ? s_tabs : rlen;  // global: rinc follows rlen
     const int kk = (int)in.k;
     const bool cwarp = threadIdx.x < 32;  // carry warp / start-value warp
-    const int64_t s = blockIdx.x * (int64_t)32 + (threadIdx.x & 31);
-    if (s >= in.n_seg) return;
+    const int64_t li = blockIdx.x * (int64_t)32 + (threadIdx.x & 31);
+    if (li >= nlist) return;
+    const int64_t s = list ? list[li] : li;
     unsigned char* my = ring + threadIdx.x * RSTRIDE;
     const int64_t a = in.seg_offsets[s], b = in.seg_offsets[s + 1];
     const double* tl = cwarp ? tabs : tabs + kk;
     double carry = 0.0, v = in.anchors[s];
     bool badlab = false;
-    int64_t g = grp_off[s];
+    int64_t g = grp_off[li];
     long long gacc = 0;
     int gcnt = 0;
     auto lab_ok = [&](uint32_t lab) -> uint32_t {  // invalid labels flag the segment
@@ -195,12 +199,14 @@ struct GroupRec {
 __global__ void k_inv_segfix(InverseIn in, int32_t* __restrict__ qlen,
                              const int64_t* __restrict__ grp_off, int64_t* __restrict__ gsum,
                              GroupRec* __restrict__ rec, int32_t* __restrict__ gmeta,
-                             double* __restrict__ out, unsigned long long* __restrict__ err) {
+                             double* __restrict__ out, unsigned long long* __restrict__ err,
+                             const int64_t* __restrict__ list, int64_t nlist) {
     const int lane = threadIdx.x & 31;
-    for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; s < in.n_seg;
-         s += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    for (int64_t li = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; li < nlist;
+         li += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t s = list ? list[li] : li;
         const int64_t a = in.seg_offsets[s], b = in.seg_offsets[s + 1];
-        const int64_t g0 = grp_off[s], g1 = grp_off[s + 1];
+        const int64_t g0 = grp_off[li], g1 = grp_off[li + 1];
         long long total = 0;
         for (int64_t g = g0 + lane; g < g1; g += 32) total += gsum[g];
         for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
@@ -496,7 +502,8 @@ template <bool SMEM_TABS>
 __global__ void __launch_bounds__(FUSED_TB, 3) k_inv_fused(InverseIn in, const double* __restrict__ rlen,
                                                            const double* __restrict__ rinc,
                                                            double* __restrict__ out, TailScratch tail,
-                                                           unsigned long long* __restrict__ err) {
+                                                           unsigned long long* __restrict__ err,
+                                                           unsigned char* __restrict__ bailed) {
     extern __shared__ __align__(128) unsigned char dsm[];
     const int kk = (int)in.k;
     const size_t toff = SMEM_TABS ? ((size_t)2 * kk * sizeof(double) + 127) & ~(size_t)127 : 0;
@@ -650,11 +657,15 @@ __global__ void __launch_bounds__(FUSED_TB, 3) k_inv_fused(InverseIn in, const d
         double carry = 0.0;
         long long total = 0, pos = 1, pos_tail = 1;  // positions from the anchor
         bool bail = S.bail[lane];
-        if (bail) atomicAdd(err + 1, 1ULL);
+        if (bail) {
+            atomicAdd(err + 1, 1ULL);
+            bailed[s] = 1;
+        }
         auto do_bail = [&]() {
             if (!bail) {
                 bail = true;
                 atomicAdd(err + 1, 1ULL);
+                bailed[s] = 1;
             }
         };
         for (int it = 0; it < maxT; ++it) {
@@ -888,18 +899,26 @@ static void throw_inverse_error(unsigned long long e, uint64_t k) {
 // Used when some segment's cascade reaches further back than the fused
 // kernel's window.
 static void inverse_general(const InverseIn& in, const double* tabp, uint64_t kk,
-                            DArr<unsigned long long>& err, double* d_out, cudaStream_t st) {
-    // group layout (host: segment piece counts are needed anyway for the offsets)
-    std::vector<int64_t> h_off(in.n_seg + 1), h_goff(in.n_seg + 1);
+                            DArr<unsigned long long>& err, double* d_out, cudaStream_t st,
+                            const std::vector<int64_t>* segs = nullptr) {
+    // segs: the segments to (re)write (null: all). Group layout on the host
+    // (segment piece counts are needed anyway for the offsets), by list position
+    std::vector<int64_t> h_off(in.n_seg + 1);
     JB_CUDA(cudaMemcpyAsync(h_off.data(), in.seg_offsets, sizeof(int64_t) * (in.n_seg + 1),
                             cudaMemcpyDeviceToHost, st));
     JB_CUDA(cudaStreamSynchronize(st));
+    const int64_t nlist = segs ? (int64_t)segs->size() : in.n_seg;
+    std::vector<int64_t> h_goff(nlist + 1);
     h_goff[0] = 0;
-    for (int64_t s = 0; s < in.n_seg; ++s)
-        h_goff[s + 1] = h_goff[s] + (h_off[s + 1] - h_off[s] + GROUP - 1) / GROUP;
-    const int64_t n_groups = h_goff[in.n_seg];
-    DArr<int64_t> goff(in.n_seg + 1, st);
-    goff.upload(h_goff.data(), in.n_seg + 1);
+    for (int64_t li = 0; li < nlist; ++li) {
+        const int64_t s = segs ? (*segs)[li] : li;
+        h_goff[li + 1] = h_goff[li] + (h_off[s + 1] - h_off[s] + GROUP - 1) / GROUP;
+    }
+    const int64_t n_groups = h_goff[nlist];
+    DArr<int64_t> goff(nlist + 1, st), dlist(segs ? std::max<int64_t>(nlist, 1) : 0, st);
+    goff.upload(h_goff.data(), nlist + 1);
+    if (segs) dlist.upload(segs->data(), nlist);
+    const int64_t* lp = segs ? dlist.p : nullptr;
     const int64_t ng = std::max<int64_t>(n_groups, 1);
     DArr<int32_t> qlen(std::max<int64_t>(in.N, 1) + 4, st), gmeta(ng, st);
     DArr<double> vstart(std::max<int64_t>(in.N, 1) + 4, st);
@@ -912,12 +931,13 @@ static void inverse_general(const InverseIn& in, const double* tabp, uint64_t kk
         if (tsmem + 64 * RSTRIDE > 48 * 1024)
             JB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)tsmem));
-        kern<<<(int)((in.n_seg + 31) / 32), 64, tsmem, st>>>(in, tabp, tabp + kk, qlen.p,
-                                                              vstart.p, goff.p, gsum.p, err.p);
+        kern<<<(int)std::max<int64_t>(1, (nlist + 31) / 32), 64, tsmem, st>>>(
+            in, tabp, tabp + kk, qlen.p, vstart.p, goff.p, gsum.p, err.p, lp, nlist);
         JB_LAUNCH_CHECK();
-        k_inv_segfix<<<(int)std::max<int64_t>(1, std::min<int64_t>((in.n_seg * 32 + 255) / 256,
+        k_inv_segfix<<<(int)std::max<int64_t>(1, std::min<int64_t>((nlist * 32 + 255) / 256,
                                                                    (int64_t)num_sms() * 16)),
-                       256, 0, st>>>(in, qlen.p, goff.p, gsum.p, rec.p, gmeta.p, d_out, err.p);
+                       256, 0, st>>>(in, qlen.p, goff.p, gsum.p, rec.p, gmeta.p, d_out, err.p, lp,
+                                     nlist);
         JB_LAUNCH_CHECK();
     }
     unsigned long long e;
@@ -954,6 +974,7 @@ void inverse_transform_device(const InverseIn& in, double* d_out, cudaStream_t s
     }
     if (in.n_seg == 0) return;
     unsigned long long h[2];
+    DArr<unsigned char> bailed;  // segments whose cascade left the fused kernel's window
     {
         JB_PROF("inverse_fused", st);
         const size_t tsmem = sizeof(double) * 2 * kk <= kInvTabSmem ? sizeof(double) * 2 * kk : 0;
@@ -976,8 +997,10 @@ void inverse_transform_device(const InverseIn& in, double* d_out, cudaStream_t s
         DArr<int32_t> tq(ntail, st), tpe(ntail, st);
         DArr<double> tinc(ntail, st), tv(ntail, st);
         const TailScratch tail{toff.p, tq.p, tpe.p, tinc.p, tv.p};
+        bailed.alloc(in.n_seg, st);
+        bailed.zero();
         kern<<<(int)((in.n_seg + 31) / 32), FUSED_TB, smem, st>>>(in, tab.p, tab.p + kk, d_out,
-                                                                   tail, err.p);
+                                                                   tail, err.p, bailed.p);
         JB_LAUNCH_CHECK();
         err.download(h, 2);
         JB_CUDA(cudaStreamSynchronize(st));
@@ -994,9 +1017,18 @@ void inverse_transform_device(const InverseIn& in, double* d_out, cudaStream_t s
         JB_CUDA(cudaMemcpyToSymbol(g_fused_prof, z, sizeof(z)));
     }
 #endif
-    if (h[1] != 0) {  // a cascade outside the window: redo everything on the general path
-        err.upload(init, 2);
-        inverse_general(in, tab.p, kk, err, d_out, st);
+    if (h[1] != 0) {  // cascades outside the window: those segments again, on the general path
+        std::vector<unsigned char> hb(in.n_seg);
+        bailed.download(hb.data(), in.n_seg);
+        JB_CUDA(cudaStreamSynchronize(st));
+        std::vector<int64_t> segs;
+        for (int64_t s = 0; s < in.n_seg; ++s)
+            if (hb[s]) segs.push_back(s);
+        // err[0] keeps the fused pass's errors (labels everywhere, cascades of
+        // the other segments); the listed segments' own cascades are decided now
+        const unsigned long long keep[2] = {h[0], 0ULL};
+        err.upload(keep, 2);
+        inverse_general(in, tab.p, kk, err, d_out, st, &segs);
         return;
     }
     throw_inverse_error(h[0], in.k);
