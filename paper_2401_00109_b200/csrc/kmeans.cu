@@ -1293,9 +1293,10 @@ __global__ void __launch_bounds__(D2P_TB, 1) k_d2_seed(D2Seed P) {
             s_part[2 * (j - r0) + 1] = (unsigned long long)(v >> 64);
             mine += (i128)v;
         }
+        i128 my_ex;  // this thread's blocks before it in the range (kept for the pick)
         {
             i128 rt;
-            block_exscan_i128(mine, &rt, s_lo, s_hi);
+            my_ex = block_exscan_i128(mine, &rt, s_lo, s_hi);
             if (t == 0) {
                 __stcg(P.rtot + 2 * b, (unsigned long long)(u128)rt);
                 __stcg(P.rtot + 2 * b + 1, (unsigned long long)((u128)rt >> 64));
@@ -1336,7 +1337,7 @@ __global__ void __launch_bounds__(D2P_TB, 1) k_d2_seed(D2Seed P) {
             __syncthreads();
             if (rc >= 0) {
                 i128 dummy;
-                const i128 ex = fx_load(s_before) + block_exscan_i128(mine, &dummy, s_lo, s_hi);
+                const i128 ex = fx_load(s_before) + my_ex;
                 if (U >= ex && U < ex + mine) {
                     i128 run = ex;
                     for (int j = q0; j < q1; ++j) {
