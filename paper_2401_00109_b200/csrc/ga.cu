@@ -165,15 +165,23 @@ __device__ void ga_phase_a(const GaSweep& a) {
         if (t == 0) a.ctl[0] = 1;
         return;
     }
+    // the candidates' points and window ends, staged once (the pair tests
+    // below read each of them up to GA_M times)
+    __shared__ double2 s_pt[GA_M];
+    __shared__ int64_t s_wend[GA_M];
+    if (t < m) {
+        s_pt[t] = a.spt[cand[t]];
+        s_wend[t] = a.wend[cand[t]];
+    }
     // row t: the earlier candidates whose start would claim cand[t]
     for (int q = 0; q < GA_M / 32; ++q) adj[t][q] = 0u;
+    __syncthreads();
     if (t < m) {
         const int64_t j = cand[t];
-        const double2 pj = a.spt[j];
+        const double2 pj = s_pt[t];
         for (int i = 0; i < t; ++i) {
-            const int64_t ci = cand[i];
-            if (j < a.wend[ci]) {
-                const double2 pi = a.spt[ci];
+            if (j < s_wend[i]) {
+                const double2 pi = s_pt[i];
                 if (dist2(pi.x, pi.y, pj.x, pj.y) <= a.alpha2) adj[t][i >> 5] |= 1u << (i & 31);
             }
         }
