@@ -136,28 +136,38 @@ __device__ void ga_phase_a(const GaSweep& a) {
     __syncthreads();
     int64_t p0 = *a.cursor;
     // the next GA_M unassigned points in key order (those the last claims
-    // reached are decided: marked here)
+    // reached are decided: marked here); GA_SCAN positions per thread and
+    // pass, so a stretch the last claims covered is crossed in few passes
+    constexpr int GA_SCAN = 8;
     while (s_m < GA_M && p0 < a.n) {
-        const int64_t p = p0 + t;
-        bool c = false;
-        if (p < a.n && a.status[p] == 0) {
-            if (a.owner[p] != kNoOwner) a.status[p] = 2;
-            else c = true;
+        const int64_t pb = p0 + (int64_t)t * GA_SCAN;
+        uint32_t cm = 0;  // candidate bits of this thread's positions
+#pragma unroll
+        for (int r = 0; r < GA_SCAN; ++r) {
+            const int64_t p = pb + r;
+            if (p < a.n && a.status[p] == 0) {
+                if (a.owner[p] != kNoOwner) a.status[p] = 2;
+                else cm |= 1u << r;
+            }
         }
-        const unsigned m = __ballot_sync(0xffffffffu, c);
-        if (lane == 0) wcnt[w] = __popc(m);
+        const int cnt = __popc(cm);
+        int incl = cnt;  // block exclusive scan of the counts, in position order
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) wcnt[w] = incl;
         __syncthreads();
-        int off = s_m;
+        int off = s_m + incl - cnt;
         for (int q = 0; q < w; ++q) off += wcnt[q];
-        off += __popc(m & ((1u << lane) - 1u));
-        if (c && off < GA_M) cand[off] = p;
+        for (uint32_t bits = cm; bits && off < GA_M; bits &= bits - 1) cand[off++] = pb + __ffs(bits) - 1;
         __syncthreads();
         if (t == 0) {
             int tot = s_m;
             for (int q = 0; q < GA_M / 32; ++q) tot += wcnt[q];
             s_m = tot < GA_M ? tot : GA_M;
         }
-        p0 += GA_M;
+        p0 += (int64_t)GA_M * GA_SCAN;
         __syncthreads();
     }
     const int m = s_m;
@@ -187,30 +197,71 @@ __device__ void ga_phase_a(const GaSweep& a) {
         }
     }
     __syncthreads();
-    if (t == 0) {  // in order: a start unless an earlier start claims it
-        uint32_t realm[GA_M / 32];
-        for (int q = 0; q < GA_M / 32; ++q) realm[q] = 0u;
-        int nr = 0;
+    // in order: a start unless an earlier start claims it. Warp 0, lane q
+    // holding the start bits of candidates 32q..32q+31: per candidate one
+    // masked row read and a ballot find the first claiming start.
+    __shared__ int s_first[GA_M];
+    if (w == 0) {
+        uint32_t realm = 0u;
         for (int c = 0; c < m; ++c) {
+            const uint32_t hit = lane < GA_M / 32 ? (adj[c][lane] & realm) : 0u;
+            const unsigned hb = __ballot_sync(0xffffffffu, hit != 0u);
             int first = -1;
-            for (int q = 0; q < GA_M / 32 && first < 0; ++q) {
-                const uint32_t hit = adj[c][q] & realm[q];
-                if (hit) first = 32 * q + __ffs(hit) - 1;
+            if (hb) {
+                const int q0 = __ffs(hb) - 1;
+                first = 32 * q0 + __ffs(__shfl_sync(0xffffffffu, hit, q0)) - 1;
             }
-            const int64_t j = cand[c];
-            if (first < 0) {
-                realm[c >> 5] |= 1u << (c & 31);
-                a.status[j] = 1;
-                a.owner[j] = (unsigned long long)j;
-                s_real[nr++] = j;
-            } else {
-                a.status[j] = 2;
-                a.owner[j] = (unsigned long long)cand[first];
-            }
+            if (first < 0 && lane == (c >> 5)) realm |= 1u << (c & 31);
+            if (lane == 0) s_first[c] = first;
+        }
+    }
+    __syncthreads();
+    // claims written in parallel; the starts compacted in candidate order with
+    // the prefix of their window sizes (the windows' points after the start)
+    const bool isst = t < m && s_first[t] < 0;
+    if (t < m) {
+        const int64_t j = cand[t];
+        a.status[j] = isst ? 1 : 2;
+        a.owner[j] = isst ? (unsigned long long)j : (unsigned long long)cand[s_first[t]];
+    }
+    const int64_t win = isst ? s_wend[t] - cand[t] - 1 : 0;
+    int rk = isst ? 1 : 0;
+    int64_t wp = win;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int yr = __shfl_up_sync(0xffffffffu, rk, o);
+        const int64_t yw = __shfl_up_sync(0xffffffffu, wp, o);
+        if (lane >= o) {
+            rk += yr;
+            wp += yw;
+        }
+    }
+    __shared__ int s_wr[GA_M / 32];
+    __shared__ int64_t s_ww[GA_M / 32];
+    if (lane == 31) {
+        s_wr[w] = rk;
+        s_ww[w] = wp;
+    }
+    __syncthreads();
+    int rb = 0;
+    int64_t wb = 0;
+    for (int q = 0; q < w; ++q) {
+        rb += s_wr[q];
+        wb += s_ww[q];
+    }
+    if (isst) {
+        const int r = rb + rk - 1;
+        s_real[r] = cand[t];
+        s_pre[r] = wb + wp - win;
+    }
+    if (t == 0) {
+        int nr = 0;
+        int64_t tw = 0;
+        for (int q = 0; q < GA_M / 32; ++q) {
+            nr += s_wr[q];
+            tw += s_ww[q];
         }
         s_nreal = nr;
-        s_pre[0] = 0;
-        for (int r = 0; r < nr; ++r) s_pre[r + 1] = s_pre[r] + (a.wend[s_real[r]] - s_real[r] - 1);
+        s_pre[nr] = tw;
         *a.cursor = cand[m - 1] + 1;
         a.ctl[1] = nr;
         a.ctl[2] += 1;
@@ -220,25 +271,39 @@ __device__ void ga_phase_a(const GaSweep& a) {
     for (int r = t; r <= s_nreal; r += GA_M) a.wpre[r] = s_pre[r];
 }
 
-// every new start claims the unassigned points of its window within alpha
+// every new start claims the unassigned points of its window within alpha;
+// the batch's starts (sorted position, point, window prefix) staged in
+// shared memory for the per-position lookups
 __device__ void ga_phase_b(const GaSweep& a) {
-    const int nr = ((volatile int*)a.ctl)[1];
-    const int64_t total = ((volatile int64_t*)a.wpre)[nr];
+    __shared__ int64_t s_wp[GA_M + 1], s_rl[GA_M];
+    __shared__ double2 s_ps[GA_M];
+    const int nr = __ldcg(a.ctl + 1);
+    for (int r = threadIdx.x; r <= nr; r += blockDim.x) {
+        s_wp[r] = __ldcg(a.wpre + r);
+        if (r < nr) {
+            const int64_t sr = __ldcg(a.real + r);
+            s_rl[r] = sr;
+            s_ps[r] = a.spt[sr];
+        }
+    }
+    __syncthreads();
+    const int64_t total = s_wp[nr];
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
          q += (int64_t)gridDim.x * blockDim.x) {
         int lo = 0, hi = nr;  // the start whose window slice holds q
         while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
-            if (((volatile int64_t*)a.wpre)[mid] <= q) lo = mid;
+            if (s_wp[mid] <= q) lo = mid;
             else hi = mid;
         }
-        const int64_t s = ((volatile int64_t*)a.real)[lo];
-        const int64_t j = s + 1 + (q - ((volatile int64_t*)a.wpre)[lo]);
-        if (((volatile uint8_t*)a.status)[j] != 0) continue;
-        const double2 ps = a.spt[s], pj = a.spt[j];
+        const int64_t s = s_rl[lo];
+        const int64_t j = s + 1 + (q - s_wp[lo]);
+        if (__ldcg(a.status + j) != 0) continue;
+        const double2 ps = s_ps[lo], pj = a.spt[j];
         if (dist2(ps.x, ps.y, pj.x, pj.y) <= a.alpha2)
             atomicMin(a.owner + j, (unsigned long long)s);  // the first start claims it
     }
+    __syncthreads();  // s_* are rewritten by the next batch's phase
 }
 
 __global__ void __launch_bounds__(GA_M) k_ga_sweep(GaSweep a) {
