@@ -19,6 +19,8 @@
 #include <cub/cub.cuh>
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "jb_device.hpp"
 
@@ -117,15 +119,27 @@ struct GaSweep {
     const int64_t* wend;
     int64_t n;
     double alpha2;
-    uint8_t* status;             // 0 unassigned, 1 start, 2 claimed
-    unsigned long long* owner;   // claiming start (sorted position), kNoOwner: none yet
+    unsigned long long* owner;   // claiming start (sorted position; a start owns itself),
+                                 // kNoOwner: undecided
     int64_t* real;               // GA_M: the batch's starts
     int64_t* wpre;               // GA_M + 1: prefix of their window sizes
     int* ctl;                    // [0] done, [1] starts in this batch, [2] batches
     int64_t* cursor;             // every position before it is decided
+    unsigned long long* trace;   // JB_GA_TRACE: per batch 4 globaltimer stamps (else null)
 };
 
-__device__ void ga_phase_a(const GaSweep& a) {
+constexpr int kGaTraceMax = 8192;
+
+__device__ __forceinline__ void ga_stamp(const GaSweep& a, int round, int k) {
+    // the warp sync holds the read until a preceding bar.sync has completed
+    // (the clock read itself may issue before a deferred-blocking barrier)
+    if (a.trace && blockIdx.x == 0 && threadIdx.x < 32 && round < kGaTraceMax) {
+        __syncwarp();
+        if (threadIdx.x == 0) a.trace[8 * round + k] = (unsigned long long)clock64();
+    }
+}
+
+__device__ void ga_phase_a(const GaSweep& a, int round) {
     __shared__ int64_t cand[GA_M];
     __shared__ uint32_t adj[GA_M][GA_M / 32];
     __shared__ int wcnt[GA_M / 32];
@@ -134,21 +148,28 @@ __device__ void ga_phase_a(const GaSweep& a) {
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     if (t == 0) s_m = 0;
     __syncthreads();
-    int64_t p0 = *a.cursor;
-    // the next GA_M unassigned points in key order (those the last claims
-    // reached are decided: marked here); GA_SCAN positions per thread and
-    // pass, so a stretch the last claims covered is crossed in few passes
+    // from the cursor rounded down to 8 (every earlier position is decided:
+    // owner set). A position is a candidate iff no start owns it yet, so the
+    // scan reads only the owners: GA_SCAN consecutive ones per thread and
+    // pass, 16-byte loads, so a stretch the last claims covered is crossed in
+    // few passes
+    int64_t p0 = *a.cursor & ~(int64_t)7;
     constexpr int GA_SCAN = 8;
     while (s_m < GA_M && p0 < a.n) {
         const int64_t pb = p0 + (int64_t)t * GA_SCAN;
         uint32_t cm = 0;  // candidate bits of this thread's positions
+        if (pb + GA_SCAN <= a.n) {
+            const ulonglong2* o2 = reinterpret_cast<const ulonglong2*>(a.owner + pb);
+            ulonglong2 v[GA_SCAN / 2];
 #pragma unroll
-        for (int r = 0; r < GA_SCAN; ++r) {
-            const int64_t p = pb + r;
-            if (p < a.n && a.status[p] == 0) {
-                if (a.owner[p] != kNoOwner) a.status[p] = 2;
-                else cm |= 1u << r;
-            }
+            for (int r = 0; r < GA_SCAN / 2; ++r) v[r] = __ldcg(o2 + r);
+#pragma unroll
+            for (int r = 0; r < GA_SCAN / 2; ++r)
+                cm |= (v[r].x == kNoOwner ? 1u : 0u) << (2 * r) |
+                      (v[r].y == kNoOwner ? 2u : 0u) << (2 * r);
+        } else {
+            for (int r = 0; r < GA_SCAN; ++r)
+                if (pb + r < a.n && __ldcg(a.owner + pb + r) == kNoOwner) cm |= 1u << r;
         }
         const int cnt = __popc(cm);
         int incl = cnt;  // block exclusive scan of the counts, in position order
@@ -170,6 +191,7 @@ __device__ void ga_phase_a(const GaSweep& a) {
         p0 += (int64_t)GA_M * GA_SCAN;
         __syncthreads();
     }
+    ga_stamp(a, round, 4);
     const int m = s_m;
     if (m == 0) {
         if (t == 0) a.ctl[0] = 1;
@@ -183,37 +205,86 @@ __device__ void ga_phase_a(const GaSweep& a) {
         s_pt[t] = a.spt[cand[t]];
         s_wend[t] = a.wend[cand[t]];
     }
-    // row t: the earlier candidates whose start would claim cand[t]
-    for (int q = 0; q < GA_M / 32; ++q) adj[t][q] = 0u;
     __syncthreads();
-    if (t < m) {
-        const int64_t j = cand[t];
-        const double2 pj = s_pt[t];
-        for (int i = 0; i < t; ++i) {
-            if (j < s_wend[i]) {
-                const double2 pi = s_pt[i];
-                if (dist2(pi.x, pi.y, pj.x, pj.y) <= a.alpha2) adj[t][i >> 5] |= 1u << (i & 31);
+    ga_stamp(a, round, 5);
+    // row r: the earlier candidates whose start would claim cand[r]. Warp w
+    // takes rows w, w+8, ... (balanced), GA_RB of them at a time for
+    // independent tests in flight; lane l holds candidates 32q+l in registers
+    // and a ballot forms each row's word q (words past the last row's
+    // diagonal are zero)
+    {
+        constexpr int GA_RB = 4, NW = GA_M / 32;
+        double2 cp[NW];
+        int64_t cw[NW];
+#pragma unroll
+        for (int q = 0; q < NW; ++q) {
+            cp[q] = s_pt[32 * q + lane];
+            cw[q] = s_wend[32 * q + lane];
+        }
+        for (int r0 = w; r0 < m; r0 += NW * GA_RB) {
+            int64_t j[GA_RB];
+            double2 pj[GA_RB];
+#pragma unroll
+            for (int u = 0; u < GA_RB; ++u) {
+                const int r = r0 + NW * u < m ? r0 + NW * u : r0;
+                j[u] = cand[r];
+                pj[u] = s_pt[r];
+            }
+            const int rl = min(r0 + NW * (GA_RB - 1), m - 1);
+#pragma unroll
+            for (int q = 0; q < NW; ++q) {
+                if (32 * q < rl) {
+                    unsigned b[GA_RB];
+#pragma unroll
+                    for (int u = 0; u < GA_RB; ++u) {
+                        const int r = r0 + NW * u;
+                        const double d = dist2(cp[q].x, cp[q].y, pj[u].x, pj[u].y);
+                        const bool hit = (32 * q + lane < r) & (r < m) & (j[u] < cw[q]) & (d <= a.alpha2);
+                        b[u] = __ballot_sync(0xffffffffu, hit);
+                    }
+                    if (lane < GA_RB && r0 + NW * lane < m) {
+                        unsigned bb = b[0];
+#pragma unroll
+                        for (int u = 1; u < GA_RB; ++u) bb = lane == u ? b[u] : bb;
+                        adj[r0 + NW * lane][q] = bb;
+                    }
+                } else if (lane < GA_RB && r0 + NW * lane < m) {
+                    adj[r0 + NW * lane][q] = 0u;
+                }
             }
         }
     }
     __syncthreads();
-    // in order: a start unless an earlier start claims it. Warp 0, lane q
-    // holding the start bits of candidates 32q..32q+31: per candidate one
-    // masked row read and a ballot find the first claiming start.
+    ga_stamp(a, round, 7);
+    // in order: a start unless an earlier start claims it. Warp 0 takes the
+    // candidates 32 at a time (lane l: candidate 32q+l): the starts of the
+    // earlier chunks (lane q' holds chunk q''s start bits) are tested in
+    // parallel, then the chunk's own 32 decisions run as a register-only
+    // chain over its intra-chunk rows (shuffled in ahead of the chain).
     __shared__ int s_first[GA_M];
     if (w == 0) {
         uint32_t realm = 0u;
-        for (int c = 0; c < m; ++c) {
-            const uint32_t hit = lane < GA_M / 32 ? (adj[c][lane] & realm) : 0u;
-            const unsigned hb = __ballot_sync(0xffffffffu, hit != 0u);
+        const int nq = (m + 31) >> 5;
+        for (int q = 0; q < nq; ++q) {
+            const int c = 32 * q + lane;
             int first = -1;
-            if (hb) {
-                const int q0 = __ffs(hb) - 1;
-                first = 32 * q0 + __ffs(__shfl_sync(0xffffffffu, hit, q0)) - 1;
+            for (int q2 = 0; q2 < q; ++q2) {
+                const uint32_t h = adj[c][q2] & __shfl_sync(0xffffffffu, realm, q2);
+                if (first < 0 && h) first = 32 * q2 + __ffs(h) - 1;
             }
-            if (first < 0 && lane == (c >> 5)) realm |= 1u << (c & 31);
-            if (lane == 0) s_first[c] = first;
+            const unsigned blk = __ballot_sync(0xffffffffu, first >= 0 || c >= m);
+            const uint32_t intra = adj[c][q];
+            uint32_t rq = 0u;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const uint32_t in_i = __shfl_sync(0xffffffffu, intra, i);
+                if (!((blk >> i) & 1u) && !(in_i & rq)) rq |= 1u << i;
+            }
+            if (lane == q) realm = rq;
+            if (first < 0 && !((rq >> lane) & 1u)) first = 32 * q + __ffs(intra & rq) - 1;
+            if (c < m) s_first[c] = first;
         }
+        ga_stamp(a, round, 6);
     }
     __syncthreads();
     // claims written in parallel; the starts compacted in candidate order with
@@ -221,7 +292,6 @@ __device__ void ga_phase_a(const GaSweep& a) {
     const bool isst = t < m && s_first[t] < 0;
     if (t < m) {
         const int64_t j = cand[t];
-        a.status[j] = isst ? 1 : 2;
         a.owner[j] = isst ? (unsigned long long)j : (unsigned long long)cand[s_first[t]];
     }
     const int64_t win = isst ? s_wend[t] - cand[t] - 1 : 0;
@@ -298,7 +368,7 @@ __device__ void ga_phase_b(const GaSweep& a) {
         }
         const int64_t s = s_rl[lo];
         const int64_t j = s + 1 + (q - s_wp[lo]);
-        if (__ldcg(a.status + j) != 0) continue;
+        if (__ldcg(a.owner + j) <= (unsigned long long)s) continue;  // decided before s
         const double2 ps = s_ps[lo], pj = a.spt[j];
         if (dist2(ps.x, ps.y, pj.x, pj.y) <= a.alpha2)
             atomicMin(a.owner + j, (unsigned long long)s);  // the first start claims it
@@ -309,27 +379,24 @@ __device__ void ga_phase_b(const GaSweep& a) {
 __global__ void __launch_bounds__(GA_M) k_ga_sweep(GaSweep a) {
     namespace cgx = cooperative_groups;
     cgx::grid_group grid = cgx::this_grid();
-    for (;;) {
-        if (blockIdx.x == 0) ga_phase_a(a);
+    for (int round = 0;; ++round) {
+        ga_stamp(a, round, 0);
+        if (blockIdx.x == 0) ga_phase_a(a, round);
+        ga_stamp(a, round, 1);
         grid.sync();
+        ga_stamp(a, round, 2);
         if (((volatile int*)a.ctl)[0]) break;
         ga_phase_b(a);
+        ga_stamp(a, round, 3);
         grid.sync();
     }
 }
 
-__global__ void k_ga_finish(uint8_t* __restrict__ status,
-                            const unsigned long long* __restrict__ owner, int64_t n) {
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
-         j += (int64_t)gridDim.x * blockDim.x)
-        if (status[j] == 0 && owner[j] != kNoOwner) status[j] = 2;
-}
-
-__global__ void k_start_flags(const uint8_t* __restrict__ status, int64_t n,
+__global__ void k_start_flags(const unsigned long long* __restrict__ owner, int64_t n,
                               int64_t* __restrict__ is_start) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
          j += (int64_t)gridDim.x * blockDim.x)
-        is_start[j] = status[j] == 1 ? 1 : 0;
+        is_start[j] = owner[j] == (unsigned long long)j ? 1 : 0;
 }
 
 __global__ void k_ga_labels(const unsigned long long* __restrict__ owner,
@@ -407,14 +474,17 @@ void greedy_aggregate_device(const double* d_pts, int64_t n, double alpha, int s
                                        skey.p, wend.p);
     }
     JB_LAUNCH_CHECK();
-    DArr<uint8_t> status(n, st);
-    status.zero();
     JB_CUDA(cudaMemsetAsync(owner.p, 0xFF, sizeof(unsigned long long) * n, st));
     DArr<int64_t> real(GA_M, st), wpre(GA_M + 1, st), cursor(1, st);
     DArr<int> ctl(3, st);
     ctl.zero();
     cursor.zero();
-    GaSweep a{spt.p, wend.p, n, alpha2, status.p, owner.p, real.p, wpre.p, ctl.p, cursor.p};
+    const char* tr = std::getenv("JB_GA_TRACE");
+    const bool trace = tr && tr[0] == '1';
+    DArr<unsigned long long> trbuf(trace ? 8 * kGaTraceMax : 0, st);
+    if (trace) trbuf.zero();
+    GaSweep a{spt.p, wend.p, n, alpha2, owner.p, real.p, wpre.p, ctl.p, cursor.p,
+              trace ? trbuf.p : nullptr};
     int per_sm = 0;
     JB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ga_sweep, GA_M, 0));
     if (per_sm < 1) throw Error(INTERNAL, "greedy_aggregate: sweep kernel does not fit");
@@ -426,15 +496,25 @@ void greedy_aggregate_device(const double* d_pts, int64_t n, double alpha, int s
                                             st));
     }
     JB_LAUNCH_CHECK();
-    k_ga_finish<<<gcap(n), 256, 0, st>>>(status.p, owner.p, n);
-    JB_LAUNCH_CHECK();
     int hctl[3];
     ctl.download(hctl, 3);
     JB_CUDA(cudaStreamSynchronize(st));
     const int rounds = hctl[2];
+    if (trace) {  // mean SM cycles per batch of each phase (block 0's clock)
+        auto h = trbuf.to_host(8 * kGaTraceMax);
+        const int nb = std::min(rounds, kGaTraceMax - 1);
+        const char* names[8] = {"select", "stage", "adjacency", "resolve", "claims", "sync", "B", "sync"};
+        const int from[8] = {0, 4, 5, 7, 6, 1, 2, 3}, to[8] = {4, 5, 7, 6, 1, 2, 3, 8};
+        double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int r = 0; r < nb; ++r)
+            for (int k = 0; k < 8; ++k) s[k] += (double)(h[8 * r + to[k]] - h[8 * r + from[k]]);
+        std::fprintf(stderr, "ga trace: %d batches, kcycles/batch:", nb);
+        for (int k = 0; k < 8; ++k) std::fprintf(stderr, " %s %.2f", names[k], s[k] / nb / 1e3);
+        std::fprintf(stderr, "\n");
+    }
     // group ids in sorted order of their starting points
     DArr<int64_t> flg(n + 1, st), gid(n + 1, st);
-    k_start_flags<<<gcap(n), 256, 0, st>>>(status.p, n, flg.p);
+    k_start_flags<<<gcap(n), 256, 0, st>>>(owner.p, n, flg.p);
     JB_CUDA(cudaMemsetAsync(flg.p + n, 0, 8, st));
     {
         size_t tb = 0;
