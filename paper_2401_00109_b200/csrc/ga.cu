@@ -3,24 +3,29 @@
 // The reference sweeps points in stable key order: an unassigned point
 // becomes a starting point and claims every unassigned later point of its key
 // window (early stop on key gap > alpha) within distance alpha. The sweep is
-// reproduced exactly in BATCHES of starts by one cooperative kernel:
-//   A. (one block) the next GA_M unassigned points in key order are the
-//      candidates; every earlier point is decided, so a candidate is a start
-//      iff no earlier candidate that is a start claims it (window and
-//      distance test). Their GA_M x GA_M adjacency bits are built in parallel
-//      and resolved by one sequential pass over the bitmasks.
-//   B. (whole grid) every new start claims the unassigned points of its
+// reproduced exactly in BATCHES by one cooperative kernel:
+//   A. (one block) the next GA_M undecided points in key order (no owner yet)
+//      are the candidates; every earlier point is decided. One warp walks
+//      them in order with the candidates in registers: the smallest undecided
+//      candidate is a start and claims the later undecided candidates of its
+//      window within alpha (all tests of a step in flight together). After
+//      GA_SMAX starts the batch is cut at the next undecided candidate.
+//   B. (whole grid) every new start claims the undecided points of its
 //      window within alpha; a point reached by several takes the FIRST start
 //      (atomicMin on the sorted position), exactly as the sequential sweep.
-// Work is the sequential sweep's (the starts' windows) plus the candidates'
-// pairwise tests; a batch costs two grid barriers. Keys are sorted with a
-// stable CUB radix sort on (key, index), matching std::stable_sort (:335-338).
+// Work is the sequential sweep's (the starts' windows) plus one test per
+// (start, later candidate) pair; a batch costs two grid barriers. Keys are
+// sorted with a stable CUB radix sort on (key, index), matching
+// std::stable_sort (:335-338). JB_GA_TRACE=1 prints block 0's cycles per
+// phase and the batch statistics.
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
+#include <vector>
 
 #include "jb_device.hpp"
 
@@ -111,7 +116,8 @@ __global__ void k_windows(const double2* __restrict__ pts, const unsigned long l
     }
 }
 
-constexpr int GA_M = 256;  // candidates per batch (= block size of the sweep)
+constexpr int GA_M = 256;   // candidates per batch (= block size of the sweep)
+constexpr int GA_SMAX = 64; // starts per batch at most
 constexpr unsigned long long kNoOwner = ~0ULL;
 
 struct GaSweep {
@@ -135,7 +141,7 @@ __device__ __forceinline__ void ga_stamp(const GaSweep& a, int round, int k) {
     // (the clock read itself may issue before a deferred-blocking barrier)
     if (a.trace && blockIdx.x == 0 && threadIdx.x < 32 && round < kGaTraceMax) {
         __syncwarp();
-        if (threadIdx.x == 0) a.trace[8 * round + k] = (unsigned long long)clock64();
+        if (threadIdx.x == 0) a.trace[16 * round + k] = (unsigned long long)clock64();
     }
 }
 
@@ -207,90 +213,61 @@ __device__ void ga_phase_a(const GaSweep& a, int round) {
     }
     __syncthreads();
     ga_stamp(a, round, 5);
-    // row r: the earlier candidates whose start would claim cand[r]. Warp w
-    // takes rows w, w+8, ... (balanced), GA_RB of them at a time for
-    // independent tests in flight; lane l holds candidates 32q+l in registers
-    // and a ballot forms each row's word q (words past the last row's
-    // diagonal are zero)
-    {
-        constexpr int GA_RB = 4, NW = GA_M / 32;
-        double2 cp[NW];
-        int64_t cw[NW];
-#pragma unroll
-        for (int q = 0; q < NW; ++q) {
-            cp[q] = s_pt[32 * q + lane];
-            cw[q] = s_wend[32 * q + lane];
-        }
-        for (int r0 = w; r0 < m; r0 += NW * GA_RB) {
-            int64_t j[GA_RB];
-            double2 pj[GA_RB];
-#pragma unroll
-            for (int u = 0; u < GA_RB; ++u) {
-                const int r = r0 + NW * u < m ? r0 + NW * u : r0;
-                j[u] = cand[r];
-                pj[u] = s_pt[r];
-            }
-            const int rl = min(r0 + NW * (GA_RB - 1), m - 1);
-#pragma unroll
-            for (int q = 0; q < NW; ++q) {
-                if (32 * q < rl) {
-                    unsigned b[GA_RB];
-#pragma unroll
-                    for (int u = 0; u < GA_RB; ++u) {
-                        const int r = r0 + NW * u;
-                        const double d = dist2(cp[q].x, cp[q].y, pj[u].x, pj[u].y);
-                        const bool hit = (32 * q + lane < r) & (r < m) & (j[u] < cw[q]) & (d <= a.alpha2);
-                        b[u] = __ballot_sync(0xffffffffu, hit);
-                    }
-                    if (lane < GA_RB && r0 + NW * lane < m) {
-                        unsigned bb = b[0];
-#pragma unroll
-                        for (int u = 1; u < GA_RB; ++u) bb = lane == u ? b[u] : bb;
-                        adj[r0 + NW * lane][q] = bb;
-                    }
-                } else if (lane < GA_RB && r0 + NW * lane < m) {
-                    adj[r0 + NW * lane][q] = 0u;
-                }
-            }
-        }
-    }
-    __syncthreads();
-    ga_stamp(a, round, 7);
-    // in order: a start unless an earlier start claims it. Warp 0 takes the
-    // candidates 32 at a time (lane l: candidate 32q+l): the starts of the
-    // earlier chunks (lane q' holds chunk q''s start bits) are tested in
-    // parallel, then the chunk's own 32 decisions run as a register-only
-    // chain over its intra-chunk rows (shuffled in ahead of the chain).
+    // Starts in order (warp 0; lane l holds candidates 32k+l in registers):
+    // the smallest undecided candidate is a start, and it claims every later
+    // undecided candidate of its window within alpha (the sequential sweep
+    // restricted to the batch). After GA_SMAX starts the batch is cut at
+    // the next undecided candidate, which the next batch takes up.
     __shared__ int s_first[GA_M];
+    __shared__ int s_cut;
     if (w == 0) {
-        uint32_t realm = 0u;
-        const int nq = (m + 31) >> 5;
-        for (int q = 0; q < nq; ++q) {
-            const int c = 32 * q + lane;
-            int first = -1;
-            for (int q2 = 0; q2 < q; ++q2) {
-                const uint32_t h = adj[c][q2] & __shfl_sync(0xffffffffu, realm, q2);
-                if (first < 0 && h) first = 32 * q2 + __ffs(h) - 1;
-            }
-            const unsigned blk = __ballot_sync(0xffffffffu, first >= 0 || c >= m);
-            const uint32_t intra = adj[c][q];
-            uint32_t rq = 0u;
+        constexpr int NK = GA_M / 32;
+        double2 cp[NK];
+        int64_t cj[NK];
+        uint32_t und = 0u;  // bit k: candidate 32k+lane undecided
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const uint32_t in_i = __shfl_sync(0xffffffffu, intra, i);
-                if (!((blk >> i) & 1u) && !(in_i & rq)) rq |= 1u << i;
-            }
-            if (lane == q) realm = rq;
-            if (first < 0 && !((rq >> lane) & 1u)) first = 32 * q + __ffs(intra & rq) - 1;
-            if (c < m) s_first[c] = first;
+        for (int k = 0; k < NK; ++k) {
+            const int c = 32 * k + lane;
+            cp[k] = s_pt[c];
+            cj[k] = cand[c];
+            if (c < m) und |= 1u << k;
         }
-        ga_stamp(a, round, 6);
+        int cut = m, nst = 0;
+        for (;;) {
+            const unsigned mine = und ? 32u * (__ffs(und) - 1) + lane : 0xffffffffu;
+            const unsigned cu = __reduce_min_sync(0xffffffffu, mine);
+            if (cu == 0xffffffffu) break;
+            const int c = (int)cu;
+            if (nst == GA_SMAX) {
+                cut = c;
+                break;
+            }
+            ++nst;
+            if (lane == (c & 31)) und &= ~(1u << (c >> 5));
+            if (lane == 0) s_first[c] = -1;
+            const double2 pc = s_pt[c];
+            const int64_t wc = s_wend[c];
+            uint32_t hit = 0u;  // all NK tests independent (in flight together)
+#pragma unroll
+            for (int k = 0; k < NK; ++k) {
+                const double d = dist2(pc.x, pc.y, cp[k].x, cp[k].y);
+                hit |= (uint32_t)((cj[k] < wc) & (d <= a.alpha2)) << k;
+            }
+            hit &= und;
+            und &= ~hit;
+#pragma unroll
+            for (int k = 0; k < NK; ++k)
+                if ((hit >> k) & 1u) s_first[32 * k + lane] = c;
+        }
+        if (lane == 0) s_cut = cut;
     }
     __syncthreads();
+    ga_stamp(a, round, 6);
+    const int mc = s_cut;  // candidates decided in this batch
     // claims written in parallel; the starts compacted in candidate order with
     // the prefix of their window sizes (the windows' points after the start)
-    const bool isst = t < m && s_first[t] < 0;
-    if (t < m) {
+    const bool isst = t < mc && s_first[t] < 0;
+    if (t < mc) {
         const int64_t j = cand[t];
         a.owner[j] = isst ? (unsigned long long)j : (unsigned long long)cand[s_first[t]];
     }
@@ -332,7 +309,11 @@ __device__ void ga_phase_a(const GaSweep& a, int round) {
         }
         s_nreal = nr;
         s_pre[nr] = tw;
-        *a.cursor = cand[m - 1] + 1;
+        if (a.trace && round < kGaTraceMax) {
+            a.trace[16 * round + 8] = (unsigned long long)tw;
+            a.trace[16 * round + 9] = (unsigned long long)nr;
+        }
+        *a.cursor = mc < m ? cand[mc] : cand[m - 1] + 1;
         a.ctl[1] = nr;
         a.ctl[2] += 1;
     }
@@ -481,7 +462,7 @@ void greedy_aggregate_device(const double* d_pts, int64_t n, double alpha, int s
     cursor.zero();
     const char* tr = std::getenv("JB_GA_TRACE");
     const bool trace = tr && tr[0] == '1';
-    DArr<unsigned long long> trbuf(trace ? 8 * kGaTraceMax : 0, st);
+    DArr<unsigned long long> trbuf(trace ? 16 * kGaTraceMax : 0, st);
     if (trace) trbuf.zero();
     GaSweep a{spt.p, wend.p, n, alpha2, owner.p, real.p, wpre.p, ctl.p, cursor.p,
               trace ? trbuf.p : nullptr};
@@ -501,16 +482,25 @@ void greedy_aggregate_device(const double* d_pts, int64_t n, double alpha, int s
     JB_CUDA(cudaStreamSynchronize(st));
     const int rounds = hctl[2];
     if (trace) {  // mean SM cycles per batch of each phase (block 0's clock)
-        auto h = trbuf.to_host(8 * kGaTraceMax);
+        auto h = trbuf.to_host(16 * kGaTraceMax);
         const int nb = std::min(rounds, kGaTraceMax - 1);
-        const char* names[8] = {"select", "stage", "adjacency", "resolve", "claims", "sync", "B", "sync"};
-        const int from[8] = {0, 4, 5, 7, 6, 1, 2, 3}, to[8] = {4, 5, 7, 6, 1, 2, 3, 8};
-        double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        const char* names[7] = {"select", "stage", "starts", "claims", "sync", "B", "sync"};
+        const int from[7] = {0, 4, 5, 6, 1, 2, 3}, to[7] = {4, 5, 6, 1, 2, 3, 16};
+        double s[7] = {0, 0, 0, 0, 0, 0, 0};
         for (int r = 0; r < nb; ++r)
-            for (int k = 0; k < 8; ++k) s[k] += (double)(h[8 * r + to[k]] - h[8 * r + from[k]]);
+            for (int k = 0; k < 7; ++k) s[k] += (double)(h[16 * r + to[k]] - h[16 * r + from[k]]);
         std::fprintf(stderr, "ga trace: %d batches, kcycles/batch:", nb);
-        for (int k = 0; k < 8; ++k) std::fprintf(stderr, " %s %.2f", names[k], s[k] / nb / 1e3);
-        std::fprintf(stderr, "\n");
+        for (int k = 0; k < 7; ++k) std::fprintf(stderr, " %s %.2f", names[k], s[k] / nb / 1e3);
+        // claim positions and starts per batch: mean, quantiles
+        std::vector<unsigned long long> tot(nb), nst(nb);
+        for (int r = 0; r < nb; ++r) {
+            tot[r] = h[16 * r + 8];
+            nst[r] = h[16 * r + 9];
+        }
+        std::sort(tot.begin(), tot.end());
+        std::sort(nst.begin(), nst.end());
+        std::fprintf(stderr, "; claims/batch p50 %llu p90 %llu max %llu; starts/batch p50 %llu max %llu\n",
+                     tot[nb / 2], tot[nb * 9 / 10], tot[nb - 1], nst[nb / 2], nst[nb - 1]);
     }
     // group ids in sorted order of their starting points
     DArr<int64_t> flg(n + 1, st), gid(n + 1, st);
