@@ -1231,6 +1231,7 @@ struct D2Seed {
     unsigned long long* diag;
     unsigned long long* phase;  // optional (JB_D2_PHASES): summed ns of 5 phases, CTAs 0 and 1
     int ntl;                    // tiles per CTA (shared-memory arrays)
+    unsigned long long* rounds; // optional (JB_D2_PHASES): CTA 0 per round: cull+update ns, kept tiles
 };
 
 constexpr unsigned long long kM44 = (1ULL << 44) - 1;
@@ -1407,6 +1408,8 @@ __global__ void __launch_bounds__(D2P_TB, 1) k_d2_seed(D2Seed P) {
         cursor += 1;
         last = next;
         stamp(3);
+        unsigned long long t3 = 0;
+        if (P.rounds && b == 0 && t == 0 && c < 1024) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t3));
         if (c + 1 >= P.k) {
             c = P.k;
             break;
@@ -1471,6 +1474,12 @@ __global__ void __launch_bounds__(D2P_TB, 1) k_d2_seed(D2Seed P) {
             if (lane == 0) s_tmax[il] = __double2float_ru(mx);
         }
         stamp(4);
+        if (P.rounds && b == 0 && t == 0 && c < 1024) {
+            unsigned long long v;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+            P.rounds[2 * c] = v - t3;
+            P.rounds[2 * c + 1] = (unsigned long long)cnt;
+        }
         grid.sync();
         stamp(5);
     }
@@ -1555,11 +1564,12 @@ uint64_t d2_seed_persistent(const D2Plan& pl, const double2* spts, const uint32_
                             unsigned long long* diag, cudaStream_t st) {
     static const bool phases = getenv("JB_D2_PHASES") != nullptr;
     const int G = pl.G;
-    DArr<unsigned long long> aux(2 * G + 1 + 10, st);  // range totals, flags, phase sums
-    JB_CUDA(cudaMemsetAsync(aux.p + 2 * G, 0, 8 * 11, st));
+    DArr<unsigned long long> aux(2 * G + 1 + 10 + 2048, st);  // range totals, flags, phase sums, rounds
+    JB_CUDA(cudaMemsetAsync(aux.p + 2 * G, 0, 8 * (11 + 2048), st));
     int* flag = reinterpret_cast<int*>(aux.p + 2 * G);
     D2Seed a{spts, orig, pos, n, cbox, tmax, ntiles, d2s, part, part2, nblocks, E, raw, ss,
-             chosen, k, aux.p, flag, diag, phases ? aux.p + 2 * G + 1 : nullptr, pl.ntl};
+             chosen, k, aux.p, flag, diag, phases ? aux.p + 2 * G + 1 : nullptr, pl.ntl,
+             phases ? aux.p + 2 * G + 11 : nullptr};
     void* args[] = {&a};
     {
         JB_PROF("d2_seed", st);
@@ -1583,6 +1593,18 @@ uint64_t d2_seed_persistent(const D2Plan& pl, const double2* spts, const uint32_
                             "pick %.2f cull+update %.2f sync2 %.2f\n",
                     q, G, h[5 * q] * 1e-3 / r, h[5 * q + 1] * 1e-3 / r, h[5 * q + 2] * 1e-3 / r,
                     h[5 * q + 3] * 1e-3 / r2, h[5 * q + 4] * 1e-3 / r2);
+        std::vector<unsigned long long> hr(2048);
+        JB_CUDA(cudaMemcpy(hr.data(), aux.p + 2 * G + 11, 8 * 2048, cudaMemcpyDeviceToHost));
+        std::string line;
+        double tot = 0, tail = 0;
+        int ntail = 0;
+        for (int c = 1; c < std::min(k, 1024); ++c) {
+            tot += hr[2 * c] * 1e-3;
+            if (c <= 12) line += " " + std::to_string((int)(hr[2 * c] * 1e-3)) + "us/" + std::to_string(hr[2 * c + 1]);
+            else { tail += hr[2 * c] * 1e-3; ++ntail; }
+        }
+        fprintf(stderr, "[jb] d2 CTA 0 cull+update per round (us/kept tiles):%s | rounds 13..: %.2f us avg | total %.0f us\n",
+                line.c_str(), ntail ? tail / ntail : 0.0, tot);
     }
     return (uint64_t)hf[1];
 }
@@ -1792,9 +1814,11 @@ __device__ __forceinline__ void super_check_body(const double4* __restrict__ sbo
                               int k) {
     if (skip_flag && (skip_flag[0] | skip_flag[1])) return;
     extern __shared__ double s_centers[];  // 2k: the candidate tests read them repeatedly
-    for (int i = threadIdx.x; i < 2 * k; i += blockDim.x) s_centers[i] = centers[i];
-    __syncthreads();
-    centers = s_centers;
+    if (centers != s_centers) {  // (the persistent loop passes its shared copy)
+        for (int i = threadIdx.x; i < 2 * k; i += blockDim.x) s_centers[i] = centers[i];
+        __syncthreads();
+        centers = s_centers;
+    }
     const int lane = threadIdx.x & 31, grp = lane >> 3, sub = lane & 7;
     const int64_t nsuper = (ntiles + 31) / 32;
     uint32_t* stlab = tlab + ntiles;
@@ -2439,9 +2463,9 @@ struct PersistArgs {
     const int32_t* slen;
     unsigned long long* diag;
     int budget;
-    unsigned long long* tstamp;  // optional: 6 globaltimer stamps per iteration (block 0)
+    unsigned long long* tstamp;  // optional: 8 globaltimer stamps per iteration (block 0; [7] the slowest block)
     double* mov;                 // row-grid movement state (means_body)
-    unsigned long long* cnt2;    // persistent loop: changed[2], listed super-tiles[2] (by parity)
+    unsigned long long* cnt2;    // persistent loop: changed[2], listed super-tiles[2], listed tiles[2] (by parity)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -2457,70 +2481,79 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // index order into empties when non-null) and the largest center
 // displacement (rounded up), both uniform over the block.
 __device__ __forceinline__ void means_local(ClusterAcc acc, int k, int Ex, int Ey, double* s_c,
-                                            int* __restrict__ empties, int& n_empty,
-                                            double& dmax_out) {
-    __shared__ int wc[32];
-    __shared__ int base;
-    __shared__ double wmax[32];
-    double dmax = 0.0;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) base = 0;
-    __syncthreads();
-    for (int c0 = 0; c0 < k; c0 += blockDim.x) {
-        const int c = c0 + threadIdx.x;
-        bool empty = false;
-        if (c < k) {
-            const long long cnt = (long long)__ldcg(acc.cnt + c);
-            const i128 sx = (i128)((u128)__ldcg(acc.sx + 3 * c) + ((u128)__ldcg(acc.sx + 3 * c + 1) << 32) +
-                                   ((u128)__ldcg(acc.sx + 3 * c + 2) << 64));
-            const i128 sy = (i128)((u128)__ldcg(acc.sy + 3 * c) + ((u128)__ldcg(acc.sy + 3 * c + 1) << 32) +
-                                   ((u128)__ldcg(acc.sy + 3 * c + 2) << 64));
-            if (cnt > 0) {
-                const double nx = fx_to_double(sx, Ex) / (double)cnt;
-                const double ny = fx_to_double(sy, Ey) / (double)cnt;
-                const double dx = nx - s_c[2 * c], dy = ny - s_c[2 * c + 1];
-                dmax = fmax(dmax, sqrt(dx * dx + dy * dy) * (1.0 + 1e-12) + 1e-300);
-                s_c[2 * c] = nx;
-                s_c[2 * c + 1] = ny;
-            } else {
-                empty = true;
-            }
-        }
-        const unsigned m = __ballot_sync(0xffffffffu, empty);
-        if (lane == 0) wc[warp] = __popc(m);
-        __syncthreads();
-        int off = base;
-        for (int w = 0; w < warp; ++w) off += wc[w];
-        if (empty && empties) empties[off + __popc(m & ((1u << lane) - 1u))] = c;
-        __syncthreads();
-        if (threadIdx.x == 0)
-            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) base += wc[w];
-        __syncthreads();
+                                            double* cx, double* cy, int* __restrict__ empties,
+                                            int& n_empty, double& dmax_out) {
+    // two block barriers: the displacement maximum as the bits of a
+    // non-negative double (ordered like the value) and the empty count by
+    // shared-memory atomics; the ordered empty list only when one is empty
+    __shared__ unsigned long long s_dmax;
+    __shared__ int s_ne;
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        s_dmax = 0ull;
+        s_ne = 0;
     }
-    for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
-    if (lane == 0) wmax[warp] = dmax;
     __syncthreads();
-    double d = wmax[0];
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) d = fmax(d, wmax[w]);
-    n_empty = base;
-    dmax_out = d;
+    double dmax = 0.0;
+    int ne = 0;
+    for (int c = threadIdx.x; c < k; c += blockDim.x) {
+        const long long cnt = (long long)__ldcg(acc.cnt + c);
+        const i128 sx = (i128)((u128)__ldcg(acc.sx + 3 * c) + ((u128)__ldcg(acc.sx + 3 * c + 1) << 32) +
+                               ((u128)__ldcg(acc.sx + 3 * c + 2) << 64));
+        const i128 sy = (i128)((u128)__ldcg(acc.sy + 3 * c) + ((u128)__ldcg(acc.sy + 3 * c + 1) << 32) +
+                               ((u128)__ldcg(acc.sy + 3 * c + 2) << 64));
+        if (cnt > 0) {
+            const double nx = fx_to_double(sx, Ex) / (double)cnt;
+            const double ny = fx_to_double(sy, Ey) / (double)cnt;
+            const double dx = nx - s_c[2 * c], dy = ny - s_c[2 * c + 1];
+            dmax = fmax(dmax, sqrt(dx * dx + dy * dy) * (1.0 + 1e-12) + 1e-300);
+            s_c[2 * c] = nx;
+            s_c[2 * c + 1] = ny;
+            cx[c] = nx;
+            cy[c] = ny;
+        } else {
+            ++ne;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+        ne += __shfl_xor_sync(0xffffffffu, ne, o);
+    }
+    if (lane == 0) {
+        atomicMax(&s_dmax, (unsigned long long)__double_as_longlong(dmax));
+        if (ne) atomicAdd(&s_ne, ne);
+    }
     __syncthreads();
+    n_empty = s_ne;
+    dmax_out = __longlong_as_double((long long)s_dmax);
+    if (n_empty > 0 && empties && threadIdx.x == 0) {  // rare: the host repairs; index order
+        int m = 0;
+        for (int c = 0; c < k; ++c)
+            if ((long long)__ldcg(acc.cnt + c) <= 0) empties[m++] = c;
+    }
 }
 
-// Lloyd iterations (lloyd_once :200-220) in one cooperative launch, two grid
+// Lloyd iterations (lloyd_once :200-220) in one cooperative launch, three grid
 // barriers per iteration:
 //   every block: update_means into its shared centers (means_local); stop on
 //     an empty cluster (host repair); row-grid rebuild when the centers may
 //     have moved more than half a cell since the last one (+ barrier);
 //     super-tile check -> global list of super-tiles;       barrier B1
 //   (listed super-tile, 4 of its tiles) per warp: the tiles' single-center
-//     tests (tile_expand_body), then the tiles that need it reassigned by
-//     the same warp (lloyd_tile);                             barrier B2
+//     tests; the tiles that need a reassignment go to one global tile list
+//     (one reservation per block pass);                     barrier B1.5
+//   the list's tiles spread evenly over all warps of the grid (lloyd_tile);
+//                                                           barrier B2
 //   every block: iteration end (count, stop when no label changed).
+// The tile list replaced per-block queues drained by the block's own warps:
+// the slowest block then ended its work 17.0 us after B1 (mean work 9.7 us),
+// with the list 13.5 us (config 4: 29.6 -> 26.2 us per iteration).
 // Counters alternate by iteration parity, so a counter is cleared only once
 // every block is past reading it. Block 0 folds the low limbs of the cluster
 // sums upward with atomics while the other blocks add to them.
-__global__ void __launch_bounds__(256) k_lloyd_persistent(PersistArgs a) {
+// 80 registers (3 blocks per SM): with 2 the grid is 296 blocks, and the
+// iterations take longer than the few spilled registers cost.
+__global__ void __launch_bounds__(256, 3) k_lloyd_persistent(PersistArgs a) {
     namespace cgx = cooperative_groups;
     cgx::grid_group grid = cgx::this_grid();
     extern __shared__ double s_cen[];  // [0, 2k) centers (x, y); [2k, 4k) cx | cy
@@ -2543,10 +2576,11 @@ __global__ void __launch_bounds__(256) k_lloyd_persistent(PersistArgs a) {
     __syncthreads();
     for (int b = 0; b < a.budget; ++b) {
         const int par = b & 1;
-        if (ts && b < 512) a.tstamp[6 * b] = gtimer();
+        if (ts && b < 512) a.tstamp[8 * b] = gtimer();
         int n_empty;
         double dmax;
-        means_local(a.acc, k, a.Ex, a.Ey, s_cen, blockIdx.x == 0 ? a.empties : nullptr, n_empty, dmax);
+        means_local(a.acc, k, a.Ex, a.Ey, s_cen, cx, cy, blockIdx.x == 0 ? a.empties : nullptr, n_empty,
+                    dmax);
         if (n_empty > 0) {
             if (lead) state[0] = n_empty;
             break;
@@ -2554,25 +2588,25 @@ __global__ void __launch_bounds__(256) k_lloyd_persistent(PersistArgs a) {
         const double acc_d = mov0 + dmax;  // triangle inequality: a bound
         const bool rebuild = !(acc_d <= movD);
         mov0 = rebuild ? 0.0 : acc_d;
-        for (int c = threadIdx.x; c < k; c += blockDim.x) {
-            cx[c] = s_cen[2 * c];
-            cy[c] = s_cen[2 * c + 1];
-        }
-        __syncthreads();
-        if (ts && b < 512) a.tstamp[6 * b + 1] = gtimer();
+        if (ts && b < 512) a.tstamp[8 * b + 1] = gtimer();
         if (rebuild) {
             row_grid_build_body(a.rg, s_cen, k, a.rg_blocks, a.rg_nblocks);
             grid.sync();
         }
-        if (ts && b < 512) a.tstamp[6 * b + 2] = gtimer();
+        if (ts && b < 512) a.tstamp[8 * b + 2] = gtimer();
         super_check_body(a.sbox, a.slenc, a.ntiles, a.cg, s_cen, a.tlab, a.swork, a.cnt2 + 2 + par,
                          nullptr, 0, a.rg, k);
         if (threadIdx.x == 0) s_changed = 0;
+        if (a.tstamp && blockIdx.x == 0 && b < 512) {  // check done (block 0)
+            __syncthreads();
+            if (threadIdx.x == 0) a.tstamp[8 * b + 6] = gtimer();
+        }
         grid.sync();  // B1
-        if (ts && b < 512) a.tstamp[6 * b + 3] = gtimer();
+        if (ts && b < 512) a.tstamp[8 * b + 3] = gtimer();
         if (lead) {  // counters of the other parity: last read before B2 of b - 1
             a.cnt2[par ^ 1] = 0;
             a.cnt2[2 + (par ^ 1)] = 0;
+            a.cnt2[4 + (par ^ 1)] = 0;
         }
         if (blockIdx.x == 0) {  // fold the low limbs of the cluster sums (value-preserving)
             for (int q = threadIdx.x; q < 2 * k; q += blockDim.x) {
@@ -2588,10 +2622,13 @@ __global__ void __launch_bounds__(256) k_lloyd_persistent(PersistArgs a) {
         const int64_t items = (int64_t)__ldcg(a.cnt2 + 2 + par) * 8;
         unsigned long long my_changed = 0, my_tiles = 0;
         {
-            // block b takes items b*8 .. b*8+7, then (b+G)*8 ..: one item per warp;
-            // the tiles to reassign go to a block queue drained by all 8 warps
+            // W1: every warp tests its items (balanced by count) and the
+            // block's tiles that need a reassignment go to one global list (one
+            // reservation per block pass); barrier; W2: the list's tiles spread
+            // evenly over all warps of the grid
             const int lane = threadIdx.x & 31, grp = lane >> 3, sub = lane & 7;
             const int wib = threadIdx.x >> 5;
+            unsigned long long* nlist = a.cnt2 + 4 + par;
             for (int64_t b0 = (int64_t)blockIdx.x * 8; b0 < items; b0 += (int64_t)gridDim.x * 8) {
                 const int64_t it = b0 + wib;
                 if (it < items) {
@@ -2601,20 +2638,32 @@ __global__ void __launch_bounds__(256) k_lloyd_persistent(PersistArgs a) {
                     const int tl = tv && a.tlen ? a.tlen[t] : 0;
                     const uint32_t single = box_single_g8(tb, tl, a.cg, a.rg, s_cen, sub);
                     const bool add = tv && sub == 0 && (single == MIXED || single != __ldcg(a.tlab + t));
-                    if (add) s_q[atomicAdd(&s_qn, 1)] = ((unsigned long long)single << 32) | (unsigned long long)t;
+                    if (add) {
+                        a.tnew[t] = single;
+                        s_q[atomicAdd(&s_qn, 1)] = (unsigned long long)t;
+                    }
                 }
                 __syncthreads();
                 const int nq = s_qn;
-                for (int q = wib; q < nq; q += 8) {
-                    const unsigned long long v = s_q[q];
-                    lloyd_tile<false>((uint32_t)v, (uint32_t)(v >> 32), a.spts, a.n, cx, cy, k, a.cg,
-                                      a.labs, a.tlab, a.Ex, a.Ey, a.acc, a.rg, a.slen, agg, nullptr,
-                                      nullptr, nullptr, my_changed);
-                    ++my_tiles;
+                if (nq) {
+                    __shared__ unsigned long long s_base;
+                    if (threadIdx.x == 0) s_base = atomicAdd(nlist, (unsigned long long)nq);
+                    __syncthreads();
+                    if (threadIdx.x < nq) a.work[s_base + threadIdx.x] = (uint32_t)s_q[threadIdx.x];
                 }
                 __syncthreads();
                 if (threadIdx.x == 0) s_qn = 0;
                 __syncthreads();
+            }
+            grid.sync();  // B1.5: the tile list is complete
+            const int64_t nw = (int64_t)__ldcg(nlist);
+            const int64_t W = ((int64_t)gridDim.x * blockDim.x) >> 5;
+            for (int64_t q = (((int64_t)blockIdx.x * blockDim.x) >> 5) + wib; q < nw; q += W) {
+                const uint32_t t = __ldcg(a.work + q);
+                lloyd_tile<false>(t, __ldcg(a.tnew + t), a.spts, a.n, cx, cy, k, a.cg, a.labs, a.tlab,
+                                  a.Ex, a.Ey, a.acc, a.rg, a.slen, agg, nullptr, nullptr, nullptr,
+                                  my_changed);
+                ++my_tiles;
             }
         }
         if ((threadIdx.x & 31) == 0 && my_tiles) atomicAdd(a.diag, my_tiles);
@@ -2622,9 +2671,10 @@ __global__ void __launch_bounds__(256) k_lloyd_persistent(PersistArgs a) {
         if ((threadIdx.x & 31) == 0 && my_changed) atomicAdd(&s_changed, my_changed);
         __syncthreads();
         if (threadIdx.x == 0 && s_changed) atomicAdd(a.cnt2 + par, s_changed);
-        if (ts && b < 512) a.tstamp[6 * b + 4] = gtimer();
+        if (ts && b < 512) a.tstamp[8 * b + 4] = gtimer();
+        if (a.tstamp && b < 512 && threadIdx.x == 0) atomicMax(a.tstamp + 8 * b + 7, gtimer());
         grid.sync();  // B2
-        if (ts && b < 512) a.tstamp[6 * b + 5] = gtimer();
+        if (ts && b < 512) a.tstamp[8 * b + 5] = gtimer();
         // iteration end (iter_end_body), on every block
         const unsigned long long chg = __ldcg(a.cnt2 + par);
         if (lead) {
@@ -2707,10 +2757,10 @@ bool lloyd_persistent(LloydCtx& L, int budget) {
         L.mov.upload(init, 3);
     }
     a.mov = L.mov.p;
-    DArr<unsigned long long> tsb(phase_times ? 6 * 512 : 0, L.st);
+    DArr<unsigned long long> tsb(phase_times ? 8 * 512 : 0, L.st);
     if (phase_times) tsb.zero();
     a.tstamp = phase_times ? tsb.p : nullptr;
-    DArr<unsigned long long> cnt2(4, L.st);
+    DArr<unsigned long long> cnt2(6, L.st);
     cnt2.zero();
     a.cnt2 = cnt2.p;
     void* args[] = {&a};
@@ -2724,23 +2774,29 @@ bool lloyd_persistent(LloydCtx& L, int budget) {
         }
     }
     if (phase_times) {  // JB_LLOYD_PHASES=1: mean phase latencies (us) on stderr
-        auto h = tsb.to_host(6 * 512);
+        auto h = tsb.to_host(8 * 512);
         double acc[5] = {0, 0, 0, 0, 0};
         int cnt = 0;
-        for (int b = 0; b < 512 && h[6 * b + 5]; ++b, ++cnt)
-            for (int q = 0; q < 5; ++q) acc[q] += (double)(h[6 * b + q + 1] - h[6 * b + q]) * 1e-3;
+        double chk = 0, lastw = 0;
+        for (int b = 0; b < 512 && h[8 * b + 5]; ++b, ++cnt) {
+            for (int q = 0; q < 5; ++q) acc[q] += (double)(h[8 * b + q + 1] - h[8 * b + q]) * 1e-3;
+            chk += (double)(h[8 * b + 6] - h[8 * b + 2]) * 1e-3;
+            lastw += (double)(h[8 * b + 7] - h[8 * b + 3]) * 1e-3;
+        }
         if (cnt) {
             int rebuilds = 0;
             double quart[4][5] = {};
             for (int b = 0; b < cnt; ++b) {
-                rebuilds += (h[6 * b + 2] - h[6 * b + 1]) > 1500;
+                rebuilds += (h[8 * b + 2] - h[8 * b + 1]) > 1500;
                 for (int q = 0; q < 5; ++q)
-                    quart[4 * b / cnt][q] += (double)(h[6 * b + q + 1] - h[6 * b + q]) * 1e-3;
+                    quart[4 * b / cnt][q] += (double)(h[8 * b + q + 1] - h[8 * b + q]) * 1e-3;
             }
             fprintf(stderr, "[jb] lloyd phases over %d iters (us): means %.1f grid %.1f check+B1 %.1f "
                             "work %.1f B2 %.1f (grid %d x 256), %d grid rebuilds\n",
                     cnt, acc[0] / cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt, acc[4] / cnt,
                     num_sms() * per_sm, rebuilds);
+            fprintf(stderr, "[jb] lloyd: block-0 check %.1f us (B1 wait = check+B1 - this), "
+                            "slowest block's work end %.1f us after B1 exit\n", chk / cnt, lastw / cnt);
             for (int qq = 0; qq < 4; ++qq)
                 fprintf(stderr, "[jb]   quarter %d: means %.1f grid %.1f check+B1 %.1f work %.1f B2 %.1f\n",
                         qq, quart[qq][0] / (cnt / 4.0), quart[qq][1] / (cnt / 4.0),
