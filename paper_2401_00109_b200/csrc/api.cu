@@ -206,6 +206,7 @@ struct jb_context {
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;  // svq sampling, concurrent with scale_pieces
     cudaEvent_t side_done = nullptr;
+    cudaStream_t aux = nullptr;  // scale_pieces: the increments' sums beside the lengths' sequential sum
 };
 
 struct jb_fit {
@@ -533,7 +534,8 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
     // ---- digitize: scale_pieces ----
     auto t1 = Clock::now();
     Scaled sc;
-    scale_pieces(fit->pieces, steps_glob, c.scl, sc, st, &cm);
+    if (!ctx->aux) JB_CUDA(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+    scale_pieces(fit->pieces, steps_glob, c.scl, sc, st, &cm, ctx->aux);
     JB_TRACE("fit: scaled", st);
     fit->scaling[0] = sc.scl;
     fit->scaling[1] = sc.sigma_len;
@@ -722,6 +724,47 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
     assign_and_stats(pv, fit->pieces.len.p, N, backend_centers, k, bb, assign_needed,
                      labels.p, gs, st, sc.max_len_global, sc.scl, sc.sigma_len, &cm, base,
                      k <= 2048 ? &xh : nullptr);
+    // ranking (digitization.hpp:257-262) needs only the counts and first
+    // indices: the labels are rewritten in rank order on the aux stream, out of
+    // place, while the sequential x sums below read the backend's labels
+    std::vector<uint64_t> order(k);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) {
+        if (gs.counts[a] != gs.counts[b]) return gs.counts[a] > gs.counts[b];
+        return gs.first_seen[a] < gs.first_seen[b];
+    });
+    std::vector<uint32_t> rank_of(k);
+    for (uint64_t r = 0; r < k; ++r) rank_of[order[r]] = (uint32_t)r;
+    DArr<uint32_t> ranked;
+    cudaEvent_t ev_ranked = nullptr;
+    if (k > 0 && N > 0) {
+        ranked.alloc(N, st);
+        cudaEvent_t ev;
+        JB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        JB_CUDA(cudaEventRecord(ev, st));
+        JB_CUDA(cudaStreamWaitEvent(ctx->aux, ev, 0));
+        JB_CUDA(cudaEventDestroy(ev));
+        relabel(labels.p, N, rank_of, ctx->aux, ranked.p, false);
+        JB_CUDA(cudaEventCreateWithFlags(&ev_ranked, cudaEventDisableTiming));
+        JB_CUDA(cudaEventRecord(ev_ranked, ctx->aux));
+    }
+    struct EvGuard {  // the join also runs when the sums below throw
+        cudaEvent_t& e;
+        cudaStream_t st;
+        void join() {
+            if (e) {
+                cudaStreamWaitEvent(st, e, 0);
+                cudaEventDestroy(e);
+                e = nullptr;
+            }
+        }
+        ~EvGuard() {
+            if (e) {
+                cudaEventSynchronize(e);
+                cudaEventDestroy(e);
+            }
+        }
+    } ranked_guard{ev_ranked, st};
     // the x sums bit-exact as the reference accumulates them: then the
     // codebook's x and every reconstructed length match (inverse.hpp:46,63-74)
     if (k > 0) {
@@ -771,14 +814,6 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
             mean_lengths[g] = lc > 0 ? (double)sls[g] / (double)lc : 1.0;
         }
     }
-    std::vector<uint64_t> order(k);
-    std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) {
-        if (gs.counts[a] != gs.counts[b]) return gs.counts[a] > gs.counts[b];
-        return gs.first_seen[a] < gs.first_seen[b];
-    });
-    std::vector<uint32_t> rank_of(k);
-    for (uint64_t r = 0; r < k; ++r) rank_of[order[r]] = (uint32_t)r;
     fit->k = k;
     fit->centers.resize(2 * k);
     fit->mean_lengths.resize(k);
@@ -789,7 +824,8 @@ void run_fit(jb_context* ctx, const double* values, int64_t n_values, bool on_de
         if (!std::isfinite(fit->centers[2 * r]) || !std::isfinite(fit->centers[2 * r + 1]))
             throw Error(INVALID_INPUT, "codebook: non-finite center");  // core.hpp:173-175
     }
-    if (k > 0 && N > 0) relabel(labels.p, N, rank_of, st);
+    ranked_guard.join();  // st waits for the ranked labels
+    if (k > 0 && N > 0) labels = std::move(ranked);  // the old array returns to st's cache
     fit->labels = std::move(labels);
     fit->d_centers.alloc(std::max<uint64_t>(2 * k, 1), st);
     fit->d_mean_lengths.alloc(std::max<uint64_t>(k, 1), st);
@@ -868,6 +904,12 @@ void jb_context_destroy(jb_context* ctx) {
         jb::dev_cache_drop(ctx->side);
         cudaStreamSynchronize(ctx->side);
         cudaEventDestroy(ctx->side_done);
+    }
+    if (ctx->aux) {
+        cudaStreamSynchronize(ctx->aux);
+        jb::dev_cache_drop(ctx->aux);
+        cudaStreamSynchronize(ctx->aux);
+        cudaStreamDestroy(ctx->aux);
     }
     // buffers of fits that outlive the context stay valid (the stream handle
     // is not destroyed: a jb_fit still references it)

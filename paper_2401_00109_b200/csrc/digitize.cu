@@ -83,47 +83,83 @@ __global__ void k_sum_inc(const double* __restrict__ inc, int64_t n, int E,
     if (threadIdx.x == 0) fx_atomic_add(acc, s);
 }
 
-// scale_pieces' second pass (digitization.hpp:39-45): var_inc as an exact
-// fixed-point sum, and var_len's range histogram (seqsum.cu: ranges of
-// VB_R pieces, counts per length <= RH, longer pieces listed) from which the
-// reference's sequential var_len is reproduced bit for bit. Warp per range.
+// scale_pieces' second pass (digitization.hpp:39-45), split by input so the
+// two halves run on different streams: var_inc as an exact fixed-point sum
+// (k_var_inc, reads inc only) ...
+__global__ void k_var_inc(const double* __restrict__ inc, int64_t n, double mean_inc, int Ei,
+                          unsigned long long* __restrict__ acc) {
+    i128 si = 0;
+    constexpr int U = 4;  // independent loads in flight per thread
+    for (int64_t b = blockIdx.x * (int64_t)kTB * U + threadIdx.x; b < n;
+         b += (int64_t)gridDim.x * kTB * U) {
+        double V[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = b + (int64_t)u * kTB;
+            V[u] = i < n ? inc[i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (b + (int64_t)u * kTB >= n) break;
+            const double di = V[u] - mean_inc;  // digitization.hpp:42,44
+            si += fx_from_double(di * di, Ei);
+        }
+    }
+    si = block_sum_i128<kTB>(si);
+    if (threadIdx.x == 0) fx_atomic_add(acc + 2, si);
+}
+
+// ... and var_len's range histogram (k_len_hist, reads len only; seqsum.cu:
+// ranges of VB_R pieces, counts per length <= RH, longer pieces listed) from
+// which the reference's sequential var_len is reproduced bit for bit. It
+// needs only mean_len = total steps / N, known before any pass. Warp per range.
 constexpr int VB_R = 2048;
 
-__global__ void __launch_bounds__(256) k_var_blocks(
-    const int32_t* __restrict__ len, const double* __restrict__ inc, int64_t n, double mean_len,
-    double mean_inc, int Ei, unsigned long long* __restrict__ acc, uint16_t* __restrict__ hist,
+// SMALL (RH <= 16, e.g. config 4's lengths 1..9): each lane counts its 64
+// pieces of a range in two registers of 8-bit fields (no shared-memory
+// atomics, no match), widened to 16-bit fields for the warp reduction.
+__device__ __forceinline__ unsigned long long spread8to16(uint32_t x) {
+    return (unsigned long long)(x & 0xFFu) | ((unsigned long long)(x & 0xFF00u) << 8) |
+           ((unsigned long long)(x & 0xFF0000u) << 16) | ((unsigned long long)(x & 0xFF000000u) << 24);
+}
+
+template <bool SMALL>
+__global__ void __launch_bounds__(256) k_len_hist(
+    const int32_t* __restrict__ len, int64_t n, double mean_len, uint16_t* __restrict__ hist,
     double* __restrict__ approx, uint32_t* __restrict__ long_idx,
     unsigned long long* __restrict__ long_n, int RH) {
     __shared__ uint32_t sh[8][64];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t nr = (n + VB_R - 1) / VB_R;
-    i128 si = 0;
     for (int64_t r = (int64_t)blockIdx.x * 8 + w; r < nr; r += (int64_t)gridDim.x * 8) {
-        for (int l = lane; l < RH; l += 32) sh[w][l] = 0;
-        __syncwarp();
+        if (!SMALL) {
+            for (int l = lane; l < RH; l += 32) sh[w][l] = 0;
+            __syncwarp();
+        }
+        unsigned long long c0 = 0, c1 = 0;
         double lsum = 0.0;
         const int64_t i0 = r * VB_R, i1 = min(i0 + VB_R, n);
         for (int64_t c = i0; c < i1; c += 32 * 8) {
             int32_t L[8];
-            double I[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const int64_t i = c + u * 32 + lane;
                 L[u] = i < i1 ? len[i] : 0;
-                I[u] = i < i1 ? inc[i] : 0.0;
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const int64_t i = c + u * 32 + lane;
                 const bool v = i < i1;
-                if (v) {
-                    const double di = I[u] - mean_inc;  // digitization.hpp:42,44
-                    si += fx_from_double(di * di, Ei);
-                }
                 const int l = L[u];
                 const bool in = v && l >= 1 && l <= RH;
-                const unsigned grp = __match_any_sync(0xffffffffu, in ? l : -1);
-                if (in && (__ffs(grp) - 1) == lane) atomicAdd(&sh[w][l - 1], (uint32_t)__popc(grp));
+                if (SMALL) {
+                    const unsigned long long one = in ? 1ull << (8 * ((l - 1) & 7)) : 0ull;
+                    if (l <= 8) c0 += one;
+                    else c1 += one;
+                } else {
+                    const unsigned grp = __match_any_sync(0xffffffffu, in ? l : -1);
+                    if (in && (__ffs(grp) - 1) == lane) atomicAdd(&sh[w][l - 1], (uint32_t)__popc(grp));
+                }
                 const bool lg = v && !in;
                 const unsigned lm = __ballot_sync(0xffffffffu, lg);
                 if (lm) {
@@ -138,18 +174,31 @@ __global__ void __launch_bounds__(256) k_var_blocks(
                 }
             }
         }
-        __syncwarp();
-        for (int l = lane; l < RH; l += 32) {
-            hist[r * RH + l] = (uint16_t)sh[w][l];
-            const double dl = (double)(l + 1) - mean_len;
-            lsum += (double)sh[w][l] * (dl * dl);  // the record's approximate sum
+        if (SMALL) {
+            unsigned long long e[4] = {spread8to16((uint32_t)c0), spread8to16((uint32_t)(c0 >> 32)),
+                                       spread8to16((uint32_t)c1), spread8to16((uint32_t)(c1 >> 32))};
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                for (int o = 16; o; o >>= 1) e[q] += __shfl_xor_sync(0xffffffffu, e[q], o);
+            if (lane < RH) {
+                const unsigned long long ew = lane < 4 ? e[0] : lane < 8 ? e[1] : lane < 12 ? e[2] : e[3];
+                const uint32_t cnt = (uint32_t)(ew >> (16 * (lane & 3))) & 0xFFFFu;
+                hist[r * RH + lane] = (uint16_t)cnt;
+                const double dl = (double)(lane + 1) - mean_len;
+                lsum += (double)cnt * (dl * dl);  // the record's approximate sum
+            }
+        } else {
+            __syncwarp();
+            for (int l = lane; l < RH; l += 32) {
+                hist[r * RH + l] = (uint16_t)sh[w][l];
+                const double dl = (double)(l + 1) - mean_len;
+                lsum += (double)sh[w][l] * (dl * dl);  // the record's approximate sum
+            }
         }
         for (int o = 16; o; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
         if (lane == 0) approx[r] = lsum;
         __syncwarp();
     }
-    si = block_sum_i128<256>(si);
-    if (threadIdx.x == 0) fx_atomic_add(acc + 2, si);
 }
 
 // ScalingParams::apply (core.hpp:130-132): materialised points (GA only)
@@ -168,7 +217,7 @@ int grid_for(int64_t n) {
 }  // namespace
 
 void scale_pieces(const Pieces& pc, int64_t total_steps, double scl, Scaled& out,
-                  cudaStream_t st, const Comm* cm) {
+                  cudaStream_t st, const Comm* cm, cudaStream_t aux) {
     const Comm one;
     const Comm& C = cm ? *cm : one;
     // global N, max|inc|, max len (identical fixed-point exponents on every rank)
@@ -193,45 +242,62 @@ void scale_pieces(const Pieces& pc, int64_t total_steps, double scl, Scaled& out
     if (N == 0) throw Error(INVALID_INPUT, "digitize: no pieces");
     if (scl < 0.0) throw Error(INVALID_INPUT, "scale_pieces: scl must be >= 0");
     const double n = (double)N;
+    // Two independent chains: the increments (sum -> mean_inc -> var_inc, HBM
+    // bound) on `si_st` and the lengths (range histogram -> the sequential
+    // var_len of seqsum.cu, latency bound) on `st`. With an aux stream they
+    // overlap; without one they run back to back on `st` (same results: every
+    // sum is exact or bit-exact sequential, whatever the schedule).
+    cudaStream_t si_st = aux ? aux : st;
+    if (aux) {  // the pieces were written on st
+        cudaEvent_t ev;
+        JB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        JB_CUDA(cudaEventRecord(ev, st));
+        JB_CUDA(cudaStreamWaitEvent(aux, ev, 0));
+        JB_CUDA(cudaEventDestroy(ev));
+    }
     // sum of lens over all pieces == total steps of all segments (exact)
-    DArr<unsigned long long> acc(6, st);
+    DArr<unsigned long long> acc(6, si_st);
     acc.zero();
     const int Einc = fx_exponent_for(max_abs_inc * n * 1.0000001 + 1e-300);
-    DArr<unsigned long long> mm(2, st);  // extremes of inc (order-preserving bits)
+    DArr<unsigned long long> mm(2, si_st);  // extremes of inc (order-preserving bits)
     {
         const unsigned long long init[2] = {~0ULL, 0ULL};
         mm.upload(init, 2);
     }
     if (pc.N > 0) {
-        JB_PROF("scale_sum_inc", st);
-        k_sum_inc<<<grid_for(pc.N), kTB, 0, st>>>(pc.inc.p, pc.N, Einc, acc.p, mm.p);
+        JB_PROF("scale_sum_inc", si_st);
+        k_sum_inc<<<grid_for(pc.N), kTB, 0, si_st>>>(pc.inc.p, pc.N, Einc, acc.p, mm.p);
     }
     JB_LAUNCH_CHECK();
-    JB_TRACE("scale: sum inc", st);
+    // mean_len: sequential double sum of integer lens is exact (< 2^53)
+    const double mean_len = (double)total_steps / n;
+    RangeHist vh;  // var_len's range histogram (seqsum.cu)
+    const int RH = (int)std::min<int32_t>(std::max<int32_t>(pc.max_len, 1), 64);
+    vh.alloc(pc.N, VB_R, 1, RH, pc.max_len > RH, st);
+    if (pc.N > 0) {
+        JB_PROF("scale_len_hist", st);
+        const int64_t nr = vh.nr;
+        auto kern = RH <= 16 ? k_len_hist<true> : k_len_hist<false>;
+        kern<<<(int)std::max<int64_t>(1, std::min<int64_t>((nr + 7) / 8, (int64_t)num_sms() * 8)), 256,
+               0, st>>>(pc.len.p, pc.N, mean_len, vh.hist.p, vh.approx.p, vh.long_idx.p, vh.long_n.p,
+                        RH);
+    }
+    JB_LAUNCH_CHECK();
+    if (!aux) JB_TRACE("scale: sum inc + len hist", st);
     std::vector<unsigned long long> h = acc.to_host(2);
     h = C.sum_i128(h);
     const std::vector<unsigned long long> hm = mm.to_host(2);
-    // mean_len: sequential double sum of integer lens is exact (< 2^53)
-    const double mean_len = (double)total_steps / n;
     const double mean_inc = fx_to_double(fx_load(h.data()), Einc) / n;
 
     const double dimax = max_abs_inc + std::fabs(mean_inc) + 1e-300;
     const int Ei = fx_exponent_for(dimax * dimax * n * 1.001 + 1e-300);
     acc.zero();
-    RangeHist vh;  // var_len's range histogram (seqsum.cu)
-    const int RH = (int)std::min<int32_t>(std::max<int32_t>(pc.max_len, 1), 64);
-    vh.alloc(pc.N, VB_R, 1, RH, pc.max_len > RH, st);
     if (pc.N > 0) {
-        JB_PROF("scale_sum_var", st);
-        const int64_t nr = vh.nr;
-        k_var_blocks<<<(int)std::max<int64_t>(1, std::min<int64_t>((nr + 7) / 8, (int64_t)num_sms() * 8)),
-                       256, 0, st>>>(pc.len.p, pc.inc.p, pc.N, mean_len, mean_inc, Ei, acc.p,
-                                     vh.hist.p, vh.approx.p, vh.long_idx.p, vh.long_n.p, RH);
+        JB_PROF("scale_sum_var", si_st);
+        k_var_inc<<<grid_for(pc.N), kTB, 0, si_st>>>(pc.inc.p, pc.N, mean_inc, Ei, acc.p);
     }
     JB_LAUNCH_CHECK();
-    h = acc.to_host(4);
-    h = C.sum_i128(h);
-    JB_TRACE("scale: variances", st);
+    if (!aux) JB_TRACE("scale: var inc", st);
     // var_len: the reference's left-to-right sum of (len - mean_len)^2,
     // bit-exact (seqsum.cu); sigma_len then fixes every x = scl*len/sigma_len
     // and every reconstructed length (inverse.hpp:46)
@@ -240,6 +306,9 @@ void scale_pieces(const Pieces& pc, int64_t total_steps, double scl, Scaled& out
     vt.kind = SeqTerms::VAR_LEN;
     vt.a = mean_len;
     const double var_len = range_seq_sums(vh, vt, nullptr, st, cm)[0];
+    JB_TRACE("scale: var len (sequential)", st);
+    h = acc.to_host(4);  // joins the increments' stream
+    h = C.sum_i128(h);
     const double var_inc = fx_to_double(fx_load(h.data() + 2), Ei);
     double sl = N > 1 ? std::sqrt(var_len / (n - 1.0)) : 0.0;
     double si = N > 1 ? std::sqrt(var_inc / (n - 1.0)) : 0.0;
@@ -507,30 +576,32 @@ __global__ void k_stats_global(const PtsView pv, const int32_t* __restrict__ len
     }
 }
 
-__global__ void k_relabel(uint32_t* __restrict__ labels, int64_t n,
+// out may be the input itself (in place) or a second array
+__global__ void k_relabel(const uint32_t* labels, uint32_t* out, int64_t n,
                           const uint32_t* __restrict__ rank_of, int k) {
     extern __shared__ uint32_t rk[];
     for (int c = threadIdx.x; c < k; c += blockDim.x) rk[c] = rank_of[c];
     __syncthreads();
     // 16-byte accesses, two in flight per thread (labels are 256-byte aligned)
-    uint4* l4 = reinterpret_cast<uint4*>(labels);
+    const uint4* l4 = reinterpret_cast<const uint4*>(labels);
+    uint4* o4 = reinterpret_cast<uint4*>(out);
     const int64_t n4 = n >> 2, stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += 2 * stride) {
         uint4 a = l4[i], b = make_uint4(0, 0, 0, 0);
         const bool two = i + stride < n4;
         if (two) b = l4[i + stride];
-        l4[i] = make_uint4(rk[a.x], rk[a.y], rk[a.z], rk[a.w]);
-        if (two) l4[i + stride] = make_uint4(rk[b.x], rk[b.y], rk[b.z], rk[b.w]);
+        o4[i] = make_uint4(rk[a.x], rk[a.y], rk[a.z], rk[a.w]);
+        if (two) o4[i + stride] = make_uint4(rk[b.x], rk[b.y], rk[b.z], rk[b.w]);
     }
     for (int64_t i = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
-        labels[i] = rk[labels[i]];
+        out[i] = rk[labels[i]];
 }
 
-__global__ void k_relabel_global(uint32_t* __restrict__ labels, int64_t n,
+__global__ void k_relabel_global(const uint32_t* labels, uint32_t* out, int64_t n,
                                  const uint32_t* __restrict__ rank_of) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
-        labels[i] = rank_of[labels[i]];
+        out[i] = rank_of[labels[i]];
 }
 
 __global__ void k_sample_len(const uint64_t* __restrict__ sample,
@@ -746,18 +817,19 @@ std::vector<double> exact_group_sum_x(const int32_t* d_len, const uint32_t* d_la
 }
 
 void relabel(uint32_t* d_labels, int64_t n, const std::vector<uint32_t>& rank_of,
-             cudaStream_t st) {
+             cudaStream_t st, uint32_t* d_out, bool sync) {
     const int k = (int)rank_of.size();
-    DArr<uint32_t> rk(k, st);
+    uint32_t* out = d_out ? d_out : d_labels;
+    DArr<uint32_t> rk(k, st);  // returns to st's cache: reuse is ordered after the kernel
     rk.upload(rank_of.data(), k);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, num_sms() * 8));
     JB_PROF("relabel", st);
-    if ((size_t)k * 4 <= 48 * 1024 && ((uintptr_t)d_labels & 15) == 0)
-        k_relabel<<<grid, 256, k * 4, st>>>(d_labels, n, rk.p, k);
+    if ((size_t)k * 4 <= 48 * 1024 && (((uintptr_t)d_labels | (uintptr_t)out) & 15) == 0)
+        k_relabel<<<grid, 256, k * 4, st>>>(d_labels, out, n, rk.p, k);
     else
-        k_relabel_global<<<grid, 256, 0, st>>>(d_labels, n, rk.p);
+        k_relabel_global<<<grid, 256, 0, st>>>(d_labels, out, n, rk.p);
     JB_LAUNCH_CHECK();
-    JB_CUDA(cudaStreamSynchronize(st));
+    if (sync) JB_CUDA(cudaStreamSynchronize(st));
 }
 
 void sample_len_stats(const uint64_t* d_sample, const uint32_t* d_sample_labels, int64_t S,

@@ -205,9 +205,11 @@ struct Scaled {
 };
 
 // total_steps: of ALL ranks' segments; cm: null or world == 1 for one GPU.
-// Computes sigma and the bounding box; the points stay virtual.
+// Computes sigma and the bounding box; the points stay virtual. aux: an
+// optional second stream for the increments' sums, which then overlap the
+// lengths' sequential sum on st (both joined before the call returns).
 void scale_pieces(const Pieces& pc, int64_t total_steps, double scl, Scaled& out,
-                  cudaStream_t st, const Comm* cm = nullptr);
+                  cudaStream_t st, const Comm* cm = nullptr, cudaStream_t aux = nullptr);
 PtsView points_view(const Pieces& pc, const Scaled& sc);
 // materialises sc.pts (GA backends sort and sweep the points many times)
 void materialize_points(const Pieces& pc, Scaled& sc, cudaStream_t st);
@@ -371,8 +373,10 @@ void symbolize_pieces(const int32_t* d_len, const double* d_inc, int64_t n,
                       const std::vector<double>& centers, uint64_t k, const double scaling[3],
                       uint32_t* d_labels, cudaStream_t st);
 
+// d_out: null for in place, else a second array; sync = false leaves the
+// kernel in flight on st (the caller joins the stream)
 void relabel(uint32_t* d_labels, int64_t n, const std::vector<uint32_t>& rank_of,
-             cudaStream_t st);
+             cudaStream_t st, uint32_t* d_out = nullptr, bool sync = true);
 
 // The reference's sequential per-group sums of x = scl*len/sigma_len over the
 // pieces in index order (digitization.hpp:224-231), bit-exact: labels are the
