@@ -382,6 +382,9 @@ namespace {
 // atomics (native in L2). Everything is exact integer arithmetic, hence
 // independent of the schedule; the host removes the bias (count * B).
 constexpr int AS_TB = 256, AS_U = 4;
+#ifndef JB_AS_MINB
+#define JB_AS_MINB 4  // 64 registers, no spills: 4 CTAs per SM (3 at 75 registers: 7.55 -> 7.23 ms, config 4)
+#endif
 constexpr int kXRow = 64;
 
 // Per-range output of the group statistics (seqsum.cu RangeHist): per range
@@ -395,7 +398,7 @@ struct RangeOut {
     int64_t R = 1024;
 };
 
-__global__ void __launch_bounds__(AS_TB) k_assign_stats(
+__global__ void __launch_bounds__(AS_TB, JB_AS_MINB) k_assign_stats(
     const PtsView pv, const int32_t* __restrict__ len, int64_t n,
     const double* __restrict__ centers, int k, int do_assign, uint32_t* __restrict__ labels,
     int Ex, int Ey, unsigned long long Bx, unsigned long long By,

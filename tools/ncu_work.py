@@ -23,7 +23,8 @@ BENCH = {
     "d2_seed": r"k_d2_seed",
     "assign_stats": r"k_assign_stats", "d2_update": r"k_d2_tiles|k_d2_cull",
     "d2_pick": r"k_pick\b", "compress_spec": r"k_spec", "compress_emit": r"k_emit",
-    "scale_sum_var": r"k_sum_var", "scale_sum_inc": r"k_sum_inc", "inverse_fused": r"k_inv_fused",
+    "scale_sum_var": r"k_var_inc", "scale_len_hist": r"k_len_hist", "relabel": r"k_relabel",
+    "scale_sum_inc": r"k_sum_inc", "inverse_fused": r"k_inv_fused",
     "sample_order": r"k_rowkey_jorder", "sample_unpack": r"k_rec_unpack",
 }
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
