@@ -372,6 +372,12 @@ class NativeFit:
                                           inc.ctypes.data))
         return off, ln[: self.n_pieces], inc[: self.n_pieces]
 
+    def piece_offsets(self) -> np.ndarray:
+        """First piece of every segment (n_seg + 1 offsets), without the pieces."""
+        off = np.zeros(self.n_seg + 1, np.int64)
+        _check(N.lib().jb_fit_copy_pieces(self.h, off.ctypes.data, None, None))
+        return off
+
     def symbolic_arrays(self, labels=True):
         k = self.k
         lab = np.zeros(max(self.n_pieces, 1), np.uint32)
