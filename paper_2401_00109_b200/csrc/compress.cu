@@ -150,7 +150,10 @@ constexpr int kRcp = 256;  // k_spec reciprocal tables cover d <= kRcp
 // becomes that piece's d = 1 candidate (always accepted, compression.hpp:54).
 // Identical decisions to piece_end, with no re-loads and a uniform
 // per-sample loop across the warp.
-__global__ void __launch_bounds__(128) k_spec(const double* __restrict__ v, ChunkGeom g,
+#ifndef JB_SPEC_MINB
+#define JB_SPEC_MINB 8  // 64 registers (8 bytes spilled): 8 CTAs per SM, 6.01 -> 5.67 ms (9: 56 registers, 7.98 ms)
+#endif
+__global__ void __launch_bounds__(128, JB_SPEC_MINB) k_spec(const double* __restrict__ v, ChunkGeom g,
                                               int64_t n_chunks, double tol2, int64_t max_len,
                                               uint32_t* __restrict__ fb,
                                               int64_t* __restrict__ exit_spec,

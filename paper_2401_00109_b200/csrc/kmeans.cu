@@ -1207,7 +1207,10 @@ __global__ void __cluster_dims__(PC, 1, 1) __launch_bounds__(PICK_TB)
 // The prefix arithmetic is exact on these integers, as in k_pick. If the
 // total reaches 0 (every remaining point duplicates a center), the launch
 // stops before that round (flag[1]) and the per-round path finishes.
-constexpr int D2P_TB = 1024;
+#ifndef JB_D2P_TB
+#define JB_D2P_TB 512  // 128 registers, no spills (1024 threads: 64 registers, 172 bytes spilled): 8.39 -> 7.93 ms; 256: 8.76
+#endif
+constexpr int D2P_TB = JB_D2P_TB;
 
 struct D2Seed {
     const double2* spts;
